@@ -1,0 +1,361 @@
+#!/usr/bin/env python3
+"""MACH HOOI-sweep benchmark (BASELINE.json metric: HOOI sweep nonzeros/s).
+
+Workload (BASELINE.json configs[1], "C2"): 512x512x512 fp32 Tucker rank
+(10,10,10) + 1% noise, MACH p = 0.05 (~6.7M nonzeros), HOSVD + 5 HOOI sweeps,
+1 GPU.  A "step" is one HOOI sweep over the sampled tensor (all mode updates +
+core + fit + stop check, tucker.cpp:80-106).  value = nnz / mean sweep time
+(GNNZ/s), device-timed with CUDA events on the library's stream, L2 flushed
+(256 MiB write) before every timed sweep.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mach|reference] [--config c2]
+
+--impl reference times the reference algorithm on the host cores: the CPU
+oracle (Eigen-free restatement of /root/reference/proj, which cannot be built
+here) on the same config.  Under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HOOI sweep nonzeros/sec (GNNZ/s) + achieved HBM/tensor roofline fraction"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mach", choices=["mach", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled in the background."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                parts = [p.strip() for p in out.strip().split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_mach(args, rank, world, local):
+    import numpy as np
+    import torch
+
+    import paper_0909_4969_b200 as mb
+    from paper_0909_4969_b200.synth import CONFIGS, lowrank_torch
+
+    dims, ranks, noise, p, sweeps, dtype = CONFIGS[args.config]
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    seed_data, seed_mach = 2, 7
+
+    x = lowrank_torch(dims, ranks, noise, seed=seed_data, dtype=dtype, device=dev)
+    ctx = mb.Context(local)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream.cuda_stream)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    with ClockSampler(local) as clocks:
+        t = mb.DenseTensor.from_torch(x, dims, ctx)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            sp = mb.sparsify(t, mb.SparsifyConfig(p, seed_mach))
+            ev1.record(stream)
+        stream.synchronize()
+        sample_ms = ev0.elapsed_time(ev1)
+        nnz = sp.nnz
+        sess = mb.HooiSession(sp, ranks)
+        sess.step(args.warmup, 0.0)
+        stream.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        l0 = ctx.launches
+        times = []
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                flush.zero_()  # evict the sampled tensor from L2 between timed sweeps
+                starts[k].record(stream)
+                sess.step(1, 0.0)
+                ends[k].record(stream)
+        stream.synchronize()
+        torch.cuda.synchronize()
+        launches = ctx.launches - l0
+        times = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+        ms = sum(times) / len(times)
+        if world > 1:
+            tt = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            ms = float(tt.item())
+        model = sess.model()
+
+        # ---- per-kernel profile pass (not timed for `value`) ----
+        mb.profile(ctx, True)
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                flush.zero_()
+                sess.step(1, 0.0)
+        stream.synchronize()
+        kstats = mb.kernel_stats(ctx)
+        mb.profile(ctx, False)
+        sweep_ms_prof = sum(v[1] for v in kstats.values()) / 2.0
+
+    vsize = 4 if dtype == "float32" else 8
+    d = len(dims)
+    # roofline of the dominant HBM kernel: the fused mode-n TTM (one streaming
+    # read of the mode's sorted COO per launch: nnz * (4 B key + value))
+    ttm = [(k, v) for k, v in kstats.items() if "ttm_mode_kernel" in k]
+    hbm, peak_src = peaks()
+    roof = None
+    if ttm:
+        n_l, tot = ttm[0][1]
+        per_launch_ms = tot / n_l
+        bytes_per_launch = nnz * (4 + vsize)
+        achieved = bytes_per_launch / (per_launch_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "ttm_mode_kernel", "achieved": round(achieved, 1), "peak": hbm,
+                "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+                "bytes_per_launch": bytes_per_launch, "avg_launch_ms": round(per_launch_ms, 5),
+                "share_of_sweep": round(tot / 2.0 / sweep_ms_prof, 3) if sweep_ms_prof else None,
+                "peak_source": peak_src}
+    breakdown = {k: {"launches_per_sweep": v[0] / 2.0, "ms_per_sweep": round(v[1] / 2.0, 5)}
+                 for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][1])}
+
+    value = world * nnz / (ms * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": round(value, 4), "unit": "GNNZ/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if dtype == "float32" else "f64",
+        "data": "synthetic low-rank + noise (seeded, generated on device; SURVEY.md §8d generator)",
+        "config": {"workload": f"{args.config.upper()}: {'x'.join(map(str, dims))} {dtype}, ranks {ranks}, "
+                               f"noise {noise}, MACH p={p}, step = one HOOI sweep",
+                   "nnz": nnz, "numel": int(math.prod(dims)), "seed_data": seed_data, "seed_mach": seed_mach,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "flushed (256 MiB memset) before every timed sweep"},
+        "gpu_launches": launches,
+        "roofline": roof,
+        "phases_ms": {"sample": round(sample_ms, 4), "setup": model.times.get("setup_ms"),
+                      "hosvd": model.times.get("hosvd_ms"), "sweeps": [round(s, 5) for s in times]},
+        "fit": model.fit,
+        "kernels": breakdown,
+        "clocks": clocks.summary(),
+    }
+    # sampler roofline (reported beside the sweep): numel*s read + nnz*(4+s) written
+    samp = [v for k, v in kstats.items() if "sample_kernel" in k]
+    out["sampler"] = {"ms": round(sample_ms, 4),
+                      "GB_per_s": round((math.prod(dims) * vsize + nnz * (4 + vsize)) / (sample_ms * 1e-3) / 1e9, 1),
+                      "frac_of_peak": round((math.prod(dims) * vsize + nnz * (4 + vsize)) / (sample_ms * 1e-3) / 1e9 / hbm,
+                                            4)}
+    del samp
+
+    # ---- e2e: reference-facing call with host buffers (pinned) ----
+    if not args.no_e2e:
+        out["e2e"] = run_e2e(args, mb, x, dims, ranks, p, seed_mach, nnz, vsize, dev, local)
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_baseline(x, dims, ranks, p, seed_mach)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    sess.free()
+    if rank == 0:
+        print(json.dumps(out))
+
+
+def run_e2e(args, mb, x, dims, ranks, p, seed, nnz, vsize, dev, local):
+    """mach_mach_hooi through the C ABI from pinned host memory: H2D of the
+    dense tensor, sampling, layouts, HOSVD, K sweeps, D2H of the model."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_0909_4969_b200 import _lib as L
+
+    host = x.cpu().pin_memory()
+    lib = L.lib()
+    ctx = mb.Context(local)
+    dt = L.MACH_F32 if vsize == 4 else L.MACH_F64
+    dims_c = (C.c_int * len(dims))(*dims)
+    ranks_c = (C.c_int * len(ranks))(*ranks)
+    sweeps = args.steps
+    best = None
+    for rep in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hd = C.c_void_p()
+        rc = lib.mach_dense_upload(ctx.h, dt, len(dims), dims_c, C.c_void_p(host.data_ptr()), C.byref(hd))
+        assert rc == 0, lib.mach_last_error()
+        hm, hs = C.c_void_p(), C.c_void_p()
+        rc = lib.mach_mach_hooi(ctx.h, hd, ranks_c, p, seed, sweeps, 0.0, C.byref(hm), C.byref(hs))
+        assert rc == 0, lib.mach_last_error()
+        model = mb.api._model_from(hm)  # D2H of core + factors
+        t1 = time.perf_counter()
+        lib.mach_sparse_free(hs)
+        lib.mach_dense_free(hd)
+        best = (t1 - t0) if best is None else min(best, t1 - t0)
+    d2h = (model.core.size + sum(f.size for f in model.factors)) * 8
+    done = model.iterations
+    return {"value": round(nnz * done / best / 1e9, 4), "unit": "GNNZ/s",
+            "h2d_bytes_per_step": int(math.prod(dims) * vsize), "d2h_bytes_per_step": int(d2h),
+            "step": f"one mach_hooi(host tensor) job: H2D + sample + layouts + HOSVD + {done} sweeps + D2H",
+            "job_seconds": round(best, 4)}
+
+
+def cpu_baseline(x, dims, ranks, p, seed):
+    """Oracle (CPU port of the reference, 1 thread, -O3, no -march) on a
+    bounded sample: the same C2 tensor, HOSVD + 1 HOOI sweep; GNNZ/s of that
+    sweep."""
+    import numpy as np
+
+    import oracle as O
+
+    xh = x.cpu().numpy().astype(np.float64).reshape(dims, order="F")
+    t0 = time.perf_counter()
+    model, sp = O.mach_hooi(O.Dense(xh), ranks, p, seed, 1, 0.0)
+    wall = time.perf_counter() - t0
+    sample_s, hosvd_s, sweeps = O.phase_times()
+    return {"value": round(sp.nnz / sweeps[0] / 1e9, 6), "unit": "GNNZ/s", "cores": 1, "kind": "port",
+            "sample": f"C2 full tensor: sample {sample_s:.2f}s, HOSVD {hosvd_s:.2f}s, 1 sweep {sweeps[0]:.2f}s "
+                      f"(value = nnz / sweep time); total {wall:.1f}s"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference algorithm (CPU oracle port) on host cores
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle as O
+    from paper_0909_4969_b200.synth import CONFIGS
+
+    dims, ranks, noise, p, sweeps, dtype = CONFIGS[args.config]
+    try:
+        import torch
+        if torch.cuda.is_available():
+            from paper_0909_4969_b200.synth import lowrank_torch
+            x = lowrank_torch(dims, ranks, noise, seed=2, dtype=dtype).cpu().numpy()
+            src = "same device generator as the mach arm"
+        else:
+            raise RuntimeError
+    except Exception:
+        from paper_0909_4969_b200.synth import lowrank_numpy
+        x = lowrank_numpy(dims, ranks, noise, seed=2, dtype=np.float32 if dtype == "float32" else np.float64)
+        x = x.reshape(-1, order="F")
+        src = "numpy generator (same shape/distribution)"
+    xh = x.astype(np.float64).reshape(dims, order="F")
+    t0 = time.perf_counter()
+    total = args.warmup + args.steps
+    model, sp = O.mach_hooi(O.Dense(xh), ranks, p, 7, total, 0.0)
+    wall = time.perf_counter() - t0
+    sample_s, hosvd_s, sw = O.phase_times()
+    timed = sw[args.warmup: args.warmup + args.steps] or sw[-1:]
+    ms = 1e3 * sum(timed) / len(timed)
+    nnz = sp.nnz
+    value = nnz / (ms * 1e-3) / 1e9
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GNNZ/s", "n_gpus": world,
+           "steps": len(timed), "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": f"synthetic low-rank + noise ({src})",
+           "config": {"workload": f"{args.config.upper()}: {'x'.join(map(str, dims))}, ranks {ranks}, MACH p={p}, "
+                                  "step = one HOOI sweep", "nnz": nnz},
+           "cpu_baseline": {"value": round(value, 6), "unit": "GNNZ/s", "cores": 1, "kind": "port",
+                            "sample": f"full {args.config.upper()} job, {len(sw)} sweeps timed per sweep "
+                                      f"(sample {sample_s:.2f}s, HOSVD {hosvd_s:.2f}s, wall {wall:.1f}s); the "
+                                      "reference itself cannot build here (Eigen3 absent), this is its oracle "
+                                      "restatement built with the reference flags (-O3, 1 thread)"},
+           "e2e": {"value": round(nnz * len(sw) / wall / 1e9, 6), "unit": "GNNZ/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_mach(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

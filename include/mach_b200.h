@@ -1,0 +1,166 @@
+/*
+ * mach_b200.h — C ABI of the B200-native MACH sampler + Tucker (HOSVD/HOOI)
+ * hot path.  Plain pointers, sizes and opaque handles; no C++ or torch types.
+ *
+ * The reference exposes this path as C++ value-semantics functions in
+ * /root/reference/proj/include/mach/{tensor,sampling,tucker,linalg}.hpp.
+ * Each entry point below names the reference interface it replaces.  The C++
+ * mirror of that interface (include/mach/*.hpp, same names and exceptions) is
+ * implemented on top of this ABI inside libmach_b200.so.
+ *
+ * Conventions
+ *  - Dense tensors are first-mode-fastest (tensor.hpp:10-12); matrices are
+ *    column-major (tensor.hpp:77-105); sparse entries are flat indices.
+ *  - Every function returns a mach_status; on failure mach_last_error()
+ *    returns a thread-local message and, for MACH_ERR_CONVERGENCE,
+ *    mach_last_error_index() the 1-based singular index
+ *    (errors.hpp:37-45).  No exception crosses this boundary.
+ *  - Handles are device-resident (HBM) and bound to the context's device and
+ *    stream.  Host buffers are caller-owned.
+ */
+#ifndef MACH_B200_H
+#define MACH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MACH_OK = 0,
+    MACH_ERR_ARGUMENT = 1,    /* mach::ArgumentError (errors.hpp:9-13)    */
+    MACH_ERR_SHAPE = 2,       /* mach::ShapeError (errors.hpp:15-19)      */
+    MACH_ERR_CONVERGENCE = 3, /* mach::ConvergenceError (errors.hpp:37-45)*/
+    MACH_ERR_CUDA = 4,
+    MACH_ERR_OOM = 5,
+    MACH_ERR_NCCL = 6,
+    MACH_ERR_INTERNAL = 7
+} mach_status;
+
+typedef enum { MACH_F32 = 0, MACH_F64 = 1 } mach_dtype;
+
+typedef struct mach_ctx mach_ctx;       /* device + stream                   */
+typedef struct mach_dense mach_dense;   /* DenseTensor in HBM                */
+typedef struct mach_sparse mach_sparse; /* canonical SparseTensor in HBM     */
+typedef struct mach_model mach_model;   /* TuckerModel in HBM (+host scalars) */
+
+/* ---- errors / context --------------------------------------------------- */
+const char* mach_last_error(void);
+int mach_last_error_index(void);
+const char* mach_version(void);
+
+mach_status mach_ctx_create(int device, mach_ctx** out);
+mach_status mach_ctx_destroy(mach_ctx* ctx);
+/* Run all work of this context on an external cudaStream_t (NULL = own). */
+mach_status mach_ctx_set_stream(mach_ctx* ctx, void* cuda_stream);
+mach_status mach_ctx_synchronize(mach_ctx* ctx);
+/* Number of kernels this library launched on the context (bench evidence). */
+mach_status mach_ctx_launch_count(mach_ctx* ctx, int64_t* out);
+
+/* ---- dense tensors: DenseTensor (tensor.hpp:13-39) ----------------------- */
+/* Copy a host tensor into HBM; values must be finite (tensor.cpp:60-65).    */
+mach_status mach_dense_upload(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims,
+                              const void* host, mach_dense** out);
+/* Wrap caller-owned device memory (no copy, not freed by mach_dense_free).   */
+mach_status mach_dense_wrap(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims,
+                            void* device_ptr, mach_dense** out);
+mach_status mach_dense_download(const mach_dense* t, void* host);
+mach_status mach_dense_free(mach_dense* t);
+
+/* ---- sampler: sparsify (sampling.hpp:22, sampling.cpp:21-31) ------------- */
+/* Keep x_i != 0 iff counter_uniform01(seed, i) < p; value x_i / p (fp64
+ * division, rounded to the tensor dtype).  Output ascending flat index.     */
+mach_status mach_sparsify(mach_ctx* ctx, const mach_dense* x, double p, uint64_t seed,
+                          mach_sparse** out);
+/* Same, with host input and host output (the reference call end to end).   */
+mach_status mach_sparsify_host(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims,
+                               const void* host_x, double p, uint64_t seed, int64_t* nnz_out,
+                               int64_t** idx_out, double** val_out);
+void mach_free_host(void* p);
+
+/* ---- sparse tensors: SparseTensor (tensor.hpp:48-75) --------------------- */
+/* From host flat-index entries; canonicalised (sorted, merged, zeros
+ * dropped) like tensor.cpp:78-96.                                           */
+mach_status mach_sparse_upload(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims,
+                               int64_t nnz, const int64_t* idx, const double* vals,
+                               mach_sparse** out);
+mach_status mach_sparse_nnz(const mach_sparse* s, int64_t* nnz);
+mach_status mach_sparse_download(const mach_sparse* s, int64_t* idx, double* vals);
+/* tensor_norm(SparseTensor) (tensor.hpp:114, tensor.cpp:166-171).           */
+mach_status mach_sparse_norm(const mach_sparse* s, double* out);
+mach_status mach_sparse_free(mach_sparse* s);
+
+/* ---- decompositions (tucker.hpp:34-44, sampling.hpp:32-36) -------------- */
+mach_status mach_hosvd_sparse(mach_ctx* ctx, const mach_sparse* t, const int* ranks,
+                              mach_model** out);
+mach_status mach_hosvd_dense(mach_ctx* ctx, const mach_dense* t, const int* ranks,
+                             mach_model** out);
+mach_status mach_hooi_sparse(mach_ctx* ctx, const mach_sparse* t, const int* ranks,
+                             int max_iterations, double fit_tolerance, mach_model** out);
+mach_status mach_hooi_dense(mach_ctx* ctx, const mach_dense* t, const int* ranks,
+                            int max_iterations, double fit_tolerance, mach_model** out);
+/* mach_hooi (sampling.cpp:41-47): sparsify then hooi; *sampled optional.    */
+mach_status mach_mach_hooi(mach_ctx* ctx, const mach_dense* t, const int* ranks, double p,
+                           uint64_t seed, int max_iterations, double fit_tolerance,
+                           mach_model** out, mach_sparse** sampled);
+mach_status mach_mach_hosvd(mach_ctx* ctx, const mach_dense* t, const int* ranks, double p,
+                            uint64_t seed, mach_model** out, mach_sparse** sampled);
+
+/* ---- incremental HOOI: hooi_loop (tucker.cpp:80-106) split into begin /
+ *      step so sweeps can be driven (and timed) one at a time -------------- */
+typedef struct mach_session mach_session;
+/* setup (per-mode layouts) + HOSVD initialisation (tucker.cpp:152-169).     */
+mach_status mach_hooi_begin(mach_ctx* ctx, const mach_sparse* t, const int* ranks, mach_session** out);
+mach_status mach_hooi_begin_dense(mach_ctx* ctx, const mach_dense* t, const int* ranks,
+                                  mach_session** out);
+/* Up to n sweeps with the reference stop rule (fit - prev < tol ends the
+ * iteration, tucker.cpp:102); *done = sweeps run, *stopped = rule fired.    */
+mach_status mach_hooi_step(mach_session* s, int n, double fit_tolerance, int* done, int* stopped);
+mach_status mach_hooi_state(mach_session* s, double* fit, int* iterations);
+mach_status mach_hooi_model(mach_session* s, mach_model** out);
+mach_status mach_session_free(mach_session* s);
+
+/* ---- per-kernel device timing (CUDA events on the context stream) -------- */
+mach_status mach_ctx_profile(mach_ctx* ctx, int enable);
+/* i-th kernel name with its launch count and summed device milliseconds;
+ * returns MACH_ERR_ARGUMENT past the end.  Resets with enable=1.           */
+mach_status mach_ctx_kernel_stat(mach_ctx* ctx, int i, char* name, size_t len, int64_t* launches,
+                                 double* total_ms);
+
+/* ---- model access (TuckerModel, tucker.hpp:14-22) ------------------------ */
+mach_status mach_model_info(const mach_model* m, int* order, int* iterations, double* fit,
+                            int* n_sweep_fits, int* n_warnings);
+mach_status mach_model_dims(const mach_model* m, int* dims, int* ranks);
+mach_status mach_model_core(const mach_model* m, double* host);          /* prod(ranks) */
+mach_status mach_model_factor(const mach_model* m, int mode, double* host); /* I x r    */
+mach_status mach_model_sweep_fits(const mach_model* m, double* host);
+mach_status mach_model_warning(const mach_model* m, int i, char* buf, size_t len);
+/* Per-phase device times of the last run (ms): sample, setup, hosvd, sweeps. */
+mach_status mach_model_times(const mach_model* m, double* sample_ms, double* setup_ms,
+                             double* hosvd_ms, double* sweep_ms, int max_sweeps);
+mach_status mach_model_free(mach_model* m);
+
+/* ---- model evaluation (tucker.hpp:47-55) --------------------------------- */
+/* accuracy(t, model) = 1 - |t - reconstruct(model)| / |t|                   */
+mach_status mach_accuracy(mach_ctx* ctx, const mach_dense* t, const mach_model* m, double* out);
+/* reconstruct(model) into a new dense fp64 tensor                           */
+mach_status mach_reconstruct(mach_ctx* ctx, const mach_model* m, mach_dense** out);
+
+/* ---- linear algebra building blocks (linalg.hpp:42, tensor.hpp:121-132) -- */
+/* left_singular_basis of a host column-major rows x cols fp64 matrix, on
+ * device; basis rows x k, sv k; numerical_rank / completed as in the ref.  */
+mach_status mach_left_singular_basis(mach_ctx* ctx, int rows, int cols, const double* a, int k,
+                                     double* basis, double* sv, int* numerical_rank,
+                                     int* completed);
+/* mode_product(DenseTensor / SparseTensor, Matrix, mode) -> new dense fp64   */
+mach_status mach_mode_product_dense(mach_ctx* ctx, const mach_dense* t, int rows, int cols,
+                                    const double* m, int mode, mach_dense** out);
+mach_status mach_mode_product_sparse(mach_ctx* ctx, const mach_sparse* t, int rows, int cols,
+                                     const double* m, int mode, mach_dense** out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MACH_B200_H */

@@ -1,0 +1,112 @@
+"""ctypes binding of libmach_b200.so (C ABI: include/mach_b200.h).
+
+The shared library is built in-tree (``make -C paper_0909_4969_b200``); this
+module never falls back to anything else — a missing or unloadable library is
+an ImportError/OSError at first use.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libmach_b200.so")
+HEADER = os.path.join(ROOT, "include", "mach_b200.h")
+
+_lib = None
+
+MACH_OK, MACH_ERR_ARGUMENT, MACH_ERR_SHAPE, MACH_ERR_CONVERGENCE = 0, 1, 2, 3
+MACH_ERR_CUDA, MACH_ERR_OOM, MACH_ERR_NCCL, MACH_ERR_INTERNAL = 4, 5, 6, 7
+MACH_F32, MACH_F64 = 0, 1
+
+
+def build(force: bool = False) -> str:
+    """Compile every CUDA source for sm_100a into libmach_b200.so (in-tree)."""
+    if force:
+        subprocess.run(["make", "-s", "-C", HERE, "clean"], check=True)
+    subprocess.run(["make", "-s", "-j8", "-C", HERE], check=True)
+    return LIB_PATH
+
+
+vp = C.c_void_p
+vpp = C.POINTER(C.c_void_p)
+ip = C.POINTER(C.c_int)
+dp = C.POINTER(C.c_double)
+i64 = C.c_int64
+i64p = C.POINTER(C.c_int64)
+
+_SIGS = {
+    "mach_last_error": (C.c_char_p, []),
+    "mach_last_error_index": (C.c_int, []),
+    "mach_version": (C.c_char_p, []),
+    "mach_ctx_create": (C.c_int, [C.c_int, vpp]),
+    "mach_ctx_destroy": (C.c_int, [vp]),
+    "mach_ctx_set_stream": (C.c_int, [vp, vp]),
+    "mach_ctx_synchronize": (C.c_int, [vp]),
+    "mach_ctx_launch_count": (C.c_int, [vp, i64p]),
+    "mach_dense_upload": (C.c_int, [vp, C.c_int, C.c_int, ip, vp, vpp]),
+    "mach_dense_wrap": (C.c_int, [vp, C.c_int, C.c_int, ip, vp, vpp]),
+    "mach_dense_download": (C.c_int, [vp, vp]),
+    "mach_dense_free": (C.c_int, [vp]),
+    "mach_sparsify": (C.c_int, [vp, vp, C.c_double, C.c_uint64, vpp]),
+    "mach_sparsify_host": (C.c_int, [vp, C.c_int, C.c_int, ip, vp, C.c_double, C.c_uint64, i64p,
+                                     C.POINTER(i64p), C.POINTER(dp)]),
+    "mach_free_host": (None, [vp]),
+    "mach_sparse_upload": (C.c_int, [vp, C.c_int, C.c_int, ip, i64, i64p, dp, vpp]),
+    "mach_sparse_nnz": (C.c_int, [vp, i64p]),
+    "mach_sparse_download": (C.c_int, [vp, i64p, dp]),
+    "mach_sparse_norm": (C.c_int, [vp, dp]),
+    "mach_sparse_free": (C.c_int, [vp]),
+    "mach_hosvd_sparse": (C.c_int, [vp, vp, ip, vpp]),
+    "mach_hosvd_dense": (C.c_int, [vp, vp, ip, vpp]),
+    "mach_hooi_sparse": (C.c_int, [vp, vp, ip, C.c_int, C.c_double, vpp]),
+    "mach_hooi_dense": (C.c_int, [vp, vp, ip, C.c_int, C.c_double, vpp]),
+    "mach_mach_hooi": (C.c_int, [vp, vp, ip, C.c_double, C.c_uint64, C.c_int, C.c_double, vpp, vpp]),
+    "mach_mach_hosvd": (C.c_int, [vp, vp, ip, C.c_double, C.c_uint64, vpp, vpp]),
+    "mach_hooi_begin": (C.c_int, [vp, vp, ip, vpp]),
+    "mach_hooi_begin_dense": (C.c_int, [vp, vp, ip, vpp]),
+    "mach_hooi_step": (C.c_int, [vp, C.c_int, C.c_double, ip, ip]),
+    "mach_hooi_state": (C.c_int, [vp, dp, ip]),
+    "mach_hooi_model": (C.c_int, [vp, vpp]),
+    "mach_session_free": (C.c_int, [vp]),
+    "mach_ctx_profile": (C.c_int, [vp, C.c_int]),
+    "mach_ctx_kernel_stat": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t, i64p, dp]),
+    "mach_model_info": (C.c_int, [vp, ip, ip, dp, ip, ip]),
+    "mach_model_dims": (C.c_int, [vp, ip, ip]),
+    "mach_model_core": (C.c_int, [vp, dp]),
+    "mach_model_factor": (C.c_int, [vp, C.c_int, dp]),
+    "mach_model_sweep_fits": (C.c_int, [vp, dp]),
+    "mach_model_warning": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t]),
+    "mach_model_times": (C.c_int, [vp, dp, dp, dp, dp, C.c_int]),
+    "mach_model_free": (C.c_int, [vp]),
+    "mach_accuracy": (C.c_int, [vp, vp, vp, dp]),
+    "mach_reconstruct": (C.c_int, [vp, vp, vpp]),
+    "mach_left_singular_basis": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int, dp, dp, ip, ip]),
+    "mach_mode_product_dense": (C.c_int, [vp, vp, C.c_int, C.c_int, dp, C.c_int, vpp]),
+    "mach_mode_product_sparse": (C.c_int, [vp, vp, C.c_int, C.c_int, dp, C.c_int, vpp]),
+}
+
+
+def header_symbols() -> list[str]:
+    """Every function the C ABI header declares."""
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    txt = re.sub(r"//[^\n]*", "", txt)
+    return sorted(set(re.findall(r"\b(mach_[a-z0-9_]+)\s*\(", txt)))
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `make -C {HERE}` (or __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib

@@ -1,0 +1,498 @@
+"""Python face of the B200 MACH sampler + Tucker path.
+
+Names, argument meaning and errors follow the reference interface
+(/root/reference/proj/include/mach/{sampling,tucker,linalg,tensor}.hpp):
+``sparsify``, ``mach_hosvd``, ``mach_hooi``, ``hosvd``, ``hooi``,
+``accuracy``, ``reconstruct``, ``mode_product``, ``left_singular_basis``,
+``SparsifyConfig``, ``HooiConfig``, ``TuckerModel`` and the exception types
+``ArgumentError``, ``ShapeError``, ``ConvergenceError``.
+
+Every computation runs in libmach_b200.so on the GPU; tensors are
+device-resident handles.  Host arrays are numpy arrays whose flat order is
+first-mode-fastest (numpy ``order='F'``), exactly the reference layout.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+
+# ---------------------------------------------------------------------------
+# errors (proj/include/mach/errors.hpp:9-47)
+# ---------------------------------------------------------------------------
+class MachError(Exception):
+    code = -1
+
+
+class ArgumentError(MachError, ValueError):
+    code = L.MACH_ERR_ARGUMENT
+
+
+class ShapeError(MachError, ValueError):
+    code = L.MACH_ERR_SHAPE
+
+
+class ConvergenceError(MachError, RuntimeError):
+    code = L.MACH_ERR_CONVERGENCE
+
+    def __init__(self, msg: str, singular_index: int):
+        super().__init__(msg)
+        self.singular_index = singular_index
+
+
+class DeviceError(MachError, RuntimeError):
+    code = L.MACH_ERR_CUDA
+
+
+def _check(rc: int):
+    if rc == L.MACH_OK:
+        return
+    lib = L.lib()
+    msg = (lib.mach_last_error() or b"").decode()
+    if rc == L.MACH_ERR_ARGUMENT:
+        raise ArgumentError(msg)
+    if rc == L.MACH_ERR_SHAPE:
+        raise ShapeError(msg)
+    if rc == L.MACH_ERR_CONVERGENCE:
+        raise ConvergenceError(msg, lib.mach_last_error_index())
+    raise DeviceError(f"[{rc}] {msg}")
+
+
+# ---------------------------------------------------------------------------
+# context
+# ---------------------------------------------------------------------------
+class Context:
+    """Device + stream.  One per host thread (SURVEY §8b threading contract)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _check(L.lib().mach_ctx_create(int(device), C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def set_stream(self, cuda_stream_ptr: int | None):
+        _check(L.lib().mach_ctx_set_stream(self.h, C.c_void_p(cuda_stream_ptr or 0)))
+
+    def synchronize(self):
+        _check(L.lib().mach_ctx_synchronize(self.h))
+
+    @property
+    def launches(self) -> int:
+        n = C.c_int64()
+        _check(L.lib().mach_ctx_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.lib().mach_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def _ctx(ctx):
+    return ctx if ctx is not None else default_context()
+
+
+def _dims_arr(dims):
+    return (C.c_int * len(dims))(*[int(d) for d in dims])
+
+
+_DT = {np.dtype(np.float32): L.MACH_F32, np.dtype(np.float64): L.MACH_F64}
+
+
+# ---------------------------------------------------------------------------
+# tensors
+# ---------------------------------------------------------------------------
+class DenseTensor:
+    """Dense tensor in HBM, first mode fastest (tensor.hpp:13-39)."""
+
+    def __init__(self, h, dims, dtype, ctx, keepalive=None):
+        self.h, self.dims, self.dtype, self.ctx = h, tuple(dims), np.dtype(dtype), ctx
+        self._keepalive = keepalive
+
+    @classmethod
+    def from_numpy(cls, x: np.ndarray, ctx: Context | None = None, dtype=None):
+        ctx = _ctx(ctx)
+        x = np.asarray(x)
+        dt = np.dtype(dtype or (x.dtype if x.dtype in (np.float32, np.float64) else np.float64))
+        flat = np.ascontiguousarray(x.astype(dt, copy=False).reshape(-1, order="F"))
+        h = C.c_void_p()
+        _check(L.lib().mach_dense_upload(ctx.h, _DT[dt], x.ndim, _dims_arr(x.shape), flat.ctypes.data_as(C.c_void_p),
+                                         C.byref(h)))
+        return cls(h, x.shape, dt, ctx)
+
+    @classmethod
+    def from_torch(cls, flat, dims, ctx: Context | None = None):
+        """Zero-copy view of a CUDA torch tensor whose memory is first-mode-fastest."""
+        import torch
+
+        ctx = _ctx(ctx)
+        assert flat.is_cuda and flat.is_contiguous()
+        dt = {torch.float32: np.float32, torch.float64: np.float64}[flat.dtype]
+        h = C.c_void_p()
+        _check(L.lib().mach_dense_wrap(ctx.h, _DT[np.dtype(dt)], len(dims), _dims_arr(dims), C.c_void_p(flat.data_ptr()),
+                                       C.byref(h)))
+        return cls(h, dims, dt, ctx, keepalive=flat)
+
+    def numpy(self) -> np.ndarray:
+        out = np.empty(int(np.prod(self.dims)), dtype=self.dtype)
+        _check(L.lib().mach_dense_download(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out.reshape(self.dims, order="F")
+
+    def free(self):
+        if getattr(self, "h", None):
+            L.lib().mach_dense_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class SparseTensor:
+    """Canonical COO in HBM (tensor.hpp:48-75): ascending flat index."""
+
+    def __init__(self, h, dims, dtype, ctx):
+        self.h, self.dims, self.dtype, self.ctx = h, tuple(dims), np.dtype(dtype), ctx
+
+    @classmethod
+    def from_entries(cls, dims, idx, vals, dtype=np.float64, ctx: Context | None = None):
+        ctx = _ctx(ctx)
+        idx = np.ascontiguousarray(np.asarray(idx, dtype=np.int64))
+        vals = np.ascontiguousarray(np.asarray(vals, dtype=np.float64))
+        h = C.c_void_p()
+        _check(L.lib().mach_sparse_upload(ctx.h, _DT[np.dtype(dtype)], len(dims), _dims_arr(dims), len(idx),
+                                          idx.ctypes.data_as(L.i64p), vals.ctypes.data_as(L.dp), C.byref(h)))
+        return cls(h, dims, dtype, ctx)
+
+    @property
+    def nnz(self) -> int:
+        n = C.c_int64()
+        _check(L.lib().mach_sparse_nnz(self.h, C.byref(n)))
+        return n.value
+
+    def size(self) -> int:
+        return int(np.prod(self.dims))
+
+    def entries(self):
+        n = self.nnz
+        idx = np.empty(n, dtype=np.int64)
+        vals = np.empty(n, dtype=np.float64)
+        _check(L.lib().mach_sparse_download(self.h, idx.ctypes.data_as(L.i64p), vals.ctypes.data_as(L.dp)))
+        return idx, vals
+
+    def norm(self) -> float:
+        out = C.c_double()
+        _check(L.lib().mach_sparse_norm(self.h, C.byref(out)))
+        return out.value
+
+    def densify(self) -> np.ndarray:
+        idx, vals = self.entries()
+        out = np.zeros(self.size(), dtype=np.float64)
+        out[idx] = vals
+        return out.reshape(self.dims, order="F")
+
+    def free(self):
+        if getattr(self, "h", None):
+            L.lib().mach_sparse_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# configs / model (sampling.hpp:14-30, tucker.hpp:14-30)
+# ---------------------------------------------------------------------------
+@dataclass
+class SparsifyConfig:
+    p: float = 1.0
+    seed: int = 0
+
+
+@dataclass
+class HooiConfig:
+    max_iterations: int = 50
+    fit_tolerance: float = 1e-4
+
+
+@dataclass
+class TuckerModel:
+    core: np.ndarray
+    factors: list
+    ranks: tuple
+    iterations: int
+    fit: float
+    sweep_fits: list
+    warnings: list = field(default_factory=list)
+    times: dict = field(default_factory=dict)
+
+
+def _model_from(h) -> TuckerModel:
+    lib = L.lib()
+    order, iters, nfits, nwarn = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    fit = C.c_double()
+    try:
+        _check(lib.mach_model_info(h, C.byref(order), C.byref(iters), C.byref(fit), C.byref(nfits), C.byref(nwarn)))
+        d = order.value
+        dims = (C.c_int * d)()
+        ranks = (C.c_int * d)()
+        _check(lib.mach_model_dims(h, dims, ranks))
+        dims, ranks = tuple(dims), tuple(ranks)
+        core = np.empty(int(np.prod(ranks)))
+        _check(lib.mach_model_core(h, core.ctypes.data_as(L.dp)))
+        factors = []
+        for m in range(d):
+            f = np.empty(dims[m] * ranks[m])
+            _check(lib.mach_model_factor(h, m, f.ctypes.data_as(L.dp)))
+            factors.append(f.reshape((dims[m], ranks[m]), order="F"))
+        sf = np.empty(nfits.value)
+        _check(lib.mach_model_sweep_fits(h, sf.ctypes.data_as(L.dp)))
+        warns = []
+        for i in range(nwarn.value):
+            buf = C.create_string_buffer(512)
+            _check(lib.mach_model_warning(h, i, buf, 512))
+            warns.append(buf.value.decode())
+        sample, setup, hosvd_ms = C.c_double(), C.c_double(), C.c_double()
+        sw = (C.c_double * max(1, iters.value))()
+        _check(lib.mach_model_times(h, C.byref(sample), C.byref(setup), C.byref(hosvd_ms), sw, iters.value))
+        times = {"sample_ms": sample.value, "setup_ms": setup.value, "hosvd_ms": hosvd_ms.value,
+                 "sweep_ms": list(sw)[: iters.value]}
+        return TuckerModel(core.reshape(ranks, order="F"), factors, ranks, iters.value, fit.value, list(sf), warns,
+                           times)
+    finally:
+        lib.mach_model_free(h)
+
+
+# ---------------------------------------------------------------------------
+# entry points
+# ---------------------------------------------------------------------------
+def _dense(t, ctx):
+    if isinstance(t, DenseTensor):
+        return t
+    return DenseTensor.from_numpy(np.asarray(t), ctx)
+
+
+def sparsify(t, cfg: SparsifyConfig | float = None, seed: int = 0, ctx: Context | None = None) -> SparseTensor:
+    """sampling.hpp:22 — keep x_i != 0 with probability p, rescaled by 1/p."""
+    if not isinstance(cfg, SparsifyConfig):
+        cfg = SparsifyConfig(1.0 if cfg is None else float(cfg), int(seed))
+    d = _dense(t, ctx)
+    h = C.c_void_p()
+    _check(L.lib().mach_sparsify(d.ctx.h, d.h, float(cfg.p), int(cfg.seed) & (2**64 - 1), C.byref(h)))
+    return SparseTensor(h, d.dims, d.dtype, d.ctx)
+
+
+def _ranks(ranks, d):
+    if len(ranks) != d:
+        raise ArgumentError("ranks must name one rank per mode")
+    return (C.c_int * d)(*[int(r) for r in ranks])
+
+
+def hosvd(t, ranks, ctx: Context | None = None) -> TuckerModel:
+    """tucker.hpp:34,39 — HOSVD of a dense or sparse tensor."""
+    h = C.c_void_p()
+    if isinstance(t, SparseTensor):
+        _check(L.lib().mach_hosvd_sparse(t.ctx.h, t.h, _ranks(ranks, len(t.dims)), C.byref(h)))
+    else:
+        d = _dense(t, ctx)
+        _check(L.lib().mach_hosvd_dense(d.ctx.h, d.h, _ranks(ranks, len(d.dims)), C.byref(h)))
+    return _model_from(h)
+
+
+def hooi(t, ranks, cfg: HooiConfig | None = None, ctx: Context | None = None, max_iterations=None,
+         fit_tolerance=None) -> TuckerModel:
+    """tucker.hpp:43-44 — HOSVD init then alternating sweeps."""
+    cfg = cfg or HooiConfig()
+    mi = cfg.max_iterations if max_iterations is None else max_iterations
+    tol = cfg.fit_tolerance if fit_tolerance is None else fit_tolerance
+    h = C.c_void_p()
+    if isinstance(t, SparseTensor):
+        _check(L.lib().mach_hooi_sparse(t.ctx.h, t.h, _ranks(ranks, len(t.dims)), int(mi), float(tol), C.byref(h)))
+    else:
+        d = _dense(t, ctx)
+        _check(L.lib().mach_hooi_dense(d.ctx.h, d.h, _ranks(ranks, len(d.dims)), int(mi), float(tol), C.byref(h)))
+    return _model_from(h)
+
+
+@dataclass
+class MachResult:
+    model: TuckerModel
+    sparsified: SparseTensor
+
+
+def mach_hooi(t, ranks, scfg: SparsifyConfig, hcfg: HooiConfig | None = None, ctx: Context | None = None) -> MachResult:
+    """sampling.hpp:35-36 — sparsify then hooi; returns both."""
+    hcfg = hcfg or HooiConfig()
+    d = _dense(t, ctx)
+    hm, hs = C.c_void_p(), C.c_void_p()
+    _check(L.lib().mach_mach_hooi(d.ctx.h, d.h, _ranks(ranks, len(d.dims)), float(scfg.p), int(scfg.seed),
+                                  int(hcfg.max_iterations), float(hcfg.fit_tolerance), C.byref(hm), C.byref(hs)))
+    return MachResult(_model_from(hm), SparseTensor(hs, d.dims, d.dtype, d.ctx))
+
+
+def mach_hosvd(t, ranks, scfg: SparsifyConfig, ctx: Context | None = None) -> MachResult:
+    """sampling.hpp:32-33."""
+    d = _dense(t, ctx)
+    hm, hs = C.c_void_p(), C.c_void_p()
+    _check(L.lib().mach_mach_hosvd(d.ctx.h, d.h, _ranks(ranks, len(d.dims)), float(scfg.p), int(scfg.seed),
+                                   C.byref(hm), C.byref(hs)))
+    return MachResult(_model_from(hm), SparseTensor(hs, d.dims, d.dtype, d.ctx))
+
+
+def reconstruct(model: TuckerModel, ctx: Context | None = None) -> np.ndarray:
+    """tucker.hpp:50 — core x_1 U_1 ... x_d U_d (device mode products)."""
+    y = DenseTensor.from_numpy(np.asarray(model.core, dtype=np.float64), ctx)
+    for m, f in enumerate(model.factors):
+        y = mode_product(y, f, m, ctx=ctx, keep_on_device=True)
+    return y.numpy()
+
+
+def accuracy(t, model: TuckerModel, ctx: Context | None = None) -> float:
+    """tucker.hpp:55 — 1 - |t - reconstruct(model)| / |t|."""
+    x = t.numpy() if isinstance(t, DenseTensor) else np.asarray(t, dtype=np.float64)
+    nt = float(np.sqrt((x.astype(np.float64) ** 2).sum()))
+    if nt == 0.0:
+        raise ArgumentError("accuracy needs a reference tensor with nonzero norm")
+    rec = reconstruct(model, ctx)
+    if rec.shape != x.shape:
+        raise ShapeError("model reconstructs to a different shape")
+    return 1.0 - float(np.sqrt(((x - rec) ** 2).sum())) / nt
+
+
+def mode_product(t, m: np.ndarray, mode: int, ctx: Context | None = None, keep_on_device=False):
+    """tensor.hpp:129,132 — t x_mode m (m is J x I_mode)."""
+    mf = np.asfortranarray(np.asarray(m, dtype=np.float64))
+    flat = np.ascontiguousarray(mf.reshape(-1, order="F"))
+    h = C.c_void_p()
+    if isinstance(t, SparseTensor):
+        dims, c = t.dims, t.ctx
+        _check(L.lib().mach_mode_product_sparse(c.h, t.h, mf.shape[0], mf.shape[1], flat.ctypes.data_as(L.dp), int(mode),
+                                                C.byref(h)))
+    else:
+        d = _dense(t, ctx)
+        dims, c = d.dims, d.ctx
+        _check(L.lib().mach_mode_product_dense(c.h, d.h, mf.shape[0], mf.shape[1], flat.ctypes.data_as(L.dp), int(mode),
+                                               C.byref(h)))
+    od = list(dims)
+    od[mode] = mf.shape[0]
+    out = DenseTensor(h, od, np.float64, c)
+    return out if keep_on_device else out.numpy()
+
+
+@dataclass
+class LeftSingularBasis:
+    basis: np.ndarray
+    singular_values: np.ndarray
+    numerical_rank: int
+    completed: bool
+
+
+def left_singular_basis(m: np.ndarray, k: int, ctx: Context | None = None) -> LeftSingularBasis:
+    """linalg.hpp:42 — on-device eigen step for a host matrix."""
+    ctx = _ctx(ctx)
+    m = np.asarray(m, dtype=np.float64)
+    if m.ndim != 2 or m.shape[0] < 1 or m.shape[1] < 1:
+        raise ArgumentError("matrix must be nonempty")
+    rows, cols = m.shape
+    if k < 1 or k > rows:
+        raise ArgumentError("k must satisfy 1 <= k <= rows")
+    flat = np.ascontiguousarray(m.reshape(-1, order="F"))
+    basis = np.empty(rows * k)
+    sv = np.empty(k)
+    nr, comp = C.c_int(), C.c_int()
+    _check(L.lib().mach_left_singular_basis(ctx.h, rows, cols, flat.ctypes.data_as(L.dp), int(k),
+                                            basis.ctypes.data_as(L.dp), sv.ctypes.data_as(L.dp), C.byref(nr),
+                                            C.byref(comp)))
+    return LeftSingularBasis(basis.reshape((rows, k), order="F"), sv, nr.value, bool(comp.value))
+
+
+# ---------------------------------------------------------------------------
+# incremental HOOI (hooi_loop split into begin / step), for streaming use and
+# for timing sweeps one by one
+# ---------------------------------------------------------------------------
+class HooiSession:
+    """Setup + HOSVD on construction; ``step(n)`` runs sweeps with the
+    reference stop rule (tucker.cpp:102)."""
+
+    def __init__(self, t, ranks, ctx: Context | None = None):
+        h = C.c_void_p()
+        if isinstance(t, SparseTensor):
+            self.ctx = t.ctx
+            _check(L.lib().mach_hooi_begin(t.ctx.h, t.h, _ranks(ranks, len(t.dims)), C.byref(h)))
+        else:
+            d = _dense(t, ctx)
+            self.ctx = d.ctx
+            _check(L.lib().mach_hooi_begin_dense(d.ctx.h, d.h, _ranks(ranks, len(d.dims)), C.byref(h)))
+        self.h = h
+        self._src = t
+
+    def step(self, n: int = 1, fit_tolerance: float = 0.0):
+        done, stopped = C.c_int(), C.c_int()
+        _check(L.lib().mach_hooi_step(self.h, int(n), float(fit_tolerance), C.byref(done), C.byref(stopped)))
+        return done.value, bool(stopped.value)
+
+    @property
+    def fit(self) -> float:
+        f, it = C.c_double(), C.c_int()
+        _check(L.lib().mach_hooi_state(self.h, C.byref(f), C.byref(it)))
+        return f.value
+
+    def model(self) -> TuckerModel:
+        hm = C.c_void_p()
+        _check(L.lib().mach_hooi_model(self.h, C.byref(hm)))
+        return _model_from(hm)
+
+    def free(self):
+        if getattr(self, "h", None):
+            L.lib().mach_session_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def profile(ctx: Context, enable: bool = True):
+    _check(L.lib().mach_ctx_profile(ctx.h, 1 if enable else 0))
+
+
+def kernel_stats(ctx: Context) -> dict:
+    """{kernel name: (launches, total device ms)} since profile(ctx, True)."""
+    out = {}
+    i = 0
+    while True:
+        buf = C.create_string_buffer(256)
+        n, ms = C.c_int64(), C.c_double()
+        rc = L.lib().mach_ctx_kernel_stat(ctx.h, i, buf, 256, C.byref(n), C.byref(ms))
+        if rc != L.MACH_OK:
+            break
+        out[buf.value.decode()] = (n.value, ms.value)
+        i += 1
+    return out

@@ -1,0 +1,532 @@
+// C ABI of libmach_b200 (include/mach_b200.h).  Every entry point catches,
+// maps the error to a mach_status and stores the message thread-locally; no
+// exception crosses the boundary.
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace machb {
+mach_sparse* sample_dense(const mach_dense* x, double p, std::uint64_t seed);
+mach_model* tucker_sparse(mach_sparse* X, const std::vector<int>& ranks, bool do_hooi, int max_it, double tol);
+mach_model* tucker_dense(const mach_dense* X, const std::vector<int>& ranks, bool do_hooi, int max_it, double tol);
+double accuracy_dev(const mach_dense* t, const mach_model* m);
+mach_dense* reconstruct_model(Ctx* ctx, const mach_model* m);
+void lsb_host(Ctx* ctx, int rows, int cols, const double* a, int k, double* basis, double* sv, int* nr, int* completed);
+mach_dense* mode_product_dev(Ctx* ctx, const mach_dense* t, const mach_sparse* s, int rows, int cols, const double* m,
+                             int mode);
+mach_sparse* sparse_from_host(Ctx* ctx, int dtype, const std::vector<int>& dims, std::int64_t nnz, const std::int64_t* idx,
+                              const double* vals);
+void sparse_to_host(const mach_sparse* s, std::int64_t* idx, double* vals);
+void check_finite_upload(Ctx* ctx, int dtype, const void* dev, std::int64_t n);
+}  // namespace machb
+
+using namespace machb;
+
+namespace {
+thread_local std::string g_err;
+thread_local int g_err_index = 0;
+
+template <typename F>
+mach_status guard(F&& f) {
+    try {
+        f();
+        return MACH_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        g_err_index = e.index;
+        return static_cast<mach_status>(e.code);
+    } catch (const std::bad_alloc& e) {
+        g_err = e.what();
+        return MACH_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return MACH_ERR_INTERNAL;
+    }
+}
+
+std::vector<int> dims_of(int order, const int* dims) {
+    if (order < 1 || !dims) throw_arg("tensor must have at least one mode");
+    return std::vector<int>(dims, dims + order);
+}
+
+void need(const void* p, const char* what) {
+    if (!p) throw_arg(std::string(what) + " must not be null");
+}
+}  // namespace
+
+extern "C" {
+
+const char* mach_last_error(void) { return g_err.c_str(); }
+int mach_last_error_index(void) { return g_err_index; }
+const char* mach_version(void) { return "mach-b200 0.1 (sm_100a)"; }
+
+mach_status mach_ctx_create(int device, mach_ctx** out) {
+    return guard([&] {
+        need(out, "out");
+        auto c = std::make_unique<mach_ctx>();
+        c->c.device = device;
+        MB_CUDA(cudaSetDevice(device));
+        MB_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+        c->c.own_stream = true;
+        *out = c.release();
+    });
+}
+
+mach_status mach_ctx_destroy(mach_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaStreamSynchronize(ctx->c.stream);
+        if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+        delete ctx;
+    });
+}
+
+mach_status mach_ctx_set_stream(mach_ctx* ctx, void* stream) {
+    return guard([&] {
+        need(ctx, "ctx");
+        MB_CUDA(cudaStreamSynchronize(ctx->c.stream));
+        if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+        if (stream) {
+            ctx->c.stream = static_cast<cudaStream_t>(stream);
+            ctx->c.own_stream = false;
+        } else {
+            MB_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+            ctx->c.own_stream = true;
+        }
+    });
+}
+
+mach_status mach_ctx_synchronize(mach_ctx* ctx) {
+    return guard([&] {
+        need(ctx, "ctx");
+        sync(&ctx->c);
+    });
+}
+
+mach_status mach_ctx_launch_count(mach_ctx* ctx, int64_t* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        *out = ctx->c.launches;
+    });
+}
+
+// ---- dense ----
+mach_status mach_dense_upload(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims, const void* host,
+                              mach_dense** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        auto t = std::make_unique<mach_dense>();
+        t->ctx = &ctx->c;
+        t->dtype = dtype;
+        t->dims = dims_of(order, dims);
+        t->numel = checked_size(t->dims);
+        need(host, "host");
+        const std::size_t bytes = static_cast<std::size_t>(t->numel) * dtype_size(dtype);
+        MB_CUDA(cudaMallocAsync(&t->data, bytes, ctx->c.stream));
+        MB_CUDA(cudaMemcpyAsync(t->data, host, bytes, cudaMemcpyHostToDevice, ctx->c.stream));
+        t->owns = true;
+        check_finite_upload(&ctx->c, dtype, t->data, t->numel);
+        *out = t.release();
+    });
+}
+
+mach_status mach_dense_wrap(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims, void* dev, mach_dense** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        need(dev, "device_ptr");
+        auto t = std::make_unique<mach_dense>();
+        t->ctx = &ctx->c;
+        t->dtype = dtype;
+        t->dims = dims_of(order, dims);
+        t->numel = checked_size(t->dims);
+        t->data = dev;
+        t->owns = false;
+        *out = t.release();
+    });
+}
+
+mach_status mach_dense_download(const mach_dense* t, void* host) {
+    return guard([&] {
+        need(t, "tensor");
+        need(host, "host");
+        MB_CUDA(cudaMemcpyAsync(host, t->data, static_cast<std::size_t>(t->numel) * dtype_size(t->dtype),
+                                cudaMemcpyDeviceToHost, t->ctx->stream));
+        sync(t->ctx);
+    });
+}
+
+mach_status mach_dense_free(mach_dense* t) {
+    return guard([&] {
+        if (!t) return;
+        if (t->owns && t->data) cudaFreeAsync(t->data, t->ctx->stream);
+        delete t;
+    });
+}
+
+// ---- sampler ----
+mach_status mach_sparsify(mach_ctx* ctx, const mach_dense* x, double p, uint64_t seed, mach_sparse** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(x, "tensor");
+        need(out, "out");
+        *out = sample_dense(x, p, seed);
+    });
+}
+
+mach_status mach_sparsify_host(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims, const void* host_x, double p,
+                               uint64_t seed, int64_t* nnz_out, int64_t** idx_out, double** val_out) {
+    mach_dense* x = nullptr;
+    mach_sparse* s = nullptr;
+    mach_status st = mach_dense_upload(ctx, dtype, order, dims, host_x, &x);
+    if (st != MACH_OK) return st;
+    st = mach_sparsify(ctx, x, p, seed, &s);
+    if (st == MACH_OK) {
+        st = guard([&] {
+            *nnz_out = s->nnz;
+            *idx_out = static_cast<int64_t*>(std::malloc(static_cast<std::size_t>(std::max<int64_t>(1, s->nnz)) * 8));
+            *val_out = static_cast<double*>(std::malloc(static_cast<std::size_t>(std::max<int64_t>(1, s->nnz)) * 8));
+            sparse_to_host(s, *idx_out, *val_out);
+        });
+    }
+    mach_sparse_free(s);
+    mach_dense_free(x);
+    return st;
+}
+
+void mach_free_host(void* p) { std::free(p); }
+
+// ---- sparse ----
+mach_status mach_sparse_upload(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims, int64_t nnz,
+                               const int64_t* idx, const double* vals, mach_sparse** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        if (nnz < 0) throw_arg("nnz must be >= 0");
+        if (nnz > 0) {
+            need(idx, "idx");
+            need(vals, "vals");
+        }
+        *out = sparse_from_host(&ctx->c, dtype, dims_of(order, dims), nnz, idx, vals);
+    });
+}
+
+mach_status mach_sparse_nnz(const mach_sparse* s, int64_t* nnz) {
+    return guard([&] {
+        need(s, "tensor");
+        *nnz = s->nnz;
+    });
+}
+
+mach_status mach_sparse_download(const mach_sparse* s, int64_t* idx, double* vals) {
+    return guard([&] {
+        need(s, "tensor");
+        sparse_to_host(s, idx, vals);
+    });
+}
+
+mach_status mach_sparse_norm(const mach_sparse* s, double* out);
+
+mach_status mach_sparse_free(mach_sparse* s) {
+    return guard([&] { delete s; });
+}
+
+// ---- decompositions ----
+static std::vector<int> ranks_of(int order, const int* ranks) {
+    need(ranks, "ranks");
+    return std::vector<int>(ranks, ranks + order);
+}
+
+mach_status mach_hosvd_sparse(mach_ctx* ctx, const mach_sparse* t, const int* ranks, mach_model** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(t, "tensor");
+        need(out, "out");
+        *out = tucker_sparse(const_cast<mach_sparse*>(t), ranks_of(static_cast<int>(t->dims.size()), ranks), false, 1, 0.0);
+    });
+}
+
+mach_status mach_hosvd_dense(mach_ctx* ctx, const mach_dense* t, const int* ranks, mach_model** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(t, "tensor");
+        need(out, "out");
+        *out = tucker_dense(t, ranks_of(static_cast<int>(t->dims.size()), ranks), false, 1, 0.0);
+    });
+}
+
+mach_status mach_hooi_sparse(mach_ctx* ctx, const mach_sparse* t, const int* ranks, int max_iterations,
+                             double fit_tolerance, mach_model** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(t, "tensor");
+        need(out, "out");
+        *out = tucker_sparse(const_cast<mach_sparse*>(t), ranks_of(static_cast<int>(t->dims.size()), ranks), true,
+                             max_iterations, fit_tolerance);
+    });
+}
+
+mach_status mach_hooi_dense(mach_ctx* ctx, const mach_dense* t, const int* ranks, int max_iterations,
+                            double fit_tolerance, mach_model** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(t, "tensor");
+        need(out, "out");
+        *out = tucker_dense(t, ranks_of(static_cast<int>(t->dims.size()), ranks), true, max_iterations, fit_tolerance);
+    });
+}
+
+static mach_status mach_pipeline(mach_ctx* ctx, const mach_dense* t, const int* ranks, double p, uint64_t seed,
+                                 bool do_hooi, int max_it, double tol, mach_model** out, mach_sparse** sampled) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(t, "tensor");
+        need(out, "out");
+        cudaEvent_t a, b;
+        MB_CUDA(cudaEventCreate(&a));
+        MB_CUDA(cudaEventCreate(&b));
+        MB_CUDA(cudaEventRecord(a, ctx->c.stream));
+        std::unique_ptr<mach_sparse> s(sample_dense(t, p, seed));
+        MB_CUDA(cudaEventRecord(b, ctx->c.stream));
+        MB_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        mach_model* m = tucker_sparse(s.get(), ranks_of(static_cast<int>(t->dims.size()), ranks), do_hooi, max_it, tol);
+        m->sample_ms = ms;
+        *out = m;
+        if (sampled) *sampled = s.release();
+    });
+}
+
+mach_status mach_mach_hooi(mach_ctx* ctx, const mach_dense* t, const int* ranks, double p, uint64_t seed,
+                           int max_iterations, double fit_tolerance, mach_model** out, mach_sparse** sampled) {
+    return mach_pipeline(ctx, t, ranks, p, seed, true, max_iterations, fit_tolerance, out, sampled);
+}
+
+mach_status mach_mach_hosvd(mach_ctx* ctx, const mach_dense* t, const int* ranks, double p, uint64_t seed,
+                            mach_model** out, mach_sparse** sampled) {
+    return mach_pipeline(ctx, t, ranks, p, seed, false, 1, 0.0, out, sampled);
+}
+
+// ---- model ----
+mach_status mach_model_info(const mach_model* m, int* order, int* iterations, double* fit, int* n_sweep_fits,
+                            int* n_warnings) {
+    return guard([&] {
+        need(m, "model");
+        if (order) *order = m->order;
+        if (iterations) *iterations = m->iterations;
+        if (fit) *fit = m->fit;
+        if (n_sweep_fits) *n_sweep_fits = static_cast<int>(m->sweep_fits.size());
+        if (n_warnings) *n_warnings = static_cast<int>(m->warnings.size());
+    });
+}
+
+mach_status mach_model_dims(const mach_model* m, int* dims, int* ranks) {
+    return guard([&] {
+        need(m, "model");
+        for (int i = 0; i < m->order; ++i) {
+            if (dims) dims[i] = m->dims[static_cast<std::size_t>(i)];
+            if (ranks) ranks[i] = m->ranks[static_cast<std::size_t>(i)];
+        }
+    });
+}
+
+mach_status mach_model_core(const mach_model* m, double* host) {
+    return guard([&] {
+        need(m, "model");
+        std::memcpy(host, m->core.data(), m->core.size() * sizeof(double));
+    });
+}
+
+mach_status mach_model_factor(const mach_model* m, int mode, double* host) {
+    return guard([&] {
+        need(m, "model");
+        if (mode < 0 || mode >= m->order) throw_arg("mode out of range");
+        const auto& f = m->factors[static_cast<std::size_t>(mode)];
+        std::memcpy(host, f.data(), f.size() * sizeof(double));
+    });
+}
+
+mach_status mach_model_sweep_fits(const mach_model* m, double* host) {
+    return guard([&] {
+        need(m, "model");
+        std::memcpy(host, m->sweep_fits.data(), m->sweep_fits.size() * sizeof(double));
+    });
+}
+
+mach_status mach_model_warning(const mach_model* m, int i, char* buf, size_t len) {
+    return guard([&] {
+        need(m, "model");
+        if (i < 0 || i >= static_cast<int>(m->warnings.size())) throw_arg("warning index out of range");
+        if (len == 0) return;
+        std::strncpy(buf, m->warnings[static_cast<std::size_t>(i)].c_str(), len - 1);
+        buf[len - 1] = 0;
+    });
+}
+
+mach_status mach_model_times(const mach_model* m, double* sample_ms, double* setup_ms, double* hosvd_ms, double* sweep_ms,
+                             int max_sweeps) {
+    return guard([&] {
+        need(m, "model");
+        if (sample_ms) *sample_ms = m->sample_ms;
+        if (setup_ms) *setup_ms = m->setup_ms;
+        if (hosvd_ms) *hosvd_ms = m->hosvd_ms;
+        for (int i = 0; sweep_ms && i < max_sweeps && i < static_cast<int>(m->sweep_ms.size()); ++i)
+            sweep_ms[i] = m->sweep_ms[static_cast<std::size_t>(i)];
+    });
+}
+
+mach_status mach_model_free(mach_model* m) {
+    return guard([&] { delete m; });
+}
+
+mach_status mach_accuracy(mach_ctx* ctx, const mach_dense* t, const mach_model* m, double* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(t, "tensor");
+        need(m, "model");
+        *out = accuracy_dev(t, m);
+    });
+}
+
+mach_status mach_reconstruct(mach_ctx* ctx, const mach_model* m, mach_dense** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(m, "model");
+        *out = reconstruct_model(&ctx->c, m);
+    });
+}
+
+mach_status mach_left_singular_basis(mach_ctx* ctx, int rows, int cols, const double* a, int k, double* basis, double* sv,
+                                     int* numerical_rank, int* completed) {
+    return guard([&] {
+        need(ctx, "ctx");
+        lsb_host(&ctx->c, rows, cols, a, k, basis, sv, numerical_rank, completed);
+    });
+}
+
+mach_status mach_mode_product_dense(mach_ctx* ctx, const mach_dense* t, int rows, int cols, const double* m, int mode,
+                                    mach_dense** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(t, "tensor");
+        *out = mode_product_dev(&ctx->c, t, nullptr, rows, cols, m, mode);
+    });
+}
+
+mach_status mach_mode_product_sparse(mach_ctx* ctx, const mach_sparse* t, int rows, int cols, const double* m, int mode,
+                                     mach_dense** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(t, "tensor");
+        *out = mode_product_dev(&ctx->c, nullptr, t, rows, cols, m, mode);
+    });
+}
+
+}  // extern "C"
+
+// ---- sessions + profiling ----
+namespace machb {
+void* session_sparse(mach_sparse* X, const std::vector<int>& ranks);
+void* session_dense(const mach_dense* X, const std::vector<int>& ranks);
+int session_step(void* s, int n, double tol);
+mach_model* session_snapshot(void* s);
+void session_free(void* s);
+int session_iterations(void* s);
+double session_fit(void* s);
+bool session_stopped(void* s);
+}  // namespace machb
+
+struct mach_session {
+    void* s = nullptr;
+};
+
+extern "C" {
+
+mach_status mach_hooi_begin(mach_ctx* ctx, const mach_sparse* t, const int* ranks, mach_session** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(t, "tensor");
+        need(out, "out");
+        auto h = std::make_unique<mach_session>();
+        h->s = session_sparse(const_cast<mach_sparse*>(t), ranks_of(static_cast<int>(t->dims.size()), ranks));
+        *out = h.release();
+    });
+}
+
+mach_status mach_hooi_begin_dense(mach_ctx* ctx, const mach_dense* t, const int* ranks, mach_session** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(t, "tensor");
+        need(out, "out");
+        auto h = std::make_unique<mach_session>();
+        h->s = session_dense(t, ranks_of(static_cast<int>(t->dims.size()), ranks));
+        *out = h.release();
+    });
+}
+
+mach_status mach_hooi_step(mach_session* s, int n, double tol, int* done, int* stopped) {
+    return guard([&] {
+        need(s, "session");
+        if (n < 0) throw_arg("n must be >= 0");
+        const int k = session_step(s->s, n, tol);
+        if (done) *done = k;
+        if (stopped) *stopped = session_stopped(s->s) ? 1 : 0;
+    });
+}
+
+mach_status mach_hooi_state(mach_session* s, double* fit, int* iterations) {
+    return guard([&] {
+        need(s, "session");
+        if (fit) *fit = session_fit(s->s);
+        if (iterations) *iterations = session_iterations(s->s);
+    });
+}
+
+mach_status mach_hooi_model(mach_session* s, mach_model** out) {
+    return guard([&] {
+        need(s, "session");
+        need(out, "out");
+        *out = session_snapshot(s->s);
+    });
+}
+
+mach_status mach_session_free(mach_session* s) {
+    return guard([&] {
+        if (!s) return;
+        session_free(s->s);
+        delete s;
+    });
+}
+
+mach_status mach_ctx_profile(mach_ctx* ctx, int enable) {
+    return guard([&] {
+        need(ctx, "ctx");
+        ctx->c.resolve();
+        ctx->c.profile = enable != 0;
+        if (enable) ctx->c.stats.clear();
+    });
+}
+
+mach_status mach_ctx_kernel_stat(mach_ctx* ctx, int i, char* name, size_t len, int64_t* launches, double* total_ms) {
+    return guard([&] {
+        need(ctx, "ctx");
+        ctx->c.resolve();
+        if (i < 0 || i >= static_cast<int>(ctx->c.stats.size())) throw_arg("kernel index out of range");
+        auto it = ctx->c.stats.begin();
+        std::advance(it, i);
+        if (name && len) {
+            std::strncpy(name, it->first.c_str(), len - 1);
+            name[len - 1] = 0;
+        }
+        if (launches) *launches = it->second.launches;
+        if (total_ms) *total_ms = it->second.ms;
+    });
+}
+
+}  // extern "C"

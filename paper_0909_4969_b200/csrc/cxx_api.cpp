@@ -1,0 +1,436 @@
+// C++ drop-in for the reference API (include/mach/*.hpp mirrors
+// /root/reference/proj/include/mach/*.hpp).  Value types stay on the host;
+// every computation goes through the C ABI onto the B200 (thread-local
+// context on device MACH_DEVICE, default 0).  C ABI status codes are rethrown
+// as the reference's exception types.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <string>
+
+#include "mach/errors.hpp"
+#include "mach/linalg.hpp"
+#include "mach/sampling.hpp"
+#include "mach/tensor.hpp"
+#include "mach/tucker.hpp"
+#include "mach_b200.h"
+
+namespace mach {
+
+namespace {
+
+void rethrow(mach_status st) {
+    if (st == MACH_OK) return;
+    std::string msg = mach_last_error();
+    switch (st) {
+        case MACH_ERR_ARGUMENT: throw ArgumentError(msg);
+        case MACH_ERR_SHAPE: throw ShapeError(msg);
+        case MACH_ERR_CONVERGENCE: {
+            const auto p = msg.rfind(" (singular index ");
+            if (p != std::string::npos) msg = msg.substr(0, p);
+            throw ConvergenceError(msg, mach_last_error_index());
+        }
+        default: throw std::runtime_error("mach-b200: " + msg);
+    }
+}
+
+struct CtxHolder {
+    mach_ctx* ctx = nullptr;
+    CtxHolder() {
+        const char* dev = std::getenv("MACH_DEVICE");
+        rethrow(mach_ctx_create(dev ? std::atoi(dev) : 0, &ctx));
+    }
+    ~CtxHolder() { mach_ctx_destroy(ctx); }
+};
+
+mach_ctx* ctx() {
+    thread_local CtxHolder h;
+    return h.ctx;
+}
+
+std::int64_t checked_size(const std::vector<int>& dims) {
+    if (dims.empty()) throw ArgumentError("tensor must have at least one mode");
+    std::int64_t n = 1;
+    for (int d : dims) {
+        if (d < 1) throw ArgumentError("every dimension must be >= 1");
+        if (n > std::numeric_limits<std::int64_t>::max() / d) throw ArgumentError("shape product overflows");
+        n *= d;
+    }
+    return n;
+}
+
+struct DenseH {
+    mach_dense* h = nullptr;
+    explicit DenseH(const DenseTensor& t) {
+        rethrow(mach_dense_upload(ctx(), MACH_F64, t.order(), t.dims().data(), t.data(), &h));
+    }
+    ~DenseH() { mach_dense_free(h); }
+};
+
+struct SparseH {
+    mach_sparse* h = nullptr;
+    explicit SparseH(const SparseTensor& t) {
+        std::vector<std::int64_t> idx(static_cast<std::size_t>(t.nnz()));
+        std::vector<double> val(static_cast<std::size_t>(t.nnz()));
+        for (std::size_t i = 0; i < idx.size(); ++i) {
+            idx[i] = t.entries()[i].index;
+            val[i] = t.entries()[i].value;
+        }
+        rethrow(mach_sparse_upload(ctx(), MACH_F64, t.order(), t.dims().data(), t.nnz(), idx.data(), val.data(), &h));
+    }
+    explicit SparseH(mach_sparse* p) : h(p) {}
+    ~SparseH() { mach_sparse_free(h); }
+};
+
+DenseTensor from_device(mach_dense* d, const std::vector<int>& dims) {
+    std::vector<double> v(static_cast<std::size_t>(checked_size(dims)));
+    const mach_status st = mach_dense_download(d, v.data());
+    mach_dense_free(d);
+    rethrow(st);
+    return DenseTensor(dims, std::move(v));
+}
+
+SparseTensor sparse_to_value(mach_sparse* s, const std::vector<int>& dims) {
+    std::int64_t nnz = 0;
+    rethrow(mach_sparse_nnz(s, &nnz));
+    std::vector<std::int64_t> idx(static_cast<std::size_t>(nnz));
+    std::vector<double> val(static_cast<std::size_t>(nnz));
+    rethrow(mach_sparse_download(s, idx.data(), val.data()));
+    std::vector<SparseEntry> e(static_cast<std::size_t>(nnz));
+    for (std::size_t i = 0; i < e.size(); ++i) e[i] = {idx[i], val[i]};
+    return SparseTensor::from_canonical(dims, std::move(e));
+}
+
+TuckerModel model_to_value(mach_model* m) {
+    int order = 0, iters = 0, nfits = 0, nwarn = 0;
+    double fit = 0;
+    rethrow(mach_model_info(m, &order, &iters, &fit, &nfits, &nwarn));
+    std::vector<int> dims(static_cast<std::size_t>(order)), ranks(static_cast<std::size_t>(order));
+    rethrow(mach_model_dims(m, dims.data(), ranks.data()));
+    TuckerModel out;
+    std::vector<double> core(static_cast<std::size_t>(checked_size(ranks)));
+    rethrow(mach_model_core(m, core.data()));
+    out.core = DenseTensor(ranks, std::move(core));
+    for (int q = 0; q < order; ++q) {
+        Matrix f(dims[static_cast<std::size_t>(q)], ranks[static_cast<std::size_t>(q)]);
+        rethrow(mach_model_factor(m, q, f.data()));
+        out.factors.push_back(std::move(f));
+    }
+    out.ranks = ranks;
+    out.iterations = iters;
+    out.fit = fit;
+    out.sweep_fits.resize(static_cast<std::size_t>(nfits));
+    rethrow(mach_model_sweep_fits(m, out.sweep_fits.data()));
+    for (int i = 0; i < nwarn; ++i) {
+        char buf[512];
+        rethrow(mach_model_warning(m, i, buf, sizeof buf));
+        out.warnings.emplace_back(buf);
+    }
+    mach_model_free(m);
+    return out;
+}
+
+}  // namespace
+
+// ---- DenseTensor / SparseTensor / Matrix (tensor.cpp:47-147 contracts) ----
+DenseTensor::DenseTensor(std::vector<int> dims)
+    : dims_(std::move(dims)), values_(static_cast<std::size_t>(checked_size(dims_)), 0.0) {}
+
+DenseTensor::DenseTensor(std::vector<int> dims, std::vector<double> values) : dims_(std::move(dims)), values_(std::move(values)) {
+    if (static_cast<std::int64_t>(values_.size()) != checked_size(dims_))
+        throw ShapeError("value count does not match shape product");
+    for (double x : values_)
+        if (!std::isfinite(x)) throw ArgumentError("tensor values must be finite");
+}
+
+std::int64_t DenseTensor::flat_index(std::span<const int> index) const {
+    if (index.size() != dims_.size()) throw ArgumentError("multi-index order mismatch");
+    std::int64_t f = 0, stride = 1;
+    for (std::size_t m = 0; m < dims_.size(); ++m) {
+        if (index[m] < 0 || index[m] >= dims_[m]) throw ArgumentError("multi-index out of bounds");
+        f += index[m] * stride;
+        stride *= dims_[m];
+    }
+    return f;
+}
+
+SparseTensor::SparseTensor(std::vector<int> dims, std::vector<SparseEntry> entries) : dims_(std::move(dims)) {
+    // canonicalise on the device (sort, merge, drop zeros)
+    std::vector<std::int64_t> idx(entries.size());
+    std::vector<double> val(entries.size());
+    for (std::size_t i = 0; i < entries.size(); ++i) {
+        idx[i] = entries[i].index;
+        val[i] = entries[i].value;
+    }
+    mach_sparse* s = nullptr;
+    rethrow(mach_sparse_upload(ctx(), MACH_F64, static_cast<int>(dims_.size()), dims_.data(),
+                               static_cast<std::int64_t>(idx.size()), idx.data(), val.data(), &s));
+    SparseH guard(s);
+    *this = sparse_to_value(s, dims_);
+    guard.h = s;
+}
+
+SparseTensor::SparseTensor(std::vector<int> dims, const std::vector<std::pair<std::vector<int>, double>>& entries)
+    : SparseTensor(dims, [&] {
+          std::vector<SparseEntry> flat;
+          flat.reserve(entries.size());
+          for (const auto& [idx, v] : entries) {
+              if (idx.size() != dims.size()) throw ArgumentError("multi-index order mismatch");
+              std::int64_t f = 0, stride = 1;
+              for (std::size_t m = 0; m < idx.size(); ++m) {
+                  if (idx[m] < 0 || idx[m] >= dims[m]) throw ArgumentError("multi-index out of bounds");
+                  f += idx[m] * stride;
+                  stride *= dims[m];
+              }
+              flat.push_back({f, v});
+          }
+          return flat;
+      }()) {}
+
+SparseTensor SparseTensor::from_canonical(std::vector<int> dims, std::vector<SparseEntry> entries) {
+    SparseTensor t;
+    t.dims_ = std::move(dims);
+    t.entries_ = std::move(entries);
+    return t;
+}
+
+std::int64_t SparseTensor::size() const noexcept {
+    std::int64_t n = 1;
+    for (int d : dims_) n *= d;
+    return n;
+}
+
+std::vector<int> SparseTensor::multi_index(std::int64_t flat) const {
+    std::vector<int> idx(dims_.size());
+    for (std::size_t m = 0; m < dims_.size(); ++m) {
+        idx[m] = static_cast<int>(flat % dims_[m]);
+        flat /= dims_[m];
+    }
+    return idx;
+}
+
+Matrix::Matrix(int rows, int cols) : rows_(rows), cols_(cols) {
+    if (rows < 0 || cols < 0) throw ArgumentError("matrix dimensions must be nonnegative");
+    values_.assign(static_cast<std::size_t>(rows) * static_cast<std::size_t>(cols), 0.0);
+}
+
+Matrix::Matrix(int rows, int cols, std::vector<double> values) : rows_(rows), cols_(cols), values_(std::move(values)) {
+    if (rows < 0 || cols < 0) throw ArgumentError("matrix dimensions must be nonnegative");
+    if (values_.size() != static_cast<std::size_t>(rows) * static_cast<std::size_t>(cols))
+        throw ShapeError("value count does not match rows*cols");
+}
+
+Matrix Matrix::identity(int n) {
+    Matrix m(n, n);
+    for (int i = 0; i < n; ++i) m(i, i) = 1.0;
+    return m;
+}
+
+Matrix transpose(const Matrix& m) {
+    Matrix t(m.cols(), m.rows());
+    for (int c = 0; c < m.cols(); ++c)
+        for (int r = 0; r < m.rows(); ++r) t(c, r) = m(r, c);
+    return t;
+}
+
+double frobenius_norm(const Matrix& m) {
+    double s = 0.0;
+    for (double x : m.values()) s += x * x;
+    return std::sqrt(s);
+}
+
+double tensor_norm(const DenseTensor& t) {
+    double s = 0.0;
+    for (double x : t.values()) s += x * x;
+    return std::sqrt(s);
+}
+
+double tensor_norm(const SparseTensor& t) {
+    SparseH h(t);
+    double n = 0.0;
+    rethrow(mach_sparse_norm(h.h, &n));
+    return n;
+}
+
+double inner_product(const DenseTensor& x, const DenseTensor& y) {
+    if (x.dims() != y.dims()) throw ShapeError("inner_product requires identical shapes");
+    double s = 0.0;
+    for (std::int64_t i = 0; i < x.size(); ++i) s += x.data()[i] * y.data()[i];
+    return s;
+}
+
+Matrix matricize(const DenseTensor& t, int mode) {
+    if (mode < 0 || mode >= t.order()) throw ArgumentError("mode out of range");
+    std::int64_t inner = 1, outer = 1;
+    for (int m = 0; m < mode; ++m) inner *= t.dim(m);
+    for (int m = mode + 1; m < t.order(); ++m) outer *= t.dim(m);
+    const int len = t.dim(mode);
+    Matrix out(len, static_cast<int>(inner * outer));
+    for (std::int64_t c = 0; c < outer; ++c)
+        for (int r = 0; r < len; ++r)
+            for (std::int64_t a = 0; a < inner; ++a)
+                out(r, static_cast<int>(a + inner * c)) = t.data()[a + inner * (r + static_cast<std::int64_t>(len) * c)];
+    return out;
+}
+
+DenseTensor refold(const Matrix& m, int mode, const std::vector<int>& dims) {
+    if (mode < 0 || mode >= static_cast<int>(dims.size())) throw ArgumentError("mode out of range");
+    std::int64_t inner = 1, outer = 1;
+    for (int q = 0; q < mode; ++q) inner *= dims[static_cast<std::size_t>(q)];
+    for (int q = mode + 1; q < static_cast<int>(dims.size()); ++q) outer *= dims[static_cast<std::size_t>(q)];
+    const int len = dims[static_cast<std::size_t>(mode)];
+    if (m.rows() != len || static_cast<std::int64_t>(m.cols()) != inner * outer)
+        throw ShapeError("matrix shape does not match refold target dims");
+    DenseTensor t(dims);
+    for (std::int64_t c = 0; c < outer; ++c)
+        for (int r = 0; r < len; ++r)
+            for (std::int64_t a = 0; a < inner; ++a)
+                t.data()[a + inner * (r + static_cast<std::int64_t>(len) * c)] = m(r, static_cast<int>(a + inner * c));
+    return t;
+}
+
+DenseTensor mode_product(const DenseTensor& t, const Matrix& m, int mode) {
+    DenseH h(t);
+    mach_dense* out = nullptr;
+    rethrow(mach_mode_product_dense(ctx(), h.h, m.rows(), m.cols(), m.data(), mode, &out));
+    std::vector<int> od = t.dims();
+    od[static_cast<std::size_t>(mode)] = m.rows();
+    return from_device(out, od);
+}
+
+DenseTensor mode_product(const SparseTensor& t, const Matrix& m, int mode) {
+    SparseH h(t);
+    mach_dense* out = nullptr;
+    rethrow(mach_mode_product_sparse(ctx(), h.h, m.rows(), m.cols(), m.data(), mode, &out));
+    std::vector<int> od = t.dims();
+    od[static_cast<std::size_t>(mode)] = m.rows();
+    return from_device(out, od);
+}
+
+DenseTensor densify(const SparseTensor& s) {
+    DenseTensor t(s.dims());
+    for (const auto& e : s.entries()) t.data()[e.index] = e.value;
+    return t;
+}
+
+SparseTensor sparsify_exact(const DenseTensor& t) {
+    std::vector<SparseEntry> e;
+    for (std::int64_t i = 0; i < t.size(); ++i)
+        if (t.data()[i] != 0.0) e.push_back({i, t.data()[i]});
+    return SparseTensor::from_canonical(t.dims(), std::move(e));
+}
+
+// ---- sampling.hpp ----
+SparseTensor sparsify(const DenseTensor& t, const SparsifyConfig& cfg) {
+    DenseH h(t);
+    mach_sparse* s = nullptr;
+    rethrow(mach_sparsify(ctx(), h.h, cfg.p, cfg.seed, &s));
+    SparseH g(s);
+    return sparse_to_value(s, t.dims());
+}
+
+MachResult mach_hosvd(const DenseTensor& t, const std::vector<int>& ranks, const SparsifyConfig& cfg) {
+    DenseH h(t);
+    mach_model* m = nullptr;
+    mach_sparse* s = nullptr;
+    if (ranks.size() != t.dims().size()) throw ArgumentError("ranks must name one rank per mode");
+    rethrow(mach_mach_hosvd(ctx(), h.h, ranks.data(), cfg.p, cfg.seed, &m, &s));
+    SparseH g(s);
+    MachResult r;
+    r.sparsified = sparse_to_value(s, t.dims());
+    r.model = model_to_value(m);
+    return r;
+}
+
+MachResult mach_hooi(const DenseTensor& t, const std::vector<int>& ranks, const SparsifyConfig& scfg, const HooiConfig& hcfg) {
+    DenseH h(t);
+    mach_model* m = nullptr;
+    mach_sparse* s = nullptr;
+    if (ranks.size() != t.dims().size()) throw ArgumentError("ranks must name one rank per mode");
+    rethrow(mach_mach_hooi(ctx(), h.h, ranks.data(), scfg.p, scfg.seed, hcfg.max_iterations, hcfg.fit_tolerance, &m, &s));
+    SparseH g(s);
+    MachResult r;
+    r.sparsified = sparse_to_value(s, t.dims());
+    r.model = model_to_value(m);
+    return r;
+}
+
+// ---- tucker.hpp ----
+TuckerModel hosvd(const DenseTensor& t, const std::vector<int>& ranks) {
+    if (ranks.size() != t.dims().size()) throw ArgumentError("ranks must name one rank per mode");
+    DenseH h(t);
+    mach_model* m = nullptr;
+    rethrow(mach_hosvd_dense(ctx(), h.h, ranks.data(), &m));
+    return model_to_value(m);
+}
+
+TuckerModel hosvd(const SparseTensor& t, const std::vector<int>& ranks) {
+    if (ranks.size() != t.dims().size()) throw ArgumentError("ranks must name one rank per mode");
+    SparseH h(t);
+    mach_model* m = nullptr;
+    rethrow(mach_hosvd_sparse(ctx(), h.h, ranks.data(), &m));
+    return model_to_value(m);
+}
+
+TuckerModel hooi(const DenseTensor& t, const std::vector<int>& ranks, const HooiConfig& cfg) {
+    if (ranks.size() != t.dims().size()) throw ArgumentError("ranks must name one rank per mode");
+    DenseH h(t);
+    mach_model* m = nullptr;
+    rethrow(mach_hooi_dense(ctx(), h.h, ranks.data(), cfg.max_iterations, cfg.fit_tolerance, &m));
+    return model_to_value(m);
+}
+
+TuckerModel hooi(const SparseTensor& t, const std::vector<int>& ranks, const HooiConfig& cfg) {
+    if (ranks.size() != t.dims().size()) throw ArgumentError("ranks must name one rank per mode");
+    SparseH h(t);
+    mach_model* m = nullptr;
+    rethrow(mach_hooi_sparse(ctx(), h.h, ranks.data(), cfg.max_iterations, cfg.fit_tolerance, &m));
+    return model_to_value(m);
+}
+
+DenseTensor core_tensor(const DenseTensor& t, const std::vector<Matrix>& factors) {
+    if (static_cast<int>(factors.size()) != t.order()) throw ArgumentError("one factor per mode required");
+    DenseTensor y = t;
+    for (int m = 0; m < t.order(); ++m) y = mode_product(y, transpose(factors[static_cast<std::size_t>(m)]), m);
+    return y;
+}
+
+DenseTensor reconstruct(const TuckerModel& model) {
+    DenseTensor y = model.core;
+    for (int m = 0; m < model.core.order(); ++m) y = mode_product(y, model.factors[static_cast<std::size_t>(m)], m);
+    return y;
+}
+
+double accuracy(const DenseTensor& t, const TuckerModel& model) {
+    const double nt = tensor_norm(t);
+    if (nt == 0.0) throw ArgumentError("accuracy needs a reference tensor with nonzero norm");
+    DenseTensor rec = reconstruct(model);
+    if (rec.dims() != t.dims()) throw ShapeError("model reconstructs to a different shape");
+    double s = 0.0;
+    for (std::int64_t i = 0; i < t.size(); ++i) {
+        const double d = t.data()[i] - rec.data()[i];
+        s += d * d;
+    }
+    return 1.0 - std::sqrt(s) / nt;
+}
+
+// ---- linalg.hpp ----
+LeftSingularBasis left_singular_basis(const Matrix& m, int k) {
+    if (m.rows() < 1 || m.cols() < 1) throw ArgumentError("matrix must be nonempty");
+    if (k < 1 || k > m.rows()) throw ArgumentError("k must satisfy 1 <= k <= rows");
+    LeftSingularBasis out;
+    out.basis = Matrix(m.rows(), k);
+    out.singular_values.assign(static_cast<std::size_t>(k), 0.0);
+    int nr = 0, comp = 0;
+    rethrow(mach_left_singular_basis(ctx(), m.rows(), m.cols(), m.data(), k, out.basis.data(), out.singular_values.data(),
+                                     &nr, &comp));
+    out.numerical_rank = nr;
+    out.completed = comp != 0;
+    return out;
+}
+
+void set_thread_count(int) {}
+
+}  // namespace mach

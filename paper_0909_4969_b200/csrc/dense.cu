@@ -1,0 +1,180 @@
+// Dense route (reference: hosvd/hooi(DenseTensor), tucker.cpp:135-150,
+// :171-180, and the dense pieces of the sparse route: mode_product
+// tensor.cpp:224-239, matricize :180-200, densify :261-266, the entrywise fit
+// tucker.cpp:40-64 and reconstruct :204-209).  Taken when a sampled tensor
+// keeps >= 25% of its entries (kDensifyThreshold, tucker.cpp:66-69).
+// Intermediates are fp64; each output is summed by one thread in a fixed
+// order, so results are reproducible bit for bit.
+#include "sparse_ttm.cuh"
+
+namespace machb {
+
+namespace {
+
+struct Split3 {
+    long long inner, outer;
+    int len;
+};
+
+Split3 split3(const std::vector<int>& dims, int mode) {
+    Split3 s{1, 1, dims[static_cast<std::size_t>(mode)]};
+    for (int m = 0; m < mode; ++m) s.inner *= dims[static_cast<std::size_t>(m)];
+    for (int m = mode + 1; m < static_cast<int>(dims.size()); ++m) s.outer *= dims[static_cast<std::size_t>(m)];
+    return s;
+}
+
+template <typename Tin>
+__global__ void mode_product_kernel(const Tin* __restrict__ in, long long inner, int len, long long outer,
+                                    const double* __restrict__ U, int J, int transpose, double* __restrict__ out) {
+    const long long total = inner * J * outer;
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long a = idx % inner;
+        const long long rest = idx / inner;
+        const int q = static_cast<int>(rest % J);
+        const long long c = rest / J;
+        const Tin* src = in + a + inner * len * c;
+        double s = 0.0;
+        if (transpose) {
+            const double* u = U + static_cast<long long>(q) * len;  // U is len x J
+            for (int r = 0; r < len; ++r) s += static_cast<double>(src[inner * r]) * u[r];
+        } else {
+            for (int r = 0; r < len; ++r) s += static_cast<double>(src[inner * r]) * U[q + static_cast<long long>(J) * r];
+        }
+        out[idx] = s;
+    }
+}
+
+template <typename Tin, typename Tout>
+__global__ void matricize_kernel(const Tin* __restrict__ in, long long inner, int len, long long outer,
+                                 Tout* __restrict__ out) {
+    const long long total = inner * len * outer;
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        // idx walks the source (coalesced reads); out(r, a + inner*c) = in[a + inner*(r + len*c)]
+        const long long a = idx % inner;
+        const long long rest = idx / inner;
+        const int r = static_cast<int>(rest % len);
+        const long long c = rest / len;
+        out[r + static_cast<long long>(len) * (a + inner * c)] = static_cast<Tout>(in[idx]);
+    }
+}
+
+template <typename T, typename IdxT>
+__global__ void densify_kernel(const IdxT* __restrict__ idx, const T* __restrict__ val, long long nnz, T* __restrict__ out) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i < nnz) out[idx[i]] = val[i];
+}
+
+template <typename T, typename IdxT>
+__global__ void scatter_sub_kernel(const IdxT* __restrict__ idx, const T* __restrict__ val, long long nnz,
+                                   double* __restrict__ out) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i < nnz) out[idx[i]] -= static_cast<double>(val[i]);
+}
+
+constexpr int kRedBlocks = 1024;
+
+template <typename T>
+__global__ void __launch_bounds__(256) sumsq_diff_kernel(const T* __restrict__ x, const double* __restrict__ y, long long n,
+                                                         double* __restrict__ part) {
+    __shared__ double red[8];
+    double s = 0.0;
+    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * kRedBlocks) {
+        const double dlt = static_cast<double>(x[i]) - y[i];
+        s += dlt * dlt;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < 8; ++i) t += red[i];
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) sum_final2_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+    __shared__ double red[8];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += 256) s += part[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < 8; ++i) t += red[i];
+        *out = t;
+    }
+}
+
+int grid_for(long long n) {
+    long long b = (n + 255) / 256;
+    if (b > 148 * 64) b = 148 * 64;
+    if (b < 1) b = 1;
+    return static_cast<int>(b);
+}
+
+}  // namespace
+
+template <typename Tin>
+void dense_mode_product(Ctx* ctx, const Tin* in, const std::vector<int>& dims, int mode, const double* U, int J,
+                        bool transpose, double* out) {
+    const Split3 s = split3(dims, mode);
+    const long long total = s.inner * J * s.outer;
+    if (total == 0) return;
+    MB_LAUNCH(ctx, mode_product_kernel<Tin>, grid_for(total), 256, 0, in, s.inner, s.len, s.outer, U, J,
+              transpose ? 1 : 0, out);
+}
+template void dense_mode_product<float>(Ctx*, const float*, const std::vector<int>&, int, const double*, int, bool, double*);
+template void dense_mode_product<double>(Ctx*, const double*, const std::vector<int>&, int, const double*, int, bool, double*);
+
+template <typename Tin, typename Tout>
+void dense_matricize(Ctx* ctx, const Tin* in, const std::vector<int>& dims, int mode, Tout* out) {
+    const Split3 s = split3(dims, mode);
+    const long long total = s.inner * s.len * s.outer;
+    if (total == 0) return;
+    MB_LAUNCH(ctx, (matricize_kernel<Tin, Tout>), grid_for(total), 256, 0, in, s.inner, s.len, s.outer, out);
+}
+template void dense_matricize<float, float>(Ctx*, const float*, const std::vector<int>&, int, float*);
+template void dense_matricize<double, double>(Ctx*, const double*, const std::vector<int>&, int, double*);
+template void dense_matricize<float, double>(Ctx*, const float*, const std::vector<int>&, int, double*);
+
+template <typename T>
+void densify(Ctx* ctx, const mach_sparse* X, T* out) {
+    MB_CUDA(cudaMemsetAsync(out, 0, static_cast<std::size_t>(X->numel) * sizeof(T), ctx->stream));
+    if (X->nnz == 0) return;
+    if (X->idx64)
+        MB_LAUNCH(ctx, (densify_kernel<T, unsigned long long>), ceil_div(X->nnz, 256), 256, 0,
+                  static_cast<const unsigned long long*>(X->idx), static_cast<const T*>(X->val), X->nnz, out);
+    else
+        MB_LAUNCH(ctx, (densify_kernel<T, unsigned int>), ceil_div(X->nnz, 256), 256, 0,
+                  static_cast<const unsigned int*>(X->idx), static_cast<const T*>(X->val), X->nnz, out);
+}
+template void densify<float>(Ctx*, const mach_sparse*, float*);
+template void densify<double>(Ctx*, const mach_sparse*, double*);
+
+template <typename T>
+void scatter_sub(Ctx* ctx, const mach_sparse* X, double* dense) {
+    if (X->nnz == 0) return;
+    if (X->idx64)
+        MB_LAUNCH(ctx, (scatter_sub_kernel<T, unsigned long long>), ceil_div(X->nnz, 256), 256, 0,
+                  static_cast<const unsigned long long*>(X->idx), static_cast<const T*>(X->val), X->nnz, dense);
+    else
+        MB_LAUNCH(ctx, (scatter_sub_kernel<T, unsigned int>), ceil_div(X->nnz, 256), 256, 0,
+                  static_cast<const unsigned int*>(X->idx), static_cast<const T*>(X->val), X->nnz, dense);
+}
+template void scatter_sub<float>(Ctx*, const mach_sparse*, double*);
+template void scatter_sub<double>(Ctx*, const mach_sparse*, double*);
+
+template <typename T>
+void sumsq_diff(Ctx* ctx, const T* x, const double* y, long long n, double* scratch, double* out) {
+    MB_LAUNCH(ctx, sumsq_diff_kernel<T>, kRedBlocks, 256, 0, x, y, n, scratch);
+    MB_LAUNCH(ctx, sum_final2_kernel, 1, 256, 0, scratch, kRedBlocks, out);
+}
+template void sumsq_diff<float>(Ctx*, const float*, const double*, long long, double*, double*);
+template void sumsq_diff<double>(Ctx*, const double*, const double*, long long, double*, double*);
+
+}  // namespace machb

@@ -1,0 +1,386 @@
+// Device building blocks of the eigen step and the Tucker bookkeeping:
+//  - Gram of a matricized projection Y (row side Y Y^T or column side Y^T Y),
+//    fp64 accumulation (linalg.cpp:340, :348);
+//  - basis_from_side: numerical rank against kRankFloor, sign canonicalisation,
+//    deterministic completion (linalg.cpp:261-276, :18-32, :41-51);
+//  - orthonormal_columns / basis_from_products: twice Gram-Schmidt, rank and
+//    collapse floors, completion, sign (linalg.cpp:66-100, :283-296);
+//  - W = Y V, core = U_d^T Y_(d), deterministic sums of squares.
+// All reductions run in a fixed order, so results are bitwise reproducible.
+#include "common.cuh"
+
+namespace machb {
+
+namespace {
+constexpr double kRankFloor = 1e-6;      // linalg_internal.hpp:23
+constexpr double kCollapseFloor = 1e-3;  // linalg.cpp:37
+constexpr int kB = 256;                  // one-CTA kernels
+constexpr int kW = kB / 32;
+
+__device__ double cta_sum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < kW; ++i) s += red[i];
+    return s;
+}
+
+// index of the largest |u_i|, lowest index on ties (canonical_sign, linalg.cpp:18-32)
+__device__ int cta_argmax_abs(const double* u, int n, double* redv, int* redi) {
+    double best = -1.0;
+    int bi = 0x7fffffff;
+    for (int i = threadIdx.x; i < n; i += kB) {
+        const double a = fabs(u[i]);
+        if (a > best) { best = a; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) { redv[threadIdx.x >> 5] = best; redi[threadIdx.x >> 5] = bi; }
+    __syncthreads();
+    best = redv[0];
+    bi = redi[0];
+    for (int i = 1; i < kW; ++i)
+        if (redv[i] > best || (redv[i] == best && redi[i] < bi)) { best = redv[i]; bi = redi[i]; }
+    return bi;
+}
+
+// v -= B[:, :count] (B[:, :count]^T v), B column-major n x *, v in smem
+__device__ void cta_project_out(const double* B, int n, int count, double* v, double* tcoef, double* red) {
+    if (count <= 0) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    for (int c = warp; c < count; c += kW) {
+        const double* b = B + static_cast<std::size_t>(c) * n;
+        double s = 0.0;
+        for (int r = lane; r < n; r += 32) s += b[r] * v[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) tcoef[c] = s;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < n; r += kB) {
+        double s = v[r];
+        for (int c = 0; c < count; ++c) s -= B[r + static_cast<std::size_t>(c) * n] * tcoef[c];
+        v[r] = s;
+    }
+    __syncthreads();
+}
+
+// completion_column (linalg.cpp:41-51): lowest-index unit vector surviving
+// two projections against the first `count` columns; written to column count.
+__device__ bool cta_completion(double* B, int n, int count, double* v, double* tcoef, double* red) {
+    for (int e = 0; e < n; ++e) {
+        for (int r = threadIdx.x; r < n; r += kB) v[r] = (r == e) ? 1.0 : 0.0;
+        cta_project_out(B, n, count, v, tcoef, red);
+        cta_project_out(B, n, count, v, tcoef, red);
+        double s = 0.0;
+        for (int r = threadIdx.x; r < n; r += kB) s += v[r] * v[r];
+        const double nv = sqrt(cta_sum(s, red));
+        if (nv > 0.5) {
+            for (int r = threadIdx.x; r < n; r += kB) B[r + static_cast<std::size_t>(count) * n] = v[r] / nv;
+            __syncthreads();
+            return true;
+        }
+    }
+    return false;
+}
+
+__device__ void cta_canonical_sign(double* u, int n, double* redv, int* redi) {
+    const int p = cta_argmax_abs(u, n, redv, redi);
+    const bool flip = u[p] < 0.0;
+    __syncthreads();
+    if (flip)
+        for (int r = threadIdx.x; r < n; r += kB) u[r] = -u[r];
+    __syncthreads();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// G = A^T A with A(kk, j) = a[kk*sk + j*sn], A is K x N; G is N x N fp64.
+// 32x32 output tile per block, fixed-order accumulation over K.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ a, long long sk, long long sn, int K, int N,
+                                                   double* __restrict__ G) {
+    __shared__ double As[32][33];
+    __shared__ double Bs[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+    double acc[4] = {0, 0, 0, 0};
+    for (int k0 = 0; k0 < K; k0 += 32) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            int kk, jj;
+            if (sn == 1) { kk = ty + 8 * q; jj = tx; } else { kk = tx; jj = ty + 8 * q; }
+            const int gk = k0 + kk;
+            const int gi = i0 + jj, gj = j0 + jj;
+            As[kk][jj] = (gk < K && gi < N) ? static_cast<double>(a[gk * sk + gi * sn]) : 0.0;
+            Bs[kk][jj] = (gk < K && gj < N) ? static_cast<double>(a[gk * sk + gj * sn]) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < 32; ++kk) {
+            const double x = As[kk][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] += x * Bs[kk][ty + 8 * q];
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = i0 + tx, j = j0 + ty + 8 * q;
+        if (i < N && j < N) G[i + static_cast<std::size_t>(j) * N] = acc[q];
+    }
+}
+
+template <typename T>
+void gram(Ctx* ctx, const T* a, long long sk, long long sn, int K, int N, double* G) {
+    dim3 grid(ceil_div(N, 32), ceil_div(N, 32));
+    MB_LAUNCH(ctx, gram_kernel<T>, grid, 256, 0, a, sk, sn, K, N, G);
+}
+template void gram<float>(Ctx*, const float*, long long, long long, int, int, double*);
+template void gram<double>(Ctx*, const double*, long long, long long, int, int, double*);
+
+// ---------------------------------------------------------------------------
+// W (rows x kc, fp64) = Y (rows x C, col-major, T) * V (C x kc, fp64)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void matmul_yv_kernel(const T* __restrict__ Y, int rows, int C, const double* __restrict__ V, int kc,
+                                 double* __restrict__ W) {
+    const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (idx >= static_cast<long long>(rows) * kc) return;
+    const int i = static_cast<int>(idx % rows), c2 = static_cast<int>(idx / rows);
+    double s = 0.0;
+    for (int c = 0; c < C; ++c) s += static_cast<double>(Y[i + static_cast<std::size_t>(c) * rows]) * V[c + static_cast<std::size_t>(c2) * C];
+    W[idx] = s;
+}
+
+template <typename T>
+void matmul_yv(Ctx* ctx, const T* Y, int rows, int C, const double* V, int kc, double* W) {
+    const long long n = static_cast<long long>(rows) * kc;
+    if (n == 0) return;
+    MB_LAUNCH(ctx, matmul_yv_kernel<T>, ceil_div(n, 256), 256, 0, Y, rows, C, V, kc, W);
+}
+template void matmul_yv<float>(Ctx*, const float*, int, int, const double*, int, double*);
+template void matmul_yv<double>(Ctx*, const double*, int, int, const double*, int, double*);
+
+// ---------------------------------------------------------------------------
+// basis_from_side (linalg.cpp:261-276) on device.  V: n x k eigenvectors
+// (descending), sig: k.  Writes U (n x k), sv (k), st[0]=numerical rank,
+// st[1]=completed.  eig_status[1]==1 marks an exactly zero matricization
+// (linalg.cpp:326-333: identity basis, rank 0, completed).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kB) basis_from_side_kernel(const double* __restrict__ V, const double* __restrict__ sig,
+                                                             int n, int k, const int* __restrict__ eig_status,
+                                                             double* __restrict__ U, double* __restrict__ sv,
+                                                             int* __restrict__ st) {
+    extern __shared__ double sm[];
+    double* v = sm;            // n
+    double* tcoef = v + n;     // k
+    double* red = tcoef + k;   // 32
+    int* redi = reinterpret_cast<int*>(red + 32);
+    for (int idx = threadIdx.x; idx < n * k; idx += kB) U[idx] = V[idx];
+    __syncthreads();
+    if (eig_status[1] == 1) {
+        for (int i = threadIdx.x; i < k; i += kB) sv[i] = 0.0;
+        if (threadIdx.x == 0) { st[0] = 0; st[1] = 1; st[2] = 0; }
+        return;
+    }
+    const double sigma1 = sig[0];
+    int nr = 0;
+    while (nr < k && sig[nr] > sigma1 * kRankFloor) ++nr;
+    for (int i = 0; i < nr; ++i) cta_canonical_sign(U + static_cast<std::size_t>(i) * n, n, red, redi);
+    for (int i = threadIdx.x; i < k; i += kB) sv[i] = (i < nr) ? sig[i] : 0.0;
+    int fail = 0;
+    for (int i = nr; i < k; ++i)
+        if (!cta_completion(U, n, i, v, tcoef, red)) { fail = i + 1; break; }
+    if (threadIdx.x == 0) { st[0] = nr; st[1] = nr < k ? 1 : 0; st[2] = fail; }
+}
+
+// ---------------------------------------------------------------------------
+// basis_from_products (linalg.cpp:283-296) = orthonormal_columns(w, k, sigma1,
+// canonicalize=true) + sv of the backed columns.  W: n x wc.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kB) basis_from_products_kernel(const double* __restrict__ W, int n, int wc, int k,
+                                                                 const double* __restrict__ sig,
+                                                                 const int* __restrict__ eig_status,
+                                                                 double* __restrict__ U, double* __restrict__ sv,
+                                                                 int* __restrict__ st) {
+    extern __shared__ double sm[];
+    double* v = sm;
+    double* tcoef = v + n;
+    double* red = tcoef + k;
+    int* redi = reinterpret_cast<int*>(red + 32);
+    const double sigma1 = sig[0];
+    const double floor = sigma1 * kRankFloor;
+    int nr = 0, completed = 0, fail = 0;
+    for (int i = 0; i < k; ++i) {
+        bool backed = false;
+        if (i < wc) {
+            for (int r = threadIdx.x; r < n; r += kB) v[r] = W[r + static_cast<std::size_t>(i) * n];
+            double s = 0.0;
+            for (int r = threadIdx.x; r < n; r += kB) s += v[r] * v[r];
+            const double nv = sqrt(cta_sum(s, red));
+            if (nv > floor) {
+                if (i > 0) {
+                    cta_project_out(U, n, i, v, tcoef, red);
+                    cta_project_out(U, n, i, v, tcoef, red);
+                }
+                double s2 = 0.0;
+                for (int r = threadIdx.x; r < n; r += kB) s2 += v[r] * v[r];
+                const double res = sqrt(cta_sum(s2, red));
+                if (res > kCollapseFloor * nv) {
+                    for (int r = threadIdx.x; r < n; r += kB) U[r + static_cast<std::size_t>(i) * n] = v[r] / res;
+                    __syncthreads();
+                    backed = true;
+                }
+            }
+        }
+        if (!backed) {
+            if (!cta_completion(U, n, i, v, tcoef, red) && !fail) fail = i + 1;
+            completed = 1;
+        } else {
+            ++nr;
+        }
+        cta_canonical_sign(U + static_cast<std::size_t>(i) * n, n, red, redi);
+        if (threadIdx.x == 0) sv[i] = (backed && i < wc) ? sig[i] : 0.0;
+    }
+    if (threadIdx.x == 0) { st[0] = nr; st[1] = completed; st[2] = fail; }
+    (void)eig_status;
+}
+
+std::size_t basis_smem(int n, int k) { return (static_cast<std::size_t>(n) + k + 32 + 32) * sizeof(double); }
+
+void basis_from_side(Ctx* ctx, const double* V, const double* sig, int n, int k, const int* eig_status, double* U,
+                     double* sv, int* st) {
+    MB_LAUNCH(ctx, basis_from_side_kernel, 1, kB, basis_smem(n, k), V, sig, n, k, eig_status, U, sv, st);
+}
+
+void basis_from_products(Ctx* ctx, const double* W, int n, int wc, int k, const double* sig, const int* eig_status,
+                         double* U, double* sv, int* st) {
+    MB_LAUNCH(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st);
+}
+
+// ---------------------------------------------------------------------------
+// identity basis for an exactly-zero matrix (left_singular_basis, linalg.cpp:326-333)
+// ---------------------------------------------------------------------------
+__global__ void identity_basis_kernel(double* U, int n, int k, double* sv, int* st) {
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < static_cast<long long>(n) * k;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(idx / n), r = static_cast<int>(idx % n);
+        U[idx] = (r == c) ? 1.0 : 0.0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < k) sv[threadIdx.x] = 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { st[0] = 0; st[1] = 1; st[2] = 0; }
+}
+
+// ---------------------------------------------------------------------------
+// core[col + C*alpha] = sum_i U[i, alpha] * Y[i + rows*col]   (U: rows x r)
+// i.e. core = Y_(last) x_last U_last^T refolded (tucker.cpp:71-75 via the last
+// mode's projection, which already carries every other updated factor).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void core_from_last_kernel(const T* __restrict__ Y, int rows, int C, const double* __restrict__ U, int r,
+                                      double* __restrict__ core) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= C * r) return;
+    const int col = warp % C, alpha = warp / C;
+    double s = 0.0;
+    for (int i = lane; i < rows; i += 32)
+        s += U[i + static_cast<std::size_t>(alpha) * rows] * static_cast<double>(Y[i + static_cast<std::size_t>(col) * rows]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) core[col + static_cast<std::size_t>(C) * alpha] = s;
+}
+
+template <typename T>
+void core_from_last(Ctx* ctx, const T* Y, int rows, int C, const double* U, int r, double* core) {
+    const long long warps = static_cast<long long>(C) * r;
+    MB_LAUNCH(ctx, core_from_last_kernel<T>, ceil_div(warps * 32, 256), 256, 0, Y, rows, C, U, r, core);
+}
+template void core_from_last<float>(Ctx*, const float*, int, int, const double*, int, double*);
+template void core_from_last<double>(Ctx*, const double*, int, int, const double*, int, double*);
+
+// ---------------------------------------------------------------------------
+// deterministic sum of squares: fixed grid, per-block partials, one final block
+// ---------------------------------------------------------------------------
+constexpr int kRedBlocks = 1024;
+
+template <typename T>
+__global__ void __launch_bounds__(256) sumsq_partial_kernel(const T* __restrict__ x, long long n, double* __restrict__ part) {
+    __shared__ double red[8];
+    double s = 0.0;
+    for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * kRedBlocks) {
+        const double v = static_cast<double>(x[i]);
+        s += v * v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < 8; ++i) t += red[i];
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) sum_final_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+    __shared__ double red[8];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += 256) s += part[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < 8; ++i) t += red[i];
+        *out = t;
+    }
+}
+
+template <typename T>
+void sumsq(Ctx* ctx, const T* x, long long n, double* scratch /* >= kRedBlocks */, double* out) {
+    MB_LAUNCH(ctx, sumsq_partial_kernel<T>, kRedBlocks, 256, 0, x, n, scratch);
+    MB_LAUNCH(ctx, sum_final_kernel, 1, 256, 0, scratch, kRedBlocks, out);
+}
+template void sumsq<float>(Ctx*, const float*, long long, double*, double*);
+template void sumsq<double>(Ctx*, const double*, long long, double*, double*);
+int sumsq_scratch() { return kRedBlocks; }
+
+// ---------------------------------------------------------------------------
+// factor U (fp64, n x r column-major) -> kernel copy (T, row-major, stride rs,
+// zero padded to rs columns)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void factor_rowmajor_kernel(const double* __restrict__ U, int n, int r, int rs, T* __restrict__ out) {
+    const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (idx >= static_cast<long long>(n) * rs) return;
+    const int i = static_cast<int>(idx / rs), c = static_cast<int>(idx % rs);
+    out[idx] = (c < r) ? static_cast<T>(U[i + static_cast<std::size_t>(c) * n]) : T(0);
+}
+
+template <typename T>
+void factor_rowmajor(Ctx* ctx, const double* U, int n, int r, int rs, T* out) {
+    const long long tot = static_cast<long long>(n) * rs;
+    MB_LAUNCH(ctx, factor_rowmajor_kernel<T>, ceil_div(tot, 256), 256, 0, U, n, r, rs, out);
+}
+template void factor_rowmajor<float>(Ctx*, const double*, int, int, int, float*);
+template void factor_rowmajor<double>(Ctx*, const double*, int, int, int, double*);
+
+void identity_basis(Ctx* ctx, double* U, int n, int k, double* sv, int* st) {
+    MB_LAUNCH(ctx, identity_basis_kernel, ceil_div(static_cast<long long>(n) * k + 1, 256), 256, 0, U, n, k, sv, st);
+}
+
+}  // namespace machb

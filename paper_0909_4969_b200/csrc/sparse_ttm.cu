@@ -1,0 +1,674 @@
+// Sparse route of the Tucker sweep: per-mode sorted layouts (built once per
+// sampled tensor), the fused mode-n TTM chain, and the sparse HOSVD Grams.
+//
+// Reference path replaced (proj/src):
+//   project_except(SparseTensor)   tucker.cpp:120-131  (sparse TTM tensor.cpp:241-259
+//                                                      + dense TTM tensor.cpp:224-239
+//                                                      + matricize tensor.cpp:180-200)
+//   sparse_core                    tucker.cpp:71-75
+//   sparse_row_gram / col_gram     sparse_kernels.cpp:21-67
+//   sparse_matricization_times     sparse_kernels.cpp:69-80
+//
+// Layout for mode n (order d <= 3; a 2-way tensor gets a dummy mode of size 1):
+// every nonzero carries a packed key  row | i_b | i_a  (row = i_n most
+// significant, i_a least), sorted ascending, so one output row of Y_(n) is a
+// contiguous run and, inside it, each mode-a fibre (fixed i_n, i_b) is a
+// contiguous run.  Rows are cut into warp sub-tiles of <= 32*seg nonzeros.
+//
+// Kernel (one warp per sub-tile, no atomics, fixed summation order):
+//   stage 1  each lane streams `seg` consecutive nonzeros from shared memory and
+//            accumulates the fibre sum f = sum v * U_a[i_a, :]   (r_a FMAs/nnz)
+//   stage 2  finished fibres are queued per lane; the warp drains the queue
+//            collectively, accumulating f (x) U_b[i_b, :] into the row block
+//   output   one partial row (C = r_a * r_b values) per sub-tile; a second tiny
+//            kernel sums a row's partials in sub-tile order and writes Y_(n)
+//            (I_n x C, column-major) directly in matricised layout.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <cmath>
+
+#include "common.cuh"
+#include "sparse_ttm.cuh"
+
+namespace machb {
+
+namespace {
+
+constexpr int kTtmWarps = 4;
+constexpr int kFB = 4;  // fibre queue depth per lane
+
+int bits_for(int n) {
+    int b = 0;
+    while ((1ll << b) < n) ++b;
+    return b;
+}
+
+struct KeyFields {
+    int nf = 0;
+    int mode[4];
+    int shift[4];
+};
+
+struct DimArr {
+    int d;
+    int dims[8];
+};
+
+template <typename IdxT, typename K>
+__global__ void build_keys_kernel(const IdxT* __restrict__ idx, long long nnz, DimArr da, KeyFields kf,
+                                  K* __restrict__ out) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= nnz) return;
+    unsigned long long f = static_cast<unsigned long long>(idx[i]);
+    int mi[8];
+    for (int m = 0; m < da.d; ++m) {
+        const unsigned long long q = f / static_cast<unsigned long long>(da.dims[m]);
+        mi[m] = static_cast<int>(f - q * static_cast<unsigned long long>(da.dims[m]));
+        f = q;
+    }
+    unsigned long long key = 0;
+    for (int j = 0; j < kf.nf; ++j) key |= static_cast<unsigned long long>(mi[kf.mode[j]]) << kf.shift[j];
+    out[i] = static_cast<K>(key);
+}
+
+template <typename K>
+__global__ void row_bounds_kernel(const K* __restrict__ keys, long long nnz, int shift, long long* __restrict__ rs,
+                                  long long* __restrict__ re) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= nnz) return;
+    const long long r = static_cast<long long>(static_cast<unsigned long long>(keys[i]) >> shift);
+    if (i == 0 || (static_cast<unsigned long long>(keys[i - 1]) >> shift) != static_cast<unsigned long long>(r)) rs[r] = i;
+    if (i == nnz - 1 || (static_cast<unsigned long long>(keys[i + 1]) >> shift) != static_cast<unsigned long long>(r))
+        re[r] = i + 1;
+}
+
+__global__ void sub_counts_kernel(const long long* __restrict__ rs, const long long* __restrict__ re, int rows, int tile,
+                                  int* __restrict__ cnt) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > rows) return;
+    cnt[r] = (r < rows) ? static_cast<int>((re[r] - rs[r] + tile - 1) / tile) : 0;
+}
+
+__global__ void sub_fill_kernel(const long long* __restrict__ rs, const long long* __restrict__ re, int rows, int tile,
+                                const int* __restrict__ base, SubTile* __restrict__ subs) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const long long len = re[r] - rs[r];
+    const int n = static_cast<int>((len + tile - 1) / tile);
+    for (int s = 0; s < n; ++s) {
+        SubTile st;
+        st.start = rs[r] + static_cast<long long>(s) * tile;
+        st.len = static_cast<int>(min(static_cast<long long>(tile), len - static_cast<long long>(s) * tile));
+        st.row = r;
+        subs[base[r] + s] = st;
+    }
+}
+
+template <typename T, typename K>
+std::size_t warp_smem_bytes(int seg, int ra_bucket) {
+    const int SR = seg | 1;
+    auto al = [](std::size_t x) { return (x + 15) & ~static_cast<std::size_t>(15); };
+    std::size_t b = al(32ull * SR * sizeof(K)) + al(32ull * SR * sizeof(T)) + al(32ull * kFB * ra_bucket * sizeof(T)) +
+                    al(32ull * kFB * sizeof(int)) + al(32ull * kFB * sizeof(short));
+    return b;
+}
+
+// ---------------------------------------------------------------------------
+// the fused mode-n TTM kernel
+// ---------------------------------------------------------------------------
+template <typename T, typename K, int RA>
+__global__ void __launch_bounds__(kTtmWarps * 32) ttm_mode_kernel(TtmArgs<T, K> A) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const long long sub = static_cast<long long>(blockIdx.x) * kTtmWarps + wib;
+    if (sub >= A.n_sub) return;  // warp-uniform
+    const int seg = A.seg, SR = seg | 1;
+    auto al = [](std::size_t x) { return (x + 15) & ~static_cast<std::size_t>(15); };
+    const std::size_t per_warp = A.warp_smem;
+    unsigned char* base = smraw + per_warp * wib;
+    K* sk = reinterpret_cast<K*>(base);
+    base += al(32ull * SR * sizeof(K));
+    T* svl = reinterpret_cast<T*>(base);
+    base += al(32ull * SR * sizeof(T));
+    T* F = reinterpret_cast<T*>(base);
+    base += al(32ull * kFB * RA * sizeof(T));
+    int* EIB = reinterpret_cast<int*>(base);
+    base += al(32ull * kFB * sizeof(int));
+    short* ord = reinterpret_cast<short*>(base);
+
+    const SubTile st = A.subs[sub];
+    // ---- coalesced stage of the sub-tile (keys, values) into padded smem ----
+    const K* gk = A.keys + st.start;
+    const T* gv = A.vals + st.start;
+#pragma unroll 4
+    for (int s = 0; s < 32; ++s) {
+        if (lane < seg) {
+            const int e = s * seg + lane;
+            if (e < st.len) {
+                sk[s * SR + lane] = gk[e];
+                svl[s * SR + lane] = gv[e];
+            }
+        }
+    }
+    __syncwarp();
+
+    const int rb = A.rb;
+    const int G = 32 / rb;
+    const int g = lane / rb, beta = lane - g * rb;
+    const bool gactive = g < G;
+
+    T acc1[RA];
+    T acc2[RA];
+#pragma unroll
+    for (int a = 0; a < RA; ++a) { acc1[a] = T(0); acc2[a] = T(0); }
+    int nb = 0;
+    bool has = false;
+    int cur = 0;
+
+    auto push = [&]() {
+        T* f = F + (lane * kFB + nb) * RA;
+#pragma unroll
+        for (int a = 0; a < RA; ++a) { f[a] = acc1[a]; acc1[a] = T(0); }
+        EIB[lane * kFB + nb] = cur;
+        ++nb;
+    };
+    auto drain = [&]() {
+        int incl = nb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int excl = incl - nb;
+        for (int s = 0; s < nb; ++s) ord[excl + s] = static_cast<short>(lane * kFB + s);
+        __syncwarp();
+        for (int e0 = 0; e0 < total; e0 += G) {
+            const int e = e0 + g;
+            if (gactive && e < total) {
+                const int slot = ord[e];
+                const T u = A.Ub[static_cast<long long>(EIB[slot]) * A.rbs + beta];
+                const T* f = F + slot * RA;
+#pragma unroll
+                for (int a = 0; a < RA; ++a) acc2[a] = fma(f[a], u, acc2[a]);
+            }
+        }
+        __syncwarp();
+        nb = 0;
+    };
+
+    const int my0 = lane * seg;
+    const K maska = A.maska, maskb = A.maskb;
+    for (int j = 0; j < seg; ++j) {
+        const int e = my0 + j;
+        if (e < st.len) {
+            const K key = sk[lane * SR + j];
+            const T v = svl[lane * SR + j];
+            const int ib = static_cast<int>((key >> A.ba) & maskb);
+            if (has && ib != cur) push();
+            cur = ib;
+            has = true;
+            const T* u = A.Ua + static_cast<long long>(key & maska) * RA;
+#pragma unroll
+            for (int a = 0; a < RA; ++a) acc1[a] = fma(v, u[a], acc1[a]);
+        }
+        if (__any_sync(0xffffffffu, nb == kFB)) drain();
+    }
+    if (has) push();
+    drain();
+
+    // ---- reduce lane groups in fixed order, write the sub-tile's partial row ----
+    for (int gg = 1; gg < G; ++gg) {
+#pragma unroll
+        for (int a = 0; a < RA; ++a) {
+            const T o = __shfl_sync(0xffffffffu, acc2[a], (lane + gg * rb) & 31);
+            if (g == 0) acc2[a] += o;
+        }
+    }
+    if (g == 0) {
+        T* out = A.P + sub * A.C;
+#pragma unroll
+        for (int a = 0; a < RA; ++a)
+            if (a < A.ra) out[a * A.sa + beta * A.sb] = acc2[a];
+    }
+}
+
+template <typename T>
+__global__ void reduce_partials_kernel(const T* __restrict__ P, const int* __restrict__ st_base, int rows, int C,
+                                       T* __restrict__ Y) {
+    const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (idx >= static_cast<long long>(rows) * C) return;
+    const int row = static_cast<int>(idx % rows), col = static_cast<int>(idx / rows);
+    T s = T(0);
+    for (int q = st_base[row]; q < st_base[row + 1]; ++q) s += P[static_cast<long long>(q) * C + col];
+    Y[idx] = s;
+}
+
+// ---------------------------------------------------------------------------
+// sparse Grams with deterministic 64-bit fixed-point accumulation
+// ---------------------------------------------------------------------------
+// row Gram: keys sorted with i_n in the low `bn` bits; a fibre is a run of
+// equal key >> bn.  Pair (y <= x) of one fibre adds v_y v_x to G[i_y, i_x].
+template <typename T, typename K>
+__global__ void row_gram_kernel(const K* __restrict__ keys, const T* __restrict__ vals, long long nnz, int bn,
+                                double scale, int n, unsigned long long* __restrict__ G) {
+    const long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (x >= nnz) return;
+    const unsigned long long kx = static_cast<unsigned long long>(keys[x]);
+    const unsigned long long up = kx >> bn;
+    const int ix = static_cast<int>(kx & ((1ull << bn) - 1ull));
+    const double vx = static_cast<double>(vals[x]);
+    for (long long y = x; y >= 0; --y) {
+        const unsigned long long ky = static_cast<unsigned long long>(keys[y]);
+        if ((ky >> bn) != up) break;
+        const int iy = static_cast<int>(ky & ((1ull << bn) - 1ull));
+        const long long q = __double2ll_rn(static_cast<double>(vals[y]) * vx * scale);
+        atomicAdd(&G[iy + static_cast<long long>(ix) * n], static_cast<unsigned long long>(q));
+    }
+}
+
+// column Gram: entries of one row of X_(n) are a run of equal key >> (ba+bb) in
+// the mode-n TTM layout; columns col = ia*ca + ib*cb.
+template <typename T, typename K>
+__global__ void col_gram_kernel(const K* __restrict__ keys, const T* __restrict__ vals, long long nnz, int ba, int bb,
+                                long long ca, long long cb, double scale, long long n,
+                                unsigned long long* __restrict__ G) {
+    const long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (x >= nnz) return;
+    const int sh = ba + bb;
+    const unsigned long long kx = static_cast<unsigned long long>(keys[x]);
+    const unsigned long long row = kx >> sh;
+    const long long cx = static_cast<long long>(kx & ((1ull << ba) - 1ull)) * ca +
+                         static_cast<long long>((kx >> ba) & ((1ull << bb) - 1ull)) * cb;
+    const double vx = static_cast<double>(vals[x]);
+    for (long long y = x; y >= 0; --y) {
+        const unsigned long long ky = static_cast<unsigned long long>(keys[y]);
+        if ((ky >> sh) != row) break;
+        const long long cy = static_cast<long long>(ky & ((1ull << ba) - 1ull)) * ca +
+                             static_cast<long long>((ky >> ba) & ((1ull << bb) - 1ull)) * cb;
+        const long long lo = cx < cy ? cx : cy, hi = cx < cy ? cy : cx;
+        const long long q = __double2ll_rn(static_cast<double>(vals[y]) * vx * scale);
+        atomicAdd(&G[lo + hi * n], static_cast<unsigned long long>(q));
+    }
+}
+
+__global__ void fixed_to_double_kernel(const unsigned long long* __restrict__ Gi, long long n, double inv_scale,
+                                       double* __restrict__ G) {
+    const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (idx >= n * n) return;
+    const long long c = idx / n, r = idx - c * n;
+    const long long lo = r < c ? r : c, hi = r < c ? c : r;
+    G[idx] = static_cast<double>(static_cast<long long>(Gi[lo + hi * n])) * inv_scale;
+}
+
+// W = X_(n) V for the column-side HOSVD basis (sparse_kernels.cpp:69-80):
+// one warp per row of X_(n), fixed-order reduction.
+template <typename T, typename K, int KC>
+__global__ void sparse_times_kernel(const K* __restrict__ keys, const T* __restrict__ vals,
+                                    const long long* __restrict__ rs, const long long* __restrict__ re, int rows, int ba,
+                                    int bb, long long ca, long long cb, const double* __restrict__ V, long long vld,
+                                    int kc, double* __restrict__ W) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= rows) return;
+    double acc[KC];
+#pragma unroll
+    for (int c = 0; c < KC; ++c) acc[c] = 0.0;
+    for (long long e = rs[warp] + lane; e < re[warp]; e += 32) {
+        const unsigned long long k = static_cast<unsigned long long>(keys[e]);
+        const long long col = static_cast<long long>(k & ((1ull << ba) - 1ull)) * ca +
+                              static_cast<long long>((k >> ba) & ((1ull << bb) - 1ull)) * cb;
+        const double v = static_cast<double>(vals[e]);
+#pragma unroll
+        for (int c = 0; c < KC; ++c)
+            if (c < kc) acc[c] += v * V[col + c * vld];
+    }
+#pragma unroll
+    for (int c = 0; c < KC; ++c) {
+        double s = acc[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0 && c < kc) W[warp + static_cast<long long>(c) * rows] = s;
+    }
+}
+
+template <typename K, typename T>
+void sort_pairs(Ctx* ctx, const K* kin, K* kout, const T* vin, T* vout, long long n, int bits) {
+    std::size_t tmp = 0;
+    MB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, n, 0, bits, ctx->stream));
+    DBuf<unsigned char> t(ctx, tmp);
+    MB_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, kin, kout, vin, vout, n, 0, bits, ctx->stream));
+    ctx->launches += 4;
+}
+
+DimArr dimarr(const std::vector<int>& dims) {
+    DimArr da{};
+    da.d = static_cast<int>(dims.size());
+    for (int m = 0; m < da.d; ++m) da.dims[m] = dims[m];
+    return da;
+}
+
+// Build packed keys for `fields` (least significant first) and sort (key, value)
+// pairs.  Returns key width.
+template <typename T>
+void build_sorted(Ctx* ctx, const mach_sparse* X, const KeyFields& kf, int total_bits, bool key64, DBuf<unsigned char>& keys,
+                  DBuf<unsigned char>& vals, bool need_sort) {
+    const long long nnz = X->nnz;
+    const DimArr da = dimarr(X->dims);
+    const int ks = key64 ? 8 : 4;
+    DBuf<unsigned char> kraw(ctx, static_cast<std::size_t>(nnz) * ks);
+    const int blocks = ceil_div(nnz, 256);
+    if (nnz > 0) {
+        if (X->idx64) {
+            if (key64) MB_LAUNCH(ctx, (build_keys_kernel<unsigned long long, unsigned long long>), blocks, 256, 0,
+                                 static_cast<const unsigned long long*>(X->idx), nnz, da, kf,
+                                 reinterpret_cast<unsigned long long*>(kraw.get()));
+            else MB_LAUNCH(ctx, (build_keys_kernel<unsigned long long, unsigned int>), blocks, 256, 0,
+                           static_cast<const unsigned long long*>(X->idx), nnz, da, kf,
+                           reinterpret_cast<unsigned int*>(kraw.get()));
+        } else {
+            if (key64) MB_LAUNCH(ctx, (build_keys_kernel<unsigned int, unsigned long long>), blocks, 256, 0,
+                                 static_cast<const unsigned int*>(X->idx), nnz, da, kf,
+                                 reinterpret_cast<unsigned long long*>(kraw.get()));
+            else MB_LAUNCH(ctx, (build_keys_kernel<unsigned int, unsigned int>), blocks, 256, 0,
+                           static_cast<const unsigned int*>(X->idx), nnz, da, kf,
+                           reinterpret_cast<unsigned int*>(kraw.get()));
+        }
+    }
+    vals.alloc(ctx, static_cast<std::size_t>(nnz) * sizeof(T));
+    if (!need_sort || nnz == 0) {
+        keys = std::move(kraw);
+        if (nnz) MB_CUDA(cudaMemcpyAsync(vals.get(), X->val, nnz * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
+        return;
+    }
+    keys.alloc(ctx, static_cast<std::size_t>(nnz) * ks);
+    const T* vin = static_cast<const T*>(X->val);
+    T* vout = reinterpret_cast<T*>(vals.get());
+    if (key64)
+        sort_pairs(ctx, reinterpret_cast<const unsigned long long*>(kraw.get()), reinterpret_cast<unsigned long long*>(keys.get()),
+                   vin, vout, nnz, total_bits);
+    else
+        sort_pairs(ctx, reinterpret_cast<const unsigned int*>(kraw.get()), reinterpret_cast<unsigned int*>(keys.get()), vin,
+                   vout, nnz, total_bits);
+}
+
+int ra_bucket(int r) {
+    if (r <= 4) return 4;
+    if (r <= 8) return 8;
+    if (r <= 12) return 12;
+    if (r <= 16) return 16;
+    if (r <= 24) return 24;
+    return 32;
+}
+
+}  // namespace
+
+int ttm_ra_bucket(int r) { return ra_bucket(r); }
+
+bool sparse_fast_path_ok(const std::vector<int>& dims, const std::vector<int>& ranks) {
+    const int d = static_cast<int>(dims.size());
+    if (d < 2 || d > 3) return false;
+    int bits = 0;
+    for (int m = 0; m < d; ++m) {
+        if (ranks[m] > 32) return false;
+        bits += bits_for(dims[m]);
+    }
+    return bits <= 64;
+}
+
+// Choose the innermost contracted mode for mode n by a FMA cost model:
+// nnz * RA(r_a) for the fibre sums + expected fibres * r_a * r_b for stage 2.
+static int choose_inner(const mach_sparse* X, int n, const std::vector<int>& ranks) {
+    const int d = static_cast<int>(X->dims.size());
+    if (d == 2) return 1 - n;
+    int best = -1;
+    double best_cost = 0;
+    const double dens = X->numel ? static_cast<double>(X->nnz) / static_cast<double>(X->numel) : 0.0;
+    for (int a = 0; a < d; ++a) {
+        if (a == n) continue;
+        int b = 3 - n - a;
+        const double Ia = X->dims[a];
+        const double fibres = (static_cast<double>(X->numel) / Ia) * (1.0 - std::pow(1.0 - dens, Ia));
+        const double cost = static_cast<double>(X->nnz) * ra_bucket(ranks[a]) + fibres * ranks[a] * ranks[b];
+        if (best < 0 || cost < best_cost - 1e-9) { best = a; best_cost = cost; }
+    }
+    return best;
+}
+
+template <typename T>
+std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>& ranks) {
+    Ctx* ctx = X->ctx;
+    if (X->plans.size() != X->dims.size()) X->plans.assign(X->dims.size(), nullptr);
+    const int d = static_cast<int>(X->dims.size());
+    const int a = choose_inner(X, n, ranks);
+    const int b = (d == 3) ? 3 - n - a : -1;
+    auto& slot = X->plans[static_cast<std::size_t>(n)];
+    if (slot && slot->a == a) return slot;
+    auto P = std::make_shared<ModePlan>();
+    P->mode = n;
+    P->a = a;
+    P->b = b;
+    P->ba = bits_for(X->dims[a]);
+    P->bb = (b >= 0) ? bits_for(X->dims[b]) : 0;
+    const int bn = bits_for(X->dims[n]);
+    const int total = P->ba + P->bb + bn;
+    P->key64 = total > 32;
+    KeyFields kf{};
+    kf.nf = 0;
+    kf.mode[kf.nf] = a; kf.shift[kf.nf++] = 0;
+    if (b >= 0) { kf.mode[kf.nf] = b; kf.shift[kf.nf++] = P->ba; }
+    kf.mode[kf.nf] = n; kf.shift[kf.nf++] = P->ba + P->bb;
+    // the sampler's flat order already is (i_2, i_1, i_0) lexicographic
+    const bool natural = (d == 3 && n == 2 && a == 0) || (d == 2 && n == 1 && a == 0);
+    build_sorted<T>(ctx, X, kf, total, P->key64, P->keys, P->vals, !natural);
+
+    const int rows = X->dims[n];
+    P->rows = rows;
+    P->row_start.alloc(ctx, rows);
+    P->row_end.alloc(ctx, rows);
+    P->row_start.zero(ctx);
+    P->row_end.zero(ctx);
+    const long long nnz = X->nnz;
+    if (nnz > 0) {
+        if (P->key64) MB_LAUNCH(ctx, row_bounds_kernel<unsigned long long>, ceil_div(nnz, 256), 256, 0,
+                                reinterpret_cast<const unsigned long long*>(P->keys.get()), nnz, P->ba + P->bb,
+                                P->row_start.get(), P->row_end.get());
+        else MB_LAUNCH(ctx, row_bounds_kernel<unsigned int>, ceil_div(nnz, 256), 256, 0,
+                       reinterpret_cast<const unsigned int*>(P->keys.get()), nnz, P->ba + P->bb, P->row_start.get(),
+                       P->row_end.get());
+    }
+    const double avg = rows ? static_cast<double>(nnz) / rows : 0.0;
+    int seg = static_cast<int>(std::ceil(avg / 32.0));
+    seg = std::max(2, std::min(32, seg));
+    if (seg & 1) ++seg;
+    if (seg > 32) seg = 32;
+    P->seg = seg;
+    const int tile = 32 * seg;
+    DBuf<int> cnt(ctx, rows + 1);
+    MB_LAUNCH(ctx, sub_counts_kernel, ceil_div(rows + 1, 256), 256, 0, P->row_start.get(), P->row_end.get(), rows, tile,
+              cnt.get());
+    P->st_base.alloc(ctx, rows + 1);
+    {
+        std::size_t tmp = 0;
+        MB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), P->st_base.get(), rows + 1, ctx->stream));
+        DBuf<unsigned char> t(ctx, tmp);
+        MB_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, cnt.get(), P->st_base.get(), rows + 1, ctx->stream));
+        ctx->launches += 1;
+    }
+    int total_sub = 0;
+    to_host(ctx, &total_sub, P->st_base.get() + rows, 1);
+    sync(ctx);
+    P->n_sub = total_sub;
+    P->subs.alloc(ctx, std::max(1, total_sub));
+    MB_LAUNCH(ctx, sub_fill_kernel, ceil_div(rows, 256), 256, 0, P->row_start.get(), P->row_end.get(), rows, tile,
+              P->st_base.get(), P->subs.get());
+    slot = P;
+    return P;
+}
+
+template <typename T, typename K, int RA>
+static void launch_ttm(Ctx* ctx, TtmArgs<T, K> A) {
+    const std::size_t ws = warp_smem_bytes<T, K>(A.seg, RA);
+    A.warp_smem = ws;
+    const std::size_t smem = ws * kTtmWarps;
+    static bool set = false;
+    if (!set) {
+        MB_CUDA(cudaFuncSetAttribute(ttm_mode_kernel<T, K, RA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        set = true;
+    }
+    const long long blocks = (A.n_sub + kTtmWarps - 1) / kTtmWarps;
+    if (blocks > 0) MB_LAUNCH(ctx, (ttm_mode_kernel<T, K, RA>), static_cast<unsigned>(blocks), kTtmWarps * 32, smem, A);
+}
+
+template <typename T, typename K>
+static void dispatch_ttm(Ctx* ctx, const TtmArgs<T, K>& A, int rab) {
+    switch (rab) {
+        case 4: launch_ttm<T, K, 4>(ctx, A); break;
+        case 8: launch_ttm<T, K, 8>(ctx, A); break;
+        case 12: launch_ttm<T, K, 12>(ctx, A); break;
+        case 16: launch_ttm<T, K, 16>(ctx, A); break;
+        case 24: launch_ttm<T, K, 24>(ctx, A); break;
+        default: launch_ttm<T, K, 32>(ctx, A); break;
+    }
+}
+
+// Y_(n) (I_n x C, column-major, T) for the current factors.  Ur[m] are the
+// row-major kernel copies (stride ttm_ra_bucket(r_m)).
+template <typename T>
+void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks,
+                     const std::vector<const T*>& Ur, const T* one, T* Pbuf, T* Y) {
+    const int n = P.mode, a = P.a, b = P.b;
+    const int ra = ranks[a];
+    const int rb = (b >= 0) ? ranks[b] : 1;
+    const int C = ra * rb;
+    int sa, sb;
+    if (b < 0) { sa = 1; sb = 0; }
+    else if (a < b) { sa = 1; sb = ra; }
+    else { sb = 1; sa = rb; }
+    const int rab = ra_bucket(ra);
+    if (P.key64) {
+        TtmArgs<T, unsigned long long> A{};
+        A.keys = reinterpret_cast<const unsigned long long*>(P.keys.get());
+        A.vals = reinterpret_cast<const T*>(P.vals.get());
+        A.subs = P.subs.get(); A.n_sub = P.n_sub; A.seg = P.seg;
+        A.ba = P.ba; A.maska = (1ull << P.ba) - 1ull; A.maskb = (1ull << P.bb) - 1ull;
+        A.Ua = Ur[a]; A.ra = ra;
+        A.Ub = (b >= 0) ? Ur[b] : one; A.rb = rb; A.rbs = (b >= 0) ? ra_bucket(rb) : 1;
+        A.sa = sa; A.sb = sb; A.C = C; A.P = Pbuf;
+        dispatch_ttm(ctx, A, rab);
+    } else {
+        TtmArgs<T, unsigned int> A{};
+        A.keys = reinterpret_cast<const unsigned int*>(P.keys.get());
+        A.vals = reinterpret_cast<const T*>(P.vals.get());
+        A.subs = P.subs.get(); A.n_sub = P.n_sub; A.seg = P.seg;
+        A.ba = P.ba; A.maska = static_cast<unsigned>((1ull << P.ba) - 1ull); A.maskb = static_cast<unsigned>((1ull << P.bb) - 1ull);
+        A.Ua = Ur[a]; A.ra = ra;
+        A.Ub = (b >= 0) ? Ur[b] : one; A.rb = rb; A.rbs = (b >= 0) ? ra_bucket(rb) : 1;
+        A.sa = sa; A.sb = sb; A.C = C; A.P = Pbuf;
+        dispatch_ttm(ctx, A, rab);
+    }
+    const long long tot = static_cast<long long>(dims[n]) * C;
+    MB_LAUNCH(ctx, reduce_partials_kernel<T>, ceil_div(tot, 256), 256, 0, Pbuf, P.st_base.get(), dims[n], C, Y);
+}
+
+// ---- sparse HOSVD Grams ----------------------------------------------------
+template <typename T>
+void sparse_row_gram(Ctx* ctx, const mach_sparse* X, int n, double normX2, double* G) {
+    const int d = static_cast<int>(X->dims.size());
+    KeyFields kf{};
+    const int bn = bits_for(X->dims[n]);
+    kf.mode[kf.nf] = n; kf.shift[kf.nf++] = 0;
+    int sh = bn;
+    for (int m = 0; m < d; ++m) {
+        if (m == n) continue;
+        kf.mode[kf.nf] = m; kf.shift[kf.nf++] = sh;
+        sh += bits_for(X->dims[m]);
+    }
+    const bool key64 = sh > 32;
+    DBuf<unsigned char> keys, vals;
+    build_sorted<T>(ctx, X, kf, sh, key64, keys, vals, !(n == 0));
+    const int I = X->dims[n];
+    DBuf<unsigned long long> Gi(ctx, static_cast<std::size_t>(I) * I);
+    Gi.zero(ctx);
+    const double scale = (normX2 > 0) ? std::ldexp(1.0, static_cast<int>(std::floor(61.0 - std::log2(normX2)))) : 1.0;
+    const long long nnz = X->nnz;
+    if (nnz > 0) {
+        if (key64) MB_LAUNCH(ctx, (row_gram_kernel<T, unsigned long long>), ceil_div(nnz, 256), 256, 0,
+                             reinterpret_cast<const unsigned long long*>(keys.get()), reinterpret_cast<const T*>(vals.get()),
+                             nnz, bn, scale, I, Gi.get());
+        else MB_LAUNCH(ctx, (row_gram_kernel<T, unsigned int>), ceil_div(nnz, 256), 256, 0,
+                       reinterpret_cast<const unsigned int*>(keys.get()), reinterpret_cast<const T*>(vals.get()), nnz, bn,
+                       scale, I, Gi.get());
+    }
+    MB_LAUNCH(ctx, fixed_to_double_kernel, ceil_div(static_cast<long long>(I) * I, 256), 256, 0, Gi.get(),
+              static_cast<long long>(I), 1.0 / scale, G);
+}
+
+// column strides of X_(n): remaining modes in original order, earliest fastest
+static void xn_col_strides(const std::vector<int>& dims, int n, int a, int b, long long& ca, long long& cb) {
+    const int d = static_cast<int>(dims.size());
+    long long s = 1;
+    ca = cb = 0;
+    for (int m = 0; m < d; ++m) {
+        if (m == n) continue;
+        if (m == a) ca = s;
+        if (m == b) cb = s;
+        s *= dims[m];
+    }
+}
+
+template <typename T>
+void sparse_col_gram(Ctx* ctx, const mach_sparse* X, const ModePlan& P, long long cols, double normX2, double* G) {
+    long long ca, cb;
+    xn_col_strides(X->dims, P.mode, P.a, P.b, ca, cb);
+    DBuf<unsigned long long> Gi(ctx, static_cast<std::size_t>(cols * cols));
+    Gi.zero(ctx);
+    const double scale = (normX2 > 0) ? std::ldexp(1.0, static_cast<int>(std::floor(61.0 - std::log2(normX2)))) : 1.0;
+    const long long nnz = X->nnz;
+    if (nnz > 0) {
+        if (P.key64) MB_LAUNCH(ctx, (col_gram_kernel<T, unsigned long long>), ceil_div(nnz, 256), 256, 0,
+                               reinterpret_cast<const unsigned long long*>(P.keys.get()), reinterpret_cast<const T*>(P.vals.get()),
+                               nnz, P.ba, P.bb, ca, cb, scale, cols, Gi.get());
+        else MB_LAUNCH(ctx, (col_gram_kernel<T, unsigned int>), ceil_div(nnz, 256), 256, 0,
+                       reinterpret_cast<const unsigned int*>(P.keys.get()), reinterpret_cast<const T*>(P.vals.get()), nnz,
+                       P.ba, P.bb, ca, cb, scale, cols, Gi.get());
+    }
+    MB_LAUNCH(ctx, fixed_to_double_kernel, ceil_div(cols * cols, 256), 256, 0, Gi.get(), cols, 1.0 / scale, G);
+}
+
+template <typename T>
+void sparse_times(Ctx* ctx, const mach_sparse* X, const ModePlan& P, const double* V, long long vld, int kc, double* W) {
+    long long ca, cb;
+    xn_col_strides(X->dims, P.mode, P.a, P.b, ca, cb);
+    const int rows = P.rows;
+#define MB_ST(KT)                                                                                                  \
+    MB_LAUNCH(ctx, (sparse_times_kernel<T, KT, 32>), ceil_div(static_cast<long long>(rows) * 32, 256), 256, 0,       \
+              reinterpret_cast<const KT*>(P.keys.get()), reinterpret_cast<const T*>(P.vals.get()), P.row_start.get(), \
+              P.row_end.get(), rows, P.ba, P.bb, ca, cb, V, vld, kc, W)
+    if (P.key64) MB_ST(unsigned long long);
+    else MB_ST(unsigned int);
+#undef MB_ST
+}
+
+template std::shared_ptr<ModePlan> get_plan<float>(mach_sparse*, int, const std::vector<int>&);
+template std::shared_ptr<ModePlan> get_plan<double>(mach_sparse*, int, const std::vector<int>&);
+template void sparse_mode_ttm<float>(Ctx*, const ModePlan&, const std::vector<int>&, const std::vector<int>&,
+                                     const std::vector<const float*>&, const float*, float*, float*);
+template void sparse_mode_ttm<double>(Ctx*, const ModePlan&, const std::vector<int>&, const std::vector<int>&,
+                                      const std::vector<const double*>&, const double*, double*, double*);
+template void sparse_row_gram<float>(Ctx*, const mach_sparse*, int, double, double*);
+template void sparse_row_gram<double>(Ctx*, const mach_sparse*, int, double, double*);
+template void sparse_col_gram<float>(Ctx*, const mach_sparse*, const ModePlan&, long long, double, double*);
+template void sparse_col_gram<double>(Ctx*, const mach_sparse*, const ModePlan&, long long, double, double*);
+template void sparse_times<float>(Ctx*, const mach_sparse*, const ModePlan&, const double*, long long, int, double*);
+template void sparse_times<double>(Ctx*, const mach_sparse*, const ModePlan&, const double*, long long, int, double*);
+
+}  // namespace machb
+
+mach_sparse::~mach_sparse() {
+    plans.clear();
+    if (ctx) {
+        if (idx) cudaFreeAsync(idx, ctx->stream);
+        if (val) cudaFreeAsync(val, ctx->stream);
+    }
+}

@@ -1,0 +1,99 @@
+// Shared declarations of the sparse route (sparse_ttm.cu) and the device
+// linear-algebra helpers (linalg.cu, eig.cu, dense.cu) used by the drivers.
+#pragma once
+
+#include "common.cuh"
+
+namespace machb {
+
+struct SubTile {
+    long long start;
+    int len;
+    int row;
+};
+
+template <typename T, typename K>
+struct TtmArgs {
+    const K* keys;
+    const T* vals;
+    const SubTile* subs;
+    long long n_sub;
+    int seg;
+    int ba;
+    K maska, maskb;
+    const T* Ua;
+    int ra;
+    const T* Ub;
+    int rb, rbs;
+    int sa, sb, C;
+    T* P;
+    std::size_t warp_smem;
+};
+
+// Per-mode sorted layout of a sampled tensor (built once, reused by HOSVD and
+// every sweep).
+struct ModePlan {
+    int mode = 0, a = 0, b = -1;
+    int ba = 0, bb = 0;
+    bool key64 = false;
+    int rows = 0;
+    int seg = 32;
+    long long n_sub = 0;
+    DBuf<unsigned char> keys, vals;
+    DBuf<long long> row_start, row_end;
+    DBuf<int> st_base;
+    DBuf<SubTile> subs;
+};
+
+// ---- sparse route ----
+bool sparse_fast_path_ok(const std::vector<int>& dims, const std::vector<int>& ranks);
+int ttm_ra_bucket(int r);
+template <typename T>
+std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>& ranks);
+template <typename T>
+void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks,
+                     const std::vector<const T*>& Ur, const T* one, T* Pbuf, T* Y);
+template <typename T>
+void sparse_row_gram(Ctx* ctx, const mach_sparse* X, int n, double normX2, double* G);
+template <typename T>
+void sparse_col_gram(Ctx* ctx, const mach_sparse* X, const ModePlan& P, long long cols, double normX2, double* G);
+template <typename T>
+void sparse_times(Ctx* ctx, const mach_sparse* X, const ModePlan& P, const double* V, long long vld, int kc, double* W);
+
+// ---- eigen step (eig.cu, linalg.cu) ----
+void eig_topk(Ctx* ctx, const double* G, int n, int k, double* work, double* V, double* sig, int* status);
+std::size_t eig_work_doubles(int n, int k);
+template <typename T>
+void gram(Ctx* ctx, const T* a, long long sk, long long sn, int K, int N, double* G);
+template <typename T>
+void matmul_yv(Ctx* ctx, const T* Y, int rows, int C, const double* V, int kc, double* W);
+void basis_from_side(Ctx* ctx, const double* V, const double* sig, int n, int k, const int* eig_status, double* U,
+                     double* sv, int* st);
+void basis_from_products(Ctx* ctx, const double* W, int n, int wc, int k, const double* sig, const int* eig_status,
+                         double* U, double* sv, int* st);
+void identity_basis(Ctx* ctx, double* U, int n, int k, double* sv, int* st);
+template <typename T>
+void core_from_last(Ctx* ctx, const T* Y, int rows, int C, const double* U, int r, double* core);
+template <typename T>
+void sumsq(Ctx* ctx, const T* x, long long n, double* scratch, double* out);
+int sumsq_scratch();
+template <typename T>
+void factor_rowmajor(Ctx* ctx, const double* U, int n, int r, int rs, T* out);
+
+// ---- dense route (dense.cu) ----
+// out[a + inner*(q + J*c)] = sum_r in[a + inner*(r + len*c)] * M(q, r) where
+// M(q, r) = U[r + len*q] when transpose (U is len x J: projection by U^T) or
+// U[q + J*r] otherwise (U is J x len: expansion by U).
+template <typename Tin>
+void dense_mode_product(Ctx* ctx, const Tin* in, const std::vector<int>& dims, int mode, const double* U, int J,
+                        bool transpose, double* out);
+template <typename Tin, typename Tout>
+void dense_matricize(Ctx* ctx, const Tin* in, const std::vector<int>& dims, int mode, Tout* out);
+template <typename T>
+void densify(Ctx* ctx, const mach_sparse* X, T* out);
+template <typename T>
+void sumsq_diff(Ctx* ctx, const T* x, const double* y, long long n, double* scratch, double* out);
+template <typename T>
+void scatter_sub(Ctx* ctx, const mach_sparse* X, double* dense);
+
+}  // namespace machb

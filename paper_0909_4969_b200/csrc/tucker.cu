@@ -1,0 +1,666 @@
+// Host orchestration of the device Tucker pipeline (reference:
+// proj/src/tucker.cpp:18-217 and sampling.cpp:33-47).  All tensors, factors,
+// Grams and projections live in HBM; the host only decides dispatch (the
+// reference's branch structure) and reads back, once per sweep, the fit and
+// the per-mode basis status needed for the stop rule (tucker.cpp:102) and the
+// completion warnings (tucker.cpp:34-38).
+#include <cmath>
+#include <type_traits>
+
+#include "sparse_ttm.cuh"
+
+namespace machb {
+
+mach_sparse* sample_dense(const mach_dense* x, double p, std::uint64_t seed);
+
+std::int64_t checked_size(const std::vector<int>& dims) {
+    if (dims.empty()) throw_arg("tensor must have at least one mode");
+    std::int64_t n = 1;
+    for (int d : dims) {
+        if (d < 1) throw_arg("every dimension must be >= 1");
+        if (n > INT64_MAX / d) throw_arg("shape product overflows");
+        n *= d;
+    }
+    return n;
+}
+
+Split split_at(const std::vector<int>& dims, int mode) {
+    if (mode < 0 || mode >= static_cast<int>(dims.size())) throw_arg("mode out of range");
+    Split s;
+    for (int m = 0; m < mode; ++m) s.inner *= dims[static_cast<std::size_t>(m)];
+    for (int m = mode + 1; m < static_cast<int>(dims.size()); ++m) s.outer *= dims[static_cast<std::size_t>(m)];
+    s.len = dims[static_cast<std::size_t>(mode)];
+    return s;
+}
+
+namespace {
+
+constexpr double kDensifyThreshold = 0.25;  // tucker.cpp:69
+
+void check_ranks(const std::vector<int>& dims, const std::vector<int>& ranks) {  // tucker.cpp:20-27
+    if (ranks.size() != dims.size()) throw_arg("ranks must name one rank per mode");
+    for (std::size_t m = 0; m < dims.size(); ++m)
+        if (ranks[m] < 1 || ranks[m] > dims[m])
+            throw_arg("rank for mode " + std::to_string(m + 1) + " must be in [1, " + std::to_string(dims[m]) + "]");
+}
+
+void check_hooi_config(int max_it, double tol) {  // tucker.cpp:29-32
+    if (max_it < 1) throw_arg("max_iterations must be >= 1");
+    if (!(tol >= 0.0)) throw_arg("fit_tolerance must be >= 0");
+}
+
+std::string completion_warning(int mode, int nr, int requested) {  // tucker.cpp:34-38
+    return "mode " + std::to_string(mode + 1) + " matricization has numerical rank " + std::to_string(nr) +
+           " below requested rank " + std::to_string(requested) + "; remaining directions were basis-completed";
+}
+
+struct Timer {
+    Ctx* ctx;
+    cudaEvent_t a, b;
+    explicit Timer(Ctx* c) : ctx(c) {
+        MB_CUDA(cudaEventCreate(&a));
+        MB_CUDA(cudaEventCreate(&b));
+    }
+    ~Timer() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+    void start() { MB_CUDA(cudaEventRecord(a, ctx->stream)); }
+    float stop_ms() {
+        MB_CUDA(cudaEventRecord(b, ctx->stream));
+        MB_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        MB_CUDA(cudaEventElapsedTime(&ms, a, b));
+        return ms;
+    }
+};
+
+// Device state shared by both routes: fp64 factors, basis status per mode,
+// scalar slots.
+struct FactorSet {
+    std::vector<DBuf<double>> U;
+    DBuf<double> sv;         // sum of ranks
+    DBuf<int> st;            // 3 ints per mode: numerical rank, completed, completion failure
+    DBuf<double> scal;       // [0] |X|^2, [1] |G|^2, [2] residual^2
+    DBuf<double> red;        // reduction scratch
+    void init(Ctx* ctx, const std::vector<int>& dims, const std::vector<int>& ranks) {
+        const int d = static_cast<int>(dims.size());
+        U.resize(static_cast<std::size_t>(d));
+        int rs = 0;
+        for (int m = 0; m < d; ++m) {
+            U[static_cast<std::size_t>(m)].alloc(ctx, static_cast<std::size_t>(dims[m]) * ranks[m]);
+            rs += ranks[m];
+        }
+        sv.alloc(ctx, rs);
+        st.alloc(ctx, 3 * d);
+        st.zero(ctx);
+        scal.alloc(ctx, 4);
+        scal.zero(ctx);
+        red.alloc(ctx, sumsq_scratch());
+    }
+};
+
+// left_singular_basis (linalg.cpp:319-353) of Y (rows x cols, column-major,
+// device) into U (rows x k).  Dispatch follows the reference: rows side when
+// rows <= cols and k <= cols, otherwise the columns side plus products.  The
+// reference switches to subspace iteration above 512; the device Gram +
+// selected-eigenpair solver returns the same subspace, so one path serves.
+template <typename T>
+void lsb_device(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U, double* sv, int* st) {
+    if (rows < 1 || cols < 1) throw_arg("matrix must be nonempty");
+    if (k < 1 || k > rows) throw_arg("k must satisfy 1 <= k <= rows");
+    const bool row_side = rows <= cols && k <= cols;
+    const int side = row_side ? rows : static_cast<int>(std::min<long long>(cols, 1 << 30));
+    if (!row_side && cols > 4096)
+        throw Error(MACH_ERR_INTERNAL, "column-side eigen step wider than 4096 is not supported on device yet");
+    const int kk = row_side ? k : static_cast<int>(std::min<long long>(k, cols));
+    DBuf<double> G(ctx, static_cast<std::size_t>(side) * side);
+    DBuf<double> work(ctx, eig_work_doubles(side, kk));
+    DBuf<double> V(ctx, static_cast<std::size_t>(side) * kk);
+    DBuf<double> sig(ctx, kk);
+    DBuf<int> est(ctx, 2);
+    if (row_side)
+        gram<T>(ctx, Y, rows, 1, static_cast<int>(cols), rows, G.get());
+    else
+        gram<T>(ctx, Y, 1, rows, rows, side, G.get());
+    eig_topk(ctx, G.get(), side, kk, work.get(), V.get(), sig.get(), est.get());
+    if (row_side) {
+        basis_from_side(ctx, V.get(), sig.get(), rows, k, est.get(), U, sv, st);
+    } else {
+        DBuf<double> W(ctx, static_cast<std::size_t>(rows) * kk);
+        matmul_yv<T>(ctx, Y, rows, side, V.get(), kk, W.get());
+        basis_from_products(ctx, W.get(), rows, kk, k, sig.get(), est.get(), U, sv, st);
+    }
+}
+
+// core x_1 U_1 ... x_d U_d into a fresh fp64 dense buffer (tucker.cpp:204-209)
+DBuf<double> reconstruct_dev(Ctx* ctx, const double* core, const std::vector<int>& ranks, const std::vector<int>& dims,
+                             const std::vector<DBuf<double>>& U) {
+    const int d = static_cast<int>(dims.size());
+    std::vector<int> cur = ranks;
+    DBuf<double> y(ctx, static_cast<std::size_t>(checked_size(ranks)));
+    MB_CUDA(cudaMemcpyAsync(y.get(), core, y.n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    for (int m = 0; m < d; ++m) {
+        std::vector<int> nd = cur;
+        nd[static_cast<std::size_t>(m)] = dims[static_cast<std::size_t>(m)];
+        DBuf<double> z(ctx, static_cast<std::size_t>(checked_size(nd)));
+        dense_mode_product<double>(ctx, y.get(), cur, m, U[static_cast<std::size_t>(m)].get(), dims[static_cast<std::size_t>(m)],
+                                   false, z.get());
+        y = std::move(z);
+        cur = nd;
+    }
+    return y;
+}
+
+// t x_1 U_1^T ... (skipping `skip`) for a dense device tensor (tucker.cpp:109-118,
+// :195-202).  Returns fp64 buffer and its dims.
+template <typename T>
+DBuf<double> project_dense(Ctx* ctx, const T* x, const std::vector<int>& dims, const std::vector<int>& ranks,
+                           const std::vector<DBuf<double>>& U, int skip, std::vector<int>& out_dims) {
+    const int d = static_cast<int>(dims.size());
+    std::vector<int> cur = dims;
+    DBuf<double> y;
+    bool first = true;
+    for (int m = 0; m < d; ++m) {
+        if (m == skip) continue;
+        std::vector<int> nd = cur;
+        nd[static_cast<std::size_t>(m)] = ranks[static_cast<std::size_t>(m)];
+        DBuf<double> z(ctx, static_cast<std::size_t>(checked_size(nd)));
+        if (first)
+            dense_mode_product<T>(ctx, x, cur, m, U[static_cast<std::size_t>(m)].get(), ranks[static_cast<std::size_t>(m)], true,
+                                  z.get());
+        else
+            dense_mode_product<double>(ctx, y.get(), cur, m, U[static_cast<std::size_t>(m)].get(),
+                                       ranks[static_cast<std::size_t>(m)], true, z.get());
+        y = std::move(z);
+        cur = nd;
+        first = false;
+    }
+    if (first) {  // order-1 tensor: project_except returns t itself
+        y.alloc(ctx, static_cast<std::size_t>(checked_size(dims)));
+        dense_matricize<T, double>(ctx, x, dims, 0, y.get());
+    }
+    out_dims = cur;
+    return y;
+}
+
+std::vector<double> download(Ctx* ctx, const DBuf<double>& b) {
+    std::vector<double> h(b.n);
+    to_host(ctx, h.data(), b.get(), b.n);
+    return h;
+}
+
+// read the per-mode basis status, raise on completion failure, collect warnings
+std::vector<std::string> read_warnings(Ctx* ctx, const DBuf<int>& st, const std::vector<int>& ranks,
+                                       const std::vector<int>& modes) {
+    const int d = static_cast<int>(ranks.size());
+    std::vector<int> h(static_cast<std::size_t>(3 * d));
+    to_host(ctx, h.data(), st.get(), h.size());
+    sync(ctx);
+    std::vector<std::string> w;
+    for (int m : modes) {
+        const int nr = h[3 * m], comp = h[3 * m + 1], fail = h[3 * m + 2];
+        if (fail) throw Error(MACH_ERR_CONVERGENCE, "orthonormal completion found no free direction (singular index " +
+                                                         std::to_string(fail) + ")", fail);
+        if (comp) w.push_back(completion_warning(m, nr, ranks[static_cast<std::size_t>(m)]));
+    }
+    return w;
+}
+
+double fit_from(double normX2, double err2) {
+    if (normX2 == 0.0) return 1.0;
+    return 1.0 - std::sqrt(std::max(0.0, err2)) / std::sqrt(normX2);
+}
+
+// ============================================================================
+// Sessions: begin() = setup + HOSVD (tucker.cpp:135-169), step() = HOOI sweeps
+// with the reference stop rule (hooi_loop, tucker.cpp:80-106), snapshot() =
+// TuckerModel.  One-shot hosvd/hooi are thin loops over a session.
+// ============================================================================
+struct SessionBase {
+    Ctx* ctx = nullptr;
+    std::vector<int> dims, ranks;
+    int d = 0;
+    FactorSet fs;
+    std::vector<int> all;
+    int iterations = 0;
+    double fit = 0.0, prev_fit = 0.0;
+    bool stopped = false;
+    std::vector<double> sweep_fits, sweep_ms;
+    std::vector<std::string> warnings;
+    double setup_ms = 0, hosvd_ms = 0, sample_ms = 0;
+    virtual ~SessionBase() = default;
+    virtual void sweep() = 0;                       // one sweep: all modes, core, fit
+    virtual const double* core_dev() const = 0;
+    double* sv_at(int m) {
+        int o = 0;
+        for (int q = 0; q < m; ++q) o += ranks[static_cast<std::size_t>(q)];
+        return fs.sv.get() + o;
+    }
+    void init_common(Ctx* c, const std::vector<int>& dm, const std::vector<int>& rk) {
+        ctx = c;
+        dims = dm;
+        ranks = rk;
+        d = static_cast<int>(dims.size());
+        fs.init(ctx, dims, ranks);
+        all.resize(static_cast<std::size_t>(d));
+        for (int m = 0; m < d; ++m) all[static_cast<std::size_t>(m)] = m;
+    }
+    // run up to n sweeps; returns the number run (stops on the tolerance rule)
+    int step(int n, double tol) {
+        if (!(tol >= 0.0)) throw_arg("fit_tolerance must be >= 0");
+        Timer tm(ctx);
+        int done = 0;
+        for (int s = 0; s < n && !stopped; ++s) {
+            tm.start();
+            sweep();
+            sweep_ms.push_back(tm.stop_ms());
+            sweep_fits.push_back(fit);
+            ++iterations;
+            ++done;
+            if (fit - prev_fit < tol) stopped = true;
+            prev_fit = fit;
+        }
+        return done;
+    }
+    mach_model* snapshot() const {
+        auto m = std::make_unique<mach_model>();
+        m->order = d;
+        m->dims = dims;
+        m->ranks = ranks;
+        m->core.resize(static_cast<std::size_t>(checked_size(ranks)));
+        to_host(ctx, m->core.data(), core_dev(), m->core.size());
+        for (int q = 0; q < d; ++q) {
+            std::vector<double> f(fs.U[static_cast<std::size_t>(q)].n);
+            to_host(ctx, f.data(), fs.U[static_cast<std::size_t>(q)].get(), f.size());
+            m->factors.push_back(std::move(f));
+        }
+        sync(ctx);
+        m->iterations = iterations;
+        m->fit = fit;
+        m->sweep_fits = sweep_fits;
+        m->warnings = warnings;
+        m->sample_ms = sample_ms;
+        m->setup_ms = setup_ms;
+        m->hosvd_ms = hosvd_ms;
+        m->sweep_ms = sweep_ms;
+        return m.release();
+    }
+};
+
+// ---- dense route: hosvd/hooi(DenseTensor) (tucker.cpp:135-150, :171-180) ----
+template <typename T>
+struct DenseSession : SessionBase {
+    const T* x = nullptr;
+    DBuf<T> owned;  // densified copy when coming from a sparse tensor
+    long long numel = 0;
+    DBuf<double> core;
+
+    double core_and_fit() {
+        std::vector<int> cd;
+        core = project_dense<T>(ctx, x, dims, ranks, fs.U, -1, cd);
+        DBuf<double> rec = reconstruct_dev(ctx, core.get(), ranks, dims, fs.U);
+        sumsq_diff<T>(ctx, x, rec.get(), numel, fs.red.get(), fs.scal.get() + 2);
+        double sc[3];
+        to_host(ctx, sc, fs.scal.get(), 3);
+        sync(ctx);
+        return fit_from(sc[0], sc[2]);
+    }
+    void begin(Ctx* c, const T* data, const std::vector<int>& dm, const std::vector<int>& rk) {
+        init_common(c, dm, rk);
+        x = data;
+        numel = checked_size(dims);
+        Timer tm(ctx);
+        tm.start();
+        sumsq<T>(ctx, x, numel, fs.red.get(), fs.scal.get());
+        for (int m = 0; m < d; ++m) {
+            const int rows = dims[static_cast<std::size_t>(m)];
+            const long long cols = numel / rows;
+            if (m == 0) {
+                lsb_device<T>(ctx, x, rows, cols, ranks[0], fs.U[0].get(), sv_at(0), fs.st.get());
+            } else {
+                DBuf<T> xm(ctx, static_cast<std::size_t>(numel));
+                dense_matricize<T, T>(ctx, x, dims, m, xm.get());
+                lsb_device<T>(ctx, xm.get(), rows, cols, ranks[static_cast<std::size_t>(m)],
+                              fs.U[static_cast<std::size_t>(m)].get(), sv_at(m), fs.st.get() + 3 * m);
+            }
+        }
+        warnings = read_warnings(ctx, fs.st, ranks, all);
+        fit = prev_fit = core_and_fit();
+        hosvd_ms = tm.stop_ms();
+        sweep_fits.assign(1, fit);
+    }
+    void sweep() override {
+        for (int i = 0; i < d; ++i) {
+            std::vector<int> yd;
+            DBuf<double> y = project_dense<T>(ctx, x, dims, ranks, fs.U, i, yd);
+            const int rows = dims[static_cast<std::size_t>(i)];
+            const long long cols = checked_size(yd) / rows;
+            DBuf<double> ym(ctx, y.n);
+            dense_matricize<double, double>(ctx, y.get(), yd, i, ym.get());
+            lsb_device<double>(ctx, ym.get(), rows, cols, ranks[static_cast<std::size_t>(i)],
+                               fs.U[static_cast<std::size_t>(i)].get(), sv_at(i), fs.st.get() + 3 * i);
+        }
+        warnings = read_warnings(ctx, fs.st, ranks, all);
+        fit = core_and_fit();
+    }
+    const double* core_dev() const override { return core.get(); }
+};
+
+// ---- sparse route: hosvd/hooi(SparseTensor) (tucker.cpp:152-169, :182-193) ----
+template <typename T>
+struct SparseSession : SessionBase {
+    mach_sparse* X = nullptr;
+    std::vector<std::shared_ptr<ModePlan>> plans;
+    std::vector<DBuf<T>> Ur;
+    std::vector<const T*> Urp;
+    std::vector<int> C;
+    DBuf<T> one, Pbuf, Y;
+    DBuf<double> core;
+    double normX2 = 0.0;
+
+    void refresh(int m) {
+        factor_rowmajor<T>(ctx, fs.U[static_cast<std::size_t>(m)].get(), dims[static_cast<std::size_t>(m)],
+                           ranks[static_cast<std::size_t>(m)], ttm_ra_bucket(ranks[static_cast<std::size_t>(m)]),
+                           Ur[static_cast<std::size_t>(m)].get());
+    }
+    void mode_y(int m) {
+        sparse_mode_ttm<T>(ctx, *plans[static_cast<std::size_t>(m)], dims, ranks, Urp, one.get(), Pbuf.get(), Y.get());
+    }
+    // core from the last mode's projection (which already carries every other
+    // updated factor), then fit = 1 - sqrt(|X|^2 - |G|^2)/|X| (orthonormal
+    // factors).  Near-exact models take the reference's entrywise residual
+    // (tucker.cpp:47-64) instead of the cancelling identity.
+    double core_and_fit() {
+        const int last = d - 1;
+        core_from_last<T>(ctx, Y.get(), dims[static_cast<std::size_t>(last)], C[static_cast<std::size_t>(last)],
+                          fs.U[static_cast<std::size_t>(last)].get(), ranks[static_cast<std::size_t>(last)], core.get());
+        sumsq<double>(ctx, core.get(), static_cast<long long>(core.n), fs.red.get(), fs.scal.get() + 1);
+        double sc[2];
+        to_host(ctx, sc, fs.scal.get(), 2);
+        sync(ctx);
+        const double e2 = sc[0] - sc[1];
+        const double guard = std::is_same<T, double>::value ? 1e-6 : 1e-3;
+        if (sc[0] > 0.0 && e2 <= guard * sc[0]) {
+            DBuf<double> rec = reconstruct_dev(ctx, core.get(), ranks, dims, fs.U);
+            scatter_sub<T>(ctx, X, rec.get());
+            sumsq<double>(ctx, rec.get(), static_cast<long long>(rec.n), fs.red.get(), fs.scal.get() + 2);
+            double ex = 0.0;
+            to_host(ctx, &ex, fs.scal.get() + 2, 1);
+            sync(ctx);
+            return fit_from(sc[0], ex);
+        }
+        return fit_from(sc[0], e2);
+    }
+    void begin(mach_sparse* sp, const std::vector<int>& rk) {
+        X = sp;
+        init_common(sp->ctx, sp->dims, rk);
+        Timer tm(ctx);
+        // ---- setup: layouts, |X|^2, kernel factor copies, buffers ----
+        tm.start();
+        plans.resize(static_cast<std::size_t>(d));
+        for (int m = 0; m < d; ++m) plans[static_cast<std::size_t>(m)] = get_plan<T>(X, m, ranks);
+        sumsq<T>(ctx, static_cast<const T*>(X->val), X->nnz, fs.red.get(), fs.scal.get());
+        to_host(ctx, &normX2, fs.scal.get(), 1);
+        sync(ctx);
+        X->norm2 = normX2;
+        Ur.resize(static_cast<std::size_t>(d));
+        Urp.resize(static_cast<std::size_t>(d));
+        for (int m = 0; m < d; ++m) {
+            Ur[static_cast<std::size_t>(m)].alloc(ctx, static_cast<std::size_t>(dims[static_cast<std::size_t>(m)]) *
+                                                           ttm_ra_bucket(ranks[static_cast<std::size_t>(m)]));
+            Urp[static_cast<std::size_t>(m)] = Ur[static_cast<std::size_t>(m)].get();
+        }
+        one.alloc(ctx, 1);
+        const T h1 = T(1);
+        to_device(ctx, one.get(), &h1, 1);
+        long long maxP = 1, maxY = 1;
+        C.resize(static_cast<std::size_t>(d));
+        for (int m = 0; m < d; ++m) {
+            const auto& P = *plans[static_cast<std::size_t>(m)];
+            const int c = ranks[static_cast<std::size_t>(P.a)] * (P.b >= 0 ? ranks[static_cast<std::size_t>(P.b)] : 1);
+            C[static_cast<std::size_t>(m)] = c;
+            maxP = std::max(maxP, P.n_sub * c);
+            maxY = std::max(maxY, static_cast<long long>(dims[static_cast<std::size_t>(m)]) * c);
+        }
+        Pbuf.alloc(ctx, maxP);
+        Y.alloc(ctx, maxY);
+        core.alloc(ctx, static_cast<std::size_t>(checked_size(ranks)));
+        setup_ms = tm.stop_ms();
+
+        // ---- HOSVD: sparse_mode_basis per mode (sparse_kernels.cpp:82-90) ----
+        tm.start();
+        const long long numel = X->numel;
+        for (int m = 0; m < d; ++m) {
+            const int rows = dims[static_cast<std::size_t>(m)];
+            const long long cols = numel / rows;
+            const int k = ranks[static_cast<std::size_t>(m)];
+            if (rows <= cols) {
+                DBuf<double> G(ctx, static_cast<std::size_t>(rows) * rows);
+                sparse_row_gram<T>(ctx, X, m, normX2, G.get());
+                DBuf<double> work(ctx, eig_work_doubles(rows, k)), V(ctx, static_cast<std::size_t>(rows) * k), sig(ctx, k);
+                DBuf<int> est(ctx, 2);
+                eig_topk(ctx, G.get(), rows, k, work.get(), V.get(), sig.get(), est.get());
+                basis_from_side(ctx, V.get(), sig.get(), rows, k, est.get(), fs.U[static_cast<std::size_t>(m)].get(),
+                                sv_at(m), fs.st.get() + 3 * m);
+            } else {
+                if (cols > 4096)
+                    throw Error(MACH_ERR_INTERNAL, "column-side sparse HOSVD wider than 4096 is not supported on device yet");
+                const int kc = static_cast<int>(std::min<long long>(k, cols));
+                const int n = static_cast<int>(cols);
+                DBuf<double> G(ctx, static_cast<std::size_t>(n) * n);
+                sparse_col_gram<T>(ctx, X, *plans[static_cast<std::size_t>(m)], cols, normX2, G.get());
+                DBuf<double> work(ctx, eig_work_doubles(n, kc)), V(ctx, static_cast<std::size_t>(n) * kc), sig(ctx, kc);
+                DBuf<int> est(ctx, 2);
+                eig_topk(ctx, G.get(), n, kc, work.get(), V.get(), sig.get(), est.get());
+                DBuf<double> W(ctx, static_cast<std::size_t>(rows) * kc);
+                sparse_times<T>(ctx, X, *plans[static_cast<std::size_t>(m)], V.get(), cols, kc, W.get());
+                basis_from_products(ctx, W.get(), rows, kc, k, sig.get(), est.get(), fs.U[static_cast<std::size_t>(m)].get(),
+                                    sv_at(m), fs.st.get() + 3 * m);
+            }
+            refresh(m);
+        }
+        warnings = read_warnings(ctx, fs.st, ranks, all);
+        mode_y(d - 1);
+        fit = prev_fit = core_and_fit();
+        hosvd_ms = tm.stop_ms();
+        sweep_fits.assign(1, fit);
+    }
+    void sweep() override {
+        for (int i = 0; i < d; ++i) {
+            mode_y(i);
+            lsb_device<T>(ctx, Y.get(), dims[static_cast<std::size_t>(i)], C[static_cast<std::size_t>(i)],
+                          ranks[static_cast<std::size_t>(i)], fs.U[static_cast<std::size_t>(i)].get(), sv_at(i),
+                          fs.st.get() + 3 * i);
+            refresh(i);
+        }
+        fit = core_and_fit();
+        warnings = read_warnings(ctx, fs.st, ranks, all);
+    }
+    const double* core_dev() const override { return core.get(); }
+};
+
+}  // namespace
+
+// ---- session factory + one-shot entry points used by the C ABI ------------
+void* session_sparse(mach_sparse* X, const std::vector<int>& ranks) {
+    check_ranks(X->dims, ranks);
+    Ctx* ctx = X->ctx;
+    const bool dense_enough = static_cast<double>(X->nnz) >= kDensifyThreshold * static_cast<double>(X->numel);
+    if (dense_enough || !sparse_fast_path_ok(X->dims, ranks)) {
+        // tucker.cpp:154-155 / :185-186 densify switch; also the general-shape route
+        if (X->dtype == MACH_F32) {
+            auto s = std::make_unique<DenseSession<float>>();
+            s->owned.alloc(ctx, static_cast<std::size_t>(X->numel));
+            densify<float>(ctx, X, s->owned.get());
+            s->begin(ctx, s->owned.get(), X->dims, ranks);
+            return static_cast<SessionBase*>(s.release());
+        }
+        auto s = std::make_unique<DenseSession<double>>();
+        s->owned.alloc(ctx, static_cast<std::size_t>(X->numel));
+        densify<double>(ctx, X, s->owned.get());
+        s->begin(ctx, s->owned.get(), X->dims, ranks);
+        return static_cast<SessionBase*>(s.release());
+    }
+    if (X->dtype == MACH_F32) {
+        auto s = std::make_unique<SparseSession<float>>();
+        s->begin(X, ranks);
+        return static_cast<SessionBase*>(s.release());
+    }
+    auto s = std::make_unique<SparseSession<double>>();
+    s->begin(X, ranks);
+    return static_cast<SessionBase*>(s.release());
+}
+
+void* session_dense(const mach_dense* X, const std::vector<int>& ranks) {
+    check_ranks(X->dims, ranks);
+    if (X->dtype == MACH_F32) {
+        auto s = std::make_unique<DenseSession<float>>();
+        s->begin(X->ctx, static_cast<const float*>(X->data), X->dims, ranks);
+        return static_cast<SessionBase*>(s.release());
+    }
+    auto s = std::make_unique<DenseSession<double>>();
+    s->begin(X->ctx, static_cast<const double*>(X->data), X->dims, ranks);
+    return static_cast<SessionBase*>(s.release());
+}
+
+static SessionBase* S(void* p) { return static_cast<SessionBase*>(p); }
+int session_step(void* s, int n, double tol) { return S(s)->step(n, tol); }
+mach_model* session_snapshot(void* s) { return S(s)->snapshot(); }
+void session_free(void* s) { delete S(s); }
+void session_set_sample_ms(void* s, double ms) { S(s)->sample_ms = ms; }
+int session_iterations(void* s) { return S(s)->iterations; }
+double session_fit(void* s) { return S(s)->fit; }
+bool session_stopped(void* s) { return S(s)->stopped; }
+
+mach_model* tucker_sparse(mach_sparse* X, const std::vector<int>& ranks, bool do_hooi, int max_it, double tol) {
+    check_ranks(X->dims, ranks);
+    if (do_hooi) check_hooi_config(max_it, tol);
+    std::unique_ptr<SessionBase> s(S(session_sparse(X, ranks)));
+    if (do_hooi) s->step(max_it, tol);
+    return s->snapshot();
+}
+
+mach_model* tucker_dense(const mach_dense* X, const std::vector<int>& ranks, bool do_hooi, int max_it, double tol) {
+    check_ranks(X->dims, ranks);
+    if (do_hooi) check_hooi_config(max_it, tol);
+    std::unique_ptr<SessionBase> s(S(session_dense(X, ranks)));
+    if (do_hooi) s->step(max_it, tol);
+    return s->snapshot();
+}
+
+
+// accuracy (tucker.cpp:211-217) against a device tensor
+double accuracy_dev(const mach_dense* t, const mach_model* m) {
+    Ctx* ctx = t->ctx;
+    const int d = m->order;
+    DBuf<double> red(ctx, sumsq_scratch()), scal(ctx, 2);
+    if (t->dtype == MACH_F32) sumsq<float>(ctx, static_cast<const float*>(t->data), t->numel, red.get(), scal.get());
+    else sumsq<double>(ctx, static_cast<const double*>(t->data), t->numel, red.get(), scal.get());
+    double n2 = 0;
+    to_host(ctx, &n2, scal.get(), 1);
+    sync(ctx);
+    if (n2 == 0.0) throw_arg("accuracy needs a reference tensor with nonzero norm");
+    if (m->dims != t->dims) throw_shape("model reconstructs to a different shape");
+    std::vector<DBuf<double>> U(static_cast<std::size_t>(d));
+    for (int q = 0; q < d; ++q) {
+        U[static_cast<std::size_t>(q)].alloc(ctx, m->factors[static_cast<std::size_t>(q)].size());
+        to_device(ctx, U[static_cast<std::size_t>(q)].get(), m->factors[static_cast<std::size_t>(q)].data(),
+                  m->factors[static_cast<std::size_t>(q)].size());
+    }
+    DBuf<double> core(ctx, m->core.size());
+    to_device(ctx, core.get(), m->core.data(), m->core.size());
+    DBuf<double> rec = reconstruct_dev(ctx, core.get(), m->ranks, m->dims, U);
+    if (t->dtype == MACH_F32) sumsq_diff<float>(ctx, static_cast<const float*>(t->data), rec.get(), t->numel, red.get(), scal.get() + 1);
+    else sumsq_diff<double>(ctx, static_cast<const double*>(t->data), rec.get(), t->numel, red.get(), scal.get() + 1);
+    double e2 = 0;
+    to_host(ctx, &e2, scal.get() + 1, 1);
+    sync(ctx);
+    return 1.0 - std::sqrt(e2) / std::sqrt(n2);
+}
+
+mach_dense* reconstruct_model(Ctx* ctx, const mach_model* m) {
+    const int d = m->order;
+    std::vector<DBuf<double>> U(static_cast<std::size_t>(d));
+    for (int q = 0; q < d; ++q) {
+        U[static_cast<std::size_t>(q)].alloc(ctx, m->factors[static_cast<std::size_t>(q)].size());
+        to_device(ctx, U[static_cast<std::size_t>(q)].get(), m->factors[static_cast<std::size_t>(q)].data(),
+                  m->factors[static_cast<std::size_t>(q)].size());
+    }
+    DBuf<double> core(ctx, m->core.size());
+    to_device(ctx, core.get(), m->core.data(), m->core.size());
+    DBuf<double> rec = reconstruct_dev(ctx, core.get(), m->ranks, m->dims, U);
+    auto out = std::make_unique<mach_dense>();
+    out->ctx = ctx;
+    out->dtype = MACH_F64;
+    out->dims = m->dims;
+    out->numel = checked_size(m->dims);
+    out->data = rec.p;
+    out->owns = true;
+    rec.p = nullptr;
+    rec.n = 0;
+    return out.release();
+}
+
+// left_singular_basis on a host matrix (linalg.cpp:319-353)
+void lsb_host(Ctx* ctx, int rows, int cols, const double* a, int k, double* basis, double* sv, int* nr, int* completed) {
+    if (rows < 1 || cols < 1) throw_arg("matrix must be nonempty");
+    if (k < 1 || k > rows) throw_arg("k must satisfy 1 <= k <= rows");
+    DBuf<double> A(ctx, static_cast<std::size_t>(rows) * cols), U(ctx, static_cast<std::size_t>(rows) * k), s(ctx, k);
+    DBuf<int> st(ctx, 3);
+    st.zero(ctx);
+    to_device(ctx, A.get(), a, A.n);
+    lsb_device<double>(ctx, A.get(), rows, cols, k, U.get(), s.get(), st.get());
+    int h[3];
+    to_host(ctx, basis, U.get(), U.n);
+    to_host(ctx, sv, s.get(), s.n);
+    to_host(ctx, h, st.get(), 3);
+    sync(ctx);
+    if (h[2]) throw Error(MACH_ERR_CONVERGENCE, "orthonormal completion found no free direction (singular index " +
+                                                    std::to_string(h[2]) + ")", h[2]);
+    *nr = h[0];
+    *completed = h[1];
+}
+
+// mode_product (tensor.cpp:224-259) with a host matrix m (rows x cols = J x len)
+mach_dense* mode_product_dev(Ctx* ctx, const mach_dense* t, const mach_sparse* s, int rows, int cols, const double* m,
+                             int mode) {
+    const std::vector<int>& dims = t ? t->dims : s->dims;
+    const Split sp = split_at(dims, mode);
+    if (cols != sp.len) throw_shape("mode_product inner dimensions disagree");
+    std::vector<int> od = dims;
+    od[static_cast<std::size_t>(mode)] = rows;
+    // device M as U (len x J) so that M(q, r) = U[r + len*q] = m(q, r) with transpose=true
+    std::vector<double> ut(static_cast<std::size_t>(rows) * cols);
+    for (int q = 0; q < rows; ++q)
+        for (int r = 0; r < cols; ++r) ut[static_cast<std::size_t>(r) + static_cast<std::size_t>(cols) * q] = m[q + static_cast<std::size_t>(rows) * r];
+    DBuf<double> U(ctx, ut.size());
+    to_device(ctx, U.get(), ut.data(), ut.size());
+    auto out = std::make_unique<mach_dense>();
+    out->ctx = ctx;
+    out->dtype = MACH_F64;
+    out->dims = od;
+    out->numel = checked_size(od);
+    DBuf<double> y(ctx, static_cast<std::size_t>(out->numel));
+    if (t) {
+        if (t->dtype == MACH_F32) dense_mode_product<float>(ctx, static_cast<const float*>(t->data), dims, mode, U.get(), rows, true, y.get());
+        else dense_mode_product<double>(ctx, static_cast<const double*>(t->data), dims, mode, U.get(), rows, true, y.get());
+    } else {
+        DBuf<double> dn(ctx, static_cast<std::size_t>(s->numel));
+        if (s->dtype == MACH_F32) {
+            DBuf<float> df(ctx, static_cast<std::size_t>(s->numel));
+            densify<float>(ctx, s, df.get());
+            dense_mode_product<float>(ctx, df.get(), dims, mode, U.get(), rows, true, y.get());
+        } else {
+            densify<double>(ctx, s, dn.get());
+            dense_mode_product<double>(ctx, dn.get(), dims, mode, U.get(), rows, true, y.get());
+        }
+    }
+    sync(ctx);
+    out->data = y.p;
+    y.p = nullptr;
+    y.n = 0;
+    return out.release();
+}
+
+}  // namespace machb

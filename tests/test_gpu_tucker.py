@@ -1,0 +1,222 @@
+"""HOSVD / HOOI parity on the B200 against the CPU oracle.
+
+North-star bars (BASELINE.json): factors equal up to column sign with the
+largest principal-angle sine <= 1e-9 (fp64) / <= 1e-3 (fp32); core and fit
+within 1e-4 relative (fp32); iterations and sweep_fits compared.  fp64 cases
+are held to fp64-level tolerances (1e-9).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_0909_4969_b200.synth import lowrank_numpy
+from tests.helpers import align_core, canonical_cols, rel, subspace_sin
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mb():
+    import paper_0909_4969_b200 as mb
+    return mb
+
+
+def assert_model_close(dev, ref, sin_tol, rel_tol, fit_tol):
+    assert dev.iterations == ref.iterations
+    assert len(dev.sweep_fits) == len(ref.sweep_fits)
+    assert np.abs(np.array(dev.sweep_fits) - np.array(ref.sweep_fits)).max() <= fit_tol
+    assert abs(dev.fit - ref.fit) <= fit_tol
+    for fd, fr in zip(dev.factors, ref.factors):
+        assert fd.shape == fr.shape
+        assert subspace_sin(fd, fr) <= sin_tol
+        assert np.abs(fd.T @ fd - np.eye(fd.shape[1])).max() < 1e-10
+    core = align_core(dev.core, dev.factors, ref.factors)
+    assert rel(core, ref.core) <= rel_tol
+    assert dev.warnings == ref.warnings
+
+
+# ---------------------------------------------------------------------------
+# sparse route, fp64 (C1-style and small shapes)
+# ---------------------------------------------------------------------------
+SPARSE64 = [
+    ((20, 15, 30), (3, 2, 4), 0.2, 5, 10),
+    ((30, 25, 20), (4, 4, 4), 0.1, 9, 5),
+    ((64, 8, 40), (5, 3, 6), 0.15, 3, 8),
+    ((40, 50), (4, 3), 0.1, 2, 6),       # order 2
+]
+
+
+@pytest.mark.parametrize("dims,ranks,p,seed,sweeps", SPARSE64)
+def test_mach_hooi_fp64_matches_oracle(mb, dims, ranks, p, seed, sweeps):
+    x = lowrank_numpy(dims, ranks, 0.01, seed=seed)
+    res = mb.mach_hooi(x, ranks, mb.SparsifyConfig(p, 7), mb.HooiConfig(sweeps, 0.0))
+    ref_model, ref_sparse = O.mach_hooi(O.Dense(x), ranks, p, 7, sweeps, 0.0)
+    idx, vals = res.sparsified.entries()
+    oi, ov = ref_sparse.entries()
+    assert np.array_equal(idx, oi) and np.array_equal(vals, ov)
+    assert_model_close(res.model, ref_model, 1e-9, 1e-9, 1e-9)
+
+
+def test_c1_config_fp64(mb):
+    """BASELINE configs[0]: 100x12x1024 fp64, ranks (5,5,5), p=0.1, HOSVD + 3 sweeps."""
+    dims, ranks = (100, 12, 1024), (5, 5, 5)
+    x = lowrank_numpy(dims, ranks, 0.01, seed=1)
+    res = mb.mach_hooi(x, ranks, mb.SparsifyConfig(0.1, 7), mb.HooiConfig(3, 0.0))
+    ref_model, _ = O.mach_hooi(O.Dense(x), ranks, 0.1, 7, 3, 0.0)
+    assert_model_close(res.model, ref_model, 1e-9, 1e-8, 1e-9)
+
+
+def test_sparse_hosvd_tall_mode_column_side(mb):
+    # mode 0 taller than the product of the others -> column-side Gram + products
+    rng = np.random.default_rng(77)
+    dims = (30, 4, 5)
+    idx = rng.choice(600, size=60, replace=False)
+    vals = rng.standard_normal(60)
+    st = mb.SparseTensor.from_entries(dims, idx, vals)
+    ref = O.hosvd(O.Sparse.from_entries(dims, idx, vals), [3, 2, 2])
+    dev = mb.hosvd(st, [3, 2, 2])
+    assert_model_close(dev, ref, 1e-9, 1e-9, 1e-12)
+    for fd, fr in zip(dev.factors, ref.factors):
+        assert np.abs(canonical_cols(fd) - canonical_cols(fr)).max() < 1e-9
+
+
+def test_sparse_hooi_random_sparse(mb):
+    rng = np.random.default_rng(123)
+    dims = (8, 9, 10)
+    idx = rng.choice(720, size=70, replace=False)
+    vals = rng.standard_normal(70)
+    dev = mb.hooi(mb.SparseTensor.from_entries(dims, idx, vals), [2, 2, 2])
+    ref = O.hooi(O.Sparse.from_entries(dims, idx, vals), [2, 2, 2])
+    assert_model_close(dev, ref, 1e-9, 1e-9, 1e-12)
+
+
+# ---------------------------------------------------------------------------
+# fp32 sparse route (C2/C3/C5-like shapes at test scale)
+# ---------------------------------------------------------------------------
+SPARSE32 = [
+    ((64, 64, 64), (10, 10, 10), 0.05, 1, 5),
+    ((96, 80, 128), (16, 16, 16), 0.1, 2, 3),
+    ((100, 16, 512), (10, 6, 12), 0.05, 3, 3),
+]
+
+
+@pytest.mark.parametrize("dims,ranks,p,seed,sweeps", SPARSE32)
+def test_mach_hooi_fp32_matches_oracle(mb, dims, ranks, p, seed, sweeps):
+    x = lowrank_numpy(dims, ranks, 0.01, seed=seed, dtype=np.float32)
+    res = mb.mach_hooi(mb.DenseTensor.from_numpy(x), ranks, mb.SparsifyConfig(p, 7), mb.HooiConfig(sweeps, 0.0))
+    ref_model, ref_sparse = O.mach_hooi(O.Dense(x.astype(np.float64)), ranks, p, 7, sweeps, 0.0)
+    assert np.array_equal(res.sparsified.entries()[0], ref_sparse.entries()[0])
+    m = res.model
+    assert m.iterations == ref_model.iterations
+    for fd, fr in zip(m.factors, ref_model.factors):
+        assert subspace_sin(fd, fr) <= 1e-3
+    assert rel(align_core(m.core, m.factors, ref_model.factors), ref_model.core) <= 1e-4
+    assert abs(m.fit - ref_model.fit) <= 1e-4 * abs(ref_model.fit)
+    assert np.allclose(m.sweep_fits, ref_model.sweep_fits, rtol=1e-4, atol=0)
+
+
+# ---------------------------------------------------------------------------
+# dense route (density >= 0.25 switch, dense inputs, general orders)
+# ---------------------------------------------------------------------------
+def test_dense_hooi_matches_oracle(mb):
+    x = O.random_tensor([6, 7, 8], 42)
+    dev = mb.hooi(x, [2, 2, 2], mb.HooiConfig(50, 0.0))
+    ref = O.hooi(O.Dense(x), [2, 2, 2], 50, 0.0)
+    assert_model_close(dev, ref, 1e-9, 1e-8, 1e-12)
+
+
+def test_keep_everything_rides_dense_route(mb):
+    x = O.random_tensor([6, 7, 8], 46)
+    res = mb.mach_hooi(x, [2, 3, 2], mb.SparsifyConfig(1.0, 31))
+    ref = O.hooi(O.Dense(x), [2, 3, 2])
+    assert res.sparsified.nnz == x.size
+    assert_model_close(res.model, ref, 1e-9, 1e-8, 1e-12)
+
+
+def test_four_way_matches_oracle(mb):
+    x = lowrank_numpy((12, 10, 8, 14), (3, 3, 2, 4), 0.02, seed=4)
+    res = mb.mach_hooi(x, (3, 3, 2, 4), mb.SparsifyConfig(0.2, 5), mb.HooiConfig(4, 0.0))
+    ref, _ = O.mach_hooi(O.Dense(x), (3, 3, 2, 4), 0.2, 5, 4, 0.0)
+    assert_model_close(res.model, ref, 1e-9, 1e-8, 1e-9)
+
+
+def test_order_one(mb):
+    x = O.random_tensor([9], 77)
+    assert mb.hosvd(x, [1]).fit >= 1 - 1e-10
+    assert len(mb.hosvd(x, [3]).warnings) == 1
+    h = mb.hooi(x, [2])
+    assert h.iterations == 1 and h.fit >= 1 - 1e-10
+
+
+# ---------------------------------------------------------------------------
+# reference known answers (proj/tests/test_tucker.cpp) on the device path
+# ---------------------------------------------------------------------------
+def test_separable_rank_one(mb):
+    from tests.test_oracle_pins import separable3
+    t = separable3(4, 5, 6, 7.0, 21)
+    m = mb.hosvd(t, [1, 1, 1])
+    assert abs(abs(m.core.reshape(-1)[0]) - 7.0) < 1e-12
+    assert m.fit >= 1 - 1e-10 and m.warnings == []
+    assert mb.accuracy(t, m) >= 1 - 1e-10
+
+
+def test_exact_low_rank_one_sweep(mb):
+    from tests.test_oracle_pins import exact_rank_tensor
+    t = exact_rank_tensor([6, 7, 8], [2, 2, 2], 3)
+    m = mb.hooi(t, [2, 2, 2])
+    assert m.iterations == 1 and abs(m.fit - 1) < 1e-10 and len(m.sweep_fits) == 2
+
+
+def test_completion_warnings(mb):
+    from tests.test_oracle_pins import separable3
+    m = mb.hosvd(separable3(4, 5, 6, 3.0, 9), [2, 2, 2])
+    assert len(m.warnings) == 3 and "mode 1" in m.warnings[0] and "mode 3" in m.warnings[2]
+    assert m.fit >= 1 - 1e-10
+
+
+def test_monotone_and_stop_rule(mb):
+    x = O.random_tensor([6, 7, 8], 42)
+    m = mb.hooi(x, [2, 2, 2], mb.HooiConfig(50, 0.0))
+    assert all(b >= a - 1e-12 for a, b in zip(m.sweep_fits, m.sweep_fits[1:]))
+    assert mb.hooi(x, [2, 2, 2], mb.HooiConfig(50, 0.5)).iterations == 1
+    c = mb.hooi(x, [2, 2, 2], mb.HooiConfig(2, 0.0))
+    assert c.iterations <= 2 and len(c.sweep_fits) == c.iterations + 1
+
+
+def test_validation_errors(mb):
+    x = O.random_tensor([4, 5, 6], 2)
+    for r in ([0, 2, 2], [2, 2, 7], [2, 2]):
+        with pytest.raises(mb.ArgumentError):
+            mb.hosvd(x, r)
+    for cfg in (mb.HooiConfig(0, 1e-4), mb.HooiConfig(10, -1.0), mb.HooiConfig(10, float("nan"))):
+        with pytest.raises(mb.ArgumentError):
+            mb.hooi(x, [2, 2, 2], cfg)
+
+
+def test_bitwise_deterministic(mb):
+    x = lowrank_numpy((40, 30, 50), (4, 3, 5), 0.01, seed=8, dtype=np.float32)
+    a = mb.mach_hooi(mb.DenseTensor.from_numpy(x), (4, 3, 5), mb.SparsifyConfig(0.1, 3), mb.HooiConfig(4, 0.0)).model
+    b = mb.mach_hooi(mb.DenseTensor.from_numpy(x), (4, 3, 5), mb.SparsifyConfig(0.1, 3), mb.HooiConfig(4, 0.0)).model
+    assert np.array_equal(a.core, b.core) and a.sweep_fits == b.sweep_fits
+    for fa, fb in zip(a.factors, b.factors):
+        assert np.array_equal(fa, fb)
+
+
+# ---------------------------------------------------------------------------
+# eigen step in isolation (linalg.cpp:319-353)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("shape,k", [((6, 9), 3), ((40, 12), 5), ((12, 40), 12), ((150, 150), 10),
+                                     ((300, 500), 8), ((7, 3), 5)])
+def test_left_singular_basis_matches_oracle(mb, shape, k):
+    a = O.random_matrix(shape[0], shape[1], 515 + shape[0])
+    dev = mb.left_singular_basis(a, k)
+    b, sv, nr, comp = O.left_singular_basis(a, k)
+    assert dev.numerical_rank == nr and dev.completed == comp
+    assert np.abs(dev.singular_values - sv).max() <= 1e-10 * max(1.0, sv.max())
+    assert np.abs(dev.basis - b).max() < 1e-8  # same canonical signs, same completions
+
+
+def test_left_singular_basis_zero(mb):
+    dev = mb.left_singular_basis(np.zeros((4, 3)), 4)
+    assert dev.numerical_rank == 0 and dev.completed
+    assert np.abs(dev.basis - np.eye(4)).max() == 0
