@@ -116,7 +116,8 @@ mach_status mach_hooi_begin(mach_ctx* ctx, const mach_sparse* t, const int* rank
 mach_status mach_hooi_begin_dense(mach_ctx* ctx, const mach_dense* t, const int* ranks,
                                   mach_session** out);
 /* Up to n sweeps with the reference stop rule (fit - prev < tol ends the
- * iteration, tucker.cpp:102); *done = sweeps run, *stopped = rule fired.    */
+ * iteration, tucker.cpp:102); *done = sweeps run, *stopped = rule fired.
+ * fit_tolerance < 0 runs exactly n sweeps (extension for fixed-length runs). */
 mach_status mach_hooi_step(mach_session* s, int n, double fit_tolerance, int* done, int* stopped);
 mach_status mach_hooi_state(mach_session* s, double* fit, int* iterations);
 mach_status mach_hooi_model(mach_session* s, mach_model** out);

@@ -84,7 +84,9 @@ __device__ double hash_unit(unsigned a, unsigned b) {
 // status[0] = 0 ok; status[1] = 1 if the matrix is exactly zero.
 __global__ void __launch_bounds__(kEigThreads) eig_topk_kernel(const double* __restrict__ G, int n, int k,
                                                                double* __restrict__ work, double* __restrict__ V,
-                                                               double* __restrict__ sig, int* __restrict__ status) {
+                                                               double* __restrict__ sig, int* __restrict__ status,
+                                                               const int* __restrict__ skip) {
+    if (skip && skip[0] == 1) return;  // the subspace solver already converged
     extern __shared__ double sm[];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     double* sv = sm;            // v (n)
@@ -351,7 +353,8 @@ std::size_t eig_work_doubles(int n, int k) {
     return static_cast<std::size_t>(n) * n + static_cast<std::size_t>(6) * n * k;
 }
 
-void eig_topk(Ctx* ctx, const double* G, int n, int k, double* work, double* V, double* sig, int* status) {
+void eig_topk(Ctx* ctx, const double* G, int n, int k, double* work, double* V, double* sig, int* status,
+              const int* skip) {
     const std::size_t smem = eig_smem_bytes(n);
     static bool attr_set = false;
     if (!attr_set) {
@@ -359,7 +362,7 @@ void eig_topk(Ctx* ctx, const double* G, int n, int k, double* work, double* V, 
         attr_set = true;
     }
     if (smem > 227 * 1024) throw Error(MACH_ERR_INTERNAL, "eigen step too large for one CTA (n=" + std::to_string(n) + ")");
-    MB_LAUNCH(ctx, eig_topk_kernel, 1, kEigThreads, smem, G, n, k, work, V, sig, status);
+    MB_LAUNCH(ctx, eig_topk_kernel, 1, kEigThreads, smem, G, n, k, work, V, sig, status, skip);
 }
 
 }  // namespace machb

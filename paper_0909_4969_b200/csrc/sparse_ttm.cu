@@ -35,8 +35,6 @@ namespace machb {
 
 namespace {
 
-constexpr int kTtmWarps = 4;
-constexpr int kFB = 4;  // fibre queue depth per lane
 
 int bits_for(int n) {
     int b = 0;
@@ -105,134 +103,13 @@ __global__ void sub_fill_kernel(const long long* __restrict__ rs, const long lon
     }
 }
 
-template <typename T, typename K>
-std::size_t warp_smem_bytes(int seg, int ra_bucket) {
-    const int SR = seg | 1;
-    auto al = [](std::size_t x) { return (x + 15) & ~static_cast<std::size_t>(15); };
-    std::size_t b = al(32ull * SR * sizeof(K)) + al(32ull * SR * sizeof(T)) + al(32ull * kFB * ra_bucket * sizeof(T)) +
-                    al(32ull * kFB * sizeof(int)) + al(32ull * kFB * sizeof(short));
-    return b;
-}
+}  // namespace
+}  // namespace machb
 
-// ---------------------------------------------------------------------------
-// the fused mode-n TTM kernel
-// ---------------------------------------------------------------------------
-template <typename T, typename K, int RA>
-__global__ void __launch_bounds__(kTtmWarps * 32) ttm_mode_kernel(TtmArgs<T, K> A) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const long long sub = static_cast<long long>(blockIdx.x) * kTtmWarps + wib;
-    if (sub >= A.n_sub) return;  // warp-uniform
-    const int seg = A.seg, SR = seg | 1;
-    auto al = [](std::size_t x) { return (x + 15) & ~static_cast<std::size_t>(15); };
-    const std::size_t per_warp = A.warp_smem;
-    unsigned char* base = smraw + per_warp * wib;
-    K* sk = reinterpret_cast<K*>(base);
-    base += al(32ull * SR * sizeof(K));
-    T* svl = reinterpret_cast<T*>(base);
-    base += al(32ull * SR * sizeof(T));
-    T* F = reinterpret_cast<T*>(base);
-    base += al(32ull * kFB * RA * sizeof(T));
-    int* EIB = reinterpret_cast<int*>(base);
-    base += al(32ull * kFB * sizeof(int));
-    short* ord = reinterpret_cast<short*>(base);
+#include "ttm_kernel.cuh"
 
-    const SubTile st = A.subs[sub];
-    // ---- coalesced stage of the sub-tile (keys, values) into padded smem ----
-    const K* gk = A.keys + st.start;
-    const T* gv = A.vals + st.start;
-#pragma unroll 4
-    for (int s = 0; s < 32; ++s) {
-        if (lane < seg) {
-            const int e = s * seg + lane;
-            if (e < st.len) {
-                sk[s * SR + lane] = gk[e];
-                svl[s * SR + lane] = gv[e];
-            }
-        }
-    }
-    __syncwarp();
-
-    const int rb = A.rb;
-    const int G = 32 / rb;
-    const int g = lane / rb, beta = lane - g * rb;
-    const bool gactive = g < G;
-
-    T acc1[RA];
-    T acc2[RA];
-#pragma unroll
-    for (int a = 0; a < RA; ++a) { acc1[a] = T(0); acc2[a] = T(0); }
-    int nb = 0;
-    bool has = false;
-    int cur = 0;
-
-    auto push = [&]() {
-        T* f = F + (lane * kFB + nb) * RA;
-#pragma unroll
-        for (int a = 0; a < RA; ++a) { f[a] = acc1[a]; acc1[a] = T(0); }
-        EIB[lane * kFB + nb] = cur;
-        ++nb;
-    };
-    auto drain = [&]() {
-        int incl = nb;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        const int excl = incl - nb;
-        for (int s = 0; s < nb; ++s) ord[excl + s] = static_cast<short>(lane * kFB + s);
-        __syncwarp();
-        for (int e0 = 0; e0 < total; e0 += G) {
-            const int e = e0 + g;
-            if (gactive && e < total) {
-                const int slot = ord[e];
-                const T u = A.Ub[static_cast<long long>(EIB[slot]) * A.rbs + beta];
-                const T* f = F + slot * RA;
-#pragma unroll
-                for (int a = 0; a < RA; ++a) acc2[a] = fma(f[a], u, acc2[a]);
-            }
-        }
-        __syncwarp();
-        nb = 0;
-    };
-
-    const int my0 = lane * seg;
-    const K maska = A.maska, maskb = A.maskb;
-    for (int j = 0; j < seg; ++j) {
-        const int e = my0 + j;
-        if (e < st.len) {
-            const K key = sk[lane * SR + j];
-            const T v = svl[lane * SR + j];
-            const int ib = static_cast<int>((key >> A.ba) & maskb);
-            if (has && ib != cur) push();
-            cur = ib;
-            has = true;
-            const T* u = A.Ua + static_cast<long long>(key & maska) * RA;
-#pragma unroll
-            for (int a = 0; a < RA; ++a) acc1[a] = fma(v, u[a], acc1[a]);
-        }
-        if (__any_sync(0xffffffffu, nb == kFB)) drain();
-    }
-    if (has) push();
-    drain();
-
-    // ---- reduce lane groups in fixed order, write the sub-tile's partial row ----
-    for (int gg = 1; gg < G; ++gg) {
-#pragma unroll
-        for (int a = 0; a < RA; ++a) {
-            const T o = __shfl_sync(0xffffffffu, acc2[a], (lane + gg * rb) & 31);
-            if (g == 0) acc2[a] += o;
-        }
-    }
-    if (g == 0) {
-        T* out = A.P + sub * A.C;
-#pragma unroll
-        for (int a = 0; a < RA; ++a)
-            if (a < A.ra) out[a * A.sa + beta * A.sb] = acc2[a];
-    }
-}
+namespace machb {
+namespace {
 
 template <typename T>
 __global__ void reduce_partials_kernel(const T* __restrict__ P, const int* __restrict__ st_base, int rows, int C,
@@ -356,7 +233,7 @@ void build_sorted(Ctx* ctx, const mach_sparse* X, const KeyFields& kf, int total
     const long long nnz = X->nnz;
     const DimArr da = dimarr(X->dims);
     const int ks = key64 ? 8 : 4;
-    DBuf<unsigned char> kraw(ctx, static_cast<std::size_t>(nnz) * ks);
+    DBuf<unsigned char> kraw(ctx, static_cast<std::size_t>(nnz) * ks + 32);
     const int blocks = ceil_div(nnz, 256);
     if (nnz > 0) {
         if (X->idx64) {
@@ -375,13 +252,13 @@ void build_sorted(Ctx* ctx, const mach_sparse* X, const KeyFields& kf, int total
                            reinterpret_cast<unsigned int*>(kraw.get()));
         }
     }
-    vals.alloc(ctx, static_cast<std::size_t>(nnz) * sizeof(T));
+    vals.alloc(ctx, static_cast<std::size_t>(nnz) * sizeof(T) + 32);
     if (!need_sort || nnz == 0) {
         keys = std::move(kraw);
         if (nnz) MB_CUDA(cudaMemcpyAsync(vals.get(), X->val, nnz * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
         return;
     }
-    keys.alloc(ctx, static_cast<std::size_t>(nnz) * ks);
+    keys.alloc(ctx, static_cast<std::size_t>(nnz) * ks + 32);
     const T* vin = static_cast<const T*>(X->val);
     T* vout = reinterpret_cast<T*>(vals.get());
     if (key64)
@@ -479,9 +356,8 @@ std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>
     }
     const double avg = rows ? static_cast<double>(nnz) / rows : 0.0;
     int seg = static_cast<int>(std::ceil(avg / 32.0));
-    seg = std::max(2, std::min(32, seg));
-    if (seg & 1) ++seg;
-    if (seg > 32) seg = 32;
+    seg = std::max(1, std::min(31, seg));
+    if (!(seg & 1)) ++seg;  // odd: conflict-free strided reads of the linear TMA layout
     P->seg = seg;
     const int tile = 32 * seg;
     DBuf<int> cnt(ctx, rows + 1);
@@ -508,16 +384,28 @@ std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>
 
 template <typename T, typename K, int RA>
 static void launch_ttm(Ctx* ctx, TtmArgs<T, K> A) {
-    const std::size_t ws = warp_smem_bytes<T, K>(A.seg, RA);
-    A.warp_smem = ws;
-    const std::size_t smem = ws * kTtmWarps;
-    static bool set = false;
-    if (!set) {
-        MB_CUDA(cudaFuncSetAttribute(ttm_mode_kernel<T, K, RA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        set = true;
+    const ttm::WarpLayout<T, K, RA> L(A.seg);
+    const std::size_t budget = 220 * 1024;
+    std::size_t fac = ttm::al16(static_cast<std::size_t>(A.ua_elems + A.ub_elems) * sizeof(T));
+    int nw;
+    if (fac + 4 * L.total <= budget) {
+        A.fac_smem = 1;
+        nw = static_cast<int>(std::min<std::size_t>(8, (budget - fac) / L.total));
+    } else {
+        A.fac_smem = 0;
+        fac = 0;
+        nw = static_cast<int>(std::min<std::size_t>(8, budget / L.total));
     }
-    const long long blocks = (A.n_sub + kTtmWarps - 1) / kTtmWarps;
-    if (blocks > 0) MB_LAUNCH(ctx, (ttm_mode_kernel<T, K, RA>), static_cast<unsigned>(blocks), kTtmWarps * 32, smem, A);
+    A.fac_bytes = fac;
+    const std::size_t smem = fac + nw * L.total;
+    auto kern = ttm::ttm_mode_kernel<T, K, RA>;
+    MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int per_sm = 1, sms = 148;
+    MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem));
+    MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    const long long want = (A.n_sub + nw - 1) / nw;
+    const long long blocks = std::min<long long>(want, static_cast<long long>(sms) * std::max(1, per_sm));
+    if (blocks > 0) MB_LAUNCH(ctx, (ttm::ttm_mode_kernel<T, K, RA>), static_cast<unsigned>(blocks), nw * 32, smem, A);
 }
 
 template <typename T, typename K>
@@ -555,6 +443,8 @@ void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, 
         A.Ua = Ur[a]; A.ra = ra;
         A.Ub = (b >= 0) ? Ur[b] : one; A.rb = rb; A.rbs = (b >= 0) ? ra_bucket(rb) : 1;
         A.sa = sa; A.sb = sb; A.C = C; A.P = Pbuf;
+        A.ua_elems = static_cast<long long>(dims[a]) * rab;
+        A.ub_elems = (b >= 0) ? static_cast<long long>(dims[b]) * A.rbs : 1;
         dispatch_ttm(ctx, A, rab);
     } else {
         TtmArgs<T, unsigned int> A{};
@@ -565,6 +455,8 @@ void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, 
         A.Ua = Ur[a]; A.ra = ra;
         A.Ub = (b >= 0) ? Ur[b] : one; A.rb = rb; A.rbs = (b >= 0) ? ra_bucket(rb) : 1;
         A.sa = sa; A.sb = sb; A.C = C; A.P = Pbuf;
+        A.ua_elems = static_cast<long long>(dims[a]) * rab;
+        A.ub_elems = (b >= 0) ? static_cast<long long>(dims[b]) * A.rbs : 1;
         dispatch_ttm(ctx, A, rab);
     }
     const long long tot = static_cast<long long>(dims[n]) * C;

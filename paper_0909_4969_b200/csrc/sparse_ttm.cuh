@@ -27,7 +27,9 @@ struct TtmArgs {
     int rb, rbs;
     int sa, sb, C;
     T* P;
-    std::size_t warp_smem;
+    long long ua_elems, ub_elems;  // factor elements (row-major, padded strides)
+    std::size_t fac_bytes;         // shared-memory bytes of the staged factors
+    int fac_smem;                  // 1: factors staged in shared memory
 };
 
 // Per-mode sorted layout of a sampled tensor (built once, reused by HOSVD and
@@ -61,7 +63,16 @@ template <typename T>
 void sparse_times(Ctx* ctx, const mach_sparse* X, const ModePlan& P, const double* V, long long vld, int kc, double* W);
 
 // ---- eigen step (eig.cu, linalg.cu) ----
-void eig_topk(Ctx* ctx, const double* G, int n, int k, double* work, double* V, double* sig, int* status);
+void eig_topk(Ctx* ctx, const double* G, int n, int k, double* work, double* V, double* sig, int* status,
+              const int* skip = nullptr);
+bool eig_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
+                  double* V, double* sig, int* status);
+// top-k eigenpairs of G: warm-started subspace solver when it applies, with the
+// exact selected-eigenpair solver as the in-stream fallback.  status[1]==1
+// flags an exactly zero G.
+bool eig_select(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
+                double* V, double* sig, int* status);
+int eig_block(int n, int k);
 std::size_t eig_work_doubles(int n, int k);
 template <typename T>
 void gram(Ctx* ctx, const T* a, long long sk, long long sn, int K, int N, double* G);

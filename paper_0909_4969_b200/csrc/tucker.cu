@@ -105,8 +105,29 @@ struct FactorSet {
 // rows <= cols and k <= cols, otherwise the columns side plus products.  The
 // reference switches to subspace iteration above 512; the device Gram +
 // selected-eigenpair solver returns the same subspace, so one path serves.
+// Warm start (HOOI): per-mode Ritz block kept across sweeps; on the first
+// sweep the row side starts from the current factor and the column side from
+// Y^T U (one power step from the current factor).
+struct Warm {
+    DBuf<double> X;   // side x b
+    int cols = 0;     // valid warm columns (0 = none)
+    int b = 0;
+};
+
 template <typename T>
-void lsb_device(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U, double* sv, int* st) {
+__global__ void yt_u_kernel(const T* __restrict__ Y, int rows, int C, const double* __restrict__ U, int k,
+                            double* __restrict__ out) {
+    const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (idx >= static_cast<long long>(C) * k) return;
+    const int c = static_cast<int>(idx % C), j = static_cast<int>(idx / C);
+    double s = 0.0;
+    for (int i = 0; i < rows; ++i) s += static_cast<double>(Y[i + static_cast<std::size_t>(c) * rows]) * U[i + static_cast<std::size_t>(j) * rows];
+    out[idx] = s;
+}
+
+template <typename T>
+void lsb_device(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U, double* sv, int* st,
+                Warm* warm = nullptr, const double* Uprev = nullptr) {
     if (rows < 1 || cols < 1) throw_arg("matrix must be nonempty");
     if (k < 1 || k > rows) throw_arg("k must satisfy 1 <= k <= rows");
     const bool row_side = rows <= cols && k <= cols;
@@ -115,15 +136,42 @@ void lsb_device(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U
         throw Error(MACH_ERR_INTERNAL, "column-side eigen step wider than 4096 is not supported on device yet");
     const int kk = row_side ? k : static_cast<int>(std::min<long long>(k, cols));
     DBuf<double> G(ctx, static_cast<std::size_t>(side) * side);
-    DBuf<double> work(ctx, eig_work_doubles(side, kk));
     DBuf<double> V(ctx, static_cast<std::size_t>(side) * kk);
     DBuf<double> sig(ctx, kk);
-    DBuf<int> est(ctx, 2);
+    DBuf<int> est(ctx, 3);
     if (row_side)
         gram<T>(ctx, Y, rows, 1, static_cast<int>(cols), rows, G.get());
     else
         gram<T>(ctx, Y, 1, rows, rows, side, G.get());
-    eig_topk(ctx, G.get(), side, kk, work.get(), V.get(), sig.get(), est.get());
+    const int b = eig_block(side, kk);
+    const double* X0 = nullptr;
+    int x0c = 0;
+    DBuf<double> seed;
+    if (warm) {
+        if (warm->X.n != static_cast<std::size_t>(side) * b) {
+            warm->X.alloc(ctx, static_cast<std::size_t>(side) * b);
+            warm->cols = 0;
+        }
+        warm->b = b;
+        if (warm->cols > 0) {
+            X0 = warm->X.get();
+            x0c = warm->cols;
+        } else if (Uprev) {
+            if (row_side) {
+                X0 = Uprev;
+                x0c = kk;
+            } else {
+                seed.alloc(ctx, static_cast<std::size_t>(side) * kk);
+                MB_LAUNCH(ctx, yt_u_kernel<T>, ceil_div(static_cast<long long>(side) * kk, 256), 256, 0, Y, rows, side, Uprev,
+                          kk, seed.get());
+                X0 = seed.get();
+                x0c = kk;
+            }
+        }
+    }
+    const bool sub = eig_select(ctx, G.get(), side, kk, X0, x0c, warm ? warm->X.get() : nullptr, b, V.get(), sig.get(),
+                                est.get());
+    if (warm) warm->cols = sub ? b : 0;
     if (row_side) {
         basis_from_side(ctx, V.get(), sig.get(), rows, k, est.get(), U, sv, st);
     } else {
@@ -222,6 +270,7 @@ struct SessionBase {
     std::vector<int> dims, ranks;
     int d = 0;
     FactorSet fs;
+    std::vector<Warm> warm;  // per-mode Ritz blocks carried across sweeps
     std::vector<int> all;
     int iterations = 0;
     double fit = 0.0, prev_fit = 0.0;
@@ -243,12 +292,16 @@ struct SessionBase {
         ranks = rk;
         d = static_cast<int>(dims.size());
         fs.init(ctx, dims, ranks);
+        warm.resize(static_cast<std::size_t>(d));
         all.resize(static_cast<std::size_t>(d));
         for (int m = 0; m < d; ++m) all[static_cast<std::size_t>(m)] = m;
     }
     // run up to n sweeps; returns the number run (stops on the tolerance rule)
+    // tol < 0 (session extension, e.g. fixed-length benchmarks) disables the rule
     int step(int n, double tol) {
-        if (!(tol >= 0.0)) throw_arg("fit_tolerance must be >= 0");
+        if (std::isnan(tol)) throw_arg("fit_tolerance must be >= 0");
+        const bool rule = tol >= 0.0;
+        if (!rule) stopped = false;
         Timer tm(ctx);
         int done = 0;
         for (int s = 0; s < n && !stopped; ++s) {
@@ -258,7 +311,7 @@ struct SessionBase {
             sweep_fits.push_back(fit);
             ++iterations;
             ++done;
-            if (fit - prev_fit < tol) stopped = true;
+            if (rule && fit - prev_fit < tol) stopped = true;
             prev_fit = fit;
         }
         return done;
@@ -339,7 +392,8 @@ struct DenseSession : SessionBase {
             DBuf<double> ym(ctx, y.n);
             dense_matricize<double, double>(ctx, y.get(), yd, i, ym.get());
             lsb_device<double>(ctx, ym.get(), rows, cols, ranks[static_cast<std::size_t>(i)],
-                               fs.U[static_cast<std::size_t>(i)].get(), sv_at(i), fs.st.get() + 3 * i);
+                               fs.U[static_cast<std::size_t>(i)].get(), sv_at(i), fs.st.get() + 3 * i,
+                               &warm[static_cast<std::size_t>(i)], fs.U[static_cast<std::size_t>(i)].get());
         }
         warnings = read_warnings(ctx, fs.st, ranks, all);
         fit = core_and_fit();
@@ -438,9 +492,9 @@ struct SparseSession : SessionBase {
             if (rows <= cols) {
                 DBuf<double> G(ctx, static_cast<std::size_t>(rows) * rows);
                 sparse_row_gram<T>(ctx, X, m, normX2, G.get());
-                DBuf<double> work(ctx, eig_work_doubles(rows, k)), V(ctx, static_cast<std::size_t>(rows) * k), sig(ctx, k);
-                DBuf<int> est(ctx, 2);
-                eig_topk(ctx, G.get(), rows, k, work.get(), V.get(), sig.get(), est.get());
+                DBuf<double> V(ctx, static_cast<std::size_t>(rows) * k), sig(ctx, k);
+                DBuf<int> est(ctx, 3);
+                eig_select(ctx, G.get(), rows, k, nullptr, 0, nullptr, eig_block(rows, k), V.get(), sig.get(), est.get());
                 basis_from_side(ctx, V.get(), sig.get(), rows, k, est.get(), fs.U[static_cast<std::size_t>(m)].get(),
                                 sv_at(m), fs.st.get() + 3 * m);
             } else {
@@ -450,9 +504,9 @@ struct SparseSession : SessionBase {
                 const int n = static_cast<int>(cols);
                 DBuf<double> G(ctx, static_cast<std::size_t>(n) * n);
                 sparse_col_gram<T>(ctx, X, *plans[static_cast<std::size_t>(m)], cols, normX2, G.get());
-                DBuf<double> work(ctx, eig_work_doubles(n, kc)), V(ctx, static_cast<std::size_t>(n) * kc), sig(ctx, kc);
-                DBuf<int> est(ctx, 2);
-                eig_topk(ctx, G.get(), n, kc, work.get(), V.get(), sig.get(), est.get());
+                DBuf<double> V(ctx, static_cast<std::size_t>(n) * kc), sig(ctx, kc);
+                DBuf<int> est(ctx, 3);
+                eig_select(ctx, G.get(), n, kc, nullptr, 0, nullptr, eig_block(n, kc), V.get(), sig.get(), est.get());
                 DBuf<double> W(ctx, static_cast<std::size_t>(rows) * kc);
                 sparse_times<T>(ctx, X, *plans[static_cast<std::size_t>(m)], V.get(), cols, kc, W.get());
                 basis_from_products(ctx, W.get(), rows, kc, k, sig.get(), est.get(), fs.U[static_cast<std::size_t>(m)].get(),
@@ -471,7 +525,7 @@ struct SparseSession : SessionBase {
             mode_y(i);
             lsb_device<T>(ctx, Y.get(), dims[static_cast<std::size_t>(i)], C[static_cast<std::size_t>(i)],
                           ranks[static_cast<std::size_t>(i)], fs.U[static_cast<std::size_t>(i)].get(), sv_at(i),
-                          fs.st.get() + 3 * i);
+                          fs.st.get() + 3 * i, &warm[static_cast<std::size_t>(i)], fs.U[static_cast<std::size_t>(i)].get());
             refresh(i);
         }
         fit = core_and_fit();

@@ -21,10 +21,25 @@ def mb():
     return mb
 
 
+def assert_same_iterations(dev, ref, fit_tol):
+    """The stop rule (fit - prev < tol, tucker.cpp:102) is compared, not
+    assumed.  With tol = 0 a converged model stops on a rounding-level fit
+    decrease, which either side may hit first; that is the only accepted
+    difference, and the shared prefix of sweep_fits must agree."""
+    n = min(len(dev.sweep_fits), len(ref.sweep_fits))
+    assert np.abs(np.array(dev.sweep_fits[:n]) - np.array(ref.sweep_fits[:n])).max() <= fit_tol
+    if dev.iterations != ref.iterations:
+        short = dev if dev.iterations < ref.iterations else ref
+        k = short.iterations
+        assert abs(short.sweep_fits[k] - short.sweep_fits[k - 1]) <= 1e-12, (dev.sweep_fits, ref.sweep_fits)
+        return False
+    return True
+
+
 def assert_model_close(dev, ref, sin_tol, rel_tol, fit_tol):
-    assert dev.iterations == ref.iterations
-    assert len(dev.sweep_fits) == len(ref.sweep_fits)
-    assert np.abs(np.array(dev.sweep_fits) - np.array(ref.sweep_fits)).max() <= fit_tol
+    if assert_same_iterations(dev, ref, fit_tol):
+        assert len(dev.sweep_fits) == len(ref.sweep_fits)
+        assert np.abs(np.array(dev.sweep_fits) - np.array(ref.sweep_fits)).max() <= fit_tol
     assert abs(dev.fit - ref.fit) <= fit_tol
     for fd, fr in zip(dev.factors, ref.factors):
         assert fd.shape == fr.shape
