@@ -131,8 +131,10 @@ __device__ void orthonormalize(double* X, int n, int b, double* coef, double* re
 
 // one-warp cyclic Jacobi on H (b x b, ld kMaxB) -> eigenvectors W, values th
 // (descending, W columns permuted alike)
-__device__ void warp_jacobi(double* H, double* W, double* th, int b) {
+__device__ void warp_jacobi(double* H, double* W, double* th, int b, int max_sweeps) {
     const int lane = threadIdx.x & 31;
+    __shared__ int jp[kMaxB / 2], jq[kMaxB / 2];
+    __shared__ double jc[kMaxB / 2], js[kMaxB / 2];
     const int bp = (b + 1) & ~1;  // even player count (a dummy when b is odd)
     for (int e = lane; e < kMaxB * kMaxB; e += 32) W[e] = ((e % kMaxB) == (e / kMaxB)) ? 1.0 : 0.0;
     __syncwarp();
@@ -144,7 +146,7 @@ __device__ void warp_jacobi(double* H, double* W, double* th, int b) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
     const int M = bp - 1;
-    for (int sweep = 0; sweep < 30 && b > 1; ++sweep) {
+    for (int sweep = 0; sweep < max_sweeps && b > 1; ++sweep) {
         double off = 0.0;
         for (int e = lane; e < b * b; e += 32) {
             const int i = e % b, j = e / b;
@@ -153,50 +155,53 @@ __device__ void warp_jacobi(double* H, double* W, double* th, int b) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
         if (off <= 1e-30 * nrm) break;
+        const int np = bp / 2;
         for (int r = 0; r < M; ++r) {
-            // pair of this lane (circle method)
-            int p = -1, q = -1;
-            if (lane < bp / 2) {
+            // pair of this lane (circle method), rotation angle from H
+            if (lane < np) {
+                int p, q;
                 if (lane == 0) { p = 0; q = r + 1; }
                 else { p = (r + lane) % M + 1; q = (r - lane + M) % M + 1; }
                 if (p > q) { const int t = p; p = q; q = t; }
-                if (q >= b) { p = -1; q = -1; }
-            }
-            double c = 1.0, s = 0.0;
-            if (p >= 0) {
-                const double hpq = H[p + q * kMaxB];
-                if (hpq != 0.0) {
-                    const double tau = (H[q + q * kMaxB] - H[p + p * kMaxB]) / (2.0 * hpq);
-                    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                    c = 1.0 / sqrt(1.0 + t * t);
-                    s = t * c;
+                double c = 1.0, s = 0.0;
+                if (q < b) {
+                    const double hpq = H[p + q * kMaxB];
+                    if (hpq != 0.0) {
+                        const double tau = (H[q + q * kMaxB] - H[p + p * kMaxB]) / (2.0 * hpq);
+                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + t * t);
+                        s = t * c;
+                    }
+                } else {
+                    p = q = 0;
                 }
-            }
-            __syncwarp();
-            // rows: H[p,:], H[q,:]
-            for (int pr = 0; pr < bp / 2; ++pr) {
-                const int pp = __shfl_sync(0xffffffffu, p, pr), qq = __shfl_sync(0xffffffffu, q, pr);
-                const double cc = __shfl_sync(0xffffffffu, c, pr), ss = __shfl_sync(0xffffffffu, s, pr);
-                if (pp < 0 || ss == 0.0) continue;
-                for (int j = lane; j < b; j += 32) {
-                    const double a = H[pp + j * kMaxB], bq = H[qq + j * kMaxB];
-                    H[pp + j * kMaxB] = cc * a - ss * bq;
-                    H[qq + j * kMaxB] = ss * a + cc * bq;
-                }
+                jp[lane] = p; jq[lane] = q; jc[lane] = c; js[lane] = s;
             }
             __syncwarp();
-            for (int pr = 0; pr < bp / 2; ++pr) {
-                const int pp = __shfl_sync(0xffffffffu, p, pr), qq = __shfl_sync(0xffffffffu, q, pr);
-                const double cc = __shfl_sync(0xffffffffu, c, pr), ss = __shfl_sync(0xffffffffu, s, pr);
-                if (pp < 0 || ss == 0.0) continue;
-                for (int j = lane; j < b; j += 32) {
-                    const double a = H[j + pp * kMaxB], bq = H[j + qq * kMaxB];
-                    H[j + pp * kMaxB] = cc * a - ss * bq;
-                    H[j + qq * kMaxB] = ss * a + cc * bq;
-                    const double wa = W[j + pp * kMaxB], wb = W[j + qq * kMaxB];
-                    W[j + pp * kMaxB] = cc * wa - ss * wb;
-                    W[j + qq * kMaxB] = ss * wa + cc * wb;
-                }
+            // rows p, q of H (all pairs at once: np * b items over the warp)
+            for (int w = lane; w < np * b; w += 32) {
+                const int t = w / b, j = w - t * b;
+                const double s = js[t];
+                if (s == 0.0) continue;
+                const double c = jc[t];
+                const int p = jp[t], q = jq[t];
+                const double a = H[p + j * kMaxB], bq = H[q + j * kMaxB];
+                H[p + j * kMaxB] = c * a - s * bq;
+                H[q + j * kMaxB] = s * a + c * bq;
+            }
+            __syncwarp();
+            for (int w = lane; w < np * b; w += 32) {
+                const int t = w / b, j = w - t * b;
+                const double s = js[t];
+                if (s == 0.0) continue;
+                const double c = jc[t];
+                const int p = jp[t], q = jq[t];
+                const double a = H[j + p * kMaxB], bq = H[j + q * kMaxB];
+                H[j + p * kMaxB] = c * a - s * bq;
+                H[j + q * kMaxB] = s * a + c * bq;
+                const double wa = W[j + p * kMaxB], wb = W[j + q * kMaxB];
+                W[j + p * kMaxB] = c * wa - s * wb;
+                W[j + q * kMaxB] = s * wa + c * wb;
             }
             __syncwarp();
         }
@@ -295,7 +300,7 @@ __global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __
         // ---- Rayleigh-Ritz ----
         gemm_gx(G, X, AX, n, b);
         gram_ab(X, AX, H, n, b, true);
-        if (warp == 0) warp_jacobi(H, W, th, b);
+        if (warp == 0) warp_jacobi(H, W, th, b, it == 0 ? 12 : 3);
         __syncthreads();
         rotate(X, W, Y0, n, b);
         rotate(AX, W, Y0, n, b);

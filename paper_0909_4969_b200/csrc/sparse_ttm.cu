@@ -398,14 +398,18 @@ static void launch_ttm(Ctx* ctx, TtmArgs<T, K> A) {
     }
     A.fac_bytes = fac;
     const std::size_t smem = fac + nw * L.total;
-    auto kern = ttm::ttm_mode_kernel<T, K, RA>;
+    auto kern = A.fac_smem ? ttm::ttm_mode_kernel<T, K, RA, true> : ttm::ttm_mode_kernel<T, K, RA, false>;
     MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 1, sms = 148;
     MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem));
     MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
     const long long want = (A.n_sub + nw - 1) / nw;
     const long long blocks = std::min<long long>(want, static_cast<long long>(sms) * std::max(1, per_sm));
-    if (blocks > 0) MB_LAUNCH(ctx, (ttm::ttm_mode_kernel<T, K, RA>), static_cast<unsigned>(blocks), nw * 32, smem, A);
+    if (blocks <= 0) return;
+    if (A.fac_smem)
+        MB_LAUNCH(ctx, (ttm::ttm_mode_kernel<T, K, RA, true>), static_cast<unsigned>(blocks), nw * 32, smem, A);
+    else
+        MB_LAUNCH(ctx, (ttm::ttm_mode_kernel<T, K, RA, false>), static_cast<unsigned>(blocks), nw * 32, smem, A);
 }
 
 template <typename T, typename K>

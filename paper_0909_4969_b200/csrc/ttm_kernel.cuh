@@ -6,7 +6,7 @@
 // is in flight while the previous sub-tile is reduced; lanes then walk `seg`
 // consecutive nonzeros each (seg odd => conflict-free shared-memory reads of
 // the linear TMA layout).  Factor rows (U_a, U_b) are staged once per CTA in
-// shared memory when they fit.
+// shared memory when they fit (FS = true) and read with 128-bit loads.
 #pragma once
 
 namespace machb {
@@ -42,6 +42,19 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 
 inline std::size_t al16(std::size_t x) { return (x + 15) & ~static_cast<std::size_t>(15); }
 
+template <typename T>
+struct Vec4;
+template <>
+struct Vec4<float> {
+    using type = float4;
+    static constexpr int n = 4;
+};
+template <>
+struct Vec4<double> {
+    using type = double2;
+    static constexpr int n = 2;
+};
+
 // Per-warp shared-memory carve-up (host and device agree on this).
 template <typename T, typename K, int RA>
 struct WarpLayout {
@@ -50,36 +63,41 @@ struct WarpLayout {
     __host__ __device__ explicit WarpLayout(int s) : seg(s) {
         kbuf = ((32ull * s * sizeof(K) + 32 + 15) / 16) * 16;  // +32: alignment slack of the bulk copy
         vbuf = ((32ull * s * sizeof(T) + 32 + 15) / 16) * 16;
-        f = ((32ull * kFB * RA * sizeof(T) + 15) / 16) * 16;
+        // per-lane fibre queue blocks padded by 16 B so the lanes' 128-bit push
+        // stores land in different bank groups
+        f = ((32ull * (kFB * RA * sizeof(T) + 16) + 15) / 16) * 16;
         eib = ((32ull * kFB * sizeof(int) + 15) / 16) * 16;
         ord = ((32ull * kFB * sizeof(short) + 15) / 16) * 16;
         total = 16 /*2 mbarriers*/ + 2 * (kbuf + vbuf) + f + eib + ord;
     }
 };
 
-template <typename T, typename K, int RA>
+template <typename T, typename K, int RA, bool FS>
 __global__ void __launch_bounds__(256) ttm_mode_kernel(TtmArgs<T, K> A) {
+    using V = typename Vec4<T>::type;
+    constexpr int VN = Vec4<T>::n;
+    constexpr int LB = kFB * RA + 16 / static_cast<int>(sizeof(T));  // padded per-lane queue block
     extern __shared__ __align__(128) unsigned char smraw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
     const WarpLayout<T, K, RA> L(A.seg);
 
     // ---- CTA-shared factor rows ----
-    unsigned char* fac = smraw;
-    const T* Ua = A.Ua;
-    const T* Ub = A.Ub;
-    if (A.fac_smem) {
-        T* ua = reinterpret_cast<T*>(fac);
-        T* ub = ua + A.ua_elems;
-        for (long long i = threadIdx.x; i < A.ua_elems; i += blockDim.x) ua[i] = A.Ua[i];
-        for (long long i = threadIdx.x; i < A.ub_elems; i += blockDim.x) ub[i] = A.Ub[i];
-        Ua = ua;
-        Ub = ub;
+    T* ua_s = reinterpret_cast<T*>(smraw);
+    T* ub_s = ua_s + A.ua_elems;
+    if (FS) {
+        const V* ga = reinterpret_cast<const V*>(A.Ua);
+        V* sa = reinterpret_cast<V*>(ua_s);
+        for (long long i = threadIdx.x; i < A.ua_elems / VN; i += blockDim.x) sa[i] = ga[i];
+        for (long long i = threadIdx.x; i < A.ub_elems; i += blockDim.x) ub_s[i] = A.Ub[i];
     }
+    const T* Ua = FS ? ua_s : A.Ua;
+    const T* Ub = FS ? ub_s : A.Ub;
+
     unsigned char* wbase = smraw + A.fac_bytes + L.total * wib;
     std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(wbase);
-    unsigned char* kb[2] = {wbase + 16, wbase + 16 + L.kbuf};
-    unsigned char* vb[2] = {wbase + 16 + 2 * L.kbuf, wbase + 16 + 2 * L.kbuf + L.vbuf};
+    unsigned char* kbuf0 = wbase + 16;
+    unsigned char* vbuf0 = wbase + 16 + 2 * L.kbuf;
     T* F = reinterpret_cast<T*>(wbase + 16 + 2 * (L.kbuf + L.vbuf));
     int* EIB = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(F) + L.f);
     short* ord = reinterpret_cast<short*>(reinterpret_cast<unsigned char*>(EIB) + L.eib);
@@ -104,8 +122,8 @@ __global__ void __launch_bounds__(256) ttm_mode_kernel(TtmArgs<T, K> A) {
         const std::uint32_t vbytes = static_cast<std::uint32_t>(((vg - v0) + st.len * sizeof(T) + 15) & ~std::size_t(15));
         fence_proxy_async();
         mbar_expect_tx(&bars[b], kbytes + vbytes);
-        bulk_g2s(kb[b], k0, kbytes, &bars[b]);
-        bulk_g2s(vb[b], v0, vbytes, &bars[b]);
+        bulk_g2s(kbuf0 + b * L.kbuf, k0, kbytes, &bars[b]);
+        bulk_g2s(vbuf0 + b * L.vbuf, v0, vbytes, &bars[b]);
     };
 
     const int rb = A.rb;
@@ -114,29 +132,41 @@ __global__ void __launch_bounds__(256) ttm_mode_kernel(TtmArgs<T, K> A) {
     const bool gactive = g < G;
     const int seg = A.seg;
     const K maska = A.maska, maskb = A.maskb;
+    const int ba = A.ba;
+    const int rbs = A.rbs;
 
     if (gw < A.n_sub && lane == 0) prefetch(gw, 0);
+    SubTile st = (gw < A.n_sub) ? A.subs[gw] : SubTile{0, 0, 0};
     int it = 0;
     for (long long s = gw; s < A.n_sub; s += stride, ++it) {
         const int b = it & 1;
-        if (s + stride < A.n_sub && lane == 0) prefetch(s + stride, b ^ 1);
-        const SubTile st = A.subs[s];
+        SubTile nxt{0, 0, 0};
+        if (s + stride < A.n_sub) {
+            nxt = A.subs[s + stride];
+            if (lane == 0) prefetch(s + stride, b ^ 1);
+        }
         mbar_wait(&bars[b], static_cast<std::uint32_t>((it >> 1) & 1));
-        const K* sk = reinterpret_cast<const K*>(kb[b]) + ((st.start * sizeof(K)) & 15) / sizeof(K);
-        const T* sv = reinterpret_cast<const T*>(vb[b]) + ((st.start * sizeof(T)) & 15) / sizeof(T);
+        const K* sk = reinterpret_cast<const K*>(kbuf0 + b * L.kbuf) + ((st.start * sizeof(K)) & 15) / sizeof(K);
+        const T* sv = reinterpret_cast<const T*>(vbuf0 + b * L.vbuf) + ((st.start * sizeof(T)) & 15) / sizeof(T);
 
         T acc1[RA];
         T acc2[RA];
 #pragma unroll
         for (int a = 0; a < RA; ++a) { acc1[a] = T(0); acc2[a] = T(0); }
         int nb = 0;
-        bool has = false;
-        int cur = 0;
+        int cur = -1;
 
         auto push = [&]() {
-            T* f = F + (lane * kFB + nb) * RA;
+            T* f = F + lane * LB + nb * RA;
 #pragma unroll
-            for (int a = 0; a < RA; ++a) { f[a] = acc1[a]; acc1[a] = T(0); }
+            for (int a = 0; a < RA; a += VN) {
+                V v;
+                if constexpr (VN == 4) v = V{acc1[a], acc1[a + 1], acc1[a + 2], acc1[a + 3]};
+                else v = V{acc1[a], acc1[a + 1]};
+                *reinterpret_cast<V*>(f + a) = v;
+            }
+#pragma unroll
+            for (int a = 0; a < RA; ++a) acc1[a] = T(0);
             EIB[lane * kFB + nb] = cur;
             ++nb;
         };
@@ -155,10 +185,21 @@ __global__ void __launch_bounds__(256) ttm_mode_kernel(TtmArgs<T, K> A) {
                 const int e = e0 + g;
                 if (gactive && e < total) {
                     const int slot = ord[e];
-                    const T u = Ub[static_cast<long long>(EIB[slot]) * A.rbs + beta];
-                    const T* f = F + slot * RA;
+                    const T u = Ub[static_cast<long long>(EIB[slot]) * rbs + beta];
+                    const T* f = F + (slot / kFB) * LB + (slot % kFB) * RA;
 #pragma unroll
-                    for (int a = 0; a < RA; ++a) acc2[a] = fma(f[a], u, acc2[a]);
+                    for (int a = 0; a < RA; a += VN) {
+                        const V fv = *reinterpret_cast<const V*>(f + a);
+                        if constexpr (VN == 4) {
+                            acc2[a] = fma(fv.x, u, acc2[a]);
+                            acc2[a + 1] = fma(fv.y, u, acc2[a + 1]);
+                            acc2[a + 2] = fma(fv.z, u, acc2[a + 2]);
+                            acc2[a + 3] = fma(fv.w, u, acc2[a + 3]);
+                        } else {
+                            acc2[a] = fma(fv.x, u, acc2[a]);
+                            acc2[a + 1] = fma(fv.y, u, acc2[a + 1]);
+                        }
+                    }
                 }
             }
             __syncwarp();
@@ -166,22 +207,34 @@ __global__ void __launch_bounds__(256) ttm_mode_kernel(TtmArgs<T, K> A) {
         };
 
         const int my0 = lane * seg;
+        const int cnt = max(0, min(seg, st.len - my0));
         for (int j = 0; j < seg; ++j) {
-            const int e = my0 + j;
-            if (e < st.len) {
-                const K key = sk[e];
-                const T v = sv[e];
-                const int ib = static_cast<int>((key >> A.ba) & maskb);
-                if (has && ib != cur) push();
-                cur = ib;
-                has = true;
-                const T* u = Ua + static_cast<long long>(key & maska) * RA;
+            if (j < cnt) {
+                const K key = sk[my0 + j];
+                const T v = sv[my0 + j];
+                const int ib = static_cast<int>((key >> ba) & maskb);
+                if (ib != cur) {
+                    if (cur >= 0) push();
+                    cur = ib;
+                }
+                const V* u = reinterpret_cast<const V*>(Ua + static_cast<long long>(key & maska) * RA);
 #pragma unroll
-                for (int a = 0; a < RA; ++a) acc1[a] = fma(v, u[a], acc1[a]);
+                for (int a = 0; a < RA; a += VN) {
+                    const V uv = FS ? u[a / VN] : __ldg(u + a / VN);
+                    if constexpr (VN == 4) {
+                        acc1[a] = fma(v, uv.x, acc1[a]);
+                        acc1[a + 1] = fma(v, uv.y, acc1[a + 1]);
+                        acc1[a + 2] = fma(v, uv.z, acc1[a + 2]);
+                        acc1[a + 3] = fma(v, uv.w, acc1[a + 3]);
+                    } else {
+                        acc1[a] = fma(v, uv.x, acc1[a]);
+                        acc1[a + 1] = fma(v, uv.y, acc1[a + 1]);
+                    }
+                }
             }
             if (__any_sync(0xffffffffu, nb == kFB)) drain();
         }
-        if (has) push();
+        if (cur >= 0) push();
         drain();
 
         for (int gg = 1; gg < G; ++gg) {
@@ -197,6 +250,7 @@ __global__ void __launch_bounds__(256) ttm_mode_kernel(TtmArgs<T, K> A) {
             for (int a = 0; a < RA; ++a)
                 if (a < A.ra) out[a * A.sa + beta * A.sb] = acc2[a];
         }
+        st = nxt;
         __syncwarp();  // buffer b is refilled two iterations later
     }
 }
