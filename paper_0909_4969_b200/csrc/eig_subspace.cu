@@ -148,10 +148,8 @@ __device__ void warp_jacobi(double* H, double* W, double* th, int b, int max_swe
     const int M = bp - 1;
     for (int sweep = 0; sweep < max_sweeps && b > 1; ++sweep) {
         double off = 0.0;
-        for (int e = lane; e < b * b; e += 32) {
-            const int i = e % b, j = e / b;
-            if (i < j) off += H[i + j * kMaxB] * H[i + j * kMaxB];
-        }
+        if (lane < b)
+            for (int i = 0; i < lane; ++i) off += H[i + lane * kMaxB] * H[i + lane * kMaxB];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
         if (off <= 1e-30 * nrm) break;
@@ -178,30 +176,33 @@ __device__ void warp_jacobi(double* H, double* W, double* th, int b, int max_swe
                 jp[lane] = p; jq[lane] = q; jc[lane] = c; js[lane] = s;
             }
             __syncwarp();
-            // rows p, q of H (all pairs at once: np * b items over the warp)
-            for (int w = lane; w < np * b; w += 32) {
-                const int t = w / b, j = w - t * b;
-                const double s = js[t];
-                if (s == 0.0) continue;
-                const double c = jc[t];
-                const int p = jp[t], q = jq[t];
-                const double a = H[p + j * kMaxB], bq = H[q + j * kMaxB];
-                H[p + j * kMaxB] = c * a - s * bq;
-                H[q + j * kMaxB] = s * a + c * bq;
+            // rows p, q of H: lane j owns column j, all pairs (disjoint) in turn
+            if (lane < b) {
+                const int j = lane;
+#pragma unroll 4
+                for (int t = 0; t < np; ++t) {
+                    const double s = js[t], c = jc[t];
+                    const int p = jp[t], q = jq[t];
+                    const double a = H[p + j * kMaxB], bq = H[q + j * kMaxB];
+                    H[p + j * kMaxB] = c * a - s * bq;
+                    H[q + j * kMaxB] = s * a + c * bq;
+                }
             }
             __syncwarp();
-            for (int w = lane; w < np * b; w += 32) {
-                const int t = w / b, j = w - t * b;
-                const double s = js[t];
-                if (s == 0.0) continue;
-                const double c = jc[t];
-                const int p = jp[t], q = jq[t];
-                const double a = H[j + p * kMaxB], bq = H[j + q * kMaxB];
-                H[j + p * kMaxB] = c * a - s * bq;
-                H[j + q * kMaxB] = s * a + c * bq;
-                const double wa = W[j + p * kMaxB], wb = W[j + q * kMaxB];
-                W[j + p * kMaxB] = c * wa - s * wb;
-                W[j + q * kMaxB] = s * wa + c * wb;
+            // columns p, q of H and W: lane j owns row j
+            if (lane < b) {
+                const int j = lane;
+#pragma unroll 4
+                for (int t = 0; t < np; ++t) {
+                    const double s = js[t], c = jc[t];
+                    const int p = jp[t], q = jq[t];
+                    const double a = H[j + p * kMaxB], bq = H[j + q * kMaxB];
+                    H[j + p * kMaxB] = c * a - s * bq;
+                    H[j + q * kMaxB] = s * a + c * bq;
+                    const double wa = W[j + p * kMaxB], wb = W[j + q * kMaxB];
+                    W[j + p * kMaxB] = c * wa - s * wb;
+                    W[j + q * kMaxB] = s * wa + c * wb;
+                }
             }
             __syncwarp();
         }
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __
         // ---- Rayleigh-Ritz ----
         gemm_gx(G, X, AX, n, b);
         gram_ab(X, AX, H, n, b, true);
-        if (warp == 0) warp_jacobi(H, W, th, b, it == 0 ? 12 : 3);
+        if (warp == 0) warp_jacobi(H, W, th, b, it == 0 ? 10 : 4);
         __syncthreads();
         rotate(X, W, Y0, n, b);
         rotate(AX, W, Y0, n, b);
@@ -406,7 +407,7 @@ bool eig_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, int
 namespace machb {
 
 int eig_block(int n, int k) {
-    const int p = k < 8 ? 4 : 8;
+    const int p = 4;
     return std::min(n, std::min(kMaxB, k + p));
 }
 

@@ -5,6 +5,8 @@
 // the per-mode basis status needed for the stop rule (tucker.cpp:102) and the
 // completion warnings (tucker.cpp:34-38).
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "sparse_ttm.cuh"
@@ -172,6 +174,13 @@ void lsb_device(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U
     const bool sub = eig_select(ctx, G.get(), side, kk, X0, x0c, warm ? warm->X.get() : nullptr, b, V.get(), sig.get(),
                                 est.get());
     if (warm) warm->cols = sub ? b : 0;
+    if (std::getenv("MACH_DEBUG_EIG")) {
+        int h[3] = {0, 0, 0};
+        to_host(ctx, h, est.get(), 3);
+        sync(ctx);
+        std::fprintf(stderr, "[eig] side=%d k=%d b=%d subspace=%d converged=%d iters=%d warm=%d\n", side, kk, b,
+                     sub ? 1 : 0, h[0], h[2], x0c);
+    }
     if (row_side) {
         basis_from_side(ctx, V.get(), sig.get(), rows, k, est.get(), U, sv, st);
     } else {
