@@ -9,13 +9,17 @@
 //   X <- previous sweep's Ritz block (or a deterministic random block)
 //   repeat: Rayleigh-Ritz (H = X^T G X, one-warp cyclic Jacobi on H),
 //           residual test |G x_i - theta_i x_i| <= tol * theta_1 for i < k,
-//           degree-m Chebyshev filter damping [0, theta_b], CGS2 orthonormalise
+//           degree-m Chebyshev filter damping [0, theta_b], CholQR2
+//           orthonormalisation (CGS2 when Cholesky breaks down)
 // The residual certificate bounds each Ritz vector's angle to its eigenvector
 // by residual / gap, so converged output equals the reference's exact
 // eigendecomposition to that precision.  When the residual test is not met
 // within max_iters (tiny spectral gaps), status[0] stays 0 and the exact
 // selected-eigenpair solver (eig.cu) runs instead — it checks status and is a
 // no-op otherwise.
+#include <cstdio>
+#include <cstdlib>
+
 #include "sparse_ttm.cuh"
 
 namespace machb {
@@ -25,6 +29,7 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxB = 32;
+constexpr int kLd = kMaxB + 1;  // odd leading dimension of the b x b smem matrices
 
 __device__ double cta_sum(double v, double* red) {
 #pragma unroll
@@ -46,50 +51,52 @@ __device__ double rnd_unit(unsigned c, unsigned i) {
     return static_cast<double>(z >> 11) * 0x1.0p-53 * 2.0 - 1.0;
 }
 
-// OUT (n x b) = G X, G n x n column-major (smem or global), X/OUT in smem ld n
+// OUT (n x b) = G X; b is a multiple of 4; G n x n column-major; X/OUT ld n
 __device__ void gemm_gx(const double* G, const double* X, double* OUT, int n, int b) {
-    const int ncg = (b + 3) / 4;  // column groups of 4
+    const int ncg = b >> 2;
     for (int w = threadIdx.x; w < n * ncg; w += kThreads) {
-        const int i = w % n, cg = w / n;
-        const int j0 = cg * 4;
+        const int cg = w / n, i = w - cg * n;
+        const double* x0 = X + static_cast<std::size_t>(cg * 4) * n;
         double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-        const double* x0 = X + static_cast<std::size_t>(j0) * n;
+#pragma unroll 4
         for (int l = 0; l < n; ++l) {
             const double g = G[i + static_cast<std::size_t>(l) * n];
             a0 = fma(g, x0[l], a0);
-            if (j0 + 1 < b) a1 = fma(g, x0[l + n], a1);
-            if (j0 + 2 < b) a2 = fma(g, x0[l + 2 * n], a2);
-            if (j0 + 3 < b) a3 = fma(g, x0[l + 3 * n], a3);
+            a1 = fma(g, x0[l + n], a1);
+            a2 = fma(g, x0[l + 2 * n], a2);
+            a3 = fma(g, x0[l + 3 * n], a3);
         }
-        OUT[i + static_cast<std::size_t>(j0) * n] = a0;
-        if (j0 + 1 < b) OUT[i + static_cast<std::size_t>(j0 + 1) * n] = a1;
-        if (j0 + 2 < b) OUT[i + static_cast<std::size_t>(j0 + 2) * n] = a2;
-        if (j0 + 3 < b) OUT[i + static_cast<std::size_t>(j0 + 3) * n] = a3;
+        double* o = OUT + static_cast<std::size_t>(cg * 4) * n + i;
+        o[0] = a0;
+        o[n] = a1;
+        o[2 * n] = a2;
+        o[3 * n] = a3;
     }
     __syncthreads();
 }
 
-// C (b x b) = A^T B for n x b blocks (warp per entry, fixed order)
-__device__ void gram_ab(const double* A, const double* B, double* C, int n, int b, bool sym) {
+// C (b x b, ld kMaxB) = A^T B for n x b blocks; warp per entry, fixed order
+__device__ void gram_ab(const double* A, const double* B, double* C, int n, int b) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int e = warp; e < b * b; e += kWarps) {
-        const int i = e % b, j = e / b;
-        if (sym && i > j) continue;
+        const int j = e / b, i = e - j * b;
+        if (i > j) continue;
+        const double* a = A + static_cast<std::size_t>(i) * n;
+        const double* c = B + static_cast<std::size_t>(j) * n;
         double s = 0.0;
-        for (int r = lane; r < n; r += 32) s += A[r + static_cast<std::size_t>(i) * n] * B[r + static_cast<std::size_t>(j) * n];
+        for (int r = lane; r < n; r += 32) s = fma(a[r], c[r], s);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) {
-            C[i + j * kMaxB] = s;
-            if (sym) C[j + i * kMaxB] = s;
+            C[i + j * kLd] = s;
+            C[j + i * kLd] = s;
         }
     }
     __syncthreads();
 }
 
-// classical Gram-Schmidt applied twice (CGS2), column by column; returns
-// false if a column collapses (then it is re-randomised once)
-__device__ void orthonormalize(double* X, int n, int b, double* coef, double* red) {
+// CGS2 column by column (robust fallback)
+__device__ void orth_cgs2(double* X, int n, int b, double* coef, double* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int j = 0; j < b; ++j) {
         double* xj = X + static_cast<std::size_t>(j) * n;
@@ -129,136 +136,312 @@ __device__ void orthonormalize(double* X, int n, int b, double* coef, double* re
     }
 }
 
-// one-warp cyclic Jacobi on H (b x b, ld kMaxB) -> eigenvectors W, values th
-// (descending, W columns permuted alike)
-__device__ void warp_jacobi(double* H, double* W, double* th, int b, int max_sweeps) {
-    const int lane = threadIdx.x & 31;
-    __shared__ int jp[kMaxB / 2], jq[kMaxB / 2];
-    __shared__ double jc[kMaxB / 2], js[kMaxB / 2];
-    const int bp = (b + 1) & ~1;  // even player count (a dummy when b is odd)
-    for (int e = lane; e < kMaxB * kMaxB; e += 32) W[e] = ((e % kMaxB) == (e / kMaxB)) ? 1.0 : 0.0;
-    __syncwarp();
-    double nrm = 0.0;
-    for (int e = lane; e < b * b; e += 32) {
-        const double h = H[(e % b) + (e / b) * kMaxB];
-        nrm += h * h;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
-    const int M = bp - 1;
-    for (int sweep = 0; sweep < max_sweeps && b > 1; ++sweep) {
-        double off = 0.0;
-        if (lane < b)
-            for (int i = 0; i < lane; ++i) off += H[i + lane * kMaxB] * H[i + lane * kMaxB];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
-        if (off <= 1e-30 * nrm) break;
-        const int np = bp / 2;
-        for (int r = 0; r < M; ++r) {
-            // pair of this lane (circle method), rotation angle from H
-            if (lane < np) {
-                int p, q;
-                if (lane == 0) { p = 0; q = r + 1; }
-                else { p = (r + lane) % M + 1; q = (r - lane + M) % M + 1; }
-                if (p > q) { const int t = p; p = q; q = t; }
-                double c = 1.0, s = 0.0;
-                if (q < b) {
-                    const double hpq = H[p + q * kMaxB];
-                    if (hpq != 0.0) {
-                        const double tau = (H[q + q * kMaxB] - H[p + p * kMaxB]) / (2.0 * hpq);
-                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                        c = 1.0 / sqrt(1.0 + t * t);
-                        s = t * c;
-                    }
-                } else {
-                    p = q = 0;
-                }
-                jp[lane] = p; jq[lane] = q; jc[lane] = c; js[lane] = s;
+// One CholQR pass on X (and the same right-multiplication on Y when given):
+// S = X^T X = R^T R, X <- X R^{-1}.  Returns false when S is not numerically
+// positive definite (the caller then falls back to CGS2).
+__device__ bool cholqr(double* X, double* Y, int n, int b, double* S, double* rinv, int* flag) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    gram_ab(X, X, S, n, b);
+    if (warp == 0) {
+        // Cholesky S = R^T R (upper R stored in S), lane l owns column l
+        bool ok = true;
+        for (int j = 0; j < b; ++j) {
+            double d = 0.0;
+            if (lane == j) {
+                d = S[j + j * kLd];
+                for (int p = 0; p < j; ++p) d -= S[p + j * kLd] * S[p + j * kLd];
             }
-            __syncwarp();
-            // rows p, q of H: lane j owns column j, all pairs (disjoint) in turn
-            if (lane < b) {
-                const int j = lane;
-#pragma unroll 4
-                for (int t = 0; t < np; ++t) {
-                    const double s = js[t], c = jc[t];
-                    const int p = jp[t], q = jq[t];
-                    const double a = H[p + j * kMaxB], bq = H[q + j * kMaxB];
-                    H[p + j * kMaxB] = c * a - s * bq;
-                    H[q + j * kMaxB] = s * a + c * bq;
-                }
+            d = __shfl_sync(0xffffffffu, d, j);
+            const double orig = S[j + j * kLd];
+            if (!(d > 1e-14 * orig) || !(orig > 0.0)) {
+                ok = false;
+                break;
             }
+            const double rjj = sqrt(d);
+            const double inv = 1.0 / rjj;
             __syncwarp();
-            // columns p, q of H and W: lane j owns row j
-            if (lane < b) {
-                const int j = lane;
-#pragma unroll 4
-                for (int t = 0; t < np; ++t) {
-                    const double s = js[t], c = jc[t];
-                    const int p = jp[t], q = jq[t];
-                    const double a = H[j + p * kMaxB], bq = H[j + q * kMaxB];
-                    H[j + p * kMaxB] = c * a - s * bq;
-                    H[j + q * kMaxB] = s * a + c * bq;
-                    const double wa = W[j + p * kMaxB], wb = W[j + q * kMaxB];
-                    W[j + p * kMaxB] = c * wa - s * wb;
-                    W[j + q * kMaxB] = s * wa + c * wb;
-                }
+            if (lane > j && lane < b) {
+                double v = S[j + lane * kLd];
+                for (int p = 0; p < j; ++p) v -= S[p + j * kLd] * S[p + lane * kLd];
+                S[j + lane * kLd] = v * inv;
+            }
+            if (lane == j) {
+                S[j + j * kLd] = rjj;
+                rinv[j] = inv;
             }
             __syncwarp();
         }
+        if (lane == 0) *flag = ok ? 1 : 0;
     }
-    // sort descending (selection sort by lane 0 on indices, then permute)
-    __shared__ int perm[kMaxB];
-    if (lane == 0) {
-        for (int i = 0; i < b; ++i) perm[i] = i;
-        for (int i = 0; i < b; ++i) {
-            int best = i;
-            for (int j = i + 1; j < b; ++j)
-                if (H[perm[j] + perm[j] * kMaxB] > H[perm[best] + perm[best] * kMaxB]) best = j;
-            const int t = perm[i]; perm[i] = perm[best]; perm[best] = t;
+    __syncthreads();
+    if (!*flag) return false;
+    // row-wise triangular solve z R = x, in place (each thread owns its rows)
+    for (int r = threadIdx.x; r < n; r += kThreads) {
+        for (int pass = 0; pass < (Y ? 2 : 1); ++pass) {
+            double* M = pass ? Y : X;
+            for (int l = 0; l < b; ++l) {
+                double v = M[r + static_cast<std::size_t>(l) * n];
+                for (int p = 0; p < l; ++p) v -= M[r + static_cast<std::size_t>(p) * n] * S[p + l * kLd];
+                M[r + static_cast<std::size_t>(l) * n] = v * rinv[l];
+            }
         }
     }
-    __syncwarp();
-    for (int i = lane; i < b; i += 32) th[i] = H[perm[i] + perm[i] * kMaxB];
-    __syncwarp();
-    // W columns permuted into H's (now free) storage, then copied back
-    for (int e = lane; e < b * b; e += 32) {
-        const int r = e % b, cidx = e / b;
-        H[r + cidx * kMaxB] = W[r + perm[cidx] * kMaxB];
-    }
-    __syncwarp();
-    for (int e = lane; e < b * b; e += 32) W[(e % b) + (e / b) * kMaxB] = H[(e % b) + (e / b) * kMaxB];
-    __syncwarp();
+    __syncthreads();
+    return true;
 }
 
-// X <- X W (n x b) in place using tmp (n x b)
-__device__ void rotate(double* X, const double* W, double* tmp, int n, int b) {
-    for (int e = threadIdx.x; e < n * b; e += kThreads) {
-        const int i = e % n, j = e / n;
-        double s = 0.0;
-        for (int l = 0; l < b; ++l) s += X[i + static_cast<std::size_t>(l) * n] * W[l + j * kMaxB];
-        tmp[e] = s;
+__device__ void orthonormalize(double* X, int n, int b, double* S, double* rinv, double* coef, double* red, int* flag) {
+    if (!cholqr(X, nullptr, n, b, S, rinv, flag) || !cholqr(X, nullptr, n, b, S, rinv, flag)) orth_cgs2(X, n, b, coef, red);
+}
+
+// Jacobi rotation annihilating H[p][q]: angle in fp32 (fast SFU), the (c, s)
+// pair renormalised in fp64 so the applied rotation is orthogonal to fp64.
+__device__ void jacobi_cs(double hpp, double hqq, double hpq, double& c, double& s) {
+    c = 1.0;
+    s = 0.0;
+    const float fpq = static_cast<float>(hpq);
+    if (fpq == 0.0f) return;
+    const float tau = static_cast<float>(hqq - hpp) / (2.0f * fpq);
+    float t;
+    if (fabsf(tau) > 1e18f) t = 0.5f / tau;
+    else t = copysignf(1.0f, tau) / (fabsf(tau) + sqrtf(1.0f + tau * tau));
+    const float c32 = rsqrtf(1.0f + t * t);
+    double cc = c32, ss = static_cast<double>(t) * c32;
+    const double delta = cc * cc + ss * ss - 1.0;
+    const double sc = 1.0 - 0.5 * delta + 0.375 * delta * delta;
+    c = cc * sc;
+    s = ss * sc;
+}
+
+// CTA-parallel cyclic Jacobi on H (b x b, ld kLd) -> eigenvectors W, values
+// th (descending, W columns permuted alike).  Each round annihilates np
+// disjoint pairs (circle method); thread (t, j) = (tid >> 5, tid & 31)
+// rotates element j of pair t, so a round is three barrier-separated phases.
+// Rotation angles in fp32 (jacobi_cs), applied rotations orthogonal in fp64.
+__device__ int cta_jacobi(double* H, double* W, double* th, int b, int max_sweeps, double* red) {
+    __shared__ int jp[kMaxB / 2], jq[kMaxB / 2], perm[kMaxB];
+    __shared__ double jc[kMaxB / 2], js[kMaxB / 2];
+    const int tid = threadIdx.x;
+    const int bp = (b + 1) & ~1;
+    const int np = bp / 2;
+    const int M = bp - 1;
+    for (int e = tid; e < kMaxB * kMaxB; e += kThreads) {
+        const int c = e >> 5, r = e & 31;
+        W[r + c * kLd] = (r == c) ? 1.0 : 0.0;
+    }
+    double nrm = 0.0;
+    for (int e = tid; e < b * kMaxB; e += kThreads) {
+        const int c = e >> 5, r = e & 31;
+        if (r < b) nrm += H[r + c * kLd] * H[r + c * kLd];
+    }
+    nrm = cta_sum(nrm, red);
+    const int t = tid >> 5, j = tid & 31;
+    int sweep = 0;
+    for (; sweep < max_sweeps && b > 1; ++sweep) {
+        double off = 0.0;
+        for (int e = tid; e < b * kMaxB; e += kThreads) {
+            const int c = e >> 5, r = e & 31;
+            if (r < c) off += H[r + c * kLd] * H[r + c * kLd];
+        }
+        off = cta_sum(off, red);
+        if (off <= 1e-30 * nrm) break;
+        for (int r = 0; r < M; ++r) {
+            if (tid < np) {
+                int p, q;
+                if (tid == 0) {
+                    p = 0;
+                    q = r + 1;
+                } else {
+                    int x = r + tid;
+                    if (x >= M) x -= M;
+                    int y = r - tid;
+                    if (y < 0) y += M;
+                    p = x + 1;
+                    q = y + 1;
+                }
+                if (p > q) { const int tt = p; p = q; q = tt; }
+                double c = 1.0, s = 0.0;
+                if (q < b) jacobi_cs(H[p + p * kLd], H[q + q * kLd], H[p + q * kLd], c, s);
+                else p = q = 0;
+                jp[tid] = p; jq[tid] = q; jc[tid] = c; js[tid] = s;
+            }
+            __syncthreads();
+            if (t < np && j < b) {  // rows p, q
+                const double s = js[t];
+                if (s != 0.0) {
+                    const double c = jc[t];
+                    const int p = jp[t], q = jq[t];
+                    const double a = H[p + j * kLd], bq = H[q + j * kLd];
+                    H[p + j * kLd] = c * a - s * bq;
+                    H[q + j * kLd] = s * a + c * bq;
+                }
+            }
+            __syncthreads();
+            if (t < np && j < b) {  // columns p, q of H and W
+                const double s = js[t];
+                if (s != 0.0) {
+                    const double c = jc[t];
+                    const int p = jp[t], q = jq[t];
+                    const double a = H[j + p * kLd], bq = H[j + q * kLd];
+                    H[j + p * kLd] = c * a - s * bq;
+                    H[j + q * kLd] = s * a + c * bq;
+                    const double wa = W[j + p * kLd], wb = W[j + q * kLd];
+                    W[j + p * kLd] = c * wa - s * wb;
+                    W[j + q * kLd] = s * wa + c * wb;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // descending order: rank of each diagonal entry (ties by index)
+    if (tid < b) {
+        const double di = H[tid + tid * kLd];
+        int rank = 0;
+        for (int q = 0; q < b; ++q) {
+            const double dq = H[q + q * kLd];
+            rank += (dq > di) || (dq == di && q < tid);
+        }
+        perm[rank] = tid;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < n * b; e += kThreads) X[e] = tmp[e];
+    if (tid < b) th[tid] = H[perm[tid] + perm[tid] * kLd];
+    for (int e = tid; e < b * kMaxB; e += kThreads) {  // permuted W staged in H
+        const int c = e >> 5, r = e & 31;
+        if (r < b) H[r + c * kLd] = W[r + perm[c] * kLd];
+    }
     __syncthreads();
+    for (int e = tid; e < b * kMaxB; e += kThreads) {
+        const int c = e >> 5, r = e & 31;
+        if (r < b) W[r + c * kLd] = H[r + c * kLd];
+    }
+    __syncthreads();
+    return sweep;
+}
+
+// Quick Rayleigh-Ritz for a nearly diagonal H (warm, converging blocks):
+// second-order perturbation W = I + Z + Z^2/2 with Z_ij = H_ij / (D_j - D_i),
+// i.e. exp(Z) to O(|Z|^3).  Returns false (W untouched) when some pair that
+// involves a wanted index (< k) is not well separated, so the caller runs the
+// full Jacobi instead.  Exactness is enforced by the caller's residual test.
+__device__ bool quick_rr(double* H, double* W, double* th, int b, int k, double* Zs, int* flag) {
+    __shared__ int perm[kMaxB];
+    const int tid = threadIdx.x;
+    if (tid == 0) *flag = 1;
+    __syncthreads();
+    for (int e = tid; e < b * kMaxB; e += kThreads) {
+        const int j = e >> 5, i = e & 31;
+        if (i >= b) continue;
+        double z = 0.0;
+        if (i != j) {
+            const double hij = H[i + j * kLd];
+            const double gap = H[j + j * kLd] - H[i + i * kLd];
+            const bool wanted = i < k || j < k;
+            if (fabs(hij) > 0.02 * fabs(gap)) {
+                if (wanted && hij != 0.0) *flag = 0;
+            } else if (gap != 0.0) {
+                z = hij / gap;
+            }
+        }
+        Zs[i + j * kLd] = z;
+    }
+    __syncthreads();
+    if (!*flag) return false;
+    // W = I + Z + Z^2 / 2
+    for (int e = tid; e < b * kMaxB; e += kThreads) {
+        const int j = e >> 5, i = e & 31;
+        if (i >= b) continue;
+        double z2 = 0.0;
+        for (int l = 0; l < b; ++l) z2 = fma(Zs[i + l * kLd], Zs[l + j * kLd], z2);
+        W[i + j * kLd] = (i == j ? 1.0 : 0.0) + Zs[i + j * kLd] + 0.5 * z2;
+    }
+    __syncthreads();
+    // Ritz values th_j = w_j^T H w_j (Zs reused for H W)
+    for (int e = tid; e < b * kMaxB; e += kThreads) {
+        const int j = e >> 5, i = e & 31;
+        if (i >= b) continue;
+        double s = 0.0;
+        for (int l = 0; l < b; ++l) s = fma(H[i + l * kLd], W[l + j * kLd], s);
+        Zs[i + j * kLd] = s;
+    }
+    __syncthreads();
+    if (tid < b) {
+        double s = 0.0;
+        for (int l = 0; l < b; ++l) s = fma(W[l + tid * kLd], Zs[l + tid * kLd], s);
+        H[tid + tid * kLd] = s;  // diagonal now holds the Ritz values
+    }
+    __syncthreads();
+    if (tid < b) {
+        const double di = H[tid + tid * kLd];
+        int rank = 0;
+        for (int q = 0; q < b; ++q) {
+            const double dq = H[q + q * kLd];
+            rank += (dq > di) || (dq == di && q < tid);
+        }
+        perm[rank] = tid;
+    }
+    __syncthreads();
+    if (tid < b) th[tid] = H[perm[tid] + perm[tid] * kLd];
+    for (int e = tid; e < b * kMaxB; e += kThreads) {
+        const int c = e >> 5, r = e & 31;
+        if (r < b) Zs[r + c * kLd] = W[r + perm[c] * kLd];
+    }
+    __syncthreads();
+    for (int e = tid; e < b * kMaxB; e += kThreads) {
+        const int c = e >> 5, r = e & 31;
+        if (r < b) W[r + c * kLd] = Zs[r + c * kLd];
+    }
+    __syncthreads();
+    return true;
+}
+
+// X <- X W and AX <- AX W (n x b) using tmp (n x b)
+__device__ void rotate2(double* X, double* AX, const double* W, double* tmp, int n, int b) {
+    for (int pass = 0; pass < 2; ++pass) {
+        double* M = pass ? AX : X;
+        for (int e = threadIdx.x; e < n * b; e += kThreads) {
+            const int j = e / n, i = e - j * n;
+            double s = 0.0;
+            for (int l = 0; l < b; ++l) s = fma(M[i + static_cast<std::size_t>(l) * n], W[l + j * kLd], s);
+            tmp[e] = s;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < n * b; e += kThreads) M[e] = tmp[e];
+        __syncthreads();
+    }
 }
 
 }  // namespace
 
 // status: [0] converged, [1] zero matrix, [2] iterations used
 __global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __restrict__ Gin, int n, int k, int b, int m,
-                                                                int maxit, double tol, const double* X0,
-                                                                int x0_cols, double* Xkeep,  // may alias X0
+                                                                int maxit, double tol, const double* X0, int x0_cols,
+                                                                double* Xkeep,  // may alias X0
                                                                 double* __restrict__ V, double* __restrict__ sig,
-                                                                int* __restrict__ status, int g_in_smem) {
+                                                                int* __restrict__ status, int g_in_smem,
+                                                                long long* __restrict__ tstamp) {
     extern __shared__ double sm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* H = sm;                        // kMaxB^2
-    double* W = H + kMaxB * kMaxB;         // kMaxB^2
-    double* th = W + kMaxB * kMaxB;        // kMaxB
+    int ns_ = 0;
+    if (tstamp && threadIdx.x == 0) tstamp[239] = clock64();
+#define STAMP(tag)                                                                     \
+    do {                                                                               \
+        if (tstamp && threadIdx.x == 0 && ns_ < 118) {                                 \
+            long long t_;                                                              \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+            tstamp[2 * ns_] = (tag);                                                   \
+            tstamp[2 * ns_ + 1] = t_;                                                  \
+            ++ns_;                                                                     \
+        }                                                                              \
+    } while (0)
+    STAMP(0);
+    __shared__ int flag;
+    double* H = sm;                        // kLd * kMaxB
+    double* W = H + kLd * kMaxB;           // kLd * kMaxB
+    double* S = W + kLd * kMaxB;           // kLd * kMaxB
+    double* th = S + kLd * kMaxB;          // kMaxB
     double* coef = th + kMaxB;             // kMaxB
-    double* red = coef + kMaxB;            // 32
+    double* rinv = coef + kMaxB;           // kMaxB
+    double* red = rinv + kMaxB;            // 32
     double* X = red + 32;                  // n*b
     double* AX = X + static_cast<std::size_t>(n) * b;
     double* Y0 = AX + static_cast<std::size_t>(n) * b;
@@ -289,22 +472,27 @@ __global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __
 
     // ---- start block ----
     for (int e = threadIdx.x; e < n * b; e += kThreads) {
-        const int r = e % n, c = e / n;
-        X[e] = (c < x0_cols && X0) ? X0[r + static_cast<std::size_t>(c) * n] : rnd_unit(static_cast<unsigned>(c), static_cast<unsigned>(r));
+        const int c = e / n, r = e - c * n;
+        X[e] = (c < x0_cols && X0) ? X0[e] : rnd_unit(static_cast<unsigned>(c), static_cast<unsigned>(r));
     }
     __syncthreads();
-    orthonormalize(X, n, b, coef, red);
+    STAMP(1);
+    if (x0_cols < b || !X0) orthonormalize(X, n, b, S, rinv, coef, red, &flag);  // a kept Ritz block is orthonormal
+    STAMP(2);
 
     int it = 0;
     bool conv = false;
     for (;; ++it) {
         // ---- Rayleigh-Ritz ----
         gemm_gx(G, X, AX, n, b);
-        gram_ab(X, AX, H, n, b, true);
-        if (warp == 0) warp_jacobi(H, W, th, b, it == 0 ? 10 : 4);
-        __syncthreads();
-        rotate(X, W, Y0, n, b);
-        rotate(AX, W, Y0, n, b);
+        STAMP(10);
+        gram_ab(X, AX, H, n, b);
+        STAMP(11);
+        int nsw = 99;
+        if (!quick_rr(H, W, th, b, k, S, &flag)) nsw = cta_jacobi(H, W, th, b, it == 0 ? 10 : 5, red);
+        STAMP(1000 + nsw);
+        rotate2(X, AX, W, Y0, n, b);
+        STAMP(13);
         // ---- residual certificate for the wanted k ----
         double rmax = 0.0;
         for (int c = warp; c < k; c += kWarps) {
@@ -323,6 +511,7 @@ __global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __
         rmax = 0.0;
         for (int i = 0; i < kWarps; ++i) rmax = fmax(rmax, red[i]);
         const double scale = fmax(fabs(th[0]), 1e-300);
+        STAMP(14);
         if (rmax <= tol * scale) { conv = true; break; }
         if (it >= maxit) break;
         __syncthreads();
@@ -335,17 +524,18 @@ __global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __
             for (int q = threadIdx.x; q < n * b; q += kThreads) X[q] = Y0[q];
             __syncthreads();
         } else {
+            const double ie = 1.0 / e;
             // Y0 = X, Y1 = (G X - c X) / e ; Y_{j+1} = 2 (G Y_j - c Y_j)/e - Y_{j-1}
             gemm_gx(G, X, Y1, n, b);
             for (int q = threadIdx.x; q < n * b; q += kThreads) {
                 Y0[q] = X[q];
-                Y1[q] = (Y1[q] - cen * X[q]) / e;
+                Y1[q] = (Y1[q] - cen * X[q]) * ie;
             }
             __syncthreads();
             for (int j = 2; j <= m; ++j) {
                 gemm_gx(G, Y1, AX, n, b);
                 for (int q = threadIdx.x; q < n * b; q += kThreads) {
-                    const double y2 = 2.0 * (AX[q] - cen * Y1[q]) / e - Y0[q];
+                    const double y2 = 2.0 * (AX[q] - cen * Y1[q]) * ie - Y0[q];
                     Y0[q] = Y1[q];
                     Y1[q] = y2;
                 }
@@ -369,8 +559,13 @@ __global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __
             for (int q = threadIdx.x; q < n * b; q += kThreads) X[q] = Y1[q];
             __syncthreads();
         }
-        orthonormalize(X, n, b, coef, red);
+        STAMP(15);
+        orthonormalize(X, n, b, S, rinv, coef, red, &flag);
+        STAMP(16);
     }
+    STAMP(99);
+#undef STAMP
+    if (tstamp && threadIdx.x == 0) tstamp[238] = clock64();
     // ---- outputs ----
     for (int e = threadIdx.x; e < n * k; e += kThreads) V[e] = X[e];
     if (Xkeep)
@@ -380,7 +575,7 @@ __global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __
 }
 
 std::size_t subspace_smem(int n, int b, bool g_smem) {
-    std::size_t w = 2 * kMaxB * kMaxB + 2 * kMaxB + 32 + 4ull * n * b;
+    std::size_t w = 3 * kLd * kMaxB + 3 * kMaxB + 32 + 4ull * n * b;
     if (g_smem) w += static_cast<std::size_t>(n) * n;
     return w * sizeof(double);
 }
@@ -388,8 +583,8 @@ std::size_t subspace_smem(int n, int b, bool g_smem) {
 // Returns true when the subspace path applies (else the caller runs eig_topk).
 bool eig_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
                   double* V, double* sig, int* status) {
-    if (b > kMaxB || b >= n) return false;
-    bool g_smem = subspace_smem(n, b, true) <= 200 * 1024;
+    if (b > kMaxB || b >= n || (b & 3)) return false;
+    const bool g_smem = subspace_smem(n, b, true) <= 200 * 1024;
     const std::size_t smem = subspace_smem(n, b, g_smem);
     if (smem > 220 * 1024) return false;
     static bool attr = false;
@@ -397,24 +592,41 @@ bool eig_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, int
         MB_CUDA(cudaFuncSetAttribute(eig_subspace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         attr = true;
     }
+    static const bool dbg = std::getenv("MACH_DEBUG_EIG_T") != nullptr;
+    DBuf<long long> ts;
+    if (dbg) {
+        ts.alloc(ctx, 240);
+        ts.zero(ctx);
+    }
     MB_LAUNCH(ctx, eig_subspace_kernel, 1, kThreads, smem, G, n, k, b, 4, 40, 1e-12, X0, x0_cols, Xkeep, V, sig, status,
-              g_smem ? 1 : 0);
+              g_smem ? 1 : 0, dbg ? ts.get() : nullptr);
+    if (dbg) {
+        long long h[240];
+        to_host(ctx, h, ts.get(), 240);
+        sync(ctx);
+        std::fprintf(stderr, "[eig-t] n=%d b=%d:", n, b);
+        long long t_end = h[1];
+        for (int i = 1; i < 118 && h[2 * i + 1]; ++i) {
+            std::fprintf(stderr, " %lld:%.1f", h[2 * i], (h[2 * i + 1] - h[2 * i - 1]) * 1e-3);
+            t_end = h[2 * i + 1];
+        }
+        const double us = (t_end - h[1]) * 1e-3;
+        std::fprintf(stderr, " total=%.1fus cycles=%lld clock=%.0fMHz\n", us, h[238] - h[239],
+                     us > 0 ? (h[238] - h[239]) / us : 0.0);
+    }
     return true;
 }
 
-}  // namespace machb
-
-namespace machb {
-
 int eig_block(int n, int k) {
-    const int p = 4;
-    return std::min(n, std::min(kMaxB, k + p));
+    int b = ((k + 4 + 3) / 4) * 4;  // >= k + 4 oversampling, multiple of 4
+    if (b > kMaxB) b = kMaxB;
+    return std::min(n, b);
 }
 
 bool eig_select(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
                 double* V, double* sig, int* status) {
     bool launched = false;
-    if (n > 48 && b < n && b <= kMaxB)
+    if (n > 48 && b < n && b <= kMaxB && k <= b - 2)
         launched = eig_subspace(ctx, G, n, k, X0, x0_cols, Xkeep, b, V, sig, status);
     DBuf<double> work(ctx, eig_work_doubles(n, k));
     eig_topk(ctx, G, n, k, work.get(), V, sig, status, launched ? status : nullptr);

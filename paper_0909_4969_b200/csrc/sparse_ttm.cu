@@ -356,7 +356,7 @@ std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>
     }
     const double avg = rows ? static_cast<double>(nnz) / rows : 0.0;
     int seg = static_cast<int>(std::ceil(avg / 32.0));
-    seg = std::max(1, std::min(31, seg));
+    seg = std::max(1, std::min(15, seg));  // <= 480-nonzero sub-tiles: more warps fit per SM
     if (!(seg & 1)) ++seg;  // odd: conflict-free strided reads of the linear TMA layout
     P->seg = seg;
     const int tile = 32 * seg;
@@ -388,13 +388,13 @@ static void launch_ttm(Ctx* ctx, TtmArgs<T, K> A) {
     const std::size_t budget = 220 * 1024;
     std::size_t fac = ttm::al16(static_cast<std::size_t>(A.ua_elems + A.ub_elems) * sizeof(T));
     int nw;
-    if (fac + 4 * L.total <= budget) {
+    if (fac + 8 * L.total <= budget) {
         A.fac_smem = 1;
-        nw = static_cast<int>(std::min<std::size_t>(8, (budget - fac) / L.total));
+        nw = static_cast<int>(std::min<std::size_t>(16, (budget - fac) / L.total));
     } else {
         A.fac_smem = 0;
         fac = 0;
-        nw = static_cast<int>(std::min<std::size_t>(8, budget / L.total));
+        nw = static_cast<int>(std::min<std::size_t>(16, budget / L.total));
     }
     A.fac_bytes = fac;
     const std::size_t smem = fac + nw * L.total;

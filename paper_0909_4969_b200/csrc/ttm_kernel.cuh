@@ -73,7 +73,7 @@ struct WarpLayout {
 };
 
 template <typename T, typename K, int RA, bool FS>
-__global__ void __launch_bounds__(256) ttm_mode_kernel(TtmArgs<T, K> A) {
+__global__ void __launch_bounds__(512) ttm_mode_kernel(TtmArgs<T, K> A) {
     using V = typename Vec4<T>::type;
     constexpr int VN = Vec4<T>::n;
     constexpr int LB = kFB * RA + 16 / static_cast<int>(sizeof(T));  // padded per-lane queue block
@@ -208,19 +208,41 @@ __global__ void __launch_bounds__(256) ttm_mode_kernel(TtmArgs<T, K> A) {
 
         const int my0 = lane * seg;
         const int cnt = max(0, min(seg, st.len - my0));
+        // software pipeline: the next nonzero's key, value and factor row are
+        // loaded while the current one is accumulated
+        auto load_row = [&](K key, V* dst) {
+            const V* u = reinterpret_cast<const V*>(Ua + static_cast<long long>(key & maska) * RA);
+#pragma unroll
+            for (int a = 0; a < RA / VN; ++a) dst[a] = FS ? u[a] : __ldg(u + a);
+        };
+        K key_n = K(0);
+        T v_n = T(0);
+        V un[RA / VN];
+        if (cnt > 0) {
+            key_n = sk[my0];
+            v_n = sv[my0];
+            load_row(key_n, un);
+        }
         for (int j = 0; j < seg; ++j) {
+            const K key = key_n;
+            const T v = v_n;
+            V u[RA / VN];
+#pragma unroll
+            for (int a = 0; a < RA / VN; ++a) u[a] = un[a];
+            if (j + 1 < cnt) {
+                key_n = sk[my0 + j + 1];
+                v_n = sv[my0 + j + 1];
+                load_row(key_n, un);
+            }
             if (j < cnt) {
-                const K key = sk[my0 + j];
-                const T v = sv[my0 + j];
                 const int ib = static_cast<int>((key >> ba) & maskb);
                 if (ib != cur) {
                     if (cur >= 0) push();
                     cur = ib;
                 }
-                const V* u = reinterpret_cast<const V*>(Ua + static_cast<long long>(key & maska) * RA);
 #pragma unroll
                 for (int a = 0; a < RA; a += VN) {
-                    const V uv = FS ? u[a / VN] : __ldg(u + a / VN);
+                    const V uv = u[a / VN];
                     if constexpr (VN == 4) {
                         acc1[a] = fma(v, uv.x, acc1[a]);
                         acc1[a + 1] = fma(v, uv.y, acc1[a + 1]);
