@@ -5,18 +5,23 @@
 // Why not a full tridiagonal eigensolver per mode: the n sequential Householder
 // steps are latency-bound on a GPU (hundreds of microseconds at n = 100),
 // while HOOI asks for only k << n eigenvectors of a Gram that barely moves
-// between sweeps.  This kernel keeps G in shared memory and runs, in one CTA:
+// between sweeps.  One CTA keeps G and the n x B block in shared memory and
+// runs:
 //   X <- previous sweep's Ritz block (or a deterministic random block)
-//   repeat: Rayleigh-Ritz (H = X^T G X, one-warp cyclic Jacobi on H),
+//   repeat: Rayleigh-Ritz (H = X^T G X; second-order perturbation rotation
+//           when H is nearly diagonal, CTA-parallel cyclic Jacobi otherwise),
 //           residual test |G x_i - theta_i x_i| <= tol * theta_1 for i < k,
-//           degree-m Chebyshev filter damping [0, theta_b], CholQR2
-//           orthonormalisation (CGS2 when Cholesky breaks down)
+//           degree-m Chebyshev filter damping [0, theta_B], CholQR2
 // The residual certificate bounds each Ritz vector's angle to its eigenvector
 // by residual / gap, so converged output equals the reference's exact
-// eigendecomposition to that precision.  When the residual test is not met
-// within max_iters (tiny spectral gaps), status[0] stays 0 and the exact
-// selected-eigenpair solver (eig.cu) runs instead — it checks status and is a
-// no-op otherwise.
+// eigendecomposition to that precision.  Unconverged calls (tiny gaps) leave
+// status[0] = 0 and the exact selected-eigenpair solver (eig.cu) runs next in
+// the stream — it checks status and is a no-op otherwise.
+//
+// Layout: the block size B is a template parameter (multiple of 4, <= 32);
+// n x B blocks are row-major with a padded row stride (B + 2 doubles) so a
+// row is two-to-eight 128-bit loads and different rows hit different banks;
+// B x B matrices use an odd leading dimension (B + 1).
 #include <cstdio>
 #include <cstdlib>
 
@@ -26,14 +31,18 @@ namespace machb {
 
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxB = 32;
-constexpr int kLd = kMaxB + 1;  // odd leading dimension of the b x b smem matrices
 
-__device__ double cta_sum(double v, double* red) {
+__device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ double cta_sum(double v, double* red) {
+    v = warp_sum(v);
     __syncthreads();
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
     __syncthreads();
@@ -43,155 +52,24 @@ __device__ double cta_sum(double v, double* red) {
     return s;
 }
 
+__device__ double cta_max(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) s = fmax(s, red[i]);
+    return s;
+}
+
 __device__ double rnd_unit(unsigned c, unsigned i) {
     unsigned long long z = 0x9E3779B97F4A7C15ULL * (static_cast<unsigned long long>(c) * 0x100000001B3ull + i + 7ull);
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
     z ^= z >> 31;
     return static_cast<double>(z >> 11) * 0x1.0p-53 * 2.0 - 1.0;
-}
-
-// OUT (n x b) = G X; b is a multiple of 4; G n x n column-major; X/OUT ld n
-__device__ void gemm_gx(const double* G, const double* X, double* OUT, int n, int b) {
-    const int ncg = b >> 2;
-    for (int w = threadIdx.x; w < n * ncg; w += kThreads) {
-        const int cg = w / n, i = w - cg * n;
-        const double* x0 = X + static_cast<std::size_t>(cg * 4) * n;
-        double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-#pragma unroll 4
-        for (int l = 0; l < n; ++l) {
-            const double g = G[i + static_cast<std::size_t>(l) * n];
-            a0 = fma(g, x0[l], a0);
-            a1 = fma(g, x0[l + n], a1);
-            a2 = fma(g, x0[l + 2 * n], a2);
-            a3 = fma(g, x0[l + 3 * n], a3);
-        }
-        double* o = OUT + static_cast<std::size_t>(cg * 4) * n + i;
-        o[0] = a0;
-        o[n] = a1;
-        o[2 * n] = a2;
-        o[3 * n] = a3;
-    }
-    __syncthreads();
-}
-
-// C (b x b, ld kMaxB) = A^T B for n x b blocks; warp per entry, fixed order
-__device__ void gram_ab(const double* A, const double* B, double* C, int n, int b) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int e = warp; e < b * b; e += kWarps) {
-        const int j = e / b, i = e - j * b;
-        if (i > j) continue;
-        const double* a = A + static_cast<std::size_t>(i) * n;
-        const double* c = B + static_cast<std::size_t>(j) * n;
-        double s = 0.0;
-        for (int r = lane; r < n; r += 32) s = fma(a[r], c[r], s);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) {
-            C[i + j * kLd] = s;
-            C[j + i * kLd] = s;
-        }
-    }
-    __syncthreads();
-}
-
-// CGS2 column by column (robust fallback)
-__device__ void orth_cgs2(double* X, int n, int b, double* coef, double* red) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int j = 0; j < b; ++j) {
-        double* xj = X + static_cast<std::size_t>(j) * n;
-        for (int attempt = 0; attempt < 2; ++attempt) {
-            double n0 = 0.0;
-            for (int r = threadIdx.x; r < n; r += kThreads) n0 += xj[r] * xj[r];
-            n0 = sqrt(cta_sum(n0, red));
-            for (int pass = 0; pass < 2 && j > 0; ++pass) {
-                for (int c = warp; c < j; c += kWarps) {
-                    const double* xc = X + static_cast<std::size_t>(c) * n;
-                    double s = 0.0;
-                    for (int r = lane; r < n; r += 32) s += xc[r] * xj[r];
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-                    if (lane == 0) coef[c] = s;
-                }
-                __syncthreads();
-                for (int r = threadIdx.x; r < n; r += kThreads) {
-                    double v = xj[r];
-                    for (int c = 0; c < j; ++c) v -= X[r + static_cast<std::size_t>(c) * n] * coef[c];
-                    xj[r] = v;
-                }
-                __syncthreads();
-            }
-            double nn = 0.0;
-            for (int r = threadIdx.x; r < n; r += kThreads) nn += xj[r] * xj[r];
-            nn = sqrt(cta_sum(nn, red));
-            if (nn > 1e-10 * n0 && nn > 0.0) {
-                const double inv = 1.0 / nn;
-                for (int r = threadIdx.x; r < n; r += kThreads) xj[r] *= inv;
-                __syncthreads();
-                break;
-            }
-            for (int r = threadIdx.x; r < n; r += kThreads) xj[r] = rnd_unit(1000u + j + 97u * attempt, r);
-            __syncthreads();
-        }
-    }
-}
-
-// One CholQR pass on X (and the same right-multiplication on Y when given):
-// S = X^T X = R^T R, X <- X R^{-1}.  Returns false when S is not numerically
-// positive definite (the caller then falls back to CGS2).
-__device__ bool cholqr(double* X, double* Y, int n, int b, double* S, double* rinv, int* flag) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    gram_ab(X, X, S, n, b);
-    if (warp == 0) {
-        // Cholesky S = R^T R (upper R stored in S), lane l owns column l
-        bool ok = true;
-        for (int j = 0; j < b; ++j) {
-            double d = 0.0;
-            if (lane == j) {
-                d = S[j + j * kLd];
-                for (int p = 0; p < j; ++p) d -= S[p + j * kLd] * S[p + j * kLd];
-            }
-            d = __shfl_sync(0xffffffffu, d, j);
-            const double orig = S[j + j * kLd];
-            if (!(d > 1e-14 * orig) || !(orig > 0.0)) {
-                ok = false;
-                break;
-            }
-            const double rjj = sqrt(d);
-            const double inv = 1.0 / rjj;
-            __syncwarp();
-            if (lane > j && lane < b) {
-                double v = S[j + lane * kLd];
-                for (int p = 0; p < j; ++p) v -= S[p + j * kLd] * S[p + lane * kLd];
-                S[j + lane * kLd] = v * inv;
-            }
-            if (lane == j) {
-                S[j + j * kLd] = rjj;
-                rinv[j] = inv;
-            }
-            __syncwarp();
-        }
-        if (lane == 0) *flag = ok ? 1 : 0;
-    }
-    __syncthreads();
-    if (!*flag) return false;
-    // row-wise triangular solve z R = x, in place (each thread owns its rows)
-    for (int r = threadIdx.x; r < n; r += kThreads) {
-        for (int pass = 0; pass < (Y ? 2 : 1); ++pass) {
-            double* M = pass ? Y : X;
-            for (int l = 0; l < b; ++l) {
-                double v = M[r + static_cast<std::size_t>(l) * n];
-                for (int p = 0; p < l; ++p) v -= M[r + static_cast<std::size_t>(p) * n] * S[p + l * kLd];
-                M[r + static_cast<std::size_t>(l) * n] = v * rinv[l];
-            }
-        }
-    }
-    __syncthreads();
-    return true;
-}
-
-__device__ void orthonormalize(double* X, int n, int b, double* S, double* rinv, double* coef, double* red, int* flag) {
-    if (!cholqr(X, nullptr, n, b, S, rinv, flag) || !cholqr(X, nullptr, n, b, S, rinv, flag)) orth_cgs2(X, n, b, coef, red);
 }
 
 // Jacobi rotation annihilating H[p][q]: angle in fp32 (fast SFU), the (c, s)
@@ -206,221 +84,459 @@ __device__ void jacobi_cs(double hpp, double hqq, double hpq, double& c, double&
     if (fabsf(tau) > 1e18f) t = 0.5f / tau;
     else t = copysignf(1.0f, tau) / (fabsf(tau) + sqrtf(1.0f + tau * tau));
     const float c32 = rsqrtf(1.0f + t * t);
-    double cc = c32, ss = static_cast<double>(t) * c32;
+    const double cc = c32, ss = static_cast<double>(t) * c32;
     const double delta = cc * cc + ss * ss - 1.0;
     const double sc = 1.0 - 0.5 * delta + 0.375 * delta * delta;
     c = cc * sc;
     s = ss * sc;
 }
 
-// CTA-parallel cyclic Jacobi on H (b x b, ld kLd) -> eigenvectors W, values
-// th (descending, W columns permuted alike).  Each round annihilates np
-// disjoint pairs (circle method); thread (t, j) = (tid >> 5, tid & 31)
-// rotates element j of pair t, so a round is three barrier-separated phases.
-// Rotation angles in fp32 (jacobi_cs), applied rotations orthogonal in fp64.
-__device__ int cta_jacobi(double* H, double* W, double* th, int b, int max_sweeps, double* red) {
-    __shared__ int jp[kMaxB / 2], jq[kMaxB / 2], perm[kMaxB];
-    __shared__ double jc[kMaxB / 2], js[kMaxB / 2];
-    const int tid = threadIdx.x;
-    const int bp = (b + 1) & ~1;
-    const int np = bp / 2;
-    const int M = bp - 1;
-    for (int e = tid; e < kMaxB * kMaxB; e += kThreads) {
-        const int c = e >> 5, r = e & 31;
-        W[r + c * kLd] = (r == c) ? 1.0 : 0.0;
-    }
-    double nrm = 0.0;
-    for (int e = tid; e < b * kMaxB; e += kThreads) {
-        const int c = e >> 5, r = e & 31;
-        if (r < b) nrm += H[r + c * kLd] * H[r + c * kLd];
-    }
-    nrm = cta_sum(nrm, red);
-    const int t = tid >> 5, j = tid & 31;
-    int sweep = 0;
-    for (; sweep < max_sweeps && b > 1; ++sweep) {
-        double off = 0.0;
-        for (int e = tid; e < b * kMaxB; e += kThreads) {
-            const int c = e >> 5, r = e & 31;
-            if (r < c) off += H[r + c * kLd] * H[r + c * kLd];
-        }
-        off = cta_sum(off, red);
-        if (off <= 1e-30 * nrm) break;
-        for (int r = 0; r < M; ++r) {
-            if (tid < np) {
-                int p, q;
-                if (tid == 0) {
-                    p = 0;
-                    q = r + 1;
-                } else {
-                    int x = r + tid;
-                    if (x >= M) x -= M;
-                    int y = r - tid;
-                    if (y < 0) y += M;
-                    p = x + 1;
-                    q = y + 1;
-                }
-                if (p > q) { const int tt = p; p = q; q = tt; }
-                double c = 1.0, s = 0.0;
-                if (q < b) jacobi_cs(H[p + p * kLd], H[q + q * kLd], H[p + q * kLd], c, s);
-                else p = q = 0;
-                jp[tid] = p; jq[tid] = q; jc[tid] = c; js[tid] = s;
-            }
-            __syncthreads();
-            if (t < np && j < b) {  // rows p, q
-                const double s = js[t];
-                if (s != 0.0) {
-                    const double c = jc[t];
-                    const int p = jp[t], q = jq[t];
-                    const double a = H[p + j * kLd], bq = H[q + j * kLd];
-                    H[p + j * kLd] = c * a - s * bq;
-                    H[q + j * kLd] = s * a + c * bq;
-                }
-            }
-            __syncthreads();
-            if (t < np && j < b) {  // columns p, q of H and W
-                const double s = js[t];
-                if (s != 0.0) {
-                    const double c = jc[t];
-                    const int p = jp[t], q = jq[t];
-                    const double a = H[j + p * kLd], bq = H[j + q * kLd];
-                    H[j + p * kLd] = c * a - s * bq;
-                    H[j + q * kLd] = s * a + c * bq;
-                    const double wa = W[j + p * kLd], wb = W[j + q * kLd];
-                    W[j + p * kLd] = c * wa - s * wb;
-                    W[j + q * kLd] = s * wa + c * wb;
-                }
-            }
-            __syncthreads();
-        }
-    }
-    // descending order: rank of each diagonal entry (ties by index)
-    if (tid < b) {
-        const double di = H[tid + tid * kLd];
-        int rank = 0;
-        for (int q = 0; q < b; ++q) {
-            const double dq = H[q + q * kLd];
-            rank += (dq > di) || (dq == di && q < tid);
-        }
-        perm[rank] = tid;
-    }
-    __syncthreads();
-    if (tid < b) th[tid] = H[perm[tid] + perm[tid] * kLd];
-    for (int e = tid; e < b * kMaxB; e += kThreads) {  // permuted W staged in H
-        const int c = e >> 5, r = e & 31;
-        if (r < b) H[r + c * kLd] = W[r + perm[c] * kLd];
-    }
-    __syncthreads();
-    for (int e = tid; e < b * kMaxB; e += kThreads) {
-        const int c = e >> 5, r = e & 31;
-        if (r < b) W[r + c * kLd] = H[r + c * kLd];
-    }
-    __syncthreads();
-    return sweep;
+// D += A B on the fp64 tensor cores (m8n8k4): lane l holds A[l/4][l%4],
+// B[l%4][l/4] and D[l/4][2(l%4) + {0,1}].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
 }
 
-// Quick Rayleigh-Ritz for a nearly diagonal H (warm, converging blocks):
-// second-order perturbation W = I + Z + Z^2/2 with Z_ij = H_ij / (D_j - D_i),
-// i.e. exp(Z) to O(|Z|^3).  Returns false (W untouched) when some pair that
-// involves a wanted index (< k) is not well separated, so the caller runs the
-// full Jacobi instead.  Exactness is enforced by the caller's residual test.
-__device__ bool quick_rr(double* H, double* W, double* th, int b, int k, double* Zs, int* flag) {
-    __shared__ int perm[kMaxB];
-    const int tid = threadIdx.x;
-    if (tid == 0) *flag = 1;
-    __syncthreads();
-    for (int e = tid; e < b * kMaxB; e += kThreads) {
-        const int j = e >> 5, i = e & 31;
-        if (i >= b) continue;
-        double z = 0.0;
-        if (i != j) {
-            const double hij = H[i + j * kLd];
-            const double gap = H[j + j * kLd] - H[i + i * kLd];
-            const bool wanted = i < k || j < k;
-            if (fabs(hij) > 0.02 * fabs(gap)) {
-                if (wanted && hij != 0.0) *flag = 0;
-            } else if (gap != 0.0) {
-                z = hij / gap;
+// padded row stride: XS % 16 == 4 makes every 8x4 / 4x8 fragment load of a
+// half-warp hit 16 distinct 8-byte bank pairs
+__host__ __device__ constexpr int frag_stride(int w) { return w + ((4 - w % 16) + 16) % 16; }
+
+template <int B>
+struct Sub {
+    static_assert(B % 8 == 0 && B <= kMaxB, "block width must be a multiple of 8");
+    static constexpr int XS = frag_stride(B);  // row stride of npad x B row-major blocks (doubles)
+    static constexpr int HS = B + 1;           // leading dimension of B x B matrices
+    static constexpr int CT = B / 8;           // 8-wide column tiles
+
+    // OUT = a (G IN) + b1 P1 + b2 P2 over npad rows (rows >= n stay zero: G's
+    // padding is zero).  Warp per 8-row tile, all column tiles, fp64 MMA.
+    // OUT may alias P1 or P2 (a fragment is read and written by one lane).
+    __device__ static void gemm(const double* G, int ldg, const double* IN, double* OUT, int npad, double a,
+                                const double* P1, double b1, const double* P2, double b2) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int gr = lane >> 2, tq = lane & 3;
+        for (int rt = warp; rt < (npad >> 3); rt += kWarps) {
+            double c[CT][2];
+#pragma unroll
+            for (int t = 0; t < CT; ++t) c[t][0] = c[t][1] = 0.0;
+            const double* ga = G + (rt * 8 + gr) + tq * ldg;
+            const double* xb = IN + tq * XS + gr;
+#pragma unroll 2
+            for (int k0 = 0; k0 < npad; k0 += 4) {
+                const double av = ga[k0 * ldg];
+#pragma unroll
+                for (int t = 0; t < CT; ++t) dmma(c[t][0], c[t][1], av, xb[k0 * XS + t * 8]);
+            }
+            const int off = (rt * 8 + gr) * XS + 2 * tq;
+#pragma unroll
+            for (int t = 0; t < CT; ++t) {
+                double2 v = make_double2(a * c[t][0], a * c[t][1]);
+                if (P1) {
+                    const double2 p = *reinterpret_cast<const double2*>(P1 + off + t * 8);
+                    v.x = fma(b1, p.x, v.x);
+                    v.y = fma(b1, p.y, v.y);
+                }
+                if (P2) {
+                    const double2 p = *reinterpret_cast<const double2*>(P2 + off + t * 8);
+                    v.x = fma(b2, p.x, v.x);
+                    v.y = fma(b2, p.y, v.y);
+                }
+                *reinterpret_cast<double2*>(OUT + off + t * 8) = v;
             }
         }
-        Zs[i + j * kLd] = z;
+        __syncthreads();
     }
-    __syncthreads();
-    if (!*flag) return false;
-    // W = I + Z + Z^2 / 2
-    for (int e = tid; e < b * kMaxB; e += kThreads) {
-        const int j = e >> 5, i = e & 31;
-        if (i >= b) continue;
-        double z2 = 0.0;
-        for (int l = 0; l < b; ++l) z2 = fma(Zs[i + l * kLd], Zs[l + j * kLd], z2);
-        W[i + j * kLd] = (i == j ? 1.0 : 0.0) + Zs[i + j * kLd] + 0.5 * z2;
-    }
-    __syncthreads();
-    // Ritz values th_j = w_j^T H w_j (Zs reused for H W)
-    for (int e = tid; e < b * kMaxB; e += kThreads) {
-        const int j = e >> 5, i = e & 31;
-        if (i >= b) continue;
-        double s = 0.0;
-        for (int l = 0; l < b; ++l) s = fma(H[i + l * kLd], W[l + j * kLd], s);
-        Zs[i + j * kLd] = s;
-    }
-    __syncthreads();
-    if (tid < b) {
-        double s = 0.0;
-        for (int l = 0; l < b; ++l) s = fma(W[l + tid * kLd], Zs[l + tid * kLd], s);
-        H[tid + tid * kLd] = s;  // diagonal now holds the Ritz values
-    }
-    __syncthreads();
-    if (tid < b) {
-        const double di = H[tid + tid * kLd];
-        int rank = 0;
-        for (int q = 0; q < b; ++q) {
-            const double dq = H[q + q * kLd];
-            rank += (dq > di) || (dq == di && q < tid);
-        }
-        perm[rank] = tid;
-    }
-    __syncthreads();
-    if (tid < b) th[tid] = H[perm[tid] + perm[tid] * kLd];
-    for (int e = tid; e < b * kMaxB; e += kThreads) {
-        const int c = e >> 5, r = e & 31;
-        if (r < b) Zs[r + c * kLd] = W[r + perm[c] * kLd];
-    }
-    __syncthreads();
-    for (int e = tid; e < b * kMaxB; e += kThreads) {
-        const int c = e >> 5, r = e & 31;
-        if (r < b) W[r + c * kLd] = Zs[r + c * kLd];
-    }
-    __syncthreads();
-    return true;
-}
 
-// X <- X W and AX <- AX W (n x b) using tmp (n x b)
-__device__ void rotate2(double* X, double* AX, const double* W, double* tmp, int n, int b) {
-    for (int pass = 0; pass < 2; ++pass) {
-        double* M = pass ? AX : X;
-        for (int e = threadIdx.x; e < n * b; e += kThreads) {
-            const int j = e / n, i = e - j * n;
+    // C (B x B, ld HS) = A^T M over npad rows; 8x8 output tiles on the fp64
+    // MMA, the row range split into KG interleaved groups when there are
+    // fewer tiles than warps, partials summed in a fixed order.
+    __device__ static void gram(const double* A, const double* M, double* C, int npad) {
+        constexpr int NT = CT * CT;
+        constexpr int KG = (kWarps / NT) > 0 ? kWarps / NT : 1;
+        constexpr int TW = kWarps / KG;  // warps per k-group
+        __shared__ double part[KG > 1 ? KG * NT * 64 : 1];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int gr = lane >> 2, tq = lane & 3;
+        const int kg = warp % KG;
+        const int KS = npad >> 2;
+        for (int t = warp / KG; t < NT; t += TW) {
+            const int ti = t % CT, tj = t / CT;
+            double c0 = 0.0, c1 = 0.0;
+            const double* ap = A + tq * XS + ti * 8 + gr;
+            const double* mp = M + tq * XS + tj * 8 + gr;
+#pragma unroll 4
+            for (int ks = kg; ks < KS; ks += KG) dmma(c0, c1, ap[ks * 4 * XS], mp[ks * 4 * XS]);
+            if (KG == 1) {
+                C[(ti * 8 + gr) + (tj * 8 + 2 * tq) * HS] = c0;
+                C[(ti * 8 + gr) + (tj * 8 + 2 * tq + 1) * HS] = c1;
+            } else {
+                double* p = part + (kg * NT + t) * 64 + gr * 8 + 2 * tq;
+                p[0] = c0;
+                p[1] = c1;
+            }
+        }
+        if (KG > 1) {
+            __syncthreads();
+            for (int e = threadIdx.x; e < NT * 64; e += kThreads) {
+                double s = 0.0;
+#pragma unroll
+                for (int g = 0; g < KG; ++g) s += part[g * NT * 64 + e];
+                const int t = e >> 6, r = (e >> 3) & 7, cc = e & 7;
+                C[((t % CT) * 8 + r) + ((t / CT) * 8 + cc) * HS] = s;
+            }
+        }
+        __syncthreads();
+    }
+
+    // OUT = X W (npad x B)(B x B); warp per 8-row tile, fp64 MMA
+    __device__ static void rotate(const double* X, const double* W, double* OUT, int npad) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int gr = lane >> 2, tq = lane & 3;
+        for (int rt = warp; rt < (npad >> 3); rt += kWarps) {
+            double c[CT][2];
+#pragma unroll
+            for (int t = 0; t < CT; ++t) c[t][0] = c[t][1] = 0.0;
+            const double* xa = X + (rt * 8 + gr) * XS + tq;
+#pragma unroll
+            for (int k0 = 0; k0 < B; k0 += 4) {
+                const double av = xa[k0];
+#pragma unroll
+                for (int t = 0; t < CT; ++t) dmma(c[t][0], c[t][1], av, W[(k0 + tq) + (t * 8 + gr) * HS]);
+            }
+            const int off = (rt * 8 + gr) * XS + 2 * tq;
+#pragma unroll
+            for (int t = 0; t < CT; ++t) *reinterpret_cast<double2*>(OUT + off + t * 8) = make_double2(c[t][0], c[t][1]);
+        }
+        __syncthreads();
+    }
+
+    // CholQR: X <- X R^{-1} with S = X^T X = R^T R, the product written to T
+    // and the two pointers swapped.  Returns false (X untouched) when S is not
+    // numerically positive definite.  S is equilibrated first (D S D, D =
+    // diag(1/|x_j|)): a Chebyshev-filtered block has columns of wildly
+    // different lengths but nearly orthogonal directions, and only the
+    // latter should decide breakdown.
+    __device__ static bool cholqr(double*& X, double*& T, double* S, double* Ri, double* rinv, int npad, int* flag) {
+        __shared__ double dn[kMaxB];
+        gram(X, X, S, npad);
+        if (threadIdx.x == 0) *flag = 1;
+        if (threadIdx.x < B) {
+            const double s = S[threadIdx.x + threadIdx.x * HS];
+            dn[threadIdx.x] = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < B * B; e += kThreads) {
+            const int l = e % B, m = e / B;
+            if (l <= m) S[l + m * HS] *= dn[l] * dn[m];
+        }
+        __syncthreads();
+        // outer-product Cholesky on the upper triangle, one barrier per step
+        for (int j = 0; j < B; ++j) {
+            const double d = S[j + j * HS];
+            // breakdown: the column keeps < ~3e-8 of its length after the
+            // projections (CholQR2 is then no longer orthonormal to fp64)
+            if (!(d > 1e-15)) {
+                if (threadIdx.x == 0) *flag = 0;
+                continue;  // uniform: every thread read the same d
+            }
+            const double inv = 1.0 / d;
+            const int rem = B - 1 - j;
+            for (int e = threadIdx.x; e < rem * rem; e += kThreads) {
+                const int l = j + 1 + e % rem, m = j + 1 + e / rem;
+                if (l <= m) S[l + m * HS] -= S[j + l * HS] * S[j + m * HS] * inv;
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+        if (!*flag) return false;
+        // R[j][l] = S[j][l] / sqrt(S[j][j])
+        if (threadIdx.x < B) rinv[threadIdx.x] = 1.0 / sqrt(S[threadIdx.x + threadIdx.x * HS]);
+        __syncthreads();
+        for (int e = threadIdx.x; e < B * B; e += kThreads) {
+            const int jj = e % B, l = e / B;
+            if (jj <= l) S[jj + l * HS] *= rinv[jj];
+        }
+        __syncthreads();
+        // Ri = D R^{-1}: thread c back-substitutes R x = e_c in registers
+        if (threadIdx.x < B) {
+            const int c = threadIdx.x;
+            double x[B];
+#pragma unroll
+            for (int r = B - 1; r >= 0; --r) {
+                double v = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+                for (int p = r + 1; p < B; ++p) v = fma(-S[r + p * HS], x[p], v);
+                x[r] = v * rinv[r];
+            }
+#pragma unroll
+            for (int r = 0; r < B; ++r) Ri[r + c * HS] = x[r] * dn[r];
+        }
+        __syncthreads();
+        rotate(X, Ri, T, npad);
+        double* t = X;
+        X = T;
+        T = t;
+        return true;
+    }
+
+    // classical Gram-Schmidt twice, column by column (fallback of cholqr)
+    __device__ static void cgs2(double* X, int n, double* coef, double* red) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        for (int j = 0; j < B; ++j) {
+            for (int attempt = 0; attempt < 2; ++attempt) {
+                double n0 = 0.0;
+                for (int r = threadIdx.x; r < n; r += kThreads) n0 += X[r * XS + j] * X[r * XS + j];
+                n0 = sqrt(cta_sum(n0, red));
+                for (int pass = 0; pass < 2 && j > 0; ++pass) {
+                    for (int c = warp; c < j; c += kWarps) {
+                        double s = 0.0;
+                        for (int r = lane; r < n; r += 32) s += X[r * XS + c] * X[r * XS + j];
+                        s = warp_sum(s);
+                        if (lane == 0) coef[c] = s;
+                    }
+                    __syncthreads();
+                    for (int r = threadIdx.x; r < n; r += kThreads) {
+                        double v = X[r * XS + j];
+                        for (int c = 0; c < j; ++c) v -= X[r * XS + c] * coef[c];
+                        X[r * XS + j] = v;
+                    }
+                    __syncthreads();
+                }
+                double nn = 0.0;
+                for (int r = threadIdx.x; r < n; r += kThreads) nn += X[r * XS + j] * X[r * XS + j];
+                nn = sqrt(cta_sum(nn, red));
+                if (nn > 1e-10 * n0 && nn > 0.0) {
+                    const double inv = 1.0 / nn;
+                    for (int r = threadIdx.x; r < n; r += kThreads) X[r * XS + j] *= inv;
+                    __syncthreads();
+                    break;
+                }
+                for (int r = threadIdx.x; r < n; r += kThreads) X[r * XS + j] = rnd_unit(1000u + j + 97u * attempt, r);
+                __syncthreads();
+            }
+        }
+    }
+
+    __device__ static void orthonormalize(double*& X, double*& T, int n, int npad, double* S, double* Ri, double* rinv,
+                                          double* coef, double* red, int* flag) {
+        if (!cholqr(X, T, S, Ri, rinv, npad, flag) || !cholqr(X, T, S, Ri, rinv, npad, flag)) cgs2(X, n, coef, red);
+    }
+
+    // sort the diagonal of H descending into th, permute W's columns alike
+    __device__ static void sort_ritz(double* H, double* W, double* th, double* Z) {
+        __shared__ int perm[kMaxB];
+        const int tid = threadIdx.x;
+        if (tid < B) {
+            const double di = H[tid + tid * HS];
+            int rank = 0;
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                const double dq = H[q + q * HS];
+                rank += (dq > di) || (dq == di && q < tid);
+            }
+            perm[rank] = tid;
+        }
+        __syncthreads();
+        if (tid < B) th[tid] = H[perm[tid] + perm[tid] * HS];
+        for (int e = tid; e < B * B; e += kThreads) Z[(e % B) + (e / B) * HS] = W[(e % B) + perm[e / B] * HS];
+        __syncthreads();
+        for (int e = tid; e < B * B; e += kThreads) W[(e % B) + (e / B) * HS] = Z[(e % B) + (e / B) * HS];
+        __syncthreads();
+    }
+
+    // C = op(A) M for B x B matrices (ld HS); op = transpose when ta
+    __device__ static void mm(const double* A, bool ta, const double* M, double* C) {
+        for (int e = threadIdx.x; e < B * B; e += kThreads) {
+            const int i = e % B, j = e / B;
             double s = 0.0;
-            for (int l = 0; l < b; ++l) s = fma(M[i + static_cast<std::size_t>(l) * n], W[l + j * kLd], s);
-            tmp[e] = s;
+            if (ta) {
+#pragma unroll
+                for (int l = 0; l < B; ++l) s = fma(A[l + i * HS], M[l + j * HS], s);
+            } else {
+#pragma unroll
+                for (int l = 0; l < B; ++l) s = fma(A[i + l * HS], M[l + j * HS], s);
+            }
+            C[i + j * HS] = s;
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < n * b; e += kThreads) M[e] = tmp[e];
-        __syncthreads();
     }
-}
 
-}  // namespace
+    // Iterated perturbation Rayleigh-Ritz for a nearly diagonal H: each round
+    // takes Z_ij = h_ij / (h_jj - h_ii) (antisymmetric), Q = I + Z + Z^2/2
+    // made orthogonal to fp64 by Newton-Schulz steps Q <- Q (3I - Q^T Q) / 2,
+    // W <- W Q, H <- Q^T H Q; the off-diagonal shrinks quadratically.  Pairs
+    // of unwanted (>= k) columns that are not separated are left coupled (they
+    // only feed the filter bound).  False when a pair involving a wanted
+    // column is not separated or the rounds do not converge: the caller then
+    // runs Jacobi on the untouched H.
+    __device__ static bool refine_rr(const double* H, double* Hc, double* W, double* Z, double* Q, double* T,
+                                     double* th, int k, int* flag) {
+        __shared__ unsigned long long zmax_bits;
+        const int tid = threadIdx.x;
+        for (int e = tid; e < B * B; e += kThreads) {
+            const int i = e % B, j = e / B;
+            Hc[i + j * HS] = H[i + j * HS];
+            W[i + j * HS] = (i == j) ? 1.0 : 0.0;
+        }
+        bool ok = false;
+        for (int round = 0; round < 8; ++round) {
+            if (tid == 0) {
+                *flag = 1;
+                zmax_bits = 0ull;
+            }
+            __syncthreads();
+            for (int e = tid; e < B * B; e += kThreads) {
+                const int i = e % B, j = e / B;
+                double z = 0.0;
+                if (i != j) {
+                    const double hij = Hc[i + j * HS];
+                    const double gap = Hc[j + j * HS] - Hc[i + i * HS];
+                    if (fabs(hij) > 0.25 * fabs(gap)) {
+                        if ((i < k || j < k) && hij != 0.0) *flag = 0;
+                    } else if (gap != 0.0) {
+                        z = hij / gap;
+                    }
+                }
+                Z[i + j * HS] = z;
+                if (z != 0.0) atomicMax(&zmax_bits, static_cast<unsigned long long>(__double_as_longlong(fabs(z))));
+            }
+            __syncthreads();
+            if (!*flag) return false;
+            const double zmax = __longlong_as_double(static_cast<long long>(zmax_bits));
+            if (zmax == 0.0) {
+                ok = true;
+                break;
+            }
+            mm(Z, false, Z, T);  // T = Z^2
+            for (int e = tid; e < B * B; e += kThreads) {
+                const int i = e % B, j = e / B;
+                Q[i + j * HS] = (i == j ? 1.0 : 0.0) + Z[i + j * HS] + 0.5 * T[i + j * HS];
+            }
+            __syncthreads();
+            // orthogonality defect of Q is O(zmax^3); each step squares it
+            const int ns = zmax > 1e-3 ? 2 : (zmax > 1e-6 ? 1 : 0);
+            for (int s = 0; s < ns; ++s) {
+                mm(Q, true, Q, T);  // T = Q^T Q
+                mm(Q, false, T, Z);  // Z = Q (Q^T Q)
+                for (int e = tid; e < B * B; e += kThreads) {
+                    const int i = e % B, j = e / B;
+                    Q[i + j * HS] = 1.5 * Q[i + j * HS] - 0.5 * Z[i + j * HS];
+                }
+                __syncthreads();
+            }
+            mm(W, false, Q, T);  // T = W Q
+            mm(Hc, false, Q, Z);  // Z = Hc Q
+            for (int e = tid; e < B * B; e += kThreads) W[(e % B) + (e / B) * HS] = T[(e % B) + (e / B) * HS];
+            mm(Q, true, Z, Hc);  // Hc = Q^T Hc Q
+            if (zmax < 1e-9) {  // the next round's Z would be O(zmax^2)
+                ok = true;
+                break;
+            }
+        }
+        if (!ok) return false;
+        sort_ritz(Hc, W, th, Z);
+        return true;
+    }
 
-// status: [0] converged, [1] zero matrix, [2] iterations used
-__global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __restrict__ Gin, int n, int k, int b, int m,
+    // CTA-parallel cyclic Jacobi (circle-method rounds, 3 barrier phases each)
+    __device__ static int jacobi(double* H, double* W, double* th, int max_sweeps, double* red, double* Z) {
+        __shared__ int jp[kMaxB / 2], jq[kMaxB / 2];
+        __shared__ double jc[kMaxB / 2], js[kMaxB / 2];
+        const int tid = threadIdx.x;
+        constexpr int NP = B / 2, M = B - 1;
+        for (int e = tid; e < B * B; e += kThreads) W[(e % B) + (e / B) * HS] = ((e % B) == (e / B)) ? 1.0 : 0.0;
+        double nrm = 0.0;
+        for (int e = tid; e < B * B; e += kThreads) nrm += H[(e % B) + (e / B) * HS] * H[(e % B) + (e / B) * HS];
+        nrm = cta_sum(nrm, red);
+        const int t = tid / B, j = tid % B;
+        int sweep = 0;
+        for (; sweep < max_sweeps; ++sweep) {
+            double off = 0.0;
+            for (int e = tid; e < B * B; e += kThreads)
+                if ((e % B) < (e / B)) off += H[(e % B) + (e / B) * HS] * H[(e % B) + (e / B) * HS];
+            off = cta_sum(off, red);
+            if (off <= 1e-30 * nrm) break;
+            for (int r = 0; r < M; ++r) {
+                if (tid < NP) {
+                    int p, q;
+                    if (tid == 0) {
+                        p = 0;
+                        q = r + 1;
+                    } else {
+                        int x = r + tid;
+                        if (x >= M) x -= M;
+                        int y = r - tid;
+                        if (y < 0) y += M;
+                        p = x + 1;
+                        q = y + 1;
+                    }
+                    if (p > q) { const int tt = p; p = q; q = tt; }
+                    double c, s;
+                    jacobi_cs(H[p + p * HS], H[q + q * HS], H[p + q * HS], c, s);
+                    jp[tid] = p; jq[tid] = q; jc[tid] = c; js[tid] = s;
+                }
+                __syncthreads();
+                if (t < NP) {
+                    const double s = js[t];
+                    if (s != 0.0) {
+                        const double c = jc[t];
+                        const int p = jp[t], q = jq[t];
+                        const double a = H[p + j * HS], bq = H[q + j * HS];
+                        H[p + j * HS] = c * a - s * bq;
+                        H[q + j * HS] = s * a + c * bq;
+                    }
+                }
+                __syncthreads();
+                if (t < NP) {
+                    const double s = js[t];
+                    if (s != 0.0) {
+                        const double c = jc[t];
+                        const int p = jp[t], q = jq[t];
+                        const double a = H[j + p * HS], bq = H[j + q * HS];
+                        H[j + p * HS] = c * a - s * bq;
+                        H[j + q * HS] = s * a + c * bq;
+                        const double wa = W[j + p * HS], wb = W[j + q * HS];
+                        W[j + p * HS] = c * wa - s * wb;
+                        W[j + q * HS] = s * wa + c * wb;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        sort_ritz(H, W, th, Z);
+        return sweep;
+    }
+
+    // max over wanted columns c < k of |AX_c - th_c X_c|
+    __device__ static double residual(const double* X, const double* AX, const double* th, int n, int k, double* red) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        double rmax = 0.0;
+        for (int c = warp; c < k; c += kWarps) {
+            double s = 0.0;
+            for (int r = lane; r < n; r += 32) {
+                const double d = AX[r * XS + c] - th[c] * X[r * XS + c];
+                s = fma(d, d, s);
+            }
+            rmax = fmax(rmax, sqrt(warp_sum(s)));
+        }
+        return cta_max(rmax, red);
+    }
+};
+
+// status: [0] converged, [1] zero matrix, [2] iterations used.  Gw: global
+// workspace (npad x ldg doubles) for G when it does not fit shared memory.
+template <int B>
+__global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __restrict__ Gin, int n, int k, int m,
                                                                 int maxit, double tol, const double* X0, int x0_cols,
                                                                 double* Xkeep,  // may alias X0
                                                                 double* __restrict__ V, double* __restrict__ sig,
-                                                                int* __restrict__ status, int g_in_smem,
+                                                                int* __restrict__ status, double* Gw,
                                                                 long long* __restrict__ tstamp) {
-    extern __shared__ double sm[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    using SB = Sub<B>;
+    constexpr int XS = SB::XS, HS = SB::HS;
+    extern __shared__ __align__(16) double sm[];
     int ns_ = 0;
     if (tstamp && threadIdx.x == 0) tstamp[239] = clock64();
 #define STAMP(tag)                                                                     \
@@ -435,190 +551,235 @@ __global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __
     } while (0)
     STAMP(0);
     __shared__ int flag;
-    double* H = sm;                        // kLd * kMaxB
-    double* W = H + kLd * kMaxB;           // kLd * kMaxB
-    double* S = W + kLd * kMaxB;           // kLd * kMaxB
-    double* th = S + kLd * kMaxB;          // kMaxB
-    double* coef = th + kMaxB;             // kMaxB
-    double* rinv = coef + kMaxB;           // kMaxB
-    double* red = rinv + kMaxB;            // 32
-    double* X = red + 32;                  // n*b
-    double* AX = X + static_cast<std::size_t>(n) * b;
-    double* Y0 = AX + static_cast<std::size_t>(n) * b;
-    double* Y1 = Y0 + static_cast<std::size_t>(n) * b;
-    double* G = g_in_smem ? (Y1 + static_cast<std::size_t>(n) * b) : const_cast<double*>(Gin);
+    const int npad = (n + 7) & ~7;
+    const int ldg = frag_stride(npad);
+    double* H = sm;
+    double* W = H + B * HS;
+    double* S = W + B * HS;
+    double* Z = S + B * HS;
+    double* Q = Z + B * HS;
+    double* Hc = Q + B * HS;
+    double* th = Hc + B * HS;
+    double* rinv = th + kMaxB;
+    double* coef = rinv + kMaxB;
+    double* red = coef + kMaxB;
+    const int blk = npad * XS;  // XS even: every block stays 16-byte aligned
+    double* X = red + 32;
+    double* AX = X + blk;
+    double* Y0 = AX + blk;  // also the rotation / CholQR scratch
+    double* Y1 = Y0 + blk;
+    double* G = Gw ? Gw : (Y1 + blk);
 
-    // ---- load + symmetrise G (linalg.cpp:107), zero test ----
-    double fro = 0.0;
-    if (g_in_smem) {
-        for (int c = warp; c < n; c += kWarps)
-            for (int r = lane; r < n; r += 32) {
-                const double a = 0.5 * (Gin[r + static_cast<std::size_t>(c) * n] + Gin[c + static_cast<std::size_t>(r) * n]);
-                G[r + static_cast<std::size_t>(c) * n] = a;
-                fro += a * a;
+    // ---- load G padded to npad x npad (zeros outside n x n), symmetrise
+    // (linalg.cpp:107), zero test ----
+    {
+        constexpr int U = 8;  // eight independent global loads in flight per thread
+        const int nn = n * n;
+        for (int base = threadIdx.x; base < nn; base += U * kThreads) {
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = base + u * kThreads;
+                v[u] = e < nn ? Gin[e] : 0.0;
             }
-    } else {
-        for (int c = warp; c < n; c += kWarps)
-            for (int r = lane; r < n; r += 32) fro += Gin[r + static_cast<std::size_t>(c) * n] * Gin[r + static_cast<std::size_t>(c) * n];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = base + u * kThreads;
+                if (e < nn) G[(e % n) + (e / n) * ldg] = v[u];
+            }
+        }
     }
-    fro = cta_sum(fro, red);
+    for (int e = threadIdx.x; e < npad * npad; e += kThreads) {
+        const int r = e % npad, c = e / npad;
+        if (r >= n || c >= n) G[r + c * ldg] = 0.0;
+    }
+    __syncthreads();
+    double fro = 0.0;
+    for (int e = threadIdx.x; e < n * n; e += kThreads) {
+        const int r = e % n, c = e / n;
+        if (r < c) {
+            const double a = 0.5 * (G[r + c * ldg] + G[c + r * ldg]);
+            fro += 2.0 * a * a;
+        } else if (r == c) {
+            fro += G[r + c * ldg] * G[r + c * ldg];
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += kThreads) {
+        const int r = e % n, c = e / n;
+        if (r < c) {
+            const double a = 0.5 * (G[r + c * ldg] + G[c + r * ldg]);
+            G[r + c * ldg] = a;
+            G[c + r * ldg] = a;
+        }
+    }
+    fro = cta_sum(fro, red);  // its barriers also publish the symmetrised G
     if (fro == 0.0) {
-        for (int c = warp; c < k; c += kWarps)
-            for (int r = lane; r < n; r += 32) V[r + static_cast<std::size_t>(c) * n] = (r == c) ? 1.0 : 0.0;
+        for (int e = threadIdx.x; e < n * k; e += kThreads) V[e] = ((e % n) == (e / n)) ? 1.0 : 0.0;
         if (threadIdx.x < k) sig[threadIdx.x] = 0.0;
         if (threadIdx.x == 0) { status[0] = 1; status[1] = 1; status[2] = 0; }
         return;
     }
 
-    // ---- start block ----
-    for (int e = threadIdx.x; e < n * b; e += kThreads) {
-        const int c = e / n, r = e - c * n;
-        X[e] = (c < x0_cols && X0) ? X0[e] : rnd_unit(static_cast<unsigned>(c), static_cast<unsigned>(r));
+    // ---- start block (row-major, rows >= n zero in all four blocks) ----
+    for (int base = threadIdx.x; base < npad * B; base += 8 * kThreads) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // batched: eight loads in flight
+            const int e = base + u * kThreads;
+            const int r = e % npad, c = e / npad;
+            v[u] = (e < npad * B && r < n && c < x0_cols && X0) ? X0[r + c * n] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = base + u * kThreads;
+            if (e >= npad * B) break;
+            const int r = e % npad, c = e / npad;
+            if (r < n && !(c < x0_cols && X0)) v[u] = rnd_unit(static_cast<unsigned>(c), static_cast<unsigned>(r));
+            X[r * XS + c] = v[u];
+            AX[r * XS + c] = 0.0;
+            Y0[r * XS + c] = 0.0;
+            Y1[r * XS + c] = 0.0;
+        }
     }
     __syncthreads();
     STAMP(1);
-    if (x0_cols < b || !X0) orthonormalize(X, n, b, S, rinv, coef, red, &flag);  // a kept Ritz block is orthonormal
+    if (x0_cols < B || !X0) SB::orthonormalize(X, Y0, n, npad, S, Z, rinv, coef, red, &flag);  // a kept Ritz block is orthonormal
     STAMP(2);
 
     int it = 0;
     bool conv = false;
     for (;; ++it) {
         // ---- Rayleigh-Ritz ----
-        gemm_gx(G, X, AX, n, b);
+        SB::gemm(G, ldg, X, AX, npad, 1.0, nullptr, 0.0, nullptr, 0.0);
         STAMP(10);
-        gram_ab(X, AX, H, n, b);
+        SB::gram(X, AX, H, npad);
         STAMP(11);
         int nsw = 99;
-        if (!quick_rr(H, W, th, b, k, S, &flag)) nsw = cta_jacobi(H, W, th, b, it == 0 ? 10 : 5, red);
+        if (!SB::refine_rr(H, Hc, W, Z, Q, S, th, k, &flag)) nsw = SB::jacobi(H, W, th, it == 0 ? 10 : 5, red, Z);
         STAMP(1000 + nsw);
-        rotate2(X, AX, W, Y0, n, b);
+        SB::rotate(X, W, Y0, npad);
+        { double* t = X; X = Y0; Y0 = t; }
+        SB::rotate(AX, W, Y0, npad);
+        { double* t = AX; AX = Y0; Y0 = t; }
         STAMP(13);
         // ---- residual certificate for the wanted k ----
-        double rmax = 0.0;
-        for (int c = warp; c < k; c += kWarps) {
-            double s = 0.0;
-            for (int r = lane; r < n; r += 32) {
-                const double d = AX[r + static_cast<std::size_t>(c) * n] - th[c] * X[r + static_cast<std::size_t>(c) * n];
-                s += d * d;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            rmax = fmax(rmax, sqrt(s));
-        }
-        __syncthreads();
-        if (lane == 0) red[warp] = rmax;
-        __syncthreads();
-        rmax = 0.0;
-        for (int i = 0; i < kWarps; ++i) rmax = fmax(rmax, red[i]);
+        const double rmax = SB::residual(X, AX, th, n, k, red);
         const double scale = fmax(fabs(th[0]), 1e-300);
         STAMP(14);
         if (rmax <= tol * scale) { conv = true; break; }
         if (it >= maxit) break;
-        __syncthreads();
-        // ---- Chebyshev filter: damp [lo, cut] = [-|theta_1| 1e-12, theta_b] ----
-        const double cut = th[b - 1];
+        // ---- Chebyshev filter: damp [lo, cut] = [-|theta_1| 1e-12, theta_B] ----
+        const double cut = th[B - 1];
         const double lo = -1e-12 * scale;
         const double e = 0.5 * (cut - lo), cen = 0.5 * (cut + lo);
-        if (!(e > 0.0)) {  // degenerate: plain power step
-            gemm_gx(G, X, Y0, n, b);
-            for (int q = threadIdx.x; q < n * b; q += kThreads) X[q] = Y0[q];
-            __syncthreads();
+        if (!(e > 0.0)) {  // degenerate spectrum estimate: plain power step
+            SB::gemm(G, ldg, X, Y1, npad, 1.0, nullptr, 0.0, nullptr, 0.0);
+            { double* t = X; X = Y1; Y1 = t; }
         } else {
             const double ie = 1.0 / e;
-            // Y0 = X, Y1 = (G X - c X) / e ; Y_{j+1} = 2 (G Y_j - c Y_j)/e - Y_{j-1}
-            gemm_gx(G, X, Y1, n, b);
-            for (int q = threadIdx.x; q < n * b; q += kThreads) {
-                Y0[q] = X[q];
-                Y1[q] = (Y1[q] - cen * X[q]) * ie;
-            }
-            __syncthreads();
+            // Y1 = (G X - c X) / e   (Y0 = X by pointer)
+            SB::gemm(G, ldg, X, Y1, npad, ie, X, -cen * ie, nullptr, 0.0);
+            double* y0 = X;
+            double* y1 = Y1;
+            double* spare = Y0;
             for (int j = 2; j <= m; ++j) {
-                gemm_gx(G, Y1, AX, n, b);
-                for (int q = threadIdx.x; q < n * b; q += kThreads) {
-                    const double y2 = 2.0 * (AX[q] - cen * Y1[q]) * ie - Y0[q];
-                    Y0[q] = Y1[q];
-                    Y1[q] = y2;
-                }
-                __syncthreads();
-                // per-column rescale (keeps the recurrence, avoids overflow)
-                for (int c = warp; c < b; c += kWarps) {
-                    double mx = 0.0;
-                    for (int r = lane; r < n; r += 32) mx = fmax(mx, fabs(Y1[r + static_cast<std::size_t>(c) * n]));
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                    if (mx > 1e100) {
-                        const double inv = 1.0 / mx;
-                        for (int r = lane; r < n; r += 32) {
-                            Y1[r + static_cast<std::size_t>(c) * n] *= inv;
-                            Y0[r + static_cast<std::size_t>(c) * n] *= inv;
-                        }
-                    }
-                }
-                __syncthreads();
+                // y2 = 2 (G y1 - c y1) / e - y0, written over the spare block
+                SB::gemm(G, ldg, y1, spare, npad, 2.0 * ie, y1, -2.0 * cen * ie, y0, -1.0);
+                double* t = y0;
+                y0 = y1;
+                y1 = spare;
+                spare = t;
             }
-            for (int q = threadIdx.x; q < n * b; q += kThreads) X[q] = Y1[q];
-            __syncthreads();
+            X = y1;  // growth is ~T_m(theta_1 / e) <= 1e20 at m = 4: no rescale needed in fp64
+            Y0 = y0;
+            Y1 = spare;
         }
         STAMP(15);
-        orthonormalize(X, n, b, S, rinv, coef, red, &flag);
+        SB::orthonormalize(X, Y0, n, npad, S, Z, rinv, coef, red, &flag);
         STAMP(16);
     }
     STAMP(99);
 #undef STAMP
     if (tstamp && threadIdx.x == 0) tstamp[238] = clock64();
-    // ---- outputs ----
-    for (int e = threadIdx.x; e < n * k; e += kThreads) V[e] = X[e];
+    // ---- outputs (column-major) ----
+    for (int e = threadIdx.x; e < n * k; e += kThreads) V[e] = X[(e % n) * XS + e / n];
     if (Xkeep)
-        for (int e = threadIdx.x; e < n * b; e += kThreads) Xkeep[e] = X[e];
+        for (int e = threadIdx.x; e < n * B; e += kThreads) Xkeep[e] = X[(e % n) * XS + e / n];
     if (threadIdx.x < k) sig[threadIdx.x] = sqrt(fmax(0.0, th[threadIdx.x]));
     if (threadIdx.x == 0) { status[0] = conv ? 1 : 0; status[1] = 0; status[2] = it; }
 }
 
-std::size_t subspace_smem(int n, int b, bool g_smem) {
-    std::size_t w = 3 * kLd * kMaxB + 3 * kMaxB + 32 + 4ull * n * b;
-    if (g_smem) w += static_cast<std::size_t>(n) * n;
+std::size_t g_doubles(int n) {
+    const int npad = (n + 7) & ~7;
+    return static_cast<std::size_t>(npad) * frag_stride(npad);
+}
+
+template <int B>
+std::size_t subspace_smem(int n, bool g_smem) {
+    const std::size_t npad = (static_cast<std::size_t>(n) + 7) & ~std::size_t(7);
+    std::size_t w = 6ull * B * Sub<B>::HS + 3 * kMaxB + 32 + 4 * npad * Sub<B>::XS;
+    if (g_smem) w += g_doubles(n);
     return w * sizeof(double);
 }
 
-// Returns true when the subspace path applies (else the caller runs eig_topk).
-bool eig_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
-                  double* V, double* sig, int* status) {
-    if (b > kMaxB || b >= n || (b & 3)) return false;
-    const bool g_smem = subspace_smem(n, b, true) <= 200 * 1024;
-    const std::size_t smem = subspace_smem(n, b, g_smem);
-    if (smem > 220 * 1024) return false;
+constexpr std::size_t kSmemCap = 200 * 1024;
+
+template <int B>
+bool launch_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, double* V,
+                     double* sig, int* status) {
+    const bool g_smem = subspace_smem<B>(n, true) <= kSmemCap;
+    const std::size_t smem = subspace_smem<B>(n, g_smem);
+    if (smem > kSmemCap) return false;
     static bool attr = false;
     if (!attr) {
-        MB_CUDA(cudaFuncSetAttribute(eig_subspace_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        MB_CUDA(cudaFuncSetAttribute(eig_subspace_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kSmemCap)));
         attr = true;
     }
+    DBuf<double> gw;
+    if (!g_smem) gw.alloc(ctx, g_doubles(n));
     static const bool dbg = std::getenv("MACH_DEBUG_EIG_T") != nullptr;
     DBuf<long long> ts;
     if (dbg) {
         ts.alloc(ctx, 240);
         ts.zero(ctx);
     }
-    MB_LAUNCH(ctx, eig_subspace_kernel, 1, kThreads, smem, G, n, k, b, 4, 40, 1e-12, X0, x0_cols, Xkeep, V, sig, status,
-              g_smem ? 1 : 0, dbg ? ts.get() : nullptr);
+    MB_LAUNCH(ctx, eig_subspace_kernel<B>, 1, kThreads, smem, G, n, k, 4, 40, 1e-12, X0, x0_cols, Xkeep, V, sig, status,
+              g_smem ? nullptr : gw.get(), dbg ? ts.get() : nullptr);
     if (dbg) {
         long long h[240];
         to_host(ctx, h, ts.get(), 240);
         sync(ctx);
-        std::fprintf(stderr, "[eig-t] n=%d b=%d:", n, b);
+        std::fprintf(stderr, "[eig-t] n=%d B=%d gsmem=%d:", n, B, g_smem ? 1 : 0);
         long long t_end = h[1];
         for (int i = 1; i < 118 && h[2 * i + 1]; ++i) {
             std::fprintf(stderr, " %lld:%.1f", h[2 * i], (h[2 * i + 1] - h[2 * i - 1]) * 1e-3);
             t_end = h[2 * i + 1];
         }
         const double us = (t_end - h[1]) * 1e-3;
-        std::fprintf(stderr, " total=%.1fus cycles=%lld clock=%.0fMHz\n", us, h[238] - h[239],
-                     us > 0 ? (h[238] - h[239]) / us : 0.0);
+        std::fprintf(stderr, " total=%.1fus cycles=%lld\n", us, h[238] - h[239]);
     }
     return true;
 }
 
+}  // namespace
+
+// Returns true when the subspace path applies (else the caller runs eig_topk).
+bool eig_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
+                  double* V, double* sig, int* status) {
+    if (b >= n || k > b - 2) return false;
+    switch (b) {
+        case 8: return launch_subspace<8>(ctx, G, n, k, X0, x0_cols, Xkeep, V, sig, status);
+        case 16: return launch_subspace<16>(ctx, G, n, k, X0, x0_cols, Xkeep, V, sig, status);
+        case 24: return launch_subspace<24>(ctx, G, n, k, X0, x0_cols, Xkeep, V, sig, status);
+        case 32: return launch_subspace<32>(ctx, G, n, k, X0, x0_cols, Xkeep, V, sig, status);
+        default: return false;
+    }
+}
+
 int eig_block(int n, int k) {
-    int b = ((k + 4 + 3) / 4) * 4;  // >= k + 4 oversampling, multiple of 4
+    int b = ((k + 4 + 7) / 8) * 8;  // >= k + 4 oversampling, multiple of 8 (MMA tiles)
     if (b > kMaxB) b = kMaxB;
     return std::min(n, b);
 }
@@ -626,7 +787,7 @@ int eig_block(int n, int k) {
 bool eig_select(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
                 double* V, double* sig, int* status) {
     bool launched = false;
-    if (n > 48 && b < n && b <= kMaxB && k <= b - 2)
+    if (n > 48 && b < n && b <= kMaxB && (b % 8) == 0 && k <= b - 2)
         launched = eig_subspace(ctx, G, n, k, X0, x0_cols, Xkeep, b, V, sig, status);
     DBuf<double> work(ctx, eig_work_doubles(n, k));
     eig_topk(ctx, G, n, k, work.get(), V, sig, status, launched ? status : nullptr);

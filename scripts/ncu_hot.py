@@ -6,7 +6,7 @@ rows = list(csv.reader(open(sys.argv[1])))
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 h = rows[1]
 ix = {c: i for i, c in enumerate(h)}
-body = [r for r in rows[2:] if len(r) == len(h)]
+body = [r for r in rows[2:] if len(r) == len(h) and r[0] != h[0]]
 tot = sum(float(r[ix["Warp Stall Sampling (All Samples)"]] or 0) for r in body)
 body.sort(key=lambda r: -float(r[ix["Warp Stall Sampling (All Samples)"]] or 0))
 stalls = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
