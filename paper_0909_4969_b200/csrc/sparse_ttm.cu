@@ -25,8 +25,12 @@
 //            (I_n x C, column-major) directly in matricised layout.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "sparse_ttm.cuh"
@@ -81,25 +85,179 @@ __global__ void row_bounds_kernel(const K* __restrict__ keys, long long nnz, int
         re[r] = i + 1;
 }
 
-__global__ void sub_counts_kernel(const long long* __restrict__ rs, const long long* __restrict__ re, int rows, int tile,
-                                  int* __restrict__ cnt) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r > rows) return;
-    cnt[r] = (r < rows) ? static_cast<int>((re[r] - rs[r] + tile - 1) / tile) : 0;
+// ---- TTM task layout -------------------------------------------------------
+// fibre = run of equal key >> ba (row, i_b); each fibre is cut into
+// ceil(len / kSegMax) balanced segments; a row's segments are grouped 32 to a
+// task; inside a task the nonzeros are re-laid in jagged-diagonal order.
+template <typename K>
+__global__ void fibre_flag_kernel(const K* __restrict__ keys, long long nnz, int ba, unsigned char* __restrict__ flag) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= nnz) return;
+    flag[i] = (i == 0 || (static_cast<unsigned long long>(keys[i]) >> ba) != (static_cast<unsigned long long>(keys[i - 1]) >> ba))
+                  ? 1 : 0;
 }
 
-__global__ void sub_fill_kernel(const long long* __restrict__ rs, const long long* __restrict__ re, int rows, int tile,
-                                const int* __restrict__ base, SubTile* __restrict__ subs) {
+__global__ void piece_count_kernel(const long long* __restrict__ fs, long long F, long long nnz, long long* __restrict__ cnt) {
+    const long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (f > F) return;
+    if (f == F) { cnt[f] = 0; return; }
+    const long long len = (f + 1 < F ? fs[f + 1] : nnz) - fs[f];
+    cnt[f] = (len + kSegMax - 1) / kSegMax;
+}
+
+template <typename K>
+__global__ void piece_fill_kernel(const K* __restrict__ keys, const long long* __restrict__ fs, long long F, long long nnz,
+                                  const long long* __restrict__ pbase, int ba, int bb, long long* __restrict__ pstart,
+                                  int* __restrict__ plen, int* __restrict__ prow, int* __restrict__ pib) {
+    const long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (f >= F) return;
+    const long long s = fs[f];
+    const long long len = (f + 1 < F ? fs[f + 1] : nnz) - s;
+    const unsigned long long key = static_cast<unsigned long long>(keys[s]);
+    const int row = static_cast<int>(key >> (ba + bb));
+    const int ib = static_cast<int>((key >> ba) & ((1ull << bb) - 1ull));
+    const long long m = pbase[f + 1] - pbase[f];
+    const long long q = len / m, r = len % m;
+    long long off = s;
+    for (long long k = 0; k < m; ++k) {
+        const long long pl = q + (k < r ? 1 : 0);
+        const long long p = pbase[f] + k;
+        pstart[p] = off;
+        plen[p] = static_cast<int>(pl);
+        prow[p] = row;
+        pib[p] = ib;
+        off += pl;
+    }
+}
+
+__global__ void piece_row_bounds_kernel(const int* __restrict__ prow, long long np, long long* __restrict__ rs,
+                                        long long* __restrict__ re) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p >= np) return;
+    const int r = prow[p];
+    if (p == 0 || prow[p - 1] != r) rs[r] = p;
+    if (p == np - 1 || prow[p + 1] != r) re[r] = p + 1;
+}
+
+__global__ void task_counts_kernel(const long long* __restrict__ rs, const long long* __restrict__ re, int rows,
+                                   int* __restrict__ cnt) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rows) return;
-    const long long len = re[r] - rs[r];
-    const int n = static_cast<int>((len + tile - 1) / tile);
-    for (int s = 0; s < n; ++s) {
-        SubTile st;
-        st.start = rs[r] + static_cast<long long>(s) * tile;
-        st.len = static_cast<int>(min(static_cast<long long>(tile), len - static_cast<long long>(s) * tile));
-        st.row = r;
-        subs[base[r] + s] = st;
+    if (r > rows) return;
+    cnt[r] = (r < rows) ? static_cast<int>((re[r] - rs[r] + 31) / 32) : 0;
+}
+
+__global__ void task_first_kernel(const int* __restrict__ prow, long long np, const long long* __restrict__ rs,
+                                  const long long* __restrict__ re, const int* __restrict__ st_base,
+                                  long long* __restrict__ first, TtmTask* __restrict__ tasks) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p >= np) return;
+    const int r = prow[p];
+    const long long rank = p - rs[r];
+    if (rank % 32) return;
+    const long long t = st_base[r] + rank / 32;
+    first[t] = p;
+    TtmTask tk{};
+    tk.row = r;
+    tk.nseg = static_cast<int>(min(32ll, re[r] - p));
+    tasks[t] = tk;
+}
+
+// One warp per task: sort the segments by length (descending, stable) so the
+// running lanes of every step are a prefix, then write the jagged-diagonal
+// layout.  The order inside each segment is free (a fibre sum), so each step
+// is scheduled to keep the TTM kernel's factor-row gathers bank-conflict free:
+// rows start at 16-byte unit 3*i_a mod 8 (48-byte stride for r <= 12 fp32), a
+// 128-bit shared load is served per group of 8 lanes, and within a group the
+// lanes greedily pick elements whose i_a mod 8 differ.
+template <typename K, typename IA, typename T>
+__global__ void jds_kernel(const K* __restrict__ keys, const T* __restrict__ vals, long long n_task,
+                           const long long* __restrict__ first, const long long* __restrict__ pstart,
+                           const int* __restrict__ plen, const int* __restrict__ pib, unsigned long long maska,
+                           TtmTask* __restrict__ tasks, IA* __restrict__ ia_out, T* __restrict__ v_out,
+                           int2* __restrict__ desc) {
+    const long long t = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= n_task) return;
+    TtmTask tk = tasks[t];
+    const long long p0 = first[t];
+    long long st0 = 0;
+    int len0 = 0, ib0 = 0;
+    if (lane < tk.nseg) {
+        st0 = pstart[p0 + lane];
+        len0 = plen[p0 + lane];
+        ib0 = pib[p0 + lane];
+    }
+    int rank = 0;
+    for (int o = 0; o < 32; ++o) {
+        const int lo = __shfl_sync(0xffffffffu, len0, o);
+        rank += (lo > len0) || (lo == len0 && o < lane);
+    }
+    const long long base = __shfl_sync(0xffffffffu, st0, 0);
+    // lane l takes the segment of rank l
+    long long st = 0;
+    int len = 0, ib = 0;
+    for (int o = 0; o < 32; ++o) {
+        const int ro = __shfl_sync(0xffffffffu, rank, o);
+        const long long so = __shfl_sync(0xffffffffu, st0, o);
+        const int lo = __shfl_sync(0xffffffffu, len0, o);
+        const int bo = __shfl_sync(0xffffffffu, ib0, o);
+        if (ro == lane) { st = so; len = lo; ib = bo; }
+    }
+    int maxlen = len, total = len;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+        total += __shfl_xor_sync(0xffffffffu, total, o);
+    }
+    unsigned cm[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) cm[c] = 0u;
+    for (int e = 0; e < len; ++e) {
+        const unsigned r = static_cast<unsigned>(static_cast<unsigned long long>(keys[st + e]) & maska);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            if ((r & 7u) == static_cast<unsigned>(c)) cm[c] |= 1u << e;
+    }
+    unsigned rem = len >= 32 ? 0xffffffffu : ((1u << len) - 1u);
+    long long ptr = base;
+    const int grp = lane & ~7;
+    unsigned short* joff = reinterpret_cast<unsigned short*>(desc + t * kDesc + 32);
+    joff[lane] = static_cast<unsigned short>(total);  // positions >= maxlen: never read
+    __syncwarp();
+    for (int j = 0; j < maxlen; ++j) {
+        const int aj = __popc(__ballot_sync(0xffffffffu, j < len));
+        if (lane == 0) joff[j] = static_cast<unsigned short>(ptr - base);
+        unsigned taken = 0u;
+        int pick = 0;
+        for (int q = 0; q < 8; ++q) {
+            if ((lane & 7) == q && j < len) {
+                unsigned pref = 0u;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (!((taken >> c) & 1u)) pref |= cm[c];
+                pref &= rem;
+                const unsigned choose = pref ? pref : rem;
+                pick = __ffs(static_cast<int>(choose)) - 1;
+                rem &= ~(1u << pick);
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if ((cm[c] >> pick) & 1u) taken |= 1u << c;
+            }
+            taken = __shfl_sync(0xffffffffu, taken, grp | q);
+        }
+        if (j < len) {
+            const long long dst = ptr + lane;
+            ia_out[dst] = static_cast<IA>(static_cast<unsigned long long>(keys[st + pick]) & maska);
+            v_out[dst] = vals[st + pick];
+        }
+        ptr += aj;
+    }
+    desc[t * kDesc + lane] = make_int2(ib, len);
+    if (lane == 0) {
+        tk.base = base;
+        tk.len = total;
+        tk.maxlen = maxlen;
+        tasks[t] = tk;
     }
 }
 
@@ -272,8 +430,10 @@ void build_sorted(Ctx* ctx, const mach_sparse* X, const KeyFields& kf, int total
 int ra_bucket(int r) {
     if (r <= 4) return 4;
     if (r <= 8) return 8;
+    if (r <= 10) return 10;
     if (r <= 12) return 12;
     if (r <= 16) return 16;
+    if (r <= 20) return 20;
     if (r <= 24) return 24;
     return 32;
 }
@@ -281,6 +441,11 @@ int ra_bucket(int r) {
 }  // namespace
 
 int ttm_ra_bucket(int r) { return ra_bucket(r); }
+int ttm_stride(int r, int elem_bytes) {
+    const int vn = 16 / elem_bytes;
+    const int rs = ((ra_bucket(r) + vn - 1) / vn) * vn;
+    return ((rs / vn) & 1) ? rs : rs + vn;  // odd number of 16-byte units (bank spread)
+}
 
 bool sparse_fast_path_ok(const std::vector<int>& dims, const std::vector<int>& ranks) {
     const int d = static_cast<int>(dims.size());
@@ -310,6 +475,97 @@ static int choose_inner(const mach_sparse* X, int n, const std::vector<int>& ran
         if (best < 0 || cost < best_cost - 1e-9) { best = a; best_cost = cost; }
     }
     return best;
+}
+
+// TTM task layout of a sorted mode plan (see the kernels above).
+template <typename T, typename K>
+void build_ttm_layout_k(Ctx* ctx, long long nnz, ModePlan& P) {
+    const K* keys = reinterpret_cast<const K*>(P.keys.get());
+    const T* vals = reinterpret_cast<const T*>(P.vals.get());
+    const int rows = P.rows;
+    P.ia16 = P.ba <= 16;
+    const std::size_t isz = P.ia16 ? 2 : 4;
+    P.ia.alloc(ctx, static_cast<std::size_t>(nnz) * isz + 32);
+    P.jv.alloc(ctx, static_cast<std::size_t>(nnz) * sizeof(T) + 32);
+    P.st_base.alloc(ctx, rows + 1);
+    if (nnz == 0) {
+        P.st_base.zero(ctx);
+        P.n_task = 0;
+        P.tasks.alloc(ctx, 1);
+        P.desc.alloc(ctx, kDesc);
+        return;
+    }
+    // fibre starts
+    DBuf<unsigned char> flag(ctx, nnz);
+    MB_LAUNCH(ctx, fibre_flag_kernel<K>, ceil_div(nnz, 256), 256, 0, keys, nnz, P.ba, flag.get());
+    DBuf<long long> fs(ctx, nnz);
+    DBuf<long long> nf_d(ctx, 1);
+    {
+        thrust::counting_iterator<long long> cnt_it(0);
+        std::size_t tmp = 0;
+        MB_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, cnt_it, flag.get(), fs.get(), nf_d.get(), nnz, ctx->stream));
+        DBuf<unsigned char> t(ctx, tmp);
+        MB_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, cnt_it, flag.get(), fs.get(), nf_d.get(), nnz, ctx->stream));
+        ctx->launches += 1;
+    }
+    long long F = 0;
+    to_host(ctx, &F, nf_d.get(), 1);
+    sync(ctx);
+    // segments (pieces) of <= kSegMax nonzeros
+    DBuf<long long> pc(ctx, F + 1), pbase(ctx, F + 1);
+    MB_LAUNCH(ctx, piece_count_kernel, ceil_div(F + 1, 256), 256, 0, fs.get(), F, nnz, pc.get());
+    {
+        std::size_t tmp = 0;
+        MB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, pc.get(), pbase.get(), F + 1, ctx->stream));
+        DBuf<unsigned char> t(ctx, tmp);
+        MB_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, pc.get(), pbase.get(), F + 1, ctx->stream));
+        ctx->launches += 1;
+    }
+    long long NP = 0;
+    to_host(ctx, &NP, pbase.get() + F, 1);
+    sync(ctx);
+    DBuf<long long> pstart(ctx, NP);
+    DBuf<int> plen(ctx, NP), prow(ctx, NP), pib(ctx, NP);
+    MB_LAUNCH(ctx, piece_fill_kernel<K>, ceil_div(F, 256), 256, 0, keys, fs.get(), F, nnz, pbase.get(), P.ba, P.bb,
+              pstart.get(), plen.get(), prow.get(), pib.get());
+    // tasks: 32 consecutive segments of one row
+    DBuf<long long> prs(ctx, rows), pre(ctx, rows);
+    prs.zero(ctx);
+    pre.zero(ctx);
+    MB_LAUNCH(ctx, piece_row_bounds_kernel, ceil_div(NP, 256), 256, 0, prow.get(), NP, prs.get(), pre.get());
+    DBuf<int> tc(ctx, rows + 1);
+    MB_LAUNCH(ctx, task_counts_kernel, ceil_div(rows + 1, 256), 256, 0, prs.get(), pre.get(), rows, tc.get());
+    {
+        std::size_t tmp = 0;
+        MB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, tc.get(), P.st_base.get(), rows + 1, ctx->stream));
+        DBuf<unsigned char> t(ctx, tmp);
+        MB_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, tc.get(), P.st_base.get(), rows + 1, ctx->stream));
+        ctx->launches += 1;
+    }
+    int nt = 0;
+    to_host(ctx, &nt, P.st_base.get() + rows, 1);
+    sync(ctx);
+    P.n_task = nt;
+    P.tasks.alloc(ctx, std::max(1, nt));
+    P.desc.alloc(ctx, static_cast<std::size_t>(std::max(1, nt)) * kDesc);
+    DBuf<long long> first(ctx, std::max(1, nt));
+    MB_LAUNCH(ctx, task_first_kernel, ceil_div(NP, 256), 256, 0, prow.get(), NP, prs.get(), pre.get(), P.st_base.get(),
+              first.get(), P.tasks.get());
+    const unsigned long long maska = (1ull << P.ba) - 1ull;
+    if (P.ia16)
+        MB_LAUNCH(ctx, (jds_kernel<K, unsigned short, T>), ceil_div(static_cast<long long>(nt) * 32, 256), 256, 0, keys, vals,
+                  static_cast<long long>(nt), first.get(), pstart.get(), plen.get(), pib.get(), maska, P.tasks.get(),
+                  reinterpret_cast<unsigned short*>(P.ia.get()), reinterpret_cast<T*>(P.jv.get()), P.desc.get());
+    else
+        MB_LAUNCH(ctx, (jds_kernel<K, unsigned int, T>), ceil_div(static_cast<long long>(nt) * 32, 256), 256, 0, keys, vals,
+                  static_cast<long long>(nt), first.get(), pstart.get(), plen.get(), pib.get(), maska, P.tasks.get(),
+                  reinterpret_cast<unsigned int*>(P.ia.get()), reinterpret_cast<T*>(P.jv.get()), P.desc.get());
+}
+
+template <typename T>
+void build_ttm_layout(Ctx* ctx, long long nnz, ModePlan& P) {
+    if (P.key64) build_ttm_layout_k<T, unsigned long long>(ctx, nnz, P);
+    else build_ttm_layout_k<T, unsigned int>(ctx, nnz, P);
 }
 
 template <typename T>
@@ -354,78 +610,90 @@ std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>
                        reinterpret_cast<const unsigned int*>(P->keys.get()), nnz, P->ba + P->bb, P->row_start.get(),
                        P->row_end.get());
     }
-    const double avg = rows ? static_cast<double>(nnz) / rows : 0.0;
-    int seg = static_cast<int>(std::ceil(avg / 32.0));
-    seg = std::max(1, std::min(15, seg));  // <= 480-nonzero sub-tiles: more warps fit per SM
-    if (!(seg & 1)) ++seg;  // odd: conflict-free strided reads of the linear TMA layout
-    P->seg = seg;
-    const int tile = 32 * seg;
-    DBuf<int> cnt(ctx, rows + 1);
-    MB_LAUNCH(ctx, sub_counts_kernel, ceil_div(rows + 1, 256), 256, 0, P->row_start.get(), P->row_end.get(), rows, tile,
-              cnt.get());
-    P->st_base.alloc(ctx, rows + 1);
-    {
-        std::size_t tmp = 0;
-        MB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), P->st_base.get(), rows + 1, ctx->stream));
-        DBuf<unsigned char> t(ctx, tmp);
-        MB_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, cnt.get(), P->st_base.get(), rows + 1, ctx->stream));
-        ctx->launches += 1;
-    }
-    int total_sub = 0;
-    to_host(ctx, &total_sub, P->st_base.get() + rows, 1);
-    sync(ctx);
-    P->n_sub = total_sub;
-    P->subs.alloc(ctx, std::max(1, total_sub));
-    MB_LAUNCH(ctx, sub_fill_kernel, ceil_div(rows, 256), 256, 0, P->row_start.get(), P->row_end.get(), rows, tile,
-              P->st_base.get(), P->subs.get());
+    build_ttm_layout<T>(ctx, nnz, *P);
     slot = P;
     return P;
 }
 
-template <typename T, typename K, int RA>
-static void launch_ttm(Ctx* ctx, TtmArgs<T, K> A) {
-    const ttm::WarpLayout<T, K, RA> L(A.seg);
-    const std::size_t budget = 220 * 1024;
-    std::size_t fac = ttm::al16(static_cast<std::size_t>(A.ua_elems + A.ub_elems) * sizeof(T));
-    int nw;
-    if (fac + 8 * L.total <= budget) {
-        A.fac_smem = 1;
-        nw = static_cast<int>(std::min<std::size_t>(16, (budget - fac) / L.total));
-    } else {
-        A.fac_smem = 0;
-        fac = 0;
-        nw = static_cast<int>(std::min<std::size_t>(16, budget / L.total));
-    }
+template <typename T, typename IA, int RA>
+static void launch_ttm(Ctx* ctx, TtmArgs<T, IA> A) {
+    constexpr int VN = 16 / static_cast<int>(sizeof(T));
+    constexpr int RS = ((RA + VN - 1) / VN) * VN;
+    constexpr int RSS = ((RS / VN) & 1) ? RS : RS + VN;
+    using L = ttm::RingLayout<T, IA, RS>;
+    const std::size_t budget = 227 * 1024;
+    std::size_t fac = ttm::al16(static_cast<std::size_t>(A.ua_rows * RSS + A.ub_elems) * sizeof(T));
+    A.fac_smem = L::bytes(fac, 6, 4) <= budget ? 1 : 0;
+    if (!A.fac_smem) fac = 0;
     A.fac_bytes = fac;
-    const std::size_t smem = fac + nw * L.total;
-    auto kern = A.fac_smem ? ttm::ttm_mode_kernel<T, K, RA, true> : ttm::ttm_mode_kernel<T, K, RA, false>;
+    // consumer warps W and ring slots S: S is a multiple of W (>= 2W) so slot
+    // q is always drained by warp q mod W, which takes its rounds in order and
+    // so never waits on a parity two phases ahead; S <= 32 (one producer lane
+    // per slot).  Defaults favour the most warps that fit.
+    static const int wmax = std::getenv("MACH_TTM_W") ? std::atoi(std::getenv("MACH_TTM_W")) : 16;
+    int W = std::max(1, std::min(16, wmax)), S = 0;
+    for (; W >= 1; --W) {
+        S = (32 / W) * W;
+        while (S >= 2 * W && L::bytes(fac, S, W) > budget) S -= W;
+        if (S >= 2 * W && L::bytes(fac, S, W) <= budget) break;
+    }
+    A.n_cons = W;
+    A.n_slot = S;
+    static const int dbg = std::getenv("MACH_TTM_DBG") ? std::atoi(std::getenv("MACH_TTM_DBG")) : 0;
+    A.dbg = dbg;
+    const std::size_t smem = L::bytes(fac, S, W);
+    auto kern = A.fac_smem ? ttm::ttm_mode_kernel<T, IA, RA, true> : ttm::ttm_mode_kernel<T, IA, RA, false>;
     MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    int per_sm = 1, sms = 148;
-    MB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem));
+    int sms = 148;
     MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
-    const long long want = (A.n_sub + nw - 1) / nw;
-    const long long blocks = std::min<long long>(want, static_cast<long long>(sms) * std::max(1, per_sm));
+    const long long blocks = std::min<long long>(A.n_task, sms);
     if (blocks <= 0) return;
+    static const bool tsdbg = std::getenv("MACH_TTM_TS") != nullptr;
+    DBuf<unsigned long long> tsb;
+    if (tsdbg) {
+        tsb.alloc(ctx, 8 * blocks);
+        tsb.zero(ctx);
+        A.ts = tsb.get();
+    }
     if (A.fac_smem)
-        MB_LAUNCH(ctx, (ttm::ttm_mode_kernel<T, K, RA, true>), static_cast<unsigned>(blocks), nw * 32, smem, A);
+        MB_LAUNCH(ctx, (ttm::ttm_mode_kernel<T, IA, RA, true>), static_cast<unsigned>(blocks), (W + 1) * 32, smem, A);
     else
-        MB_LAUNCH(ctx, (ttm::ttm_mode_kernel<T, K, RA, false>), static_cast<unsigned>(blocks), nw * 32, smem, A);
+        MB_LAUNCH(ctx, (ttm::ttm_mode_kernel<T, IA, RA, false>), static_cast<unsigned>(blocks), (W + 1) * 32, smem, A);
+    if (tsdbg) {
+        std::vector<unsigned long long> h(8 * blocks);
+        to_host(ctx, h.data(), tsb.get(), h.size());
+        sync(ctx);
+        unsigned long long t0 = ~0ull;
+        for (long long b = 0; b < blocks; ++b) t0 = std::min(t0, h[8 * b]);
+        double mean[5] = {0, 0, 0, 0, 0}, mx[5] = {0, 0, 0, 0, 0};
+        for (long long b = 0; b < blocks; ++b)
+            for (int k = 0; k < 5; ++k) {
+                const double v = (h[8 * b + k] - t0) * 1e-3;
+                mean[k] += v / blocks;
+                mx[k] = std::max(mx[k], v);
+            }
+        std::fprintf(stderr, "[ttm-ts] W=%d S=%d tasks=%lld  mean/max us: entry %.1f/%.1f init %.1f/%.1f prod %.1f/%.1f "
+                     "fac %.1f/%.1f cons %.1f/%.1f\n", W, S, A.n_task, mean[0], mx[0], mean[1], mx[1], mean[2], mx[2],
+                     mean[3], mx[3], mean[4], mx[4]);
+    }
 }
 
-template <typename T, typename K>
-static void dispatch_ttm(Ctx* ctx, const TtmArgs<T, K>& A, int rab) {
+template <typename T, typename IA>
+static void dispatch_ttm(Ctx* ctx, const TtmArgs<T, IA>& A, int rab) {
     switch (rab) {
-        case 4: launch_ttm<T, K, 4>(ctx, A); break;
-        case 8: launch_ttm<T, K, 8>(ctx, A); break;
-        case 12: launch_ttm<T, K, 12>(ctx, A); break;
-        case 16: launch_ttm<T, K, 16>(ctx, A); break;
-        case 24: launch_ttm<T, K, 24>(ctx, A); break;
-        default: launch_ttm<T, K, 32>(ctx, A); break;
+        case 4: launch_ttm<T, IA, 4>(ctx, A); break;
+        case 8: launch_ttm<T, IA, 8>(ctx, A); break;
+        case 10: launch_ttm<T, IA, 10>(ctx, A); break;
+        case 12: launch_ttm<T, IA, 12>(ctx, A); break;
+        case 16: launch_ttm<T, IA, 16>(ctx, A); break;
+        case 20: launch_ttm<T, IA, 20>(ctx, A); break;
+        case 24: launch_ttm<T, IA, 24>(ctx, A); break;
+        default: launch_ttm<T, IA, 32>(ctx, A); break;
     }
 }
 
 // Y_(n) (I_n x C, column-major, T) for the current factors.  Ur[m] are the
-// row-major kernel copies (stride ttm_ra_bucket(r_m)).
+// row-major kernel copies (stride ttm_stride(r_m, sizeof(T))).
 template <typename T>
 void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks,
                      const std::vector<const T*>& Ur, const T* one, T* Pbuf, T* Y) {
@@ -438,29 +706,26 @@ void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, 
     else if (a < b) { sa = 1; sb = ra; }
     else { sb = 1; sa = rb; }
     const int rab = ra_bucket(ra);
-    if (P.key64) {
-        TtmArgs<T, unsigned long long> A{};
-        A.keys = reinterpret_cast<const unsigned long long*>(P.keys.get());
-        A.vals = reinterpret_cast<const T*>(P.vals.get());
-        A.subs = P.subs.get(); A.n_sub = P.n_sub; A.seg = P.seg;
-        A.ba = P.ba; A.maska = (1ull << P.ba) - 1ull; A.maskb = (1ull << P.bb) - 1ull;
+    auto fill = [&](auto& A) {
+        A.vals = reinterpret_cast<const T*>(P.jv.get());
+        A.tasks = P.tasks.get();
+        A.desc = P.desc.get();
+        A.n_task = P.n_task;
         A.Ua = Ur[a]; A.ra = ra;
-        A.Ub = (b >= 0) ? Ur[b] : one; A.rb = rb; A.rbs = (b >= 0) ? ra_bucket(rb) : 1;
+        A.Ub = (b >= 0) ? Ur[b] : one; A.rb = rb; A.rbs = (b >= 0) ? ttm_stride(rb, sizeof(T)) : 1;
         A.sa = sa; A.sb = sb; A.C = C; A.P = Pbuf;
-        A.ua_elems = static_cast<long long>(dims[a]) * rab;
-        A.ub_elems = (b >= 0) ? static_cast<long long>(dims[b]) * A.rbs : 1;
+        A.ua_rows = dims[a];
+        A.ub_elems = (b >= 0) ? static_cast<long long>(dims[b]) * A.rbs : 16 / static_cast<long long>(sizeof(T));
+    };
+    if (P.ia16) {
+        TtmArgs<T, unsigned short> A{};
+        A.ia = reinterpret_cast<const unsigned short*>(P.ia.get());
+        fill(A);
         dispatch_ttm(ctx, A, rab);
     } else {
         TtmArgs<T, unsigned int> A{};
-        A.keys = reinterpret_cast<const unsigned int*>(P.keys.get());
-        A.vals = reinterpret_cast<const T*>(P.vals.get());
-        A.subs = P.subs.get(); A.n_sub = P.n_sub; A.seg = P.seg;
-        A.ba = P.ba; A.maska = static_cast<unsigned>((1ull << P.ba) - 1ull); A.maskb = static_cast<unsigned>((1ull << P.bb) - 1ull);
-        A.Ua = Ur[a]; A.ra = ra;
-        A.Ub = (b >= 0) ? Ur[b] : one; A.rb = rb; A.rbs = (b >= 0) ? ra_bucket(rb) : 1;
-        A.sa = sa; A.sb = sb; A.C = C; A.P = Pbuf;
-        A.ua_elems = static_cast<long long>(dims[a]) * rab;
-        A.ub_elems = (b >= 0) ? static_cast<long long>(dims[b]) * A.rbs : 1;
+        A.ia = reinterpret_cast<const unsigned int*>(P.ia.get());
+        fill(A);
         dispatch_ttm(ctx, A, rab);
     }
     const long long tot = static_cast<long long>(dims[n]) * C;

@@ -6,30 +6,41 @@
 
 namespace machb {
 
-struct SubTile {
-    long long start;
+// TTM work unit: <= 32 fibre segments of one output row, <= kSegMax nonzeros
+// each, stored in jagged-diagonal order at [base, base + len).
+constexpr int kSegMax = 32;
+constexpr int kTaskNnz = 32 * kSegMax;
+// task descriptor: 32 int2 {i_b, length} (lengths descending) followed by the
+// 32 u16 jagged-diagonal offsets of positions 0..31 (8 int2)
+constexpr int kDesc = 40;
+
+struct TtmTask {
+    long long base;
     int len;
     int row;
+    int nseg;
+    int maxlen;
 };
 
-template <typename T, typename K>
+template <typename T, typename IA>
 struct TtmArgs {
-    const K* keys;
-    const T* vals;
-    const SubTile* subs;
-    long long n_sub;
-    int seg;
-    int ba;
-    K maska, maskb;
+    const IA* ia;          // inner-mode index per nonzero (task JDS order)
+    const T* vals;         // values, same order
+    const TtmTask* tasks;
+    const int2* desc;      // kDesc int2 per task (see kDesc)
+    long long n_task;
     const T* Ua;
     int ra;
     const T* Ub;
     int rb, rbs;
     int sa, sb, C;
     T* P;
-    long long ua_elems, ub_elems;  // factor elements (row-major, padded strides)
+    long long ua_rows, ub_elems;   // U_a rows; U_b elements (row-major, padded stride)
     std::size_t fac_bytes;         // shared-memory bytes of the staged factors
     int fac_smem;                  // 1: factors staged in shared memory
+    int n_cons, n_slot;            // consumer warps, task slots of the TMA ring
+    int dbg;                       // experiments: 1 = stream only (no arithmetic)
+    unsigned long long* ts;        // experiments: per-CTA %globaltimer stamps (8 per CTA) or null
 };
 
 // Per-mode sorted layout of a sampled tensor (built once, reused by HOSVD and
@@ -39,17 +50,21 @@ struct ModePlan {
     int ba = 0, bb = 0;
     bool key64 = false;
     int rows = 0;
-    int seg = 32;
-    long long n_sub = 0;
-    DBuf<unsigned char> keys, vals;
+    DBuf<unsigned char> keys, vals;  // sorted (key, value) pairs (HOSVD Grams)
     DBuf<long long> row_start, row_end;
-    DBuf<int> st_base;
-    DBuf<SubTile> subs;
+    // TTM layout
+    bool ia16 = false;             // inner index stored as u16
+    long long n_task = 0;
+    DBuf<unsigned char> ia, jv;    // inner index / value per nonzero, task JDS order
+    DBuf<TtmTask> tasks;
+    DBuf<int2> desc;
+    DBuf<int> st_base;             // tasks of row r: [st_base[r], st_base[r+1])
 };
 
 // ---- sparse route ----
 bool sparse_fast_path_ok(const std::vector<int>& dims, const std::vector<int>& ranks);
 int ttm_ra_bucket(int r);
+int ttm_stride(int r, int elem_bytes);  // factor row stride of the TTM kernel copies
 template <typename T>
 std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>& ranks);
 template <typename T>

@@ -1,18 +1,24 @@
 // Fused mode-n TTM kernel (included by sparse_ttm.cu).
 //
-// Persistent warps, one sorted sub-tile (<= 32*seg nonzeros of one output row)
-// at a time.  Each warp double-buffers its sub-tiles in shared memory with 1-D
-// TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx) so the HBM stream
-// is in flight while the previous sub-tile is reduced; lanes then walk `seg`
-// consecutive nonzeros each (seg odd => conflict-free shared-memory reads of
-// the linear TMA layout).  Factor rows (U_a, U_b) are staged once per CTA in
-// shared memory when they fit (FS = true) and read with 128-bit loads.
+// Work unit: a task = up to 32 fibre segments (<= kSegMax nonzeros each) of
+// one output row, stored in jagged-diagonal order — segments sorted by length
+// (descending) and the task's nonzeros interleaved position-major, so at step
+// j the lanes whose segment is still running (lanes 0 .. a_j-1) read
+// consecutive words: ia[ptr + lane], v[ptr + lane].  One lane owns one
+// segment: it accumulates the fibre sum f = sum_j v_j * U_a[ia_j, :] in
+// registers without any cross-lane traffic (the product is one __ffma2_rn per
+// two ranks).  The warp then forms the task's partial row block
+// sum_s f_s (x) U_b[ib_s, :] (lane groups over segments, fixed order) and
+// writes it; a second small kernel sums a row's task partials in task order.
+//
+// Persistent warps double-buffer their tasks in shared memory with 1-D TMA
+// bulk copies (cp.async.bulk ... mbarrier::complete_tx): the next task's
+// nonzeros stream from HBM while the current one is reduced.  Factor rows
+// are staged once per CTA in shared memory when they fit (FS = true).
 #pragma once
 
 namespace machb {
 namespace ttm {
-
-constexpr int kFB = 4;  // fibre queue depth per lane
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -38,243 +44,273 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t pari
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 128-bit shared loads by 32-bit shared address (factor rows are immutable
+// once staged, so these need no ordering against other memory operations)
+__device__ __forceinline__ float4 lds128f(std::uint32_t a) {
+    float4 v;
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double2 lds128d(std::uint32_t a) {
+    double2 v;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
 
 inline std::size_t al16(std::size_t x) { return (x + 15) & ~static_cast<std::size_t>(15); }
 
-template <typename T>
-struct Vec4;
-template <>
-struct Vec4<float> {
-    using type = float4;
-    static constexpr int n = 4;
-};
-template <>
-struct Vec4<double> {
-    using type = double2;
-    static constexpr int n = 2;
-};
-
-// Per-warp shared-memory carve-up (host and device agree on this).
-template <typename T, typename K, int RA>
-struct WarpLayout {
-    int seg;
-    std::size_t kbuf, vbuf, f, eib, ord, total;
-    __host__ __device__ explicit WarpLayout(int s) : seg(s) {
-        kbuf = ((32ull * s * sizeof(K) + 32 + 15) / 16) * 16;  // +32: alignment slack of the bulk copy
-        vbuf = ((32ull * s * sizeof(T) + 32 + 15) / 16) * 16;
-        // per-lane fibre queue blocks padded by 16 B so the lanes' 128-bit push
-        // stores land in different bank groups
-        f = ((32ull * (kFB * RA * sizeof(T) + 16) + 15) / 16) * 16;
-        eib = ((32ull * kFB * sizeof(int) + 15) / 16) * 16;
-        ord = ((32ull * kFB * sizeof(short) + 15) / 16) * 16;
-        total = 16 /*2 mbarriers*/ + 2 * (kbuf + vbuf) + f + eib + ord;
-    }
+// Shared-memory carve-up (host and device agree on this):
+//   [factor rows][S full + S empty mbarriers][S task slots][W fibre-sum tiles]
+template <typename T, typename IA, int RS>
+struct RingLayout {
+    static constexpr std::size_t hdr = 32;  // TtmTask copy + task id
+    static constexpr std::size_t ibuf = ((kTaskNnz * sizeof(IA) + 32 + 15) / 16) * 16;  // +32: alignment slack
+    static constexpr std::size_t vbuf = ((kTaskNnz * sizeof(T) + 32 + 15) / 16) * 16;
+    static constexpr std::size_t dbuf = kDesc * sizeof(int2);
+    static constexpr std::size_t slot = hdr + ibuf + vbuf + dbuf;
+    static constexpr std::size_t fbuf = 32ull * (((RS / (16 / sizeof(T))) & 1) ? RS : RS + 16 / sizeof(T)) * sizeof(T);  // 32 rows, odd-unit stride
+    static std::size_t bytes(std::size_t fac, int S, int W) { return fac + 16ull * S + S * slot + W * fbuf; }
 };
 
-template <typename T, typename K, int RA, bool FS>
-__global__ void __launch_bounds__(512) ttm_mode_kernel(TtmArgs<T, K> A) {
-    using V = typename Vec4<T>::type;
-    constexpr int VN = Vec4<T>::n;
-    constexpr int LB = kFB * RA + 16 / static_cast<int>(sizeof(T));  // padded per-lane queue block
+// Block = W consumer warps + 1 producer warp.  The producer streams the CTA's
+// tasks (t = blockIdx.x + i * gridDim.x, i = 0, 1, ...) into a ring of S
+// slots with TMA bulk copies; consumer warp w takes i = w, w + W, ...
+template <typename T, typename IA, int RA, bool FS>
+__global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
+    constexpr int VN = 16 / static_cast<int>(sizeof(T));  // elements per 128-bit load
+    constexpr int RS = ((RA + VN - 1) / VN) * VN;         // ranks rounded to whole 16-B units
+    constexpr int RSS = ((RS / VN) & 1) ? RS : RS + VN;   // factor row stride: odd number of 16-B units
+    constexpr int FS_ = RSS;                              // fibre-sum row stride (same reason)
+    using L = RingLayout<T, IA, RS>;
     extern __shared__ __align__(128) unsigned char smraw[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int nw = blockDim.x >> 5;
-    const WarpLayout<T, K, RA> L(A.seg);
-
-    // ---- CTA-shared factor rows ----
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int W = A.n_cons, S = A.n_slot;
+    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smraw + A.fac_bytes);
+    std::uint64_t* empty = full + S;
+    unsigned char* slots = smraw + A.fac_bytes + 16ull * S;
     T* ua_s = reinterpret_cast<T*>(smraw);
-    T* ub_s = ua_s + A.ua_elems;
-    if (FS) {
-        const V* ga = reinterpret_cast<const V*>(A.Ua);
-        V* sa = reinterpret_cast<V*>(ua_s);
-        for (long long i = threadIdx.x; i < A.ua_elems / VN; i += blockDim.x) sa[i] = ga[i];
-        for (long long i = threadIdx.x; i < A.ub_elems; i += blockDim.x) ub_s[i] = A.Ub[i];
-    }
-    const T* Ua = FS ? ua_s : A.Ua;
-    const T* Ub = FS ? ub_s : A.Ub;
+    T* ub_s = ua_s + A.ua_rows * RSS;
+    __shared__ __align__(8) std::uint64_t fbar;
+    unsigned long long* ts = A.ts ? A.ts + 8ull * blockIdx.x : nullptr;
+    if (ts && threadIdx.x == 0) ts[0] = gtimer();
 
-    unsigned char* wbase = smraw + A.fac_bytes + L.total * wib;
-    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(wbase);
-    unsigned char* kbuf0 = wbase + 16;
-    unsigned char* vbuf0 = wbase + 16 + 2 * L.kbuf;
-    T* F = reinterpret_cast<T*>(wbase + 16 + 2 * (L.kbuf + L.vbuf));
-    int* EIB = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(F) + L.f);
-    short* ord = reinterpret_cast<short*>(reinterpret_cast<unsigned char*>(EIB) + L.eib);
-    if (lane == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], 1);
+        }
+        if (FS) mbar_init(&fbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if (ts && threadIdx.x == 0) ts[1] = gtimer();
 
-    const long long gw = static_cast<long long>(blockIdx.x) * nw + wib;
-    const long long stride = static_cast<long long>(gridDim.x) * nw;
+    if (warp == W) {
+        // ---------------- producer ----------------
+        if (FS && lane == 0 && A.dbg != 4) {  // factor rows (global rows already use the shared stride RSS)
+            const std::uint32_t ua_bytes = static_cast<std::uint32_t>(A.ua_rows * RSS * sizeof(T));
+            const std::uint32_t ub_bytes = static_cast<std::uint32_t>(A.ub_elems * sizeof(T));
+            fence_proxy_async();
+            mbar_expect_tx(&fbar, ua_bytes + ub_bytes);
+            bulk_g2s(ua_s, A.Ua, ua_bytes, &fbar);
+            bulk_g2s(ub_s, A.Ub, ub_bytes, &fbar);
+        }
+        // lane k < S owns slot k and feeds it tasks i = r * S + k, r = 0, 1, ...
+        // (S <= 32): the slots are refilled in parallel, and each lane's next
+        // task record is loaded while it waits for its slot to drain
+        if (lane < S) {
+            const long long G0 = gridDim.x;
+            long long t = blockIdx.x + static_cast<long long>(lane) * G0;
+            TtmTask tk{};
+            if (t < A.n_task) tk = A.tasks[t];
+            unsigned char* sl = slots + lane * L::slot;
+            for (int r = 0; t < A.n_task; ++r) {
+                const long long tn = t + static_cast<long long>(S) * G0;
+                TtmTask nx{};
+                if (tn < A.n_task) nx = A.tasks[tn];
+                if (r > 0) mbar_wait(&empty[lane], static_cast<std::uint32_t>((r - 1) & 1));
+                *reinterpret_cast<TtmTask*>(sl) = tk;
+                *reinterpret_cast<long long*>(sl + 24) = t;
+                if (A.dbg == 2 || A.dbg == 4) {
+                    mbar_arrive(&full[lane]);
+                } else {
+                    const unsigned char* ig = reinterpret_cast<const unsigned char*>(A.ia) + tk.base * sizeof(IA);
+                    const unsigned char* vg = reinterpret_cast<const unsigned char*>(A.vals) + tk.base * sizeof(T);
+                    const unsigned char* i0 = reinterpret_cast<const unsigned char*>(reinterpret_cast<std::uintptr_t>(ig) & ~std::uintptr_t(15));
+                    const unsigned char* v0 = reinterpret_cast<const unsigned char*>(reinterpret_cast<std::uintptr_t>(vg) & ~std::uintptr_t(15));
+                    const std::uint32_t ib = static_cast<std::uint32_t>(((ig - i0) + tk.len * sizeof(IA) + 15) & ~std::size_t(15));
+                    const std::uint32_t vb = static_cast<std::uint32_t>(((vg - v0) + tk.len * sizeof(T) + 15) & ~std::size_t(15));
+                    // (the empty-barrier wait orders the consumers' reads of this
+                    // slot before the bulk writes; no proxy fence is needed for WAR)
+                    mbar_expect_tx(&full[lane], ib + vb + static_cast<std::uint32_t>(L::dbuf));
+                    bulk_g2s(sl + L::hdr, i0, ib, &full[lane]);
+                    bulk_g2s(sl + L::hdr + L::ibuf, v0, vb, &full[lane]);
+                    bulk_g2s(sl + L::hdr + L::ibuf + L::vbuf, A.desc + t * kDesc, static_cast<std::uint32_t>(L::dbuf), &full[lane]);
+                }
+                tk = nx;
+                t = tn;
+            }
+        }
+        if (ts && lane == 0) ts[2] = gtimer();
+        return;
+    }
 
-    // issue the bulk copies of sub-tile s into buffer b (lane 0 only)
-    auto prefetch = [&](long long s, int b) {
-        const SubTile st = A.subs[s];
-        const unsigned char* kg = reinterpret_cast<const unsigned char*>(A.keys) + st.start * sizeof(K);
-        const unsigned char* vg = reinterpret_cast<const unsigned char*>(A.vals) + st.start * sizeof(T);
-        const unsigned char* k0 = reinterpret_cast<const unsigned char*>(reinterpret_cast<std::uintptr_t>(kg) & ~std::uintptr_t(15));
-        const unsigned char* v0 = reinterpret_cast<const unsigned char*>(reinterpret_cast<std::uintptr_t>(vg) & ~std::uintptr_t(15));
-        const std::uint32_t kbytes = static_cast<std::uint32_t>(((kg - k0) + st.len * sizeof(K) + 15) & ~std::size_t(15));
-        const std::uint32_t vbytes = static_cast<std::uint32_t>(((vg - v0) + st.len * sizeof(T) + 15) & ~std::size_t(15));
-        fence_proxy_async();
-        mbar_expect_tx(&bars[b], kbytes + vbytes);
-        bulk_g2s(kbuf0 + b * L.kbuf, k0, kbytes, &bars[b]);
-        bulk_g2s(vbuf0 + b * L.vbuf, v0, vbytes, &bars[b]);
-    };
+    // ---------------- consumers ----------------
+    if (FS && A.dbg != 4) mbar_wait(&fbar, 0);
+    if (ts && threadIdx.x == 0) ts[3] = gtimer();
+    const T* Ua = FS ? ua_s : A.Ua;
+    const T* Ub = FS ? ub_s : A.Ub;
+    T* F = reinterpret_cast<T*>(slots + S * L::slot + warp * L::fbuf);
 
     const int rb = A.rb;
     const int G = 32 / rb;
     const int g = lane / rb, beta = lane - g * rb;
     const bool gactive = g < G;
-    const int seg = A.seg;
-    const K maska = A.maska, maskb = A.maskb;
-    const int ba = A.ba;
     const int rbs = A.rbs;
 
-    if (gw < A.n_sub && lane == 0) prefetch(gw, 0);
-    SubTile st = (gw < A.n_sub) ? A.subs[gw] : SubTile{0, 0, 0};
-    int it = 0;
-    for (long long s = gw; s < A.n_sub; s += stride, ++it) {
-        const int b = it & 1;
-        SubTile nxt{0, 0, 0};
-        if (s + stride < A.n_sub) {
-            nxt = A.subs[s + stride];
-            if (lane == 0) prefetch(s + stride, b ^ 1);
-        }
-        mbar_wait(&bars[b], static_cast<std::uint32_t>((it >> 1) & 1));
-        const K* sk = reinterpret_cast<const K*>(kbuf0 + b * L.kbuf) + ((st.start * sizeof(K)) & 15) / sizeof(K);
-        const T* sv = reinterpret_cast<const T*>(vbuf0 + b * L.vbuf) + ((st.start * sizeof(T)) & 15) / sizeof(T);
-
-        T acc1[RA];
-        T acc2[RA];
+    // f += v * U_a[ia, :]
+    const std::uint32_t ua_addr = smem_u32(ua_s);
+    auto gather_fma = [&](T (&f)[RS], long long ia, T v) {
+        const T* u = Ua + ia * RSS;
+        const std::uint32_t ua = ua_addr + static_cast<std::uint32_t>(ia) * static_cast<std::uint32_t>(RSS * sizeof(T));
+        if constexpr (sizeof(T) == 4) {
+            const float2 vv = make_float2(v, v);
 #pragma unroll
-        for (int a = 0; a < RA; ++a) { acc1[a] = T(0); acc2[a] = T(0); }
-        int nb = 0;
-        int cur = -1;
-
-        auto push = [&]() {
-            T* f = F + lane * LB + nb * RA;
-#pragma unroll
-            for (int a = 0; a < RA; a += VN) {
-                V v;
-                if constexpr (VN == 4) v = V{acc1[a], acc1[a + 1], acc1[a + 2], acc1[a + 3]};
-                else v = V{acc1[a], acc1[a + 1]};
-                *reinterpret_cast<V*>(f + a) = v;
-            }
-#pragma unroll
-            for (int a = 0; a < RA; ++a) acc1[a] = T(0);
-            EIB[lane * kFB + nb] = cur;
-            ++nb;
-        };
-        auto drain = [&]() {
-            int incl = nb;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const int total = __shfl_sync(0xffffffffu, incl, 31);
-            const int excl = incl - nb;
-            for (int q = 0; q < nb; ++q) ord[excl + q] = static_cast<short>(lane * kFB + q);
-            __syncwarp();
-            for (int e0 = 0; e0 < total; e0 += G) {
-                const int e = e0 + g;
-                if (gactive && e < total) {
-                    const int slot = ord[e];
-                    const T u = Ub[static_cast<long long>(EIB[slot]) * rbs + beta];
-                    const T* f = F + (slot / kFB) * LB + (slot % kFB) * RA;
-#pragma unroll
-                    for (int a = 0; a < RA; a += VN) {
-                        const V fv = *reinterpret_cast<const V*>(f + a);
-                        if constexpr (VN == 4) {
-                            acc2[a] = fma(fv.x, u, acc2[a]);
-                            acc2[a + 1] = fma(fv.y, u, acc2[a + 1]);
-                            acc2[a + 2] = fma(fv.z, u, acc2[a + 2]);
-                            acc2[a + 3] = fma(fv.w, u, acc2[a + 3]);
-                        } else {
-                            acc2[a] = fma(fv.x, u, acc2[a]);
-                            acc2[a + 1] = fma(fv.y, u, acc2[a + 1]);
-                        }
+            for (int a = 0; a < RS; a += 4) {
+                if (a < RA) {  // a partial last unit reads the row padding
+                    const float4 q = FS ? lds128f(ua + a * 4) : __ldg(reinterpret_cast<const float4*>(u + a));
+                    const float2 lo = __ffma2_rn(vv, make_float2(q.x, q.y), make_float2(f[a], f[a + 1]));
+                    f[a] = lo.x; f[a + 1] = lo.y;
+                    if (a + 2 < RA) {
+                        const float2 hi = __ffma2_rn(vv, make_float2(q.z, q.w), make_float2(f[a + 2], f[a + 3]));
+                        f[a + 2] = hi.x; f[a + 3] = hi.y;
                     }
                 }
             }
-            __syncwarp();
-            nb = 0;
-        };
-
-        const int my0 = lane * seg;
-        const int cnt = max(0, min(seg, st.len - my0));
-        // software pipeline: the next nonzero's key, value and factor row are
-        // loaded while the current one is accumulated
-        auto load_row = [&](K key, V* dst) {
-            const V* u = reinterpret_cast<const V*>(Ua + static_cast<long long>(key & maska) * RA);
+        } else {
 #pragma unroll
-            for (int a = 0; a < RA / VN; ++a) dst[a] = FS ? u[a] : __ldg(u + a);
-        };
-        K key_n = K(0);
-        T v_n = T(0);
-        V un[RA / VN];
-        if (cnt > 0) {
-            key_n = sk[my0];
-            v_n = sv[my0];
-            load_row(key_n, un);
-        }
-        for (int j = 0; j < seg; ++j) {
-            const K key = key_n;
-            const T v = v_n;
-            V u[RA / VN];
-#pragma unroll
-            for (int a = 0; a < RA / VN; ++a) u[a] = un[a];
-            if (j + 1 < cnt) {
-                key_n = sk[my0 + j + 1];
-                v_n = sv[my0 + j + 1];
-                load_row(key_n, un);
+            for (int a = 0; a < RA; a += 2) {
+                const double2 q = FS ? lds128d(ua + a * 8) : __ldg(reinterpret_cast<const double2*>(u + a));
+                f[a] = fma(v, q.x, f[a]);
+                f[a + 1] = fma(v, q.y, f[a + 1]);
             }
-            if (j < cnt) {
-                const int ib = static_cast<int>((key >> ba) & maskb);
-                if (ib != cur) {
-                    if (cur >= 0) push();
-                    cur = ib;
-                }
+        }
+    };
+
+    int q = warp;  // slot of task i = i mod S (S a multiple of W: one wrap per step at most)
+    std::uint32_t par = 0u;
+    for (long long i = warp;; i += W) {
+        const long long t0 = blockIdx.x + i * static_cast<long long>(gridDim.x);
+        if (t0 >= A.n_task) break;
+        mbar_wait(&full[q], par);
+        const unsigned char* sl = slots + q * L::slot;
+        const TtmTask tk = *reinterpret_cast<const TtmTask*>(sl);
+        const long long t = *reinterpret_cast<const long long*>(sl + 24);
+        const IA* si = reinterpret_cast<const IA*>(sl + L::hdr) + ((tk.base * sizeof(IA)) & 15) / sizeof(IA);
+        const T* sv = reinterpret_cast<const T*>(sl + L::hdr + L::ibuf) + ((tk.base * sizeof(T)) & 15) / sizeof(T);
+        const int2* sd = reinterpret_cast<const int2*>(sl + L::hdr + L::ibuf + L::vbuf);
+        const int2 my = sd[lane];  // {i_b, length}; length 0 past nseg
+        if (A.dbg >= 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[q]);
+            q += W;
+            if (q >= S) {
+                q -= S;
+                par ^= 1u;
+            }
+            continue;
+        }
+
+        // ---- stage 1: this lane's fibre segment, eight positions per step.
+        // Position offsets come precomputed with the task. ----
+        const unsigned short* joff = reinterpret_cast<const unsigned short*>(sd + 32);
+        T f[RS];
 #pragma unroll
-                for (int a = 0; a < RA; a += VN) {
-                    const V uv = u[a / VN];
-                    if constexpr (VN == 4) {
-                        acc1[a] = fma(v, uv.x, acc1[a]);
-                        acc1[a + 1] = fma(v, uv.y, acc1[a + 1]);
-                        acc1[a + 2] = fma(v, uv.z, acc1[a + 2]);
-                        acc1[a + 3] = fma(v, uv.w, acc1[a + 3]);
+        for (int a = 0; a < RS; ++a) f[a] = T(0);
+        for (int j = 0; j < tk.maxlen; j += 8) {
+            const uint4 o8 = *reinterpret_cast<const uint4*>(joff + j);
+            const unsigned ow[4] = {o8.x, o8.y, o8.z, o8.w};
+            int ix[8];
+            T vx[8];
+            bool act[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int off = static_cast<int>((ow[k >> 1] >> (16 * (k & 1))) & 0xffffu) + lane;
+                act[k] = j + k < my.y;
+                ix[k] = act[k] ? static_cast<int>(si[off]) : 0;
+                vx[k] = act[k] ? sv[off] : T(0);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (act[k]) gather_fma(f, ix[k], vx[k]);
+        }
+
+        // ---- stage 2: sum_s f_s (x) U_b[i_b(s), :] over the task's segments ----
+        {
+            T* fr = F + lane * FS_;
+#pragma unroll
+            for (int a = 0; a < RS; a += VN) {
+                if constexpr (sizeof(T) == 4) *reinterpret_cast<float4*>(fr + a) = make_float4(f[a], f[a + 1], f[a + 2], f[a + 3]);
+                else *reinterpret_cast<double2*>(fr + a) = make_double2(f[a], f[a + 1]);
+            }
+        }
+        __syncwarp();
+        T acc[RS];
+#pragma unroll
+        for (int a = 0; a < RS; ++a) acc[a] = T(0);
+        if (gactive) {
+#pragma unroll 4
+            for (int q = g; q < tk.nseg; q += G) {
+                const T u = Ub[static_cast<long long>(sd[q].x) * rbs + beta];
+                const T* fq = F + q * FS_;
+#pragma unroll
+                for (int a = 0; a < RS; a += VN) {
+                    if constexpr (sizeof(T) == 4) {
+                        const float4 fv = *reinterpret_cast<const float4*>(fq + a);
+                        const float2 uu = make_float2(u, u);
+                        float2 lo = __ffma2_rn(uu, make_float2(fv.x, fv.y), make_float2(acc[a], acc[a + 1]));
+                        float2 hi = __ffma2_rn(uu, make_float2(fv.z, fv.w), make_float2(acc[a + 2], acc[a + 3]));
+                        acc[a] = lo.x; acc[a + 1] = lo.y; acc[a + 2] = hi.x; acc[a + 3] = hi.y;
                     } else {
-                        acc1[a] = fma(v, uv.x, acc1[a]);
-                        acc1[a + 1] = fma(v, uv.y, acc1[a + 1]);
+                        const double2 fv = *reinterpret_cast<const double2*>(fq + a);
+                        acc[a] = fma(fv.x, u, acc[a]);
+                        acc[a + 1] = fma(fv.y, u, acc[a + 1]);
                     }
                 }
             }
-            if (__any_sync(0xffffffffu, nb == kFB)) drain();
         }
-        if (cur >= 0) push();
-        drain();
-
         for (int gg = 1; gg < G; ++gg) {
 #pragma unroll
             for (int a = 0; a < RA; ++a) {
-                const T o = __shfl_sync(0xffffffffu, acc2[a], (lane + gg * rb) & 31);
-                if (g == 0) acc2[a] += o;
+                const T o = __shfl_sync(0xffffffffu, acc[a], (lane + gg * rb) & 31);
+                if (g == 0) acc[a] += o;
             }
         }
         if (g == 0) {
-            T* out = A.P + s * A.C;
+            T* out = A.P + t * A.C;
 #pragma unroll
             for (int a = 0; a < RA; ++a)
-                if (a < A.ra) out[a * A.sa + beta * A.sb] = acc2[a];
+                if (a < A.ra) out[a * A.sa + beta * A.sb] = acc[a];
         }
-        st = nxt;
-        __syncwarp();  // buffer b is refilled two iterations later
+        __syncwarp();  // all lanes are done with the slot and with F
+        if (lane == 0) mbar_arrive(&empty[q]);
+        q += W;
+        if (q >= S) {
+            q -= S;
+            par ^= 1u;
+        }
     }
+    if (ts && lane == 0) atomicMax(&ts[4], gtimer());
 }
 
 }  // namespace ttm

@@ -424,7 +424,7 @@ struct SparseSession : SessionBase {
 
     void refresh(int m) {
         factor_rowmajor<T>(ctx, fs.U[static_cast<std::size_t>(m)].get(), dims[static_cast<std::size_t>(m)],
-                           ranks[static_cast<std::size_t>(m)], ttm_ra_bucket(ranks[static_cast<std::size_t>(m)]),
+                           ranks[static_cast<std::size_t>(m)], ttm_stride(ranks[static_cast<std::size_t>(m)], sizeof(T)),
                            Ur[static_cast<std::size_t>(m)].get());
     }
     void mode_y(int m) {
@@ -471,19 +471,20 @@ struct SparseSession : SessionBase {
         Urp.resize(static_cast<std::size_t>(d));
         for (int m = 0; m < d; ++m) {
             Ur[static_cast<std::size_t>(m)].alloc(ctx, static_cast<std::size_t>(dims[static_cast<std::size_t>(m)]) *
-                                                           ttm_ra_bucket(ranks[static_cast<std::size_t>(m)]));
+                                                           ttm_stride(ranks[static_cast<std::size_t>(m)], sizeof(T)));
             Urp[static_cast<std::size_t>(m)] = Ur[static_cast<std::size_t>(m)].get();
         }
-        one.alloc(ctx, 1);
-        const T h1 = T(1);
-        to_device(ctx, one.get(), &h1, 1);
+        one.alloc(ctx, 16 / sizeof(T));  // one 16-byte unit (bulk-copy granule)
+        const T h1[2] = {T(1), T(0)};
+        one.zero(ctx);
+        to_device(ctx, one.get(), h1, 1);
         long long maxP = 1, maxY = 1;
         C.resize(static_cast<std::size_t>(d));
         for (int m = 0; m < d; ++m) {
             const auto& P = *plans[static_cast<std::size_t>(m)];
             const int c = ranks[static_cast<std::size_t>(P.a)] * (P.b >= 0 ? ranks[static_cast<std::size_t>(P.b)] : 1);
             C[static_cast<std::size_t>(m)] = c;
-            maxP = std::max(maxP, P.n_sub * c);
+            maxP = std::max(maxP, P.n_task * c);
             maxY = std::max(maxY, static_cast<long long>(dims[static_cast<std::size_t>(m)]) * c);
         }
         Pbuf.alloc(ctx, maxP);
