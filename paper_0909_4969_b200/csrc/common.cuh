@@ -87,6 +87,23 @@ struct Ctx {
         }                                                                                            \
     } while (0)
 
+// Same for an extended launch (clusters): cfgp is a cudaLaunchConfig_t*.
+#define MB_LAUNCH_EX(ctx, name, cfgp, kernel, ...)                                                 \
+    do {                                                                                             \
+        ::machb::PendingEvent pe_{name, nullptr, nullptr};                                           \
+        if ((ctx)->profile) {                                                                        \
+            MB_CUDA(cudaEventCreate(&pe_.a));                                                        \
+            MB_CUDA(cudaEventCreate(&pe_.b));                                                        \
+            MB_CUDA(cudaEventRecord(pe_.a, (ctx)->stream));                                          \
+        }                                                                                            \
+        MB_CUDA(cudaLaunchKernelEx((cfgp), kernel, __VA_ARGS__));                                    \
+        ++(ctx)->launches;                                                                           \
+        if ((ctx)->profile) {                                                                        \
+            MB_CUDA(cudaEventRecord(pe_.b, (ctx)->stream));                                          \
+            (ctx)->pending.push_back(pe_);                                                           \
+        }                                                                                            \
+    } while (0)
+
 // Stream-ordered device allocation owned by RAII.
 template <typename T>
 struct DBuf {

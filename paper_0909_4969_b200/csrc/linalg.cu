@@ -7,6 +7,8 @@
 //    collapse floors, completion, sign (linalg.cpp:66-100, :283-296);
 //  - W = Y V, core = U_d^T Y_(d), deterministic sums of squares.
 // All reductions run in a fixed order, so results are bitwise reproducible.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace machb {
@@ -143,8 +145,92 @@ __global__ void __launch_bounds__(256) gram_kernel(const T* __restrict__ a, long
     }
 }
 
+// Small-N Gram on the fp64 tensor cores: one warp per 8x8 tile (ti >= tj) and
+// K-chunk, mma.m8n8k4 with operands straight from global memory (the matrix
+// is L2-resident), eight k-steps of loads in flight.  Off-diagonal tiles are
+// written to both triangles and diagonal tiles from their lower half, so G is
+// exactly symmetric.  With nsplit > 1 the chunks go to `part` and are summed
+// in chunk order.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) gram_mma_kernel(const T* __restrict__ a, long long sk, long long sn, int K, int N,
+                                                       int nts, int kchunk, int nsplit, double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const long long w = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+    const int NT = nts * (nts + 1) / 2;
+    if (w >= static_cast<long long>(NT) * nsplit) return;
+    const int tile = static_cast<int>(w % NT), split = static_cast<int>(w / NT);
+    int ti = static_cast<int>((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
+    while ((ti + 1) * (ti + 2) / 2 <= tile) ++ti;
+    while (ti * (ti + 1) / 2 > tile) --ti;
+    const int tj = tile - ti * (ti + 1) / 2;
+    const int gr = lane >> 2, tq = lane & 3;
+    const int i = ti * 8 + gr, j = tj * 8 + gr;
+    const int k0 = split * kchunk, k1 = min(K, k0 + kchunk);
+    const bool iv = i < N, jv = j < N;
+    const T* pa = a + static_cast<long long>(iv ? i : 0) * sn;
+    const T* pb = a + static_cast<long long>(jv ? j : 0) * sn;
+    double c0 = 0.0, c1 = 0.0;
+    for (int kb = k0; kb < k1; kb += 32) {
+        double av[8], bv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int kk = kb + 4 * u + tq;
+            const bool kv = kk < k1;
+            av[u] = (kv && iv) ? static_cast<double>(pa[kk * sk]) : 0.0;
+            bv[u] = (kv && jv) ? static_cast<double>(pb[kk * sk]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dmma884(c0, c1, av[u], bv[u]);
+    }
+    double* G = out + static_cast<std::size_t>(split) * N * N;
+    const int r = ti * 8 + gr;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int c = tj * 8 + 2 * tq + e;
+        const double v = e ? c1 : c0;
+        if (r < N && c < N && (ti != tj || r >= c)) {
+            G[r + static_cast<std::size_t>(c) * N] = v;
+            G[c + static_cast<std::size_t>(r) * N] = v;
+        }
+    }
+}
+
+__global__ void sum_parts_kernel(const double* __restrict__ part, int nsplit, long long n, double* __restrict__ G) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= n) return;
+    double s = 0.0;
+    for (int q = 0; q < nsplit; ++q) s += part[q * n + e];
+    G[e] = s;
+}
+
 template <typename T>
 void gram(Ctx* ctx, const T* a, long long sk, long long sn, int K, int N, double* G) {
+    if (N <= 256 && K <= (1 << 20)) {
+        const int nts = (N + 7) / 8;
+        const int NT = nts * (nts + 1) / 2;
+        const int kchunk_min = 1024;
+        int nsplit = std::max(1, std::min(K / kchunk_min, 2368 / NT));
+        nsplit = std::min(nsplit, 64);
+        const int kchunk = ((ceil_div(K, nsplit) + 31) / 32) * 32;
+        nsplit = ceil_div(K, kchunk);
+        const long long warps = static_cast<long long>(NT) * nsplit;
+        if (nsplit == 1) {
+            MB_LAUNCH(ctx, gram_mma_kernel<T>, ceil_div(warps * 32, 256), 256, 0, a, sk, sn, K, N, nts, kchunk, 1, G);
+        } else {
+            DBuf<double> part(ctx, static_cast<std::size_t>(nsplit) * N * N);
+            MB_LAUNCH(ctx, gram_mma_kernel<T>, ceil_div(warps * 32, 256), 256, 0, a, sk, sn, K, N, nts, kchunk, nsplit,
+                      part.get());
+            const long long n2 = static_cast<long long>(N) * N;
+            MB_LAUNCH(ctx, sum_parts_kernel, ceil_div(n2, 256), 256, 0, part.get(), nsplit, n2, G);
+        }
+        return;
+    }
     dim3 grid(ceil_div(N, 32), ceil_div(N, 32));
     MB_LAUNCH(ctx, gram_kernel<T>, grid, 256, 0, a, sk, sn, K, N, G);
 }
@@ -154,9 +240,36 @@ template void gram<double>(Ctx*, const double*, long long, long long, int, int, 
 // ---------------------------------------------------------------------------
 // W (rows x kc, fp64) = Y (rows x C, col-major, T) * V (C x kc, fp64)
 // ---------------------------------------------------------------------------
+template <typename T, int KC>
+__global__ void __launch_bounds__(128) matmul_yv_kernel(const T* __restrict__ Y, int rows, int C, const double* __restrict__ V,
+                                                        int kc, double* __restrict__ W, const int* __restrict__ need) {
+    if (need && need[0] == 0) return;
+    // thread per row of W; V staged in shared memory (broadcast reads); the
+    // column loop streams Y column by column (coalesced across the rows)
+    extern __shared__ double vs[];
+    for (int e = threadIdx.x; e < C * kc; e += blockDim.x) vs[e] = V[e];
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    double acc[KC];
+#pragma unroll
+    for (int j = 0; j < KC; ++j) acc[j] = 0.0;
+#pragma unroll 4
+    for (int c = 0; c < C; ++c) {
+        const double y = static_cast<double>(Y[i + static_cast<std::size_t>(c) * rows]);
+#pragma unroll
+        for (int j = 0; j < KC; ++j)
+            if (j < kc) acc[j] = fma(y, vs[c + j * C], acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < KC; ++j)
+        if (j < kc) W[i + static_cast<std::size_t>(j) * rows] = acc[j];
+}
+
 template <typename T>
-__global__ void matmul_yv_kernel(const T* __restrict__ Y, int rows, int C, const double* __restrict__ V, int kc,
-                                 double* __restrict__ W) {
+__global__ void matmul_yv_generic_kernel(const T* __restrict__ Y, int rows, int C, const double* __restrict__ V, int kc,
+                                         double* __restrict__ W, const int* __restrict__ need) {
+    if (need && need[0] == 0) return;
     const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (idx >= static_cast<long long>(rows) * kc) return;
     const int i = static_cast<int>(idx % rows), c2 = static_cast<int>(idx / rows);
@@ -166,11 +279,26 @@ __global__ void matmul_yv_kernel(const T* __restrict__ Y, int rows, int C, const
 }
 
 template <typename T>
-void matmul_yv(Ctx* ctx, const T* Y, int rows, int C, const double* V, int kc, double* W) {
+void matmul_yv_gated(Ctx* ctx, const T* Y, int rows, int C, const double* V, int kc, double* W, const int* need) {
     const long long n = static_cast<long long>(rows) * kc;
     if (n == 0) return;
-    MB_LAUNCH(ctx, matmul_yv_kernel<T>, ceil_div(n, 256), 256, 0, Y, rows, C, V, kc, W);
+    const std::size_t vsm = static_cast<std::size_t>(C) * kc * sizeof(double);
+    if (kc <= 32 && vsm <= 48 * 1024) {
+        if (kc <= 16)
+            MB_LAUNCH(ctx, (matmul_yv_kernel<T, 16>), ceil_div(rows, 128), 128, vsm, Y, rows, C, V, kc, W, need);
+        else
+            MB_LAUNCH(ctx, (matmul_yv_kernel<T, 32>), ceil_div(rows, 128), 128, vsm, Y, rows, C, V, kc, W, need);
+        return;
+    }
+    MB_LAUNCH(ctx, matmul_yv_generic_kernel<T>, ceil_div(n, 256), 256, 0, Y, rows, C, V, kc, W, need);
 }
+
+template <typename T>
+void matmul_yv(Ctx* ctx, const T* Y, int rows, int C, const double* V, int kc, double* W) {
+    matmul_yv_gated<T>(ctx, Y, rows, C, V, kc, W, nullptr);
+}
+template void matmul_yv_gated<float>(Ctx*, const float*, int, int, const double*, int, double*, const int*);
+template void matmul_yv_gated<double>(Ctx*, const double*, int, int, const double*, int, double*, const int*);
 template void matmul_yv<float>(Ctx*, const float*, int, int, const double*, int, double*);
 template void matmul_yv<double>(Ctx*, const double*, int, int, const double*, int, double*);
 
@@ -215,7 +343,8 @@ __global__ void __launch_bounds__(kB) basis_from_products_kernel(const double* _
                                                                  const double* __restrict__ sig,
                                                                  const int* __restrict__ eig_status,
                                                                  double* __restrict__ U, double* __restrict__ sv,
-                                                                 int* __restrict__ st) {
+                                                                 int* __restrict__ st, const int* __restrict__ skip) {
+    if (skip && skip[0] == 0) return;  // the CholQR2 fast path already produced U
     extern __shared__ double sm[];
     double* v = sm;
     double* tcoef = v + n;
@@ -266,9 +395,153 @@ void basis_from_side(Ctx* ctx, const double* V, const double* sig, int n, int k,
     MB_LAUNCH(ctx, basis_from_side_kernel, 1, kB, basis_smem(n, k), V, sig, n, k, eig_status, U, sv, st);
 }
 
+// ---------------------------------------------------------------------------
+// basis_from_products fast path.  W = Y V has (numerically) orthogonal columns
+// of lengths sigma_i, so the reference's twice Gram-Schmidt (linalg.cpp:66-100)
+// equals CholQR2 here: C = W^T W = R^T R gives every column's length
+// (sqrt C_ii) and its residual after projecting out the earlier columns
+// (R_ii), i.e. the same rank and collapse tests, and U = W R^{-1} (twice).
+// When a column fails a test (rank deficiency / completion needed) the flag
+// stays 1 and the full Gram-Schmidt kernel runs next in the stream.
+// ---------------------------------------------------------------------------
+constexpr int kFastK = 32;
+
+__device__ void small_gram(const double* X, int n, int k, double* C, double* red) {
+    // C (k x k, ld kFastK) = X^T X over n rows; one warp per (i <= j) pair
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int p = warp; p < k * (k + 1) / 2; p += kW) {
+        int i = 0;
+        while ((i + 1) * (i + 2) / 2 <= p) ++i;
+        const int j = p - i * (i + 1) / 2;
+        const double* a = X + static_cast<std::size_t>(i) * n;
+        const double* b = X + static_cast<std::size_t>(j) * n;
+        double s = 0.0;
+        for (int r = lane; r < n; r += 32) s = fma(a[r], b[r], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            C[i + j * kFastK] = s;
+            C[j + i * kFastK] = s;
+        }
+    }
+    __syncthreads();
+    (void)red;
+}
+
+// upper Cholesky factor of C in place (thread 0), then Ri = R^{-1} (thread c
+// solves column c).  Returns false on a non-positive pivot.
+__device__ bool small_chol_inv(double* C, double* Ri, int k, double* diag, int* ok) {
+    if (threadIdx.x == 0) {
+        int good = 1;
+        for (int j = 0; j < k && good; ++j) {
+            double d = C[j + j * kFastK];
+            for (int p = 0; p < j; ++p) d -= C[p + j * kFastK] * C[p + j * kFastK];
+            if (!(d > 0.0)) { good = 0; break; }
+            const double rjj = sqrt(d);
+            C[j + j * kFastK] = rjj;
+            diag[j] = rjj;
+            for (int l = j + 1; l < k; ++l) {
+                double v = C[j + l * kFastK];
+                for (int p = 0; p < j; ++p) v -= C[p + j * kFastK] * C[p + l * kFastK];
+                C[j + l * kFastK] = v / rjj;
+            }
+        }
+        *ok = good;
+    }
+    __syncthreads();
+    if (!*ok) return false;
+    if (threadIdx.x < k) {
+        const int c = threadIdx.x;
+        for (int r = k - 1; r >= 0; --r) {
+            double v = (r == c) ? 1.0 : 0.0;
+            for (int p = r + 1; p < k; ++p) v -= C[r + p * kFastK] * Ri[p + c * kFastK];
+            Ri[r + c * kFastK] = (r <= c) ? v / C[r + r * kFastK] : 0.0;
+        }
+    }
+    __syncthreads();
+    return true;
+}
+
+// Y (n x k) = X Ri, column-major, X and Y distinct
+__device__ void small_apply(const double* X, const double* Ri, double* Y, int n, int k) {
+    for (long long e = threadIdx.x; e < static_cast<long long>(n) * k; e += kB) {
+        const int r = static_cast<int>(e % n), c = static_cast<int>(e / n);
+        double s = 0.0;
+        for (int p = 0; p <= c; ++p) s = fma(X[r + static_cast<std::size_t>(p) * n], Ri[p + c * kFastK], s);
+        Y[e] = s;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kB) basis_products_fast_kernel(const double* __restrict__ W, int n, int k,
+                                                                 const double* __restrict__ sig,
+                                                                 double* __restrict__ U, double* __restrict__ sv,
+                                                                 int* __restrict__ st, int* __restrict__ slow) {
+    extern __shared__ double sm[];
+    double* X = sm;                                   // n x k
+    double* Y = X + static_cast<std::size_t>(n) * k;  // n x k
+    __shared__ double C[kFastK * kFastK], Ri[kFastK * kFastK], diag[kFastK], red[32];
+    __shared__ int ok, redi[32];
+    for (long long e = threadIdx.x; e < static_cast<long long>(n) * k; e += kB) X[e] = W[e];
+    __syncthreads();
+    small_gram(X, n, k, C, red);
+    // rank test on every column (nv_i > sigma1 * floor) before factorising
+    const double floor = sig[0] * kRankFloor;
+    double nv[kFastK];
+    bool pass = true;
+    for (int i = 0; i < k; ++i) {
+        nv[i] = sqrt(C[i + i * kFastK]);
+        pass = pass && nv[i] > floor;
+    }
+    if (!pass || !small_chol_inv(C, Ri, k, diag, &ok)) {
+        if (threadIdx.x == 0) *slow = 1;
+        return;
+    }
+    for (int i = 0; i < k; ++i)
+        if (!(diag[i] > kCollapseFloor * nv[i])) {
+            if (threadIdx.x == 0) *slow = 1;
+            return;
+        }
+    small_apply(X, Ri, Y, n, k);
+    small_gram(Y, n, k, C, red);
+    if (!small_chol_inv(C, Ri, k, diag, &ok)) {
+        if (threadIdx.x == 0) *slow = 1;
+        return;
+    }
+    small_apply(Y, Ri, X, n, k);
+    for (int i = 0; i < k; ++i) cta_canonical_sign(X + static_cast<std::size_t>(i) * n, n, red, redi);
+    for (long long e = threadIdx.x; e < static_cast<long long>(n) * k; e += kB) U[e] = X[e];
+    if (threadIdx.x < k) sv[threadIdx.x] = sig[threadIdx.x];
+    if (threadIdx.x == 0) {
+        st[0] = k;
+        st[1] = 0;
+        st[2] = 0;
+        *slow = 0;
+    }
+}
+
+void basis_from_products_gated(Ctx* ctx, const double* W, int n, int wc, int k, const double* sig,
+                               const int* eig_status, double* U, double* sv, int* st, const int* need) {
+    MB_LAUNCH(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st, need);
+}
+
 void basis_from_products(Ctx* ctx, const double* W, int n, int wc, int k, const double* sig, const int* eig_status,
                          double* U, double* sv, int* st) {
-    MB_LAUNCH(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st);
+    const std::size_t fsm = 2ull * n * k * sizeof(double);
+    if (wc >= k && k <= kFastK && fsm <= 200 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            MB_CUDA(cudaFuncSetAttribute(basis_products_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr = true;
+        }
+        DBuf<int> slow(ctx, 1);
+        MB_LAUNCH(ctx, basis_products_fast_kernel, 1, kB, fsm, W, n, k, sig, U, sv, st, slow.get());
+        MB_LAUNCH(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st,
+                  static_cast<const int*>(slow.get()));
+        return;
+    }
+    MB_LAUNCH(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st,
+              static_cast<const int*>(nullptr));
 }
 
 // ---------------------------------------------------------------------------
@@ -364,7 +637,9 @@ int sumsq_scratch() { return kRedBlocks; }
 // zero padded to rs columns)
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void factor_rowmajor_kernel(const double* __restrict__ U, int n, int r, int rs, T* __restrict__ out) {
+__global__ void factor_rowmajor_kernel(const double* __restrict__ U, int n, int r, int rs, T* __restrict__ out,
+                                       const int* __restrict__ need) {
+    if (need && need[0] == 0) return;
     const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (idx >= static_cast<long long>(n) * rs) return;
     const int i = static_cast<int>(idx / rs), c = static_cast<int>(idx % rs);
@@ -372,9 +647,16 @@ __global__ void factor_rowmajor_kernel(const double* __restrict__ U, int n, int 
 }
 
 template <typename T>
-void factor_rowmajor(Ctx* ctx, const double* U, int n, int r, int rs, T* out) {
+void factor_rowmajor_gated(Ctx* ctx, const double* U, int n, int r, int rs, T* out, const int* need) {
     const long long tot = static_cast<long long>(n) * rs;
-    MB_LAUNCH(ctx, factor_rowmajor_kernel<T>, ceil_div(tot, 256), 256, 0, U, n, r, rs, out);
+    MB_LAUNCH(ctx, factor_rowmajor_kernel<T>, ceil_div(tot, 256), 256, 0, U, n, r, rs, out, need);
+}
+template void factor_rowmajor_gated<float>(Ctx*, const double*, int, int, int, float*, const int*);
+template void factor_rowmajor_gated<double>(Ctx*, const double*, int, int, int, double*, const int*);
+
+template <typename T>
+void factor_rowmajor(Ctx* ctx, const double* U, int n, int r, int rs, T* out) {
+    factor_rowmajor_gated<T>(ctx, U, n, r, rs, out, nullptr);
 }
 template void factor_rowmajor<float>(Ctx*, const double*, int, int, int, float*);
 template void factor_rowmajor<double>(Ctx*, const double*, int, int, int, double*);

@@ -1,0 +1,540 @@
+// Fused column-side mode basis on one thread-block cluster.
+//
+// The HOOI factor update for mode n (tucker.cpp:182-193 -> leading_left_basis,
+// linalg.cpp:283-296 / :335-352 column side) is, for Y = Y_(n) (rows x n,
+// n = prod of the other ranks <= ~120):
+//   G = Y^T Y,  (theta, V) = top-k eigenpairs of G,  W = Y V,
+//   U = orthonormal_columns(W) with rank / collapse tests and canonical signs,
+// plus the row-major copy of U the TTM kernel gathers from.  As separate
+// kernels these are six latency-bound launches; here one cluster of CL CTAs
+// does all of it with the operands in shared memory:
+//   CTAs 1..CL-1  stage a block of Y's rows (fp64) and form its partial Gram
+//                 on the fp64 tensor cores (mma.m8n8k4);
+//   all CTAs      reduce the partials slice by slice over distributed shared
+//                 memory (fixed order) straight into CTA 0's G;
+//   CTA 0         runs the warm-started subspace eigensolver (eig_sub.cuh) on G;
+//   CTAs 1..CL-1  read V from CTA 0, form W = Y V for their rows and the k x k
+//                 Gram of W; CTA 0 reduces it and factors it (CholQR2 = the
+//                 reference's twice Gram-Schmidt for these nearly orthogonal
+//                 columns, see linalg.cu); the row blocks apply R^{-1} twice,
+//                 vote the canonical signs and write U and the TTM copy.
+// Anything off the fast path (eigensolver not certified, a rank or collapse
+// test failing) is handed to the separate kernels through flags: G or W is
+// written out and the follow-up launches (which no-op otherwise) finish the
+// job exactly as the unfused route would.
+#include <cooperative_groups.h>
+
+#include "eig_sub.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace machb {
+
+namespace {
+
+constexpr int kCL = 8;     // cluster size (portable)
+constexpr int kMaxK = 32;  // ranks handled by the fused route
+
+template <typename T>
+struct MBArgs {
+    const T* Y;
+    int rows, n, k, rs;
+    int m, maxit;
+    double tol;
+    const double* X0;
+    int x0_cols;
+    double* Xkeep;
+    double* U;      // rows x k, column-major
+    double* sv;     // k
+    int* st;        // 3
+    T* Ur;          // rows x rs, row-major (TTM copy)
+    double* sig;    // k (also for the fallback chain)
+    int* estatus;   // 3: converged, zero, iterations
+    double* Gout;   // n x n (eigen fallback)
+    double* Wout;   // rows x k (basis fallback)
+    int* flags;     // 4: eig_topk skip, need W = Y V, need slow basis, need row-major copy
+    int ch;         // rows per row-block CTA (multiple of 4)
+};
+
+template <int B>
+struct MBLayout {
+    // CTA 0:  [G][solver workspace]          others: [Y block][partial Gram]
+    static std::size_t g_doubles(int n) {
+        const int npad = (n + 7) & ~7;
+        return static_cast<std::size_t>(npad) * frag_stride(npad);
+    }
+    static std::size_t cta0(int n) { return g_doubles(n) + SubWs<B>::doubles((n + 7) & ~7); }
+    static std::size_t block(int n, int ch) {  // the Gram region later holds V and two W blocks (phase D)
+        const int npad = (n + 7) & ~7;
+        const std::size_t ch8 = (static_cast<std::size_t>(ch) + 7) & ~std::size_t(7);
+        return ch8 * frag_stride(npad) + std::max(g_doubles(n), (2 * ch8 + npad) * frag_stride(kMaxK));
+    }
+    static std::size_t bytes(int n, int ch) { return 8 * std::max(cta0(n), block(n, ch)) + 16; }
+};
+
+template <int B, typename T>
+__global__ void __launch_bounds__(kThreads) mode_basis_kernel(MBArgs<T> A, long long* tstamp) {
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) double sm[];
+    const int rank = static_cast<int>(cluster.block_rank());
+    const int CL = static_cast<int>(cluster.num_blocks());
+    const int n = A.n, k = A.k;
+    const int npad = (n + 7) & ~7;
+    const int ldg = frag_stride(npad);
+    const int YS = ldg;  // row stride of the staged Y block
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gr = lane >> 2, tq = lane & 3;
+    int ns_ = 0;
+    if (rank != 0) tstamp = nullptr;  // the stamps follow CTA 0
+    MB_STAMP(0);
+
+    __shared__ double Mk[kMaxK * kMaxK];   // k x k Gram partial / reduced (ld kMaxK)
+    __shared__ double Rk[kMaxK * kMaxK];   // R^{-1} (CTA 0)
+    __shared__ double dg[kMaxK];
+    __shared__ double amax[kMaxK];         // per-column max |u| of this block
+    __shared__ int aidx[kMaxK];            // ... and its (global) row
+    __shared__ double sgn[kMaxK];          // canonical signs (CTA 0)
+    __shared__ int mflag;                  // CTA 0: 0 fast, 1 basis fallback, 2 eigen fallback
+    __shared__ int flagw;
+
+    // row block of this CTA (CTAs 1..CL-1)
+    const int r0 = (rank - 1) * A.ch;
+    const int nr = rank == 0 ? 0 : max(0, min(A.rows, r0 + A.ch) - r0);
+    const int nr4 = (nr + 3) & ~3;
+    double* Yb = sm;                                                // nr4 x YS
+    double* P = sm + static_cast<std::size_t>((A.ch + 7) & ~7) * YS;  // npad x ldg
+    double* G = sm;                                                 // CTA 0
+    double* wsp = sm + static_cast<std::size_t>(npad) * ldg;        // CTA 0
+
+    // ---- phase A: partial Gram of this row block ----
+    if (rank > 0) {
+        const int nr8z = (nr + 7) & ~7;  // rows zero-filled to a whole MMA tile
+        for (int base = threadIdx.x; base < nr8z * npad; base += 8 * kThreads) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {  // eight global loads in flight
+                const int e = base + u * kThreads;
+                const int c = e / nr8z, i = e - c * nr8z;  // consecutive threads: consecutive rows (coalesced)
+                v[u] = (e < nr8z * npad && i < nr && c < n) ? static_cast<double>(A.Y[(r0 + i) + static_cast<std::size_t>(c) * A.rows]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = base + u * kThreads;
+                if (e < nr8z * npad) {
+                    const int c = e / nr8z, i = e - c * nr8z;
+                    Yb[i * YS + c] = v[u];
+                }
+            }
+        }
+        __syncthreads();
+        const int nts = npad / 8;
+        for (int t = warp; t < nts * (nts + 1) / 2; t += kThreads / 32) {
+            int ti = 0;
+            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+            const int tj = t - ti * (ti + 1) / 2;
+            double c0 = 0.0, c1 = 0.0;
+            const double* pa = Yb + tq * YS + ti * 8 + gr;
+            const double* pb = Yb + tq * YS + tj * 8 + gr;
+#pragma unroll 4
+            for (int k0 = 0; k0 < nr4; k0 += 4) dmma(c0, c1, pa[k0 * YS], pb[k0 * YS]);
+            const int r = ti * 8 + gr;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int c = tj * 8 + 2 * tq + e;
+                const double v = e ? c1 : c0;
+                if (ti != tj || r >= c) {
+                    P[r + c * ldg] = v;
+                    P[c + r * ldg] = v;
+                }
+            }
+        }
+    }
+    cluster.sync();  // #1: partials complete
+    MB_STAMP(1);
+
+    // ---- phase B: G = sum of partials, slice by slice, into CTA 0 ----
+    {
+        double* G0 = cluster.map_shared_rank(G, 0);
+        const int E = npad * npad;
+        const int e0 = static_cast<int>((static_cast<long long>(E) * rank) / CL);
+        const int e1 = static_cast<int>((static_cast<long long>(E) * (rank + 1)) / CL);
+        for (int e = e0 + threadIdx.x; e < e1; e += kThreads) {
+            const int r = e % npad, c = e / npad;
+            const int off = r + c * ldg;
+            double s = 0.0;
+            for (int q = 1; q < CL; ++q) s += cluster.map_shared_rank(P, q)[off];
+            G0[off] = s;
+        }
+    }
+    cluster.sync();  // #2: G complete in CTA 0
+    MB_STAMP(2);
+
+    // ---- phase C: eigensolver on CTA 0 ----
+    if (rank == 0) {
+        double fro = 0.0;
+        for (int e = threadIdx.x; e < n * n; e += kThreads) {
+            const double g = G[(e % n) + (e / n) * ldg];
+            fro = fma(g, g, fro);
+        }
+        SubWs<B> ws(wsp, npad);
+        fro = cta_sum(fro, ws.red);
+        if (threadIdx.x == 0) mflag = 0;
+        if (fro == 0.0) {
+            // exactly zero matricisation: identity basis, rank 0 (linalg.cpp:326-333)
+            if (threadIdx.x == 0) mflag = 3;
+        } else {
+            bool conv = false;
+            int it = 0;
+            double* X = subspace_core<B>(ws, G, ldg, n, k, A.m, A.maxit, A.tol, A.X0, A.x0_cols, conv, it, &flagw,
+                                         tstamp, ns_);
+            if (A.Xkeep)
+                for (int e = threadIdx.x; e < n * B; e += kThreads) A.Xkeep[e] = X[(e % n) * Sub<B>::XS + e / n];
+            if (threadIdx.x < k) A.sig[threadIdx.x] = sqrt(fmax(0.0, ws.th[threadIdx.x]));
+            if (threadIdx.x == 0) {
+                A.estatus[0] = conv ? 1 : 0;
+                A.estatus[1] = 0;
+                A.estatus[2] = it;
+                if (!conv) mflag = 2;
+            }
+            __syncthreads();
+            if (!conv)  // hand G to the exact solver
+                for (int e = threadIdx.x; e < n * n; e += kThreads) A.Gout[e] = G[(e % n) + (e / n) * ldg];
+            // V (first k Ritz vectors) stays in ws.X for the row blocks
+            if (threadIdx.x == 0) flagw = static_cast<int>(X - wsp);  // offset of the final block
+        }
+        __syncthreads();
+    }
+    cluster.sync();  // #3: V (or a fallback decision) ready
+    MB_STAMP(3);
+
+    const int mode = *cluster.map_shared_rank(&mflag, 0);
+    if (mode >= 2) {  // eigen fallback or zero matrix: the unfused kernels finish
+        if (rank == 0 && threadIdx.x == 0) {
+            A.flags[0] = mode == 2 ? 0 : 1;  // eig_topk runs (skip = 0) only for the fallback
+            A.flags[1] = mode == 2 ? 1 : 0;
+            A.flags[2] = mode == 2 ? 1 : 0;
+            A.flags[3] = 1;
+            if (mode == 3) { A.estatus[0] = 1; A.estatus[1] = 1; A.estatus[2] = 0; }
+        }
+        if (mode == 3 && rank == 0) {  // identity basis right here
+            for (int e = threadIdx.x; e < A.rows * k; e += kThreads) A.U[e] = ((e % A.rows) == (e / A.rows)) ? 1.0 : 0.0;
+            if (threadIdx.x < k) { A.sv[threadIdx.x] = 0.0; A.sig[threadIdx.x] = 0.0; }
+            if (threadIdx.x == 0) { A.st[0] = 0; A.st[1] = 1; A.st[2] = 0; }
+        }
+        cluster.sync();
+        return;
+    }
+
+    // ---- phase D: W = Y V on the row blocks (fp64 MMA), then CholQR2 ----
+    constexpr int XS = Sub<B>::XS;
+    const int KP = (k + 7) & ~7;         // k rounded to MMA tiles
+    const int VS = frag_stride(KP);      // row stride of V / W blocks
+    const int nr8 = (nr + 7) & ~7;
+    double* Vl = P;                                          // npad x VS
+    double* Wb = Vl + static_cast<std::size_t>(npad) * VS;   // nr8 x VS
+    double* Wt = Wb + static_cast<std::size_t>(nr8) * VS;    // nr8 x VS
+    if (rank > 0) {
+        const int xoff = *cluster.map_shared_rank(&flagw, 0);
+        const double* Xr = cluster.map_shared_rank(wsp, 0) + xoff;
+        for (int e = threadIdx.x; e < npad * KP; e += kThreads) {
+            const int r = e / KP, j = e - (e / KP) * KP;
+            Vl[r * VS + j] = (r < n && j < k) ? Xr[r * XS + j] : 0.0;
+        }
+        __syncthreads();
+        // W (nr8 x KP) = Yb (nr8 x npad) Vl (npad x KP): warp per 8-row tile
+        for (int rt = warp; rt < nr8 / 8; rt += kThreads / 32) {
+            double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+            const double* ya = Yb + (rt * 8 + gr) * YS + tq;
+            for (int k0 = 0; k0 < npad; k0 += 4) {
+                const double av = ya[k0];
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (t * 8 < KP) dmma(c[t][0], c[t][1], av, Vl[(k0 + tq) * VS + t * 8 + gr]);
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (t * 8 < KP) {
+                    Wb[(rt * 8 + gr) * VS + t * 8 + 2 * tq] = c[t][0];
+                    Wb[(rt * 8 + gr) * VS + t * 8 + 2 * tq + 1] = c[t][1];
+                }
+        }
+        __syncthreads();
+    }
+
+    // k x k Gram of this row block (warp per 8x8 tile, fp64 MMA) into Mk
+    auto block_gram = [&](const double* X) {
+        const int nt = KP / 8;
+        for (int t = warp; t < nt * nt; t += kThreads / 32) {
+            const int ti = t % nt, tj = t / nt;
+            double c0 = 0.0, c1 = 0.0;
+            for (int k0 = 0; k0 < nr8; k0 += 4)
+                dmma(c0, c1, X[(k0 + tq) * VS + ti * 8 + gr], X[(k0 + tq) * VS + tj * 8 + gr]);
+            Mk[(ti * 8 + gr) + (tj * 8 + 2 * tq) * kMaxK] = c0;
+            Mk[(ti * 8 + gr) + (tj * 8 + 2 * tq + 1) * kMaxK] = c1;
+        }
+        __syncthreads();
+    };
+    // CTA 0: M = sum of the blocks' Grams (fixed order), R = chol(M) by warp 0,
+    // Rk = R^{-1}.  With `tests`, also the reference's rank and collapse tests
+    // (||w_j|| > sigma_1 * kRankFloor, residual R_jj > kCollapseFloor ||w_j||).
+    auto reduce_factor = [&](bool tests) -> bool {
+        for (int e = threadIdx.x; e < k * k; e += kThreads) {
+            const int i = e % k, j = e / k;
+            double s = 0.0;
+            for (int q = 1; q < CL; ++q) s += cluster.map_shared_rank(Mk, q)[i + j * kMaxK];
+            Rk[i + j * kMaxK] = s;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int good = 1;
+            const double floor = A.sig[0] * 1e-6;  // kRankFloor (linalg_internal.hpp:23)
+            if (lane < k) dg[lane] = sqrt(fmax(0.0, Rk[lane + lane * kMaxK]));
+            __syncwarp();
+            for (int j = 0; j < k; ++j) {
+                const double d = Rk[j + j * kMaxK];
+                if (!(d > 0.0)) { good = 0; break; }
+                const double rjj = sqrt(d);
+                if (tests && (!(dg[j] > floor) || !(rjj > 1e-3 * dg[j]))) good = 0;  // kCollapseFloor
+                __syncwarp();
+                for (int m = j + lane; m < k; m += 32) Rk[j + m * kMaxK] = (m == j) ? rjj : Rk[j + m * kMaxK] / rjj;
+                __syncwarp();
+                const int rem = k - j - 1;
+                for (int e = lane; e < rem * rem; e += 32) {
+                    const int l = j + 1 + e % rem, m = j + 1 + e / rem;
+                    if (l <= m) Rk[l + m * kMaxK] -= Rk[j + l * kMaxK] * Rk[j + m * kMaxK];
+                }
+                __syncwarp();
+            }
+            if (lane == 0) flagw = good;
+            __syncwarp();
+            if (good && lane < k) {  // lane c: column c of R^{-1} into Mk
+                const int c = lane;
+                for (int r = k - 1; r >= 0; --r) {
+                    double v = (r == c) ? 1.0 : 0.0;
+                    for (int p = r + 1; p <= c; ++p) v -= Rk[r + p * kMaxK] * Mk[p + c * kMaxK];
+                    Mk[r + c * kMaxK] = (r <= c) ? v / Rk[r + r * kMaxK] : 0.0;
+                }
+            }
+        }
+        __syncthreads();
+        if (!flagw) return false;
+        for (int e = threadIdx.x; e < k * k; e += kThreads) Rk[e % k + (e / k) * kMaxK] = Mk[e % k + (e / k) * kMaxK];
+        __syncthreads();
+        return true;
+    };
+    // row block: Wt = Wb R^{-1} (R^{-1} from CTA 0, zero-padded to KP x KP), swap
+    auto apply_rinv = [&]() {
+        const double* R0 = cluster.map_shared_rank(Rk, 0);
+        for (int e = threadIdx.x; e < KP * KP; e += kThreads) {
+            const int i = e % KP, j = e / KP;
+            Mk[i + j * kMaxK] = (i < k && j < k) ? R0[i + j * kMaxK] : 0.0;
+        }
+        __syncthreads();
+        for (int rt = warp; rt < nr8 / 8; rt += kThreads / 32) {
+            double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+            for (int k0 = 0; k0 < KP; k0 += 4) {
+                const double av = Wb[(rt * 8 + gr) * VS + k0 + tq];
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (t * 8 < KP) dmma(c[t][0], c[t][1], av, Mk[(k0 + tq) + (t * 8 + gr) * kMaxK]);
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (t * 8 < KP) {
+                    Wt[(rt * 8 + gr) * VS + t * 8 + 2 * tq] = c[t][0];
+                    Wt[(rt * 8 + gr) * VS + t * 8 + 2 * tq + 1] = c[t][1];
+                }
+        }
+        __syncthreads();
+        double* tmp = Wb;
+        Wb = Wt;
+        Wt = tmp;
+    };
+
+    // pass 1 (with the reference's rank and collapse tests)
+    if (rank > 0) block_gram(Wb);
+    cluster.sync();  // #4
+    if (rank == 0) {
+        const bool ok = reduce_factor(true);
+        if (threadIdx.x == 0) mflag = ok ? 0 : 1;
+        __syncthreads();
+    }
+    cluster.sync();  // #5
+    MB_STAMP(5);
+    if (*cluster.map_shared_rank(&mflag, 0) == 1) {  // basis fallback: hand W over
+        if (rank > 0)
+            for (int e = threadIdx.x; e < nr * k; e += kThreads) {
+                const int i = e % nr, j = e / nr;
+                A.Wout[(r0 + i) + static_cast<std::size_t>(j) * A.rows] = Wb[i * VS + j];
+            }
+        if (rank == 0 && threadIdx.x == 0) { A.flags[0] = 1; A.flags[1] = 0; A.flags[2] = 1; A.flags[3] = 1; }
+        cluster.sync();
+        return;
+    }
+    if (rank > 0) {
+        apply_rinv();
+        block_gram(Wb);
+    }
+    cluster.sync();  // #6
+    if (rank == 0) {
+        const bool ok = reduce_factor(false);
+        if (threadIdx.x == 0 && !ok) mflag = 4;  // pass 2 cannot fail after pass 1; guard anyway
+        __syncthreads();
+    }
+    cluster.sync();  // #7
+    if (rank > 0) {
+        apply_rinv();
+        // canonical sign vote: largest |u| per column, lowest row on ties (linalg.cpp:18-32)
+        for (int j = warp; j < k; j += kThreads / 32) {
+            double best = -1.0;
+            int bi = 0x7fffffff;
+            for (int r = lane; r < nr; r += 32) {
+                const double a = fabs(Wb[r * VS + j]);
+                if (a > best) { best = a; bi = r0 + r; }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            if (lane == 0) {
+                amax[j] = best;
+                aidx[j] = bi;
+                dg[j] = (bi < 0x7fffffff) ? Wb[(bi - r0) * VS + j] : 0.0;
+            }
+        }
+    }
+    cluster.sync();  // #8
+    MB_STAMP(8);
+    if (rank == 0 && threadIdx.x < k) {
+        const int j = threadIdx.x;
+        double best = -1.0, val = 0.0;
+        int bi = 0x7fffffff;
+        for (int q = 1; q < CL; ++q) {
+            const double b = cluster.map_shared_rank(amax, q)[j];
+            const int i = cluster.map_shared_rank(aidx, q)[j];
+            if (b > best || (b == best && i < bi)) { best = b; bi = i; val = cluster.map_shared_rank(dg, q)[j]; }
+        }
+        sgn[j] = val < 0.0 ? -1.0 : 1.0;
+        A.sv[j] = A.sig[j];
+        if (j == 0) {
+            A.st[0] = k; A.st[1] = 0; A.st[2] = 0;
+            A.flags[0] = 1; A.flags[1] = 0; A.flags[2] = 0; A.flags[3] = 0;
+        }
+    }
+    cluster.sync();  // #9
+    if (rank > 0) {
+        const double* s0 = cluster.map_shared_rank(sgn, 0);
+        if (threadIdx.x < k) dg[threadIdx.x] = s0[threadIdx.x];
+        __syncthreads();
+        for (int e = threadIdx.x; e < nr * k; e += kThreads) {
+            const int i = e % nr, j = e / nr;
+            A.U[(r0 + i) + static_cast<std::size_t>(j) * A.rows] = dg[j] * Wb[i * VS + j];
+        }
+        if (A.Ur)
+            for (int e = threadIdx.x; e < nr * A.rs; e += kThreads) {
+                const int i = e / A.rs, j = e - (e / A.rs) * A.rs;
+                A.Ur[static_cast<std::size_t>(r0 + i) * A.rs + j] = j < k ? static_cast<T>(dg[j] * Wb[i * VS + j]) : T(0);
+            }
+    }
+    cluster.sync();  // #10: CTA 0's shared memory is no longer read remotely
+    MB_STAMP(10);
+    if (tstamp && threadIdx.x == 0) {
+        long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        tstamp[238] = t_;
+    }
+}
+
+template <int B, typename T>
+bool launch_mode_basis(Ctx* ctx, MBArgs<T> A) {
+    const int CL = kCL;
+    A.ch = ((A.rows + CL - 2) / (CL - 1) + 3) & ~3;
+    auto kern = mode_basis_kernel<B, T>;
+    static int dyn_max = -1;
+    if (dyn_max < 0) {
+        cudaFuncAttributes fa{};
+        MB_CUDA(cudaFuncGetAttributes(&fa, kern));
+        int optin = 0;
+        MB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+        dyn_max = optin - static_cast<int>(fa.sharedSizeBytes);
+        MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max));
+    }
+    const std::size_t smem = MBLayout<B>::bytes(A.n, A.ch);
+    if (smem > static_cast<std::size_t>(dyn_max)) return false;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(CL, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static const bool dbg = std::getenv("MACH_DEBUG_EIG_T") != nullptr;
+    DBuf<long long> tsb;
+    if (dbg) {
+        tsb.alloc(ctx, 240);
+        tsb.zero(ctx);
+    }
+    long long* ts = dbg ? tsb.get() : nullptr;
+    MB_LAUNCH_EX(ctx, "mode_basis_kernel<B, T>", &cfg, kern, A, ts);
+    if (dbg) {
+        long long h[240];
+        to_host(ctx, h, tsb.get(), 240);
+        sync(ctx);
+        std::fprintf(stderr, "[mb-t] n=%d B=%d rows=%d:", A.n, B, A.rows);
+        for (int i = 1; i < 118 && h[2 * i + 1]; ++i)
+            std::fprintf(stderr, " %lld:%.1f", h[2 * i], (h[2 * i + 1] - h[2 * i - 1]) * 1e-3);
+        std::fprintf(stderr, " | end-start %.1fus\n", (h[238] - h[1]) * 1e-3);
+    }
+    return true;
+}
+
+}  // namespace
+
+// Fused column-side basis for Y (rows x n) when it applies; false = use the
+// unfused route.  On true, U / sv / st / Ur (and warm Xkeep) are produced in
+// the stream, with the unfused kernels queued behind as flag-gated fallbacks.
+template <typename T>
+bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
+                      double* U, double* sv, int* st, T* Ur, int rs) {
+    if (k < 1 || k > kMaxK || n <= 48 || b >= n || k > b - 2 || (b % 8) != 0 || rows < 2 * kCL) return false;
+    MBArgs<T> A{};
+    A.Y = Y; A.rows = rows; A.n = n; A.k = k; A.rs = rs;
+    A.m = 4; A.maxit = 40; A.tol = 1e-12;
+    A.X0 = X0; A.x0_cols = x0_cols; A.Xkeep = Xkeep;
+    A.U = U; A.sv = sv; A.st = st; A.Ur = Ur;
+    DBuf<double> sig(ctx, k), Gout(ctx, static_cast<std::size_t>(n) * n), Wout(ctx, static_cast<std::size_t>(rows) * k),
+        V(ctx, static_cast<std::size_t>(n) * k);
+    DBuf<int> est(ctx, 3), flags(ctx, 4);
+    A.sig = sig.get(); A.estatus = est.get(); A.Gout = Gout.get(); A.Wout = Wout.get(); A.flags = flags.get();
+    bool ok = false;
+    switch (b) {
+        case 8: ok = launch_mode_basis<8, T>(ctx, A); break;
+        case 16: ok = launch_mode_basis<16, T>(ctx, A); break;
+        case 24: ok = launch_mode_basis<24, T>(ctx, A); break;
+        case 32: ok = launch_mode_basis<32, T>(ctx, A); break;
+        default: break;
+    }
+    if (!ok) return false;
+    // flag-gated fallbacks (each returns immediately on the fast path)
+    const int* f = flags.get();
+    DBuf<double> work(ctx, eig_work_doubles(n, k));
+    eig_topk(ctx, Gout.get(), n, k, work.get(), V.get(), sig.get(), est.get(), f + 0);
+    matmul_yv_gated<T>(ctx, Y, rows, n, V.get(), k, Wout.get(), f + 1);
+    basis_from_products_gated(ctx, Wout.get(), rows, k, k, sig.get(), est.get(), U, sv, st, f + 2);
+    if (Ur) factor_rowmajor_gated<T>(ctx, U, rows, k, rs, Ur, f + 3);
+    return true;
+}
+
+template bool mode_basis_fused<float>(Ctx*, const float*, int, int, int, const double*, int, double*, int, double*,
+                                      double*, int*, float*, int);
+template bool mode_basis_fused<double>(Ctx*, const double*, int, int, int, const double*, int, double*, int, double*,
+                                       double*, int*, double*, int);
+
+}  // namespace machb

@@ -272,12 +272,14 @@ namespace {
 template <typename T>
 __global__ void reduce_partials_kernel(const T* __restrict__ P, const int* __restrict__ st_base, int rows, int C,
                                        T* __restrict__ Y) {
+    // consecutive threads take consecutive columns of one row: the task
+    // partials P[q][:] are read coalesced (the Y stores are strided)
     const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (idx >= static_cast<long long>(rows) * C) return;
-    const int row = static_cast<int>(idx % rows), col = static_cast<int>(idx / rows);
+    const int col = static_cast<int>(idx % C), row = static_cast<int>(idx / C);
     T s = T(0);
     for (int q = st_base[row]; q < st_base[row + 1]; ++q) s += P[static_cast<long long>(q) * C + col];
-    Y[idx] = s;
+    Y[row + static_cast<long long>(col) * rows] = s;
 }
 
 // ---------------------------------------------------------------------------

@@ -105,6 +105,17 @@ void sumsq(Ctx* ctx, const T* x, long long n, double* scratch, double* out);
 int sumsq_scratch();
 template <typename T>
 void factor_rowmajor(Ctx* ctx, const double* U, int n, int r, int rs, T* out);
+// flag-gated variants (run only when need[0] != 0; the fused mode basis queues them as fallbacks)
+template <typename T>
+void matmul_yv_gated(Ctx* ctx, const T* Y, int rows, int C, const double* V, int kc, double* W, const int* need);
+void basis_from_products_gated(Ctx* ctx, const double* W, int n, int wc, int k, const double* sig,
+                               const int* eig_status, double* U, double* sv, int* st, const int* need);
+template <typename T>
+void factor_rowmajor_gated(Ctx* ctx, const double* U, int n, int r, int rs, T* out, const int* need);
+// fused column-side mode basis (mode_basis.cu); false = not applicable
+template <typename T>
+bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
+                      double* U, double* sv, int* st, T* Ur, int rs);
 
 // ---- dense route (dense.cu) ----
 // out[a + inner*(q + J*c)] = sum_r in[a + inner*(r + len*c)] * M(q, r) where

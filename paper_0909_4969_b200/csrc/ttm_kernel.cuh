@@ -231,27 +231,26 @@ __global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
             continue;
         }
 
-        // ---- stage 1: this lane's fibre segment, eight positions per step.
+        // ---- stage 1: this lane's fibre segment, PU positions per step.
         // Position offsets come precomputed with the task. ----
         const unsigned short* joff = reinterpret_cast<const unsigned short*>(sd + 32);
         T f[RS];
 #pragma unroll
         for (int a = 0; a < RS; ++a) f[a] = T(0);
-        for (int j = 0; j < tk.maxlen; j += 8) {
-            const uint4 o8 = *reinterpret_cast<const uint4*>(joff + j);
-            const unsigned ow[4] = {o8.x, o8.y, o8.z, o8.w};
-            int ix[8];
-            T vx[8];
-            bool act[8];
+        constexpr int PU = sizeof(T) == 4 ? 8 : 4;  // positions per step (register budget)
+        for (int j = 0; j < tk.maxlen; j += PU) {
+            int ix[PU];
+            T vx[PU];
+            bool act[PU];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int off = static_cast<int>((ow[k >> 1] >> (16 * (k & 1))) & 0xffffu) + lane;
+            for (int k = 0; k < PU; ++k) {
+                const int off = static_cast<int>(joff[j + k]) + lane;
                 act[k] = j + k < my.y;
                 ix[k] = act[k] ? static_cast<int>(si[off]) : 0;
                 vx[k] = act[k] ? sv[off] : T(0);
             }
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
+            for (int k = 0; k < PU; ++k)
                 if (act[k]) gather_fma(f, ix[k], vx[k]);
         }
 

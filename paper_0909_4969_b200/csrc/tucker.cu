@@ -190,6 +190,40 @@ void lsb_device(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U
     }
 }
 
+// Column-side factor update through the fused cluster kernel (mode_basis.cu),
+// including the TTM kernel's row-major factor copy.  False when the fused
+// route does not apply (the caller then runs lsb_device + the copy).
+template <typename T>
+bool lsb_fused(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U, double* sv, int* st, Warm* warm,
+               const double* Uprev, T* Ur, int rs) {
+    if (!warm || rows < 1 || cols < 1 || k < 1 || k > rows) return false;
+    const bool row_side = rows <= cols && k <= cols;
+    if (row_side || cols > 4096 || k > cols) return false;
+    const int side = static_cast<int>(cols);
+    const int b = eig_block(side, k);
+    if (warm->X.n != static_cast<std::size_t>(side) * b) {
+        warm->X.alloc(ctx, static_cast<std::size_t>(side) * b);
+        warm->cols = 0;
+    }
+    warm->b = b;
+    const double* X0 = nullptr;
+    int x0c = 0;
+    DBuf<double> seed;
+    if (warm->cols > 0) {
+        X0 = warm->X.get();
+        x0c = warm->cols;
+    } else if (Uprev) {
+        seed.alloc(ctx, static_cast<std::size_t>(side) * k);
+        MB_LAUNCH(ctx, yt_u_kernel<T>, ceil_div(static_cast<long long>(side) * k, 256), 256, 0, Y, rows, side, Uprev, k,
+                  seed.get());
+        X0 = seed.get();
+        x0c = k;
+    }
+    if (!mode_basis_fused<T>(ctx, Y, rows, side, k, X0, x0c, warm->X.get(), b, U, sv, st, Ur, rs)) return false;
+    warm->cols = b;
+    return true;
+}
+
 // core x_1 U_1 ... x_d U_d into a fresh fp64 dense buffer (tucker.cpp:204-209)
 DBuf<double> reconstruct_dev(Ctx* ctx, const double* core, const std::vector<int>& ranks, const std::vector<int>& dims,
                              const std::vector<DBuf<double>>& U) {
@@ -531,11 +565,16 @@ struct SparseSession : SessionBase {
         sweep_fits.assign(1, fit);
     }
     void sweep() override {
+        static const bool nofuse = std::getenv("MACH_NO_FUSED_BASIS") != nullptr;
         for (int i = 0; i < d; ++i) {
+            const std::size_t si = static_cast<std::size_t>(i);
             mode_y(i);
-            lsb_device<T>(ctx, Y.get(), dims[static_cast<std::size_t>(i)], C[static_cast<std::size_t>(i)],
-                          ranks[static_cast<std::size_t>(i)], fs.U[static_cast<std::size_t>(i)].get(), sv_at(i),
-                          fs.st.get() + 3 * i, &warm[static_cast<std::size_t>(i)], fs.U[static_cast<std::size_t>(i)].get());
+            if (!nofuse && lsb_fused<T>(ctx, Y.get(), dims[si], C[si], ranks[si], fs.U[si].get(), sv_at(i),
+                                        fs.st.get() + 3 * i, &warm[si], fs.U[si].get(), Ur[si].get(),
+                                        ttm_stride(ranks[si], sizeof(T))))
+                continue;
+            lsb_device<T>(ctx, Y.get(), dims[si], C[si], ranks[si], fs.U[si].get(), sv_at(i), fs.st.get() + 3 * i,
+                          &warm[si], fs.U[si].get());
             refresh(i);
         }
         fit = core_and_fit();
