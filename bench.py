@@ -177,6 +177,7 @@ def run_mach(args, rank, world, local):
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             ms = float(tt.item())
         model = sess.model()
+        sess_bytes = [b for b in (sess.ttm_bytes(m) for m in range(len(dims))) if b > 0] or [0]
 
         # ---- per-kernel profile pass (not timed for `value`) ----
         mb.profile(ctx, True)
@@ -191,19 +192,25 @@ def run_mach(args, rank, world, local):
 
     vsize = 4 if dtype == "float32" else 8
     d = len(dims)
-    # roofline of the dominant HBM kernel: the fused mode-n TTM (one streaming
-    # read of the mode's sorted COO per launch: nnz * (4 B key + value))
+    # roofline of the dominant HBM kernel: the fused mode-n TTM.  Algorithmic
+    # bytes per launch come from the library (inner index + value per nonzero,
+    # task records, partial rows written), averaged over the d modes.
     ttm = [(k, v) for k, v in kstats.items() if "ttm_mode_kernel" in k]
     hbm, peak_src = peaks()
     roof = None
     if ttm:
         n_l, tot = ttm[0][1]
         per_launch_ms = tot / n_l
-        bytes_per_launch = nnz * (4 + vsize)
+        bytes_per_launch = int(sum(sess_bytes) / len(sess_bytes))
         achieved = bytes_per_launch / (per_launch_ms * 1e-3) / 1e9
+        traffic = measured_traffic(args.config)
         roof = {"bound": "hbm", "kernel": "ttm_mode_kernel", "achieved": round(achieved, 1), "peak": hbm,
-                "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
-                "bytes_per_launch": bytes_per_launch, "avg_launch_ms": round(per_launch_ms, 5),
+                "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                "traffic_source": traffic.get("source") if traffic else None,
+                "bytes_per_launch": bytes_per_launch,
+                "bytes_model": "nnz*(inner index 2|4 B + value) + tasks*(344 B record+descriptor + partial row block)",
+                "avg_launch_ms": round(per_launch_ms, 5),
                 "share_of_sweep": round(tot / 2.0 / sweep_ms_prof, 3) if sweep_ms_prof else None,
                 "peak_source": peak_src}
     breakdown = {k: {"launches_per_sweep": v[0] / 2.0, "ms_per_sweep": round(v[1] / 2.0, 5)}
@@ -247,6 +254,21 @@ def run_mach(args, rank, world, local):
     sess.free()
     if rank == 0:
         print(json.dumps(out))
+
+
+def measured_traffic(config):
+    """DRAM bytes per TTM launch from the committed ncu --set full capture
+    (profiles/*ttm_ncu*.json, written by scripts/ncu_summary.py)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ttm_ncu*.json")), reverse=True):
+        try:
+            with open(path) as f:
+                j = json.load(f)
+            if j.get("config") == config:
+                return {"dram_bytes_per_launch": j["dram_bytes_per_launch"], "source": os.path.relpath(path, ROOT)}
+        except Exception:
+            continue
+    return None
 
 
 def run_e2e(args, mb, x, dims, ranks, p, seed, nnz, vsize, dev, local):

@@ -121,6 +121,10 @@ mach_status mach_hooi_begin_dense(mach_ctx* ctx, const mach_dense* t, const int*
 mach_status mach_hooi_step(mach_session* s, int n, double fit_tolerance, int* done, int* stopped);
 mach_status mach_hooi_state(mach_session* s, double* fit, int* iterations);
 mach_status mach_hooi_model(mach_session* s, mach_model** out);
+/* Algorithmic bytes one mode-`mode` TTM launch moves on the sparse route
+   (inner indices + values, task records, partial rows written); -1 when the
+   session is on the dense route.  Used for the roofline report. */
+mach_status mach_hooi_ttm_bytes(mach_session* s, int mode, long long* bytes);
 mach_status mach_session_free(mach_session* s);
 
 /* ---- per-kernel device timing (CUDA events on the context stream) -------- */

@@ -71,6 +71,7 @@ _SIGS = {
     "mach_hooi_step": (C.c_int, [vp, C.c_int, C.c_double, ip, ip]),
     "mach_hooi_state": (C.c_int, [vp, dp, ip]),
     "mach_hooi_model": (C.c_int, [vp, vpp]),
+    "mach_hooi_ttm_bytes": (C.c_int, [vp, C.c_int, C.POINTER(C.c_longlong)]),
     "mach_session_free": (C.c_int, [vp]),
     "mach_ctx_profile": (C.c_int, [vp, C.c_int]),
     "mach_ctx_kernel_stat": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t, i64p, dp]),

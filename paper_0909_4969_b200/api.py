@@ -467,6 +467,12 @@ class HooiSession:
         _check(L.lib().mach_hooi_model(self.h, C.byref(hm)))
         return _model_from(hm)
 
+    def ttm_bytes(self, mode: int) -> int:
+        """Algorithmic bytes of one mode-`mode` TTM launch (-1 on the dense route)."""
+        b = C.c_longlong()
+        _check(L.lib().mach_hooi_ttm_bytes(self.h, int(mode), C.byref(b)))
+        return int(b.value)
+
     def free(self):
         if getattr(self, "h", None):
             L.lib().mach_session_free(self.h)

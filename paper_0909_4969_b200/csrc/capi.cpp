@@ -440,6 +440,7 @@ void session_free(void* s);
 int session_iterations(void* s);
 double session_fit(void* s);
 bool session_stopped(void* s);
+long long session_ttm_bytes(void* s, int m);
 }  // namespace machb
 
 struct mach_session {
@@ -485,6 +486,14 @@ mach_status mach_hooi_state(mach_session* s, double* fit, int* iterations) {
         need(s, "session");
         if (fit) *fit = session_fit(s->s);
         if (iterations) *iterations = session_iterations(s->s);
+    });
+}
+
+mach_status mach_hooi_ttm_bytes(mach_session* s, int mode, long long* bytes) {
+    return guard([&] {
+        need(s, "session");
+        need(bytes, "bytes");
+        *bytes = session_ttm_bytes(s->s, mode);
     });
 }
 

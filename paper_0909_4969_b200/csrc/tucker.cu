@@ -323,6 +323,7 @@ struct SessionBase {
     double setup_ms = 0, hosvd_ms = 0, sample_ms = 0;
     virtual ~SessionBase() = default;
     virtual void sweep() = 0;                       // one sweep: all modes, core, fit
+    virtual long long ttm_bytes(int) const { return -1; }  // algorithmic bytes of one mode-n TTM launch
     virtual const double* core_dev() const = 0;
     double* sv_at(int m) {
         int o = 0;
@@ -581,6 +582,17 @@ struct SparseSession : SessionBase {
         warnings = read_warnings(ctx, fs.st, ranks, all);
     }
     const double* core_dev() const override { return core.get(); }
+    // bytes one mode-n TTM launch must move: per nonzero the inner index and
+    // the value, per task its record and descriptor, per task the partial
+    // row block it writes (the factor rows come from L2, not counted)
+    long long ttm_bytes(int m) const override {
+        if (m < 0 || m >= d || !plans[static_cast<std::size_t>(m)]) return -1;
+        const ModePlan& P = *plans[static_cast<std::size_t>(m)];
+        const long long nnz = X->nnz;
+        return nnz * ((P.ia16 ? 2 : 4) + static_cast<long long>(sizeof(T))) +
+               P.n_task * (static_cast<long long>(kDesc * sizeof(int2) + sizeof(TtmTask)) +
+                           static_cast<long long>(C[static_cast<std::size_t>(m)]) * static_cast<long long>(sizeof(T)));
+    }
 };
 
 }  // namespace
@@ -635,6 +647,7 @@ void session_set_sample_ms(void* s, double ms) { S(s)->sample_ms = ms; }
 int session_iterations(void* s) { return S(s)->iterations; }
 double session_fit(void* s) { return S(s)->fit; }
 bool session_stopped(void* s) { return S(s)->stopped; }
+long long session_ttm_bytes(void* s, int m) { return S(s)->ttm_bytes(m); }
 
 mach_model* tucker_sparse(mach_sparse* X, const std::vector<int>& ranks, bool do_hooi, int max_it, double tol) {
     check_ranks(X->dims, ranks);
