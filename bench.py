@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="time-slab sharded sweeps (default when WORLD_SIZE > 1; forces it at N = 1)")
     return ap.parse_args()
 
 
@@ -145,14 +147,58 @@ def run_mach(args, rank, world, local):
         stream.synchronize()
         sample_ms = ev0.elapsed_time(ev1)
         nnz = sp.nnz
+        sharded = args.sharded or world > 1
         if os.environ.get("MACH_BENCH_VERBOSE"):
             mb.profile(ctx, True)
-        sess = mb.HooiSession(sp, ranks)
+        if sharded:
+            # time-slab sharding (paper_0909_4969_b200/sharded.py): this rank
+            # samples its slab; HOSVD once on the gathered tensor; every sweep
+            # all-reduces each mode's partial Y_(n) over NCCL
+            from paper_0909_4969_b200 import sharded as SH
+            group = torch.distributed.group.WORLD if world > 1 else None
+            if world == 1:
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29533")
+                torch.distributed.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+            S = math.prod(dims[:-1])
+            t0, t1 = SH.slab_bounds(dims[-1], world, rank)
+            with torch.cuda.stream(stream):
+                slab = mb.DenseTensor.from_torch(x[t0 * S: t1 * S], list(dims[:-1]) + [t1 - t0], ctx)
+                sp_local = mb.sparsify_slab(slab, dims, t0 * S, mb.SparsifyConfig(p, seed_mach), ctx)
+                ip, vp, ib = sp_local.device_view()
+                ln = sp_local.nnz
+                np_dt = np.float32 if dtype == "float32" else np.float64
+                idx_t = SH.device_view(ip, ln, np.int32 if ib == 4 else np.int64, dev)
+                val_t = SH.device_view(vp, ln, np_dt, dev)
+                gidx = SH._allgather_varlen(idx_t, group)
+                gval = SH._allgather_varlen(val_t, group)
+                full = mb.SparseTensor.from_device(dims, gidx.numel(), gidx.data_ptr(), gval.data_ptr(), np_dt, ctx)
+                hs = mb.HooiSession(full, ranks)
+                sess = mb.HooiSession.from_session(sp_local, ranks, hs)
+                n2 = (val_t.double() ** 2).sum().reshape(1)
+                torch.distributed.all_reduce(n2, group=group)
+                sess.set_norm2(float(n2.item()))
+                hs_model = hs.model()
+                hs.free()
+                full.free()
+            engine = SH.CudaEngine(sess, np_dt, dev)
+
+            def allreduce_(y):
+                torch.distributed.all_reduce(y, group=group)
+
+            def run_sweeps(n):
+                SH.sharded_sweeps(engine, allreduce_, len(dims), n, -1.0)
+        else:
+            sess = mb.HooiSession(sp, ranks)
+
+            def run_sweeps(n):
+                sess.step(n, -1.0)
         if os.environ.get("MACH_BENCH_VERBOSE"):
             for k_, v_ in sorted(mb.kernel_stats(ctx).items(), key=lambda kv: -kv[1][1]):
                 print(f"[setup+hosvd] {k_}: {v_[0]} launches, {v_[1]:.3f} ms", file=sys.stderr)
             mb.profile(ctx, False)
-        sess.step(args.warmup, -1.0)
+        with torch.cuda.stream(stream):
+            run_sweeps(args.warmup)
         stream.synchronize()
         if world > 1:
             torch.distributed.barrier()
@@ -165,7 +211,7 @@ def run_mach(args, rank, world, local):
             for k in range(args.steps):
                 flush.zero_()  # evict the sampled tensor from L2 between timed sweeps
                 starts[k].record(stream)
-                sess.step(1, -1.0)
+                run_sweeps(1)
                 ends[k].record(stream)
         stream.synchronize()
         torch.cuda.synchronize()
@@ -184,7 +230,7 @@ def run_mach(args, rank, world, local):
         with torch.cuda.stream(stream):
             for _ in range(2):
                 flush.zero_()
-                sess.step(1, -1.0)
+                run_sweeps(1)
         stream.synchronize()
         kstats = mb.kernel_stats(ctx)
         mb.profile(ctx, False)
@@ -216,16 +262,18 @@ def run_mach(args, rank, world, local):
     breakdown = {k: {"launches_per_sweep": v[0] / 2.0, "ms_per_sweep": round(v[1] / 2.0, 5)}
                  for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][1])}
 
-    value = world * nnz / (ms * 1e-3) / 1e9
+    value = (nnz if sharded else world * nnz) / (ms * 1e-3) / 1e9  # sharded: every rank's sweep covers all nnz
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": "GNNZ/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f32" if dtype == "float32" else "f64",
         "data": "synthetic low-rank + noise (seeded, generated on device; SURVEY.md §8d generator)",
         "config": {"workload": f"{args.config.upper()}: {'x'.join(map(str, dims))} {dtype}, ranks {ranks}, "
                                f"noise {noise}, MACH p={p}, step = one HOOI sweep",
                    "nnz": nnz, "numel": int(math.prod(dims)), "seed_data": seed_data, "seed_mach": seed_mach,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": (f"time-slab shards x{world} (NCCL all-reduce of Y_(n) per mode)" if sharded
+                                   else "single"),
                    "l2": "flushed (256 MiB memset) before every timed sweep"},
         "gpu_launches": launches,
         "roofline": roof,
@@ -248,12 +296,12 @@ def run_mach(args, rank, world, local):
         out["e2e"] = run_e2e(args, mb, x, dims, ranks, p, seed_mach, nnz, vsize, dev, local)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = cpu_baseline(x, dims, ranks, p, seed_mach)
-    if world > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     sess.free()
     if rank == 0:
-        print(json.dumps(out))
+        print(json.dumps(out), flush=True)
 
 
 def measured_traffic(config):
@@ -377,10 +425,11 @@ def run_reference(args, rank, world):
                                       "restatement built with the reference flags (-O3, 1 thread)"},
            "e2e": {"value": round(nnz * len(sw) / wall / 1e9, 6), "unit": "GNNZ/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
+    print(json.dumps(out), flush=True)
 
 
 def main():
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":

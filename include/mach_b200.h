@@ -79,6 +79,12 @@ mach_status mach_sparsify_host(mach_ctx* ctx, mach_dtype dtype, int order, const
                                const void* host_x, double p, uint64_t seed, int64_t* nnz_out,
                                int64_t** idx_out, double** val_out);
 void mach_free_host(void* p);
+/* Sample the flat range [offset, offset + numel(slab)) of a tensor of dims
+   global_dims whose values are `slab` (a time slab under first-mode-fastest
+   layout).  The RNG counter and the stored indices are global, so the kept set
+   equals the full tensor's restricted to the slab (sampling.cpp:21-31). */
+mach_status mach_sparsify_slab(mach_ctx* ctx, const mach_dense* slab, int order, const int* global_dims,
+                               int64_t offset, double p, uint64_t seed, mach_sparse** out);
 
 /* ---- sparse tensors: SparseTensor (tensor.hpp:48-75) --------------------- */
 /* From host flat-index entries; canonicalised (sorted, merged, zeros
@@ -91,6 +97,12 @@ mach_status mach_sparse_download(const mach_sparse* s, int64_t* idx, double* val
 /* tensor_norm(SparseTensor) (tensor.hpp:114, tensor.cpp:166-171).           */
 mach_status mach_sparse_norm(const mach_sparse* s, double* out);
 mach_status mach_sparse_free(mach_sparse* s);
+/* device pointers of the (ascending flat index, value) arrays; idx_bytes 4|8 */
+mach_status mach_sparse_device_view(const mach_sparse* s, void** idx, void** vals, int* idx_bytes);
+/* new tensor from device arrays already in canonical form (ascending unique
+   flat indices, u32 when numel < 2^32 else u64; values of dtype), copied */
+mach_status mach_sparse_from_device(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims, int64_t nnz,
+                                    const void* idx, const void* vals, mach_sparse** out);
 
 /* ---- decompositions (tucker.hpp:34-44, sampling.hpp:32-36) -------------- */
 mach_status mach_hosvd_sparse(mach_ctx* ctx, const mach_sparse* t, const int* ranks,
@@ -125,6 +137,21 @@ mach_status mach_hooi_model(mach_session* s, mach_model** out);
    (inner indices + values, task records, partial rows written); -1 when the
    session is on the dense route.  Used for the roofline report. */
 mach_status mach_hooi_ttm_bytes(mach_session* s, int mode, long long* bytes);
+
+/* ---- split sweeps (time-slab sharding) ----------------------
+   A rank holds the nonzeros of its time slab in a tensor of the GLOBAL dims
+   (mach_sparsify_slab).  Each sweep, per mode: mach_hooi_mode_y runs the TTM
+   of the local nonzeros and returns the device buffer Y_(mode) (rows x cols,
+   column-major, the tensor dtype); the caller sums it over the ranks in place
+   (e.g. ncclAllReduce); mach_hooi_mode_update then updates the factor from
+   the summed Y.  mach_hooi_sweep_end computes core and fit from the last
+   mode's Y (tucker.cpp:80-106 bookkeeping and stop rule). */
+mach_status mach_hooi_begin_from(mach_ctx* ctx, const mach_sparse* t, const int* ranks, const mach_model* init,
+                                 mach_session** out);  /* start from init's factors (e.g. a replicated HOSVD) */
+mach_status mach_hooi_set_norm2(mach_session* s, double norm2);  /* global |X|^2 for the fit */
+mach_status mach_hooi_mode_y(mach_session* s, int mode, void** y, int* rows, int* cols);
+mach_status mach_hooi_mode_update(mach_session* s, int mode);
+mach_status mach_hooi_sweep_end(mach_session* s, double fit_tolerance, int* stopped);
 mach_status mach_session_free(mach_session* s);
 
 /* ---- per-kernel device timing (CUDA events on the context stream) -------- */

@@ -31,6 +31,7 @@ from .api import (  # noqa: F401
     mode_product,
     reconstruct,
     sparsify,
+    sparsify_slab,
 )
 
 __version__ = "0.1.0"

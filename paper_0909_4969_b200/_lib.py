@@ -72,6 +72,14 @@ _SIGS = {
     "mach_hooi_state": (C.c_int, [vp, dp, ip]),
     "mach_hooi_model": (C.c_int, [vp, vpp]),
     "mach_hooi_ttm_bytes": (C.c_int, [vp, C.c_int, C.POINTER(C.c_longlong)]),
+    "mach_hooi_begin_from": (C.c_int, [vp, vp, ip, vp, vpp]),
+    "mach_hooi_set_norm2": (C.c_int, [vp, C.c_double]),
+    "mach_hooi_mode_y": (C.c_int, [vp, C.c_int, vpp, ip, ip]),
+    "mach_hooi_mode_update": (C.c_int, [vp, C.c_int]),
+    "mach_hooi_sweep_end": (C.c_int, [vp, C.c_double, ip]),
+    "mach_sparsify_slab": (C.c_int, [vp, vp, C.c_int, ip, C.c_int64, C.c_double, C.c_uint64, vpp]),
+    "mach_sparse_device_view": (C.c_int, [vp, vpp, vpp, ip]),
+    "mach_sparse_from_device": (C.c_int, [vp, C.c_int, C.c_int, ip, C.c_int64, vp, vp, vpp]),
     "mach_session_free": (C.c_int, [vp]),
     "mach_ctx_profile": (C.c_int, [vp, C.c_int]),
     "mach_ctx_kernel_stat": (C.c_int, [vp, C.c_int, C.c_char_p, C.c_size_t, i64p, dp]),

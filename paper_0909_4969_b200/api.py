@@ -207,6 +207,21 @@ class SparseTensor:
         _check(L.lib().mach_sparse_norm(self.h, C.byref(out)))
         return out.value
 
+    def device_view(self):
+        """(idx device pointer, value device pointer, index bytes 4|8)."""
+        ip_, vp_, ib = C.c_void_p(), C.c_void_p(), C.c_int()
+        _check(L.lib().mach_sparse_device_view(self.h, C.byref(ip_), C.byref(vp_), C.byref(ib)))
+        return ip_.value, vp_.value, ib.value
+
+    @classmethod
+    def from_device(cls, dims, nnz, idx_ptr, val_ptr, dtype, ctx: Context | None = None):
+        """Copy canonical device arrays (ascending unique flat indices)."""
+        ctx = _ctx(ctx)
+        h = C.c_void_p()
+        _check(L.lib().mach_sparse_from_device(ctx.h, _DT[np.dtype(dtype)], len(dims), _dims_arr(dims), int(nnz),
+                                               C.c_void_p(idx_ptr), C.c_void_p(val_ptr), C.byref(h)))
+        return cls(h, dims, dtype, ctx)
+
     def densify(self) -> np.ndarray:
         idx, vals = self.entries()
         out = np.zeros(self.size(), dtype=np.float64)
@@ -306,6 +321,17 @@ def sparsify(t, cfg: SparsifyConfig | float = None, seed: int = 0, ctx: Context 
     _check(L.lib().mach_sparsify(d.ctx.h, d.h, float(cfg.p), int(cfg.seed) & (2**64 - 1), C.byref(h)))
     return SparseTensor(h, d.dims, d.dtype, d.ctx)
 
+
+
+def sparsify_slab(slab, global_dims, offset: int, cfg: "SparsifyConfig", ctx: Context | None = None) -> "SparseTensor":
+    """Sample the flat range [offset, offset + slab.size) of a tensor of dims
+    global_dims (a time slab): global RNG counter and global indices, so the
+    kept set equals the full tensor's restricted to the slab."""
+    d = _dense(slab, ctx)
+    h = C.c_void_p()
+    _check(L.lib().mach_sparsify_slab(d.ctx.h, d.h, len(global_dims), _dims_arr(global_dims), int(offset),
+                                      float(cfg.p), int(cfg.seed) & 0xFFFFFFFFFFFFFFFF, C.byref(h)))
+    return SparseTensor(h, global_dims, d.dtype, d.ctx)
 
 def _ranks(ranks, d):
     if len(ranks) != d:
@@ -466,6 +492,37 @@ class HooiSession:
         hm = C.c_void_p()
         _check(L.lib().mach_hooi_model(self.h, C.byref(hm)))
         return _model_from(hm)
+
+    @classmethod
+    def from_session(cls, t: "SparseTensor", ranks, init: "HooiSession"):
+        """Session on `t` starting from `init`'s current factors (no HOSVD)."""
+        hm = C.c_void_p()
+        _check(L.lib().mach_hooi_model(init.h, C.byref(hm)))
+        try:
+            h = C.c_void_p()
+            _check(L.lib().mach_hooi_begin_from(t.ctx.h, t.h, _ranks(ranks, len(t.dims)), hm, C.byref(h)))
+        finally:
+            L.lib().mach_model_free(hm)
+        self = cls.__new__(cls)
+        self.h, self.ctx, self._src = h, t.ctx, t
+        return self
+
+    def set_norm2(self, norm2: float):
+        _check(L.lib().mach_hooi_set_norm2(self.h, float(norm2)))
+
+    def mode_y(self, mode: int):
+        """TTM of the local nonzeros: (device pointer, rows, cols) of Y_(mode)."""
+        y, r, c = C.c_void_p(), C.c_int(), C.c_int()
+        _check(L.lib().mach_hooi_mode_y(self.h, int(mode), C.byref(y), C.byref(r), C.byref(c)))
+        return y.value, r.value, c.value
+
+    def mode_update(self, mode: int):
+        _check(L.lib().mach_hooi_mode_update(self.h, int(mode)))
+
+    def sweep_end(self, fit_tolerance: float = 0.0) -> bool:
+        st = C.c_int()
+        _check(L.lib().mach_hooi_sweep_end(self.h, float(fit_tolerance), C.byref(st)))
+        return bool(st.value)
 
     def ttm_bytes(self, mode: int) -> int:
         """Algorithmic bytes of one mode-`mode` TTM launch (-1 on the dense route)."""

@@ -9,6 +9,8 @@
 
 namespace machb {
 mach_sparse* sample_dense(const mach_dense* x, double p, std::uint64_t seed);
+mach_sparse* sample_slab(const mach_dense* x, const std::vector<int>& gdims, std::int64_t offset, double p,
+                         std::uint64_t seed);
 mach_model* tucker_sparse(mach_sparse* X, const std::vector<int>& ranks, bool do_hooi, int max_it, double tol);
 mach_model* tucker_dense(const mach_dense* X, const std::vector<int>& ranks, bool do_hooi, int max_it, double tol);
 double accuracy_dev(const mach_dense* t, const mach_model* m);
@@ -174,6 +176,52 @@ mach_status mach_sparsify(mach_ctx* ctx, const mach_dense* x, double p, uint64_t
         need(x, "tensor");
         need(out, "out");
         *out = sample_dense(x, p, seed);
+    });
+}
+
+mach_status mach_sparsify_slab(mach_ctx* ctx, const mach_dense* slab, int order, const int* global_dims,
+                               int64_t offset, double p, uint64_t seed, mach_sparse** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(slab, "slab");
+        need(out, "out");
+        *out = sample_slab(slab, dims_of(order, global_dims), offset, p, seed);
+    });
+}
+
+mach_status mach_sparse_device_view(const mach_sparse* s, void** idx, void** vals, int* idx_bytes) {
+    return guard([&] {
+        need(s, "tensor");
+        if (idx) *idx = s->idx;
+        if (vals) *vals = s->val;
+        if (idx_bytes) *idx_bytes = s->idx64 ? 8 : 4;
+    });
+}
+
+mach_status mach_sparse_from_device(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims, int64_t nnz,
+                                    const void* idx, const void* vals, mach_sparse** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(out, "out");
+        if (nnz < 0) throw_arg("nnz must be >= 0");
+        auto t = std::make_unique<mach_sparse>();
+        t->ctx = &ctx->c;
+        t->dtype = dtype;
+        t->dims = dims_of(order, dims);
+        t->numel = checked_size(t->dims);
+        t->idx64 = t->numel > 0xFFFFFFFFll;
+        t->nnz = nnz;
+        if (nnz > 0) {
+            need(idx, "idx");
+            need(vals, "vals");
+            const std::size_t ib = static_cast<std::size_t>(nnz) * (t->idx64 ? 8 : 4);
+            const std::size_t vb = static_cast<std::size_t>(nnz) * (dtype == MACH_F32 ? 4 : 8);
+            MB_CUDA(cudaMallocAsync(&t->idx, ib, ctx->c.stream));
+            MB_CUDA(cudaMallocAsync(&t->val, vb, ctx->c.stream));
+            MB_CUDA(cudaMemcpyAsync(t->idx, idx, ib, cudaMemcpyDeviceToDevice, ctx->c.stream));
+            MB_CUDA(cudaMemcpyAsync(t->val, vals, vb, cudaMemcpyDeviceToDevice, ctx->c.stream));
+        }
+        *out = t.release();
     });
 }
 
@@ -441,6 +489,11 @@ int session_iterations(void* s);
 double session_fit(void* s);
 bool session_stopped(void* s);
 long long session_ttm_bytes(void* s, int m);
+void* session_sparse_from(mach_sparse* X, const std::vector<int>& ranks, const mach_model* init);
+void* session_mode_y(void* s, int m, int* rows, int* cols);
+void session_mode_update(void* s, int m);
+int session_sweep_end(void* s, double tol);
+void session_set_norm2(void* s, double v);
 }  // namespace machb
 
 struct mach_session {
@@ -486,6 +539,52 @@ mach_status mach_hooi_state(mach_session* s, double* fit, int* iterations) {
         need(s, "session");
         if (fit) *fit = session_fit(s->s);
         if (iterations) *iterations = session_iterations(s->s);
+    });
+}
+
+mach_status mach_hooi_begin_from(mach_ctx* ctx, const mach_sparse* t, const int* ranks, const mach_model* init,
+                                 mach_session** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(t, "tensor");
+        need(init, "init");
+        need(out, "out");
+        auto h = std::make_unique<mach_session>();
+        h->s = session_sparse_from(const_cast<mach_sparse*>(t), ranks_of(static_cast<int>(t->dims.size()), ranks), init);
+        *out = h.release();
+    });
+}
+
+mach_status mach_hooi_set_norm2(mach_session* s, double norm2) {
+    return guard([&] {
+        need(s, "session");
+        session_set_norm2(s->s, norm2);
+    });
+}
+
+mach_status mach_hooi_mode_y(mach_session* s, int mode, void** y, int* rows, int* cols) {
+    return guard([&] {
+        need(s, "session");
+        need(y, "y");
+        need(rows, "rows");
+        need(cols, "cols");
+        *y = session_mode_y(s->s, mode, rows, cols);
+    });
+}
+
+mach_status mach_hooi_mode_update(mach_session* s, int mode) {
+    return guard([&] {
+        need(s, "session");
+        session_mode_update(s->s, mode);
+    });
+}
+
+mach_status mach_hooi_sweep_end(mach_session* s, double fit_tolerance, int* stopped) {
+    return guard([&] {
+        need(s, "session");
+        if (std::isnan(fit_tolerance)) throw_arg("fit_tolerance must be a number");
+        const int st = session_sweep_end(s->s, fit_tolerance);
+        if (stopped) *stopped = st;
     });
 }
 

@@ -62,6 +62,7 @@ __device__ __forceinline__ bool is_finite_bits(double x) {
 // (16-bit fields; a block-wide per-v total is <= kThreads * VEC <= 1024).
 template <typename T, typename IdxT>
 __global__ void __launch_bounds__(kThreads) sample_kernel(const T* __restrict__ x, std::int64_t numel,
+                                                          std::int64_t gofs,  // global flat index of x[0]
                                                           std::uint64_t seed, std::uint64_t thr_shift,
                                                           int keep_all, double p, IdxT* __restrict__ out_idx,
                                                           T* __restrict__ out_val, std::int64_t capacity,
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(const T* __restrict__ 
             for (int j = 0; j < VEC; ++j) vals[v][j] = (e0 + j < numel) ? x[e0 + j] : T(0);
         }
         // z_j = seed + (i + 1) * golden for consecutive i: incremental adds.
-        std::uint64_t z = seed + (static_cast<std::uint64_t>(e0) + 1ull) * 0x9E3779B97F4A7C15ULL;
+        std::uint64_t z = seed + (static_cast<std::uint64_t>(gofs + e0) + 1ull) * 0x9E3779B97F4A7C15ULL;
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
             const T xv = vals[v][j];
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(const T* __restrict__ 
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
             if ((keep_bits >> (v * VEC + j)) & 1u) {
-                s_idx[o] = static_cast<IdxT>(e0 + j);
+                s_idx[o] = static_cast<IdxT>(gofs + e0 + j);
                 s_val[o] = static_cast<T>(__ddiv_rn(static_cast<double>(vals[v][j]), p));
                 ++o;
             }
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(const T* __restrict__ 
 }
 
 template <typename T, typename IdxT>
-std::int64_t launch_sample(Ctx* ctx, const T* x, std::int64_t numel, std::uint64_t seed, double p,
+std::int64_t launch_sample(Ctx* ctx, const T* x, std::int64_t numel, std::int64_t gofs, std::uint64_t seed, double p,
                            std::int64_t capacity, IdxT* out_idx, T* out_val, int* flags_host) {
     constexpr int VEC = Vec<T>::n;
     constexpr int TILE = kThreads * 4 * VEC;
@@ -223,7 +224,7 @@ std::int64_t launch_sample(Ctx* ctx, const T* x, std::int64_t numel, std::uint64
         attr = true;
     }
     if (ntiles > 0)
-        MB_LAUNCH(ctx, (sample_kernel<T, IdxT>), static_cast<unsigned>(ntiles), kThreads, smem, x, numel, seed, thr,
+        MB_LAUNCH(ctx, (sample_kernel<T, IdxT>), static_cast<unsigned>(ntiles), kThreads, smem, x, numel, gofs, seed, thr,
                   keep_all ? 1 : 0, p, out_idx, out_val, capacity, status, ticket, total, flags);
     long long tot = 0;
     int fl = 0;
@@ -236,16 +237,22 @@ std::int64_t launch_sample(Ctx* ctx, const T* x, std::int64_t numel, std::uint64
 
 }  // namespace
 
-// Host entry: returns a new canonical sparse tensor in HBM.
-mach_sparse* sample_dense(const mach_dense* x, double p, std::uint64_t seed) {
+// Host entry: returns a new canonical sparse tensor in HBM.  With a slab, x
+// holds the flat range [offset, offset + x->numel) of a tensor of dims gdims
+// (a time slab under first-mode-fastest layout): the RNG counter and the
+// stored index are the global flat index, so the kept set is exactly the
+// full tensor's restricted to the slab.
+mach_sparse* sample_slab(const mach_dense* x, const std::vector<int>& gdims, std::int64_t offset, double p,
+                         std::uint64_t seed) {
     if (!(p > 0.0 && p <= 1.0)) throw_arg("p must be in (0, 1]");
     Ctx* ctx = x->ctx;
     auto out = std::make_unique<mach_sparse>();
     out->ctx = ctx;
     out->dtype = x->dtype;
-    out->dims = x->dims;
-    out->numel = x->numel;
-    out->idx64 = x->numel > 0xFFFFFFFFll;
+    out->dims = gdims;
+    out->numel = checked_size(gdims);
+    if (offset < 0 || offset + x->numel > out->numel) throw Error(MACH_ERR_SHAPE, "slab exceeds the global tensor");
+    out->idx64 = out->numel > 0xFFFFFFFFll;
     const int isz = out->idx64 ? 8 : 4;
     const int vsz = dtype_size(x->dtype);
     const double mean = p * static_cast<double>(x->numel);
@@ -261,21 +268,23 @@ mach_sparse* sample_dense(const mach_dense* x, double p, std::uint64_t seed) {
         std::int64_t nnz = 0;
         if (x->dtype == MACH_F32) {
             if (out->idx64)
-                nnz = launch_sample<float, unsigned long long>(ctx, static_cast<const float*>(x->data), x->numel, seed, p,
-                                                               cap, static_cast<unsigned long long*>(di),
+                nnz = launch_sample<float, unsigned long long>(ctx, static_cast<const float*>(x->data), x->numel, offset,
+                                                               seed, p, cap, static_cast<unsigned long long*>(di),
                                                                static_cast<float*>(dv), &flags);
             else
-                nnz = launch_sample<float, unsigned int>(ctx, static_cast<const float*>(x->data), x->numel, seed, p, cap,
-                                                         static_cast<unsigned int*>(di), static_cast<float*>(dv), &flags);
+                nnz = launch_sample<float, unsigned int>(ctx, static_cast<const float*>(x->data), x->numel, offset, seed,
+                                                         p, cap, static_cast<unsigned int*>(di), static_cast<float*>(dv),
+                                                         &flags);
         } else {
             if (out->idx64)
-                nnz = launch_sample<double, unsigned long long>(ctx, static_cast<const double*>(x->data), x->numel, seed,
-                                                                p, cap, static_cast<unsigned long long*>(di),
+                nnz = launch_sample<double, unsigned long long>(ctx, static_cast<const double*>(x->data), x->numel,
+                                                                offset, seed, p, cap,
+                                                                static_cast<unsigned long long*>(di),
                                                                 static_cast<double*>(dv), &flags);
             else
-                nnz = launch_sample<double, unsigned int>(ctx, static_cast<const double*>(x->data), x->numel, seed, p,
-                                                          cap, static_cast<unsigned int*>(di), static_cast<double*>(dv),
-                                                          &flags);
+                nnz = launch_sample<double, unsigned int>(ctx, static_cast<const double*>(x->data), x->numel, offset,
+                                                          seed, p, cap, static_cast<unsigned int*>(di),
+                                                          static_cast<double*>(dv), &flags);
         }
         if (flags & 1) {
             if (di) cudaFreeAsync(di, ctx->stream);
@@ -295,5 +304,7 @@ mach_sparse* sample_dense(const mach_dense* x, double p, std::uint64_t seed) {
     }
     throw Error(MACH_ERR_INTERNAL, "sampler capacity retry failed");
 }
+
+mach_sparse* sample_dense(const mach_dense* x, double p, std::uint64_t seed) { return sample_slab(x, x->dims, 0, p, seed); }
 
 }  // namespace machb

@@ -324,6 +324,21 @@ struct SessionBase {
     virtual ~SessionBase() = default;
     virtual void sweep() = 0;                       // one sweep: all modes, core, fit
     virtual long long ttm_bytes(int) const { return -1; }  // algorithmic bytes of one mode-n TTM launch
+    // split sweep for an external reduction between the TTM and the basis
+    // (time-slab sharding): Y_(m) of the local nonzeros, then the update
+    virtual void* ext_mode_y(int, int*, int*) { throw Error(MACH_ERR_ARGUMENT, "split sweeps need a sparse session"); }
+    virtual void ext_mode_update(int) { throw Error(MACH_ERR_ARGUMENT, "split sweeps need a sparse session"); }
+    virtual void ext_core_fit() { throw Error(MACH_ERR_ARGUMENT, "split sweeps need a sparse session"); }
+    virtual void set_norm2(double) { throw Error(MACH_ERR_ARGUMENT, "split sweeps need a sparse session"); }
+    int ext_sweep_end(double tol) {
+        ext_core_fit();
+        sweep_ms.push_back(0.0);
+        sweep_fits.push_back(fit);
+        ++iterations;
+        if (tol >= 0.0 && fit - prev_fit < tol) stopped = true;
+        prev_fit = fit;
+        return stopped ? 1 : 0;
+    }
     virtual const double* core_dev() const = 0;
     double* sv_at(int m) {
         int o = 0;
@@ -479,7 +494,7 @@ struct SparseSession : SessionBase {
         sync(ctx);
         const double e2 = sc[0] - sc[1];
         const double guard = std::is_same<T, double>::value ? 1e-6 : 1e-3;
-        if (sc[0] > 0.0 && e2 <= guard * sc[0]) {
+        if (!sharded && sc[0] > 0.0 && e2 <= guard * sc[0]) {
             DBuf<double> rec = reconstruct_dev(ctx, core.get(), ranks, dims, fs.U);
             scatter_sub<T>(ctx, X, rec.get());
             sumsq<double>(ctx, rec.get(), static_cast<long long>(rec.n), fs.red.get(), fs.scal.get() + 2);
@@ -490,7 +505,26 @@ struct SparseSession : SessionBase {
         }
         return fit_from(sc[0], e2);
     }
+    bool sharded = false;  // |X|^2 set externally; no local entrywise residual guard
     void begin(mach_sparse* sp, const std::vector<int>& rk) {
+        setup(sp, rk);
+        hosvd_init();
+    }
+    // start from given factors (a replicated HOSVD) instead of computing them
+    void begin_from(mach_sparse* sp, const std::vector<int>& rk, const mach_model* init) {
+        setup(sp, rk);
+        if (init->order != d || init->ranks != ranks || init->dims != dims)
+            throw Error(MACH_ERR_SHAPE, "initial model does not match the tensor and ranks");
+        for (int m = 0; m < d; ++m) {
+            to_device(ctx, fs.U[static_cast<std::size_t>(m)].get(), init->factors[static_cast<std::size_t>(m)].data(),
+                      init->factors[static_cast<std::size_t>(m)].size());
+            refresh(m);
+        }
+        fit = prev_fit = init->fit;
+        sweep_fits.assign(1, fit);
+        warnings = init->warnings;
+    }
+    void setup(mach_sparse* sp, const std::vector<int>& rk) {
         X = sp;
         init_common(sp->ctx, sp->dims, rk);
         Timer tm(ctx);
@@ -526,7 +560,9 @@ struct SparseSession : SessionBase {
         Y.alloc(ctx, maxY);
         core.alloc(ctx, static_cast<std::size_t>(checked_size(ranks)));
         setup_ms = tm.stop_ms();
-
+    }
+    void hosvd_init() {
+        Timer tm(ctx);
         // ---- HOSVD: sparse_mode_basis per mode (sparse_kernels.cpp:82-90) ----
         tm.start();
         const long long numel = X->numel;
@@ -565,21 +601,46 @@ struct SparseSession : SessionBase {
         hosvd_ms = tm.stop_ms();
         sweep_fits.assign(1, fit);
     }
-    void sweep() override {
+    // factor update of mode i from Y (tucker.cpp:182-193)
+    void mode_update(int i) {
         static const bool nofuse = std::getenv("MACH_NO_FUSED_BASIS") != nullptr;
+        const std::size_t si = static_cast<std::size_t>(i);
+        if (!nofuse && lsb_fused<T>(ctx, Y.get(), dims[si], C[si], ranks[si], fs.U[si].get(), sv_at(i),
+                                    fs.st.get() + 3 * i, &warm[si], fs.U[si].get(), Ur[si].get(),
+                                    ttm_stride(ranks[si], sizeof(T))))
+            return;
+        lsb_device<T>(ctx, Y.get(), dims[si], C[si], ranks[si], fs.U[si].get(), sv_at(i), fs.st.get() + 3 * i,
+                      &warm[si], fs.U[si].get());
+        refresh(i);
+    }
+    void sweep() override {
         for (int i = 0; i < d; ++i) {
-            const std::size_t si = static_cast<std::size_t>(i);
             mode_y(i);
-            if (!nofuse && lsb_fused<T>(ctx, Y.get(), dims[si], C[si], ranks[si], fs.U[si].get(), sv_at(i),
-                                        fs.st.get() + 3 * i, &warm[si], fs.U[si].get(), Ur[si].get(),
-                                        ttm_stride(ranks[si], sizeof(T))))
-                continue;
-            lsb_device<T>(ctx, Y.get(), dims[si], C[si], ranks[si], fs.U[si].get(), sv_at(i), fs.st.get() + 3 * i,
-                          &warm[si], fs.U[si].get());
-            refresh(i);
+            mode_update(i);
         }
         fit = core_and_fit();
         warnings = read_warnings(ctx, fs.st, ranks, all);
+    }
+    void* ext_mode_y(int m, int* rows, int* cols) override {
+        if (m < 0 || m >= d) throw_arg("mode out of range");
+        mode_y(m);
+        *rows = dims[static_cast<std::size_t>(m)];
+        *cols = C[static_cast<std::size_t>(m)];
+        return Y.get();
+    }
+    void ext_mode_update(int m) override {
+        if (m < 0 || m >= d) throw_arg("mode out of range");
+        mode_update(m);
+    }
+    void ext_core_fit() override {
+        fit = core_and_fit();
+        warnings = read_warnings(ctx, fs.st, ranks, all);
+    }
+    void set_norm2(double v) override {
+        if (!(v >= 0.0)) throw_arg("norm2 must be >= 0");
+        normX2 = v;
+        sharded = true;
+        to_device(ctx, fs.scal.get(), &v, 1);
     }
     const double* core_dev() const override { return core.get(); }
     // bytes one mode-n TTM launch must move: per nonzero the inner index and
@@ -627,6 +688,20 @@ void* session_sparse(mach_sparse* X, const std::vector<int>& ranks) {
     return static_cast<SessionBase*>(s.release());
 }
 
+void* session_sparse_from(mach_sparse* X, const std::vector<int>& ranks, const mach_model* init) {
+    check_ranks(X->dims, ranks);
+    if (!sparse_fast_path_ok(X->dims, ranks))
+        throw Error(MACH_ERR_ARGUMENT, "split sweeps need the sparse route (order <= 3, ranks <= 32)");
+    if (X->dtype == MACH_F32) {
+        auto s = std::make_unique<SparseSession<float>>();
+        s->begin_from(X, ranks, init);
+        return static_cast<SessionBase*>(s.release());
+    }
+    auto s = std::make_unique<SparseSession<double>>();
+    s->begin_from(X, ranks, init);
+    return static_cast<SessionBase*>(s.release());
+}
+
 void* session_dense(const mach_dense* X, const std::vector<int>& ranks) {
     check_ranks(X->dims, ranks);
     if (X->dtype == MACH_F32) {
@@ -648,6 +723,10 @@ int session_iterations(void* s) { return S(s)->iterations; }
 double session_fit(void* s) { return S(s)->fit; }
 bool session_stopped(void* s) { return S(s)->stopped; }
 long long session_ttm_bytes(void* s, int m) { return S(s)->ttm_bytes(m); }
+void* session_mode_y(void* s, int m, int* rows, int* cols) { return S(s)->ext_mode_y(m, rows, cols); }
+void session_mode_update(void* s, int m) { S(s)->ext_mode_update(m); }
+int session_sweep_end(void* s, double tol) { return S(s)->ext_sweep_end(tol); }
+void session_set_norm2(void* s, double v) { S(s)->set_norm2(v); }
 
 mach_model* tucker_sparse(mach_sparse* X, const std::vector<int>& ranks, bool do_hooi, int max_it, double tol) {
     check_ranks(X->dims, ranks);
