@@ -104,8 +104,24 @@ struct Sub {
             for (int t = 0; t < CT; ++t) c[t][0] = c[t][1] = 0.0;
             const double* ga = G + (rt * 8 + gr) + tq * ldg;
             const double* xb = IN + tq * XS + gr;
-#pragma unroll 2
-            for (int k0 = 0; k0 < npad; k0 += 4) {
+            // batches of KB k-steps: all operand loads of a batch are issued
+            // before its MMAs (G may live in global memory for large n)
+            constexpr int KB = CT <= 2 ? 8 : 4;
+            int k0 = 0;
+            for (; k0 + 4 * KB <= npad; k0 += 4 * KB) {
+                double av[KB], bv[KB][CT];
+#pragma unroll
+                for (int u = 0; u < KB; ++u) {
+                    av[u] = ga[(k0 + 4 * u) * ldg];
+#pragma unroll
+                    for (int t = 0; t < CT; ++t) bv[u][t] = xb[(k0 + 4 * u) * XS + t * 8];
+                }
+#pragma unroll
+                for (int u = 0; u < KB; ++u)
+#pragma unroll
+                    for (int t = 0; t < CT; ++t) dmma(c[t][0], c[t][1], av[u], bv[u][t]);
+            }
+            for (; k0 < npad; k0 += 4) {
                 const double av = ga[k0 * ldg];
 #pragma unroll
                 for (int t = 0; t < CT; ++t) dmma(c[t][0], c[t][1], av, xb[k0 * XS + t * 8]);
@@ -510,7 +526,9 @@ struct Sub {
 template <int B>
 struct SubWs {
     double *H, *W, *S, *Z, *Q, *Hc, *th, *rinv, *coef, *red, *X, *AX, *Y0, *Y1;
-    __device__ SubWs(double* sm, int npad) {
+    // blocks: if non-null, the four n x B blocks live there (global memory,
+    // for n too large for shared memory) instead of after the small matrices
+    __device__ SubWs(double* sm, int npad, double* blocks = nullptr) {
         constexpr int HS = Sub<B>::HS, XS = Sub<B>::XS;
         H = sm;
         W = H + B * HS;
@@ -522,14 +540,14 @@ struct SubWs {
         rinv = th + kMaxB;
         coef = rinv + kMaxB;
         red = coef + kMaxB;
-        X = red + 32;
+        X = blocks ? blocks : red + 32;
         AX = X + npad * XS;
         Y0 = AX + npad * XS;
         Y1 = Y0 + npad * XS;
     }
-    __host__ __device__ static std::size_t doubles(int npad) {
-        return 6ull * B * Sub<B>::HS + 3 * kMaxB + 32 + 4ull * npad * Sub<B>::XS;
-    }
+    __host__ __device__ static std::size_t doubles(int npad) { return small_doubles() + block_doubles(npad); }
+    __host__ __device__ static std::size_t small_doubles() { return 6ull * B * Sub<B>::HS + 3 * kMaxB + 32; }
+    __host__ __device__ static std::size_t block_doubles(int npad) { return 4ull * npad * Sub<B>::XS; }
 };
 
 #define MB_STAMP(tag)                                                                  \

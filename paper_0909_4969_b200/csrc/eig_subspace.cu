@@ -31,11 +31,11 @@ namespace {
 // status: [0] converged, [1] zero matrix, [2] iterations used.  Gw: global
 // workspace (npad x ldg doubles) for G when it does not fit shared memory.
 template <int B>
-__global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __restrict__ Gin, int n, int k, int m,
+__global__ void __launch_bounds__(kThreads, 1) eig_subspace_kernel(const double* __restrict__ Gin, int n, int k, int m,
                                                                 int maxit, double tol, const double* X0, int x0_cols,
                                                                 double* Xkeep,  // may alias X0
                                                                 double* __restrict__ V, double* __restrict__ sig,
-                                                                int* __restrict__ status, double* Gw,
+                                                                int* __restrict__ status, double* Gw, double* Bw,
                                                                 long long* __restrict__ tstamp) {
     using SB = Sub<B>;
     constexpr int XS = SB::XS;
@@ -46,8 +46,10 @@ __global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __
     __shared__ int flag;
     const int npad = (n + 7) & ~7;
     const int ldg = frag_stride(npad);
-    double* G = Gw ? Gw : (sm + SubWs<B>::doubles(npad));
-    double* red = SubWs<B>(sm, npad).red;
+    // shared memory: [small matrices][blocks unless Bw][G unless Gw]
+    const std::size_t blk_sm = Bw ? 0 : SubWs<B>::block_doubles(npad);
+    double* G = Gw ? Gw : (sm + SubWs<B>::small_doubles() + blk_sm);
+    double* red = SubWs<B>(sm, npad, Bw).red;
 
     // ---- load G padded to npad x npad (zeros outside n x n).  Every
     // producer of G (gram_mma_kernel, the fixed-point sparse Grams) writes it
@@ -91,7 +93,7 @@ __global__ void __launch_bounds__(kThreads) eig_subspace_kernel(const double* __
 
     int it = 0;
     bool conv = false;
-    SubWs<B> ws(sm, npad);
+    SubWs<B> ws(sm, npad, Bw);
     double* X = subspace_core<B>(ws, G, ldg, n, k, m, maxit, tol, X0, x0_cols, conv, it, &flag, tstamp, ns_);
     const double* th = ws.th;
     if (tstamp && threadIdx.x == 0) tstamp[238] = clock64();
@@ -109,9 +111,10 @@ std::size_t g_doubles(int n) {
 }
 
 template <int B>
-std::size_t subspace_smem(int n, bool g_smem) {
-    const std::size_t npad = (static_cast<std::size_t>(n) + 7) & ~std::size_t(7);
-    std::size_t w = SubWs<B>::doubles(static_cast<int>(npad));
+std::size_t subspace_smem(int n, bool g_smem, bool b_smem) {
+    const int npad = (n + 7) & ~7;
+    std::size_t w = SubWs<B>::small_doubles();
+    if (b_smem) w += SubWs<B>::block_doubles(npad);
     if (g_smem) w += g_doubles(n);
     return w * sizeof(double);
 }
@@ -121,8 +124,12 @@ constexpr std::size_t kSmemCap = 200 * 1024;
 template <int B>
 bool launch_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, double* V,
                      double* sig, int* status) {
-    const bool g_smem = subspace_smem<B>(n, true) <= kSmemCap;
-    const std::size_t smem = subspace_smem<B>(n, g_smem);
+    // shared memory first for G and the blocks; what does not fit lives in
+    // global memory (L2-resident at these sizes): G first, then the blocks
+    bool g_smem = true, b_smem = true;
+    if (subspace_smem<B>(n, true, true) > kSmemCap) g_smem = false;
+    if (subspace_smem<B>(n, g_smem, true) > kSmemCap) b_smem = false;
+    const std::size_t smem = subspace_smem<B>(n, g_smem, b_smem);
     if (smem > kSmemCap) return false;
     static bool attr = false;
     if (!attr) {
@@ -130,8 +137,9 @@ bool launch_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, 
                                      static_cast<int>(kSmemCap)));
         attr = true;
     }
-    DBuf<double> gw;
+    DBuf<double> gw, bw;
     if (!g_smem) gw.alloc(ctx, g_doubles(n));
+    if (!b_smem) bw.alloc(ctx, SubWs<B>::block_doubles((n + 7) & ~7));
     static const bool dbg = std::getenv("MACH_DEBUG_EIG_T") != nullptr;
     DBuf<long long> ts;
     if (dbg) {
@@ -139,12 +147,12 @@ bool launch_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, 
         ts.zero(ctx);
     }
     MB_LAUNCH(ctx, eig_subspace_kernel<B>, 1, kThreads, smem, G, n, k, 4, 40, 1e-12, X0, x0_cols, Xkeep, V, sig, status,
-              g_smem ? nullptr : gw.get(), dbg ? ts.get() : nullptr);
+              g_smem ? nullptr : gw.get(), b_smem ? nullptr : bw.get(), dbg ? ts.get() : nullptr);
     if (dbg) {
         long long h[240];
         to_host(ctx, h, ts.get(), 240);
         sync(ctx);
-        std::fprintf(stderr, "[eig-t] n=%d B=%d gsmem=%d:", n, B, g_smem ? 1 : 0);
+        std::fprintf(stderr, "[eig-t] n=%d B=%d gsmem=%d bsmem=%d:", n, B, g_smem ? 1 : 0, b_smem ? 1 : 0);
         long long t_end = h[1];
         for (int i = 1; i < 118 && h[2 * i + 1]; ++i) {
             std::fprintf(stderr, " %lld:%.1f", h[2 * i], (h[2 * i + 1] - h[2 * i - 1]) * 1e-3);

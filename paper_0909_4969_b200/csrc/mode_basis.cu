@@ -73,7 +73,7 @@ struct MBLayout {
 };
 
 template <int B, typename T>
-__global__ void __launch_bounds__(kThreads) mode_basis_kernel(MBArgs<T> A, long long* tstamp) {
+__global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, long long* tstamp) {
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) double sm[];
     const int rank = static_cast<int>(cluster.block_rank());
