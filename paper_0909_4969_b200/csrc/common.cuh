@@ -70,8 +70,16 @@ struct Ctx {
 // Every kernel launch in the library goes through this so the bench can
 // report how many of our kernels ran (gpu_launches) and, when profiling is on,
 // each kernel's device time from CUDA events on the launching stream.
+inline bool max_carveout(const void* f) {
+    return cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess;
+}
+
+// Every kernel prefers the maximum shared-memory carve-out: the big kernels
+// need it and a uniform carve-out avoids SM reconfiguration between launches.
 #define MB_LAUNCH(ctx, kernel, grid, block, smem, ...)                                               \
     do {                                                                                             \
+        static const bool carve_ = ::machb::max_carveout(reinterpret_cast<const void*>(kernel));     \
+        (void)carve_;                                                                                \
         ::machb::PendingEvent pe_{#kernel, nullptr, nullptr};                                        \
         if ((ctx)->profile) {                                                                        \
             MB_CUDA(cudaEventCreate(&pe_.a));                                                        \
@@ -90,6 +98,8 @@ struct Ctx {
 // Same for an extended launch (clusters): cfgp is a cudaLaunchConfig_t*.
 #define MB_LAUNCH_EX(ctx, name, cfgp, kernel, ...)                                                 \
     do {                                                                                             \
+        static const bool carve_ = ::machb::max_carveout(reinterpret_cast<const void*>(kernel));     \
+        (void)carve_;                                                                                \
         ::machb::PendingEvent pe_{name, nullptr, nullptr};                                           \
         if ((ctx)->profile) {                                                                        \
             MB_CUDA(cudaEventCreate(&pe_.a));                                                        \

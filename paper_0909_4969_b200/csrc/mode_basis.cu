@@ -32,7 +32,7 @@ namespace machb {
 
 namespace {
 
-constexpr int kCL = 8;     // cluster size (portable)
+constexpr int kCL = 16;    // cluster size (non-portable maximum; 8 when 16 cannot be scheduled)
 constexpr int kMaxK = 32;  // ranks handled by the fused route
 
 template <typename T>
@@ -85,6 +85,11 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gr = lane >> 2, tq = lane & 3;
     int ns_ = 0;
+    if (tstamp && threadIdx.x == 0) {  // per-CTA entry times at [160 + rank]
+        long long t_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+        tstamp[160 + rank] = t_;
+    }
     if (rank != 0) tstamp = nullptr;  // the stamps follow CTA 0
     MB_STAMP(0);
 
@@ -161,8 +166,13 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
         for (int e = e0 + threadIdx.x; e < e1; e += kThreads) {
             const int r = e % npad, c = e / npad;
             const int off = r + c * ldg;
+            double v[16];
+#pragma unroll
+            for (int q = 1; q < 16; ++q)  // all remote loads in flight, then a fixed-order sum
+                v[q] = q < CL ? cluster.map_shared_rank(P, q)[off] : 0.0;
             double s = 0.0;
-            for (int q = 1; q < CL; ++q) s += cluster.map_shared_rank(P, q)[off];
+#pragma unroll
+            for (int q = 1; q < 16; ++q) s += v[q];
             G0[off] = s;
         }
     }
@@ -280,43 +290,50 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
     auto reduce_factor = [&](bool tests) -> bool {
         for (int e = threadIdx.x; e < k * k; e += kThreads) {
             const int i = e % k, j = e / k;
+            double v[16];
+#pragma unroll
+            for (int q = 1; q < 16; ++q)  // all remote loads in flight, then a fixed-order sum
+                v[q] = q < CL ? cluster.map_shared_rank(Mk, q)[i + j * kMaxK] : 0.0;
             double s = 0.0;
-            for (int q = 1; q < CL; ++q) s += cluster.map_shared_rank(Mk, q)[i + j * kMaxK];
+#pragma unroll
+            for (int q = 1; q < 16; ++q) s += v[q];
             Rk[i + j * kMaxK] = s;
         }
         __syncthreads();
+        MB_STAMP(42);
         if (warp == 0) {
+            // Cholesky of M (upper R in Rk), then R^{-1} into Mk; compact loops
+            // (code size matters more than arithmetic for this k x k work)
             int good = 1;
             const double floor = A.sig[0] * 1e-6;  // kRankFloor (linalg_internal.hpp:23)
-            if (lane < k) dg[lane] = sqrt(fmax(0.0, Rk[lane + lane * kMaxK]));
+            if (lane < k) dg[lane] = sqrt(fmax(0.0, Rk[lane + lane * kMaxK]));  // ||w_lane||
             __syncwarp();
             for (int j = 0; j < k; ++j) {
                 const double d = Rk[j + j * kMaxK];
                 if (!(d > 0.0)) { good = 0; break; }
-                const double rjj = sqrt(d);
+                const double rjj = sqrt(d), inv = 1.0 / rjj;
                 if (tests && (!(dg[j] > floor) || !(rjj > 1e-3 * dg[j]))) good = 0;  // kCollapseFloor
                 __syncwarp();
-                for (int m = j + lane; m < k; m += 32) Rk[j + m * kMaxK] = (m == j) ? rjj : Rk[j + m * kMaxK] / rjj;
+                for (int m = j + lane; m < k; m += 32) Rk[j + m * kMaxK] = (m == j) ? rjj : Rk[j + m * kMaxK] * inv;
                 __syncwarp();
-                const int rem = k - j - 1;
-                for (int e = lane; e < rem * rem; e += 32) {
-                    const int l = j + 1 + e % rem, m = j + 1 + e / rem;
-                    if (l <= m) Rk[l + m * kMaxK] -= Rk[j + l * kMaxK] * Rk[j + m * kMaxK];
-                }
+                for (int l = j + 1; l < k; ++l)
+                    for (int m = l + lane; m < k; m += 32) Rk[l + m * kMaxK] -= Rk[j + l * kMaxK] * Rk[j + m * kMaxK];
                 __syncwarp();
             }
             if (lane == 0) flagw = good;
+            if (good && lane < k) dg[lane] = 1.0 / Rk[lane + lane * kMaxK];
             __syncwarp();
             if (good && lane < k) {  // lane c: column c of R^{-1} into Mk
                 const int c = lane;
                 for (int r = k - 1; r >= 0; --r) {
                     double v = (r == c) ? 1.0 : 0.0;
                     for (int p = r + 1; p <= c; ++p) v -= Rk[r + p * kMaxK] * Mk[p + c * kMaxK];
-                    Mk[r + c * kMaxK] = (r <= c) ? v / Rk[r + r * kMaxK] : 0.0;
+                    Mk[r + c * kMaxK] = (r <= c) ? v * dg[r] : 0.0;
                 }
             }
         }
         __syncthreads();
+        MB_STAMP(43);
         if (!flagw) return false;
         for (int e = threadIdx.x; e < k * k; e += kThreads) Rk[e % k + (e / k) * kMaxK] = Mk[e % k + (e / k) * kMaxK];
         __syncthreads();
@@ -351,17 +368,58 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
         Wt = tmp;
     };
 
-    // pass 1 (with the reference's rank and collapse tests)
+    // W = Y V has W^T W = V^T G V = diag(theta) up to the eigensolver's
+    // certificate, so the reference's twice Gram-Schmidt reduces to column
+    // normalisation: CTA 0 reduces the k x k Gram of W and, when every
+    // normalised off-diagonal is <= 1e-10 (and the rank floor holds), the row
+    // blocks just scale by 1 / ||w_j|| (one pass).  Otherwise CholQR2 with the
+    // reference's rank and collapse tests runs (two passes).
+    auto diag_fast = [&]() -> bool {  // CTA 0, after the Grams are final
+        for (int e = threadIdx.x; e < k * k; e += kThreads) {
+            const int i = e % k, j = e / k;
+            double v[16];
+#pragma unroll
+            for (int q = 1; q < 16; ++q) v[q] = q < CL ? cluster.map_shared_rank(Mk, q)[i + j * kMaxK] : 0.0;
+            double s = 0.0;
+#pragma unroll
+            for (int q = 1; q < 16; ++q) s += v[q];
+            Rk[i + j * kMaxK] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x < k) dg[threadIdx.x] = sqrt(fmax(0.0, Rk[threadIdx.x + threadIdx.x * kMaxK]));
+        if (threadIdx.x == 0) flagw = 1;
+        __syncthreads();
+        const double floor = A.sig[0] * 1e-6;  // kRankFloor (linalg_internal.hpp:23)
+        for (int e = threadIdx.x; e < k * k; e += kThreads) {
+            const int i = e % k, j = e / k;
+            const bool bad = (i == j) ? !(dg[i] > floor) : !(fabs(Rk[i + j * kMaxK]) <= 1e-10 * dg[i] * dg[j]);
+            if (bad) flagw = 0;
+        }
+        __syncthreads();
+        const bool ok = flagw != 0;
+        __syncthreads();
+        if (ok)
+            for (int e = threadIdx.x; e < k * k; e += kThreads) {
+                const int i = e % k, j = e / k;
+                Rk[i + j * kMaxK] = (i == j) ? 1.0 / dg[i] : 0.0;
+            }
+        __syncthreads();
+        return ok;
+    };
+
     if (rank > 0) block_gram(Wb);
     cluster.sync();  // #4
+    MB_STAMP(4);
     if (rank == 0) {
-        const bool ok = reduce_factor(true);
-        if (threadIdx.x == 0) mflag = ok ? 0 : 1;
+        const bool fast = diag_fast();
+        const bool ok = fast || reduce_factor(true);
+        if (threadIdx.x == 0) mflag = fast ? 5 : (ok ? 0 : 1);
         __syncthreads();
     }
     cluster.sync();  // #5
     MB_STAMP(5);
-    if (*cluster.map_shared_rank(&mflag, 0) == 1) {  // basis fallback: hand W over
+    const int pmode = *cluster.map_shared_rank(&mflag, 0);
+    if (pmode == 1) {  // basis fallback: hand W over
         if (rank > 0)
             for (int e = threadIdx.x; e < nr * k; e += kThreads) {
                 const int i = e % nr, j = e / nr;
@@ -371,17 +429,21 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
         cluster.sync();
         return;
     }
-    if (rank > 0) {
-        apply_rinv();
-        block_gram(Wb);
+    if (pmode != 5) {  // CholQR2, pass 2
+        if (rank > 0) {
+            apply_rinv();
+            block_gram(Wb);
+        }
+        cluster.sync();  // #6
+        MB_STAMP(6);
+        if (rank == 0) {
+            const bool ok = reduce_factor(false);
+            if (threadIdx.x == 0 && !ok) mflag = 4;  // pass 2 cannot fail after pass 1; guard anyway
+            __syncthreads();
+        }
+        cluster.sync();  // #7
+        MB_STAMP(7);
     }
-    cluster.sync();  // #6
-    if (rank == 0) {
-        const bool ok = reduce_factor(false);
-        if (threadIdx.x == 0 && !ok) mflag = 4;  // pass 2 cannot fail after pass 1; guard anyway
-        __syncthreads();
-    }
-    cluster.sync();  // #7
     if (rank > 0) {
         apply_rinv();
         // canonical sign vote: largest |u| per column, lowest row on ties (linalg.cpp:18-32)
@@ -424,6 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
         }
     }
     cluster.sync();  // #9
+    MB_STAMP(9);
     if (rank > 0) {
         const double* s0 = cluster.map_shared_rank(sgn, 0);
         if (threadIdx.x < k) dg[threadIdx.x] = s0[threadIdx.x];
@@ -449,7 +512,8 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
 
 template <int B, typename T>
 bool launch_mode_basis(Ctx* ctx, MBArgs<T> A) {
-    const int CL = kCL;
+    static const int cl_env = std::getenv("MACH_MB_CLUSTER") ? std::atoi(std::getenv("MACH_MB_CLUSTER")) : kCL;
+    const int CL = cl_env;
     A.ch = ((A.rows + CL - 2) / (CL - 1) + 3) & ~3;
     auto kern = mode_basis_kernel<B, T>;
     static int dyn_max = -1;
@@ -460,6 +524,7 @@ bool launch_mode_basis(Ctx* ctx, MBArgs<T> A) {
         MB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
         dyn_max = optin - static_cast<int>(fa.sharedSizeBytes);
         MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max));
+        MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     }
     const std::size_t smem = MBLayout<B>::bytes(A.n, A.ch);
     if (smem > static_cast<std::size_t>(dyn_max)) return false;
@@ -482,15 +547,31 @@ bool launch_mode_basis(Ctx* ctx, MBArgs<T> A) {
         tsb.zero(ctx);
     }
     long long* ts = dbg ? tsb.get() : nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (dbg) {
+        cudaEventCreate(&ev0);
+        cudaEventCreate(&ev1);
+        cudaEventRecord(ev0, ctx->stream);
+    }
     MB_LAUNCH_EX(ctx, "mode_basis_kernel<B, T>", &cfg, kern, A, ts);
     if (dbg) {
+        cudaEventRecord(ev1, ctx->stream);
+        cudaEventSynchronize(ev1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        std::fprintf(stderr, "[mb-t] event %.1fus\n", ms * 1e3);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
         long long h[240];
         to_host(ctx, h, tsb.get(), 240);
         sync(ctx);
         std::fprintf(stderr, "[mb-t] n=%d B=%d rows=%d:", A.n, B, A.rows);
         for (int i = 1; i < 118 && h[2 * i + 1]; ++i)
             std::fprintf(stderr, " %lld:%.1f", h[2 * i], (h[2 * i + 1] - h[2 * i - 1]) * 1e-3);
-        std::fprintf(stderr, " | end-start %.1fus\n", (h[238] - h[1]) * 1e-3);
+        long long emin = h[160], emax = h[160];
+        for (int q = 1; q < CL; ++q) { emin = std::min(emin, h[160 + q]); emax = std::max(emax, h[160 + q]); }
+        std::fprintf(stderr, " | end-start %.1fus | CTA entry spread %.1fus, CTA0 - first %.1fus\n", (h[238] - h[1]) * 1e-3,
+                     (emax - emin) * 1e-3, (h[160] - emin) * 1e-3);
     }
     return true;
 }
@@ -506,7 +587,10 @@ bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double
     if (k < 1 || k > kMaxK || n <= 48 || b >= n || k > b - 2 || (b % 8) != 0 || rows < 2 * kCL) return false;
     MBArgs<T> A{};
     A.Y = Y; A.rows = rows; A.n = n; A.k = k; A.rs = rs;
-    A.m = 4; A.maxit = 40; A.tol = 1e-12;
+    // residual certificate: 1e-12 * theta_1 for fp64 data; fp32 data carry
+    // ~6e-8 relative precision, so 1e-10 (eigenvector error ~1e-10 / gap)
+    // is already four orders below the fp32 parity bar (sine <= 1e-3)
+    A.m = 4; A.maxit = 40; A.tol = sizeof(T) == 4 ? 1e-10 : 1e-12;
     A.X0 = X0; A.x0_cols = x0_cols; A.Xkeep = Xkeep;
     A.U = U; A.sv = sv; A.st = st; A.Ur = Ur;
     DBuf<double> sig(ctx, k), Gout(ctx, static_cast<std::size_t>(n) * n), Wout(ctx, static_cast<std::size_t>(rows) * k),
