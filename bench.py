@@ -337,7 +337,7 @@ def run_e2e(args, mb, x, dims, ranks, p, seed, nnz, vsize, dev, local):
     ranks_c = (C.c_int * len(ranks))(*ranks)
     sweeps = args.steps
     best = None
-    for rep in range(2):
+    for rep in range(3):  # best of 3 (the first pays one-time module loading)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         hd = C.c_void_p()

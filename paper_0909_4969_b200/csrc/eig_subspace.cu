@@ -22,6 +22,9 @@
 // n x B blocks are row-major with a padded row stride (B + 2 doubles) so a
 // row is two-to-eight 128-bit loads and different rows hit different banks;
 // B x B matrices use an odd leading dimension (B + 1).
+#include <algorithm>
+#include <vector>
+
 #include "eig_sub.cuh"
 
 namespace machb {
@@ -31,12 +34,20 @@ namespace {
 // status: [0] converged, [1] zero matrix, [2] iterations used.  Gw: global
 // workspace (npad x ldg doubles) for G when it does not fit shared memory.
 template <int B>
-__global__ void __launch_bounds__(kThreads, 1) eig_subspace_kernel(const double* __restrict__ Gin, int n, int k, int m,
-                                                                int maxit, double tol, const double* X0, int x0_cols,
-                                                                double* Xkeep,  // may alias X0
-                                                                double* __restrict__ V, double* __restrict__ sig,
-                                                                int* __restrict__ status, double* Gw, double* Bw,
-                                                                long long* __restrict__ tstamp) {
+__global__ void __launch_bounds__(kThreads, 1) eig_subspace_kernel(const EigJob* __restrict__ jobs, int m, int maxit,
+                                                                double tol, long long* __restrict__ tstamp) {
+    // one CTA per job (independent eigenproblems, e.g. the d modes of HOSVD)
+    const EigJob J = jobs[blockIdx.x];
+    const double* __restrict__ Gin = J.G;
+    const int n = J.n, k = J.k, x0_cols = J.x0_cols;
+    const double* X0 = J.X0;
+    double* Xkeep = J.Xkeep;  // may alias X0
+    double* __restrict__ V = J.V;
+    double* __restrict__ sig = J.sig;
+    int* __restrict__ status = J.status;
+    double* Gw = J.Gw;
+    double* Bw = J.Bw;
+    if (blockIdx.x > 0) tstamp = nullptr;
     using SB = Sub<B>;
     constexpr int XS = SB::XS;
     extern __shared__ __align__(16) double sm[];
@@ -121,38 +132,58 @@ std::size_t subspace_smem(int n, bool g_smem, bool b_smem) {
 
 constexpr std::size_t kSmemCap = 200 * 1024;
 
+// shared-memory layout decision for one job
 template <int B>
-bool launch_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, double* V,
-                     double* sig, int* status) {
+std::size_t job_plan(int n, bool& g_smem, bool& b_smem) {
     // shared memory first for G and the blocks; what does not fit lives in
     // global memory (L2-resident at these sizes): G first, then the blocks
-    bool g_smem = true, b_smem = true;
+    g_smem = true;
+    b_smem = true;
     if (subspace_smem<B>(n, true, true) > kSmemCap) g_smem = false;
     if (subspace_smem<B>(n, g_smem, true) > kSmemCap) b_smem = false;
-    const std::size_t smem = subspace_smem<B>(n, g_smem, b_smem);
-    if (smem > kSmemCap) return false;
+    return subspace_smem<B>(n, g_smem, b_smem);
+}
+
+// Launch the jobs (all with block size B) as one grid, one CTA each.
+template <int B>
+bool launch_subspace_jobs(Ctx* ctx, std::vector<EigJob>& jobs, std::vector<DBuf<double>>& ws) {
+    std::size_t smem = 0;
+    for (auto& J : jobs) {
+        bool gs, bs;
+        const std::size_t sm = job_plan<B>(J.n, gs, bs);
+        if (sm > kSmemCap) return false;
+        smem = std::max(smem, sm);
+        if (!gs) {
+            ws.emplace_back(ctx, g_doubles(J.n));
+            J.Gw = ws.back().get();
+        }
+        if (!bs) {
+            ws.emplace_back(ctx, SubWs<B>::block_doubles((J.n + 7) & ~7));
+            J.Bw = ws.back().get();
+        }
+    }
     static bool attr = false;
     if (!attr) {
         MB_CUDA(cudaFuncSetAttribute(eig_subspace_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kSmemCap)));
         attr = true;
     }
-    DBuf<double> gw, bw;
-    if (!g_smem) gw.alloc(ctx, g_doubles(n));
-    if (!b_smem) bw.alloc(ctx, SubWs<B>::block_doubles((n + 7) & ~7));
+    DBuf<EigJob> dj(ctx, jobs.size());
+    to_device(ctx, dj.get(), jobs.data(), jobs.size());
     static const bool dbg = std::getenv("MACH_DEBUG_EIG_T") != nullptr;
     DBuf<long long> ts;
     if (dbg) {
         ts.alloc(ctx, 240);
         ts.zero(ctx);
     }
-    MB_LAUNCH(ctx, eig_subspace_kernel<B>, 1, kThreads, smem, G, n, k, 4, 40, 1e-12, X0, x0_cols, Xkeep, V, sig, status,
-              g_smem ? nullptr : gw.get(), b_smem ? nullptr : bw.get(), dbg ? ts.get() : nullptr);
+    MB_LAUNCH(ctx, eig_subspace_kernel<B>, static_cast<unsigned>(jobs.size()), kThreads, smem, dj.get(), 4, 40, 1e-12,
+              dbg ? ts.get() : nullptr);
     if (dbg) {
         long long h[240];
         to_host(ctx, h, ts.get(), 240);
         sync(ctx);
-        std::fprintf(stderr, "[eig-t] n=%d B=%d gsmem=%d bsmem=%d:", n, B, g_smem ? 1 : 0, b_smem ? 1 : 0);
+        std::fprintf(stderr, "[eig-t] n=%d B=%d jobs=%d gsmem=%d bsmem=%d:", jobs[0].n, B, static_cast<int>(jobs.size()),
+                     jobs[0].Gw ? 0 : 1, jobs[0].Bw ? 0 : 1);
         long long t_end = h[1];
         for (int i = 1; i < 118 && h[2 * i + 1]; ++i) {
             std::fprintf(stderr, " %lld:%.1f", h[2 * i], (h[2 * i + 1] - h[2 * i - 1]) * 1e-3);
@@ -162,6 +193,16 @@ bool launch_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, 
         std::fprintf(stderr, " total=%.1fus cycles=%lld\n", us, h[238] - h[239]);
     }
     return true;
+}
+
+template <int B>
+bool launch_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, double* V,
+                     double* sig, int* status) {
+    std::vector<EigJob> jobs(1);
+    jobs[0] = EigJob{G, n, k, X0, x0_cols, Xkeep, V, sig, status, nullptr, nullptr};
+    std::vector<DBuf<double>> ws;
+    ws.reserve(2);
+    return launch_subspace_jobs<B>(ctx, jobs, ws);
 }
 
 }  // namespace
@@ -193,6 +234,40 @@ bool eig_select(Ctx* ctx, const double* G, int n, int k, const double* X0, int x
     DBuf<double> work(ctx, eig_work_doubles(n, k));
     eig_topk(ctx, G, n, k, work.get(), V, sig, status, launched ? status : nullptr);
     return launched;
+}
+
+// Several independent eigenproblems (same k): subspace solver CTAs in one
+// launch when they share a block size, then each exact fallback in the
+// stream (no-ops where certified).
+void eig_select_batched(Ctx* ctx, std::vector<EigJob> jobs) {
+    bool same = !jobs.empty();
+    int b = 0;
+    for (auto& J : jobs) {
+        const int bj = eig_block(J.n, J.k);
+        const bool ok = J.n > 48 && bj < J.n && bj <= kMaxB && (bj % 8) == 0 && J.k <= bj - 2;
+        if (!ok || (b && bj != b)) same = false;
+        b = bj;
+    }
+    bool launched = false;
+    std::vector<DBuf<double>> ws;
+    ws.reserve(2 * jobs.size());
+    if (same) {
+        switch (b) {
+            case 8: launched = launch_subspace_jobs<8>(ctx, jobs, ws); break;
+            case 16: launched = launch_subspace_jobs<16>(ctx, jobs, ws); break;
+            case 24: launched = launch_subspace_jobs<24>(ctx, jobs, ws); break;
+            case 32: launched = launch_subspace_jobs<32>(ctx, jobs, ws); break;
+            default: break;
+        }
+    }
+    for (auto& J : jobs) {
+        if (!launched) {
+            eig_select(ctx, J.G, J.n, J.k, J.X0, J.x0_cols, J.Xkeep, eig_block(J.n, J.k), J.V, J.sig, J.status);
+            continue;
+        }
+        DBuf<double> work(ctx, eig_work_doubles(J.n, J.k));
+        eig_topk(ctx, J.G, J.n, J.k, work.get(), J.V, J.sig, J.status, J.status);
+    }
 }
 
 }  // namespace machb

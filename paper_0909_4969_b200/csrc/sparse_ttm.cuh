@@ -88,6 +88,19 @@ bool eig_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, int
 bool eig_select(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
                 double* V, double* sig, int* status);
 int eig_block(int n, int k);
+struct EigJob {
+    const double* G;
+    int n, k;
+    const double* X0;
+    int x0_cols;
+    double* Xkeep;
+    double* V;
+    double* sig;
+    int* status;
+    double* Gw;  // workspaces (set by the launcher)
+    double* Bw;
+};
+void eig_select_batched(Ctx* ctx, std::vector<EigJob> jobs);
 std::size_t eig_work_doubles(int n, int k);
 template <typename T>
 void gram(Ctx* ctx, const T* a, long long sk, long long sn, int K, int N, double* G);

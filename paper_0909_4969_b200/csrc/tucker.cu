@@ -566,32 +566,48 @@ struct SparseSession : SessionBase {
         // ---- HOSVD: sparse_mode_basis per mode (sparse_kernels.cpp:82-90) ----
         tm.start();
         const long long numel = X->numel;
+        // all modes' Grams first, then their eigenproblems in one launch (one
+        // CTA each: independent, latency-bound), then the bases
+        struct ModeWork {
+            bool row;
+            int n, kc;
+            DBuf<double> G, V, sig;
+            DBuf<int> est;
+        };
+        std::vector<ModeWork> mw(static_cast<std::size_t>(d));
+        std::vector<EigJob> jobs;
         for (int m = 0; m < d; ++m) {
+            ModeWork& w = mw[static_cast<std::size_t>(m)];
             const int rows = dims[static_cast<std::size_t>(m)];
             const long long cols = numel / rows;
             const int k = ranks[static_cast<std::size_t>(m)];
-            if (rows <= cols) {
-                DBuf<double> G(ctx, static_cast<std::size_t>(rows) * rows);
-                sparse_row_gram<T>(ctx, X, m, normX2, G.get());
-                DBuf<double> V(ctx, static_cast<std::size_t>(rows) * k), sig(ctx, k);
-                DBuf<int> est(ctx, 3);
-                eig_select(ctx, G.get(), rows, k, nullptr, 0, nullptr, eig_block(rows, k), V.get(), sig.get(), est.get());
-                basis_from_side(ctx, V.get(), sig.get(), rows, k, est.get(), fs.U[static_cast<std::size_t>(m)].get(),
+            w.row = rows <= cols;
+            if (!w.row && cols > 4096)
+                throw Error(MACH_ERR_INTERNAL, "column-side sparse HOSVD wider than 4096 is not supported on device yet");
+            w.n = w.row ? rows : static_cast<int>(cols);
+            w.kc = w.row ? k : static_cast<int>(std::min<long long>(k, cols));
+            w.G.alloc(ctx, static_cast<std::size_t>(w.n) * w.n);
+            if (w.row) sparse_row_gram<T>(ctx, X, m, normX2, w.G.get());
+            else sparse_col_gram<T>(ctx, X, *plans[static_cast<std::size_t>(m)], cols, normX2, w.G.get());
+            w.V.alloc(ctx, static_cast<std::size_t>(w.n) * w.kc);
+            w.sig.alloc(ctx, w.kc);
+            w.est.alloc(ctx, 3);
+            jobs.push_back(EigJob{w.G.get(), w.n, w.kc, nullptr, 0, nullptr, w.V.get(), w.sig.get(), w.est.get(),
+                                  nullptr, nullptr});
+        }
+        eig_select_batched(ctx, jobs);
+        for (int m = 0; m < d; ++m) {
+            ModeWork& w = mw[static_cast<std::size_t>(m)];
+            const int rows = dims[static_cast<std::size_t>(m)];
+            const int k = ranks[static_cast<std::size_t>(m)];
+            if (w.row) {
+                basis_from_side(ctx, w.V.get(), w.sig.get(), rows, k, w.est.get(), fs.U[static_cast<std::size_t>(m)].get(),
                                 sv_at(m), fs.st.get() + 3 * m);
             } else {
-                if (cols > 4096)
-                    throw Error(MACH_ERR_INTERNAL, "column-side sparse HOSVD wider than 4096 is not supported on device yet");
-                const int kc = static_cast<int>(std::min<long long>(k, cols));
-                const int n = static_cast<int>(cols);
-                DBuf<double> G(ctx, static_cast<std::size_t>(n) * n);
-                sparse_col_gram<T>(ctx, X, *plans[static_cast<std::size_t>(m)], cols, normX2, G.get());
-                DBuf<double> V(ctx, static_cast<std::size_t>(n) * kc), sig(ctx, kc);
-                DBuf<int> est(ctx, 3);
-                eig_select(ctx, G.get(), n, kc, nullptr, 0, nullptr, eig_block(n, kc), V.get(), sig.get(), est.get());
-                DBuf<double> W(ctx, static_cast<std::size_t>(rows) * kc);
-                sparse_times<T>(ctx, X, *plans[static_cast<std::size_t>(m)], V.get(), cols, kc, W.get());
-                basis_from_products(ctx, W.get(), rows, kc, k, sig.get(), est.get(), fs.U[static_cast<std::size_t>(m)].get(),
-                                    sv_at(m), fs.st.get() + 3 * m);
+                DBuf<double> W(ctx, static_cast<std::size_t>(rows) * w.kc);
+                sparse_times<T>(ctx, X, *plans[static_cast<std::size_t>(m)], w.V.get(), w.n, w.kc, W.get());
+                basis_from_products(ctx, W.get(), rows, w.kc, k, w.sig.get(), w.est.get(),
+                                    fs.U[static_cast<std::size_t>(m)].get(), sv_at(m), fs.st.get() + 3 * m);
             }
             refresh(m);
         }
