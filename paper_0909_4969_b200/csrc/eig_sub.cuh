@@ -215,15 +215,28 @@ struct Sub {
     // diag(1/|x_j|)): a Chebyshev-filtered block has columns of wildly
     // different lengths but nearly orthogonal directions, and only the
     // latter should decide breakdown.
-    __device__ static bool cholqr(double*& X, double*& T, double* S, double* Ri, double* rinv, int npad, int* flag) {
+    __device__ static bool cholqr(double*& X, double*& T, double* S, double* Ri, double* rinv, int npad, int* flag,
+                                  bool allow_skip = false) {
         __shared__ double dn[kMaxB];
+        __shared__ int near_identity;
         gram(X, X, S, npad);
-        if (threadIdx.x == 0) *flag = 1;
+        if (threadIdx.x == 0) {
+            *flag = 1;
+            near_identity = 1;
+        }
         if (threadIdx.x < B) {
             const double s = S[threadIdx.x + threadIdx.x * HS];
             dn[threadIdx.x] = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
         }
         __syncthreads();
+        if (allow_skip) {  // already orthonormal to ~1e-14: leave X as it is
+            for (int e = threadIdx.x; e < B * B; e += kThreads) {
+                const int l = e % B, m = e / B;
+                if (!(fabs(S[l + m * HS] - (l == m ? 1.0 : 0.0)) <= 1e-14)) near_identity = 0;
+            }
+            __syncthreads();
+            if (near_identity) return true;
+        }
         for (int e = threadIdx.x; e < B * B; e += kThreads) {
             const int l = e % B, m = e / B;
             if (l <= m) S[l + m * HS] *= dn[l] * dn[m];
@@ -318,7 +331,9 @@ struct Sub {
 
     __device__ static void orthonormalize(double*& X, double*& T, int n, int npad, double* S, double* Ri, double* rinv,
                                           double* coef, double* red, int* flag) {
-        if (!cholqr(X, T, S, Ri, rinv, npad, flag) || !cholqr(X, T, S, Ri, rinv, npad, flag)) cgs2(X, n, coef, red);
+        // CholQR2; the second pass is skipped when the first already left an
+        // orthonormal block (its Gram is the identity to 1e-14)
+        if (!cholqr(X, T, S, Ri, rinv, npad, flag) || !cholqr(X, T, S, Ri, rinv, npad, flag, true)) cgs2(X, n, coef, red);
     }
 
     // sort the diagonal of H descending into th, permute W's columns alike
@@ -567,7 +582,7 @@ struct SubWs {
 template <int B>
 __device__ double* subspace_core(SubWs<B>& ws, const double* G, int ldg, int n, int k, int m, int maxit, double tol,
                                  const double* X0, int x0_cols, bool& conv, int& iters, int* flagp,
-                                 long long* tstamp, int& ns_) {
+                                 long long* tstamp, int& ns_, const double* th0 = nullptr) {
     using SB = Sub<B>;
     constexpr int XS = SB::XS;
     const int npad = (n + 7) & ~7;
@@ -601,9 +616,16 @@ __device__ double* subspace_core(SubWs<B>& ws, const double* G, int ldg, int n, 
     if (x0_cols < B || !X0) SB::orthonormalize(X, Y0, n, npad, S, Z, rinv, coef, red, &flag);  // a kept Ritz block is orthonormal
     MB_STAMP(2);
 
+    // A warm block that comes with its Ritz values (th0, the previous call's)
+    // starts with a filter step: the previous G's spectrum bounds the filter,
+    // and one Rayleigh-Ritz pass is saved per call.
+    const bool filter_first = X0 && x0_cols >= B && th0;
+    if (filter_first && threadIdx.x < B) th[threadIdx.x] = th0[threadIdx.x];
+    __syncthreads();
     int it = 0;
     conv = false;
     for (;; ++it) {
+      if (!(filter_first && it == 0)) {
         // ---- Rayleigh-Ritz ----
         SB::gemm(G, ldg, X, AX, npad, 1.0, nullptr, 0.0, nullptr, 0.0);
         MB_STAMP(10);
@@ -623,7 +645,9 @@ __device__ double* subspace_core(SubWs<B>& ws, const double* G, int ldg, int n, 
         MB_STAMP(14);
         if (rmax <= tol * scale) { conv = true; break; }
         if (it >= maxit) break;
+      }
         // ---- Chebyshev filter: damp [lo, cut] = [-|theta_1| 1e-12, theta_B] ----
+        const double scale = fmax(fabs(th[0]), 1e-300);
         const double cut = th[B - 1];
         const double lo = -1e-12 * scale;
         const double e = 0.5 * (cut - lo), cen = 0.5 * (cut + lo);

@@ -105,13 +105,16 @@ __global__ void __launch_bounds__(kThreads, 1) eig_subspace_kernel(const EigJob*
     int it = 0;
     bool conv = false;
     SubWs<B> ws(sm, npad, Bw);
-    double* X = subspace_core<B>(ws, G, ldg, n, k, m, maxit, tol, X0, x0_cols, conv, it, &flag, tstamp, ns_);
+    const double* th0 = (X0 && x0_cols >= B) ? J.th0 : nullptr;
+    double* X = subspace_core<B>(ws, G, ldg, n, k, m, maxit, tol, X0, x0_cols, conv, it, &flag, tstamp, ns_, th0);
     const double* th = ws.th;
     if (tstamp && threadIdx.x == 0) tstamp[238] = clock64();
     // ---- outputs (column-major) ----
     for (int e = threadIdx.x; e < n * k; e += kThreads) V[e] = X[(e % n) * XS + e / n];
-    if (Xkeep)
+    if (Xkeep) {
         for (int e = threadIdx.x; e < n * B; e += kThreads) Xkeep[e] = X[(e % n) * XS + e / n];
+        if (threadIdx.x < B) Xkeep[n * B + threadIdx.x] = th[threadIdx.x];  // Ritz values travel with the block
+    }
     if (threadIdx.x < k) sig[threadIdx.x] = sqrt(fmax(0.0, th[threadIdx.x]));
     if (threadIdx.x == 0) { status[0] = conv ? 1 : 0; status[1] = 0; status[2] = it; }
 }
@@ -200,6 +203,7 @@ bool launch_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, 
                      double* sig, int* status) {
     std::vector<EigJob> jobs(1);
     jobs[0] = EigJob{G, n, k, X0, x0_cols, Xkeep, V, sig, status, nullptr, nullptr};
+    if (X0 && x0_cols >= B) jobs[0].th0 = X0 + static_cast<std::size_t>(n) * B;  // a kept warm block
     std::vector<DBuf<double>> ws;
     ws.reserve(2);
     return launch_subspace_jobs<B>(ctx, jobs, ws);

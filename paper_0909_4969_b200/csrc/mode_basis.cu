@@ -54,6 +54,7 @@ struct MBArgs {
     double* Wout;   // rows x k (basis fallback)
     int* flags;     // 4: eig_topk skip, need W = Y V, need slow basis, need row-major copy
     int ch;         // rows per row-block CTA (multiple of 4)
+    int filter_first;  // warm start: filter with the previous Ritz values before the first Rayleigh-Ritz
 };
 
 template <int B>
@@ -195,10 +196,13 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
         } else {
             bool conv = false;
             int it = 0;
+            const double* th0 = (A.filter_first && A.X0 && A.x0_cols >= B) ? A.X0 + static_cast<std::size_t>(n) * B : nullptr;
             double* X = subspace_core<B>(ws, G, ldg, n, k, A.m, A.maxit, A.tol, A.X0, A.x0_cols, conv, it, &flagw,
-                                         tstamp, ns_);
-            if (A.Xkeep)
+                                         tstamp, ns_, th0);
+            if (A.Xkeep) {
                 for (int e = threadIdx.x; e < n * B; e += kThreads) A.Xkeep[e] = X[(e % n) * Sub<B>::XS + e / n];
+                if (threadIdx.x < B) A.Xkeep[n * B + threadIdx.x] = ws.th[threadIdx.x];
+            }
             if (threadIdx.x < k) A.sig[threadIdx.x] = sqrt(fmax(0.0, ws.th[threadIdx.x]));
             if (threadIdx.x == 0) {
                 A.estatus[0] = conv ? 1 : 0;
@@ -591,6 +595,8 @@ bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double
     // ~6e-8 relative precision, so 1e-10 (eigenvector error ~1e-10 / gap)
     // is already four orders below the fp32 parity bar (sine <= 1e-3)
     A.m = 4; A.maxit = 40; A.tol = sizeof(T) == 4 ? 1e-10 : 1e-12;
+    static const int ff = std::getenv("MACH_FILTER_FIRST") ? std::atoi(std::getenv("MACH_FILTER_FIRST")) : 0;
+    A.filter_first = ff;
     A.X0 = X0; A.x0_cols = x0_cols; A.Xkeep = Xkeep;
     A.U = U; A.sv = sv; A.st = st; A.Ur = Ur;
     DBuf<double> sig(ctx, k), Gout(ctx, static_cast<std::size_t>(n) * n), Wout(ctx, static_cast<std::size_t>(rows) * k),

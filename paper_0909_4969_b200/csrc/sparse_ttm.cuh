@@ -82,6 +82,8 @@ void eig_topk(Ctx* ctx, const double* G, int n, int k, double* work, double* V, 
               const int* skip = nullptr);
 bool eig_subspace(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
                   double* V, double* sig, int* status);
+// Warm blocks (Xkeep) hold n*b vectors followed by their b Ritz values.
+inline std::size_t warm_doubles(int n, int b) { return static_cast<std::size_t>(n) * b + b; }
 // top-k eigenpairs of G: warm-started subspace solver when it applies, with the
 // exact selected-eigenpair solver as the in-stream fallback.  status[1]==1
 // flags an exactly zero G.
@@ -99,6 +101,7 @@ struct EigJob {
     int* status;
     double* Gw;  // workspaces (set by the launcher)
     double* Bw;
+    const double* th0 = nullptr;  // Ritz values of X0 (warm start with them: filter first)
 };
 void eig_select_batched(Ctx* ctx, std::vector<EigJob> jobs);
 std::size_t eig_work_doubles(int n, int k);

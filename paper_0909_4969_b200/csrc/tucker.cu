@@ -150,8 +150,8 @@ void lsb_device(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U
     int x0c = 0;
     DBuf<double> seed;
     if (warm) {
-        if (warm->X.n != static_cast<std::size_t>(side) * b) {
-            warm->X.alloc(ctx, static_cast<std::size_t>(side) * b);
+        if (warm->X.n != warm_doubles(side, b)) {
+            warm->X.alloc(ctx, warm_doubles(side, b));
             warm->cols = 0;
         }
         warm->b = b;
@@ -201,8 +201,8 @@ bool lsb_fused(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U,
     if (row_side || cols > 4096 || k > cols) return false;
     const int side = static_cast<int>(cols);
     const int b = eig_block(side, k);
-    if (warm->X.n != static_cast<std::size_t>(side) * b) {
-        warm->X.alloc(ctx, static_cast<std::size_t>(side) * b);
+    if (warm->X.n != warm_doubles(side, b)) {
+        warm->X.alloc(ctx, warm_doubles(side, b));
         warm->cols = 0;
     }
     warm->b = b;
