@@ -65,29 +65,64 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled in the background."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled in a background thread through NVML
+    (every ~1 ms, so even a few-millisecond timed region gets samples);
+    nvidia-smi as the fallback.  mark(True/False) brackets the timed region:
+    the summary reports the samples taken inside it when there are any."""
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (in_timed, sm_mhz, max_mhz, reasons bitmask or names)
         self._stop = threading.Event()
         self._t = None
+        self._timed = False
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._nvml = pynvml
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+
+    def mark(self, timed: bool):
+        self._timed = timed
+
+    def _reasons(self, mask):
+        n = self._nvml
+        names = []
+        for attr, name in (("nvmlClocksThrottleReasonHwSlowdown", "hw_slowdown"),
+                           ("nvmlClocksThrottleReasonHwThermalSlowdown", "hw_thermal_slowdown"),
+                           ("nvmlClocksThrottleReasonSwThermalSlowdown", "sw_thermal_slowdown"),
+                           ("nvmlClocksThrottleReasonSwPowerCap", "sw_power_cap")):
+            bit = getattr(n, attr, None)
+            if bit is not None and mask & bit:
+                names.append(name)
+        return names
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                if self._nvml is not None:
+                    n = self._nvml
+                    sm = n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)
+                    mask = n.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                    self.samples.append((self._timed, float(sm), float(self._max), self._reasons(mask)))
+                    self._stop.wait(0.001)
+                    continue
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                                      "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                                      "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
                 parts = [p.strip() for p in out.strip().split(",")]
-                if len(parts) >= 7:
-                    self.samples.append(parts)
+                if len(parts) >= 6:
+                    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                    self.samples.append((self._timed, float(parts[0]), float(parts[1]),
+                                         [names[i] for i in range(4) if parts[2 + i].lower().startswith("active")]))
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -99,14 +134,14 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        timed = [s for s in self.samples if s[0]]
+        use = timed or self.samples
+        if not use:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"]}
+        return {"sm_mhz": statistics.median(s[1] for s in use), "sm_max_mhz": max(s[2] for s in use),
+                "reasons": sorted({r for s in use for r in s[3]}), "samples": len(use),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi",
+                "window": "timed region" if timed else "whole run"}
 
 
 # ---------------------------------------------------------------------------
@@ -207,6 +242,7 @@ def run_mach(args, rank, world, local):
         times = []
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        clocks.mark(True)
         with torch.cuda.stream(stream):
             for k in range(args.steps):
                 flush.zero_()  # evict the sampled tensor from L2 between timed sweeps
@@ -215,6 +251,7 @@ def run_mach(args, rank, world, local):
                 ends[k].record(stream)
         stream.synchronize()
         torch.cuda.synchronize()
+        clocks.mark(False)
         launches = ctx.launches - l0
         times = [s.elapsed_time(e) for s, e in zip(starts, ends)]
         ms = sum(times) / len(times)
