@@ -72,6 +72,14 @@ mach_status mach_ctx_create(int device, mach_ctx** out) {
         MB_CUDA(cudaSetDevice(device));
         MB_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
         c->c.own_stream = true;
+        // keep freed stream-ordered allocations cached in the device pool
+        // (the default threshold returns them to the driver at every sync,
+        // so each job would pay for fresh allocations)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            std::uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
         *out = c.release();
     });
 }

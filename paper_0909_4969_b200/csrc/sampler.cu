@@ -37,15 +37,18 @@ __device__ __forceinline__ std::uint64_t splitmix_finalize(std::uint64_t z) {
 
 template <typename T>
 struct Vec;
+// per thread and vector: one 16-byte load (4 fp32 / 2 fp64 elements)
 template <>
 struct Vec<float> {
     using type = float4;
+    static constexpr int per = 4;
     static constexpr int n = 4;
     __device__ static void unpack(const float4& v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
 };
 template <>
 struct Vec<double> {
     using type = double2;
+    static constexpr int per = 2;
     static constexpr int n = 2;
     __device__ static void unpack(const double2& v, double* o) { o[0] = v.x; o[1] = v.y; }
 };
@@ -59,9 +62,9 @@ __device__ __forceinline__ bool is_finite_bits(double x) {
 // the tile is (v, thread, j) which is ascending flat index, so an exclusive
 // scan of the per-(v, thread) kept counts in that order gives each kept
 // element its output slot.  The NV counts of a thread are packed into one u64
-// (16-bit fields; a block-wide per-v total is <= kThreads * VEC <= 1024).
+// (16-bit fields; a block-wide per-v total is <= kThreads * VEC <= 2048).
 template <typename T, typename IdxT>
-__global__ void __launch_bounds__(kThreads) sample_kernel(const T* __restrict__ x, std::int64_t numel,
+__global__ void __launch_bounds__(kThreads, 4) sample_kernel(const T* __restrict__ x, std::int64_t numel,
                                                           std::int64_t gofs,  // global flat index of x[0]
                                                           std::uint64_t seed, std::uint64_t thr_shift,
                                                           int keep_all, double p, IdxT* __restrict__ out_idx,
@@ -89,33 +92,64 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(const T* __restrict__ 
     const std::int64_t tile = s_tile;
     const std::int64_t base = tile * TILE;
 
-    // ---- load + hash ----
+    // ---- load (all vectors in flight first) + hash ----
     T vals[NV][VEC];
-    unsigned keep_bits = 0;  // bit (v*VEC + j)
-    bool bad = false;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         const std::int64_t e0 = base + (static_cast<std::int64_t>(v) * kThreads + tid) * VEC;
         if (e0 + VEC <= numel) {
-            const auto raw = __ldcs(reinterpret_cast<const typename V::type*>(x + e0));
-            V::unpack(raw, vals[v]);
+#pragma unroll
+            for (int l = 0; l < VEC / V::per; ++l) {
+                const auto raw = __ldcs(reinterpret_cast<const typename V::type*>(x + e0) + l);
+                V::unpack(raw, vals[v] + l * V::per);
+            }
         } else {
 #pragma unroll
             for (int j = 0; j < VEC; ++j) vals[v][j] = (e0 + j < numel) ? x[e0 + j] : T(0);
         }
+    }
+    unsigned keep_bits = 0;  // bit (v*VEC + j)
+    unsigned tie_bits = 0;   // high word of the hash equal to the threshold's (exact check below)
+    T nanacc = T(0);         // x * 0 is NaN exactly for inf / NaN inputs
+    const unsigned thr_hi = static_cast<unsigned>(thr_shift >> 32);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const std::int64_t e0 = base + (static_cast<std::int64_t>(v) * kThreads + tid) * VEC;
+        const std::int64_t rem = numel - e0;
+        const int lim = rem >= VEC ? VEC : (rem > 0 ? static_cast<int>(rem) : 0);
         // z_j = seed + (i + 1) * golden for consecutive i: incremental adds.
         std::uint64_t z = seed + (static_cast<std::uint64_t>(gofs + e0) + 1ull) * 0x9E3779B97F4A7C15ULL;
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
             const T xv = vals[v][j];
-            bad |= !is_finite_bits(xv);
-            const std::uint64_t h = splitmix_finalize(z);
-            const bool k = (xv != T(0)) && (keep_all || h < thr_shift) && (e0 + j < numel);
-            keep_bits |= (k ? 1u : 0u) << (v * VEC + j);
+            nanacc = fma(xv, T(0), nanacc);
+            // keep iff hash < thr_shift.  The final xor-shift's high word needs
+            // only the high word of the last product; the low words matter
+            // only on a high-word tie (probability 2^-32), handled after.
+            std::uint64_t y = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+            y ^= y >> 27;
+            const unsigned ylo = static_cast<unsigned>(y), yhi = static_cast<unsigned>(y >> 32);
+            const unsigned zhi = __umulhi(ylo, 0x133111EBu) + ylo * 0x94D049BBu + yhi * 0x133111EBu;
+            const unsigned hhi = zhi ^ (zhi >> 31);
+            const bool live = (xv != T(0)) & (j < lim);
+            keep_bits |= static_cast<unsigned>(live & (keep_all | (hhi < thr_hi))) << (v * VEC + j);
+            tie_bits |= static_cast<unsigned>(live & (hhi == thr_hi)) << (v * VEC + j);
             z += 0x9E3779B97F4A7C15ULL;
         }
     }
-    if (bad) atomicOr(flags, 1);
+    if (tie_bits && !keep_all) {  // exact 64-bit comparison for the (rare) ties
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const std::int64_t e0 = base + (static_cast<std::int64_t>(v) * kThreads + tid) * VEC;
+#pragma unroll
+            for (int j = 0; j < VEC; ++j)
+                if ((tie_bits >> (v * VEC + j)) & 1u) {
+                    const std::uint64_t z = seed + (static_cast<std::uint64_t>(gofs + e0 + j) + 1ull) * 0x9E3779B97F4A7C15ULL;
+                    if (splitmix_finalize(z) < thr_shift) keep_bits |= 1u << (v * VEC + j);
+                }
+        }
+    }
+    if (nanacc != nanacc) atomicOr(flags, 1);
 
     unsigned long long packed = 0;
 #pragma unroll
@@ -132,8 +166,10 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(const T* __restrict__ 
         run += static_cast<unsigned>((tot_packed >> (16 * v)) & 0xFFFFu);
     }
     const unsigned tile_total = run;
+    // publish this tile's aggregate as early as possible (successors' look-back)
+    if (tid == 0 && tile > 0) atomicExch(&status[tile], kFlagAgg | tile_total);
 
-    // ---- stage kept entries in shared memory in tile order ----
+    // ---- stage kept entries (raw values) in shared memory in tile order ----
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         unsigned o = offv[v];
@@ -142,26 +178,25 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(const T* __restrict__ 
         for (int j = 0; j < VEC; ++j) {
             if ((keep_bits >> (v * VEC + j)) & 1u) {
                 s_idx[o] = static_cast<IdxT>(gofs + e0 + j);
-                s_val[o] = static_cast<T>(__ddiv_rn(static_cast<double>(vals[v][j]), p));
+                s_val[o] = vals[v][j];
                 ++o;
             }
         }
     }
+    __syncthreads();
 
-    // ---- decoupled look-back (warp 0) ----
     if (tid < 32) {
+        // ---- decoupled look-back (warp 0) ----
         const int lane = tid;
         long long excl = 0;
         if (tile == 0) {
-            if (lane == 0) {
-                atomicExch(&status[0], kFlagPre | tile_total);
-            }
+            if (lane == 0) atomicExch(&status[0], kFlagPre | tile_total);
         } else {
-            if (lane == 0) atomicExch(&status[tile], kFlagAgg | tile_total);
             std::int64_t look = tile - 1;
             while (true) {
                 const std::int64_t j = look - lane;
-                unsigned long long s = (j >= 0) ? atomicAdd(&status[j], 0ull) : (kFlagPre | 0ull);
+                unsigned long long s = kFlagPre | 0ull;
+                if (j >= 0) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(s) : "l"(status + j) : "memory");
                 const bool unset = (s >> 62) == 0;
                 if (__any_sync(0xffffffffu, unset)) continue;
                 const unsigned pmask = __ballot_sync(0xffffffffu, (s & ~kValMask) == kFlagPre);
@@ -183,6 +218,11 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(const T* __restrict__ 
             const std::int64_t ntiles = (numel + TILE - 1) / TILE;
             if (tile == ntiles - 1) *total_out = excl + tile_total;
         }
+    } else {
+        // ---- meanwhile the other warps form x / p (correctly rounded fp64
+        // division, sampling.cpp:28) for the staged entries, coalesced ----
+        for (unsigned k = tid - 32; k < tile_total; k += kThreads - 32)
+            s_val[k] = static_cast<T>(__ddiv_rn(static_cast<double>(s_val[k]), p));
     }
     __syncthreads();
 
@@ -202,7 +242,7 @@ template <typename T, typename IdxT>
 std::int64_t launch_sample(Ctx* ctx, const T* x, std::int64_t numel, std::int64_t gofs, std::uint64_t seed, double p,
                            std::int64_t capacity, IdxT* out_idx, T* out_val, int* flags_host) {
     constexpr int VEC = Vec<T>::n;
-    constexpr int TILE = kThreads * 4 * VEC;
+    constexpr int TILE = kThreads * 4 * VEC;  // NV = 4
     const std::int64_t ntiles = (numel + TILE - 1) / TILE;
     // threshold: keep iff (h >> 11) < ceil(p * 2^53)  <=>  h < ceil(p*2^53) << 11
     const double t53 = std::ceil(std::ldexp(p, 53));
