@@ -33,11 +33,16 @@ namespace {
 
 // status: [0] converged, [1] zero matrix, [2] iterations used.  Gw: global
 // workspace (npad x ldg doubles) for G when it does not fit shared memory.
+constexpr int kMaxJobs = 8;
+struct EigJobs {  // by value (kernel parameter): no host->device copy, graph-capturable
+    EigJob j[kMaxJobs];
+};
+
 template <int B>
-__global__ void __launch_bounds__(kThreads, 1) eig_subspace_kernel(const EigJob* __restrict__ jobs, int m, int maxit,
-                                                                double tol, long long* __restrict__ tstamp) {
+__global__ void __launch_bounds__(kThreads, 1) eig_subspace_kernel(const EigJobs jobs, int m, int maxit, double tol,
+                                                                long long* __restrict__ tstamp) {
     // one CTA per job (independent eigenproblems, e.g. the d modes of HOSVD)
-    const EigJob J = jobs[blockIdx.x];
+    const EigJob J = jobs.j[blockIdx.x];
     const double* __restrict__ Gin = J.G;
     const int n = J.n, k = J.k, x0_cols = J.x0_cols;
     const double* X0 = J.X0;
@@ -171,15 +176,16 @@ bool launch_subspace_jobs(Ctx* ctx, std::vector<EigJob>& jobs, std::vector<DBuf<
                                      static_cast<int>(kSmemCap)));
         attr = true;
     }
-    DBuf<EigJob> dj(ctx, jobs.size());
-    to_device(ctx, dj.get(), jobs.data(), jobs.size());
+    if (jobs.size() > static_cast<std::size_t>(kMaxJobs)) return false;
+    EigJobs dj{};
+    for (std::size_t i = 0; i < jobs.size(); ++i) dj.j[i] = jobs[i];
     static const bool dbg = std::getenv("MACH_DEBUG_EIG_T") != nullptr;
     DBuf<long long> ts;
     if (dbg) {
         ts.alloc(ctx, 240);
         ts.zero(ctx);
     }
-    MB_LAUNCH(ctx, eig_subspace_kernel<B>, static_cast<unsigned>(jobs.size()), kThreads, smem, dj.get(), 4, 40, 1e-12,
+    MB_LAUNCH(ctx, eig_subspace_kernel<B>, static_cast<unsigned>(jobs.size()), kThreads, smem, dj, 4, 40, 1e-12,
               dbg ? ts.get() : nullptr);
     if (dbg) {
         long long h[240];

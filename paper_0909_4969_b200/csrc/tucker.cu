@@ -484,11 +484,17 @@ struct SparseSession : SessionBase {
     // updated factor), then fit = 1 - sqrt(|X|^2 - |G|^2)/|X| (orthonormal
     // factors).  Near-exact models take the reference's entrywise residual
     // (tucker.cpp:47-64) instead of the cancelling identity.
-    double core_and_fit() {
+    void core_device() {
         const int last = d - 1;
         core_from_last<T>(ctx, Y.get(), dims[static_cast<std::size_t>(last)], C[static_cast<std::size_t>(last)],
                           fs.U[static_cast<std::size_t>(last)].get(), ranks[static_cast<std::size_t>(last)], core.get());
         sumsq<double>(ctx, core.get(), static_cast<long long>(core.n), fs.red.get(), fs.scal.get() + 1);
+    }
+    double core_and_fit() {
+        core_device();
+        return fit_host();
+    }
+    double fit_host() {
         double sc[2];
         to_host(ctx, sc, fs.scal.get(), 2);
         sync(ctx);
@@ -629,12 +635,56 @@ struct SparseSession : SessionBase {
                       &warm[si], fs.U[si].get());
         refresh(i);
     }
-    void sweep() override {
+    // Steady-state sweeps (every mode warm-started) are captured once into a
+    // CUDA graph and replayed: one launch per sweep instead of ~40 host
+    // submissions.  Only the fit read-back (and its rare entrywise-residual
+    // guard) stays outside the graph.
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    std::int64_t graph_launches = 0;
+    ~SparseSession() override {
+        if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        if (graph) cudaGraphDestroy(graph);
+    }
+    bool graph_ok() const {
+        static const bool off = std::getenv("MACH_NO_GRAPH") || std::getenv("MACH_DEBUG_EIG") ||
+                                std::getenv("MACH_DEBUG_EIG_T") || std::getenv("MACH_TTM_TS");
+        if (off || ctx->profile || sharded) return false;
+        for (int i = 0; i < d; ++i)
+            if (warm[static_cast<std::size_t>(i)].cols <= 0) return false;  // first sweep seeds the warm blocks
+        return true;
+    }
+    void sweep_body() {
         for (int i = 0; i < d; ++i) {
             mode_y(i);
             mode_update(i);
         }
-        fit = core_and_fit();
+        core_device();
+    }
+    void sweep() override {
+        if (graph_ok()) {
+            if (!graph_exec) {
+                const std::int64_t l0 = ctx->launches;
+                MB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+                try {
+                    sweep_body();
+                } catch (...) {
+                    cudaGraph_t g = nullptr;
+                    cudaStreamEndCapture(ctx->stream, &g);
+                    if (g) cudaGraphDestroy(g);
+                    throw;
+                }
+                MB_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+                MB_CUDA(cudaGraphInstantiate(&graph_exec, graph, 0));
+                graph_launches = ctx->launches - l0;
+                ctx->launches = l0;
+            }
+            MB_CUDA(cudaGraphLaunch(graph_exec, ctx->stream));
+            ctx->launches += graph_launches;
+        } else {
+            sweep_body();
+        }
+        fit = fit_host();
         warnings = read_warnings(ctx, fs.st, ranks, all);
     }
     void* ext_mode_y(int m, int* rows, int* cols) override {
