@@ -462,7 +462,6 @@ struct Sub {
         double nrm = 0.0;
         for (int e = tid; e < B * B; e += kThreads) nrm += H[(e % B) + (e / B) * HS] * H[(e % B) + (e / B) * HS];
         nrm = cta_sum(nrm, red);
-        const int t = tid / B, j = tid % B;
         int sweep = 0;
         for (; sweep < max_sweeps; ++sweep) {
             double off = 0.0;
@@ -490,7 +489,9 @@ struct Sub {
                     jp[tid] = p; jq[tid] = q; jc[tid] = c; js[tid] = s;
                 }
                 __syncthreads();
-                if (t < NP) {
+                // (pair t, column j) items: NP * B of them, strided over the CTA
+                for (int e = tid; e < NP * B; e += kThreads) {
+                    const int t = e / B, j = e - t * B;
                     const double s = js[t];
                     if (s != 0.0) {
                         const double c = jc[t];
@@ -501,7 +502,8 @@ struct Sub {
                     }
                 }
                 __syncthreads();
-                if (t < NP) {
+                for (int e = tid; e < NP * B; e += kThreads) {
+                    const int t = e / B, j = e - t * B;
                     const double s = js[t];
                     if (s != 0.0) {
                         const double c = jc[t];

@@ -261,7 +261,24 @@ void eig_select_batched(Ctx* ctx, std::vector<EigJob> jobs) {
     bool launched = false;
     std::vector<DBuf<double>> ws;
     ws.reserve(2 * jobs.size());
-    if (same) {
+    if (same && !std::getenv("MACH_EIG_LARGE_OFF")) {
+        // G beyond one CTA's shared memory: the multi-kernel solver spreads
+        // the G X products over many SMs
+        bool big = true;
+        for (auto& J : jobs) {
+            bool gs = true, bs = true;
+            switch (b) {
+                case 8: job_plan<8>(J.n, gs, bs); break;
+                case 16: job_plan<16>(J.n, gs, bs); break;
+                case 24: job_plan<24>(J.n, gs, bs); break;
+                default: job_plan<32>(J.n, gs, bs); break;
+            }
+            if (gs) big = false;
+        }
+        static const int bf = std::getenv("MACH_LG_B") ? std::atoi(std::getenv("MACH_LG_B")) : 0;
+        if (big) launched = eig_large_batched(ctx, jobs, bf ? bf : b);
+    }
+    if (same && !launched) {
         switch (b) {
             case 8: launched = launch_subspace_jobs<8>(ctx, jobs, ws); break;
             case 16: launched = launch_subspace_jobs<16>(ctx, jobs, ws); break;

@@ -182,11 +182,9 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
 
     // ---- phase C: eigensolver on CTA 0 ----
     if (rank == 0) {
+        // G = Y^T Y is zero iff its trace is
         double fro = 0.0;
-        for (int e = threadIdx.x; e < n * n; e += kThreads) {
-            const double g = G[(e % n) + (e / n) * ldg];
-            fro = fma(g, g, fro);
-        }
+        for (int e = threadIdx.x; e < n; e += kThreads) fro += G[e + e * ldg];
         SubWs<B> ws(wsp, npad);
         fro = cta_sum(fro, ws.red);
         if (threadIdx.x == 0) mflag = 0;

@@ -28,6 +28,7 @@
 #include <cub/device/device_select.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -57,20 +58,45 @@ struct DimArr {
     int dims[8];
 };
 
+// per-mode shift of the coordinate in the packed key (-1: not in the key)
+struct ModeShift {
+    int sh[8];
+};
+
+inline ModeShift mode_shift(const KeyFields& kf) {
+    ModeShift ms;
+    for (int m = 0; m < 8; ++m) ms.sh[m] = -1;
+    for (int j = 0; j < kf.nf; ++j) ms.sh[kf.mode[j]] = kf.shift[j];
+    return ms;
+}
+
 template <typename IdxT, typename K>
-__global__ void build_keys_kernel(const IdxT* __restrict__ idx, long long nnz, DimArr da, KeyFields kf,
+__global__ void build_keys_kernel(const IdxT* __restrict__ idx, long long nnz, DimArr da, ModeShift ms,
                                   K* __restrict__ out) {
     const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (i >= nnz) return;
-    unsigned long long f = static_cast<unsigned long long>(idx[i]);
-    int mi[8];
-    for (int m = 0; m < da.d; ++m) {
-        const unsigned long long q = f / static_cast<unsigned long long>(da.dims[m]);
-        mi[m] = static_cast<int>(f - q * static_cast<unsigned long long>(da.dims[m]));
-        f = q;
-    }
     unsigned long long key = 0;
-    for (int j = 0; j < kf.nf; ++j) key |= static_cast<unsigned long long>(mi[kf.mode[j]]) << kf.shift[j];
+    if (sizeof(IdxT) == 4) {  // 32-bit mixed-radix decode
+        unsigned f = static_cast<unsigned>(idx[i]);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            if (m >= da.d) break;
+            const unsigned q = f / static_cast<unsigned>(da.dims[m]);
+            const unsigned c = f - q * static_cast<unsigned>(da.dims[m]);
+            f = q;
+            if (ms.sh[m] >= 0) key |= static_cast<unsigned long long>(c) << ms.sh[m];
+        }
+    } else {
+        unsigned long long f = static_cast<unsigned long long>(idx[i]);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            if (m >= da.d) break;
+            const unsigned long long q = f / static_cast<unsigned long long>(da.dims[m]);
+            const unsigned long long c = f - q * static_cast<unsigned long long>(da.dims[m]);
+            f = q;
+            if (ms.sh[m] >= 0) key |= c << ms.sh[m];
+        }
+    }
     out[i] = static_cast<K>(key);
 }
 
@@ -395,20 +421,21 @@ void build_sorted(Ctx* ctx, const mach_sparse* X, const KeyFields& kf, int total
     const int ks = key64 ? 8 : 4;
     DBuf<unsigned char> kraw(ctx, static_cast<std::size_t>(nnz) * ks + 32);
     const int blocks = ceil_div(nnz, 256);
+    const ModeShift ms = mode_shift(kf);
     if (nnz > 0) {
         if (X->idx64) {
             if (key64) MB_LAUNCH(ctx, (build_keys_kernel<unsigned long long, unsigned long long>), blocks, 256, 0,
-                                 static_cast<const unsigned long long*>(X->idx), nnz, da, kf,
+                                 static_cast<const unsigned long long*>(X->idx), nnz, da, ms,
                                  reinterpret_cast<unsigned long long*>(kraw.get()));
             else MB_LAUNCH(ctx, (build_keys_kernel<unsigned long long, unsigned int>), blocks, 256, 0,
-                           static_cast<const unsigned long long*>(X->idx), nnz, da, kf,
+                           static_cast<const unsigned long long*>(X->idx), nnz, da, ms,
                            reinterpret_cast<unsigned int*>(kraw.get()));
         } else {
             if (key64) MB_LAUNCH(ctx, (build_keys_kernel<unsigned int, unsigned long long>), blocks, 256, 0,
-                                 static_cast<const unsigned int*>(X->idx), nnz, da, kf,
+                                 static_cast<const unsigned int*>(X->idx), nnz, da, ms,
                                  reinterpret_cast<unsigned long long*>(kraw.get()));
             else MB_LAUNCH(ctx, (build_keys_kernel<unsigned int, unsigned int>), blocks, 256, 0,
-                           static_cast<const unsigned int*>(X->idx), nnz, da, kf,
+                           static_cast<const unsigned int*>(X->idx), nnz, da, ms,
                            reinterpret_cast<unsigned int*>(kraw.get()));
         }
     }

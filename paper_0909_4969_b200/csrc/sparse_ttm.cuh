@@ -104,6 +104,8 @@ struct EigJob {
     const double* th0 = nullptr;  // Ritz values of X0 (warm start with them: filter first)
 };
 void eig_select_batched(Ctx* ctx, std::vector<EigJob> jobs);
+// multi-kernel subspace solver for G too large for one CTA's shared memory
+bool eig_large_batched(Ctx* ctx, const std::vector<EigJob>& jobs, int b);
 std::size_t eig_work_doubles(int n, int k);
 template <typename T>
 void gram(Ctx* ctx, const T* a, long long sk, long long sn, int K, int N, double* G);

@@ -235,3 +235,32 @@ def test_left_singular_basis_zero(mb):
     dev = mb.left_singular_basis(np.zeros((4, 3)), 4)
     assert dev.numerical_rank == 0 and dev.completed
     assert np.abs(dev.basis - np.eye(4)).max() == 0
+
+
+# ---------------------------------------------------------------------------
+# large row Grams: the multi-kernel eigensolver (n beyond one CTA's shared
+# memory) against the oracle and against the single-CTA global-memory solver
+# ---------------------------------------------------------------------------
+def _hosvd_env(mb, monkeypatch, st, ranks, **env):
+    monkeypatch.delenv("MACH_EIG_LARGE_OFF", raising=False)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    return mb.hosvd(st, ranks)
+
+
+@pytest.mark.parametrize("dims,ranks,p", [((300, 30, 40), (5, 4, 4), 0.2), ((600, 20, 24), (8, 3, 3), 0.3),
+                                          ((520, 16, 70), (10, 4, 6), 0.1),
+                                          ((300, 40, 40), (20, 6, 6), 0.2),    # block size 24
+                                          ((260, 36, 36), (28, 4, 4), 0.3)])   # block size 32
+def test_large_gram_eigensolver(mb, monkeypatch, dims, ranks, p):
+    x = lowrank_numpy(dims, ranks, 0.01, seed=4)
+    rng = np.random.default_rng(5)
+    keep = rng.random(x.size) < p
+    idx = np.flatnonzero(keep)
+    vals = x.reshape(-1, order="F")[idx]
+    st = mb.SparseTensor.from_entries(dims, idx, vals)
+    ref = O.hosvd(O.Sparse.from_entries(dims, idx, vals), list(ranks))
+    large = _hosvd_env(mb, monkeypatch, st, ranks)
+    assert_model_close(large, ref, 1e-9, 1e-9, 1e-12)
+    single = _hosvd_env(mb, monkeypatch, st, ranks, MACH_EIG_LARGE_OFF="1")
+    assert_model_close(single, ref, 1e-9, 1e-9, 1e-12)
