@@ -592,7 +592,11 @@ bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double
     // residual certificate: 1e-12 * theta_1 for fp64 data; fp32 data carry
     // ~6e-8 relative precision, so 1e-10 (eigenvector error ~1e-10 / gap)
     // is already four orders below the fp32 parity bar (sine <= 1e-3)
-    A.m = 4; A.maxit = 40; A.tol = sizeof(T) == 4 ? 1e-10 : 1e-12;
+    // Chebyshev degree: 4 from a cold block; 2 from the previous sweep's Ritz
+    // block, which one mild filter step already certifies (and whose
+    // filtered block CholQR makes orthonormal in one pass)
+    A.m = (X0 && x0_cols >= b) ? 2 : 4;
+    A.maxit = 40; A.tol = sizeof(T) == 4 ? 1e-10 : 1e-12;
     static const int ff = std::getenv("MACH_FILTER_FIRST") ? std::atoi(std::getenv("MACH_FILTER_FIRST")) : 0;
     A.filter_first = ff;
     A.X0 = X0; A.x0_cols = x0_cols; A.Xkeep = Xkeep;
