@@ -264,3 +264,30 @@ def test_large_gram_eigensolver(mb, monkeypatch, dims, ranks, p):
     assert_model_close(large, ref, 1e-9, 1e-9, 1e-12)
     single = _hosvd_env(mb, monkeypatch, st, ranks, MACH_EIG_LARGE_OFF="1")
     assert_model_close(single, ref, 1e-9, 1e-9, 1e-12)
+
+
+def test_mode_basis_fallback_inside_sweep_graph(mb, monkeypatch):
+    """The fused mode-basis kernel hands off to flag-gated fallback kernels
+    that sit in every sweep (and in the captured sweep graph); forcing the
+    fallback on every mode must give the same model as the fast path (and
+    the oracle)."""
+    dims, ranks, p, sweeps = (64, 64, 64), (10, 10, 10), 0.05, 5
+    x = lowrank_numpy(dims, ranks, 0.01, seed=1, dtype=np.float32)
+
+    def run(force):
+        if force:
+            monkeypatch.setenv("MACH_FORCE_MB_FALLBACK", "1")
+        else:
+            monkeypatch.delenv("MACH_FORCE_MB_FALLBACK", raising=False)
+        return mb.mach_hooi(mb.DenseTensor.from_numpy(x), ranks, mb.SparsifyConfig(p, 7),
+                            mb.HooiConfig(sweeps, 0.0)).model
+
+    fast, forced = run(False), run(True)
+    ref, _ = O.mach_hooi(O.Dense(x.astype(np.float64)), ranks, p, 7, sweeps, 0.0)
+    assert forced.iterations == fast.iterations >= 3  # >= 2 sweeps replayed from the graph
+    for a, b, r in zip(fast.factors, forced.factors, ref.factors):
+        assert subspace_sin(a, b) <= 1e-6
+        assert subspace_sin(b, r) <= 1e-3
+    assert np.allclose(forced.sweep_fits, fast.sweep_fits, rtol=1e-6, atol=0)
+    n = min(len(forced.sweep_fits), len(ref.sweep_fits))
+    assert np.allclose(forced.sweep_fits[:n], ref.sweep_fits[:n], rtol=1e-4, atol=0)
