@@ -725,7 +725,7 @@ static void dispatch_ttm(Ctx* ctx, const TtmArgs<T, IA>& A, int rab) {
 // row-major kernel copies (stride ttm_stride(r_m, sizeof(T))).
 template <typename T>
 void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks,
-                     const std::vector<const T*>& Ur, const T* one, T* Pbuf, T* Y) {
+                     const std::vector<const T*>& Ur, const T* one, T* Pbuf, T* Y, T* fseg, const int* fpos) {
     const int n = P.mode, a = P.a, b = P.b;
     const int ra = ranks[a];
     const int rb = (b >= 0) ? ranks[b] : 1;
@@ -745,6 +745,8 @@ void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, 
         A.sa = sa; A.sb = sb; A.C = C; A.P = Pbuf;
         A.ua_rows = dims[a];
         A.ub_elems = (b >= 0) ? static_cast<long long>(dims[b]) * A.rbs : 16 / static_cast<long long>(sizeof(T));
+        A.fseg = fseg;
+        A.fpos = fpos;
     };
     if (P.ia16) {
         TtmArgs<T, unsigned short> A{};
@@ -760,6 +762,190 @@ void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, 
     const long long tot = static_cast<long long>(dims[n]) * C;
     MB_LAUNCH(ctx, reduce_partials_kernel<T>, ceil_div(tot, 256), 256, 0, Pbuf, P.st_base.get(), dims[n], C, Y);
 }
+
+// ---- Y_(b) from the previous mode's fibre sums ------------------------------
+namespace {
+
+__global__ void seg_keys_kernel(const TtmTask* __restrict__ tasks, const int2* __restrict__ desc, long long n_task,
+                                int sentinel, int* __restrict__ key, int* __restrict__ id) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= n_task * 32) return;
+    const long long t = i >> 5;
+    const int lane = static_cast<int>(i & 31);
+    key[i] = lane < tasks[t].nseg ? desc[t * kDesc + lane].x : sentinel;
+    id[i] = static_cast<int>(i);
+}
+
+// ptr[r] = first position with key >= r (r = 0 .. rows)
+__global__ void seg_bounds_kernel(const int* __restrict__ key, long long n, int rows, int* __restrict__ ptr) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > rows) return;
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (key[mid] < r) lo = mid + 1;
+        else hi = mid;
+    }
+    ptr[r] = static_cast<int>(lo);
+}
+
+// inverse permutation (segment -> position) and each position's i_n
+__global__ void seg_pos_kernel(const int* __restrict__ ids, long long n, const TtmTask* __restrict__ tasks,
+                               int* __restrict__ pos, int* __restrict__ row) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int s = ids[i];
+    pos[s] = static_cast<int>(i);
+    row[i] = tasks[s >> 5].row;
+}
+
+// One CTA per output row i_b.  The row's fibre sums and their i_n are
+// contiguous (the TTM wrote them in i_b order) and U_n is small: all three
+// arrive by 1-D TMA bulk copies (16-byte-aligned supersets of the ranges),
+// chunk by chunk.  Thread t = g * ra + r_a (g < G groups) keeps the RN
+// accumulators of Y_(b)[i_b, (r_a, 0 .. rn)] in registers and takes the
+// chunk's segments j = g mod G (one fibre-sum value times one U_n row each);
+// the G partial rows are summed in group order at the end (deterministic).
+template <typename T, int RN>
+__global__ void __launch_bounds__(512) y_from_segments_kernel(const int* __restrict__ seg_ptr,
+                                                              const int* __restrict__ seg_row, const T* __restrict__ fseg,
+                                                              int ra, const T* __restrict__ Un, int rns, int rn, int sa,
+                                                              int sn, int rows, int un_rows, int chunk,
+                                                              T* __restrict__ Y) {
+    extern __shared__ __align__(128) unsigned char ysm[];
+    __shared__ __align__(8) std::uint64_t bar;
+    const int G = blockDim.x / ra;
+    const int tid = threadIdx.x;
+    const int g = tid / ra, r_a = tid - (tid / ra) * ra;
+    const bool on = g < G;
+    const std::size_t ub = static_cast<std::size_t>(un_rows) * rns * sizeof(T);  // multiple of 16
+    T* sU = reinterpret_cast<T*>(ysm);
+    unsigned char* sFb = ysm + ub;
+    unsigned char* sRb = sFb + ((static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16 + 15) & ~std::size_t(15));
+    T* part = reinterpret_cast<T*>(sRb + ((static_cast<std::size_t>(chunk) * sizeof(int) + 16 + 15) & ~std::size_t(15)));
+    if (tid == 0) {
+        ttm::mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int row = blockIdx.x;
+    const int s0 = seg_ptr[row], s1 = seg_ptr[row + 1];
+    T acc[RN];
+#pragma unroll
+    for (int q = 0; q < RN; ++q) acc[q] = T(0);
+    std::uint32_t phase = 0;
+    for (int base = s0, first = 1; base < s1 || first; base += chunk, first = 0) {
+        const int m = max(0, min(chunk, s1 - base));
+        const unsigned char* fsrc = reinterpret_cast<const unsigned char*>(fseg + static_cast<long long>(base) * ra);
+        const unsigned char* rsrc = reinterpret_cast<const unsigned char*>(seg_row + base);
+        const unsigned char* f0 = reinterpret_cast<const unsigned char*>(reinterpret_cast<std::uintptr_t>(fsrc) & ~std::uintptr_t(15));
+        const unsigned char* r0 = reinterpret_cast<const unsigned char*>(reinterpret_cast<std::uintptr_t>(rsrc) & ~std::uintptr_t(15));
+        const std::uint32_t fb = static_cast<std::uint32_t>(((fsrc - f0) + static_cast<std::size_t>(m) * ra * sizeof(T) + 15) & ~std::size_t(15));
+        const std::uint32_t rb = static_cast<std::uint32_t>(((rsrc - r0) + static_cast<std::size_t>(m) * sizeof(int) + 15) & ~std::size_t(15));
+        if (tid == 0) {
+            const std::uint32_t ubytes = first && un_rows > 0 ? static_cast<std::uint32_t>(ub) : 0u;
+            ttm::mbar_expect_tx(&bar, ubytes + (m ? fb + rb : 0u));
+            if (ubytes) ttm::bulk_g2s(sU, Un, ubytes, &bar);
+            if (m) {
+                ttm::bulk_g2s(sFb, f0, fb, &bar);
+                ttm::bulk_g2s(sRb, r0, rb, &bar);
+            }
+        }
+        ttm::mbar_wait(&bar, phase);
+        phase ^= 1u;
+        const T* sF = reinterpret_cast<const T*>(sFb + (fsrc - f0));
+        const int* sR = reinterpret_cast<const int*>(sRb + (rsrc - r0));
+        const T* U = un_rows > 0 ? sU : Un;
+        if (on) {
+            for (int j = g; j < m; j += G) {
+                const T fv = sF[j * ra + r_a];
+                const T* ur = U + sR[j] * rns;
+#pragma unroll
+                for (int q = 0; q < RN; ++q)
+                    if (q < rn) acc[q] = fma(fv, ur[q], acc[q]);
+            }
+        }
+        __syncthreads();  // the next chunk's bulk copies overwrite sF / sR
+    }
+    const int C = ra * rn;
+    if (on)
+#pragma unroll
+        for (int q = 0; q < RN; ++q)
+            if (q < rn) part[g * C + r_a + q * ra] = acc[q];
+    __syncthreads();
+    for (int cc = tid; cc < C; cc += blockDim.x) {
+        T s = T(0);
+        for (int q = 0; q < G; ++q) s += part[q * C + cc];
+        const int a_ = cc % ra, n_ = cc / ra;
+        Y[row + static_cast<long long>(a_ * sa + n_ * sn) * rows] = s;
+    }
+}
+
+}  // namespace
+
+bool build_segment_groups(Ctx* ctx, ModePlan& P, int b_rows) {
+    if (P.b < 0) return false;
+    if (P.seg_ptr.get()) return true;
+    const long long nslot = P.n_task * 32;
+    DBuf<int> key(ctx, nslot + 1), id(ctx, nslot + 1), skey(ctx, nslot + 1), sid(ctx, nslot + 1);
+    P.seg_pos.alloc(ctx, nslot + 1);
+    P.seg_row.alloc(ctx, nslot + 8);  // +8: bulk copies read 16-byte-aligned supersets
+    P.seg_ptr.alloc(ctx, b_rows + 1);
+    if (nslot > 0) {
+        MB_LAUNCH(ctx, seg_keys_kernel, ceil_div(nslot, 256), 256, 0, P.tasks.get(), P.desc.get(), P.n_task, b_rows,
+                  key.get(), id.get());
+        std::size_t tmp = 0;
+        const int bits = bits_for(b_rows + 1);
+        MB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.get(), skey.get(), id.get(), sid.get(), nslot, 0, bits,
+                                                ctx->stream));
+        DBuf<unsigned char> t(ctx, tmp);
+        MB_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, key.get(), skey.get(), id.get(), sid.get(), nslot, 0, bits,
+                                                ctx->stream));
+        ctx->launches += 4;
+        MB_LAUNCH(ctx, seg_pos_kernel, ceil_div(nslot, 256), 256, 0, sid.get(), nslot, P.tasks.get(), P.seg_pos.get(),
+                  P.seg_row.get());
+    }
+    MB_LAUNCH(ctx, seg_bounds_kernel, ceil_div(b_rows + 1, 256), 256, 0, skey.get(), nslot, b_rows, P.seg_ptr.get());
+    return true;
+}
+
+template <typename T>
+void y_from_segments(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks, const T* fseg,
+                     const T* Un, T* Y) {
+    const int n = P.mode, a = P.a, b = P.b;
+    const int rows = dims[b];
+    build_segment_groups(ctx, P, rows);
+    const int ra = ranks[a], rn = ranks[n];
+    int sa, sn;  // Y_(b) columns: the two remaining modes, earliest fastest
+    if (a < n) { sa = 1; sn = ra; }
+    else { sn = 1; sa = rn; }
+    const int threads = (512 / ra) * ra;  // whole groups of ra threads
+    const int G = threads / ra;
+    const int rns = ttm_stride(rn, sizeof(T));
+    const std::size_t ubytes = static_cast<std::size_t>(dims[n]) * rns * sizeof(T);
+    const bool stage = ubytes <= 64 * 1024;
+    const int chunk = static_cast<int>(std::min<std::size_t>(2048, (48 * 1024) / (ra * sizeof(T))));
+    const std::size_t smem = (stage ? ubytes : 0) + ((static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16 + 15) & ~std::size_t(15)) +
+                             ((static_cast<std::size_t>(chunk) * sizeof(int) + 16 + 15) & ~std::size_t(15)) +
+                             static_cast<std::size_t>(G) * ra * rn * sizeof(T);
+    auto launch = [&](auto kern) {
+        MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        MB_LAUNCH(ctx, kern, rows, threads, smem, P.seg_ptr.get(), P.seg_row.get(), fseg, ra, Un, rns, rn, sa, sn, rows,
+                  stage ? dims[n] : 0, chunk, Y);
+    };
+    // RN >= rn register accumulators
+    if (rn <= 4) launch(y_from_segments_kernel<T, 4>);
+    else if (rn <= 8) launch(y_from_segments_kernel<T, 8>);
+    else if (rn <= 12) launch(y_from_segments_kernel<T, 12>);
+    else if (rn <= 16) launch(y_from_segments_kernel<T, 16>);
+    else if (rn <= 24) launch(y_from_segments_kernel<T, 24>);
+    else launch(y_from_segments_kernel<T, 32>);
+}
+
+template void y_from_segments<float>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&, const float*,
+                                     const float*, float*);
+template void y_from_segments<double>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&, const double*,
+                                      const double*, double*);
 
 // ---- sparse HOSVD Grams ----------------------------------------------------
 template <typename T>
@@ -843,9 +1029,11 @@ void sparse_times(Ctx* ctx, const mach_sparse* X, const ModePlan& P, const doubl
 template std::shared_ptr<ModePlan> get_plan<float>(mach_sparse*, int, const std::vector<int>&);
 template std::shared_ptr<ModePlan> get_plan<double>(mach_sparse*, int, const std::vector<int>&);
 template void sparse_mode_ttm<float>(Ctx*, const ModePlan&, const std::vector<int>&, const std::vector<int>&,
-                                     const std::vector<const float*>&, const float*, float*, float*);
+                                     const std::vector<const float*>&, const float*, float*, float*, float*,
+                                     const int*);
 template void sparse_mode_ttm<double>(Ctx*, const ModePlan&, const std::vector<int>&, const std::vector<int>&,
-                                      const std::vector<const double*>&, const double*, double*, double*);
+                                      const std::vector<const double*>&, const double*, double*, double*, double*,
+                                      const int*);
 template void sparse_row_gram<float>(Ctx*, const mach_sparse*, int, double, double*);
 template void sparse_row_gram<double>(Ctx*, const mach_sparse*, int, double, double*);
 template void sparse_col_gram<float>(Ctx*, const mach_sparse*, const ModePlan&, long long, double, double*);

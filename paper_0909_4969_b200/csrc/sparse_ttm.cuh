@@ -41,6 +41,8 @@ struct TtmArgs {
     int n_cons, n_slot;            // consumer warps, task slots of the TMA ring
     int dbg;                       // experiments: 1 = stream only (no arithmetic)
     unsigned long long* ts;        // experiments: per-CTA %globaltimer stamps (8 per CTA) or null
+    T* fseg;                       // optional: every segment's fibre sum (ra values at fpos[t * 32 + lane] * ra)
+    const int* fpos;               // position of each segment in the i_b-grouped order (with fseg)
 };
 
 // Per-mode sorted layout of a sampled tensor (built once, reused by HOSVD and
@@ -59,7 +61,13 @@ struct ModePlan {
     DBuf<TtmTask> tasks;
     DBuf<int2> desc;
     DBuf<int> st_base;             // tasks of row r: [st_base[r], st_base[r+1])
+    // segments grouped by their i_b (built on first use): the fibre sums of
+    // this mode's TTM give mode b's Y_(b) without another pass over X
+    DBuf<int> seg_pos, seg_ptr;    // segment t * 32 + lane -> position in i_b order; row i_b: [seg_ptr[i], seg_ptr[i+1])
+    DBuf<int> seg_row;             // i_n (this mode's row) of the segment at each position
 };
+// group P's segments by i_b (once); false when P has no b mode
+bool build_segment_groups(Ctx* ctx, ModePlan& P, int b_rows);
 
 // ---- sparse route ----
 bool sparse_fast_path_ok(const std::vector<int>& dims, const std::vector<int>& ranks);
@@ -69,7 +77,15 @@ template <typename T>
 std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>& ranks);
 template <typename T>
 void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks,
-                     const std::vector<const T*>& Ur, const T* one, T* Pbuf, T* Y);
+                     const std::vector<const T*>& Ur, const T* one, T* Pbuf, T* Y, T* fseg = nullptr,
+                     const int* fpos = nullptr);
+// Y_(b) (b = P.b) from the fibre sums F (= X x_a U_a, one ra-vector per
+// segment of P's TTM, written by sparse_mode_ttm with fseg) and U_n (row-major
+// kernel copy of mode P.mode's factor): Y_(b)[i_b, :] = sum over the segments
+// s with i_b(s) = i_b of F_s (x) U_n[i_n(s), :], segments in a fixed order.
+template <typename T>
+void y_from_segments(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks, const T* fseg,
+                     const T* Un, T* Y);
 template <typename T>
 void sparse_row_gram(Ctx* ctx, const mach_sparse* X, int n, double normX2, double* G);
 template <typename T>

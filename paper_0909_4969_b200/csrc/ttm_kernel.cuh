@@ -254,6 +254,19 @@ __global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
                 if (act[k]) gather_fma(f, ix[k], vx[k]);
         }
 
+        if (A.fseg && lane < tk.nseg) {  // fibre sums for the next mode (y_from_segments)
+            T* o = A.fseg + static_cast<long long>(A.fpos[t * 32 + lane]) * A.ra;
+            if (sizeof(T) == 4 && (A.ra & 1) == 0) {  // 8-byte stores (pos * ra even: 8-byte aligned)
+#pragma unroll
+                for (int a = 0; a < RA; a += 2)
+                    if (a < A.ra) *reinterpret_cast<float2*>(o + a) = make_float2(f[a], f[a + 1]);
+            } else {
+#pragma unroll
+                for (int a = 0; a < RA; ++a)
+                    if (a < A.ra) o[a] = f[a];
+            }
+        }
+
         // ---- stage 2: sum_s f_s (x) U_b[i_b(s), :] over the task's segments ----
         {
             T* fr = F + lane * FS_;

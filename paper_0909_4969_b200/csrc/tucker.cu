@@ -477,8 +477,36 @@ struct SparseSession : SessionBase {
                            ranks[static_cast<std::size_t>(m)], ttm_stride(ranks[static_cast<std::size_t>(m)], sizeof(T)),
                            Ur[static_cast<std::size_t>(m)].get());
     }
+    // Fibre-sum reuse (d = 3): when mode m's layout has b = m + 1, its TTM
+    // also writes every segment's fibre sum F = X x_a U_a, and Y_(m+1) is
+    // formed from F and the freshly updated U_m instead of a second pass over
+    // X.  F stays valid while U_a is unchanged: a != m, m + 1, and mode a is
+    // not updated between the two projections of a sweep.
+    DBuf<T> fseg;
+    int fseg_for = -1;  // mode whose Y_(.) the current fibre sums give (-1: none)
+    bool fseg_use(int m) const {
+        static const bool off = std::getenv("MACH_NO_FIBRE_REUSE") != nullptr;
+        if (off || d != 3 || m + 1 >= d) return false;
+        return plans[static_cast<std::size_t>(m)]->b == m + 1;
+    }
     void mode_y(int m) {
-        sparse_mode_ttm<T>(ctx, *plans[static_cast<std::size_t>(m)], dims, ranks, Urp, one.get(), Pbuf.get(), Y.get());
+        const std::size_t sm = static_cast<std::size_t>(m);
+        if (m >= 1 && fseg_for == m) {
+            y_from_segments<T>(ctx, *plans[sm - 1], dims, ranks, fseg.get(), Urp[sm - 1], Y.get());
+            return;
+        }
+        T* fs_out = nullptr;
+        const int* fpos = nullptr;
+        if (fseg_use(m)) {
+            auto& P = *plans[sm];
+            build_segment_groups(ctx, P, dims[static_cast<std::size_t>(P.b)]);
+            const std::size_t need = static_cast<std::size_t>(P.n_task) * 32 * ranks[static_cast<std::size_t>(P.a)];
+            if (fseg.n < need + 16) fseg.alloc(ctx, need + 16);  // slack: bulk copies read aligned supersets
+            fs_out = fseg.get();
+            fpos = P.seg_pos.get();
+        }
+        sparse_mode_ttm<T>(ctx, *plans[sm], dims, ranks, Urp, one.get(), Pbuf.get(), Y.get(), fs_out, fpos);
+        fseg_for = fs_out ? m + 1 : -1;
     }
     // core from the last mode's projection (which already carries every other
     // updated factor), then fit = 1 - sqrt(|X|^2 - |G|^2)/|X| (orthonormal
@@ -529,6 +557,7 @@ struct SparseSession : SessionBase {
         fit = prev_fit = init->fit;
         sweep_fits.assign(1, fit);
         warnings = init->warnings;
+        fseg_for = -1;
     }
     void setup(mach_sparse* sp, const std::vector<int>& rk) {
         X = sp;
@@ -618,6 +647,7 @@ struct SparseSession : SessionBase {
             refresh(m);
         }
         warnings = read_warnings(ctx, fs.st, ranks, all);
+        fseg_for = -1;
         mode_y(d - 1);
         fit = prev_fit = core_and_fit();
         hosvd_ms = tm.stop_ms();
@@ -627,6 +657,7 @@ struct SparseSession : SessionBase {
     void mode_update(int i) {
         static const bool nofuse = std::getenv("MACH_NO_FUSED_BASIS") != nullptr;
         const std::size_t si = static_cast<std::size_t>(i);
+        if (fseg_for >= 1 && plans[static_cast<std::size_t>(fseg_for - 1)]->a == i) fseg_for = -1;  // F used U_i
         if (!nofuse && lsb_fused<T>(ctx, Y.get(), dims[si], C[si], ranks[si], fs.U[si].get(), sv_at(i),
                                     fs.st.get() + 3 * i, &warm[si], fs.U[si].get(), Ur[si].get(),
                                     ttm_stride(ranks[si], sizeof(T))))
