@@ -598,7 +598,10 @@ bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double
     // filtered block CholQR makes orthonormal in one pass)
     A.m = (X0 && x0_cols >= b) ? 2 : 4;
     A.maxit = 40; A.tol = sizeof(T) == 4 ? 1e-10 : 1e-12;
-    static const int ff = std::getenv("MACH_FILTER_FIRST") ? std::atoi(std::getenv("MACH_FILTER_FIRST")) : 0;
+    // warm start: one degree-2 filter step bounded by the previous Ritz values
+    // before the first Rayleigh-Ritz (the previous block's residual against
+    // the new G never passes the certificate, so that Rayleigh-Ritz is skipped)
+    static const int ff = std::getenv("MACH_FILTER_FIRST") ? std::atoi(std::getenv("MACH_FILTER_FIRST")) : 1;
     A.filter_first = ff;
     A.X0 = X0; A.x0_cols = x0_cols; A.Xkeep = Xkeep;
     A.U = U; A.sv = sv; A.st = st; A.Ur = Ur;

@@ -906,6 +906,10 @@ bool build_segment_groups(Ctx* ctx, ModePlan& P, int b_rows) {
                   P.seg_row.get());
     }
     MB_LAUNCH(ctx, seg_bounds_kernel, ceil_div(b_rows + 1, 256), 256, 0, skey.get(), nslot, b_rows, P.seg_ptr.get());
+    int nseg = 0;
+    to_host(ctx, &nseg, P.seg_ptr.get() + b_rows, 1);
+    sync(ctx);
+    P.n_seg = nseg;
     return true;
 }
 

@@ -65,6 +65,7 @@ struct ModePlan {
     // this mode's TTM give mode b's Y_(b) without another pass over X
     DBuf<int> seg_pos, seg_ptr;    // segment t * 32 + lane -> position in i_b order; row i_b: [seg_ptr[i], seg_ptr[i+1])
     DBuf<int> seg_row;             // i_n (this mode's row) of the segment at each position
+    long long n_seg = -1;          // segments (valid positions), known once grouped
 };
 // group P's segments by i_b (once); false when P has no b mode
 bool build_segment_groups(Ctx* ctx, ModePlan& P, int b_rows);

@@ -743,13 +743,20 @@ struct SparseSession : SessionBase {
     // bytes one mode-n TTM launch must move: per nonzero the inner index and
     // the value, per task its record and descriptor, per task the partial
     // row block it writes (the factor rows come from L2, not counted)
+    // algorithmic bytes of mode m's TTM launch in a steady sweep; -1 when the
+    // mode runs no TTM (its Y_(m) comes from the previous mode's fibre sums)
     long long ttm_bytes(int m) const override {
         if (m < 0 || m >= d || !plans[static_cast<std::size_t>(m)]) return -1;
+        if (m >= 1 && fseg_use(m - 1)) return -1;
         const ModePlan& P = *plans[static_cast<std::size_t>(m)];
         const long long nnz = X->nnz;
-        return nnz * ((P.ia16 ? 2 : 4) + static_cast<long long>(sizeof(T))) +
-               P.n_task * (static_cast<long long>(kDesc * sizeof(int2) + sizeof(TtmTask)) +
-                           static_cast<long long>(C[static_cast<std::size_t>(m)]) * static_cast<long long>(sizeof(T)));
+        long long b = nnz * ((P.ia16 ? 2 : 4) + static_cast<long long>(sizeof(T))) +
+                      P.n_task * (static_cast<long long>(kDesc * sizeof(int2) + sizeof(TtmTask)) +
+                                  static_cast<long long>(C[static_cast<std::size_t>(m)]) * static_cast<long long>(sizeof(T)));
+        if (fseg_use(m) && P.n_seg > 0)  // + the fibre sums written (and their positions read)
+            b += P.n_task * 32 * static_cast<long long>(sizeof(int)) +
+                 P.n_seg * ranks[static_cast<std::size_t>(P.a)] * static_cast<long long>(sizeof(T));
+        return b;
     }
 };
 
