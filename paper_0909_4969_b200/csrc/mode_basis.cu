@@ -74,6 +74,12 @@ struct MBLayout {
     static std::size_t bytes(int n, int ch) { return 8 * std::max(cta0(n), block(n, ch)) + 16; }
 };
 
+__device__ __forceinline__ unsigned long long mb_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <int B, typename T>
 __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, long long* tstamp) {
     cg::cluster_group cluster = cg::this_cluster();
@@ -92,6 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
         tstamp[160 + rank] = t_;
     }
+    long long* tsa = tstamp;          // rank-1 phase-D stamps at [219..223]
     if (rank != 0) tstamp = nullptr;  // the stamps follow CTA 0
     MB_STAMP(0);
 
@@ -134,26 +141,47 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
             }
         }
         __syncthreads();
+        // lower triangle of 8x8 tiles in 2x2 macro tiles: each k-step loads two
+        // A and two B fragments for up to four MMAs (half the shared-memory
+        // fragment traffic of one tile at a time)
         const int nts = npad / 8;
-        for (int t = warp; t < nts * (nts + 1) / 2; t += kThreads / 32) {
-            int ti = 0;
-            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-            const int tj = t - ti * (ti + 1) / 2;
-            double c0 = 0.0, c1 = 0.0;
-            const double* pa = Yb + tq * YS + ti * 8 + gr;
-            const double* pb = Yb + tq * YS + tj * 8 + gr;
-#pragma unroll 4
-            for (int k0 = 0; k0 < nr4; k0 += 4) dmma(c0, c1, pa[k0 * YS], pb[k0 * YS]);
-            const int r = ti * 8 + gr;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int c = tj * 8 + 2 * tq + e;
-                const double v = e ? c1 : c0;
-                if (ti != tj || r >= c) {
-                    P[r + c * ldg] = v;
-                    P[c + r * ldg] = v;
-                }
+        const int nm = (nts + 1) / 2;
+        for (int t = warp; t < nm * (nm + 1) / 2; t += kThreads / 32) {
+            int I = 0;
+            while ((I + 1) * (I + 2) / 2 <= t) ++I;
+            const int J = t - I * (I + 1) / 2;
+            const int ti0 = 2 * I, tj0 = 2 * J;
+            const bool i1 = ti0 + 1 < nts, j1 = tj0 + 1 < nts;
+            double c[2][2][2] = {{{0, 0}, {0, 0}}, {{0, 0}, {0, 0}}};
+            const double* pa0 = Yb + tq * YS + ti0 * 8 + gr;
+            const double* pa1 = pa0 + (i1 ? 8 : 0);
+            const double* pb0 = Yb + tq * YS + tj0 * 8 + gr;
+            const double* pb1 = pb0 + (j1 ? 8 : 0);
+#pragma unroll 2
+            for (int k0 = 0; k0 < nr4; k0 += 4) {
+                const double a0 = pa0[k0 * YS], a1 = pa1[k0 * YS], b0 = pb0[k0 * YS], b1 = pb1[k0 * YS];
+                dmma(c[0][0][0], c[0][0][1], a0, b0);
+                dmma(c[1][0][0], c[1][0][1], a1, b0);
+                dmma(c[1][1][0], c[1][1][1], a1, b1);
+                if (I != J) dmma(c[0][1][0], c[0][1][1], a0, b1);
             }
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    const int ti = ti0 + a, tj = tj0 + b;
+                    if (ti >= nts || tj >= nts || tj > ti) continue;
+                    const int r = ti * 8 + gr;
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int cc = tj * 8 + 2 * tq + e;
+                        const double v = c[a][b][e];
+                        if (ti != tj || r >= cc) {
+                            P[r + cc * ldg] = v;
+                            P[cc + r * ldg] = v;
+                        }
+                    }
+                }
         }
     }
     cluster.sync();  // #1: partials complete
@@ -220,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
     cluster.sync();  // #3: V (or a fallback decision) ready
     MB_STAMP(3);
 
+    if (tsa && rank == 1 && threadIdx.x == 0) tsa[219] = static_cast<long long>(mb_gtimer());
     const int mode = *cluster.map_shared_rank(&mflag, 0);
     if (mode >= 2) {  // eigen fallback or zero matrix: the unfused kernels finish
         if (rank == 0 && threadIdx.x == 0) {
@@ -254,15 +283,33 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
             Vl[r * VS + j] = (r < n && j < k) ? Xr[r * XS + j] : 0.0;
         }
         __syncthreads();
+        if (tsa && rank == 1 && threadIdx.x == 0) tsa[220] = static_cast<long long>(mb_gtimer());
         // W (nr8 x KP) = Yb (nr8 x npad) Vl (npad x KP): warp per 8-row tile
         for (int rt = warp; rt < nr8 / 8; rt += kThreads / 32) {
+            // two accumulator sets (even / odd k-steps): twice the independent MMA chains
             double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+            double d[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
             const double* ya = Yb + (rt * 8 + gr) * YS + tq;
-            for (int k0 = 0; k0 < npad; k0 += 4) {
+            int k0 = 0;
+            for (; k0 + 8 <= npad; k0 += 8) {
+                const double a0 = ya[k0], a1 = ya[k0 + 4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (t * 8 < KP) {
+                        dmma(c[t][0], c[t][1], a0, Vl[(k0 + tq) * VS + t * 8 + gr]);
+                        dmma(d[t][0], d[t][1], a1, Vl[(k0 + 4 + tq) * VS + t * 8 + gr]);
+                    }
+            }
+            for (; k0 < npad; k0 += 4) {
                 const double av = ya[k0];
 #pragma unroll
                 for (int t = 0; t < 4; ++t)
                     if (t * 8 < KP) dmma(c[t][0], c[t][1], av, Vl[(k0 + tq) * VS + t * 8 + gr]);
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                c[t][0] += d[t][0];
+                c[t][1] += d[t][1];
             }
 #pragma unroll
             for (int t = 0; t < 4; ++t)
@@ -410,8 +457,11 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
         return ok;
     };
 
+    if (tsa && rank == 1 && threadIdx.x == 0) tsa[221] = static_cast<long long>(mb_gtimer());
     if (rank > 0) block_gram(Wb);
+    if (tsa && rank == 1 && threadIdx.x == 0) tsa[222] = static_cast<long long>(mb_gtimer());
     cluster.sync();  // #4
+    if (tsa && rank == 1 && threadIdx.x == 0) tsa[223] = static_cast<long long>(mb_gtimer());
     MB_STAMP(4);
     if (rank == 0) {
         const bool fast = diag_fast();
@@ -575,6 +625,8 @@ bool launch_mode_basis(Ctx* ctx, MBArgs<T> A) {
         for (int q = 1; q < CL; ++q) { emin = std::min(emin, h[160 + q]); emax = std::max(emax, h[160 + q]); }
         std::fprintf(stderr, " | end-start %.1fus | CTA entry spread %.1fus, CTA0 - first %.1fus\n", (h[238] - h[1]) * 1e-3,
                      (emax - emin) * 1e-3, (h[160] - emin) * 1e-3);
+        std::fprintf(stderr, "[mb-t] D(rank1): vload %.1f W %.1f bgram %.1f csync %.1f\n", (h[220] - h[219]) * 1e-3,
+                     (h[221] - h[220]) * 1e-3, (h[222] - h[221]) * 1e-3, (h[223] - h[222]) * 1e-3);
     }
     return true;
 }
