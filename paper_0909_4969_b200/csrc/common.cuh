@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -112,6 +113,38 @@ inline bool max_carveout(const void* f) {
             MB_CUDA(cudaEventRecord(pe_.b, (ctx)->stream));                                          \
             (ctx)->pending.push_back(pe_);                                                           \
         }                                                                                            \
+    } while (0)
+
+// Programmatic dependent launch for the sweep's kernel chain: the launch of
+// kernel N+1 (and its CTAs' prologue) overlaps kernel N; every kernel launched
+// this way starts with pdl_enter(), whose griddepcontrol.wait blocks until the
+// predecessor grid has completed and its writes are visible (a no-op when the
+// kernel was launched without the attribute).  MACH_NO_PDL=1 disables it.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+inline bool pdl_on() {
+    static const bool off = std::getenv("MACH_NO_PDL") != nullptr;
+    return !off;
+}
+#define MB_LAUNCH_PDL(ctx, kernel, grid, block, smem, ...)                                           \
+    do {                                                                                             \
+        if (!::machb::pdl_on()) {                                                                    \
+            MB_LAUNCH(ctx, kernel, grid, block, smem, __VA_ARGS__);                                  \
+            break;                                                                                   \
+        }                                                                                            \
+        cudaLaunchConfig_t cfg_{};                                                                   \
+        cfg_.gridDim = dim3(grid);                                                                   \
+        cfg_.blockDim = dim3(block);                                                                 \
+        cfg_.dynamicSmemBytes = (smem);                                                              \
+        cfg_.stream = (ctx)->stream;                                                                 \
+        cudaLaunchAttribute at_[1];                                                                  \
+        at_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                              \
+        at_[0].val.programmaticStreamSerializationAllowed = 1;                                       \
+        cfg_.attrs = at_;                                                                            \
+        cfg_.numAttrs = 1;                                                                           \
+        MB_LAUNCH_EX(ctx, #kernel, &cfg_, kernel, __VA_ARGS__);                                      \
     } while (0)
 
 // Stream-ordered device allocation owned by RAII.

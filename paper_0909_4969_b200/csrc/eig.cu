@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kEigThreads) eig_topk_kernel(const double* __r
                                                                double* __restrict__ work, double* __restrict__ V,
                                                                double* __restrict__ sig, int* __restrict__ status,
                                                                const int* __restrict__ skip) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     if (skip && skip[0] == 1) return;  // the subspace solver already converged
     extern __shared__ double sm[];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -362,7 +363,7 @@ void eig_topk(Ctx* ctx, const double* G, int n, int k, double* work, double* V, 
         attr_set = true;
     }
     if (smem > 227 * 1024) throw Error(MACH_ERR_INTERNAL, "eigen step too large for one CTA (n=" + std::to_string(n) + ")");
-    MB_LAUNCH(ctx, eig_topk_kernel, 1, kEigThreads, smem, G, n, k, work, V, sig, status, skip);
+    MB_LAUNCH_PDL(ctx, eig_topk_kernel, 1, kEigThreads, smem, G, n, k, work, V, sig, status, skip);
 }
 
 }  // namespace machb

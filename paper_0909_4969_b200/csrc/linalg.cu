@@ -243,6 +243,7 @@ template void gram<double>(Ctx*, const double*, long long, long long, int, int, 
 template <typename T, int KC>
 __global__ void __launch_bounds__(128) matmul_yv_kernel(const T* __restrict__ Y, int rows, int C, const double* __restrict__ V,
                                                         int kc, double* __restrict__ W, const int* __restrict__ need) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     if (need && need[0] == 0) return;
     // thread per row of W; V staged in shared memory (broadcast reads); the
     // column loop streams Y column by column (coalesced across the rows)
@@ -269,6 +270,7 @@ __global__ void __launch_bounds__(128) matmul_yv_kernel(const T* __restrict__ Y,
 template <typename T>
 __global__ void matmul_yv_generic_kernel(const T* __restrict__ Y, int rows, int C, const double* __restrict__ V, int kc,
                                          double* __restrict__ W, const int* __restrict__ need) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     if (need && need[0] == 0) return;
     const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (idx >= static_cast<long long>(rows) * kc) return;
@@ -285,12 +287,12 @@ void matmul_yv_gated(Ctx* ctx, const T* Y, int rows, int C, const double* V, int
     const std::size_t vsm = static_cast<std::size_t>(C) * kc * sizeof(double);
     if (kc <= 32 && vsm <= 48 * 1024) {
         if (kc <= 16)
-            MB_LAUNCH(ctx, (matmul_yv_kernel<T, 16>), ceil_div(rows, 128), 128, vsm, Y, rows, C, V, kc, W, need);
+            MB_LAUNCH_PDL(ctx, (matmul_yv_kernel<T, 16>), ceil_div(rows, 128), 128, vsm, Y, rows, C, V, kc, W, need);
         else
-            MB_LAUNCH(ctx, (matmul_yv_kernel<T, 32>), ceil_div(rows, 128), 128, vsm, Y, rows, C, V, kc, W, need);
+            MB_LAUNCH_PDL(ctx, (matmul_yv_kernel<T, 32>), ceil_div(rows, 128), 128, vsm, Y, rows, C, V, kc, W, need);
         return;
     }
-    MB_LAUNCH(ctx, matmul_yv_generic_kernel<T>, ceil_div(n, 256), 256, 0, Y, rows, C, V, kc, W, need);
+    MB_LAUNCH_PDL(ctx, matmul_yv_generic_kernel<T>, ceil_div(n, 256), 256, 0, Y, rows, C, V, kc, W, need);
 }
 
 template <typename T>
@@ -344,6 +346,7 @@ __global__ void __launch_bounds__(kB) basis_from_products_kernel(const double* _
                                                                  const int* __restrict__ eig_status,
                                                                  double* __restrict__ U, double* __restrict__ sv,
                                                                  int* __restrict__ st, const int* __restrict__ skip) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     if (skip && skip[0] == 0) return;  // the CholQR2 fast path already produced U
     extern __shared__ double sm[];
     double* v = sm;
@@ -522,7 +525,7 @@ __global__ void __launch_bounds__(kB) basis_products_fast_kernel(const double* _
 
 void basis_from_products_gated(Ctx* ctx, const double* W, int n, int wc, int k, const double* sig,
                                const int* eig_status, double* U, double* sv, int* st, const int* need) {
-    MB_LAUNCH(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st, need);
+    MB_LAUNCH_PDL(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st, need);
 }
 
 void basis_from_products(Ctx* ctx, const double* W, int n, int wc, int k, const double* sig, const int* eig_status,
@@ -536,11 +539,11 @@ void basis_from_products(Ctx* ctx, const double* W, int n, int wc, int k, const 
         }
         DBuf<int> slow(ctx, 1);
         MB_LAUNCH(ctx, basis_products_fast_kernel, 1, kB, fsm, W, n, k, sig, U, sv, st, slow.get());
-        MB_LAUNCH(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st,
+        MB_LAUNCH_PDL(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st,
                   static_cast<const int*>(slow.get()));
         return;
     }
-    MB_LAUNCH(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st,
+    MB_LAUNCH_PDL(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st,
               static_cast<const int*>(nullptr));
 }
 
@@ -565,6 +568,7 @@ __global__ void identity_basis_kernel(double* U, int n, int k, double* sv, int* 
 template <typename T>
 __global__ void core_from_last_kernel(const T* __restrict__ Y, int rows, int C, const double* __restrict__ U, int r,
                                       double* __restrict__ core) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= C * r) return;
     const int col = warp % C, alpha = warp / C;
@@ -579,7 +583,7 @@ __global__ void core_from_last_kernel(const T* __restrict__ Y, int rows, int C, 
 template <typename T>
 void core_from_last(Ctx* ctx, const T* Y, int rows, int C, const double* U, int r, double* core) {
     const long long warps = static_cast<long long>(C) * r;
-    MB_LAUNCH(ctx, core_from_last_kernel<T>, ceil_div(warps * 32, 256), 256, 0, Y, rows, C, U, r, core);
+    MB_LAUNCH_PDL(ctx, core_from_last_kernel<T>, ceil_div(warps * 32, 256), 256, 0, Y, rows, C, U, r, core);
 }
 template void core_from_last<float>(Ctx*, const float*, int, int, const double*, int, double*);
 template void core_from_last<double>(Ctx*, const double*, int, int, const double*, int, double*);
@@ -591,6 +595,7 @@ constexpr int kRedBlocks = 1024;
 
 template <typename T>
 __global__ void __launch_bounds__(256) sumsq_partial_kernel(const T* __restrict__ x, long long n, double* __restrict__ part) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     __shared__ double red[8];
     double s = 0.0;
     for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += 256ll * kRedBlocks) {
@@ -609,6 +614,7 @@ __global__ void __launch_bounds__(256) sumsq_partial_kernel(const T* __restrict_
 }
 
 __global__ void __launch_bounds__(256) sum_final_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     __shared__ double red[8];
     double s = 0.0;
     for (int i = threadIdx.x; i < n; i += 256) s += part[i];
@@ -625,8 +631,8 @@ __global__ void __launch_bounds__(256) sum_final_kernel(const double* __restrict
 
 template <typename T>
 void sumsq(Ctx* ctx, const T* x, long long n, double* scratch /* >= kRedBlocks */, double* out) {
-    MB_LAUNCH(ctx, sumsq_partial_kernel<T>, kRedBlocks, 256, 0, x, n, scratch);
-    MB_LAUNCH(ctx, sum_final_kernel, 1, 256, 0, scratch, kRedBlocks, out);
+    MB_LAUNCH_PDL(ctx, sumsq_partial_kernel<T>, kRedBlocks, 256, 0, x, n, scratch);
+    MB_LAUNCH_PDL(ctx, sum_final_kernel, 1, 256, 0, scratch, kRedBlocks, out);
 }
 template void sumsq<float>(Ctx*, const float*, long long, double*, double*);
 template void sumsq<double>(Ctx*, const double*, long long, double*, double*);
@@ -639,6 +645,7 @@ int sumsq_scratch() { return kRedBlocks; }
 template <typename T>
 __global__ void factor_rowmajor_kernel(const double* __restrict__ U, int n, int r, int rs, T* __restrict__ out,
                                        const int* __restrict__ need) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     if (need && need[0] == 0) return;
     const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (idx >= static_cast<long long>(n) * rs) return;
@@ -649,7 +656,7 @@ __global__ void factor_rowmajor_kernel(const double* __restrict__ U, int n, int 
 template <typename T>
 void factor_rowmajor_gated(Ctx* ctx, const double* U, int n, int r, int rs, T* out, const int* need) {
     const long long tot = static_cast<long long>(n) * rs;
-    MB_LAUNCH(ctx, factor_rowmajor_kernel<T>, ceil_div(tot, 256), 256, 0, U, n, r, rs, out, need);
+    MB_LAUNCH_PDL(ctx, factor_rowmajor_kernel<T>, ceil_div(tot, 256), 256, 0, U, n, r, rs, out, need);
 }
 template void factor_rowmajor_gated<float>(Ctx*, const double*, int, int, int, float*, const int*);
 template void factor_rowmajor_gated<double>(Ctx*, const double*, int, int, int, double*, const int*);

@@ -82,6 +82,7 @@ __device__ __forceinline__ unsigned long long mb_gtimer() {
 
 template <int B, typename T>
 __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, long long* tstamp) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) double sm[];
     const int rank = static_cast<int>(cluster.block_rank());
@@ -586,13 +587,15 @@ bool launch_mode_basis(Ctx* ctx, MBArgs<T> A) {
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CL;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_on() ? 2 : 1;
     static const bool dbg = std::getenv("MACH_DEBUG_EIG_T") != nullptr;
     DBuf<long long> tsb;
     if (dbg) {

@@ -298,6 +298,7 @@ namespace {
 template <typename T>
 __global__ void reduce_partials_kernel(const T* __restrict__ P, const int* __restrict__ st_base, int rows, int C,
                                        T* __restrict__ Y) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     // consecutive threads take consecutive columns of one row: the task
     // partials P[q][:] are read coalesced (the Y stores are strided)
     const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -685,9 +686,9 @@ static void launch_ttm(Ctx* ctx, TtmArgs<T, IA> A) {
         A.ts = tsb.get();
     }
     if (A.fac_smem)
-        MB_LAUNCH(ctx, (ttm::ttm_mode_kernel<T, IA, RA, true>), static_cast<unsigned>(blocks), (W + 1) * 32, smem, A);
+        MB_LAUNCH_PDL(ctx, (ttm::ttm_mode_kernel<T, IA, RA, true>), static_cast<unsigned>(blocks), (W + 1) * 32, smem, A);
     else
-        MB_LAUNCH(ctx, (ttm::ttm_mode_kernel<T, IA, RA, false>), static_cast<unsigned>(blocks), (W + 1) * 32, smem, A);
+        MB_LAUNCH_PDL(ctx, (ttm::ttm_mode_kernel<T, IA, RA, false>), static_cast<unsigned>(blocks), (W + 1) * 32, smem, A);
     if (tsdbg) {
         std::vector<unsigned long long> h(8 * blocks);
         to_host(ctx, h.data(), tsb.get(), h.size());
@@ -760,7 +761,7 @@ void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, 
         dispatch_ttm(ctx, A, rab);
     }
     const long long tot = static_cast<long long>(dims[n]) * C;
-    MB_LAUNCH(ctx, reduce_partials_kernel<T>, ceil_div(tot, 256), 256, 0, Pbuf, P.st_base.get(), dims[n], C, Y);
+    MB_LAUNCH_PDL(ctx, reduce_partials_kernel<T>, ceil_div(tot, 256), 256, 0, Pbuf, P.st_base.get(), dims[n], C, Y);
 }
 
 // ---- Y_(b) from the previous mode's fibre sums ------------------------------
@@ -812,6 +813,7 @@ __global__ void __launch_bounds__(512) y_from_segments_kernel(const int* __restr
                                                               int ra, const T* __restrict__ Un, int rns, int rn, int sa,
                                                               int sn, int rows, int un_rows, int chunk,
                                                               T* __restrict__ Y) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     extern __shared__ __align__(128) unsigned char ysm[];
     __shared__ __align__(8) std::uint64_t bar;
     const int G = blockDim.x / ra;
@@ -934,7 +936,7 @@ void y_from_segments(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const 
                              static_cast<std::size_t>(G) * ra * rn * sizeof(T);
     auto launch = [&](auto kern) {
         MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        MB_LAUNCH(ctx, kern, rows, threads, smem, P.seg_ptr.get(), P.seg_row.get(), fseg, ra, Un, rns, rn, sa, sn, rows,
+        MB_LAUNCH_PDL(ctx, kern, rows, threads, smem, P.seg_ptr.get(), P.seg_row.get(), fseg, ra, Un, rns, rn, sa, sn, rows,
                   stage ? dims[n] : 0, chunk, Y);
     };
     // RN >= rn register accumulators

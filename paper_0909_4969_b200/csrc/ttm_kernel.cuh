@@ -87,6 +87,7 @@ struct RingLayout {
 // slots with TMA bulk copies; consumer warp w takes i = w, w + W, ...
 template <typename T, typename IA, int RA, bool FS>
 __global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     constexpr int VN = 16 / static_cast<int>(sizeof(T));  // elements per 128-bit load
     constexpr int RS = ((RA + VN - 1) / VN) * VN;         // ranks rounded to whole 16-B units
     constexpr int RSS = ((RS / VN) & 1) ? RS : RS + VN;   // factor row stride: odd number of 16-B units
