@@ -221,6 +221,8 @@ __global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
         const T* sv = reinterpret_cast<const T*>(sl + L::hdr + L::ibuf) + ((tk.base * sizeof(T)) & 15) / sizeof(T);
         const int2* sd = reinterpret_cast<const int2*>(sl + L::hdr + L::ibuf + L::vbuf);
         const int2 my = sd[lane];  // {i_b, length}; length 0 past nseg
+        // fibre-sum position (fseg): loaded now, used after stage 1 (latency hidden)
+        const int fpos = (A.fseg && lane < tk.nseg) ? __ldg(A.fpos + t * 32 + lane) : 0;
         if (A.dbg >= 1) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[q]);
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
         }
 
         if (A.fseg && lane < tk.nseg) {  // fibre sums for the next mode (y_from_segments)
-            T* o = A.fseg + static_cast<long long>(A.fpos[t * 32 + lane]) * A.ra;
+            T* o = A.fseg + static_cast<long long>(fpos) * A.ra;
             if (sizeof(T) == 4 && (A.ra & 1) == 0) {  // 8-byte stores (pos * ra even: 8-byte aligned)
 #pragma unroll
                 for (int a = 0; a < RA; a += 2)
