@@ -310,7 +310,9 @@ bool run_large(Ctx* ctx, const std::vector<EigJob>& jobs) {
     const unsigned nj = static_cast<unsigned>(jobs.size());
     const std::size_t smem = SubWs<B>::small_doubles() * sizeof(double);
     const int slabs = npmax / 8;  // one 8-row tile of G per gemm CTA
-    static const int kM = std::getenv("MACH_LG_M") ? std::atoi(std::getenv("MACH_LG_M")) : 4;  // filter degree
+    // filter degree 6 from the cold random block (growth T_6(theta_1 / e) stays
+    // far inside fp64 range; the equilibrated CholQR2 absorbs the column scales)
+    static const int kM = std::getenv("MACH_LG_M") ? std::atoi(std::getenv("MACH_LG_M")) : 6;
     static const int kMaxIt = std::getenv("MACH_LG_IT") ? std::atoi(std::getenv("MACH_LG_IT")) : 16;
     static bool attr = false;
     if (!attr) {
@@ -321,10 +323,26 @@ bool run_large(Ctx* ctx, const std::vector<EigJob>& jobs) {
     }
     MB_LAUNCH(ctx, lg_pad_kernel, dim3(64, nj), 256, 0, L);
     MB_LAUNCH(ctx, lg_init_kernel<B>, nj, kThreads, smem, L);
+    // Eager (not under stream capture): iterations in batches, polling the
+    // per-job state between batches so no launches are spent after every job
+    // is certified.  Captured: the fixed sequence (finished jobs no-op).
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    MB_CUDA(cudaStreamIsCapturing(ctx->stream, &cs));
+    const bool poll = cs == cudaStreamCaptureStatusNone;
+    std::vector<LState> hs(jobs.size());
+    int next_poll = 5;
     for (int it = 0; it <= kMaxIt; ++it) {
         MB_LAUNCH(ctx, lg_gemm_kernel<B>, dim3(slabs, nj), kThreads, 0, L, 0);
         MB_LAUNCH(ctx, lg_rr_kernel<B>, nj, kThreads, smem, L, kMaxIt, 1e-12);
         if (it == kMaxIt) break;
+        if (poll && it + 1 == next_poll) {
+            to_host(ctx, hs.data(), st.get(), jobs.size());
+            sync(ctx);
+            bool done = true;
+            for (const LState& q : hs) done = done && (q.conv || q.fail || q.zero);
+            if (done) break;
+            next_poll += 2;
+        }
         for (int s = 1; s <= kM; ++s) MB_LAUNCH(ctx, lg_gemm_kernel<B>, dim3(slabs, nj), kThreads, 0, L, s);
         MB_LAUNCH(ctx, lg_orth_kernel<B>, nj, kThreads, smem, L, kM);
     }
