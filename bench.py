@@ -344,18 +344,26 @@ def run_mach(args, rank, world, local):
 
 
 def measured_traffic(config):
-    """DRAM bytes per TTM launch from the committed ncu --set full capture
-    (profiles/*ttm_ncu*.json, written by scripts/ncu_summary.py)."""
+    """DRAM bytes per TTM launch from the committed ncu --set full captures
+    (profiles/<round>_ttm*_ncu.json, written by scripts/ncu_summary.py): the
+    newest round's captures for this config, averaged over its launches (one
+    per mode that runs a TTM)."""
     import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ttm_ncu*.json")), reverse=True):
+    found = {}
+    for path in glob.glob(os.path.join(ROOT, "profiles", "*ttm*ncu*.json")):
         try:
             with open(path) as f:
                 j = json.load(f)
-            if j.get("config") == config:
-                return {"dram_bytes_per_launch": j["dram_bytes_per_launch"], "source": os.path.relpath(path, ROOT)}
         except Exception:
             continue
-    return None
+        if j.get("config") != config or "dram_bytes_per_launch" not in j:
+            continue
+        tag = os.path.basename(path).split("_ttm")[0]
+        found.setdefault(tag, []).append((os.path.relpath(path, ROOT), j["dram_bytes_per_launch"]))
+    if not found:
+        return None
+    sel = found[max(found)]
+    return {"dram_bytes_per_launch": sum(b for _, b in sel) / len(sel), "source": ", ".join(sorted(p for p, _ in sel))}
 
 
 def run_e2e(args, mb, x, dims, ranks, p, seed, nnz, vsize, dev, local):
