@@ -341,14 +341,11 @@ __global__ void __launch_bounds__(kB) basis_from_side_kernel(const double* __res
 // basis_from_products (linalg.cpp:283-296) = orthonormal_columns(w, k, sigma1,
 // canonicalize=true) + sv of the backed columns.  W: n x wc.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kB) basis_from_products_kernel(const double* __restrict__ W, int n, int wc, int k,
-                                                                 const double* __restrict__ sig,
-                                                                 const int* __restrict__ eig_status,
-                                                                 double* __restrict__ U, double* __restrict__ sv,
-                                                                 int* __restrict__ st, const int* __restrict__ skip) {
-    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
-    if (skip && skip[0] == 0) return;  // the CholQR2 fast path already produced U
-    extern __shared__ double sm[];
+std::size_t basis_smem(int n, int k);
+
+// CTA body (kB threads, shared memory basis_smem(n, k) at sm)
+__device__ void basis_from_products_cta(const double* __restrict__ W, int n, int wc, int k, const double* __restrict__ sig,
+                                        double* __restrict__ U, double* __restrict__ sv, int* __restrict__ st, double* sm) {
     double* v = sm;
     double* tcoef = v + n;
     double* red = tcoef + k;
@@ -388,8 +385,63 @@ __global__ void __launch_bounds__(kB) basis_from_products_kernel(const double* _
         if (threadIdx.x == 0) sv[i] = (backed && i < wc) ? sig[i] : 0.0;
     }
     if (threadIdx.x == 0) { st[0] = nr; st[1] = completed; st[2] = fail; }
+}
+
+__global__ void __launch_bounds__(kB) basis_from_products_kernel(const double* __restrict__ W, int n, int wc, int k,
+                                                                 const double* __restrict__ sig,
+                                                                 const int* __restrict__ eig_status,
+                                                                 double* __restrict__ U, double* __restrict__ sv,
+                                                                 int* __restrict__ st, const int* __restrict__ skip) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
+    if (skip && skip[0] == 0) return;  // the CholQR2 fast path already produced U
+    extern __shared__ double sm[];
+    basis_from_products_cta(W, n, wc, k, sig, U, sv, st, sm);
     (void)eig_status;
 }
+
+// The fused mode basis's fallback chain after the exact eigensolver, in one
+// CTA (it runs only off the fast path, where its speed does not matter; on the
+// fast path it is one no-op launch instead of three):
+//   flags[1]: W = Y V;  flags[2]: U from W (basis_from_products);
+//   flags[3]: the row-major kernel copy of U.
+template <typename T>
+__global__ void __launch_bounds__(kB) mb_fallback_kernel(const T* __restrict__ Y, int rows, int C, const double* __restrict__ V,
+                                                         int k, double* __restrict__ W, const double* __restrict__ sig,
+                                                         double* __restrict__ U, double* __restrict__ sv,
+                                                         int* __restrict__ st, T* __restrict__ Ur, int rs,
+                                                         const int* __restrict__ flags) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
+    const int need_w = flags[1], need_basis = flags[2], need_rm = flags[3];
+    if (!need_w && !need_basis && !need_rm) return;
+    extern __shared__ double sm[];
+    if (need_w) {
+        for (long long idx = threadIdx.x; idx < static_cast<long long>(rows) * k; idx += kB) {
+            const int i = static_cast<int>(idx % rows), j = static_cast<int>(idx / rows);
+            double acc = 0.0;
+            for (int c = 0; c < C; ++c)
+                acc = fma(static_cast<double>(Y[i + static_cast<std::size_t>(c) * rows]), V[c + static_cast<std::size_t>(j) * C], acc);
+            W[idx] = acc;
+        }
+        __syncthreads();
+    }
+    if (need_basis) basis_from_products_cta(W, rows, k, k, sig, U, sv, st, sm);
+    __syncthreads();
+    if (need_rm && Ur)
+        for (long long idx = threadIdx.x; idx < static_cast<long long>(rows) * rs; idx += kB) {
+            const int i = static_cast<int>(idx / rs), c = static_cast<int>(idx % rs);
+            Ur[idx] = (c < k) ? static_cast<T>(U[i + static_cast<std::size_t>(c) * rows]) : T(0);
+        }
+}
+
+template <typename T>
+void mb_fallback(Ctx* ctx, const T* Y, int rows, int C, const double* V, int k, double* W, const double* sig, double* U,
+                 double* sv, int* st, T* Ur, int rs, const int* flags) {
+    MB_LAUNCH_PDL(ctx, mb_fallback_kernel<T>, 1, kB, basis_smem(rows, k), Y, rows, C, V, k, W, sig, U, sv, st, Ur, rs, flags);
+}
+template void mb_fallback<float>(Ctx*, const float*, int, int, const double*, int, double*, const double*, double*,
+                                 double*, int*, float*, int, const int*);
+template void mb_fallback<double>(Ctx*, const double*, int, int, const double*, int, double*, const double*, double*,
+                                  double*, int*, double*, int, const int*);
 
 std::size_t basis_smem(int n, int k) { return (static_cast<std::size_t>(n) + k + 32 + 32) * sizeof(double); }
 

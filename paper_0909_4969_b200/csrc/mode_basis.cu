@@ -674,15 +674,14 @@ bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double
         default: break;
     }
     if (!ok) return false;
-    // flag-gated fallbacks (each returns immediately on the fast path).  A
+    // flag-gated fallbacks: the exact eigensolver, then W / basis / row-major
+    // copy in one launch (each returns immediately on the fast path).  A
     // conditional graph node around them was measured slower (~6 us per node
-    // per mode) than these four no-op launches inside the sweep graph.
+    // per mode) than these no-op launches inside the sweep graph.
     const int* f = flags.get();
     DBuf<double> work(ctx, eig_work_doubles(n, k));
     eig_topk(ctx, Gout.get(), n, k, work.get(), V.get(), sig.get(), est.get(), f + 0);
-    matmul_yv_gated<T>(ctx, Y, rows, n, V.get(), k, Wout.get(), f + 1);
-    basis_from_products_gated(ctx, Wout.get(), rows, k, k, sig.get(), est.get(), U, sv, st, f + 2);
-    if (Ur) factor_rowmajor_gated<T>(ctx, U, rows, k, rs, Ur, f + 3);
+    mb_fallback<T>(ctx, Y, rows, n, V.get(), k, Wout.get(), sig.get(), U, sv, st, Ur, rs, f);
     return true;
 }
 

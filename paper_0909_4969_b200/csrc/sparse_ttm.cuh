@@ -147,6 +147,10 @@ void basis_from_products_gated(Ctx* ctx, const double* W, int n, int wc, int k, 
                                const int* eig_status, double* U, double* sv, int* st, const int* need);
 template <typename T>
 void factor_rowmajor_gated(Ctx* ctx, const double* U, int n, int r, int rs, T* out, const int* need);
+// the fused mode basis's fallback chain (W = Y V, basis, row-major copy) in one flag-gated launch
+template <typename T>
+void mb_fallback(Ctx* ctx, const T* Y, int rows, int C, const double* V, int k, double* W, const double* sig, double* U,
+                 double* sv, int* st, T* Ur, int rs, const int* flags);
 // fused column-side mode basis (mode_basis.cu); false = not applicable
 template <typename T>
 bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
