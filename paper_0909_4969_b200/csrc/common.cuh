@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -49,6 +50,9 @@ struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // launched right after the next fused mode-basis kernel, ahead of its
+    // fallback kernels (consumed once): the overlapped sweep's next stage 1
+    std::function<void()> after_basis;
     std::int64_t launches = 0;
     bool profile = false;                      // per-kernel CUDA-event timing (bench roofline)
     std::map<std::string, KStat> stats;

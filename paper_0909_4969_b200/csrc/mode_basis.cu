@@ -665,6 +665,7 @@ bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double
         V(ctx, static_cast<std::size_t>(n) * k);
     DBuf<int> est(ctx, 3), flags(ctx, 4);
     A.sig = sig.get(); A.estatus = est.get(); A.Gout = Gout.get(); A.Wout = Wout.get(); A.flags = flags.get();
+    DBuf<double> work(ctx, eig_work_doubles(n, k));  // allocated before the launch: nothing may sit between it and after_basis
     bool ok = false;
     switch (b) {
         case 8: ok = launch_mode_basis<8, T>(ctx, A); break;
@@ -674,12 +675,16 @@ bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double
         default: break;
     }
     if (!ok) return false;
+    if (ctx->after_basis) {  // e.g. the next mode's stage 1, overlapping this kernel (programmatic launch)
+        auto cb = std::move(ctx->after_basis);
+        ctx->after_basis = nullptr;
+        cb();
+    }
     // flag-gated fallbacks: the exact eigensolver, then W / basis / row-major
     // copy in one launch (each returns immediately on the fast path).  A
     // conditional graph node around them was measured slower (~6 us per node
     // per mode) than these no-op launches inside the sweep graph.
     const int* f = flags.get();
-    DBuf<double> work(ctx, eig_work_doubles(n, k));
     eig_topk(ctx, Gout.get(), n, k, work.get(), V.get(), sig.get(), est.get(), f + 0);
     mb_fallback<T>(ctx, Y, rows, n, V.get(), k, Wout.get(), sig.get(), U, sv, st, Ur, rs, f);
     return true;

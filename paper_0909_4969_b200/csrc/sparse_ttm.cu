@@ -599,11 +599,11 @@ void build_ttm_layout(Ctx* ctx, long long nnz, ModePlan& P) {
 }
 
 template <typename T>
-std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>& ranks) {
+std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>& ranks, int force_a) {
     Ctx* ctx = X->ctx;
     if (X->plans.size() != X->dims.size()) X->plans.assign(X->dims.size(), nullptr);
     const int d = static_cast<int>(X->dims.size());
-    const int a = choose_inner(X, n, ranks);
+    const int a = (force_a >= 0 && force_a < d && force_a != n) ? force_a : choose_inner(X, n, ranks);
     const int b = (d == 3) ? 3 - n - a : -1;
     auto& slot = X->plans[static_cast<std::size_t>(n)];
     if (slot && slot->a == a) return slot;
@@ -646,7 +646,7 @@ std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>
 }
 
 template <typename T, typename IA, int RA>
-static void launch_ttm(Ctx* ctx, TtmArgs<T, IA> A) {
+static void launch_ttm(Ctx* ctx, TtmArgs<T, IA> A, int max_ctas) {
     constexpr int VN = 16 / static_cast<int>(sizeof(T));
     constexpr int RS = ((RA + VN - 1) / VN) * VN;
     constexpr int RSS = ((RS / VN) & 1) ? RS : RS + VN;
@@ -676,7 +676,7 @@ static void launch_ttm(Ctx* ctx, TtmArgs<T, IA> A) {
     MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int sms = 148;
     MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
-    const long long blocks = std::min<long long>(A.n_task, sms);
+    const long long blocks = std::min<long long>(A.n_task, max_ctas > 0 ? std::min(max_ctas, sms) : sms);
     if (blocks <= 0) return;
     static const bool tsdbg = std::getenv("MACH_TTM_TS") != nullptr;
     DBuf<unsigned long long> tsb;
@@ -709,16 +709,16 @@ static void launch_ttm(Ctx* ctx, TtmArgs<T, IA> A) {
 }
 
 template <typename T, typename IA>
-static void dispatch_ttm(Ctx* ctx, const TtmArgs<T, IA>& A, int rab) {
+static void dispatch_ttm(Ctx* ctx, const TtmArgs<T, IA>& A, int rab, int max_ctas = 0) {
     switch (rab) {
-        case 4: launch_ttm<T, IA, 4>(ctx, A); break;
-        case 8: launch_ttm<T, IA, 8>(ctx, A); break;
-        case 10: launch_ttm<T, IA, 10>(ctx, A); break;
-        case 12: launch_ttm<T, IA, 12>(ctx, A); break;
-        case 16: launch_ttm<T, IA, 16>(ctx, A); break;
-        case 20: launch_ttm<T, IA, 20>(ctx, A); break;
-        case 24: launch_ttm<T, IA, 24>(ctx, A); break;
-        default: launch_ttm<T, IA, 32>(ctx, A); break;
+        case 4: launch_ttm<T, IA, 4>(ctx, A, max_ctas); break;
+        case 8: launch_ttm<T, IA, 8>(ctx, A, max_ctas); break;
+        case 10: launch_ttm<T, IA, 10>(ctx, A, max_ctas); break;
+        case 12: launch_ttm<T, IA, 12>(ctx, A, max_ctas); break;
+        case 16: launch_ttm<T, IA, 16>(ctx, A, max_ctas); break;
+        case 20: launch_ttm<T, IA, 20>(ctx, A, max_ctas); break;
+        case 24: launch_ttm<T, IA, 24>(ctx, A, max_ctas); break;
+        default: launch_ttm<T, IA, 32>(ctx, A, max_ctas); break;
     }
 }
 
@@ -808,10 +808,10 @@ __global__ void seg_pos_kernel(const int* __restrict__ ids, long long n, const T
 // chunk's segments j = g mod G (one fibre-sum value times one U_n row each);
 // the G partial rows are summed in group order at the end (deterministic).
 template <typename T, int RN>
-__global__ void __launch_bounds__(512) y_from_segments_kernel(const int* __restrict__ seg_ptr,
+__global__ void __launch_bounds__(512, 3) y_from_segments_kernel(const int* __restrict__ seg_ptr,
                                                               const int* __restrict__ seg_row, const T* __restrict__ fseg,
                                                               int ra, const T* __restrict__ Un, int rns, int rn, int sa,
-                                                              int sn, int rows, int un_rows, int chunk,
+                                                              int sn, int rows, int un_rows, int chunk, int ptr_mul,
                                                               T* __restrict__ Y) {
     pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     extern __shared__ __align__(128) unsigned char ysm[];
@@ -824,14 +824,14 @@ __global__ void __launch_bounds__(512) y_from_segments_kernel(const int* __restr
     T* sU = reinterpret_cast<T*>(ysm);
     unsigned char* sFb = ysm + ub;
     unsigned char* sRb = sFb + ((static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16 + 15) & ~std::size_t(15));
-    T* part = reinterpret_cast<T*>(sRb + ((static_cast<std::size_t>(chunk) * sizeof(int) + 16 + 15) & ~std::size_t(15)));
+    T* part = reinterpret_cast<T*>(sFb);  // the group partials reuse the fibre-sum chunk once it is consumed
     if (tid == 0) {
         ttm::mbar_init(&bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     const int row = blockIdx.x;
-    const int s0 = seg_ptr[row], s1 = seg_ptr[row + 1];
+    const int s0 = seg_ptr[row] * ptr_mul, s1 = seg_ptr[row + 1] * ptr_mul;
     T acc[RN];
 #pragma unroll
     for (int q = 0; q < RN; ++q) acc[q] = T(0);
@@ -857,8 +857,8 @@ __global__ void __launch_bounds__(512) y_from_segments_kernel(const int* __restr
         phase ^= 1u;
         const T* sF = reinterpret_cast<const T*>(sFb + (fsrc - f0));
         const int* sR = reinterpret_cast<const int*>(sRb + (rsrc - r0));
-        const T* U = un_rows > 0 ? sU : Un;
-        if (on) {
+        // two copies of the loop so the staged case compiles to shared-memory loads
+        auto run = [&](const T* U) {
             for (int j = g; j < m; j += G) {
                 const T fv = sF[j * ra + r_a];
                 const T* ur = U + sR[j] * rns;
@@ -866,6 +866,10 @@ __global__ void __launch_bounds__(512) y_from_segments_kernel(const int* __restr
                 for (int q = 0; q < RN; ++q)
                     if (q < rn) acc[q] = fma(fv, ur[q], acc[q]);
             }
+        };
+        if (on) {
+            if (un_rows > 0) run(sU);
+            else run(Un);
         }
         __syncthreads();  // the next chunk's bulk copies overwrite sF / sR
     }
@@ -930,14 +934,16 @@ void y_from_segments(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const 
     const int rns = ttm_stride(rn, sizeof(T));
     const std::size_t ubytes = static_cast<std::size_t>(dims[n]) * rns * sizeof(T);
     const bool stage = ubytes <= 64 * 1024;
-    const int chunk = static_cast<int>(std::min<std::size_t>(2048, (48 * 1024) / (ra * sizeof(T))));
-    const std::size_t smem = (stage ? ubytes : 0) + ((static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16 + 15) & ~std::size_t(15)) +
-                             ((static_cast<std::size_t>(chunk) * sizeof(int) + 16 + 15) & ~std::size_t(15)) +
-                             static_cast<std::size_t>(G) * ra * rn * sizeof(T);
+    const int chunk = static_cast<int>(std::min<std::size_t>(2048, (24 * 1024) / (ra * sizeof(T))));
+    // shared memory: [U][fibre-sum chunk, later the group partials][i_n chunk]; ~55 KB at C2: four CTAs per SM
+    const std::size_t fbytes = std::max(static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16,
+                                        static_cast<std::size_t>(G) * ra * rn * sizeof(T));
+    const std::size_t smem = (stage ? ubytes : 0) + ((fbytes + 15) & ~std::size_t(15)) +
+                             ((static_cast<std::size_t>(chunk) * sizeof(int) + 16 + 15) & ~std::size_t(15));
     auto launch = [&](auto kern) {
         MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         MB_LAUNCH_PDL(ctx, kern, rows, threads, smem, P.seg_ptr.get(), P.seg_row.get(), fseg, ra, Un, rns, rn, sa, sn, rows,
-                  stage ? dims[n] : 0, chunk, Y);
+                  stage ? dims[n] : 0, chunk, 1, Y);
     };
     // RN >= rn register accumulators
     if (rn <= 4) launch(y_from_segments_kernel<T, 4>);
@@ -947,6 +953,96 @@ void y_from_segments(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const 
     else if (rn <= 24) launch(y_from_segments_kernel<T, 24>);
     else launch(y_from_segments_kernel<T, 32>);
 }
+
+namespace {
+__global__ void seg_ib_kernel(const TtmTask* __restrict__ tasks, const int2* __restrict__ desc, long long n_task,
+                              int* __restrict__ ib) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= n_task * 32) return;
+    const long long t = i >> 5;
+    const int lane = static_cast<int>(i & 31);
+    ib[i] = lane < tasks[t].nseg ? desc[t * kDesc + lane].x : 0;
+}
+}  // namespace
+
+template <typename T>
+void sparse_mode_stage1(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks,
+                        const std::vector<const T*>& Ur, T* F, int ctas) {
+    const int a = P.a;
+    auto fill = [&](auto& A) {
+        A.vals = reinterpret_cast<const T*>(P.jv.get());
+        A.tasks = P.tasks.get();
+        A.desc = P.desc.get();
+        A.n_task = P.n_task;
+        A.Ua = Ur[a]; A.ra = ranks[a];
+        A.Ub = Ur[a]; A.rb = 1; A.rbs = 1;  // stage 2 does not run: no U_b
+        A.sa = 1; A.sb = 0; A.C = ranks[a]; A.P = nullptr;
+        A.ua_rows = dims[a];
+        A.ub_elems = 0;
+        A.fseg = F;
+        A.fpos = nullptr;
+        A.stage1 = 1;
+    };
+    const int rab = ra_bucket(ranks[a]);
+    if (P.ia16) {
+        TtmArgs<T, unsigned short> A{};
+        A.ia = reinterpret_cast<const unsigned short*>(P.ia.get());
+        fill(A);
+        dispatch_ttm(ctx, A, rab, ctas);
+    } else {
+        TtmArgs<T, unsigned int> A{};
+        A.ia = reinterpret_cast<const unsigned int*>(P.ia.get());
+        fill(A);
+        dispatch_ttm(ctx, A, rab, ctas);
+    }
+}
+
+template <typename T>
+void sparse_mode_stage2(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks, const T* F,
+                        const T* Ub, T* Y) {
+    const int n = P.mode, a = P.a, b = P.b;
+    const long long nslot = P.n_task * 32;
+    if (!P.seg_ib.get()) {
+        P.seg_ib.alloc(ctx, nslot + 8);  // +8: bulk copies read 16-byte-aligned supersets
+        if (nslot > 0)
+            MB_LAUNCH(ctx, seg_ib_kernel, ceil_div(nslot, 256), 256, 0, P.tasks.get(), P.desc.get(), P.n_task, P.seg_ib.get());
+    }
+    const int ra = ranks[a], rb = ranks[b];
+    int sa, sb;  // Y_(n) columns: the two remaining modes, earliest fastest
+    if (a < b) { sa = 1; sb = ra; }
+    else { sb = 1; sa = rb; }
+    const int rows = dims[n];
+    const int threads = (512 / ra) * ra;
+    const int G = threads / ra;
+    const int rbs = ttm_stride(rb, sizeof(T));
+    const std::size_t ubytes = static_cast<std::size_t>(dims[b]) * rbs * sizeof(T);
+    const bool stage = ubytes <= 64 * 1024;
+    const int chunk = static_cast<int>(std::min<std::size_t>(2048, (24 * 1024) / (ra * sizeof(T))));
+    const std::size_t fbytes = std::max(static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16,
+                                        static_cast<std::size_t>(G) * ra * rb * sizeof(T));
+    const std::size_t smem = (stage ? ubytes : 0) + ((fbytes + 15) & ~std::size_t(15)) +
+                             ((static_cast<std::size_t>(chunk) * sizeof(int) + 16 + 15) & ~std::size_t(15));
+    auto launch = [&](auto kern) {
+        MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        MB_LAUNCH_PDL(ctx, kern, rows, threads, smem, P.st_base.get(), P.seg_ib.get(), F, ra, Ub, rbs, rb, sa, sb, rows,
+                      stage ? dims[b] : 0, chunk, 32, Y);
+    };
+    if (rb <= 4) launch(y_from_segments_kernel<T, 4>);
+    else if (rb <= 8) launch(y_from_segments_kernel<T, 8>);
+    else if (rb <= 12) launch(y_from_segments_kernel<T, 12>);
+    else if (rb <= 16) launch(y_from_segments_kernel<T, 16>);
+    else if (rb <= 24) launch(y_from_segments_kernel<T, 24>);
+    else launch(y_from_segments_kernel<T, 32>);
+}
+
+template void sparse_mode_stage1<float>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&,
+                                        const std::vector<const float*>&, float*, int);
+template void sparse_mode_stage1<double>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&,
+                                         const std::vector<const double*>&, double*, int);
+template void sparse_mode_stage2<float>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&, const float*,
+                                        const float*, float*);
+template void sparse_mode_stage2<double>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&, const double*,
+                                         const double*, double*);
 
 template void y_from_segments<float>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&, const float*,
                                      const float*, float*);
@@ -1032,8 +1128,8 @@ void sparse_times(Ctx* ctx, const mach_sparse* X, const ModePlan& P, const doubl
 #undef MB_ST
 }
 
-template std::shared_ptr<ModePlan> get_plan<float>(mach_sparse*, int, const std::vector<int>&);
-template std::shared_ptr<ModePlan> get_plan<double>(mach_sparse*, int, const std::vector<int>&);
+template std::shared_ptr<ModePlan> get_plan<float>(mach_sparse*, int, const std::vector<int>&, int);
+template std::shared_ptr<ModePlan> get_plan<double>(mach_sparse*, int, const std::vector<int>&, int);
 template void sparse_mode_ttm<float>(Ctx*, const ModePlan&, const std::vector<int>&, const std::vector<int>&,
                                      const std::vector<const float*>&, const float*, float*, float*, float*,
                                      const int*);

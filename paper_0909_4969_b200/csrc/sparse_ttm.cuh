@@ -43,6 +43,7 @@ struct TtmArgs {
     unsigned long long* ts;        // experiments: per-CTA %globaltimer stamps (8 per CTA) or null
     T* fseg;                       // optional: every segment's fibre sum (ra values at fpos[t * 32 + lane] * ra)
     const int* fpos;               // position of each segment in the i_b-grouped order (with fseg)
+    int stage1;                    // 1: fibre sums only, to fseg in task order (see ttm_mode_kernel)
 };
 
 // Per-mode sorted layout of a sampled tensor (built once, reused by HOSVD and
@@ -66,6 +67,7 @@ struct ModePlan {
     DBuf<int> seg_pos, seg_ptr;    // segment t * 32 + lane -> position in i_b order; row i_b: [seg_ptr[i], seg_ptr[i+1])
     DBuf<int> seg_row;             // i_n (this mode's row) of the segment at each position
     long long n_seg = -1;          // segments (valid positions), known once grouped
+    DBuf<int> seg_ib;              // i_b of every segment slot t * 32 + lane, task order (0 past nseg)
 };
 // group P's segments by i_b (once); false when P has no b mode
 bool build_segment_groups(Ctx* ctx, ModePlan& P, int b_rows);
@@ -75,7 +77,7 @@ bool sparse_fast_path_ok(const std::vector<int>& dims, const std::vector<int>& r
 int ttm_ra_bucket(int r);
 int ttm_stride(int r, int elem_bytes);  // factor row stride of the TTM kernel copies
 template <typename T>
-std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>& ranks);
+std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>& ranks, int force_a = -1);
 template <typename T>
 void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks,
                      const std::vector<const T*>& Ur, const T* one, T* Pbuf, T* Y, T* fseg = nullptr,
@@ -87,6 +89,16 @@ void sparse_mode_ttm(Ctx* ctx, const ModePlan& P, const std::vector<int>& dims, 
 template <typename T>
 void y_from_segments(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks, const T* fseg,
                      const T* Un, T* Y);
+// Split TTM for overlapped sweeps: stage 1 = the fibre sums F (X x_a U_a, one
+// ra-vector per segment slot, task order) on `ctas` CTAs, launched so that it
+// may overlap the preceding kernel (see ttm_mode_kernel); stage 2 = Y_(n) =
+// sum over each row's segments of F (x) U_b[i_b, :] (fixed order).
+template <typename T>
+void sparse_mode_stage1(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks,
+                        const std::vector<const T*>& Ur, T* F, int ctas);
+template <typename T>
+void sparse_mode_stage2(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks, const T* F,
+                        const T* Ub, T* Y);
 template <typename T>
 void sparse_row_gram(Ctx* ctx, const mach_sparse* X, int n, double normX2, double* G);
 template <typename T>

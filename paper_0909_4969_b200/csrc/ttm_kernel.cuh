@@ -87,7 +87,12 @@ struct RingLayout {
 // slots with TMA bulk copies; consumer warp w takes i = w, w + W, ...
 template <typename T, typename IA, int RA, bool FS>
 __global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
-    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
+    // Stage-1-only launches (fibre sums for a later stage 2) overlap the
+    // preceding mode-basis kernel: they read only data that was complete
+    // before it started, so they skip the wait here and instead wait at the
+    // end, making their completion imply the predecessor's.
+    if (A.stage1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    else pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     constexpr int VN = 16 / static_cast<int>(sizeof(T));  // elements per 128-bit load
     constexpr int RS = ((RA + VN - 1) / VN) * VN;         // ranks rounded to whole 16-B units
     constexpr int RSS = ((RS / VN) & 1) ? RS : RS + VN;   // factor row stride: odd number of 16-B units
@@ -124,7 +129,7 @@ __global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
             fence_proxy_async();
             mbar_expect_tx(&fbar, ua_bytes + ub_bytes);
             bulk_g2s(ua_s, A.Ua, ua_bytes, &fbar);
-            bulk_g2s(ub_s, A.Ub, ub_bytes, &fbar);
+            if (ub_bytes) bulk_g2s(ub_s, A.Ub, ub_bytes, &fbar);
         }
         // lane k < S owns slot k and feeds it tasks i = r * S + k, r = 0, 1, ...
         // (S <= 32): the slots are refilled in parallel, and each lane's next
@@ -222,7 +227,7 @@ __global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
         const int2* sd = reinterpret_cast<const int2*>(sl + L::hdr + L::ibuf + L::vbuf);
         const int2 my = sd[lane];  // {i_b, length}; length 0 past nseg
         // fibre-sum position (fseg): loaded now, used after stage 1 (latency hidden)
-        const int fpos = (A.fseg && lane < tk.nseg) ? __ldg(A.fpos + t * 32 + lane) : 0;
+        const int fpos = (A.fpos && lane < tk.nseg) ? __ldg(A.fpos + t * 32 + lane) : 0;
         if (A.dbg >= 1) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[q]);
@@ -257,6 +262,26 @@ __global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
                 if (act[k]) gather_fma(f, ix[k], vx[k]);
         }
 
+        if (A.stage1) {  // fibre sums only, in task order (segments past nseg write zeros)
+            T* o = A.fseg + (t * 32 + lane) * static_cast<long long>(A.ra);
+            if (sizeof(T) == 4 && (A.ra & 1) == 0) {
+#pragma unroll
+                for (int a = 0; a < RA; a += 2)
+                    if (a < A.ra) *reinterpret_cast<float2*>(o + a) = make_float2(f[a], f[a + 1]);
+            } else {
+#pragma unroll
+                for (int a = 0; a < RA; ++a)
+                    if (a < A.ra) o[a] = f[a];
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[q]);
+            q += W;
+            if (q >= S) {
+                q -= S;
+                par ^= 1u;
+            }
+            continue;
+        }
         if (A.fseg && lane < tk.nseg) {  // fibre sums for the next mode (y_from_segments)
             T* o = A.fseg + static_cast<long long>(fpos) * A.ra;
             if (sizeof(T) == 4 && (A.ra & 1) == 0) {  // 8-byte stores (pos * ra even: 8-byte aligned)
@@ -326,6 +351,7 @@ __global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
         }
     }
     if (ts && lane == 0) atomicMax(&ts[4], gtimer());
+    if (A.stage1) asm volatile("griddepcontrol.wait;" ::: "memory");  // complete only after the predecessor
 }
 
 }  // namespace ttm

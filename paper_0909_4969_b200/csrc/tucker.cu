@@ -484,6 +484,31 @@ struct SparseSession : SessionBase {
     // not updated between the two projections of a sweep.
     DBuf<T> fseg;
     int fseg_for = -1;  // mode whose Y_(.) the current fibre sums give (-1: none)
+
+    // Overlapped sweep (d = 3; MACH_NO_OVERLAP=1 disables).  Mode n's layout
+    // takes a = n + 1 and b = n + 2 (mod 3), so its TTM splits into stage 1,
+    // F = X x_a U_a (the gathers: ~all the TTM's time), which needs only
+    // factors settled before mode n - 1's update, and a short stage 2,
+    // Y_(n) = sum F (x) U_b, which needs the U_{n-1} just computed.  Stage 1 of
+    // mode n is launched right behind mode n - 1's basis kernel and runs on
+    // the SMs that kernel's 16-CTA cluster leaves idle.
+    DBuf<T> Fov;
+    bool overlap = false;
+    bool overlap_ok() const { return overlap && !sharded; }
+    void stage1(int m) {
+        static const int dbg_skip = std::getenv("MACH_DBG_SKIP_STAGE1") ? std::atoi(std::getenv("MACH_DBG_SKIP_STAGE1")) : -1;
+        if (dbg_skip == 9 || dbg_skip == m) return;  // timing experiments only (results are wrong)
+        static const int reserve = std::getenv("MACH_OV_RESERVE") ? std::atoi(std::getenv("MACH_OV_RESERVE")) : 16;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        sparse_mode_stage1<T>(ctx, *plans[static_cast<std::size_t>(m)], dims, ranks, Urp, Fov.get(), sms - reserve);
+    }
+    void stage2(int m) {
+        static const bool dbg_skip = std::getenv("MACH_DBG_SKIP_STAGE2") != nullptr;
+        if (dbg_skip) return;  // timing experiments only (results are wrong)
+        auto& P = *plans[static_cast<std::size_t>(m)];
+        sparse_mode_stage2<T>(ctx, P, dims, ranks, Fov.get(), Urp[static_cast<std::size_t>(P.b)], Y.get());
+    }
     bool fseg_use(int m) const {
         static const bool off = std::getenv("MACH_NO_FIBRE_REUSE") != nullptr;
         if (off || d != 3 || m + 1 >= d) return false;
@@ -566,7 +591,10 @@ struct SparseSession : SessionBase {
         // ---- setup: layouts, |X|^2, kernel factor copies, buffers ----
         tm.start();
         plans.resize(static_cast<std::size_t>(d));
-        for (int m = 0; m < d; ++m) plans[static_cast<std::size_t>(m)] = get_plan<T>(X, m, ranks);
+        static const bool no_overlap = std::getenv("MACH_NO_OVERLAP") != nullptr;
+        overlap = d == 3 && !no_overlap;
+        for (int m = 0; m < d; ++m)
+            plans[static_cast<std::size_t>(m)] = get_plan<T>(X, m, ranks, overlap ? (m + 1) % 3 : -1);
         sumsq<T>(ctx, static_cast<const T*>(X->val), X->nnz, fs.red.get(), fs.scal.get());
         to_host(ctx, &normX2, fs.scal.get(), 1);
         sync(ctx);
@@ -593,6 +621,13 @@ struct SparseSession : SessionBase {
         }
         Pbuf.alloc(ctx, maxP);
         Y.alloc(ctx, maxY);
+        if (overlap) {
+            long long fmax = 0;
+            for (int m = 0; m < d; ++m)
+                fmax = std::max(fmax, plans[static_cast<std::size_t>(m)]->n_task * 32 *
+                                          ranks[static_cast<std::size_t>(plans[static_cast<std::size_t>(m)]->a)]);
+            Fov.alloc(ctx, static_cast<std::size_t>(fmax) + 16);  // slack: stage 2 bulk-copies aligned supersets
+        }
         core.alloc(ctx, static_cast<std::size_t>(checked_size(ranks)));
         setup_ms = tm.stop_ms();
     }
@@ -686,6 +721,21 @@ struct SparseSession : SessionBase {
         return true;
     }
     void sweep_body() {
+        if (overlap_ok()) {
+            stage1(0);
+            for (int i = 0; i < d; ++i) {
+                stage2(i);
+                if (i + 1 < d) ctx->after_basis = [this, i]() { stage1(i + 1); };
+                mode_update(i);
+                if (ctx->after_basis) {  // the unfused basis path ran: launch it now
+                    auto cb = std::move(ctx->after_basis);
+                    ctx->after_basis = nullptr;
+                    cb();
+                }
+            }
+            core_device();
+            return;
+        }
         for (int i = 0; i < d; ++i) {
             mode_y(i);
             mode_update(i);
@@ -747,9 +797,13 @@ struct SparseSession : SessionBase {
     // mode runs no TTM (its Y_(m) comes from the previous mode's fibre sums)
     long long ttm_bytes(int m) const override {
         if (m < 0 || m >= d || !plans[static_cast<std::size_t>(m)]) return -1;
-        if (m >= 1 && fseg_use(m - 1)) return -1;
         const ModePlan& P = *plans[static_cast<std::size_t>(m)];
         const long long nnz = X->nnz;
+        if (overlap_ok())  // stage 1: nonzeros + task records in, fibre sums (every segment slot) out
+            return nnz * ((P.ia16 ? 2 : 4) + static_cast<long long>(sizeof(T))) +
+                   P.n_task * (static_cast<long long>(kDesc * sizeof(int2) + sizeof(TtmTask)) +
+                               32 * ranks[static_cast<std::size_t>(P.a)] * static_cast<long long>(sizeof(T)));
+        if (m >= 1 && fseg_use(m - 1)) return -1;
         long long b = nnz * ((P.ia16 ? 2 : 4) + static_cast<long long>(sizeof(T))) +
                       P.n_task * (static_cast<long long>(kDesc * sizeof(int2) + sizeof(TtmTask)) +
                                   static_cast<long long>(C[static_cast<std::size_t>(m)]) * static_cast<long long>(sizeof(T)));
