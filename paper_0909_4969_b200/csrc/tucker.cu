@@ -494,6 +494,7 @@ struct SparseSession : SessionBase {
     // the SMs that kernel's 16-CTA cluster leaves idle.
     DBuf<T> Fov;
     bool overlap = false;
+    bool f0_ready = false;  // Fov holds mode 0's stage 1 for the current factors
     bool overlap_ok() const { return overlap && !sharded; }
     void stage1(int m) {
         static const int dbg_skip = std::getenv("MACH_DBG_SKIP_STAGE1") ? std::atoi(std::getenv("MACH_DBG_SKIP_STAGE1")) : -1;
@@ -510,7 +511,7 @@ struct SparseSession : SessionBase {
         sparse_mode_stage2<T>(ctx, P, dims, ranks, Fov.get(), Urp[static_cast<std::size_t>(P.b)], Y.get());
     }
     bool fseg_use(int m) const {
-        static const bool off = std::getenv("MACH_NO_FIBRE_REUSE") != nullptr;
+        const bool off = std::getenv("MACH_NO_FIBRE_REUSE") != nullptr;
         if (off || d != 3 || m + 1 >= d) return false;
         return plans[static_cast<std::size_t>(m)]->b == m + 1;
     }
@@ -583,6 +584,7 @@ struct SparseSession : SessionBase {
         sweep_fits.assign(1, fit);
         warnings = init->warnings;
         fseg_for = -1;
+        f0_ready = false;
     }
     void setup(mach_sparse* sp, const std::vector<int>& rk) {
         X = sp;
@@ -591,7 +593,7 @@ struct SparseSession : SessionBase {
         // ---- setup: layouts, |X|^2, kernel factor copies, buffers ----
         tm.start();
         plans.resize(static_cast<std::size_t>(d));
-        static const bool no_overlap = std::getenv("MACH_NO_OVERLAP") != nullptr;
+        const bool no_overlap = std::getenv("MACH_NO_OVERLAP") != nullptr;  // read per session (tests toggle it)
         overlap = d == 3 && !no_overlap;
         for (int m = 0; m < d; ++m)
             plans[static_cast<std::size_t>(m)] = get_plan<T>(X, m, ranks, overlap ? (m + 1) % 3 : -1);
@@ -683,6 +685,7 @@ struct SparseSession : SessionBase {
         }
         warnings = read_warnings(ctx, fs.st, ranks, all);
         fseg_for = -1;
+        f0_ready = false;
         mode_y(d - 1);
         fit = prev_fit = core_and_fit();
         hosvd_ms = tm.stop_ms();
@@ -693,6 +696,7 @@ struct SparseSession : SessionBase {
         static const bool nofuse = std::getenv("MACH_NO_FUSED_BASIS") != nullptr;
         const std::size_t si = static_cast<std::size_t>(i);
         if (fseg_for >= 1 && plans[static_cast<std::size_t>(fseg_for - 1)]->a == i) fseg_for = -1;  // F used U_i
+        if (plans[0]->a == i) f0_ready = false;  // the prefetched mode-0 stage 1 used U_i
         if (!nofuse && lsb_fused<T>(ctx, Y.get(), dims[si], C[si], ranks[si], fs.U[si].get(), sv_at(i),
                                     fs.st.get() + 3 * i, &warm[si], fs.U[si].get(), Ur[si].get(),
                                     ttm_stride(ranks[si], sizeof(T))))
@@ -722,10 +726,13 @@ struct SparseSession : SessionBase {
     }
     void sweep_body() {
         if (overlap_ok()) {
-            stage1(0);
+            // the next sweep's stage 1 of mode 0 (it needs U_1 of this sweep)
+            // runs behind this sweep's last basis kernel
+            if (!f0_ready) stage1(0);
             for (int i = 0; i < d; ++i) {
                 stage2(i);
                 if (i + 1 < d) ctx->after_basis = [this, i]() { stage1(i + 1); };
+                else ctx->after_basis = [this]() { stage1(0); };
                 mode_update(i);
                 if (ctx->after_basis) {  // the unfused basis path ran: launch it now
                     auto cb = std::move(ctx->after_basis);
@@ -733,6 +740,7 @@ struct SparseSession : SessionBase {
                     cb();
                 }
             }
+            f0_ready = true;
             core_device();
             return;
         }

@@ -294,20 +294,22 @@ def test_mode_basis_fallback_inside_sweep_graph(mb, monkeypatch):
 
 
 @pytest.mark.parametrize("dims,ranks", [((30, 25, 20), (4, 4, 4)), ((64, 40, 50), (5, 3, 6)), ((40, 70, 33), (6, 20, 5))])
-def test_fibre_sum_reuse_matches_full_ttm(mb, monkeypatch, dims, ranks):
-    """Y_(b) from the previous mode's fibre sums (default) equals the full
-    second TTM pass (MACH_NO_FIBRE_REUSE) to fp64 rounding."""
+def test_sweep_variants_match_full_ttm(mb, monkeypatch, dims, ranks):
+    """The overlapped sweep (split TTM, default), the fibre-sum reuse sweep
+    (MACH_NO_OVERLAP) and plain full TTMs for every mode (both off) give the
+    same model to fp64 rounding."""
     x = lowrank_numpy(dims, ranks, 0.01, seed=6)
 
-    def run(off):
-        if off:
-            monkeypatch.setenv("MACH_NO_FIBRE_REUSE", "1")
-        else:
-            monkeypatch.delenv("MACH_NO_FIBRE_REUSE", raising=False)
+    def run(**env):
+        for k in ("MACH_NO_OVERLAP", "MACH_NO_FIBRE_REUSE"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         return mb.mach_hooi(x, ranks, mb.SparsifyConfig(0.2, 3), mb.HooiConfig(6, 0.0)).model
 
-    a, b = run(False), run(True)
-    assert a.iterations == b.iterations
-    for fa, fb in zip(a.factors, b.factors):
-        assert subspace_sin(fa, fb) <= 1e-10
-    assert np.abs(np.array(a.sweep_fits) - np.array(b.sweep_fits)).max() <= 1e-12
+    full = run(MACH_NO_OVERLAP="1", MACH_NO_FIBRE_REUSE="1")
+    for m in (run(), run(MACH_NO_OVERLAP="1")):
+        assert m.iterations == full.iterations
+        for fa, fb in zip(m.factors, full.factors):
+            assert subspace_sin(fa, fb) <= 1e-10
+        assert np.abs(np.array(m.sweep_fits) - np.array(full.sweep_fits)).max() <= 1e-12
