@@ -830,12 +830,13 @@ __global__ void __launch_bounds__(512, 3) y_from_segments_kernel(const int* __re
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const int row = blockIdx.x;
+    std::uint32_t phase = 0;
+    bool ustaged = false;
+    for (int row = blockIdx.x; row < rows; row += gridDim.x) {  // rows share the staged U
     const int s0 = seg_ptr[row] * ptr_mul, s1 = seg_ptr[row + 1] * ptr_mul;
     T acc[RN];
 #pragma unroll
     for (int q = 0; q < RN; ++q) acc[q] = T(0);
-    std::uint32_t phase = 0;
     for (int base = s0, first = 1; base < s1 || first; base += chunk, first = 0) {
         const int m = max(0, min(chunk, s1 - base));
         const unsigned char* fsrc = reinterpret_cast<const unsigned char*>(fseg + static_cast<long long>(base) * ra);
@@ -845,7 +846,7 @@ __global__ void __launch_bounds__(512, 3) y_from_segments_kernel(const int* __re
         const std::uint32_t fb = static_cast<std::uint32_t>(((fsrc - f0) + static_cast<std::size_t>(m) * ra * sizeof(T) + 15) & ~std::size_t(15));
         const std::uint32_t rb = static_cast<std::uint32_t>(((rsrc - r0) + static_cast<std::size_t>(m) * sizeof(int) + 15) & ~std::size_t(15));
         if (tid == 0) {
-            const std::uint32_t ubytes = first && un_rows > 0 ? static_cast<std::uint32_t>(ub) : 0u;
+            const std::uint32_t ubytes = !ustaged && un_rows > 0 ? static_cast<std::uint32_t>(ub) : 0u;
             ttm::mbar_expect_tx(&bar, ubytes + (m ? fb + rb : 0u));
             if (ubytes) ttm::bulk_g2s(sU, Un, ubytes, &bar);
             if (m) {
@@ -855,6 +856,7 @@ __global__ void __launch_bounds__(512, 3) y_from_segments_kernel(const int* __re
         }
         ttm::mbar_wait(&bar, phase);
         phase ^= 1u;
+        ustaged = true;
         const T* sF = reinterpret_cast<const T*>(sFb + (fsrc - f0));
         const int* sR = reinterpret_cast<const int*>(sRb + (rsrc - r0));
         // two copies of the loop so the staged case compiles to shared-memory loads
@@ -884,6 +886,8 @@ __global__ void __launch_bounds__(512, 3) y_from_segments_kernel(const int* __re
         for (int q = 0; q < G; ++q) s += part[q * C + cc];
         const int a_ = cc % ra, n_ = cc / ra;
         Y[row + static_cast<long long>(a_ * sa + n_ * sn) * rows] = s;
+    }
+    __syncthreads();  // the next row's bulk copies overwrite the partials
     }
 }
 
@@ -1024,8 +1028,9 @@ void sparse_mode_stage2(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, con
                              ((static_cast<std::size_t>(chunk) * sizeof(int) + 16 + 15) & ~std::size_t(15));
     auto launch = [&](auto kern) {
         MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        MB_LAUNCH_PDL(ctx, kern, rows, threads, smem, P.st_base.get(), P.seg_ib.get(), F, ra, Ub, rbs, rb, sa, sb, rows,
-                      stage ? dims[b] : 0, chunk, 32, Y);
+        static const int rpc = std::getenv("MACH_S2_RPC") ? std::atoi(std::getenv("MACH_S2_RPC")) : 1;  // rows per CTA (1 measured best)
+        MB_LAUNCH_PDL(ctx, kern, (rows + rpc - 1) / rpc, threads, smem, P.st_base.get(), P.seg_ib.get(), F, ra, Ub, rbs,
+                      rb, sa, sb, rows, stage ? dims[b] : 0, chunk, 32, Y);
     };
     if (rb <= 4) launch(y_from_segments_kernel<T, 4>);
     else if (rb <= 8) launch(y_from_segments_kernel<T, 8>);
