@@ -292,9 +292,8 @@ def run_mach(args, rank, world, local):
                 "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                 "traffic_source": traffic.get("source") if traffic else None,
                 "bytes_per_launch": bytes_per_launch,
-                "bytes_model": "per TTM launch, averaged over the modes that run one: nnz*(inner index 2|4 B + value) "
-                               "+ tasks*(344 B record+descriptor + partial row block) [+ fibre sums written + positions "
-                               "read for the next mode]",
+                "bytes_model": "per TTM launch (the overlapped sweep's stage 1, one per mode): nnz*(inner index 2|4 B "
+                               "+ value) + tasks*(344 B record+descriptor + 32 fibre sums of r_a values written)",
                 "avg_launch_ms": round(per_launch_ms, 5),
                 "share_of_sweep": round(tot / 2.0 / sweep_ms_prof, 3) if sweep_ms_prof else None,
                 "peak_source": peak_src}
