@@ -282,12 +282,8 @@ std::vector<double> download(Ctx* ctx, const DBuf<double>& b) {
 }
 
 // read the per-mode basis status, raise on completion failure, collect warnings
-std::vector<std::string> read_warnings(Ctx* ctx, const DBuf<int>& st, const std::vector<int>& ranks,
+std::vector<std::string> warnings_from(const std::vector<int>& h, const std::vector<int>& ranks,
                                        const std::vector<int>& modes) {
-    const int d = static_cast<int>(ranks.size());
-    std::vector<int> h(static_cast<std::size_t>(3 * d));
-    to_host(ctx, h.data(), st.get(), h.size());
-    sync(ctx);
     std::vector<std::string> w;
     for (int m : modes) {
         const int nr = h[3 * m], comp = h[3 * m + 1], fail = h[3 * m + 2];
@@ -296,6 +292,15 @@ std::vector<std::string> read_warnings(Ctx* ctx, const DBuf<int>& st, const std:
         if (comp) w.push_back(completion_warning(m, nr, ranks[static_cast<std::size_t>(m)]));
     }
     return w;
+}
+
+std::vector<std::string> read_warnings(Ctx* ctx, const DBuf<int>& st, const std::vector<int>& ranks,
+                                       const std::vector<int>& modes) {
+    const int d = static_cast<int>(ranks.size());
+    std::vector<int> h(static_cast<std::size_t>(3 * d));
+    to_host(ctx, h.data(), st.get(), h.size());
+    sync(ctx);
+    return warnings_from(h, ranks, modes);
 }
 
 double fit_from(double normX2, double err2) {
@@ -497,16 +502,12 @@ struct SparseSession : SessionBase {
     bool f0_ready = false;  // Fov holds mode 0's stage 1 for the current factors
     bool overlap_ok() const { return overlap && !sharded; }
     void stage1(int m) {
-        static const int dbg_skip = std::getenv("MACH_DBG_SKIP_STAGE1") ? std::atoi(std::getenv("MACH_DBG_SKIP_STAGE1")) : -1;
-        if (dbg_skip == 9 || dbg_skip == m) return;  // timing experiments only (results are wrong)
         static const int reserve = std::getenv("MACH_OV_RESERVE") ? std::atoi(std::getenv("MACH_OV_RESERVE")) : 16;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
         sparse_mode_stage1<T>(ctx, *plans[static_cast<std::size_t>(m)], dims, ranks, Urp, Fov.get(), sms - reserve);
     }
     void stage2(int m) {
-        static const bool dbg_skip = std::getenv("MACH_DBG_SKIP_STAGE2") != nullptr;
-        if (dbg_skip) return;  // timing experiments only (results are wrong)
         auto& P = *plans[static_cast<std::size_t>(m)];
         sparse_mode_stage2<T>(ctx, P, dims, ranks, Fov.get(), Urp[static_cast<std::size_t>(P.b)], Y.get());
     }
@@ -548,9 +549,15 @@ struct SparseSession : SessionBase {
         core_device();
         return fit_host();
     }
-    double fit_host() {
+    // st_out: if given, the per-mode basis status is read back with the same
+    // synchronisation (one host round trip per sweep)
+    double fit_host(std::vector<int>* st_out = nullptr) {
         double sc[2];
         to_host(ctx, sc, fs.scal.get(), 2);
+        if (st_out) {
+            st_out->resize(static_cast<std::size_t>(3 * d));
+            to_host(ctx, st_out->data(), fs.st.get(), st_out->size());
+        }
         sync(ctx);
         const double e2 = sc[0] - sc[1];
         const double guard = std::is_same<T, double>::value ? 1e-6 : 1e-3;
@@ -773,8 +780,9 @@ struct SparseSession : SessionBase {
         } else {
             sweep_body();
         }
-        fit = fit_host();
-        warnings = read_warnings(ctx, fs.st, ranks, all);
+        std::vector<int> st;
+        fit = fit_host(&st);
+        warnings = warnings_from(st, ranks, all);
     }
     void* ext_mode_y(int m, int* rows, int* cols) override {
         if (m < 0 || m >= d) throw_arg("mode out of range");

@@ -39,5 +39,5 @@ for rep in range(3):
     lib.mach_sparse_free(hs)
     lib.mach_dense_free(hd)
     print(f"rep {rep}: upload {1e3*(t1-t0):.2f} ms ({math.prod(dims)*4/(t1-t0)/1e9:.1f} GB/s), job {1e3*(t2-t1):.2f} ms "
-          f"[sample {sample.value:.2f} setup {setup.value:.2f} hosvd {hosvd.value:.2f} sweeps {sum(sw):.2f}], "
+          f"[sample {sample.value:.2f} setup {setup.value:.2f} hosvd {hosvd.value:.2f} sweeps {sum(sw):.2f} = {[round(v, 2) for v in sw]}], "
           f"download {1e3*(t3-t2):.2f} ms, total {1e3*(t3-t0):.2f} ms")
