@@ -124,9 +124,17 @@ inline bool max_carveout(const void* f) {
 // this way starts with pdl_enter(), whose griddepcontrol.wait blocks until the
 // predecessor grid has completed and its writes are visible (a no-op when the
 // kernel was launched without the attribute).  MACH_NO_PDL=1 disables it.
+#ifndef MACH_PDL_TRIGGER_FIRST
+#define MACH_PDL_TRIGGER_FIRST 1
+#endif
+__device__ __forceinline__ constexpr bool pdl_trigger_first() { return MACH_PDL_TRIGGER_FIRST != 0; }
 __device__ __forceinline__ void pdl_enter() {
+    // trigger first: the dependent grid may launch (and queue its CTAs) as
+    // soon as all of this grid's CTAs have started; it still waits for this
+    // grid's completion in its own griddepcontrol.wait
+    if (pdl_trigger_first()) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (!pdl_trigger_first()) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 inline bool pdl_on() {
     static const bool off = std::getenv("MACH_NO_PDL") != nullptr;
