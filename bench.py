@@ -5,8 +5,10 @@ Workload (BASELINE.json configs[1], "C2"): 512x512x512 fp32 Tucker rank
 (10,10,10) + 1% noise, MACH p = 0.05 (~6.7M nonzeros), HOSVD + 5 HOOI sweeps,
 1 GPU.  A "step" is one HOOI sweep over the sampled tensor (all mode updates +
 core + fit + stop check, tucker.cpp:80-106).  value = nnz / mean sweep time
-(GNNZ/s), device-timed with CUDA events on the library's stream, L2 flushed
-(256 MiB write) before every timed sweep.
+(GNNZ/s) over K steady-state sweeps after W warm-up sweeps (defaults 20 / 5;
+SURVEY §8d times sweeps 2..N), device-timed with CUDA events on the library's
+stream, L2 flushed (256 MiB write) before every timed sweep.  e2e runs the
+config's whole job (C2: HOSVD + 5 sweeps) from pinned host memory.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mach|reference] [--config c2]
 
@@ -36,8 +38,8 @@ FALLBACK_HBM_GBS = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mach", choices=["mach", "reference"])
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -331,7 +333,7 @@ def run_mach(args, rank, world, local):
 
     # ---- e2e: reference-facing call with host buffers (pinned) ----
     if not args.no_e2e:
-        out["e2e"] = run_e2e(args, mb, x, dims, ranks, p, seed_mach, nnz, vsize, dev, local)
+        out["e2e"] = run_e2e(args, mb, x, dims, ranks, p, seed_mach, nnz, vsize, dev, local, sweeps)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = cpu_baseline(x, dims, ranks, p, seed_mach)
     if torch.distributed.is_initialized():
@@ -365,7 +367,7 @@ def measured_traffic(config):
     return {"dram_bytes_per_launch": sum(b for _, b in sel) / len(sel), "source": ", ".join(sorted(p for p, _ in sel))}
 
 
-def run_e2e(args, mb, x, dims, ranks, p, seed, nnz, vsize, dev, local):
+def run_e2e(args, mb, x, dims, ranks, p, seed, nnz, vsize, dev, local, sweeps):
     """mach_mach_hooi through the C ABI from pinned host memory: H2D of the
     dense tensor, sampling, layouts, HOSVD, K sweeps, D2H of the model."""
     import ctypes as C
@@ -381,7 +383,7 @@ def run_e2e(args, mb, x, dims, ranks, p, seed, nnz, vsize, dev, local):
     dt = L.MACH_F32 if vsize == 4 else L.MACH_F64
     dims_c = (C.c_int * len(dims))(*dims)
     ranks_c = (C.c_int * len(ranks))(*ranks)
-    sweeps = args.steps
+    # the config's job length (C2: HOSVD + 5 sweeps), independent of --steps
     best = None
     for rep in range(3):  # best of 3 (the first pays one-time module loading)
         torch.cuda.synchronize()
