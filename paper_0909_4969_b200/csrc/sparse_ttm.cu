@@ -29,6 +29,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -623,7 +624,15 @@ std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>
     kf.mode[kf.nf] = n; kf.shift[kf.nf++] = P->ba + P->bb;
     // the sampler's flat order already is (i_2, i_1, i_0) lexicographic
     const bool natural = (d == 3 && n == 2 && a == 0) || (d == 2 && n == 1 && a == 0);
+    static const bool tdbg = std::getenv("MACH_DEBUG_SETUP") != nullptr;
+    auto tnow = [&]() {
+        if (!tdbg) return 0.0;
+        sync(ctx);
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double t0 = tnow();
     build_sorted<T>(ctx, X, kf, total, P->key64, P->keys, P->vals, !natural);
+    const double t1 = tnow();
 
     const int rows = X->dims[n];
     P->rows = rows;
@@ -640,7 +649,11 @@ std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>
                        reinterpret_cast<const unsigned int*>(P->keys.get()), nnz, P->ba + P->bb, P->row_start.get(),
                        P->row_end.get());
     }
+    const double t2 = tnow();
     build_ttm_layout<T>(ctx, nnz, *P);
+    const double t3 = tnow();
+    if (tdbg) std::fprintf(stderr, "[setup] mode %d a=%d: sort %.3f ms, bounds %.3f ms, layout %.3f ms\n", n, a, t1 - t0,
+                           t2 - t1, t3 - t2);
     slot = P;
     return P;
 }
