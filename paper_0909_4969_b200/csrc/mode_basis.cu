@@ -122,9 +122,47 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
     double* wsp = sm + static_cast<std::size_t>(npad) * ldg;        // CTA 0
 
     // ---- phase A: partial Gram of this row block ----
+    __shared__ __align__(8) std::uint64_t ybar;
     if (rank > 0) {
         const int nr8z = (nr + 7) & ~7;  // rows zero-filled to a whole MMA tile
-        for (int base = threadIdx.x; base < nr8z * npad; base += 8 * kThreads) {
+        // the block's column segments (contiguous in the column-major Y)
+        // arrive by 1-D TMA bulk copies into the (still unused) partial-Gram
+        // region, one per column, then widen to fp64 row-major: one L2
+        // round trip instead of a dependent batch of loads per thread
+        const std::size_t seg = static_cast<std::size_t>(nr) * sizeof(T);
+        const bool bulk = nr > 0 && (seg % 16) == 0 && ((static_cast<std::size_t>(r0) * sizeof(T)) % 16) == 0 &&
+                          ((static_cast<std::size_t>(A.rows) * sizeof(T)) % 16) == 0 &&
+                          (reinterpret_cast<std::uintptr_t>(A.Y) % 16) == 0 &&
+                          static_cast<std::size_t>(n) * seg <= static_cast<std::size_t>(npad) * ldg * sizeof(double);
+        if (bulk) {
+            T* stg = reinterpret_cast<T*>(P);  // n segments of nr values
+            if (threadIdx.x == 0) {
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(&ybar))) : "memory");
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                                 static_cast<std::uint32_t>(__cvta_generic_to_shared(&ybar))),
+                             "r"(static_cast<std::uint32_t>(n * seg))
+                             : "memory");
+            }
+            __syncthreads();
+            for (int c = threadIdx.x; c < n; c += kThreads)
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 static_cast<std::uint32_t>(__cvta_generic_to_shared(stg + static_cast<std::size_t>(c) * nr))),
+                             "l"(A.Y + r0 + static_cast<std::size_t>(c) * A.rows), "r"(static_cast<std::uint32_t>(seg)),
+                             "r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(&ybar)))
+                             : "memory");
+            asm volatile(
+                "{\n\t.reg .pred p;\n"
+                "YW_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+                "@!p bra YW_%=;\n}" ::"r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(&ybar)))
+                : "memory");
+            for (int e = threadIdx.x; e < nr8z * npad; e += kThreads) {
+                const int c = e / nr8z, i = e - c * nr8z;
+                Yb[i * YS + c] = (i < nr && c < n) ? static_cast<double>(stg[static_cast<std::size_t>(c) * nr + i]) : 0.0;
+            }
+        }
+        for (int base = threadIdx.x; !bulk && base < nr8z * npad; base += 8 * kThreads) {
             double v[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {  // eight global loads in flight
