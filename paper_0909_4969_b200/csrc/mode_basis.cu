@@ -56,6 +56,7 @@ struct MBArgs {
     int ch;         // rows per row-block CTA (multiple of 4)
     int filter_first;  // warm start: filter with the previous Ritz values before the first Rayleigh-Ritz
     int force_fallback;  // test hook: treat the eigensolve as uncertified
+    double* Vg;          // npad x VS: V for the row blocks' bulk copy (null: DSMEM reads)
 };
 
 template <int B>
@@ -122,7 +123,8 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
     double* wsp = sm + static_cast<std::size_t>(npad) * ldg;        // CTA 0
 
     // ---- phase A: partial Gram of this row block ----
-    __shared__ __align__(8) std::uint64_t ybar;
+    __shared__ __align__(8) std::uint64_t ybar;  // row CTAs: phase A's Y copy (phase 0), phase D's V copy
+    std::uint32_t ybar_phase = 0u;
     if (rank > 0) {
         const int nr8z = (nr + 7) & ~7;  // rows zero-filled to a whole MMA tile
         // the block's column segments (contiguous in the column-major Y)
@@ -134,11 +136,14 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
                           ((static_cast<std::size_t>(A.rows) * sizeof(T)) % 16) == 0 &&
                           (reinterpret_cast<std::uintptr_t>(A.Y) % 16) == 0 &&
                           static_cast<std::size_t>(n) * seg <= static_cast<std::size_t>(npad) * ldg * sizeof(double);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(&ybar))) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
         if (bulk) {
+            ybar_phase = 1u;  // the V copy in phase D completes phase 1
             T* stg = reinterpret_cast<T*>(P);  // n segments of nr values
             if (threadIdx.x == 0) {
-                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(&ybar))) : "memory");
-                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                                  static_cast<std::uint32_t>(__cvta_generic_to_shared(&ybar))),
                              "r"(static_cast<std::uint32_t>(n * seg))
@@ -279,8 +284,17 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
             __syncthreads();
             if (!conv || A.force_fallback)  // hand G to the exact solver
                 for (int e = threadIdx.x; e < n * n; e += kThreads) A.Gout[e] = G[(e % n) + (e / n) * ldg];
-            // V (first k Ritz vectors) stays in ws.X for the row blocks
+            // V (first k Ritz vectors) stays in ws.X for the row blocks; in the
+            // fast path it is also written to global memory in the row blocks'
+            // layout (npad x VS, zero padded) for their single bulk copy
             if (threadIdx.x == 0) flagw = static_cast<int>(X - wsp);  // offset of the final block
+            if (conv && !A.force_fallback && A.Vg) {
+                const int KPv = (k + 7) & ~7, VSv = frag_stride(KPv);
+                for (int e = threadIdx.x; e < npad * VSv; e += kThreads) {
+                    const int r = e / VSv, j = e - (e / VSv) * VSv;
+                    A.Vg[e] = (r < n && j < k) ? X[r * Sub<B>::XS + j] : 0.0;
+                }
+            }
         }
         __syncthreads();
     }
@@ -315,11 +329,30 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
     double* Wb = Vl + static_cast<std::size_t>(npad) * VS;   // nr8 x VS
     double* Wt = Wb + static_cast<std::size_t>(nr8) * VS;    // nr8 x VS
     if (rank > 0) {
-        const int xoff = *cluster.map_shared_rank(&flagw, 0);
-        const double* Xr = cluster.map_shared_rank(wsp, 0) + xoff;
-        for (int e = threadIdx.x; e < npad * KP; e += kThreads) {
-            const int r = e / KP, j = e - (e / KP) * KP;
-            Vl[r * VS + j] = (r < n && j < k) ? Xr[r * XS + j] : 0.0;
+        if (A.Vg) {  // one bulk copy from L2 (CTA 0 wrote it before cluster barrier #3)
+            const std::uint32_t vb = static_cast<std::uint32_t>(npad * VS * sizeof(double));
+            const std::uint32_t bar = static_cast<std::uint32_t>(__cvta_generic_to_shared(&ybar));
+            if (threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(vb) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 static_cast<std::uint32_t>(__cvta_generic_to_shared(Vl))),
+                             "l"(A.Vg), "r"(vb), "r"(bar)
+                             : "memory");
+            }
+            asm volatile(
+                "{\n\t.reg .pred p;\n"
+                "VW_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                "@!p bra VW_%=;\n}" ::"r"(bar), "r"(ybar_phase)
+                : "memory");
+        } else {
+            const int xoff = *cluster.map_shared_rank(&flagw, 0);
+            const double* Xr = cluster.map_shared_rank(wsp, 0) + xoff;
+            for (int e = threadIdx.x; e < npad * KP; e += kThreads) {
+                const int r = e / KP, j = e - (e / KP) * KP;
+                Vl[r * VS + j] = (r < n && j < k) ? Xr[r * XS + j] : 0.0;
+            }
         }
         __syncthreads();
         if (tsa && rank == 1 && threadIdx.x == 0) tsa[220] = static_cast<long long>(mb_gtimer());
@@ -702,6 +735,8 @@ bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double
     DBuf<double> sig(ctx, k), Gout(ctx, static_cast<std::size_t>(n) * n), Wout(ctx, static_cast<std::size_t>(rows) * k),
         V(ctx, static_cast<std::size_t>(n) * k);
     DBuf<int> est(ctx, 3), flags(ctx, 4);
+    DBuf<double> Vg(ctx, static_cast<std::size_t>((n + 7) & ~7) * frag_stride((k + 7) & ~7));
+    A.Vg = Vg.get();
     A.sig = sig.get(); A.estatus = est.get(); A.Gout = Gout.get(); A.Wout = Wout.get(); A.flags = flags.get();
     DBuf<double> work(ctx, eig_work_doubles(n, k));  // allocated before the launch: nothing may sit between it and after_basis
     bool ok = false;
