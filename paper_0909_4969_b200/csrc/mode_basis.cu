@@ -596,37 +596,46 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
     MB_STAMP(8);
     if (rank == 0 && threadIdx.x < k) {
         const int j = threadIdx.x;
-        double best = -1.0, val = 0.0;
-        int bi = 0x7fffffff;
-        for (int q = 1; q < CL; ++q) {
-            const double b = cluster.map_shared_rank(amax, q)[j];
-            const int i = cluster.map_shared_rank(aidx, q)[j];
-            if (b > best || (b == best && i < bi)) { best = b; bi = i; val = cluster.map_shared_rank(dg, q)[j]; }
-        }
-        sgn[j] = val < 0.0 ? -1.0 : 1.0;
         A.sv[j] = A.sig[j];
         if (j == 0) {
             A.st[0] = k; A.st[1] = 0; A.st[2] = 0;
             A.flags[0] = 1; A.flags[1] = 0; A.flags[2] = 0; A.flags[3] = 0;
         }
     }
-    cluster.sync();  // #9
-    MB_STAMP(9);
     if (rank > 0) {
-        const double* s0 = cluster.map_shared_rank(sgn, 0);
-        if (threadIdx.x < k) dg[threadIdx.x] = s0[threadIdx.x];
+        // every row block combines the blocks' votes itself (all remote loads
+        // in flight, then the fixed-order scan): no extra cluster barrier
+        if (threadIdx.x < k) {
+            const int j = threadIdx.x;
+            double bq[16], vq[16];
+            int iq[16];
+#pragma unroll
+            for (int q = 1; q < 16; ++q) {
+                if (q < CL) {
+                    bq[q] = cluster.map_shared_rank(amax, q)[j];
+                    iq[q] = cluster.map_shared_rank(aidx, q)[j];
+                    vq[q] = cluster.map_shared_rank(dg, q)[j];
+                }
+            }
+            double best = -1.0, val = 0.0;
+            int bi = 0x7fffffff;
+#pragma unroll
+            for (int q = 1; q < 16; ++q)
+                if (q < CL && (bq[q] > best || (bq[q] == best && iq[q] < bi))) { best = bq[q]; bi = iq[q]; val = vq[q]; }
+            sgn[j] = val < 0.0 ? -1.0 : 1.0;
+        }
         __syncthreads();
         for (int e = threadIdx.x; e < nr * k; e += kThreads) {
             const int i = e % nr, j = e / nr;
-            A.U[(r0 + i) + static_cast<std::size_t>(j) * A.rows] = dg[j] * Wb[i * VS + j];
+            A.U[(r0 + i) + static_cast<std::size_t>(j) * A.rows] = sgn[j] * Wb[i * VS + j];
         }
         if (A.Ur)
             for (int e = threadIdx.x; e < nr * A.rs; e += kThreads) {
                 const int i = e / A.rs, j = e - (e / A.rs) * A.rs;
-                A.Ur[static_cast<std::size_t>(r0 + i) * A.rs + j] = j < k ? static_cast<T>(dg[j] * Wb[i * VS + j]) : T(0);
+                A.Ur[static_cast<std::size_t>(r0 + i) * A.rs + j] = j < k ? static_cast<T>(sgn[j] * Wb[i * VS + j]) : T(0);
             }
     }
-    cluster.sync();  // #10: CTA 0's shared memory is no longer read remotely
+    cluster.sync();  // #10: no shared memory of this cluster is read remotely any more
     MB_STAMP(10);
     if (tstamp && threadIdx.x == 0) {
         long long t_;
