@@ -14,6 +14,7 @@
 // Output: k eigenvectors (n x k, column-major) for eigenvalues in descending
 // order and sigma_i = sqrt(max(0, lambda_i)) (linalg.cpp:116-117).
 // One thread block of 256 threads does everything; no host round trip.
+#include "basis_cta.cuh"
 #include "common.cuh"
 
 namespace machb {
@@ -82,13 +83,8 @@ __device__ double hash_unit(unsigned a, unsigned b) {
 // G: n x n (column-major, ld n).  work: n*n (only used when n > kSmemMatrixN)
 // plus per-target scratch 6*n*k.  V: n x k output, sig: k output.
 // status[0] = 0 ok; status[1] = 1 if the matrix is exactly zero.
-__global__ void __launch_bounds__(kEigThreads) eig_topk_kernel(const double* __restrict__ G, int n, int k,
-                                                               double* __restrict__ work, double* __restrict__ V,
-                                                               double* __restrict__ sig, int* __restrict__ status,
-                                                               const int* __restrict__ skip) {
-    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
-    if (skip && skip[0] == 1) return;  // the subspace solver already converged
-    extern __shared__ double sm[];
+__device__ void eig_topk_cta(const double* __restrict__ G, int n, int k, double* __restrict__ work,
+                             double* __restrict__ V, double* __restrict__ sig, int* __restrict__ status, double* sm) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     double* sv = sm;            // v (n)
     double* sp = sv + n;        // p / w (n)
@@ -344,6 +340,38 @@ __global__ void __launch_bounds__(kEigThreads) eig_topk_kernel(const double* __r
     }
 }
 
+__global__ void __launch_bounds__(kEigThreads) eig_topk_kernel(const double* __restrict__ G, int n, int k,
+                                                               double* __restrict__ work, double* __restrict__ V,
+                                                               double* __restrict__ sig, int* __restrict__ status,
+                                                               const int* __restrict__ skip) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
+    if (skip && skip[0] == 1) return;  // the subspace solver already converged
+    extern __shared__ double sm[];
+    eig_topk_cta(G, n, k, work, V, sig, status, sm);
+}
+
+// The fused mode basis's whole fallback chain in one launch (one no-op launch
+// on the fast path): the exact eigensolver if the subspace solver was not
+// certified (flags[0] == 0), then W = Y V, the basis and the row-major copy
+// as flagged (mb_fallback_cta).
+template <typename T>
+__global__ void __launch_bounds__(kEigThreads) mb_fallback_all_kernel(const double* __restrict__ Gout, int n, int k,
+                                                                      double* __restrict__ work, double* __restrict__ V,
+                                                                      double* __restrict__ sig, int* __restrict__ est,
+                                                                      const T* __restrict__ Y, int rows,
+                                                                      double* __restrict__ W, double* __restrict__ U,
+                                                                      double* __restrict__ sv, int* __restrict__ st,
+                                                                      T* __restrict__ Ur, int rs,
+                                                                      const int* __restrict__ flags) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
+    const bool eig = flags[0] == 0;
+    if (!eig && !flags[1] && !flags[2] && !flags[3]) return;
+    extern __shared__ double sm[];
+    if (eig) eig_topk_cta(Gout, n, k, work, V, sig, est, sm);
+    __syncthreads();
+    mb_fallback_cta<T>(Y, rows, n, V, k, W, sig, U, sv, st, Ur, rs, flags, sm);
+}
+
 std::size_t eig_smem_bytes(int n) {
     std::size_t words = static_cast<std::size_t>(8) * n + kEigWarps * n + 32;
     if (n <= kSmemMatrixN) words += static_cast<std::size_t>(n) * n;
@@ -365,5 +393,23 @@ void eig_topk(Ctx* ctx, const double* G, int n, int k, double* work, double* V, 
     if (smem > 227 * 1024) throw Error(MACH_ERR_INTERNAL, "eigen step too large for one CTA (n=" + std::to_string(n) + ")");
     MB_LAUNCH_PDL(ctx, eig_topk_kernel, 1, kEigThreads, smem, G, n, k, work, V, sig, status, skip);
 }
+
+template <typename T>
+void mb_fallback_all(Ctx* ctx, const double* Gout, int n, int k, double* work, double* V, double* sig, int* est,
+                     const T* Y, int rows, double* W, double* U, double* sv, int* st, T* Ur, int rs, const int* flags) {
+    const std::size_t smem = std::max(eig_smem_bytes(n), basis_smem(rows, k));
+    static bool attr_set = false;
+    if (!attr_set) {
+        MB_CUDA(cudaFuncSetAttribute(mb_fallback_all_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_set = true;
+    }
+    if (smem > 227 * 1024) throw Error(MACH_ERR_INTERNAL, "eigen step too large for one CTA (n=" + std::to_string(n) + ")");
+    MB_LAUNCH_PDL(ctx, mb_fallback_all_kernel<T>, 1, kEigThreads, smem, Gout, n, k, work, V, sig, est, Y, rows, W, U, sv,
+                  st, Ur, rs, flags);
+}
+template void mb_fallback_all<float>(Ctx*, const double*, int, int, double*, double*, double*, int*, const float*, int,
+                                     double*, double*, double*, int*, float*, int, const int*);
+template void mb_fallback_all<double>(Ctx*, const double*, int, int, double*, double*, double*, int*, const double*, int,
+                                      double*, double*, double*, int*, double*, int, const int*);
 
 }  // namespace machb

@@ -767,8 +767,8 @@ bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double
     // conditional graph node around them was measured slower (~6 us per node
     // per mode) than these no-op launches inside the sweep graph.
     const int* f = flags.get();
-    eig_topk(ctx, Gout.get(), n, k, work.get(), V.get(), sig.get(), est.get(), f + 0);
-    mb_fallback<T>(ctx, Y, rows, n, V.get(), k, Wout.get(), sig.get(), U, sv, st, Ur, rs, f);
+    mb_fallback_all<T>(ctx, Gout.get(), n, k, work.get(), V.get(), sig.get(), est.get(), Y, rows, Wout.get(), U, sv, st,
+                       Ur, rs, f);
     return true;
 }
 

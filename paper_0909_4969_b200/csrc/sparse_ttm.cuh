@@ -163,6 +163,10 @@ void factor_rowmajor_gated(Ctx* ctx, const double* U, int n, int r, int rs, T* o
 template <typename T>
 void mb_fallback(Ctx* ctx, const T* Y, int rows, int C, const double* V, int k, double* W, const double* sig, double* U,
                  double* sv, int* st, T* Ur, int rs, const int* flags);
+// the whole fallback chain (exact eigensolver + mb_fallback) in one flag-gated launch (eig.cu)
+template <typename T>
+void mb_fallback_all(Ctx* ctx, const double* Gout, int n, int k, double* work, double* V, double* sig, int* est,
+                     const T* Y, int rows, double* W, double* U, double* sv, int* st, T* Ur, int rs, const int* flags);
 // fused column-side mode basis (mode_basis.cu); false = not applicable
 template <typename T>
 bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
