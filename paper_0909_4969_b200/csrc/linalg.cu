@@ -482,6 +482,55 @@ void core_from_last(Ctx* ctx, const T* Y, int rows, int C, const double* U, int 
 template void core_from_last<float>(Ctx*, const float*, int, int, const double*, int, double*);
 template void core_from_last<double>(Ctx*, const double*, int, int, const double*, int, double*);
 
+// core_from_last and |core|^2 in one launch: each CTA's partial sum of
+// squares goes to part[block]; the last CTA to finish (atomic ticket) sums
+// the partials in block order (deterministic) and re-arms the ticket.
+template <typename T>
+__global__ void __launch_bounds__(256) core_sumsq_kernel(const T* __restrict__ Y, int rows, int C,
+                                                         const double* __restrict__ U, int r, double* __restrict__ core,
+                                                         double* __restrict__ part, unsigned* __restrict__ ticket,
+                                                         double* __restrict__ out) {
+    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
+    __shared__ double red[8];
+    __shared__ bool last;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    double s = 0.0;
+    if (warp < C * r) {
+        const int col = warp % C, alpha = warp / C;
+        for (int i = lane; i < rows; i += 32)
+            s += U[i + static_cast<std::size_t>(alpha) * rows] * static_cast<double>(Y[i + static_cast<std::size_t>(col) * rows]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) core[col + static_cast<std::size_t>(C) * alpha] = s;
+    }
+    if (lane == 0) red[threadIdx.x >> 5] = s * s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < 8; ++i) t += red[i];
+        part[blockIdx.x] = t;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double tot = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) tot += const_cast<volatile double*>(part)[b];
+        *out = tot;
+        *ticket = 0u;
+    }
+}
+
+template <typename T>
+void core_sumsq(Ctx* ctx, const T* Y, int rows, int C, const double* U, int r, double* core, double* part,
+                unsigned* ticket, double* out) {
+    const long long warps = static_cast<long long>(C) * r;
+    MB_LAUNCH_PDL(ctx, core_sumsq_kernel<T>, ceil_div(warps * 32, 256), 256, 0, Y, rows, C, U, r, core, part, ticket, out);
+}
+template void core_sumsq<float>(Ctx*, const float*, int, int, const double*, int, double*, double*, unsigned*, double*);
+template void core_sumsq<double>(Ctx*, const double*, int, int, const double*, int, double*, double*, unsigned*, double*);
+
 // ---------------------------------------------------------------------------
 // deterministic sum of squares: fixed grid, per-block partials, one final block
 // ---------------------------------------------------------------------------

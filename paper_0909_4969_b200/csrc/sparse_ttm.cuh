@@ -147,6 +147,10 @@ void basis_from_products(Ctx* ctx, const double* W, int n, int wc, int k, const 
 void identity_basis(Ctx* ctx, double* U, int n, int k, double* sv, int* st);
 template <typename T>
 void core_from_last(Ctx* ctx, const T* Y, int rows, int C, const double* U, int r, double* core);
+// core_from_last + |core|^2 into *out in one launch (part: >= blocks doubles; ticket: zeroed once, re-armed)
+template <typename T>
+void core_sumsq(Ctx* ctx, const T* Y, int rows, int C, const double* U, int r, double* core, double* part,
+                unsigned* ticket, double* out);
 template <typename T>
 void sumsq(Ctx* ctx, const T* x, long long n, double* scratch, double* out);
 int sumsq_scratch();

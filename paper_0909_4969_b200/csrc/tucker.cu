@@ -539,10 +539,22 @@ struct SparseSession : SessionBase {
     // updated factor), then fit = 1 - sqrt(|X|^2 - |G|^2)/|X| (orthonormal
     // factors).  Near-exact models take the reference's entrywise residual
     // (tucker.cpp:47-64) instead of the cancelling identity.
+    DBuf<unsigned> ticket;  // core_sumsq's last-block ticket (zeroed once)
     void core_device() {
         const int last = d - 1;
-        core_from_last<T>(ctx, Y.get(), dims[static_cast<std::size_t>(last)], C[static_cast<std::size_t>(last)],
-                          fs.U[static_cast<std::size_t>(last)].get(), ranks[static_cast<std::size_t>(last)], core.get());
+        const int rows = dims[static_cast<std::size_t>(last)], cols = C[static_cast<std::size_t>(last)];
+        const int r = ranks[static_cast<std::size_t>(last)];
+        const long long blocks = (static_cast<long long>(cols) * r * 32 + 255) / 256;
+        if (blocks <= sumsq_scratch()) {  // one launch: core + |core|^2
+            if (!ticket.get()) {
+                ticket.alloc(ctx, 1);
+                ticket.zero(ctx);
+            }
+            core_sumsq<T>(ctx, Y.get(), rows, cols, fs.U[static_cast<std::size_t>(last)].get(), r, core.get(), fs.red.get(),
+                          ticket.get(), fs.scal.get() + 1);
+            return;
+        }
+        core_from_last<T>(ctx, Y.get(), rows, cols, fs.U[static_cast<std::size_t>(last)].get(), r, core.get());
         sumsq<double>(ctx, core.get(), static_cast<long long>(core.n), fs.red.get(), fs.scal.get() + 1);
     }
     double core_and_fit() {
