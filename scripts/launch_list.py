@@ -4,8 +4,8 @@
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e
   python scripts/launch_list.py L.csv --sweeps 2 --tag r01_launches_c2
 
-A sweep ends with core_from_last_kernel -> sumsq_partial_kernel ->
-sum_final_kernel; the last --sweeps sweeps are tabulated (library kernels
+A sweep ends with core_sumsq_kernel (or, in older builds, core_from_last ->
+sumsq_partial -> sum_final); the last --sweeps sweeps are tabulated (library kernels
 only; the bench's L2-flush fill is listed separately).  Writes
 profiles/<tag>.csv (the raw list) and profiles/<tag>.md.
 """
@@ -43,8 +43,9 @@ for r in rd:
     us = v / 1e3 if unit in ("ns", "nsecond") else (v if unit in ("us", "usecond") else v * 1e3)
     rows.append((d["Kernel Name"], us))
 
-ends = [i for i, (k, _) in enumerate(rows) if "sum_final_kernel" in k and i >= 2
-        and "sumsq_partial_kernel" in rows[i - 1][0] and "core_from_last_kernel" in rows[i - 2][0]]
+ends = [i for i, (k, _) in enumerate(rows) if "core_sumsq_kernel" in k or (
+    "sum_final_kernel" in k and i >= 2 and "sumsq_partial_kernel" in rows[i - 1][0]
+    and "core_from_last_kernel" in rows[i - 2][0])]
 assert len(ends) > a.sweeps, f"found {len(ends)} sweeps"
 sel = rows[ends[-a.sweeps - 1] + 1: ends[-1] + 1]
 lib = [(k, us) for k, us in sel if "machb" in k or "ttm::" in k]
