@@ -15,6 +15,16 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxB = 32;
+// smallest n for which the subspace solver (and the fused mode basis) is used
+// instead of the exact tridiagonal solver; MACH_SUB_MIN_N overrides for tests
+#ifndef MACH_SUB_MIN_N_DEFAULT
+#define MACH_SUB_MIN_N_DEFAULT 16
+#endif
+inline int sub_min_n() {
+    static const int v = std::getenv("MACH_SUB_MIN_N") ? std::atoi(std::getenv("MACH_SUB_MIN_N")) : MACH_SUB_MIN_N_DEFAULT;
+    return v;
+}
+#define kSubMinN (::machb::sub_min_n())
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

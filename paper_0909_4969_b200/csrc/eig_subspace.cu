@@ -236,10 +236,15 @@ int eig_block(int n, int k) {
     return std::min(n, b);
 }
 
+bool subspace_applies(int n, int k) {
+    const int b = eig_block(n, k);
+    return n > kSubMinN && b < n && b <= kMaxB && (b % 8) == 0 && k <= b - 2;
+}
+
 bool eig_select(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
                 double* V, double* sig, int* status) {
     bool launched = false;
-    if (n > 48 && b < n && b <= kMaxB && (b % 8) == 0 && k <= b - 2)
+    if (n > kSubMinN && b < n && b <= kMaxB && (b % 8) == 0 && k <= b - 2)
         launched = eig_subspace(ctx, G, n, k, X0, x0_cols, Xkeep, b, V, sig, status);
     DBuf<double> work(ctx, eig_work_doubles(n, k));
     eig_topk(ctx, G, n, k, work.get(), V, sig, status, launched ? status : nullptr);
@@ -254,7 +259,7 @@ void eig_select_batched(Ctx* ctx, std::vector<EigJob> jobs) {
     int b = 0;
     for (auto& J : jobs) {
         const int bj = eig_block(J.n, J.k);
-        const bool ok = J.n > 48 && bj < J.n && bj <= kMaxB && (bj % 8) == 0 && J.k <= bj - 2;
+        const bool ok = J.n > kSubMinN && bj < J.n && bj <= kMaxB && (bj % 8) == 0 && J.k <= bj - 2;
         if (!ok || (b && bj != b)) same = false;
         b = bj;
     }

@@ -722,7 +722,7 @@ bool launch_mode_basis(Ctx* ctx, MBArgs<T> A) {
 template <typename T>
 bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
                       double* U, double* sv, int* st, T* Ur, int rs) {
-    if (k < 1 || k > kMaxK || n <= 48 || b >= n || k > b - 2 || (b % 8) != 0 || rows < 2 * kCL) return false;
+    if (k < 1 || k > kMaxK || n <= kSubMinN || b >= n || k > b - 2 || (b % 8) != 0 || rows < 2 * kCL) return false;
     MBArgs<T> A{};
     A.Y = Y; A.rows = rows; A.n = n; A.k = k; A.rs = rs;
     // residual certificate: 1e-12 * theta_1 for fp64 data; fp32 data carry

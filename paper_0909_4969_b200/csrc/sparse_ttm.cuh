@@ -119,6 +119,8 @@ inline std::size_t warm_doubles(int n, int b) { return static_cast<std::size_t>(
 bool eig_select(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
                 double* V, double* sig, int* status);
 int eig_block(int n, int k);
+// whether eig_select uses the warm-startable subspace solver for this shape
+bool subspace_applies(int n, int k);
 struct EigJob {
     const double* G;
     int n, k;

@@ -158,7 +158,7 @@ void lsb_device(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U
         if (warm->cols > 0) {
             X0 = warm->X.get();
             x0c = warm->cols;
-        } else if (Uprev) {
+        } else if (Uprev && subspace_applies(side, kk)) {  // (the exact solver takes no start block)
             if (row_side) {
                 X0 = Uprev;
                 x0c = kk;
@@ -739,9 +739,9 @@ struct SparseSession : SessionBase {
         static const bool off = std::getenv("MACH_NO_GRAPH") || std::getenv("MACH_DEBUG_EIG") ||
                                 std::getenv("MACH_DEBUG_EIG_T") || std::getenv("MACH_TTM_TS");
         if (off || ctx->profile || sharded) return false;
-        for (int i = 0; i < d; ++i)
-            if (warm[static_cast<std::size_t>(i)].cols <= 0) return false;  // first sweep seeds the warm blocks
-        return true;
+        // the first sweep seeds the warm blocks of the modes that keep them;
+        // from the second on every sweep issues the same launches
+        return iterations >= 1;
     }
     void sweep_body() {
         if (overlap_ok()) {
