@@ -89,6 +89,45 @@ __global__ void __launch_bounds__(256) mode_product_fibre_kernel(const Tin* __re
     }
 }
 
+// inner == 1 (contracting the fastest mode): a fibre is contiguous, so one
+// warp takes it (lanes over r, coalesced), then reduces the J sums.
+template <typename Tin, int JB>
+__global__ void __launch_bounds__(256) mode_product_row_kernel(const Tin* __restrict__ in, int len, long long outer,
+                                                               const double* __restrict__ U, int J, int transpose,
+                                                               int stage, double* __restrict__ out) {
+    extern __shared__ double us[];  // us[q * len + r] = M(q, r): lanes (consecutive r) hit consecutive banks
+    if (stage) {
+        for (int e = threadIdx.x; e < len * J; e += blockDim.x) {
+            const int q = e / len, r = e - (e / len) * len;
+            us[e] = transpose ? U[r + static_cast<long long>(len) * q] : U[q + static_cast<long long>(J) * r];
+        }
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+    const long long nw = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+    for (long long c = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5; c < outer; c += nw) {
+        const Tin* src = in + static_cast<long long>(len) * c;
+        double acc[JB];
+#pragma unroll
+        for (int q = 0; q < JB; ++q) acc[q] = 0.0;
+        for (int r = lane; r < len; r += 32) {
+            const double x = static_cast<double>(src[r]);
+#pragma unroll
+            for (int q = 0; q < JB; ++q)
+                if (q < J)
+                    acc[q] = fma(x, stage ? us[q * len + r] : (transpose ? U[r + static_cast<long long>(len) * q] : U[q + static_cast<long long>(J) * r]), acc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < JB; ++q) {
+            if (q >= J) break;
+            double v = acc[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) out[q + static_cast<long long>(J) * c] = v;
+        }
+    }
+}
+
 template <typename Tin, typename Tout>
 __global__ void matricize_kernel(const Tin* __restrict__ in, long long inner, int len, long long outer,
                                  Tout* __restrict__ out) {
@@ -175,9 +214,19 @@ void dense_mode_product(Ctx* ctx, const Tin* in, const std::vector<int>& dims, i
         const int stage = ub <= 48 * 1024 ? 1 : 0;
         const long long fib = s.inner * s.outer;
         auto go = [&](auto mode_product_fibre_kernel_jb) {  // (the name is the profiler's kernel label)
-            MB_LAUNCH(ctx, mode_product_fibre_kernel_jb, grid_for(fib), 256, stage ? ub : 0, in, s.inner, s.len, s.outer, U,
+            MB_LAUNCH(ctx, mode_product_fibre_kernel_jb, static_cast<unsigned>(std::min<long long>(grid_for(fib), 148 * 8)), 256, stage ? ub : 0, in, s.inner, s.len, s.outer, U,
                       J, transpose ? 1 : 0, stage, out);
         };
+        if (s.inner == 1) {
+            auto gr = [&](auto mode_product_row_kernel_jb) {  // (the name is the profiler's kernel label)
+                MB_LAUNCH(ctx, mode_product_row_kernel_jb, static_cast<unsigned>(std::min<long long>(grid_for(s.outer * 32), 148 * 8)), 256, stage ? ub : 0, in, s.len, s.outer,
+                          U, J, transpose ? 1 : 0, stage, out);
+            };
+            if (J <= 8) gr(mode_product_row_kernel<Tin, 8>);
+            else if (J <= 16) gr(mode_product_row_kernel<Tin, 16>);
+            else gr(mode_product_row_kernel<Tin, 32>);
+            return;
+        }
         if (J <= 8) go(mode_product_fibre_kernel<Tin, 8>);
         else if (J <= 16) go(mode_product_fibre_kernel<Tin, 16>);
         else go(mode_product_fibre_kernel<Tin, 32>);
