@@ -586,9 +586,52 @@ struct SparseSession : SessionBase {
     }
     bool sharded = false;  // |X|^2 set externally; no local entrywise residual guard
     void begin(mach_sparse* sp, const std::vector<int>& rk) {
+        want_hosvd = true;
         setup(sp, rk);
         hosvd_init();
     }
+    // HOSVD's row-side sparse Grams (atomic-throughput-bound, independent of
+    // the TTM layouts) run on a side stream while setup builds the layouts
+    // (small kernels and host syncs that leave the GPU mostly idle).
+    bool want_hosvd = false;
+    std::vector<DBuf<double>> preG;
+    cudaStream_t side = nullptr;
+    cudaEvent_t grams_done = nullptr;
+    void launch_row_grams() {
+        static const bool off = std::getenv("MACH_NO_ASYNC_GRAMS") != nullptr;
+        if (off) return;
+        preG.clear();
+        preG.resize(static_cast<std::size_t>(d));
+        bool any = false;
+        for (int m = 0; m < d; ++m) {
+            const int rows = dims[static_cast<std::size_t>(m)];
+            if (static_cast<long long>(rows) <= X->numel / rows) any = true;
+        }
+        if (!any) return;
+        if (!side) MB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        if (!grams_done) MB_CUDA(cudaEventCreateWithFlags(&grams_done, cudaEventDisableTiming));
+        cudaEvent_t ready;
+        MB_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        MB_CUDA(cudaEventRecord(ready, ctx->stream));  // the sampled tensor and |X|^2 are ready
+        MB_CUDA(cudaStreamWaitEvent(side, ready, 0));
+        cudaEventDestroy(ready);
+        cudaStream_t main = ctx->stream;
+        ctx->stream = side;
+        try {
+            for (int m = 0; m < d; ++m) {
+                const int rows = dims[static_cast<std::size_t>(m)];
+                if (static_cast<long long>(rows) > X->numel / rows) continue;  // column side: needs the layouts
+                preG[static_cast<std::size_t>(m)].alloc(ctx, static_cast<std::size_t>(rows) * rows);
+                sparse_row_gram<T>(ctx, X, m, normX2, preG[static_cast<std::size_t>(m)].get());
+            }
+        } catch (...) {
+            ctx->stream = main;
+            throw;
+        }
+        ctx->stream = main;
+        MB_CUDA(cudaEventRecord(grams_done, side));
+    }
+
     // start from given factors (a replicated HOSVD) instead of computing them
     void begin_from(mach_sparse* sp, const std::vector<int>& rk, const mach_model* init) {
         setup(sp, rk);
@@ -614,12 +657,13 @@ struct SparseSession : SessionBase {
         plans.resize(static_cast<std::size_t>(d));
         const bool no_overlap = std::getenv("MACH_NO_OVERLAP") != nullptr;  // read per session (tests toggle it)
         overlap = d == 3 && !no_overlap;
-        for (int m = 0; m < d; ++m)
-            plans[static_cast<std::size_t>(m)] = get_plan<T>(X, m, ranks, overlap ? (m + 1) % 3 : -1);
         sumsq<T>(ctx, static_cast<const T*>(X->val), X->nnz, fs.red.get(), fs.scal.get());
         to_host(ctx, &normX2, fs.scal.get(), 1);
         sync(ctx);
         X->norm2 = normX2;
+        if (want_hosvd) launch_row_grams();
+        for (int m = 0; m < d; ++m)
+            plans[static_cast<std::size_t>(m)] = get_plan<T>(X, m, ranks, overlap ? (m + 1) % 3 : -1);
         Ur.resize(static_cast<std::size_t>(d));
         Urp.resize(static_cast<std::size_t>(d));
         for (int m = 0; m < d; ++m) {
@@ -677,15 +721,21 @@ struct SparseSession : SessionBase {
                 throw Error(MACH_ERR_INTERNAL, "column-side sparse HOSVD wider than 4096 is not supported on device yet");
             w.n = w.row ? rows : static_cast<int>(cols);
             w.kc = w.row ? k : static_cast<int>(std::min<long long>(k, cols));
-            w.G.alloc(ctx, static_cast<std::size_t>(w.n) * w.n);
-            if (w.row) sparse_row_gram<T>(ctx, X, m, normX2, w.G.get());
-            else sparse_col_gram<T>(ctx, X, *plans[static_cast<std::size_t>(m)], cols, normX2, w.G.get());
+            if (w.row && m < static_cast<int>(preG.size()) && preG[static_cast<std::size_t>(m)].get()) {
+                w.G = std::move(preG[static_cast<std::size_t>(m)]);  // computed on the side stream during setup
+                w.G.s = ctx->stream;  // released in this stream's order, after its last use here
+            } else {
+                w.G.alloc(ctx, static_cast<std::size_t>(w.n) * w.n);
+                if (w.row) sparse_row_gram<T>(ctx, X, m, normX2, w.G.get());
+                else sparse_col_gram<T>(ctx, X, *plans[static_cast<std::size_t>(m)], cols, normX2, w.G.get());
+            }
             w.V.alloc(ctx, static_cast<std::size_t>(w.n) * w.kc);
             w.sig.alloc(ctx, w.kc);
             w.est.alloc(ctx, 3);
             jobs.push_back(EigJob{w.G.get(), w.n, w.kc, nullptr, 0, nullptr, w.V.get(), w.sig.get(), w.est.get(),
                                   nullptr, nullptr});
         }
+        if (grams_done) MB_CUDA(cudaStreamWaitEvent(ctx->stream, grams_done, 0));  // join the side stream's Grams
         eig_select_batched(ctx, jobs);
         for (int m = 0; m < d; ++m) {
             ModeWork& w = mw[static_cast<std::size_t>(m)];
@@ -734,6 +784,8 @@ struct SparseSession : SessionBase {
     ~SparseSession() override {
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         if (graph) cudaGraphDestroy(graph);
+        if (grams_done) cudaEventDestroy(grams_done);
+        if (side) cudaStreamDestroy(side);
     }
     bool graph_ok() const {
         static const bool off = std::getenv("MACH_NO_GRAPH") || std::getenv("MACH_DEBUG_EIG") ||
