@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) lg_rr_kernel(const LJobs J, int m
     const int it = st->it;
     SB::gram(X, AX, ws.H, npad);
     if (!SB::refine_rr(ws.H, ws.Hc, ws.W, ws.Z, ws.Q, ws.S, ws.th, k, &flag))
-        SB::jacobi(ws.H, ws.W, ws.th, it == 0 ? 10 : 6, ws.red, ws.Z);
+        SB::rr_hybrid(ws.H, ws.Hc, ws.W, ws.Z, ws.Q, ws.S, ws.J7, ws.th, k, &flag, ws.red, it == 0 ? 8 : 4);
     SB::rotate(X, ws.W, Y0, npad);
     SB::rotate(AX, ws.W, X, npad);  // X is free again: AX' lands there
     // roles: X' = old Y0, AX' = old X, Y0' = old AX

@@ -463,7 +463,8 @@ struct Sub {
     }
 
     // CTA-parallel cyclic Jacobi (circle-method rounds, 3 barrier phases each)
-    __device__ static int jacobi(double* H, double* W, double* th, int max_sweeps, double* red, double* Z) {
+    __device__ static int jacobi(double* H, double* W, double* th, int max_sweeps, double* red, double* Z,
+                                 bool sort = true) {
         __shared__ int jp[kMaxB / 2], jq[kMaxB / 2];
         __shared__ double jc[kMaxB / 2], js[kMaxB / 2];
         const int tid = threadIdx.x;
@@ -529,8 +530,25 @@ struct Sub {
                 __syncthreads();
             }
         }
-        sort_ritz(H, W, th, Z);
+        if (sort) sort_ritz(H, W, th, Z);
         return sweep;
+    }
+
+    // Rayleigh-Ritz of H when the perturbation rounds do not apply: two
+    // Jacobi sweeps bring H close to diagonal, then the perturbation rounds
+    // (quadratically convergent) finish; W = W_jacobi W_rounds.  Full Jacobi
+    // when the rounds still do not apply.  J7: B x B scratch.
+    __device__ static int rr_hybrid(double* H, double* Hc, double* W, double* Z, double* Q, double* S, double* J7,
+                                    double* th, int k, int* flag, double* red, int max_sweeps) {
+        jacobi(H, W, th, 2, red, Z, false);  // H <- W^T H W (unsorted)
+        for (int e = threadIdx.x; e < B * B; e += kThreads) J7[(e % B) + (e / B) * HS] = W[(e % B) + (e / B) * HS];
+        __syncthreads();
+        int nsw = 2;
+        if (!refine_rr(H, Hc, W, Z, Q, S, th, k, flag)) nsw += jacobi(H, W, th, max_sweeps, red, Z);
+        mm(J7, false, W, Z);  // Z = W_jacobi W_rest
+        for (int e = threadIdx.x; e < B * B; e += kThreads) W[(e % B) + (e / B) * HS] = Z[(e % B) + (e / B) * HS];
+        __syncthreads();
+        return nsw;
     }
 
     // max over wanted columns c < k of |AX_c - th_c X_c|
@@ -552,7 +570,7 @@ struct Sub {
 // shared-memory workspace of the solver (npad = n rounded up to 8)
 template <int B>
 struct SubWs {
-    double *H, *W, *S, *Z, *Q, *Hc, *th, *rinv, *coef, *red, *X, *AX, *Y0, *Y1;
+    double *H, *W, *S, *Z, *Q, *Hc, *J7, *th, *rinv, *coef, *red, *X, *AX, *Y0, *Y1;
     // blocks: if non-null, the four n x B blocks live there (global memory,
     // for n too large for shared memory) instead of after the small matrices
     __device__ SubWs(double* sm, int npad, double* blocks = nullptr) {
@@ -563,7 +581,8 @@ struct SubWs {
         Z = S + B * HS;
         Q = Z + B * HS;
         Hc = Q + B * HS;
-        th = Hc + B * HS;
+        J7 = Hc + B * HS;
+        th = J7 + B * HS;
         rinv = th + kMaxB;
         coef = rinv + kMaxB;
         red = coef + kMaxB;
@@ -573,7 +592,7 @@ struct SubWs {
         Y1 = Y0 + npad * XS;
     }
     __host__ __device__ static std::size_t doubles(int npad) { return small_doubles() + block_doubles(npad); }
-    __host__ __device__ static std::size_t small_doubles() { return 6ull * B * Sub<B>::HS + 3 * kMaxB + 32; }
+    __host__ __device__ static std::size_t small_doubles() { return 7ull * B * Sub<B>::HS + 3 * kMaxB + 32; }
     __host__ __device__ static std::size_t block_doubles(int npad) { return 4ull * npad * Sub<B>::XS; }
 };
 
@@ -644,7 +663,8 @@ __device__ double* subspace_core(SubWs<B>& ws, const double* G, int ldg, int n, 
         SB::gram(X, AX, H, npad);
         MB_STAMP(11);
         int nsw = 99;
-        if (!SB::refine_rr(H, Hc, W, Z, Q, S, th, k, &flag)) nsw = SB::jacobi(H, W, th, it == 0 ? 10 : 5, red, Z);
+        if (!SB::refine_rr(H, Hc, W, Z, Q, S, th, k, &flag))
+            nsw = SB::rr_hybrid(H, Hc, W, Z, Q, S, ws.J7, th, k, &flag, red, it == 0 ? 8 : 3);
         MB_STAMP(1000 + nsw);
         SB::rotate(X, W, Y0, npad);
         { double* t = X; X = Y0; Y0 = t; }
