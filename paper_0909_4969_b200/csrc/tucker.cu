@@ -598,8 +598,7 @@ struct SparseSession : SessionBase {
     cudaStream_t side = nullptr;
     cudaEvent_t grams_done = nullptr;
     void launch_row_grams() {
-        static const bool off = std::getenv("MACH_NO_ASYNC_GRAMS") != nullptr;
-        if (off) return;
+        if (std::getenv("MACH_NO_ASYNC_GRAMS")) return;  // read per session (tests toggle it)
         preG.clear();
         preG.resize(static_cast<std::size_t>(d));
         bool any = false;

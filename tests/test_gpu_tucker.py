@@ -313,3 +313,23 @@ def test_sweep_variants_match_full_ttm(mb, monkeypatch, dims, ranks):
         for fa, fb in zip(m.factors, full.factors):
             assert subspace_sin(fa, fb) <= 1e-10
         assert np.abs(np.array(m.sweep_fits) - np.array(full.sweep_fits)).max() <= 1e-12
+
+
+def test_side_stream_grams_bitwise_equal(mb, monkeypatch):
+    """HOSVD's row Grams computed on a side stream during setup (default) give
+    the same fixed-point Grams, hence bitwise the same model, as computing
+    them in line (MACH_NO_ASYNC_GRAMS)."""
+    x = lowrank_numpy((70, 60, 50), (5, 4, 6), 0.01, seed=12, dtype=np.float32)
+
+    def run(off):
+        if off:
+            monkeypatch.setenv("MACH_NO_ASYNC_GRAMS", "1")
+        else:
+            monkeypatch.delenv("MACH_NO_ASYNC_GRAMS", raising=False)
+        return mb.mach_hooi(mb.DenseTensor.from_numpy(x), (5, 4, 6), mb.SparsifyConfig(0.1, 5),
+                            mb.HooiConfig(3, 0.0)).model
+
+    a, b = run(False), run(True)
+    assert np.array_equal(a.core, b.core) and a.sweep_fits == b.sweep_fits
+    for fa, fb in zip(a.factors, b.factors):
+        assert np.array_equal(fa, fb)
