@@ -877,9 +877,23 @@ __global__ void __launch_bounds__(512, 3) y_from_segments_kernel(const int* __re
             for (int j = g; j < m; j += G) {
                 const T fv = sF[j * ra + r_a];
                 const T* ur = U + sR[j] * rns;
+                if constexpr (sizeof(T) == 4 && RN % 4 == 0) {
+                    // 128-bit row loads (rows are whole 16-byte units, zero padded)
 #pragma unroll
-                for (int q = 0; q < RN; ++q)
-                    if (q < rn) acc[q] = fma(fv, ur[q], acc[q]);
+                    for (int q = 0; q < RN; q += 4) {
+                        if (q < rn) {
+                            const float4 u4 = *reinterpret_cast<const float4*>(ur + q);
+                            acc[q] = fmaf(fv, u4.x, acc[q]);
+                            acc[q + 1] = fmaf(fv, u4.y, acc[q + 1]);
+                            acc[q + 2] = fmaf(fv, u4.z, acc[q + 2]);
+                            acc[q + 3] = fmaf(fv, u4.w, acc[q + 3]);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < RN; ++q)
+                        if (q < rn) acc[q] = fma(fv, ur[q], acc[q]);
+                }
             }
         };
         if (on) {
