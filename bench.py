@@ -154,7 +154,7 @@ def run_mach(args, rank, world, local):
     import torch
 
     import paper_0909_4969_b200 as mb
-    from paper_0909_4969_b200.synth import CONFIGS, lowrank_torch
+    from paper_0909_4969_b200.synth import CONFIGS, KIND, lowrank_torch
 
     dims, ranks, noise, p, sweeps, dtype = CONFIGS[args.config]
     torch.cuda.set_device(local)
@@ -164,7 +164,7 @@ def run_mach(args, rank, world, local):
         dist.init_process_group("nccl", device_id=dev)
     seed_data, seed_mach = 2, 7
 
-    x = lowrank_torch(dims, ranks, noise, seed=seed_data, dtype=dtype, device=dev)
+    x = lowrank_torch(dims, ranks, noise, seed=seed_data, dtype=dtype, device=dev, kind=KIND.get(args.config))
     ctx = mb.Context(local)
     stream = torch.cuda.Stream(device=dev)
     ctx.set_stream(stream.cuda_stream)

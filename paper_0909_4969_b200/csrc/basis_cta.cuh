@@ -106,10 +106,13 @@ std::size_t basis_smem(int n, int k);
 
 namespace {
 // CTA body (kB threads, shared memory basis_smem(n, k) at sm)
+// gv: optional global scratch for the n-vector (tall matricizations whose
+// n doubles do not fit in shared memory); then sm holds only the small parts
 __device__ void basis_from_products_cta(const double* __restrict__ W, int n, int wc, int k, const double* __restrict__ sig,
-                                        double* __restrict__ U, double* __restrict__ sv, int* __restrict__ st, double* sm) {
-    double* v = sm;
-    double* tcoef = v + n;
+                                        double* __restrict__ U, double* __restrict__ sv, int* __restrict__ st, double* sm,
+                                        double* gv = nullptr) {
+    double* v = gv ? gv : sm;
+    double* tcoef = gv ? sm : v + n;
     double* red = tcoef + k;
     int* redi = reinterpret_cast<int*>(red + 32);
     const double sigma1 = sig[0];

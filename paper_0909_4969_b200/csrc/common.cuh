@@ -92,7 +92,12 @@ inline bool max_carveout(const void* f) {
             MB_CUDA(cudaEventRecord(pe_.a, (ctx)->stream));                                          \
         }                                                                                            \
         kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);                              \
-        MB_CUDA(cudaGetLastError());                                                                 \
+        {                                                                                            \
+            cudaError_t le_ = cudaGetLastError();                                                    \
+            if (le_ != cudaSuccess)                                                                  \
+                throw ::machb::Error(MACH_ERR_CUDA, std::string("launch of " #kernel ": ") +         \
+                                                        cudaGetErrorString(le_));                    \
+        }                                                                                            \
         ++(ctx)->launches;                                                                           \
         if ((ctx)->profile) {                                                                        \
             MB_CUDA(cudaEventRecord(pe_.b, (ctx)->stream));                                          \
@@ -111,7 +116,12 @@ inline bool max_carveout(const void* f) {
             MB_CUDA(cudaEventCreate(&pe_.b));                                                        \
             MB_CUDA(cudaEventRecord(pe_.a, (ctx)->stream));                                          \
         }                                                                                            \
-        MB_CUDA(cudaLaunchKernelEx((cfgp), kernel, __VA_ARGS__));                                    \
+        {                                                                                            \
+            cudaError_t le_ = cudaLaunchKernelEx((cfgp), kernel, __VA_ARGS__);                       \
+            if (le_ != cudaSuccess)                                                                  \
+                throw ::machb::Error(le_ == cudaErrorMemoryAllocation ? MACH_ERR_OOM : MACH_ERR_CUDA, \
+                                     std::string("launch of ") + (name) + ": " + cudaGetErrorString(le_)); \
+        }                                                                                            \
         ++(ctx)->launches;                                                                           \
         if ((ctx)->profile) {                                                                        \
             MB_CUDA(cudaEventRecord(pe_.b, (ctx)->stream));                                          \

@@ -222,10 +222,10 @@ template void matmul_yv<double>(Ctx*, const double*, int, int, const double*, in
 __global__ void __launch_bounds__(kB) basis_from_side_kernel(const double* __restrict__ V, const double* __restrict__ sig,
                                                              int n, int k, const int* __restrict__ eig_status,
                                                              double* __restrict__ U, double* __restrict__ sv,
-                                                             int* __restrict__ st) {
+                                                             int* __restrict__ st, double* __restrict__ gv) {
     extern __shared__ double sm[];
-    double* v = sm;            // n
-    double* tcoef = v + n;     // k
+    double* v = gv ? gv : sm;             // n (global scratch for tall n)
+    double* tcoef = gv ? sm : v + n;      // k
     double* red = tcoef + k;   // 32
     int* redi = reinterpret_cast<int*>(red + 32);
     for (int idx = threadIdx.x; idx < n * k; idx += kB) U[idx] = V[idx];
@@ -254,11 +254,12 @@ __global__ void __launch_bounds__(kB) basis_from_products_kernel(const double* _
                                                                  const double* __restrict__ sig,
                                                                  const int* __restrict__ eig_status,
                                                                  double* __restrict__ U, double* __restrict__ sv,
-                                                                 int* __restrict__ st, const int* __restrict__ skip) {
+                                                                 int* __restrict__ st, const int* __restrict__ skip,
+                                                                 double* __restrict__ gv) {
     pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     if (skip && skip[0] == 0) return;  // the CholQR2 fast path already produced U
     extern __shared__ double sm[];
-    basis_from_products_cta(W, n, wc, k, sig, U, sv, st, sm);
+    basis_from_products_cta(W, n, wc, k, sig, U, sv, st, sm, gv);
     (void)eig_status;
 }
 
@@ -287,9 +288,27 @@ template void mb_fallback<double>(Ctx*, const double*, int, int, const double*, 
 
 std::size_t basis_smem(int n, int k) { return (static_cast<std::size_t>(n) + k + 32 + 32) * sizeof(double); }
 
+// n-vector scratch of the one-CTA basis kernels: shared memory, or global
+// memory for tall matricizations (C4's 65536-row time mode)
+namespace {
+constexpr std::size_t kBasisSmemMax = 160 * 1024;
+struct BasisScratch {
+    DBuf<double> g;
+    std::size_t smem = 0;
+    BasisScratch(Ctx* ctx, int n, int k) {
+        smem = basis_smem(n, k);
+        if (smem > kBasisSmemMax) {
+            g.alloc(ctx, static_cast<std::size_t>(n));
+            smem = basis_smem(0, k);
+        }
+    }
+};
+}  // namespace
+
 void basis_from_side(Ctx* ctx, const double* V, const double* sig, int n, int k, const int* eig_status, double* U,
                      double* sv, int* st) {
-    MB_LAUNCH(ctx, basis_from_side_kernel, 1, kB, basis_smem(n, k), V, sig, n, k, eig_status, U, sv, st);
+    BasisScratch bs(ctx, n, k);
+    MB_LAUNCH(ctx, basis_from_side_kernel, 1, kB, bs.smem, V, sig, n, k, eig_status, U, sv, st, bs.g.get());
 }
 
 // ---------------------------------------------------------------------------
@@ -419,7 +438,9 @@ __global__ void __launch_bounds__(kB) basis_products_fast_kernel(const double* _
 
 void basis_from_products_gated(Ctx* ctx, const double* W, int n, int wc, int k, const double* sig,
                                const int* eig_status, double* U, double* sv, int* st, const int* need) {
-    MB_LAUNCH_PDL(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st, need);
+    BasisScratch bs(ctx, n, k);
+    MB_LAUNCH_PDL(ctx, basis_from_products_kernel, 1, kB, bs.smem, W, n, wc, k, sig, eig_status, U, sv, st, need,
+                  bs.g.get());
 }
 
 void basis_from_products(Ctx* ctx, const double* W, int n, int wc, int k, const double* sig, const int* eig_status,
@@ -434,11 +455,12 @@ void basis_from_products(Ctx* ctx, const double* W, int n, int wc, int k, const 
         DBuf<int> slow(ctx, 1);
         MB_LAUNCH(ctx, basis_products_fast_kernel, 1, kB, fsm, W, n, k, sig, U, sv, st, slow.get());
         MB_LAUNCH_PDL(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st,
-                  static_cast<const int*>(slow.get()));
+                  static_cast<const int*>(slow.get()), static_cast<double*>(nullptr));
         return;
     }
-    MB_LAUNCH_PDL(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st,
-              static_cast<const int*>(nullptr));
+    BasisScratch bs(ctx, n, k);
+    MB_LAUNCH_PDL(ctx, basis_from_products_kernel, 1, kB, bs.smem, W, n, wc, k, sig, eig_status, U, sv, st,
+              static_cast<const int*>(nullptr), bs.g.get());
 }
 
 // ---------------------------------------------------------------------------

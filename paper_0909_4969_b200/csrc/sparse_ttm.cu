@@ -333,25 +333,29 @@ __global__ void row_gram_kernel(const K* __restrict__ keys, const T* __restrict_
     }
 }
 
-// column Gram: entries of one row of X_(n) are a run of equal key >> (ba+bb) in
-// the mode-n TTM layout; columns col = ia*ca + ib*cb.
+__device__ __forceinline__ long long decode_col(unsigned long long k, const ColDecode& D) {
+    long long c = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (j < D.nf) c += static_cast<long long>((k >> D.shift[j]) & D.mask[j]) * D.stride[j];
+    return c;
+}
+
+// column Gram: entries of one row of X_(n) are a run of equal key >> rsh in
+// the mode-n TTM layout; the column comes from the other fields (ColDecode).
 template <typename T, typename K>
-__global__ void col_gram_kernel(const K* __restrict__ keys, const T* __restrict__ vals, long long nnz, int ba, int bb,
-                                long long ca, long long cb, double scale, long long n,
-                                unsigned long long* __restrict__ G) {
+__global__ void col_gram_kernel(const K* __restrict__ keys, const T* __restrict__ vals, long long nnz, int rsh,
+                                ColDecode D, double scale, long long n, unsigned long long* __restrict__ G) {
     const long long x = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (x >= nnz) return;
-    const int sh = ba + bb;
     const unsigned long long kx = static_cast<unsigned long long>(keys[x]);
-    const unsigned long long row = kx >> sh;
-    const long long cx = static_cast<long long>(kx & ((1ull << ba) - 1ull)) * ca +
-                         static_cast<long long>((kx >> ba) & ((1ull << bb) - 1ull)) * cb;
+    const unsigned long long row = kx >> rsh;
+    const long long cx = decode_col(kx, D);
     const double vx = static_cast<double>(vals[x]);
     for (long long y = x; y >= 0; --y) {
         const unsigned long long ky = static_cast<unsigned long long>(keys[y]);
-        if ((ky >> sh) != row) break;
-        const long long cy = static_cast<long long>(ky & ((1ull << ba) - 1ull)) * ca +
-                             static_cast<long long>((ky >> ba) & ((1ull << bb) - 1ull)) * cb;
+        if ((ky >> rsh) != row) break;
+        const long long cy = decode_col(ky, D);
         const long long lo = cx < cy ? cx : cy, hi = cx < cy ? cy : cx;
         const long long q = __double2ll_rn(static_cast<double>(vals[y]) * vx * scale);
         atomicAdd(&G[lo + hi * n], static_cast<unsigned long long>(q));
@@ -371,18 +375,16 @@ __global__ void fixed_to_double_kernel(const unsigned long long* __restrict__ Gi
 // one warp per row of X_(n), fixed-order reduction.
 template <typename T, typename K, int KC>
 __global__ void sparse_times_kernel(const K* __restrict__ keys, const T* __restrict__ vals,
-                                    const long long* __restrict__ rs, const long long* __restrict__ re, int rows, int ba,
-                                    int bb, long long ca, long long cb, const double* __restrict__ V, long long vld,
-                                    int kc, double* __restrict__ W) {
+                                    const long long* __restrict__ rs, const long long* __restrict__ re, int rows,
+                                    ColDecode D, const double* __restrict__ V, long long vld, int kc,
+                                    double* __restrict__ W) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= rows) return;
     double acc[KC];
 #pragma unroll
     for (int c = 0; c < KC; ++c) acc[c] = 0.0;
     for (long long e = rs[warp] + lane; e < re[warp]; e += 32) {
-        const unsigned long long k = static_cast<unsigned long long>(keys[e]);
-        const long long col = static_cast<long long>(k & ((1ull << ba) - 1ull)) * ca +
-                              static_cast<long long>((k >> ba) & ((1ull << bb) - 1ull)) * cb;
+        const long long col = decode_col(static_cast<unsigned long long>(keys[e]), D);
         const double v = static_cast<double>(vals[e]);
 #pragma unroll
         for (int c = 0; c < KC; ++c)
@@ -490,19 +492,23 @@ bool sparse_fast_path_ok(const std::vector<int>& dims, const std::vector<int>& r
 }
 
 // Choose the innermost contracted mode for mode n by a FMA cost model:
-// nnz * RA(r_a) for the fibre sums + expected fibres * r_a * r_b for stage 2.
-static int choose_inner(const mach_sparse* X, int n, const std::vector<int>& ranks) {
+// nnz * RA(r_a) for the fibre sums + expected fibres * r_a * r_b for stage 2
+// (order 4: r_b = the larger rank of the two composite modes; the outer one
+// is contracted once per (row, i_b2) group, see stage2_4way_kernel).
+static int choose_inner(const mach_sparse* X, int n, const std::vector<int>& ranks, int avoid) {
     const int d = static_cast<int>(X->dims.size());
     if (d == 2) return 1 - n;
     int best = -1;
     double best_cost = 0;
     const double dens = X->numel ? static_cast<double>(X->nnz) / static_cast<double>(X->numel) : 0.0;
     for (int a = 0; a < d; ++a) {
-        if (a == n) continue;
-        int b = 3 - n - a;
+        if (a == n || a == avoid) continue;
+        int rb = 1;
+        for (int m = 0; m < d; ++m)
+            if (m != n && m != a) rb = std::max(rb, ranks[m]);
         const double Ia = X->dims[a];
         const double fibres = (static_cast<double>(X->numel) / Ia) * (1.0 - std::pow(1.0 - dens, Ia));
-        const double cost = static_cast<double>(X->nnz) * ra_bucket(ranks[a]) + fibres * ranks[a] * ranks[b];
+        const double cost = static_cast<double>(X->nnz) * ra_bucket(ranks[a]) + fibres * ranks[a] * rb;
         if (best < 0 || cost < best_cost - 1e-9) { best = a; best_cost = cost; }
     }
     return best;
@@ -604,26 +610,41 @@ std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>
     Ctx* ctx = X->ctx;
     if (X->plans.size() != X->dims.size()) X->plans.assign(X->dims.size(), nullptr);
     const int d = static_cast<int>(X->dims.size());
-    const int a = (force_a >= 0 && force_a < d && force_a != n) ? force_a : choose_inner(X, n, ranks);
-    const int b = (d == 3) ? 3 - n - a : -1;
+    // force_a >= 0 fixes the inner mode; force_a <= -2 excludes mode -force_a - 2
+    const int avoid = force_a <= -2 ? -force_a - 2 : -1;
+    const int a = (force_a >= 0 && force_a < d && force_a != n) ? force_a : choose_inner(X, n, ranks, avoid);
+    // composite i_b: the remaining modes, inner first.  Order 4: the mode
+    // with the smaller extent is outer (b2: its per-row partial block is
+    // staged in shared memory by stage 2)
+    std::vector<int> rest;
+    for (int m = 0; m < d; ++m)
+        if (m != n && m != a) rest.push_back(m);
+    if (rest.size() == 2 && X->dims[rest[0]] < X->dims[rest[1]]) std::swap(rest[0], rest[1]);
+    const int b = rest.empty() ? -1 : rest[0];
     auto& slot = X->plans[static_cast<std::size_t>(n)];
     if (slot && slot->a == a) return slot;
     auto P = std::make_shared<ModePlan>();
     P->mode = n;
     P->a = a;
     P->b = b;
+    P->bmodes = rest;
     P->ba = bits_for(X->dims[a]);
-    P->bb = (b >= 0) ? bits_for(X->dims[b]) : 0;
+    P->bb = 0;
+    for (int m : rest) P->bb += bits_for(X->dims[m]);
     const int bn = bits_for(X->dims[n]);
     const int total = P->ba + P->bb + bn;
     P->key64 = total > 32;
     KeyFields kf{};
     kf.nf = 0;
     kf.mode[kf.nf] = a; kf.shift[kf.nf++] = 0;
-    if (b >= 0) { kf.mode[kf.nf] = b; kf.shift[kf.nf++] = P->ba; }
+    int sh = P->ba;
+    for (int m : rest) { kf.mode[kf.nf] = m; kf.shift[kf.nf++] = sh; sh += bits_for(X->dims[m]); }
     kf.mode[kf.nf] = n; kf.shift[kf.nf++] = P->ba + P->bb;
-    // the sampler's flat order already is (i_2, i_1, i_0) lexicographic
-    const bool natural = (d == 3 && n == 2 && a == 0) || (d == 2 && n == 1 && a == 0);
+    P->nf = kf.nf;
+    for (int j = 0; j < kf.nf; ++j) { P->fmode[j] = kf.mode[j]; P->fshift[j] = kf.shift[j]; }
+    // the sampler's flat order already is (i_{d-1}, ..., i_0) lexicographic
+    bool natural = true;
+    for (int j = 0; j < kf.nf; ++j) natural = natural && kf.mode[j] == j;
     static const bool tdbg = std::getenv("MACH_DEBUG_SETUP") != nullptr;
     auto tnow = [&]() {
         if (!tdbg) return 0.0;
@@ -1116,23 +1137,36 @@ void sparse_row_gram(Ctx* ctx, const mach_sparse* X, int n, double normX2, doubl
               static_cast<long long>(I), 1.0 / scale, G);
 }
 
-// column strides of X_(n): remaining modes in original order, earliest fastest
-static void xn_col_strides(const std::vector<int>& dims, int n, int a, int b, long long& ca, long long& cb) {
-    const int d = static_cast<int>(dims.size());
+// X_(n) column stride of every mode (remaining modes in original order,
+// earliest fastest; tensor.hpp:119-121)
+static std::vector<long long> xn_col_strides(const std::vector<int>& dims, int n) {
+    std::vector<long long> st(dims.size(), 0);
     long long s = 1;
-    ca = cb = 0;
-    for (int m = 0; m < d; ++m) {
-        if (m == n) continue;
-        if (m == a) ca = s;
-        if (m == b) cb = s;
+    for (std::size_t m = 0; m < dims.size(); ++m) {
+        if (static_cast<int>(m) == n) continue;
+        st[m] = s;
         s *= dims[m];
     }
+    return st;
+}
+
+ColDecode plan_col_decode(const std::vector<int>& dims, const ModePlan& P) {
+    const auto st = xn_col_strides(dims, P.mode);
+    ColDecode D;
+    for (int j = 0; j < P.nf; ++j) {
+        const int m = P.fmode[j];
+        if (m == P.mode) continue;
+        D.shift[D.nf] = P.fshift[j];
+        D.mask[D.nf] = (1ull << bits_for(dims[m])) - 1ull;
+        D.stride[D.nf] = st[m];
+        ++D.nf;
+    }
+    return D;
 }
 
 template <typename T>
 void sparse_col_gram(Ctx* ctx, const mach_sparse* X, const ModePlan& P, long long cols, double normX2, double* G) {
-    long long ca, cb;
-    xn_col_strides(X->dims, P.mode, P.a, P.b, ca, cb);
+    const ColDecode D = plan_col_decode(X->dims, P);
     DBuf<unsigned long long> Gi(ctx, static_cast<std::size_t>(cols * cols));
     Gi.zero(ctx);
     const double scale = (normX2 > 0) ? std::ldexp(1.0, static_cast<int>(std::floor(61.0 - std::log2(normX2)))) : 1.0;
@@ -1140,27 +1174,85 @@ void sparse_col_gram(Ctx* ctx, const mach_sparse* X, const ModePlan& P, long lon
     if (nnz > 0) {
         if (P.key64) MB_LAUNCH(ctx, (col_gram_kernel<T, unsigned long long>), ceil_div(nnz, 256), 256, 0,
                                reinterpret_cast<const unsigned long long*>(P.keys.get()), reinterpret_cast<const T*>(P.vals.get()),
-                               nnz, P.ba, P.bb, ca, cb, scale, cols, Gi.get());
+                               nnz, P.ba + P.bb, D, scale, cols, Gi.get());
         else MB_LAUNCH(ctx, (col_gram_kernel<T, unsigned int>), ceil_div(nnz, 256), 256, 0,
                        reinterpret_cast<const unsigned int*>(P.keys.get()), reinterpret_cast<const T*>(P.vals.get()), nnz,
-                       P.ba, P.bb, ca, cb, scale, cols, Gi.get());
+                       P.ba + P.bb, D, scale, cols, Gi.get());
     }
     MB_LAUNCH(ctx, fixed_to_double_kernel, ceil_div(cols * cols, 256), 256, 0, Gi.get(), cols, 1.0 / scale, G);
 }
 
 template <typename T>
 void sparse_times(Ctx* ctx, const mach_sparse* X, const ModePlan& P, const double* V, long long vld, int kc, double* W) {
-    long long ca, cb;
-    xn_col_strides(X->dims, P.mode, P.a, P.b, ca, cb);
+    const ColDecode D = plan_col_decode(X->dims, P);
     const int rows = P.rows;
 #define MB_ST(KT)                                                                                                  \
     MB_LAUNCH(ctx, (sparse_times_kernel<T, KT, 32>), ceil_div(static_cast<long long>(rows) * 32, 256), 256, 0,       \
               reinterpret_cast<const KT*>(P.keys.get()), reinterpret_cast<const T*>(P.vals.get()), P.row_start.get(), \
-              P.row_end.get(), rows, P.ba, P.bb, ca, cb, V, vld, kc, W)
+              P.row_end.get(), rows, D, V, vld, kc, W)
     if (P.key64) MB_ST(unsigned long long);
     else MB_ST(unsigned int);
 #undef MB_ST
 }
+
+// ---- column-grouped layout of X_(n) (tall-mode basis) ----------------------
+namespace {
+template <typename K>
+__global__ void run_flag_kernel(const K* __restrict__ keys, long long nnz, int sh, unsigned char* __restrict__ flag) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= nnz) return;
+    flag[i] = (i == 0 || (static_cast<unsigned long long>(keys[i]) >> sh) != (static_cast<unsigned long long>(keys[i - 1]) >> sh))
+                  ? 1 : 0;
+}
+}  // namespace
+
+template <typename T>
+void build_col_layout(Ctx* ctx, const mach_sparse* X, int n, ColLayout& L) {
+    const int d = static_cast<int>(X->dims.size());
+    const auto st = xn_col_strides(X->dims, n);
+    KeyFields kf{};
+    L.bn = bits_for(X->dims[n]);
+    kf.mode[kf.nf] = n; kf.shift[kf.nf++] = 0;
+    int sh = L.bn;
+    L.dec = ColDecode{};
+    for (int m = 0; m < d; ++m) {
+        if (m == n) continue;
+        kf.mode[kf.nf] = m; kf.shift[kf.nf++] = sh;
+        L.dec.shift[L.dec.nf] = sh;
+        L.dec.mask[L.dec.nf] = (1ull << bits_for(X->dims[m])) - 1ull;
+        L.dec.stride[L.dec.nf] = st[static_cast<std::size_t>(m)];
+        ++L.dec.nf;
+        sh += bits_for(X->dims[m]);
+    }
+    L.key64 = sh > 32;
+    build_sorted<T>(ctx, X, kf, sh, L.key64, L.keys, L.vals, !(n == 0));
+    const long long nnz = X->nnz;
+    L.runs.alloc(ctx, nnz + 1);
+    if (nnz == 0) {
+        L.nruns = 0;
+        const long long z = 0;
+        to_device(ctx, L.runs.get(), &z, 1);
+        return;
+    }
+    DBuf<unsigned char> flag(ctx, nnz);
+    if (L.key64) MB_LAUNCH(ctx, run_flag_kernel<unsigned long long>, ceil_div(nnz, 256), 256, 0,
+                           reinterpret_cast<const unsigned long long*>(L.keys.get()), nnz, L.bn, flag.get());
+    else MB_LAUNCH(ctx, run_flag_kernel<unsigned int>, ceil_div(nnz, 256), 256, 0,
+                   reinterpret_cast<const unsigned int*>(L.keys.get()), nnz, L.bn, flag.get());
+    DBuf<long long> nf_d(ctx, 1);
+    thrust::counting_iterator<long long> cnt_it(0);
+    std::size_t tmp = 0;
+    MB_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, cnt_it, flag.get(), L.runs.get(), nf_d.get(), nnz, ctx->stream));
+    DBuf<unsigned char> t(ctx, tmp);
+    MB_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, cnt_it, flag.get(), L.runs.get(), nf_d.get(), nnz, ctx->stream));
+    ctx->launches += 1;
+    to_host(ctx, &L.nruns, nf_d.get(), 1);
+    sync(ctx);
+    to_device(ctx, L.runs.get() + L.nruns, &nnz, 1);
+    sync(ctx);  // the host value above is a stack temporary
+}
+template void build_col_layout<float>(Ctx*, const mach_sparse*, int, ColLayout&);
+template void build_col_layout<double>(Ctx*, const mach_sparse*, int, ColLayout&);
 
 template std::shared_ptr<ModePlan> get_plan<float>(mach_sparse*, int, const std::vector<int>&, int);
 template std::shared_ptr<ModePlan> get_plan<double>(mach_sparse*, int, const std::vector<int>&, int);

@@ -68,7 +68,36 @@ struct ModePlan {
     DBuf<int> seg_row;             // i_n (this mode's row) of the segment at each position
     long long n_seg = -1;          // segments (valid positions), known once grouped
     DBuf<int> seg_ib;              // i_b of every segment slot t * 32 + lane, task order (0 past nseg)
+    // packed-key fields (least significant first): mode and bit offset
+    int nf = 0;
+    int fmode[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int fshift[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    std::vector<int> bmodes;       // modes folded into the composite i_b (outer first is last)
 };
+
+// X_(n) column of a packed key: sum over the fields of ((key >> shift) &
+// mask) * stride (the column order of matricize, tensor.hpp:119-121).
+struct ColDecode {
+    int nf = 0;
+    int shift[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long mask[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long stride[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+};
+ColDecode plan_col_decode(const std::vector<int>& dims, const ModePlan& P);
+
+// Nonzeros of X_(n) grouped by column (mode n in the low key bits, the other
+// modes above it in increasing order), with the start of every nonempty
+// column run; built on demand for the tall-mode basis.
+struct ColLayout {
+    bool key64 = false;
+    int bn = 0;
+    long long nruns = 0;
+    DBuf<unsigned char> keys, vals;
+    DBuf<long long> runs;  // nruns + 1 (sentinel nnz)
+    ColDecode dec;
+};
+template <typename T>
+void build_col_layout(Ctx* ctx, const mach_sparse* X, int n, ColLayout& L);
 // group P's segments by i_b (once); false when P has no b mode
 bool build_segment_groups(Ctx* ctx, ModePlan& P, int b_rows);
 
@@ -105,6 +134,16 @@ template <typename T>
 void sparse_col_gram(Ctx* ctx, const mach_sparse* X, const ModePlan& P, long long cols, double normX2, double* G);
 template <typename T>
 void sparse_times(Ctx* ctx, const mach_sparse* X, const ModePlan& P, const double* V, long long vld, int kc, double* W);
+// Leading-k left singular basis of X_(n) when the column side is too wide for
+// a Gram (tall time modes): implicit subspace iteration on
+// X_(n) X_(n)^T (tall_basis.cu).  U (I_n x k), sv (k), st (3) as basis_from_side.
+template <typename T>
+void sparse_tall_basis(Ctx* ctx, const mach_sparse* X, const ModePlan& P, int k, double* U, double* sv, int* st);
+// Same for a dense column-major Y (rows x cols) whose column side is too wide.
+template <typename T>
+void dense_tall_basis(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U, double* sv, int* st);
+// columns of X_(n) above which the tall-mode basis replaces the column Gram
+long long tall_min_cols();
 
 // ---- eigen step (eig.cu, linalg.cu) ----
 void eig_topk(Ctx* ctx, const double* G, int n, int k, double* work, double* V, double* sig, int* status,

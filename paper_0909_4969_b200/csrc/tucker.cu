@@ -133,9 +133,15 @@ void lsb_device(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U
     if (rows < 1 || cols < 1) throw_arg("matrix must be nonempty");
     if (k < 1 || k > rows) throw_arg("k must satisfy 1 <= k <= rows");
     const bool row_side = rows <= cols && k <= cols;
+    if (!row_side && cols > tall_min_cols() && k <= 24) {
+        // column side too wide for a Gram: implicit subspace iteration (tall_basis.cu)
+        dense_tall_basis<T>(ctx, Y, rows, cols, k, U, sv, st);
+        if (warm) warm->cols = 0;
+        return;
+    }
+    if (!row_side && cols > 16384)
+        throw Error(MACH_ERR_INTERNAL, "column-side eigen step wider than 16384 with rank above 24 is not supported");
     const int side = row_side ? rows : static_cast<int>(std::min<long long>(cols, 1 << 30));
-    if (!row_side && cols > 4096)
-        throw Error(MACH_ERR_INTERNAL, "column-side eigen step wider than 4096 is not supported on device yet");
     const int kk = row_side ? k : static_cast<int>(std::min<long long>(k, cols));
     DBuf<double> G(ctx, static_cast<std::size_t>(side) * side);
     DBuf<double> V(ctx, static_cast<std::size_t>(side) * kk);
@@ -703,7 +709,7 @@ struct SparseSession : SessionBase {
         // all modes' Grams first, then their eigenproblems in one launch (one
         // CTA each: independent, latency-bound), then the bases
         struct ModeWork {
-            bool row;
+            bool row = false, tall = false;
             int n, kc;
             DBuf<double> G, V, sig;
             DBuf<int> est;
@@ -716,8 +722,10 @@ struct SparseSession : SessionBase {
             const long long cols = numel / rows;
             const int k = ranks[static_cast<std::size_t>(m)];
             w.row = rows <= cols;
-            if (!w.row && cols > 4096)
-                throw Error(MACH_ERR_INTERNAL, "column-side sparse HOSVD wider than 4096 is not supported on device yet");
+            w.tall = !w.row && cols > tall_min_cols() && k <= 24;
+            if (!w.row && !w.tall && cols > 16384)
+                throw Error(MACH_ERR_INTERNAL, "column-side sparse HOSVD wider than 16384 with rank above 24 is not supported");
+            if (w.tall) continue;  // implicit subspace iteration below, no Gram
             w.n = w.row ? rows : static_cast<int>(cols);
             w.kc = w.row ? k : static_cast<int>(std::min<long long>(k, cols));
             if (w.row && m < static_cast<int>(preG.size()) && preG[static_cast<std::size_t>(m)].get()) {
@@ -735,12 +743,15 @@ struct SparseSession : SessionBase {
                                   nullptr, nullptr});
         }
         if (grams_done) MB_CUDA(cudaStreamWaitEvent(ctx->stream, grams_done, 0));  // join the side stream's Grams
-        eig_select_batched(ctx, jobs);
+        if (!jobs.empty()) eig_select_batched(ctx, jobs);
         for (int m = 0; m < d; ++m) {
             ModeWork& w = mw[static_cast<std::size_t>(m)];
             const int rows = dims[static_cast<std::size_t>(m)];
             const int k = ranks[static_cast<std::size_t>(m)];
-            if (w.row) {
+            if (w.tall) {
+                sparse_tall_basis<T>(ctx, X, *plans[static_cast<std::size_t>(m)], k, fs.U[static_cast<std::size_t>(m)].get(),
+                                     sv_at(m), fs.st.get() + 3 * m);
+            } else if (w.row) {
                 basis_from_side(ctx, w.V.get(), w.sig.get(), rows, k, w.est.get(), fs.U[static_cast<std::size_t>(m)].get(),
                                 sv_at(m), fs.st.get() + 3 * m);
             } else {

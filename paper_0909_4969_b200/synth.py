@@ -12,6 +12,10 @@ from __future__ import annotations
 import numpy as np
 
 # name -> (dims, ranks, noise_rel, p, sweeps, dtype)
+# C4 uses the tensor-stream generator: host factor diag(l) Q with
+# l ~ lognormal(0, 1) (heavy-tailed host loads, not orthonormal), time factor
+# = orthonormalised sin/cos harmonics of a 288-tick daily period.
+KIND = {"c4": "stream"}
 CONFIGS = {
     "c1": ((100, 12, 1024), (5, 5, 5), 0.01, 0.1, 3, "float64"),
     "c2": ((512, 512, 512), (10, 10, 10), 0.01, 0.05, 5, "float32"),
@@ -21,12 +25,45 @@ CONFIGS = {
 }
 
 
-def lowrank_numpy(dims, ranks, noise_rel=0.01, seed=0, dtype=np.float64) -> np.ndarray:
+PERIOD = 288  # 5-minute buckets per day
+
+
+def harmonics(n, r, period=PERIOD) -> np.ndarray:
+    """n x r orthonormalised sin/cos harmonics of the daily period (time factor)."""
+    t = np.arange(n, dtype=np.float64)[:, None]
+    cols = []
+    h = 1
+    while len(cols) < r:
+        w = 2.0 * np.pi * h * t / period
+        cols += [np.sin(w), np.cos(w)]
+        h += 1
+    q, _ = np.linalg.qr(np.hstack(cols[:r]))
+    return q
+
+
+def stream_factors(dims, ranks, rng):
+    """Factors of the tensor-stream generator (hosts x metrics x time)."""
+    facs = []
+    for m, (n, r) in enumerate(zip(dims, ranks)):
+        if m == len(dims) - 1:
+            facs.append(harmonics(n, r))
+            continue
+        q, _ = np.linalg.qr(rng.standard_normal((n, r)))
+        if m == 0:
+            q = np.exp(rng.standard_normal(n))[:, None] * q  # lognormal(0, 1) host loads
+        facs.append(q)
+    return facs
+
+
+def lowrank_numpy(dims, ranks, noise_rel=0.01, seed=0, dtype=np.float64, kind=None) -> np.ndarray:
     rng = np.random.default_rng(seed)
     core = rng.standard_normal(ranks)
     x = core
-    for m, (n, r) in enumerate(zip(dims, ranks)):
-        q, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    if kind == "stream":
+        facs = stream_factors(dims, ranks, rng)
+    else:
+        facs = [np.linalg.qr(rng.standard_normal((n, r)))[0] for n, r in zip(dims, ranks)]
+    for m, q in enumerate(facs):
         x = np.moveaxis(np.tensordot(q, x, axes=([1], [m])), 0, m)
     if noise_rel > 0:
         sigma = noise_rel * np.sqrt((x * x).sum()) / np.sqrt(x.size)
@@ -34,7 +71,7 @@ def lowrank_numpy(dims, ranks, noise_rel=0.01, seed=0, dtype=np.float64) -> np.n
     return np.asarray(x, dtype=dtype)
 
 
-def lowrank_torch(dims, ranks, noise_rel=0.01, seed=0, dtype="float32", device="cuda"):
+def lowrank_torch(dims, ranks, noise_rel=0.01, seed=0, dtype="float32", device="cuda", kind=None):
     """Flat first-mode-fastest CUDA tensor of the config (generated on device)."""
     import torch
 
@@ -43,9 +80,14 @@ def lowrank_torch(dims, ranks, noise_rel=0.01, seed=0, dtype="float32", device="
     d = len(dims)
     core = torch.randn(*ranks, generator=g, device=device, dtype=torch.float64)
     facs = []
-    for n, r in zip(dims, ranks):
+    for m, (n, r) in enumerate(zip(dims, ranks)):
+        if kind == "stream" and m == d - 1:
+            facs.append(torch.as_tensor(harmonics(n, r), device=device))
+            continue
         a = torch.randn(n, r, generator=g, device=device, dtype=torch.float64)
         q, _ = torch.linalg.qr(a)
+        if kind == "stream" and m == 0:
+            q = torch.exp(torch.randn(n, generator=g, device=device, dtype=torch.float64))[:, None] * q
         facs.append(q)
     # X0 in C order with reversed axes == first-mode-fastest flat buffer
     letters = "abcdefgh"[:d]
