@@ -436,6 +436,92 @@ __global__ void __launch_bounds__(kB) basis_products_fast_kernel(const double* _
     }
 }
 
+// Tall version of the fast path (n * k too large for one CTA's shared memory,
+// e.g. C4's 65536-row time mode): the k x k Grams on the fp64 tensor cores
+// over many CTAs, the small factorisations and tests in one CTA, the row
+// updates and the sign vote spread over the grid.  Every kernel after the
+// first test is gated on the flag, and the one-CTA Gram-Schmidt kernel runs
+// only when a test fails, so the whole chain can sit in a captured graph.
+__global__ void __launch_bounds__(kB) tall_chol_kernel(const double* __restrict__ G, int k, const double* __restrict__ sig,
+                                                       int first, double* __restrict__ Ri, int* __restrict__ slow) {
+    __shared__ double C[kFastK * kFastK], R[kFastK * kFastK], diag[kFastK];
+    __shared__ int ok;
+    if (!first && slow[0]) return;
+    for (int e = threadIdx.x; e < k * k; e += kB) C[(e % k) + (e / k) * kFastK] = G[e];
+    __syncthreads();
+    if (first) {  // rank floor on every column before factorising (linalg.cpp:66-100)
+        const double floor = sig[0] * kRankFloor;
+        bool pass = true;
+        for (int i = 0; i < k; ++i) pass = pass && sqrt(C[i + i * kFastK]) > floor;
+        if (!pass) {
+            if (threadIdx.x == 0) slow[0] = 1;
+            return;
+        }
+    }
+    double nv[kFastK];
+    for (int i = 0; i < k; ++i) nv[i] = sqrt(C[i + i * kFastK]);
+    if (!small_chol_inv(C, R, k, diag, &ok)) {
+        if (threadIdx.x == 0) slow[0] = 1;
+        return;
+    }
+    if (first)
+        for (int i = 0; i < k; ++i)
+            if (!(diag[i] > kCollapseFloor * nv[i])) {  // kCollapseFloor (linalg.cpp:37)
+                if (threadIdx.x == 0) slow[0] = 1;
+                return;
+            }
+    for (int e = threadIdx.x; e < kFastK * kFastK; e += kB) Ri[e] = R[e];
+    if (first && threadIdx.x == 0) slow[0] = 0;
+}
+
+// Y (n x k) = X Ri (column-major; Ri upper triangular, ld kFastK), gated
+__global__ void tall_apply_kernel(const double* __restrict__ X, int n, int k, const double* __restrict__ Ri,
+                                  double* __restrict__ Y, const int* __restrict__ slow) {
+    if (slow[0]) return;
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= static_cast<long long>(n) * k) return;
+    const int r = static_cast<int>(e % n), c = static_cast<int>(e / n);
+    double s = 0.0;
+    for (int p = 0; p <= c; ++p) s = fma(X[r + static_cast<std::size_t>(p) * n], Ri[p + c * kFastK], s);
+    Y[e] = s;
+}
+
+// one CTA per column: canonical sign (largest |u|, lowest row on ties;
+// linalg.cpp:18-32), U written; sv / st from CTA 0; gated
+__global__ void __launch_bounds__(kB) tall_sign_kernel(const double* __restrict__ X, int n, int k,
+                                                       const double* __restrict__ sig, double* __restrict__ U,
+                                                       double* __restrict__ sv, int* __restrict__ st,
+                                                       const int* __restrict__ slow) {
+    if (slow[0]) return;
+    __shared__ double redv[32];
+    __shared__ int redi[32];
+    const int c = blockIdx.x;
+    const double* x = X + static_cast<std::size_t>(c) * n;
+    const int p = cta_argmax_abs(x, n, redv, redi);
+    const double sgn = x[p] < 0.0 ? -1.0 : 1.0;
+    for (int r = threadIdx.x; r < n; r += kB) U[r + static_cast<std::size_t>(c) * n] = sgn * x[r];
+    if (threadIdx.x == 0) sv[c] = sig[c];
+    if (c == 0 && threadIdx.x == 0) { st[0] = k; st[1] = 0; st[2] = 0; }
+}
+
+void basis_products_tall(Ctx* ctx, const double* W, int n, int wc, int k, const double* sig, const int* eig_status,
+                         double* U, double* sv, int* st) {
+    DBuf<double> G(ctx, static_cast<std::size_t>(k) * k), Ri(ctx, kFastK * kFastK), X(ctx, static_cast<std::size_t>(n) * k),
+        Y(ctx, static_cast<std::size_t>(n) * k);
+    DBuf<int> slow(ctx, 1);
+    const long long nk = static_cast<long long>(n) * k;
+    gram<double>(ctx, W, 1, n, n, k, G.get());
+    MB_LAUNCH(ctx, tall_chol_kernel, 1, kB, 0, G.get(), k, sig, 1, Ri.get(), slow.get());
+    MB_LAUNCH(ctx, tall_apply_kernel, ceil_div(nk, 256), 256, 0, W, n, k, Ri.get(), X.get(), slow.get());
+    gram<double>(ctx, X.get(), 1, n, n, k, G.get());
+    MB_LAUNCH(ctx, tall_chol_kernel, 1, kB, 0, G.get(), k, sig, 0, Ri.get(), slow.get());
+    MB_LAUNCH(ctx, tall_apply_kernel, ceil_div(nk, 256), 256, 0, X.get(), n, k, Ri.get(), Y.get(), slow.get());
+    MB_LAUNCH(ctx, tall_sign_kernel, k, kB, 0, Y.get(), n, k, sig, U, sv, st, slow.get());
+    BasisScratch bs(ctx, n, k);
+    MB_LAUNCH_PDL(ctx, basis_from_products_kernel, 1, kB, bs.smem, W, n, wc, k, sig, eig_status, U, sv, st,
+                  static_cast<const int*>(slow.get()), bs.g.get());
+}
+
 void basis_from_products_gated(Ctx* ctx, const double* W, int n, int wc, int k, const double* sig,
                                const int* eig_status, double* U, double* sv, int* st, const int* need) {
     BasisScratch bs(ctx, n, k);
@@ -456,6 +542,10 @@ void basis_from_products(Ctx* ctx, const double* W, int n, int wc, int k, const 
         MB_LAUNCH(ctx, basis_products_fast_kernel, 1, kB, fsm, W, n, k, sig, U, sv, st, slow.get());
         MB_LAUNCH_PDL(ctx, basis_from_products_kernel, 1, kB, basis_smem(n, k), W, n, wc, k, sig, eig_status, U, sv, st,
                   static_cast<const int*>(slow.get()), static_cast<double*>(nullptr));
+        return;
+    }
+    if (wc >= k && k <= kFastK && n <= (1 << 20)) {
+        basis_products_tall(ctx, W, n, wc, k, sig, eig_status, U, sv, st);
         return;
     }
     BasisScratch bs(ctx, n, k);
