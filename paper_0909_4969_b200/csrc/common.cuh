@@ -146,6 +146,13 @@ __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (!pdl_trigger_first()) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// Wait first, then trigger: the dependent grid launches only after this
+// grid's predecessor has completed.  Used by the kernels that bound a
+// consumer of data a later, non-waiting (overlapped) launch overwrites.
+__device__ __forceinline__ void pdl_enter_strict() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 inline bool pdl_on() {
     static const bool off = std::getenv("MACH_NO_PDL") != nullptr;
     return !off;

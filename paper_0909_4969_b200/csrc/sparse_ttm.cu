@@ -23,6 +23,7 @@
 //   output   one partial row (C = r_a * r_b values) per sub-tile; a second tiny
 //            kernel sums a row's partials in sub-tile order and writes Y_(n)
 //            (I_n x C, column-major) directly in matricised layout.
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -36,6 +37,8 @@
 
 #include "common.cuh"
 #include "sparse_ttm.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace machb {
 
@@ -201,7 +204,7 @@ __global__ void jds_kernel(const K* __restrict__ keys, const T* __restrict__ val
                            const long long* __restrict__ first, const long long* __restrict__ pstart,
                            const int* __restrict__ plen, const int* __restrict__ pib, unsigned long long maska,
                            TtmTask* __restrict__ tasks, IA* __restrict__ ia_out, T* __restrict__ v_out,
-                           int2* __restrict__ desc) {
+                           int2* __restrict__ desc, int* __restrict__ pslot) {
     const long long t = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (t >= n_task) return;
@@ -219,6 +222,7 @@ __global__ void jds_kernel(const K* __restrict__ keys, const T* __restrict__ val
         const int lo = __shfl_sync(0xffffffffu, len0, o);
         rank += (lo > len0) || (lo == len0 && o < lane);
     }
+    if (pslot && lane < tk.nseg) pslot[p0 + lane] = static_cast<int>(t * 32 + rank);  // piece (key order) -> slot
     const long long base = __shfl_sync(0xffffffffu, st0, 0);
     // lane l takes the segment of rank l
     long long st = 0;
@@ -482,13 +486,28 @@ int ttm_stride(int r, int elem_bytes) {
 
 bool sparse_fast_path_ok(const std::vector<int>& dims, const std::vector<int>& ranks) {
     const int d = static_cast<int>(dims.size());
-    if (d < 2 || d > 3) return false;
+    if (d < 2 || d > 4) return false;
     int bits = 0;
     for (int m = 0; m < d; ++m) {
         if (ranks[m] > 32) return false;
         bits += bits_for(dims[m]);
     }
-    return bits <= 64;
+    if (bits > 64) return false;
+    if (d == 4) {
+        // every mode's stage 2 (any choice of inner mode) must fit: the
+        // composite i_b in an int and the per-row Z block in shared memory
+        for (int n = 0; n < 4; ++n)
+            for (int a = 0; a < 4; ++a) {
+                if (a == n) continue;
+                int r[2], k = 0;
+                for (int m = 0; m < 4; ++m)
+                    if (m != n && m != a) r[k++] = m;
+                if (bits_for(dims[r[0]]) + bits_for(dims[r[1]]) > 30) return false;
+                const int b1 = dims[r[0]] >= dims[r[1]] ? r[0] : r[1], b2 = b1 == r[0] ? r[1] : r[0];
+                if (!stage2_4way_ok(dims, ranks, n, a, b1, b2)) return false;
+            }
+    }
+    return true;
 }
 
 // Choose the innermost contracted mode for mode n by a FMA cost model:
@@ -563,6 +582,7 @@ void build_ttm_layout_k(Ctx* ctx, long long nnz, ModePlan& P) {
     sync(ctx);
     DBuf<long long> pstart(ctx, NP);
     DBuf<int> plen(ctx, NP), prow(ctx, NP), pib(ctx, NP);
+    // (order 4 keeps pib: moved into the plan below, after the layout is built)
     MB_LAUNCH(ctx, piece_fill_kernel<K>, ceil_div(F, 256), 256, 0, keys, fs.get(), F, nnz, pbase.get(), P.ba, P.bb,
               pstart.get(), plen.get(), prow.get(), pib.get());
     // tasks: 32 consecutive segments of one row
@@ -570,6 +590,14 @@ void build_ttm_layout_k(Ctx* ctx, long long nnz, ModePlan& P) {
     prs.zero(ctx);
     pre.zero(ctx);
     MB_LAUNCH(ctx, piece_row_bounds_kernel, ceil_div(NP, 256), 256, 0, prow.get(), NP, prs.get(), pre.get());
+    if (P.keep_pieces) {  // order 4: the key-ordered piece list drives stage 2 (stage2_4way_kernel)
+        P.n_piece = NP;
+        P.pslot.alloc(ctx, std::max<long long>(1, NP));
+        P.piece_rs.alloc(ctx, rows);
+        P.piece_re.alloc(ctx, rows);
+        MB_CUDA(cudaMemcpyAsync(P.piece_rs.get(), prs.get(), rows * sizeof(long long), cudaMemcpyDeviceToDevice, ctx->stream));
+        MB_CUDA(cudaMemcpyAsync(P.piece_re.get(), pre.get(), rows * sizeof(long long), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
     DBuf<int> tc(ctx, rows + 1);
     MB_LAUNCH(ctx, task_counts_kernel, ceil_div(rows + 1, 256), 256, 0, prs.get(), pre.get(), rows, tc.get());
     {
@@ -592,11 +620,14 @@ void build_ttm_layout_k(Ctx* ctx, long long nnz, ModePlan& P) {
     if (P.ia16)
         MB_LAUNCH(ctx, (jds_kernel<K, unsigned short, T>), ceil_div(static_cast<long long>(nt) * 32, 256), 256, 0, keys, vals,
                   static_cast<long long>(nt), first.get(), pstart.get(), plen.get(), pib.get(), maska, P.tasks.get(),
-                  reinterpret_cast<unsigned short*>(P.ia.get()), reinterpret_cast<T*>(P.jv.get()), P.desc.get());
+                  reinterpret_cast<unsigned short*>(P.ia.get()), reinterpret_cast<T*>(P.jv.get()), P.desc.get(),
+                  P.pslot.get());
     else
         MB_LAUNCH(ctx, (jds_kernel<K, unsigned int, T>), ceil_div(static_cast<long long>(nt) * 32, 256), 256, 0, keys, vals,
                   static_cast<long long>(nt), first.get(), pstart.get(), plen.get(), pib.get(), maska, P.tasks.get(),
-                  reinterpret_cast<unsigned int*>(P.ia.get()), reinterpret_cast<T*>(P.jv.get()), P.desc.get());
+                  reinterpret_cast<unsigned int*>(P.ia.get()), reinterpret_cast<T*>(P.jv.get()), P.desc.get(),
+                  P.pslot.get());
+    if (P.keep_pieces) P.pib = std::move(pib);
 }
 
 template <typename T>
@@ -642,6 +673,7 @@ std::shared_ptr<ModePlan> get_plan(mach_sparse* X, int n, const std::vector<int>
     kf.mode[kf.nf] = n; kf.shift[kf.nf++] = P->ba + P->bb;
     P->nf = kf.nf;
     for (int j = 0; j < kf.nf; ++j) { P->fmode[j] = kf.mode[j]; P->fshift[j] = kf.shift[j]; }
+    P->keep_pieces = d == 4;
     // the sampler's flat order already is (i_{d-1}, ..., i_0) lexicographic
     bool natural = true;
     for (int j = 0; j < kf.nf; ++j) natural = natural && kf.mode[j] == j;
@@ -847,7 +879,11 @@ __global__ void __launch_bounds__(512, 3) y_from_segments_kernel(const int* __re
                                                               int ra, const T* __restrict__ Un, int rns, int rn, int sa,
                                                               int sn, int rows, int un_rows, int chunk, int ptr_mul,
                                                               T* __restrict__ Y) {
-    pdl_enter();  // programmatic dependent launch: predecessor complete and visible
+    // wait, then trigger: the overlapped stage 1 launched two kernels later
+    // (which does not wait at entry) then starts only after this grid's
+    // predecessors are complete: it cannot overwrite fibre sums or factor
+    // copies still being read (see SparseSession::sweep_body)
+    pdl_enter_strict();
     extern __shared__ __align__(128) unsigned char ysm[];
     __shared__ __align__(8) std::uint64_t bar;
     const int G = blockDim.x / ra;
@@ -1020,7 +1056,7 @@ __global__ void seg_ib_kernel(const TtmTask* __restrict__ tasks, const int2* __r
 
 template <typename T>
 void sparse_mode_stage1(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks,
-                        const std::vector<const T*>& Ur, T* F, int ctas) {
+                        const std::vector<const T*>& Ur, T* F, int ctas, bool overlapped) {
     const int a = P.a;
     auto fill = [&](auto& A) {
         A.vals = reinterpret_cast<const T*>(P.jv.get());
@@ -1034,7 +1070,7 @@ void sparse_mode_stage1(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, con
         A.ub_elems = 0;
         A.fseg = F;
         A.fpos = nullptr;
-        A.stage1 = 1;
+        A.stage1 = overlapped ? 1 : 2;
     };
     const int rab = ra_bucket(ranks[a]);
     if (P.ia16) {
@@ -1090,10 +1126,321 @@ void sparse_mode_stage2(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, con
     else launch(y_from_segments_kernel<T, 32>);
 }
 
+// ---- order-4 stage 2 ---------------------------------------------------------
+// Mode n of a 4-way tensor: stage 1 (the TTM kernel) leaves one fibre sum
+// F = sum_{i_a} x U_a[i_a, :] per segment slot; the segment's composite i_b
+// packs (i_b2 << bits(b1)) | i_b1.  Per row i_n of Y_(n):
+//   Z[i_b2, (r_a, r_b1)] = sum over the row's segments with that i_b2 of
+//                          F[r_a] * U_b1[i_b1, r_b1]
+//   Y_(n)[i_n, (r_a, r_b1, r_b2)] = sum_{i_b2} Z[i_b2, (r_a, r_b1)] U_b2[i_b2, r_b2]
+// (a dimension tree: the per-segment work is r_a r_b1, the r_b2 contraction
+// runs once per (row, i_b2) on the dense Z).  One CTA per row; Z lives in
+// shared memory; group g of E = r_a r_b1 threads owns the i_b2 range
+// [g Ib2 / G, (g+1) Ib2 / G) and walks only the row's tasks overlapping it
+// (a row's tasks are in key order, so i_b2 is nondecreasing across them; the
+// per-task i_b2 range is precomputed).  Each Z element has one owner thread
+// and the segments are taken in a fixed order: deterministic, no atomics.
+namespace {
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<std::uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Per row the pieces (fibre segments) are kept in key order, i.e. sorted by
+// (i_b2, i_b1), with the slot their fibre sum went to (pslot) and their
+// composite i_b (pib).  The row is cut into R slices of i_b2 (CTAs; pieces
+// found by binary search on pib) and every slice's piece range is split
+// evenly over the CTA's warps.  A warp walks its pieces in batches of 32:
+// lane l gathers piece l's fibre sum row (r_a contiguous values) into its
+// strip of shared memory and the 32 composite i_b stay in a register; then,
+// per piece (warp-uniform control), lane-owned Z elements e = lane + 32 j
+// accumulate F[r_a] U_b1[i_b1, r_b1], and whenever i_b2 changes the Z block
+// is folded into the warp's register partial of the Y row:
+//   y[e, q] += z[e] U_b2[i_b2, q].
+// The warps' partial rows are summed in warp order; with R > 1 the slices go
+// through global memory and the last CTA of the row (ticket) sums them in
+// slice order.  Fixed summation order throughout: deterministic.
+template <typename T, int EPL, int RB2>
+__global__ void __launch_bounds__(512) stage2_4way_kernel(const long long* __restrict__ prs, const long long* __restrict__ pre,
+                                                          const int* __restrict__ pslot, const int* __restrict__ pib,
+                                                          const T* __restrict__ F, int ra, int ras, int rb1, int rb2,
+                                                          const T* __restrict__ Ub1, int rb1s, const T* __restrict__ Ub2,
+                                                          int rb2s, int Ib1, int Ib2, int bits1, int sa, int sb1, int sb2,
+                                                          int rows, int R, T* __restrict__ Ypart,
+                                                          unsigned* __restrict__ ticket, T* __restrict__ Y) {
+    pdl_enter_strict();
+    extern __shared__ __align__(16) unsigned char s4raw[];
+    __shared__ bool last;
+    const int row = blockIdx.x / R, q = blockIdx.x - (blockIdx.x / R) * R;
+    const int E = ra * rb1;
+    const int C = E * rb2;
+    const int W = blockDim.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int ea[EPL], eb[EPL];
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) {
+        const int e = lane + 32 * j;
+        ea[j] = e < E ? e % ra : 0;
+        eb[j] = e < E ? e / ra : 0;
+    }
+    const int mask1 = (1 << bits1) - 1;
+    const int c0 = static_cast<int>((static_cast<long long>(Ib2) * q) / R);
+    const int c1 = static_cast<int>((static_cast<long long>(Ib2) * (q + 1)) / R);
+    T* Us1 = reinterpret_cast<T*>(s4raw);                           // Ib1 x rb1s
+    T* Us2 = Us1 + static_cast<std::size_t>(Ib1) * rb1s;            // Ib2 x rb2s
+    T* Yw = Us2 + static_cast<std::size_t>(Ib2) * rb2s;             // W x C warp partials
+    T* strip = Yw + static_cast<std::size_t>(W) * C + static_cast<std::size_t>(warp) * (2 * 32 * ras + 32 * 4 / sizeof(T));
+    for (int i = tid; i < Ib1 * rb1s; i += blockDim.x) Us1[i] = Ub1[i];
+    for (int i = tid; i < Ib2 * rb2s; i += blockDim.x) Us2[i] = Ub2[i];
+    __syncthreads();
+    T y[EPL][RB2];
+#pragma unroll
+    for (int j = 0; j < EPL; ++j)
+#pragma unroll
+        for (int k = 0; k < RB2; ++k) y[j][k] = T(0);
+    if (row < rows) {
+        // this slice's pieces: pib within the row is ascending
+        const long long r0 = prs[row], r1 = pre[row];
+        long long P0, P1;
+        {
+            long long lo = r0, hi = r1;
+            const int key = c0 << bits1;
+            while (lo < hi) { const long long m = (lo + hi) >> 1; if (pib[m] < key) lo = m + 1; else hi = m; }
+            P0 = lo;
+            hi = r1;
+            const int key1 = c1 << bits1;
+            while (lo < hi) { const long long m = (lo + hi) >> 1; if (pib[m] < key1) lo = m + 1; else hi = m; }
+            P1 = lo;
+        }
+        const long long L = P1 - P0;
+        const long long w0 = P0 + (L * warp) / W, w1 = P0 + (L * (warp + 1)) / W;
+        int cur = -1;
+        T z[EPL];
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) z[j] = T(0);
+        auto fold = [&]() {
+            const T* u2 = Us2 + cur * rb2s;
+#pragma unroll
+            for (int k = 0; k < RB2; ++k) {
+                if (k < rb2) {
+                    const T u = u2[k];
+#pragma unroll
+                    for (int j = 0; j < EPL; ++j) y[j][k] = fma(z[j], u, y[j][k]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < EPL; ++j) z[j] = T(0);
+        };
+        // software pipeline over batches of 32 pieces: batch b + 1's fibre-sum
+        // rows are in flight (cp.async into the other strip) and batch b + 2's
+        // indices in registers while batch b is consumed
+        int* su = reinterpret_cast<int*>(strip + 2 * 32 * ras);  // the batch's U_b1 row offsets
+        const int vec = (sizeof(T) == 4 && (ra & 3) == 0) ? 4 : 1;  // 16-byte copies when rows are whole units
+        auto fetch = [&](long long base, int& ib, int& slot) {
+            ib = -1;
+            slot = 0;
+            if (base < w1 && lane < static_cast<int>(min(32ll, w1 - base))) {
+                ib = pib[base + lane];
+                slot = pslot[base + lane];
+            }
+        };
+        auto issue = [&](long long base, int ib, int slot, int buf) {
+            if (base < w1 && ib >= 0) {
+                const T* fr = F + static_cast<long long>(slot) * ra;
+                T* dst = strip + buf * 32 * ras + lane * ras;
+                if (vec == 4) {
+                    for (int a2 = 0; a2 < ra; a2 += 4)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                         static_cast<std::uint32_t>(__cvta_generic_to_shared(dst + a2))),
+                                     "l"(fr + a2)
+                                     : "memory");
+                } else {
+                    for (int a2 = 0; a2 < ra; ++a2) {
+                        if constexpr (sizeof(T) == 4) cp_async4(dst + a2, fr + a2);
+                        else cp_async8(dst + a2, fr + a2);
+                    }
+                }
+            }
+            cp_async_commit();
+        };
+        int ib_c, sl_c, ib_n, sl_n;
+        fetch(w0, ib_c, sl_c);
+        issue(w0, ib_c, sl_c, 0);
+        fetch(w0 + 32, ib_n, sl_n);
+        for (long long base = w0, buf = 0; base < w1; base += 32, buf ^= 1) {
+            const int nb = static_cast<int>(min(32ll, w1 - base));
+            const int ibv = ib_c;
+            issue(base + 32, ib_n, sl_n, static_cast<int>(buf ^ 1));
+            ib_c = ib_n;
+            fetch(base + 64, ib_n, sl_n);
+            __syncwarp();
+            if (lane < nb) su[lane] = (ibv & mask1) * rb1s;
+            cp_async_wait1();  // this batch's rows have landed
+            // runs of equal i_b2 inside the batch (pib ascending): a fold only between runs
+            const int i2v = ibv >> bits1;
+            const int prev = __shfl_up_sync(0xffffffffu, i2v, 1);
+            unsigned starts = __ballot_sync(0xffffffffu, lane < nb && (lane == 0 || i2v != prev));
+            __syncwarp();
+            const T* sb = strip + buf * 32 * ras;
+            while (starts) {
+                const int s0 = __ffs(starts) - 1;
+                starts &= starts - 1;
+                const int s1 = starts ? __ffs(starts) - 1 : nb;
+                const int i2 = __shfl_sync(0xffffffffu, i2v, s0);
+                if (i2 != cur) {
+                    if (cur >= 0) fold();
+                    cur = i2;
+                }
+                const T* fl = sb + s0 * ras;
+                for (int l = s0; l < s1; ++l, fl += ras) {  // branch-free FMA run
+                    const T* ur = Us1 + su[l];
+#pragma unroll
+                    for (int j = 0; j < EPL; ++j) z[j] = fma(fl[ea[j]], ur[eb[j]], z[j]);
+                }
+            }
+        }
+        (void)sl_c;
+        if (cur >= 0) fold();
+    }
+    // warp partials -> CTA partial, in warp order
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) {
+        const int e = lane + 32 * j;
+        if (e < E)
+#pragma unroll
+            for (int k = 0; k < RB2; ++k)
+                if (k < rb2) Yw[static_cast<std::size_t>(warp) * C + e + k * E] = y[j][k];
+    }
+    __syncthreads();
+    if (row >= rows) return;
+    auto out_index = [&](int o) {
+        const int ee = o % E, qq = o / E;
+        return row + static_cast<long long>((ee % ra) * sa + (ee / ra) * sb1 + qq * sb2) * rows;
+    };
+    if (R == 1) {
+        for (int o = tid; o < C; o += blockDim.x) {
+            T sum = T(0);
+            for (int w = 0; w < W; ++w) sum += Yw[static_cast<std::size_t>(w) * C + o];
+            Y[out_index(o)] = sum;
+        }
+        return;
+    }
+    T* mine = Ypart + (static_cast<long long>(row) * R + q) * C;
+    for (int o = tid; o < C; o += blockDim.x) {
+        T sum = T(0);
+        for (int w = 0; w < W; ++w) sum += Yw[static_cast<std::size_t>(w) * C + o];
+        mine[o] = sum;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(&ticket[row], 1u) == static_cast<unsigned>(R - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const T* all = Ypart + static_cast<long long>(row) * R * C;
+    for (int o = tid; o < C; o += blockDim.x) {
+        T sum = T(0);
+        for (int p = 0; p < R; ++p) sum += __ldcg(all + static_cast<long long>(p) * C + o);
+        Y[out_index(o)] = sum;
+    }
+    if (tid == 0) ticket[row] = 0u;  // re-armed for the next launch (graph replays)
+}
+
+std::size_t stage2_4way_smem(int Ib1, int Ib2, int ra, int rb1, int rb2, int threads, int esz) {
+    const int E = ra * rb1;
+    const std::size_t rb1s = ttm_stride(rb1, esz), rb2s = ttm_stride(rb2, esz);
+    const int ras = (esz == 4 && (ra & 3) == 0) ? ra : (ra | 1);
+    return (static_cast<std::size_t>(Ib1) * rb1s + static_cast<std::size_t>(Ib2) * rb2s +
+            static_cast<std::size_t>(threads / 32) * (static_cast<std::size_t>(E) * rb2 + 2 * 32 * ras + 128 / esz)) * esz;
+}
+}  // namespace
+
+bool stage2_4way_ok(const std::vector<int>& dims, const std::vector<int>& ranks, int n, int a, int b1, int b2) {
+    const int E = ranks[a] * ranks[b1];
+    const int epl = (E + 31) / 32;
+    const int rb2 = ranks[b2];
+    const int rbb = rb2 <= 4 ? 4 : rb2 <= 8 ? 8 : rb2 <= 16 ? 16 : 32;
+    const int eplb = epl <= 1 ? 1 : epl <= 2 ? 2 : epl <= 4 ? 4 : 8;
+    if (eplb * rbb > 64) return false;  // register partial of the Y row
+    (void)n;
+    return stage2_4way_smem(dims[b1], dims[b2], ranks[a], ranks[b1], rb2, 512, 8) <= 200 * 1024;
+}
+
+template <typename T>
+void sparse_mode_stage2_4way(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks,
+                             const T* F, const std::vector<const T*>& Ur, T* Y) {
+    const int n = P.mode, a = P.a, b1 = P.bmodes[0], b2 = P.bmodes[1];
+    const int bits1 = bits_for(dims[b1]);
+    // Y_(n) columns: the remaining modes in original order, earliest fastest
+    int sa = 0, sb1 = 0, sb2 = 0, st = 1;
+    for (int m = 0; m < static_cast<int>(dims.size()); ++m) {
+        if (m == n) continue;
+        if (m == a) sa = st;
+        if (m == b1) sb1 = st;
+        if (m == b2) sb2 = st;
+        st *= ranks[m];
+    }
+    const int ra = ranks[a], rb1 = ranks[b1], rb2 = ranks[b2];
+    const int E = ra * rb1, C = E * rb2;
+    const int threads = 512;
+    const int rows = dims[n];
+    int sms = 148;
+    MB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    int R = 1;  // CTAs per row (i_b2 slices): two CTAs per SM
+    while (R < 16 && static_cast<long long>(rows) * R < 2ll * sms && R * 2 <= dims[b2]) R *= 2;
+    if (R > 1) {
+        const std::size_t need = static_cast<std::size_t>(rows) * R * C * sizeof(T);
+        if (P.s2part.n < need) P.s2part.alloc(ctx, need);
+        if (P.s2tick.n < static_cast<std::size_t>(rows)) {
+            P.s2tick.alloc(ctx, rows);
+            P.s2tick.zero(ctx);
+        }
+    }
+    const std::size_t smem = stage2_4way_smem(dims[b1], dims[b2], ra, rb1, rb2, threads, sizeof(T));
+    const int epl = (E + 31) / 32;
+    const int eplb = epl <= 1 ? 1 : epl <= 2 ? 2 : epl <= 4 ? 4 : 8;
+    const int rbb = rb2 <= 4 ? 4 : rb2 <= 8 ? 8 : rb2 <= 16 ? 16 : 32;
+    auto launch = [&](auto kern) {
+        MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        MB_LAUNCH_PDL(ctx, kern, static_cast<unsigned>(rows) * R, threads, smem, P.piece_rs.get(), P.piece_re.get(),
+                      P.pslot.get(), P.pib.get(), F, ra, (sizeof(T) == 4 && (ra & 3) == 0) ? ra : (ra | 1), rb1, rb2, Ur[b1], ttm_stride(rb1, sizeof(T)), Ur[b2],
+                      ttm_stride(rb2, sizeof(T)), dims[b1], dims[b2], bits1, sa, sb1, sb2, rows, R,
+                      reinterpret_cast<T*>(P.s2part.get()), P.s2tick.get(), Y);
+    };
+    switch (eplb * 100 + rbb) {
+        case 104: launch(stage2_4way_kernel<T, 1, 4>); break;
+        case 108: launch(stage2_4way_kernel<T, 1, 8>); break;
+        case 116: launch(stage2_4way_kernel<T, 1, 16>); break;
+        case 132: launch(stage2_4way_kernel<T, 1, 32>); break;
+        case 204: launch(stage2_4way_kernel<T, 2, 4>); break;
+        case 208: launch(stage2_4way_kernel<T, 2, 8>); break;
+        case 216: launch(stage2_4way_kernel<T, 2, 16>); break;
+        case 232: launch(stage2_4way_kernel<T, 2, 32>); break;
+        case 404: launch(stage2_4way_kernel<T, 4, 4>); break;
+        case 408: launch(stage2_4way_kernel<T, 4, 8>); break;
+        case 416: launch(stage2_4way_kernel<T, 4, 16>); break;
+        case 804: launch(stage2_4way_kernel<T, 8, 4>); break;
+        case 808: launch(stage2_4way_kernel<T, 8, 8>); break;
+        default: throw Error(MACH_ERR_INTERNAL, "order-4 stage 2: rank combination not instantiated");
+    }
+}
+template void sparse_mode_stage2_4way<float>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&, const float*,
+                                             const std::vector<const float*>&, float*);
+template void sparse_mode_stage2_4way<double>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&,
+                                              const double*, const std::vector<const double*>&, double*);
+
 template void sparse_mode_stage1<float>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&,
-                                        const std::vector<const float*>&, float*, int);
+                                        const std::vector<const float*>&, float*, int, bool);
 template void sparse_mode_stage1<double>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&,
-                                         const std::vector<const double*>&, double*, int);
+                                         const std::vector<const double*>&, double*, int, bool);
 template void sparse_mode_stage2<float>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&, const float*,
                                         const float*, float*);
 template void sparse_mode_stage2<double>(Ctx*, ModePlan&, const std::vector<int>&, const std::vector<int>&, const double*,

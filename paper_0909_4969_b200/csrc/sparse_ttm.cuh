@@ -43,7 +43,8 @@ struct TtmArgs {
     unsigned long long* ts;        // experiments: per-CTA %globaltimer stamps (8 per CTA) or null
     T* fseg;                       // optional: every segment's fibre sum (ra values at fpos[t * 32 + lane] * ra)
     const int* fpos;               // position of each segment in the i_b-grouped order (with fseg)
-    int stage1;                    // 1: fibre sums only, to fseg in task order (see ttm_mode_kernel)
+    int stage1;                    // 1: fibre sums only, to fseg in task order, overlapping the preceding
+                                   //    kernel (no wait at entry; see ttm_mode_kernel); 2: same, waiting
 };
 
 // Per-mode sorted layout of a sampled tensor (built once, reused by HOSVD and
@@ -68,6 +69,14 @@ struct ModePlan {
     DBuf<int> seg_row;             // i_n (this mode's row) of the segment at each position
     long long n_seg = -1;          // segments (valid positions), known once grouped
     DBuf<int> seg_ib;              // i_b of every segment slot t * 32 + lane, task order (0 past nseg)
+    // order 4 (stage2_4way_kernel): pieces in key order with their slot and
+    // composite i_b, each row's piece range, slice partials and row tickets
+    bool keep_pieces = false;
+    long long n_piece = 0;
+    DBuf<int> pslot, pib;
+    DBuf<long long> piece_rs, piece_re;
+    DBuf<unsigned char> s2part;
+    DBuf<unsigned> s2tick;
     // packed-key fields (least significant first): mode and bit offset
     int nf = 0;
     int fmode[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -124,10 +133,16 @@ void y_from_segments(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const 
 // sum over each row's segments of F (x) U_b[i_b, :] (fixed order).
 template <typename T>
 void sparse_mode_stage1(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks,
-                        const std::vector<const T*>& Ur, T* F, int ctas);
+                        const std::vector<const T*>& Ur, T* F, int ctas, bool overlapped = true);
 template <typename T>
 void sparse_mode_stage2(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks, const T* F,
                         const T* Ub, T* Y);
+// order 4: Y_(n) from stage 1's fibre sums through a per-row dense block
+// over the outer composite mode (see stage2_4way_kernel)
+template <typename T>
+void sparse_mode_stage2_4way(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const std::vector<int>& ranks,
+                             const T* F, const std::vector<const T*>& Ur, T* Y);
+bool stage2_4way_ok(const std::vector<int>& dims, const std::vector<int>& ranks, int n, int a, int b1, int b2);
 template <typename T>
 void sparse_row_gram(Ctx* ctx, const mach_sparse* X, int n, double normX2, double* G);
 template <typename T>

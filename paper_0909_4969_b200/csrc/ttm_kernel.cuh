@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
     // preceding mode-basis kernel: they read only data that was complete
     // before it started, so they skip the wait here and instead wait at the
     // end, making their completion imply the predecessor's.
-    if (A.stage1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (A.stage1 == 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     else pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     constexpr int VN = 16 / static_cast<int>(sizeof(T));  // elements per 128-bit load
     constexpr int RS = ((RA + VN - 1) / VN) * VN;         // ranks rounded to whole 16-B units
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(544, 1) ttm_mode_kernel(TtmArgs<T, IA> A) {
         }
     }
     if (ts && lane == 0) atomicMax(&ts[4], gtimer());
-    if (A.stage1) asm volatile("griddepcontrol.wait;" ::: "memory");  // complete only after the predecessor
+    if (A.stage1 == 1) asm volatile("griddepcontrol.wait;" ::: "memory");  // complete only after the predecessor
 }
 
 }  // namespace ttm

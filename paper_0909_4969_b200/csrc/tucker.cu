@@ -503,19 +503,27 @@ struct SparseSession : SessionBase {
     // Y_(n) = sum F (x) U_b, which needs the U_{n-1} just computed.  Stage 1 of
     // mode n is launched right behind mode n - 1's basis kernel and runs on
     // the SMs that kernel's 16-CTA cluster leaves idle.
-    DBuf<T> Fov;
+    // One fibre-sum buffer per mode: stage 1 of mode n (next sweep) may run
+    // before stage 2 of mode n - 1 has finished reading its own buffer
+    // (stage 1 does not wait at entry), so the buffers must be distinct; the
+    // strict launch order of the stage-2 kernels (pdl_enter_strict) keeps
+    // every stage 1 behind the completion of the stage 2 two modes back.
+    std::vector<DBuf<T>> Fov;
     bool overlap = false;
-    bool f0_ready = false;  // Fov holds mode 0's stage 1 for the current factors
+    bool split4 = false;    // order 4: stage 1 + the dimension-tree stage 2 (stage2_4way_kernel)
+    bool f0_ready = false;  // Fov[0] holds mode 0's stage 1 for the current factors
     bool overlap_ok() const { return overlap && !sharded; }
     void stage1(int m) {
         static const int reserve = std::getenv("MACH_OV_RESERVE") ? std::atoi(std::getenv("MACH_OV_RESERVE")) : 16;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-        sparse_mode_stage1<T>(ctx, *plans[static_cast<std::size_t>(m)], dims, ranks, Urp, Fov.get(), sms - reserve);
+        sparse_mode_stage1<T>(ctx, *plans[static_cast<std::size_t>(m)], dims, ranks, Urp,
+                              Fov[static_cast<std::size_t>(m)].get(), sms - reserve);
     }
     void stage2(int m) {
         auto& P = *plans[static_cast<std::size_t>(m)];
-        sparse_mode_stage2<T>(ctx, P, dims, ranks, Fov.get(), Urp[static_cast<std::size_t>(P.b)], Y.get());
+        sparse_mode_stage2<T>(ctx, P, dims, ranks, Fov[static_cast<std::size_t>(m)].get(),
+                              Urp[static_cast<std::size_t>(P.b)], Y.get());
     }
     bool fseg_use(int m) const {
         const bool off = std::getenv("MACH_NO_FIBRE_REUSE") != nullptr;
@@ -524,6 +532,13 @@ struct SparseSession : SessionBase {
     }
     void mode_y(int m) {
         const std::size_t sm = static_cast<std::size_t>(m);
+        if (split4) {  // order 4: fibre sums (waiting launch), then the two-level stage 2
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+            sparse_mode_stage1<T>(ctx, *plans[sm], dims, ranks, Urp, Fov[0].get(), sms, false);
+            sparse_mode_stage2_4way<T>(ctx, *plans[sm], dims, ranks, Fov[0].get(), Urp, Y.get());
+            return;
+        }
         if (m >= 1 && fseg_for == m) {
             y_from_segments<T>(ctx, *plans[sm - 1], dims, ranks, fseg.get(), Urp[sm - 1], Y.get());
             return;
@@ -662,6 +677,7 @@ struct SparseSession : SessionBase {
         plans.resize(static_cast<std::size_t>(d));
         const bool no_overlap = std::getenv("MACH_NO_OVERLAP") != nullptr;  // read per session (tests toggle it)
         overlap = d == 3 && !no_overlap;
+        split4 = d == 4;
         sumsq<T>(ctx, static_cast<const T*>(X->val), X->nnz, fs.red.get(), fs.scal.get());
         to_host(ctx, &normX2, fs.scal.get(), 1);
         sync(ctx);
@@ -684,19 +700,24 @@ struct SparseSession : SessionBase {
         C.resize(static_cast<std::size_t>(d));
         for (int m = 0; m < d; ++m) {
             const auto& P = *plans[static_cast<std::size_t>(m)];
-            const int c = ranks[static_cast<std::size_t>(P.a)] * (P.b >= 0 ? ranks[static_cast<std::size_t>(P.b)] : 1);
+            int c = 1;  // Y_(m) columns: product of the other ranks
+            for (int q = 0; q < d; ++q)
+                if (q != m) c *= ranks[static_cast<std::size_t>(q)];
             C[static_cast<std::size_t>(m)] = c;
-            maxP = std::max(maxP, P.n_task * c);
+            if (!split4) maxP = std::max(maxP, P.n_task * c);
             maxY = std::max(maxY, static_cast<long long>(dims[static_cast<std::size_t>(m)]) * c);
         }
         Pbuf.alloc(ctx, maxP);
         Y.alloc(ctx, maxY);
-        if (overlap) {
-            long long fmax = 0;
-            for (int m = 0; m < d; ++m)
-                fmax = std::max(fmax, plans[static_cast<std::size_t>(m)]->n_task * 32 *
-                                          ranks[static_cast<std::size_t>(plans[static_cast<std::size_t>(m)]->a)]);
-            Fov.alloc(ctx, static_cast<std::size_t>(fmax) + 16);  // slack: stage 2 bulk-copies aligned supersets
+        if (overlap || split4) {
+            Fov.clear();
+            Fov.resize(overlap ? static_cast<std::size_t>(d) : 1);
+            for (int m = 0; m < d; ++m) {
+                const std::size_t need = static_cast<std::size_t>(plans[static_cast<std::size_t>(m)]->n_task) * 32 *
+                                             ranks[static_cast<std::size_t>(plans[static_cast<std::size_t>(m)]->a)] + 16;
+                auto& B = Fov[overlap ? static_cast<std::size_t>(m) : 0];  // slack: stage 2 bulk-copies aligned supersets
+                if (B.n < need) B.alloc(ctx, need);
+            }
         }
         core.alloc(ctx, static_cast<std::size_t>(checked_size(ranks)));
         setup_ms = tm.stop_ms();
@@ -889,7 +910,7 @@ struct SparseSession : SessionBase {
         if (m < 0 || m >= d || !plans[static_cast<std::size_t>(m)]) return -1;
         const ModePlan& P = *plans[static_cast<std::size_t>(m)];
         const long long nnz = X->nnz;
-        if (overlap_ok())  // stage 1: nonzeros + task records in, fibre sums (every segment slot) out
+        if (overlap_ok() || split4)  // stage 1: nonzeros + task records in, fibre sums (every segment slot) out
             return nnz * ((P.ia16 ? 2 : 4) + static_cast<long long>(sizeof(T))) +
                    P.n_task * (static_cast<long long>(kDesc * sizeof(int2) + sizeof(TtmTask)) +
                                32 * ranks[static_cast<std::size_t>(P.a)] * static_cast<long long>(sizeof(T)));
@@ -939,7 +960,7 @@ void* session_sparse(mach_sparse* X, const std::vector<int>& ranks) {
 void* session_sparse_from(mach_sparse* X, const std::vector<int>& ranks, const mach_model* init) {
     check_ranks(X->dims, ranks);
     if (!sparse_fast_path_ok(X->dims, ranks))
-        throw Error(MACH_ERR_ARGUMENT, "split sweeps need the sparse route (order <= 3, ranks <= 32)");
+        throw Error(MACH_ERR_ARGUMENT, "split sweeps need the sparse route (order <= 4, ranks <= 32)");
     if (X->dtype == MACH_F32) {
         auto s = std::make_unique<SparseSession<float>>();
         s->begin_from(X, ranks, init);

@@ -155,6 +155,32 @@ def test_four_way_matches_oracle(mb):
     assert_model_close(res.model, ref, 1e-9, 1e-8, 1e-9)
 
 
+# order-4 sparse route (stage 1 fibre sums + dimension-tree stage 2), C3-like
+FOURWAY = [
+    ((20, 18, 9, 30), (3, 4, 2, 5), 0.05, np.float64, 3),
+    ((32, 32, 16, 64), (8, 8, 8, 8), 0.02, np.float32, 3),
+    ((24, 40, 7, 50), (5, 6, 3, 4), 0.1, np.float32, 4),
+]
+
+
+@pytest.mark.parametrize("dims,ranks,p,dt,sweeps", FOURWAY)
+def test_four_way_sparse_route_matches_oracle(mb, dims, ranks, p, dt, sweeps):
+    x = lowrank_numpy(dims, ranks, 0.02, seed=8, dtype=dt)
+    res = mb.mach_hooi(mb.DenseTensor.from_numpy(x), ranks, mb.SparsifyConfig(p, 7), mb.HooiConfig(sweeps, 0.0))
+    ref, ref_sp = O.mach_hooi(O.Dense(x.astype(np.float64)), ranks, p, 7, sweeps, 0.0)
+    assert np.array_equal(res.sparsified.entries()[0], ref_sp.entries()[0])
+    assert res.sparsified.nnz < 0.25 * x.size  # sparse route (below the densify switch)
+    if dt == np.float64:
+        assert_model_close(res.model, ref, 1e-9, 1e-8, 1e-9)
+        return
+    m = res.model
+    assert m.iterations == ref.iterations
+    for fd, fr in zip(m.factors, ref.factors):
+        assert subspace_sin(fd, fr) <= 1e-3
+    assert rel(align_core(m.core, m.factors, ref.factors), ref.core) <= 1e-4
+    assert np.allclose(m.sweep_fits, ref.sweep_fits, rtol=1e-4, atol=0)
+
+
 def test_order_one(mb):
     x = O.random_tensor([9], 77)
     assert mb.hosvd(x, [1]).fit >= 1 - 1e-10
