@@ -142,11 +142,16 @@ class DenseTensor:
 
     @classmethod
     def from_torch(cls, flat, dims, ctx: Context | None = None):
-        """Zero-copy view of a CUDA torch tensor whose memory is first-mode-fastest."""
+        """Zero-copy view of a CUDA torch tensor whose memory is first-mode-fastest.
+
+        The library works on its own stream: the producer's pending work on
+        torch's current stream is completed first, so the view never reads a
+        tensor that is still being written."""
         import torch
 
         ctx = _ctx(ctx)
         assert flat.is_cuda and flat.is_contiguous()
+        torch.cuda.current_stream(flat.device).synchronize()
         dt = {torch.float32: np.float32, torch.float64: np.float64}[flat.dtype]
         h = C.c_void_p()
         _check(L.lib().mach_dense_wrap(ctx.h, _DT[np.dtype(dt)], len(dims), _dims_arr(dims), C.c_void_p(flat.data_ptr()),
