@@ -14,7 +14,6 @@
 // atomic ticket, each tile publishes its kept count, and the tile's outputs
 // are staged in shared memory and written back coalesced.  The input is read
 // exactly once.
-#include <cub/block/block_scan.cuh>
 
 #include <cmath>
 
@@ -53,22 +52,47 @@ struct Vec<double> {
     __device__ static void unpack(const double2& v, double* o) { o[0] = v.x; o[1] = v.y; }
 };
 
-__device__ __forceinline__ bool is_finite_bits(float x) { return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u; }
-__device__ __forceinline__ bool is_finite_bits(double x) {
-    return (static_cast<unsigned long long>(__double_as_longlong(x)) & 0x7ff0000000000000ull) != 0x7ff0000000000000ull;
+// One CTA per tile of kThreads x NV vectors x VEC elements; element order in
+// the tile is (v, thread, j) = ascending flat index, so the exclusive scan of
+// the per-(v, thread) kept counts gives every kept element its output slot.
+// The design is latency hiding by occupancy (measured best on B200: a plain
+// streaming hash reaches ~0.52 of HBM only with 6-8 resident CTAs per SM):
+// few registers, no shared-memory staging, no per-tile pipeline state.
+//   - a ticket orders the tiles (the look-back only waits on tiles that
+//     started earlier);
+//   - all NV 16-byte vectors are loaded first, then the SplitMix64 rounds run
+//     on 32-bit halves; keep iff the hash's high word is below the
+//     threshold's, with an exact 64-bit compare on a high-word tie
+//     (probability 2^-32 per element);
+//   - packed per-v counts (16-bit fields) are scanned with warp shuffles and
+//     one pass over the warp totals; the tile's aggregate is published and
+//     warp 0 runs the decoupled look-back (relaxed polls: the status word
+//     carries its own payload);
+//   - each thread writes its kept (index, x / p) straight from registers:
+//     for one v the warp's kept entries are contiguous in the output.
+// x / p is the reference's correctly rounded fp64 division (sampling.cpp:28):
+// for fp32 data through Markstein's correction (y = RN(1/p), q = RN(x y),
+// r = x - q p exactly by FMA, RN(q + r y) = RN(x / p) for these ranges),
+// for fp64 data through __ddiv_rn.
+template <typename T>
+__device__ __forceinline__ T scaled(T xv, double p, double inv_p) {
+    if constexpr (sizeof(T) == 4) {
+        const double xd = static_cast<double>(xv);
+        const double q = xd * inv_p;
+        const double r = fma(-q, p, xd);
+        return static_cast<T>(fma(r, inv_p, q));
+    } else {
+        return __ddiv_rn(xv, p);
+    }
 }
 
-// Tile = kThreads threads x NV vector loads x VEC elements.  Element order in
-// the tile is (v, thread, j) which is ascending flat index, so an exclusive
-// scan of the per-(v, thread) kept counts in that order gives each kept
-// element its output slot.  The NV counts of a thread are packed into one u64
-// (16-bit fields; a block-wide per-v total is <= kThreads * VEC <= 2048).
 template <typename T, typename IdxT>
-__global__ void __launch_bounds__(kThreads, 4) sample_kernel(const T* __restrict__ x, std::int64_t numel,
+__global__ void __launch_bounds__(kThreads, 5) sample_kernel(const T* __restrict__ x, std::int64_t numel,
                                                           std::int64_t gofs,  // global flat index of x[0]
                                                           std::uint64_t seed, std::uint64_t thr_shift,
-                                                          int keep_all, double p, IdxT* __restrict__ out_idx,
-                                                          T* __restrict__ out_val, std::int64_t capacity,
+                                                          int keep_all, double p, double inv_p,
+                                                          IdxT* __restrict__ out_idx, T* __restrict__ out_val,
+                                                          std::int64_t capacity,
                                                           unsigned long long* __restrict__ status,
                                                           unsigned int* __restrict__ ticket,
                                                           long long* __restrict__ total_out,
@@ -77,130 +101,107 @@ __global__ void __launch_bounds__(kThreads, 4) sample_kernel(const T* __restrict
     constexpr int VEC = V::n;
     constexpr int NV = 4;
     constexpr int TILE = kThreads * NV * VEC;
-    using BlockScan = cub::BlockScan<unsigned long long, kThreads>;
-
-    __shared__ typename BlockScan::TempStorage scan_tmp;
-    extern __shared__ __align__(16) unsigned char s_dyn[];
-    IdxT* s_idx = reinterpret_cast<IdxT*>(s_dyn);
-    T* s_val = reinterpret_cast<T*>(s_dyn + TILE * sizeof(IdxT));
-    __shared__ unsigned int s_tile;
+    constexpr int NW = kThreads / 32;
+    __shared__ unsigned long long s_wtot[NW];
     __shared__ long long s_excl;
-
-    const int tid = threadIdx.x;
+    __shared__ unsigned s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const std::int64_t tile = s_tile;
     const std::int64_t base = tile * TILE;
-
-    // ---- load (all vectors in flight first) + hash ----
+    const bool full = base + TILE <= numel;
     T vals[NV][VEC];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         const std::int64_t e0 = base + (static_cast<std::int64_t>(v) * kThreads + tid) * VEC;
-        if (e0 + VEC <= numel) {
-#pragma unroll
-            for (int l = 0; l < VEC / V::per; ++l) {
-                const auto raw = __ldcs(reinterpret_cast<const typename V::type*>(x + e0) + l);
-                V::unpack(raw, vals[v] + l * V::per);
-            }
+        if (full) {
+            V::unpack(__ldcs(reinterpret_cast<const typename V::type*>(x + e0)), vals[v]);
         } else {
 #pragma unroll
             for (int j = 0; j < VEC; ++j) vals[v][j] = (e0 + j < numel) ? x[e0 + j] : T(0);
         }
     }
-    unsigned keep_bits = 0;  // bit (v*VEC + j)
-    unsigned tie_bits = 0;   // high word of the hash equal to the threshold's (exact check below)
-    T nanacc = T(0);         // x * 0 is NaN exactly for inf / NaN inputs
     const unsigned thr_hi = static_cast<unsigned>(thr_shift >> 32);
+    unsigned keep = 0;  // bit v * VEC + j
+    bool tie = false;
+    T nanacc = T(0);  // x * 0 is NaN exactly for inf / NaN inputs
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         const std::int64_t e0 = base + (static_cast<std::int64_t>(v) * kThreads + tid) * VEC;
-        const std::int64_t rem = numel - e0;
-        const int lim = rem >= VEC ? VEC : (rem > 0 ? static_cast<int>(rem) : 0);
-        // z_j = seed + (i + 1) * golden for consecutive i: incremental adds.
-        std::uint64_t z = seed + (static_cast<std::uint64_t>(gofs + e0) + 1ull) * 0x9E3779B97F4A7C15ULL;
+        // z_j = seed + (i + 1) * golden for consecutive i
+        const std::uint64_t z0 = seed + (static_cast<std::uint64_t>(gofs + e0) + 1ull) * 0x9E3779B97F4A7C15ULL;
 #pragma unroll
         for (int j = 0; j < VEC; ++j) {
             const T xv = vals[v][j];
             nanacc = fma(xv, T(0), nanacc);
-            // keep iff hash < thr_shift.  The final xor-shift's high word needs
-            // only the high word of the last product; the low words matter
-            // only on a high-word tie (probability 2^-32), handled after.
-            std::uint64_t y = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-            y ^= y >> 27;
-            const unsigned ylo = static_cast<unsigned>(y), yhi = static_cast<unsigned>(y >> 32);
-            const unsigned zhi = __umulhi(ylo, 0x133111EBu) + ylo * 0x94D049BBu + yhi * 0x133111EBu;
+            const std::uint64_t z = z0 + static_cast<std::uint64_t>(j) * 0x9E3779B97F4A7C15ULL;
+            const unsigned zl = static_cast<unsigned>(z), zh = static_cast<unsigned>(z >> 32);
+            const unsigned al = zl ^ __funnelshift_r(zl, zh, 30), ah = zh ^ (zh >> 30);
+            const std::uint64_t pm = static_cast<std::uint64_t>(al) * 0x1CE4E5B9u;
+            const unsigned yl = static_cast<unsigned>(pm);
+            const unsigned yh = static_cast<unsigned>(pm >> 32) + al * 0xBF58476Du + ah * 0x1CE4E5B9u;
+            const unsigned bl = yl ^ __funnelshift_r(yl, yh, 27), bh = yh ^ (yh >> 27);
+            const unsigned zhi = __umulhi(bl, 0x133111EBu) + bl * 0x94D049BBu + bh * 0x133111EBu;
             const unsigned hhi = zhi ^ (zhi >> 31);
-            const bool live = (xv != T(0)) & (j < lim);
-            keep_bits |= static_cast<unsigned>(live & (keep_all | (hhi < thr_hi))) << (v * VEC + j);
-            tie_bits |= static_cast<unsigned>(live & (hhi == thr_hi)) << (v * VEC + j);
-            z += 0x9E3779B97F4A7C15ULL;
+            const bool live = (xv != T(0)) & (full || e0 + j < numel);
+            if (live & (keep_all | (hhi < thr_hi))) keep |= 1u << (v * VEC + j);
+            tie |= live & (hhi == thr_hi);
         }
     }
-    if (tie_bits && !keep_all) {  // exact 64-bit comparison for the (rare) ties
+    if (tie && !keep_all) {  // exact 64-bit comparison for the rare high-word ties
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             const std::int64_t e0 = base + (static_cast<std::int64_t>(v) * kThreads + tid) * VEC;
 #pragma unroll
-            for (int j = 0; j < VEC; ++j)
-                if ((tie_bits >> (v * VEC + j)) & 1u) {
-                    const std::uint64_t z = seed + (static_cast<std::uint64_t>(gofs + e0 + j) + 1ull) * 0x9E3779B97F4A7C15ULL;
-                    if (splitmix_finalize(z) < thr_shift) keep_bits |= 1u << (v * VEC + j);
-                }
-        }
-    }
-    if (nanacc != nanacc) atomicOr(flags, 1);
-
-    unsigned long long packed = 0;
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-        packed |= static_cast<unsigned long long>(__popc((keep_bits >> (v * VEC)) & ((1u << VEC) - 1u))) << (16 * v);
-    unsigned long long excl_packed, tot_packed;
-    BlockScan(scan_tmp).ExclusiveSum(packed, excl_packed, tot_packed);
-
-    unsigned offv[NV];
-    unsigned run = 0;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-        offv[v] = run + static_cast<unsigned>((excl_packed >> (16 * v)) & 0xFFFFu);
-        run += static_cast<unsigned>((tot_packed >> (16 * v)) & 0xFFFFu);
-    }
-    const unsigned tile_total = run;
-    // publish this tile's aggregate as early as possible (successors' look-back)
-    if (tid == 0 && tile > 0) atomicExch(&status[tile], kFlagAgg | tile_total);
-
-    // ---- stage kept entries (raw values) in shared memory in tile order ----
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-        unsigned o = offv[v];
-        const std::int64_t e0 = base + (static_cast<std::int64_t>(v) * kThreads + tid) * VEC;
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-            if ((keep_bits >> (v * VEC + j)) & 1u) {
-                s_idx[o] = static_cast<IdxT>(gofs + e0 + j);
-                s_val[o] = vals[v][j];
-                ++o;
+            for (int j = 0; j < VEC; ++j) {
+                if (vals[v][j] == T(0) || !(full || e0 + j < numel)) continue;
+                const std::uint64_t h = splitmix_finalize(seed + (static_cast<std::uint64_t>(gofs + e0 + j) + 1ull) * 0x9E3779B97F4A7C15ULL);
+                if (h < thr_shift) keep |= 1u << (v * VEC + j);
             }
         }
     }
+    if (nanacc != nanacc) atomicOr(flags, 1);
+    // ---- per-v counts (16-bit fields), warp scan, warp totals ----
+    unsigned long long packed = 0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+        packed |= static_cast<unsigned long long>(__popc((keep >> (v * VEC)) & ((1u << VEC) - 1u))) << (16 * v);
+    unsigned long long inc = packed;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_wtot[warp] = inc;
     __syncthreads();
-
+    unsigned long long before = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const unsigned long long t = s_wtot[w];
+        before += (w < warp) ? t : 0ull;
+        tot += t;
+    }
+    const unsigned long long excl_packed = before + inc - packed;
+    unsigned tile_total = 0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) tile_total += static_cast<unsigned>((tot >> (16 * v)) & 0xFFFFull);
     if (tid < 32) {
         // ---- decoupled look-back (warp 0) ----
-        const int lane = tid;
         long long excl = 0;
         if (tile == 0) {
             if (lane == 0) atomicExch(&status[0], kFlagPre | tile_total);
         } else {
+            if (lane == 0) atomicExch(&status[tile], kFlagAgg | tile_total);
             std::int64_t look = tile - 1;
             while (true) {
                 const std::int64_t j = look - lane;
-                unsigned long long s = kFlagPre | 0ull;
-                if (j >= 0) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(s) : "l"(status + j) : "memory");
-                const bool unset = (s >> 62) == 0;
+                unsigned long long st = kFlagPre | 0ull;
+                if (j >= 0) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(st) : "l"(status + j) : "memory");
+                const bool unset = (st >> 62) == 0;
                 if (__any_sync(0xffffffffu, unset)) continue;
-                const unsigned pmask = __ballot_sync(0xffffffffu, (s & ~kValMask) == kFlagPre);
-                long long mine = static_cast<long long>(s & kValMask);
+                const unsigned pmask = __ballot_sync(0xffffffffu, (st & ~kValMask) == kFlagPre);
+                long long mine = static_cast<long long>(st & kValMask);
                 if (pmask) {
                     const int first = __ffs(pmask) - 1;
                     if (lane > first) mine = 0;
@@ -218,37 +219,41 @@ __global__ void __launch_bounds__(kThreads, 4) sample_kernel(const T* __restrict
             const std::int64_t ntiles = (numel + TILE - 1) / TILE;
             if (tile == ntiles - 1) *total_out = excl + tile_total;
         }
-    } else {
-        // ---- meanwhile the other warps form x / p (correctly rounded fp64
-        // division, sampling.cpp:28) for the staged entries, coalesced ----
-        for (unsigned k = tid - 32; k < tile_total; k += kThreads - 32)
-            s_val[k] = static_cast<T>(__ddiv_rn(static_cast<double>(s_val[k]), p));
     }
     __syncthreads();
-
-    // ---- coalesced write-back ----
+    // ---- write kept (index, x / p) straight from registers ----
     const long long g0 = s_excl;
     if (g0 + tile_total > capacity) {
         if (tid == 0 && tile_total) atomicOr(flags, 2);
         return;
     }
-    for (unsigned k = tid; k < tile_total; k += kThreads) {
-        out_idx[g0 + k] = s_idx[k];
-        out_val[g0 + k] = s_val[k];
+    if (!keep) return;
+    unsigned run = 0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        unsigned o = run + static_cast<unsigned>((excl_packed >> (16 * v)) & 0xFFFFull);
+        run += static_cast<unsigned>((tot >> (16 * v)) & 0xFFFFull);
+        const std::int64_t e0 = base + (static_cast<std::int64_t>(v) * kThreads + tid) * VEC;
+#pragma unroll
+        for (int j = 0; j < VEC; ++j)
+            if ((keep >> (v * VEC + j)) & 1u) {
+                out_idx[g0 + o] = static_cast<IdxT>(gofs + e0 + j);
+                out_val[g0 + o] = scaled<T>(vals[v][j], p, inv_p);
+                ++o;
+            }
     }
 }
 
 template <typename T, typename IdxT>
 std::int64_t launch_sample(Ctx* ctx, const T* x, std::int64_t numel, std::int64_t gofs, std::uint64_t seed, double p,
                            std::int64_t capacity, IdxT* out_idx, T* out_val, int* flags_host) {
-    constexpr int VEC = Vec<T>::n;
-    constexpr int TILE = kThreads * 4 * VEC;  // NV = 4
+    constexpr int TILE = kThreads * 4 * Vec<T>::n;
     const std::int64_t ntiles = (numel + TILE - 1) / TILE;
     // threshold: keep iff (h >> 11) < ceil(p * 2^53)  <=>  h < ceil(p*2^53) << 11
     const double t53 = std::ceil(std::ldexp(p, 53));
     const bool keep_all = t53 >= 9007199254740992.0;  // p == 1
     const std::uint64_t thr = keep_all ? 0 : (static_cast<std::uint64_t>(t53) << 11);
-
+    if (ntiles > 0x7fffffffll) throw_arg("tensor too large for one sampler launch");
     // scratch: status[ntiles] + ticket + total + flags, one allocation
     const std::size_t words = static_cast<std::size_t>(ntiles) + 4;
     DBuf<unsigned long long> scratch(ctx, words);
@@ -257,15 +262,9 @@ std::int64_t launch_sample(Ctx* ctx, const T* x, std::int64_t numel, std::int64_
     unsigned int* ticket = reinterpret_cast<unsigned int*>(status + ntiles);
     long long* total = reinterpret_cast<long long*>(status + ntiles + 1);
     int* flags = reinterpret_cast<int*>(status + ntiles + 2);
-    const std::size_t smem = static_cast<std::size_t>(TILE) * (sizeof(IdxT) + sizeof(T));
-    static bool attr = false;
-    if (!attr) {
-        MB_CUDA(cudaFuncSetAttribute(sample_kernel<T, IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = true;
-    }
     if (ntiles > 0)
-        MB_LAUNCH(ctx, (sample_kernel<T, IdxT>), static_cast<unsigned>(ntiles), kThreads, smem, x, numel, gofs, seed, thr,
-                  keep_all ? 1 : 0, p, out_idx, out_val, capacity, status, ticket, total, flags);
+        MB_LAUNCH(ctx, (sample_kernel<T, IdxT>), static_cast<unsigned>(ntiles), kThreads, 0, x, numel, gofs, seed, thr,
+                  keep_all ? 1 : 0, p, 1.0 / p, out_idx, out_val, capacity, status, ticket, total, flags);
     long long tot = 0;
     int fl = 0;
     to_host(ctx, &tot, total, 1);
