@@ -191,6 +191,12 @@ mach_status mach_mode_product_dense(mach_ctx* ctx, const mach_dense* t, int rows
                                     const double* m, int mode, mach_dense** out);
 mach_status mach_mode_product_sparse(mach_ctx* ctx, const mach_sparse* t, int rows, int cols,
                                      const double* m, int mode, mach_dense** out);
+/* Mode-n Gram X_(n) X_(n)^T of a dense tensor (the dense HOSVD's row-side
+ * Gram, linalg.cpp:340 via tucker.cpp:135-150), I_n x I_n column-major fp64
+ * into host.  fp32 tensors of supported shape use the tcgen05 TF32 kernel
+ * (*tensor_cores = 1); otherwise the fp64 CUDA-core Gram (*tensor_cores = 0). */
+mach_status mach_dense_mode_gram(mach_ctx* ctx, const mach_dense* t, int mode, double* host,
+                                 int* tensor_cores);
 
 #ifdef __cplusplus
 }

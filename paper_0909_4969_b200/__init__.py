@@ -28,6 +28,7 @@ from .api import (  # noqa: F401
     left_singular_basis,
     mach_hooi,
     mach_hosvd,
+    mode_gram,
     mode_product,
     reconstruct,
     sparsify,

@@ -96,6 +96,7 @@ _SIGS = {
     "mach_left_singular_basis": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int, dp, dp, ip, ip]),
     "mach_mode_product_dense": (C.c_int, [vp, vp, C.c_int, C.c_int, dp, C.c_int, vpp]),
     "mach_mode_product_sparse": (C.c_int, [vp, vp, C.c_int, C.c_int, dp, C.c_int, vpp]),
+    "mach_dense_mode_gram": (C.c_int, [vp, vp, C.c_int, dp, ip]),
 }
 
 

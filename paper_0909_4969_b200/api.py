@@ -435,6 +435,18 @@ def mode_product(t, m: np.ndarray, mode: int, ctx: Context | None = None, keep_o
     return out if keep_on_device else out.numpy()
 
 
+def mode_gram(t, mode: int, ctx: Context | None = None):
+    """X_(mode) X_(mode)^T of a dense tensor (the dense HOSVD's row-side Gram,
+    linalg.cpp:340).  Returns (G, tensor_cores): fp32 tensors of supported
+    shape go through the tcgen05 TF32 kernel (tensor_cores True)."""
+    d = _dense(t, ctx)
+    R = d.dims[mode]
+    g = np.empty(R * R, dtype=np.float64)
+    tc = C.c_int(0)
+    _check(L.lib().mach_dense_mode_gram(d.ctx.h, d.h, int(mode), g.ctypes.data_as(L.dp), C.byref(tc)))
+    return g.reshape((R, R), order="F"), bool(tc.value)
+
+
 @dataclass
 class LeftSingularBasis:
     basis: np.ndarray

@@ -6,6 +6,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "sparse_ttm.cuh"
 
 namespace machb {
 mach_sparse* sample_dense(const mach_dense* x, double p, std::uint64_t seed);
@@ -481,6 +482,39 @@ mach_status mach_mode_product_sparse(mach_ctx* ctx, const mach_sparse* t, int ro
         need(ctx, "ctx");
         need(t, "tensor");
         *out = mode_product_dev(&ctx->c, nullptr, t, rows, cols, m, mode);
+    });
+}
+
+mach_status mach_dense_mode_gram(mach_ctx* ctx, const mach_dense* t, int mode, double* host, int* tensor_cores) {
+    return guard([&] {
+        need(ctx, "ctx");
+        need(t, "tensor");
+        need(host, "host");
+        if (mode < 0 || mode >= static_cast<int>(t->dims.size())) throw_arg("mode out of range");
+        Ctx* c = &ctx->c;
+        const int R = t->dims[static_cast<std::size_t>(mode)];
+        const long long K = t->numel / std::max(1, R);
+        DBuf<double> G(c, static_cast<std::size_t>(R) * R);
+        int tc = 0;
+        if (t->dtype == MACH_F32 && gram_tc_applies(t->dims, mode)) {
+            gram_tc(c, static_cast<const float*>(t->data), t->dims, mode, G.get());
+            tc = 1;
+        } else if (K <= (1ll << 31) - 1) {
+            if (t->dtype == MACH_F32) {
+                DBuf<float> xm(c, static_cast<std::size_t>(t->numel));
+                dense_matricize<float, float>(c, static_cast<const float*>(t->data), t->dims, mode, xm.get());
+                gram<float>(c, xm.get(), R, 1, static_cast<int>(K), R, G.get());
+            } else {
+                DBuf<double> xm(c, static_cast<std::size_t>(t->numel));
+                dense_matricize<double, double>(c, static_cast<const double*>(t->data), t->dims, mode, xm.get());
+                gram<double>(c, xm.get(), R, 1, static_cast<int>(K), R, G.get());
+            }
+        } else {
+            throw_shape("mode unfolding too wide for the CUDA-core Gram");
+        }
+        to_host(c, host, G.get(), static_cast<std::size_t>(R) * R);
+        sync(c);
+        if (tensor_cores) *tensor_cores = tc;
     });
 }
 

@@ -239,6 +239,9 @@ bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double
 template <typename Tin>
 void dense_mode_product(Ctx* ctx, const Tin* in, const std::vector<int>& dims, int mode, const double* U, int J,
                         bool transpose, double* out);
+// dense mode-n Gram X_(n) X_(n)^T on tcgen05 (gram_tc.cu), read in place
+bool gram_tc_applies(const std::vector<int>& dims, int n);
+void gram_tc(Ctx* ctx, const float* x, const std::vector<int>& dims, int n, double* G);
 template <typename Tin, typename Tout>
 void dense_matricize(Ctx* ctx, const Tin* in, const std::vector<int>& dims, int mode, Tout* out);
 template <typename T>

@@ -196,6 +196,22 @@ void lsb_device(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U
     }
 }
 
+// Row-side left_singular_basis of a dense tensor's mode-m unfolding with the
+// Gram formed on the tensor cores (gram_tc.cu) — the dense HOSVD's step
+// (tucker.cpp:135-150 -> linalg.cpp:319-353 row side).
+inline void lsb_from_gram(Ctx* ctx, const float* x, const std::vector<int>& dims, int m, int k, double* U, double* sv,
+                          int* st) {
+    const int rows = dims[static_cast<std::size_t>(m)];
+    DBuf<double> G(ctx, static_cast<std::size_t>(rows) * rows);
+    gram_tc(ctx, x, dims, m, G.get());
+    DBuf<double> V(ctx, static_cast<std::size_t>(rows) * k);
+    DBuf<double> sig(ctx, k);
+    DBuf<int> est(ctx, 3);
+    const int b = eig_block(rows, k);
+    eig_select(ctx, G.get(), rows, k, nullptr, 0, nullptr, b, V.get(), sig.get(), est.get());
+    basis_from_side(ctx, V.get(), sig.get(), rows, k, est.get(), U, sv, st);
+}
+
 // Column-side factor update through the fused cluster kernel (mode_basis.cu),
 // including the TTM kernel's row-major factor copy.  False when the fused
 // route does not apply (the caller then runs lsb_device + the copy).
@@ -439,6 +455,15 @@ struct DenseSession : SessionBase {
         for (int m = 0; m < d; ++m) {
             const int rows = dims[static_cast<std::size_t>(m)];
             const long long cols = numel / rows;
+            if constexpr (std::is_same_v<T, float>) {
+                // row side (rows <= cols) with the Gram on the tensor cores,
+                // straight from the tensor (no matricised copy)
+                if (rows <= cols && ranks[static_cast<std::size_t>(m)] <= cols && gram_tc_applies(dims, m)) {
+                    lsb_from_gram(ctx, x, dims, m, ranks[static_cast<std::size_t>(m)], fs.U[static_cast<std::size_t>(m)].get(),
+                                  sv_at(m), fs.st.get() + 3 * m);
+                    continue;
+                }
+            }
             if (m == 0) {
                 lsb_device<T>(ctx, x, rows, cols, ranks[0], fs.U[0].get(), sv_at(0), fs.st.get());
             } else {

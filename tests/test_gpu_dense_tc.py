@@ -1,0 +1,86 @@
+"""Dense route on the tensor cores (gram_tc.cu): the mode-n Gram X_(n) X_(n)^T
+through tcgen05 kind::tf32 against an fp64 Gram, and the fp32 dense HOSVD /
+HOOI that uses it against the CPU oracle.
+
+Reference: hosvd(DenseTensor) (proj/src/tucker.cpp:135-150) -> row-side Gram
+a * a^T (proj/src/linalg.cpp:340).  Tolerances: the Gram carries TF32
+operands (10-bit mantissa): entrywise error <= 2e-3 of the largest diagonal
+entry; the leading eigen-subspace of a low-rank + noise Gram within sine
+1e-4 of the fp64 one; the HOSVD / HOOI model within the north_star fp32 bars
+(sine <= 1e-3, fit and core 1e-4 relative).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_0909_4969_b200.synth import lowrank_numpy
+from tests.helpers import align_core, rel, subspace_sin
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mb():
+    import paper_0909_4969_b200 as mb
+    return mb
+
+
+def unfold(x, mode):
+    return np.moveaxis(x, mode, 0).reshape(x.shape[mode], -1, order="F")
+
+
+@pytest.mark.parametrize("dims", [(256, 96, 80), (130, 68, 300), (64, 512, 36), (200, 16, 24, 40)])
+def test_mode_gram_tf32_matches_fp64(mb, dims):
+    rng = np.random.default_rng(sum(dims))
+    x = rng.standard_normal(dims).astype(np.float32)
+    t = mb.DenseTensor.from_numpy(x)
+    for m in range(len(dims)):
+        g, tc = mb.mode_gram(t, m)
+        a = unfold(x.astype(np.float64), m)
+        ref = a @ a.T
+        if dims[m] >= 64 and a.shape[1] >= 4096 and (m == 0 and dims[0] % 4 == 0 or m > 0 and np.prod(dims[:m]) % 4 == 0):
+            assert tc, f"mode {m} of {dims} should take the tensor-core Gram"
+        assert np.array_equal(g, g.T), "Gram must be exactly symmetric"
+        scale = np.abs(np.diag(ref)).max()
+        assert np.abs(g - ref).max() <= 2e-3 * scale, (m, np.abs(g - ref).max() / scale)
+
+
+def test_mode_gram_tf32_subspace(mb):
+    dims, ranks = (256, 192, 160), (6, 5, 7)
+    x = lowrank_numpy(dims, ranks, 0.01, seed=11).astype(np.float32)
+    t = mb.DenseTensor.from_numpy(x)
+    for m in range(3):
+        g, tc = mb.mode_gram(t, m)
+        assert tc
+        a = unfold(x.astype(np.float64), m)
+        ref = a @ a.T
+        k = ranks[m]
+        _, vd = np.linalg.eigh(g)
+        _, vr = np.linalg.eigh(ref)
+        assert subspace_sin(vd[:, -k:], vr[:, -k:]) <= 1e-4
+
+
+def test_dense_hosvd_fp32_tensor_cores_match_oracle(mb):
+    dims, ranks = (256, 128, 192), (8, 6, 7)
+    x = lowrank_numpy(dims, ranks, 0.01, seed=5)
+    xf = x.astype(np.float32)
+    dev = mb.hosvd(mb.DenseTensor.from_numpy(xf), ranks)
+    ref = O.hosvd(O.Dense(xf.astype(np.float64)), ranks)
+    for fd, fr in zip(dev.factors, ref.factors):
+        assert subspace_sin(fd, fr) <= 1e-3
+    assert abs(dev.fit - ref.fit) <= 1e-4 * abs(ref.fit)
+    core = align_core(dev.core, dev.factors, ref.factors)
+    assert rel(core, ref.core) <= 1e-4
+
+
+def test_dense_hooi_fp32_tensor_cores_match_oracle(mb):
+    dims, ranks = (192, 160, 128), (5, 5, 5)
+    x = lowrank_numpy(dims, ranks, 0.02, seed=9).astype(np.float32)
+    dev = mb.hooi(mb.DenseTensor.from_numpy(x), ranks, mb.HooiConfig(3, 0.0))
+    ref = O.hooi(O.Dense(x.astype(np.float64)), ranks, 3, 0.0)
+    for fd, fr in zip(dev.factors, ref.factors):
+        assert subspace_sin(fd, fr) <= 1e-3
+    n = min(len(dev.sweep_fits), len(ref.sweep_fits))
+    assert np.abs(np.array(dev.sweep_fits[:n]) - np.array(ref.sweep_fits[:n])).max() <= 1e-4
+    core = align_core(dev.core, dev.factors, ref.factors)
+    assert rel(core, ref.core) <= 1e-4
