@@ -5,6 +5,8 @@
 // keeps >= 25% of its entries (kDensifyThreshold, tucker.cpp:66-69).
 // Intermediates are fp64; each output is summed by one thread in a fixed
 // order, so results are reproducible bit for bit.
+#include <algorithm>
+
 #include "sparse_ttm.cuh"
 
 namespace machb {
@@ -86,6 +88,57 @@ __global__ void __launch_bounds__(256) mode_product_fibre_kernel(const Tin* __re
 #pragma unroll
         for (int q = 0; q < JB; ++q)
             if (q < J) o[inner * q] = acc[q];
+    }
+}
+
+// Few fibres, long contraction (e.g. the dense route's Z0 = X x_0 U_0^T, 16 x
+// 1024 x 1024, contracted over its last mode: only 16K fibres of length
+// 1024): the contraction is split into chunks over blockIdx.y, each thread
+// accumulating its fibre's chunk for all J outputs; partials are summed in
+// chunk order by sum_chunks_kernel (deterministic).
+template <typename Tin, int JB>
+__global__ void __launch_bounds__(256) mode_product_fibre_split_kernel(const Tin* __restrict__ in, long long inner,
+                                                                       int len, long long outer,
+                                                                       const double* __restrict__ U, int J,
+                                                                       int transpose, int chunk,
+                                                                       double* __restrict__ part) {
+    extern __shared__ double us[];  // us[(r - r0) * J + q] = M(q, r) for the chunk
+    const int r0 = blockIdx.y * chunk, r1 = min(len, r0 + chunk);
+    for (int e = threadIdx.x; e < (r1 - r0) * J; e += blockDim.x) {
+        const int r = r0 + e / J, q = e - (e / J) * J;
+        us[e] = transpose ? U[r + static_cast<long long>(len) * q] : U[q + static_cast<long long>(J) * r];
+    }
+    __syncthreads();
+    const long long total = inner * outer;
+    double* pp = part + static_cast<long long>(blockIdx.y) * total * J;
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long a = idx % inner, c = idx / inner;
+        const Tin* src = in + a + inner * len * c;
+        double acc[JB];
+#pragma unroll
+        for (int q = 0; q < JB; ++q) acc[q] = 0.0;
+#pragma unroll 4
+        for (int r = r0; r < r1; ++r) {
+            const double x = static_cast<double>(src[inner * r]);
+            const double* ur = us + (r - r0) * J;
+#pragma unroll
+            for (int q = 0; q < JB; ++q)
+                if (q < J) acc[q] = fma(x, ur[q], acc[q]);
+        }
+        double* o = pp + a + inner * static_cast<long long>(J) * c;
+#pragma unroll
+        for (int q = 0; q < JB; ++q)
+            if (q < J) o[inner * q] = acc[q];
+    }
+}
+
+__global__ void sum_chunks_kernel(const double* __restrict__ part, int nchunk, long long n, double* __restrict__ out) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < nchunk; ++k) s += part[static_cast<long long>(k) * n + i];
+        out[i] = s;
     }
 }
 
@@ -225,6 +278,26 @@ void dense_mode_product(Ctx* ctx, const Tin* in, const std::vector<int>& dims, i
             if (J <= 8) gr(mode_product_row_kernel<Tin, 8>);
             else if (J <= 16) gr(mode_product_row_kernel<Tin, 16>);
             else gr(mode_product_row_kernel<Tin, 32>);
+            return;
+        }
+        if (fib < 148ll * 1024 && s.len >= 128) {
+            // too few fibres to fill the GPU: split the contraction
+            int nchunk = static_cast<int>(std::min<long long>(s.len / 32, (148ll * 2048 + fib - 1) / fib));
+            nchunk = std::max(nchunk, static_cast<int>((static_cast<long long>(s.len) * J * 8 + 48 * 1024 - 1) / (48 * 1024)));
+            const int chunk = (s.len + nchunk - 1) / nchunk;
+            const int nc = (s.len + chunk - 1) / chunk;
+            DBuf<double> part(ctx, static_cast<std::size_t>(nc) * total);
+            const std::size_t cb = static_cast<std::size_t>(chunk) * J * sizeof(double);
+            dim3 grid(static_cast<unsigned>(std::max<long long>(1, std::min<long long>((fib + 255) / 256, 148 * 8))),
+                      static_cast<unsigned>(nc));
+            auto gs = [&](auto mode_product_split_kernel_jb) {  // (the name is the profiler's kernel label)
+                MB_LAUNCH(ctx, mode_product_split_kernel_jb, grid, 256, cb, in, s.inner, s.len, s.outer, U, J,
+                          transpose ? 1 : 0, chunk, part.get());
+            };
+            if (J <= 8) gs(mode_product_fibre_split_kernel<Tin, 8>);
+            else if (J <= 16) gs(mode_product_fibre_split_kernel<Tin, 16>);
+            else gs(mode_product_fibre_split_kernel<Tin, 32>);
+            MB_LAUNCH(ctx, sum_chunks_kernel, grid_for(total), 256, 0, part.get(), nc, total, out);
             return;
         }
         if (J <= 8) go(mode_product_fibre_kernel<Tin, 8>);

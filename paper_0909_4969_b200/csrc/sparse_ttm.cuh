@@ -242,6 +242,9 @@ void dense_mode_product(Ctx* ctx, const Tin* in, const std::vector<int>& dims, i
 // dense mode-n Gram X_(n) X_(n)^T on tcgen05 (gram_tc.cu), read in place
 bool gram_tc_applies(const std::vector<int>& dims, int n);
 void gram_tc(Ctx* ctx, const float* x, const std::vector<int>& dims, int n, double* G);
+// dense mode product out = x x_m U^T (U: I_m x r fp64, r <= 32) on tcgen05, 3xTF32 (ttm_tc.cu)
+bool ttm_tc_applies(const std::vector<int>& dims, int m, int r);
+void ttm_tc(Ctx* ctx, const float* x, const std::vector<int>& dims, int m, const double* U, int r, double* out);
 template <typename Tin, typename Tout>
 void dense_matricize(Ctx* ctx, const Tin* in, const std::vector<int>& dims, int mode, Tout* out);
 template <typename T>

@@ -297,6 +297,35 @@ DBuf<double> project_dense(Ctx* ctx, const T* x, const std::vector<int>& dims, c
     return y;
 }
 
+// Continue a projection chain: contract y (dims cur, fp64) over every mode
+// not in `done` and != skip, ascending (products commute: equal to the
+// reference's project_except order up to rounding).
+// y0 is read, not consumed (it may be a buffer reused across modes).
+DBuf<double> chain_rest(Ctx* ctx, const double* y0, std::vector<int> cur, const std::vector<int>& ranks,
+                        const std::vector<DBuf<double>>& U, int skip, const std::vector<bool>& done,
+                        std::vector<int>& out_dims) {
+    const int d = static_cast<int>(cur.size());
+    DBuf<double> y;
+    const double* src = y0;
+    for (int m = 0; m < d; ++m) {
+        if (m == skip || done[static_cast<std::size_t>(m)]) continue;
+        std::vector<int> nd = cur;
+        nd[static_cast<std::size_t>(m)] = ranks[static_cast<std::size_t>(m)];
+        DBuf<double> z(ctx, static_cast<std::size_t>(checked_size(nd)));
+        dense_mode_product<double>(ctx, src, cur, m, U[static_cast<std::size_t>(m)].get(),
+                                   ranks[static_cast<std::size_t>(m)], true, z.get());
+        y = std::move(z);
+        src = y.get();
+        cur = nd;
+    }
+    if (src == y0) {  // nothing left to contract: a copy
+        y.alloc(ctx, static_cast<std::size_t>(checked_size(cur)));
+        MB_CUDA(cudaMemcpyAsync(y.get(), y0, y.n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    out_dims = cur;
+    return y;
+}
+
 std::vector<double> download(Ctx* ctx, const DBuf<double>& b) {
     std::vector<double> h(b.n);
     to_host(ctx, h.data(), b.get(), b.n);
@@ -435,9 +464,57 @@ struct DenseSession : SessionBase {
     long long numel = 0;
     DBuf<double> core;
 
+    // fp32 tensors of supported shape: the streaming first contraction of each
+    // projection runs on the tensor cores (ttm_tc.cu, 3xTF32), and the mode-0
+    // projection Z0 = X x_0 U_0^T is formed once per sweep (right after U_0's
+    // update) and reused by every later mode and the core — a dimension tree
+    // with two passes over X per sweep instead of d + 1.
+    bool tc0 = false, tc1 = false;
+    DBuf<double> z0;
+    std::vector<int> z0dims;
+    bool z0_valid = false;  // Z0 formed with the current U_0
+    void form_z0() {
+        z0_valid = true;
+        z0dims = dims;
+        z0dims[0] = ranks[0];
+        z0.alloc(ctx, static_cast<std::size_t>(checked_size(z0dims)));
+        if constexpr (std::is_same_v<T, float>) ttm_tc(ctx, x, dims, 0, fs.U[0].get(), ranks[0], z0.get());
+    }
+    DBuf<double> project_tc(int skip, std::vector<int>& od) {
+        std::vector<bool> done(static_cast<std::size_t>(d), false);
+        if (skip != 0) {  // from Z0
+            done[0] = true;
+            return chain_rest(ctx, z0.get(), z0dims, ranks, fs.U, skip, done, od);
+        }
+        // mode 0's update: contract mode 1 first on the tensor cores
+        std::vector<int> cur = dims;
+        cur[1] = ranks[1];
+        DBuf<double> y(ctx, static_cast<std::size_t>(checked_size(cur)));
+        if constexpr (std::is_same_v<T, float>) ttm_tc(ctx, x, dims, 1, fs.U[1].get(), ranks[1], y.get());
+        done[1] = true;
+        return chain_rest(ctx, y.get(), cur, ranks, fs.U, 0, done, od);
+    }
     double core_and_fit() {
         std::vector<int> cd;
-        core = project_dense<T>(ctx, x, dims, ranks, fs.U, -1, cd);
+        if (tc0) {
+            if (!z0_valid) form_z0();  // HOSVD: U_0 final now (a sweep formed it after U_0's update)
+            std::vector<bool> done(static_cast<std::size_t>(d), false);
+            done[0] = true;
+            core = chain_rest(ctx, z0.get(), z0dims, ranks, fs.U, -1, done, cd);
+            // |X - X_hat|^2 = |X|^2 - |G|^2 (orthonormal factors, G the projection
+            // by the final factors; every term fp64 from exactly represented fp32
+            // data and ~2^-22-accurate products); the reference's entrywise form
+            // (tucker.cpp:47-50) only when the model is near exact (the
+            // difference then cancels: residual below 1e-3 of |X|)
+            sumsq<double>(ctx, core.get(), static_cast<long long>(core.n), fs.red.get(), fs.scal.get() + 1);
+            double sc[2];
+            to_host(ctx, sc, fs.scal.get(), 2);
+            sync(ctx);
+            const double e2 = sc[0] - sc[1];
+            if (e2 > 1e-6 * sc[0]) return fit_from(sc[0], e2);
+        } else {
+            core = project_dense<T>(ctx, x, dims, ranks, fs.U, -1, cd);
+        }
         DBuf<double> rec = reconstruct_dev(ctx, core.get(), ranks, dims, fs.U);
         sumsq_diff<T>(ctx, x, rec.get(), numel, fs.red.get(), fs.scal.get() + 2);
         double sc[3];
@@ -449,6 +526,10 @@ struct DenseSession : SessionBase {
         init_common(c, dm, rk);
         x = data;
         numel = checked_size(dims);
+        if constexpr (std::is_same_v<T, float>) {
+            tc0 = d >= 2 && ttm_tc_applies(dims, 0, ranks[0]);
+            tc1 = tc0 && ttm_tc_applies(dims, 1, ranks[1]);
+        }
         Timer tm(ctx);
         tm.start();
         sumsq<T>(ctx, x, numel, fs.red.get(), fs.scal.get());
@@ -479,9 +560,10 @@ struct DenseSession : SessionBase {
         sweep_fits.assign(1, fit);
     }
     void sweep() override {
+        z0_valid = false;
         for (int i = 0; i < d; ++i) {
             std::vector<int> yd;
-            DBuf<double> y = project_dense<T>(ctx, x, dims, ranks, fs.U, i, yd);
+            DBuf<double> y = (tc0 && (i > 0 || tc1)) ? project_tc(i, yd) : project_dense<T>(ctx, x, dims, ranks, fs.U, i, yd);
             const int rows = dims[static_cast<std::size_t>(i)];
             const long long cols = checked_size(yd) / rows;
             DBuf<double> ym(ctx, y.n);
@@ -489,6 +571,7 @@ struct DenseSession : SessionBase {
             lsb_device<double>(ctx, ym.get(), rows, cols, ranks[static_cast<std::size_t>(i)],
                                fs.U[static_cast<std::size_t>(i)].get(), sv_at(i), fs.st.get() + 3 * i,
                                &warm[static_cast<std::size_t>(i)], fs.U[static_cast<std::size_t>(i)].get());
+            if (i == 0 && tc0) form_z0();  // reused by modes 1.. and the core
         }
         warnings = read_warnings(ctx, fs.st, ranks, all);
         fit = core_and_fit();
@@ -1132,7 +1215,10 @@ mach_dense* mode_product_dev(Ctx* ctx, const mach_dense* t, const mach_sparse* s
     out->numel = checked_size(od);
     DBuf<double> y(ctx, static_cast<std::size_t>(out->numel));
     if (t) {
-        if (t->dtype == MACH_F32) dense_mode_product<float>(ctx, static_cast<const float*>(t->data), dims, mode, U.get(), rows, true, y.get());
+        // fp32 tensors stream through the tensor cores (3xTF32, ~1e-7 relative)
+        if (t->dtype == MACH_F32 && ttm_tc_applies(dims, mode, rows))
+            ttm_tc(ctx, static_cast<const float*>(t->data), dims, mode, U.get(), rows, y.get());
+        else if (t->dtype == MACH_F32) dense_mode_product<float>(ctx, static_cast<const float*>(t->data), dims, mode, U.get(), rows, true, y.get());
         else dense_mode_product<double>(ctx, static_cast<const double*>(t->data), dims, mode, U.get(), rows, true, y.get());
     } else {
         DBuf<double> dn(ctx, static_cast<std::size_t>(s->numel));

@@ -84,3 +84,17 @@ def test_dense_hooi_fp32_tensor_cores_match_oracle(mb):
     assert np.abs(np.array(dev.sweep_fits[:n]) - np.array(ref.sweep_fits[:n])).max() <= 1e-4
     core = align_core(dev.core, dev.factors, ref.factors)
     assert rel(core, ref.core) <= 1e-4
+
+
+@pytest.mark.parametrize("dims,mode,r", [((256, 64, 80), 0, 16), ((256, 64, 80), 1, 10), ((256, 64, 80), 2, 16),
+                                          ((130, 50, 300), 1, 32), ((200, 33, 257), 0, 5), ((512, 40, 70), 2, 24)])
+def test_mode_product_tf32x3_matches_fp64(mb, dims, mode, r):
+    """x_m U^T on tcgen05 with 3xTF32 (ttm_tc.cu) against numpy fp64: the
+    split keeps ~2^-22 relative accuracy per product (no truncation bias)."""
+    rng = np.random.default_rng(sum(dims) + mode + r)
+    x = rng.standard_normal(dims).astype(np.float32)
+    m = rng.standard_normal((r, dims[mode]))
+    got = mb.mode_product(mb.DenseTensor.from_numpy(x), m, mode)
+    ref = np.moveaxis(np.tensordot(m, x.astype(np.float64), axes=([1], [mode])), 0, mode)
+    scale = np.sqrt(dims[mode])  # typical magnitude of an output entry
+    assert np.abs(got - ref).max() <= 2e-6 * scale, np.abs(got - ref).max() / scale
