@@ -28,6 +28,9 @@
 // the contraction (scripts/ttm_tc_err.py measures both variants).
 // Output fp64 (the rest of the chain runs in fp64).
 //
+// Shared memory: an 8-deep TMA ring (A tile, B hi, B lo; 20 KB at NB = 16)
+// and a 3-slot ring of A lo planes.
+//
 // Persistent CTAs (one per SM), warp roles (320 threads):
 //   warp 0   TMA producer (elected lane): A tile + both B planes per stage
 //   warp 1   TMEM allocator, MMA issuer (elected lane): 4 k-steps x 3 MMAs
@@ -49,15 +52,19 @@ namespace {
 
 constexpr int XBM = 128;  // rows per tile (UMMA M)
 constexpr int XBK = 32;   // K per stage (128 B of fp32)
-constexpr int XST = 4;    // stages
+constexpr int XLO = 3;    // lo-plane slots (converter -> MMA)
 constexpr int kXThreads = 320;
 constexpr uint32_t kXA = XBM * XBK * 4;  // 16 KB
 
 template <int NB>
 struct XL {
     static constexpr uint32_t B = NB * XBK * 4;              // one B plane per stage
-    static constexpr uint32_t stage = 2 * kXA + 2 * B;       // A (hi in place), A lo, B hi, B lo
-    static constexpr std::size_t smem = static_cast<std::size_t>(XST) * stage + 1024 /*align*/ + 1024 /*barriers*/;
+    static constexpr uint32_t stage = kXA + 2 * B;           // TMA stage: A (hi written in place), B hi, B lo
+    // TMA ring as deep as shared memory allows (bytes in flight per SM set
+    // the streaming rate); the lo planes live in a short ring of their own
+    static constexpr int XST = NB <= 16 ? 8 : 7;
+    static constexpr std::size_t smem =
+        static_cast<std::size_t>(XST) * stage + static_cast<std::size_t>(XLO) * kXA + 1024 /*align*/ + 1024 /*barriers*/;
     static constexpr uint32_t tmem_cols = 256;
     static constexpr int nbuf = 256 / (4 * NB);  // TMEM ring of per-stage slots (4 k-step accumulators each)
 };
@@ -141,14 +148,17 @@ template <bool MN, int NB>
 __global__ void __launch_bounds__(kXThreads, 1)
     ttm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tbh,
                   const __grid_constant__ CUtensorMap tbl, long long inner, int len, long long outer, int r,
-                  double* __restrict__ out) {
+                  double* __restrict__ out, int dbg) {
     using L = XL<NB>;
     extern __shared__ __align__(1024) unsigned char xsm_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(xsm_raw) + 1023) & ~std::uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + XST * L::stage);
-    uint64_t* conv = full + XST;
-    uint64_t* empty = conv + XST;
-    uint64_t* ready = empty + XST;      // [nbuf] the stage's k-step products are in the TMEM slot
+    constexpr int XST = L::XST;
+    unsigned char* losm = sm + XST * L::stage;  // XLO lo planes
+    uint64_t* full = reinterpret_cast<uint64_t*>(losm + XLO * kXA);
+    uint64_t* empty = full + XST;
+    uint64_t* conv = empty + XST;    // [XLO] lo plane c written (and hi in place)
+    uint64_t* lofree = conv + XLO;   // [XLO] MMAs reading lo plane c done
+    uint64_t* ready = lofree + XLO;  // [nbuf] the stage's k-step products are in the TMEM slot
     uint64_t* drained = ready + L::nbuf;  // [nbuf] the epilogue has read the slot
     uint32_t* tslot = reinterpret_cast<uint32_t*>(drained + L::nbuf);
 
@@ -160,8 +170,11 @@ __global__ void __launch_bounds__(kXThreads, 1)
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < XST; ++s) {
             bar_init(&full[s], 1);
-            bar_init(&conv[s], 4);
             bar_init(&empty[s], 1);
+        }
+        for (int c = 0; c < XLO; ++c) {
+            bar_init(&conv[c], 4);
+            bar_init(&lofree[c], 1);
         }
         for (int b = 0; b < L::nbuf; ++b) {
             bar_init(&ready[b], 1);
@@ -192,7 +205,7 @@ __global__ void __launch_bounds__(kXThreads, 1)
                     const long long u = it / XST;
                     if (u > 0) bar_wait(&empty[s], static_cast<uint32_t>((u - 1) & 1));
                     unsigned char* a = sm + s * L::stage;
-                    unsigned char* bh = a + 2 * kXA;
+                    unsigned char* bh = a + kXA;
                     unsigned char* bl = bh + L::B;
                     bar_tx(&full[s], kXA + 2 * L::B);
                     if constexpr (MN) {
@@ -215,11 +228,13 @@ __global__ void __launch_bounds__(kXThreads, 1)
             for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 for (int ks = 0; ks < nks; ++ks, ++it) {
                     const int s = static_cast<int>(it % XST);
+                    const int cl = static_cast<int>(it % XLO);
                     const int b = static_cast<int>(it % L::nbuf);
-                    bar_wait(&conv[s], static_cast<uint32_t>((it / XST) & 1));
+                    bar_wait(&conv[cl], static_cast<uint32_t>((it / XLO) & 1));
                     if (it >= L::nbuf) bar_wait(&drained[b], static_cast<uint32_t>(((it / L::nbuf) - 1) & 1));
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t ah = s32(sm + s * L::stage), al = ah + kXA, bh = al + kXA, bl = bh + L::B;
+                    const uint32_t ah = s32(sm + s * L::stage), bh = ah + kXA, bl = bh + L::B;
+                    const uint32_t al = s32(losm + cl * kXA);
 #pragma unroll
                     for (int k = 0; k < XBK / 8; ++k) {
                         const uint32_t d = tmem + static_cast<uint32_t>((4 * b + k) * NB);  // fresh accumulator per k-step
@@ -237,6 +252,7 @@ __global__ void __launch_bounds__(kXThreads, 1)
                         mma_tf32(d, dal, dbh, idesc, 1u);
                     }
                     mma_commit(&empty[s]);
+                    mma_commit(&lofree[cl]);
                     mma_commit(&ready[b]);
                 }
             }
@@ -248,11 +264,14 @@ __global__ void __launch_bounds__(kXThreads, 1)
         for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
             for (int ks = 0; ks < nks; ++ks, ++it) {
                 const int s = static_cast<int>(it % XST);
+                const int cl = static_cast<int>(it % XLO);
                 bar_wait(&full[s], static_cast<uint32_t>((it / XST) & 1));
+                if (it >= XLO) bar_wait(&lofree[cl], static_cast<uint32_t>(((it / XLO) - 1) & 1));
                 float4* hi = reinterpret_cast<float4*>(sm + s * L::stage);
-                float4* lo = reinterpret_cast<float4*>(sm + s * L::stage + kXA);
+                float4* lo = reinterpret_cast<float4*>(losm + cl * kXA);
 #pragma unroll
                 for (int q = 0; q < static_cast<int>(kXA / 16) / 128; ++q) {
+                    if (dbg & 1) break;  // timing probe: no conversion (results wrong)
                     const int e = ct + 128 * q;
                     float4 v = hi[e], h, l;
                     h.x = rn_tf32(v.x); h.y = rn_tf32(v.y); h.z = rn_tf32(v.z); h.w = rn_tf32(v.w);
@@ -262,7 +281,7 @@ __global__ void __launch_bounds__(kXThreads, 1)
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                if (lane == 0) bar_arrive(&conv[s]);
+                if (lane == 0) bar_arrive(&conv[cl]);
             }
         }
     } else {
@@ -280,6 +299,11 @@ __global__ void __launch_bounds__(kXThreads, 1)
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t base = tmem + (static_cast<uint32_t>(32 * q4) << 16) + static_cast<uint32_t>(4 * b * NB);
                 float v[4][NB];
+                if (dbg & 2) {  // timing probe: no TMEM reads (results wrong)
+                    __syncwarp();
+                    if (lane == 0) bar_arrive(&drained[b]);
+                    continue;
+                }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) tmem_ld_issue<NB>(base + k * NB, v[k]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -381,7 +405,8 @@ void launch_ttm_tc(Ctx* ctx, const CUtensorMap& ta, const float* uh, const float
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
     const int grid = static_cast<int>(std::min<long long>(ntiles, nsm));
-    MB_LAUNCH(ctx, (ttm_tc_kernel<MN, NB>), grid, kXThreads, XL<NB>::smem, ta, tbh, tbl, inner, len, outer, r, out);
+    static const int dbg = std::getenv("MACH_TTM_TC_DBG") ? std::atoi(std::getenv("MACH_TTM_TC_DBG")) : 0;
+    MB_LAUNCH(ctx, (ttm_tc_kernel<MN, NB>), grid, kXThreads, XL<NB>::smem, ta, tbh, tbl, inner, len, outer, r, out, dbg);
 }
 
 }  // namespace
