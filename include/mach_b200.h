@@ -186,6 +186,14 @@ mach_status mach_reconstruct(mach_ctx* ctx, const mach_model* m, mach_dense** ou
 mach_status mach_left_singular_basis(mach_ctx* ctx, int rows, int cols, const double* a, int k,
                                      double* basis, double* sv, int* numerical_rank,
                                      int* completed);
+/* truncated_svd (linalg.hpp:23): top-k singular triplets of a host
+ * column-major rows x cols fp64 matrix, 1 <= k <= min(rows, cols); left
+ * rows x k, sv k, right cols x k (caller-allocated), reference sign rule.   */
+mach_status mach_truncated_svd(mach_ctx* ctx, int rows, int cols, const double* a, int k,
+                               double* left, double* sv, double* right);
+/* low_rank_approx (linalg.hpp:29): left diag(sv) right^T, rows x cols       */
+mach_status mach_low_rank_approx(mach_ctx* ctx, int rows, int cols, const double* a, int k,
+                                 double* out);
 /* mode_product(DenseTensor / SparseTensor, Matrix, mode) -> new dense fp64   */
 mach_status mach_mode_product_dense(mach_ctx* ctx, const mach_dense* t, int rows, int cols,
                                     const double* m, int mode, mach_dense** out);

@@ -99,6 +99,7 @@ def lib():
         L.orc_jacobi_eig.argtypes = [C.c_int, _dp, _dp, _dp]
         L.orc_left_singular_basis.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _dp, _dp, _ip, _ip]
         L.orc_low_rank_approx.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _dp]
+        L.orc_truncated_svd.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _dp, _dp, _dp]
         L.orc_reconstruct.argtypes = [C.c_void_p, _dp]
         L.orc_last_error.argtypes = [C.c_char_p, C.c_int]
         L.orc_phase_times.argtypes = [_dp, _dp, _dp, C.c_int, _ip]
@@ -367,6 +368,18 @@ def left_singular_basis(m: np.ndarray, k: int):
     _check(lib().orc_left_singular_basis(rows, cols, _d(flat), int(k), _d(basis), _d(sv), C.byref(nr),
                                          C.byref(comp)))
     return basis.reshape((rows, k), order="F"), sv[:k].copy(), nr.value, bool(comp.value)
+
+
+def truncated_svd(m: np.ndarray, k: int):
+    """(left rows x k, singular values k, right cols x k) — linalg.cpp:301-305."""
+    m = np.asarray(m, dtype=np.float64)
+    rows, cols = m.shape
+    left = np.empty(max(rows * k, 1))
+    right = np.empty(max(cols * k, 1))
+    sv = np.empty(max(k, 1))
+    flat = np.ascontiguousarray(m.reshape(-1, order="F"))
+    _check(lib().orc_truncated_svd(rows, cols, _d(flat), int(k), _d(left), _d(sv), _d(right)))
+    return left[: rows * k].reshape((rows, k), order="F"), sv[:k].copy(), right[: cols * k].reshape((cols, k), order="F")
 
 
 def low_rank_approx(m: np.ndarray, k: int) -> np.ndarray:

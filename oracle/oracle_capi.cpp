@@ -153,6 +153,14 @@ int orc_left_singular_basis(int rows, int cols, const double* a, int k, double* 
         *completed = b.completed ? 1 : 0;
     });
 }
+int orc_truncated_svd(int rows, int cols, const double* a, int k, double* left, double* sv, double* right) {
+    return guard([&] {
+        Svd r = truncated_svd(mk_mat(rows, cols, a), k);
+        std::memcpy(left, r.left.v.data(), r.left.v.size() * sizeof(double));
+        std::memcpy(sv, r.sv.data(), r.sv.size() * sizeof(double));
+        std::memcpy(right, r.right.v.data(), r.right.v.size() * sizeof(double));
+    });
+}
 int orc_low_rank_approx(int rows, int cols, const double* a, int k, double* out) {
     return guard([&] {
         Mat r = low_rank_approx(mk_mat(rows, cols, a), k);

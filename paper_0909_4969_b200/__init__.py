@@ -18,14 +18,18 @@ from .api import (  # noqa: F401
     ShapeError,
     SparseTensor,
     SparsifyConfig,
+    TruncatedSvd,
     TuckerModel,
+    truncated_svd,
     accuracy,
     default_context,
     hooi,
     kernel_stats,
     profile,
     hosvd,
+    leading_left_singular_vectors,
     left_singular_basis,
+    low_rank_approx,
     mach_hooi,
     mach_hosvd,
     mode_gram,

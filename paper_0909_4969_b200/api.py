@@ -448,6 +448,42 @@ def mode_gram(t, mode: int, ctx: Context | None = None):
 
 
 @dataclass
+class TruncatedSvd:
+    left: np.ndarray
+    singular_values: np.ndarray
+    right: np.ndarray
+
+
+def truncated_svd(m: np.ndarray, k: int, ctx: Context | None = None) -> TruncatedSvd:
+    """linalg.hpp:23 — top-k singular triplets (reference sign rule), on the device."""
+    m = np.asarray(m, dtype=np.float64)
+    rows, cols = m.shape
+    c = _ctx(ctx)
+    kk = max(int(k), 1)
+    left, sv, right = np.empty(rows * kk), np.empty(kk), np.empty(cols * kk)
+    flat = np.ascontiguousarray(m.reshape(-1, order="F"))
+    _check(L.lib().mach_truncated_svd(c.h, rows, cols, flat.ctypes.data_as(L.dp), int(k), left.ctypes.data_as(L.dp),
+                                      sv.ctypes.data_as(L.dp), right.ctypes.data_as(L.dp)))
+    return TruncatedSvd(left.reshape((rows, kk), order="F"), sv, right.reshape((cols, kk), order="F"))
+
+
+def leading_left_singular_vectors(m: np.ndarray, k: int, ctx: Context | None = None) -> np.ndarray:
+    """linalg.hpp:26 — the left factor of truncated_svd."""
+    return truncated_svd(m, k, ctx).left
+
+
+def low_rank_approx(m: np.ndarray, k: int, ctx: Context | None = None) -> np.ndarray:
+    """linalg.hpp:29 — left diag(sv) right^T of truncated_svd, on the device."""
+    m = np.asarray(m, dtype=np.float64)
+    rows, cols = m.shape
+    c = _ctx(ctx)
+    out = np.empty(rows * cols)
+    flat = np.ascontiguousarray(m.reshape(-1, order="F"))
+    _check(L.lib().mach_low_rank_approx(c.h, rows, cols, flat.ctypes.data_as(L.dp), int(k), out.ctypes.data_as(L.dp)))
+    return out.reshape((rows, cols), order="F")
+
+
+@dataclass
 class LeftSingularBasis:
     basis: np.ndarray
     singular_values: np.ndarray

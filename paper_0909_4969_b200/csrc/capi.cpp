@@ -1,6 +1,7 @@
 // C ABI of libmach_b200 (include/mach_b200.h).  Every entry point catches,
 // maps the error to a mach_status and stores the message thread-locally; no
 // exception crosses the boundary.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -57,6 +58,20 @@ std::vector<int> dims_of(int order, const int* dims) {
 void need(const void* p, const char* what) {
     if (!p) throw_arg(std::string(what) + " must not be null");
 }
+
+// Makes the handle's device current for the call and restores the caller's
+// afterwards: handles on different GPUs can be used from one thread, and a
+// caller (e.g. torch) may have switched devices in between.
+struct DevGuard {
+    int prev = -1, dev = -1;
+    explicit DevGuard(int d) : dev(d) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) MB_CUDA(cudaSetDevice(dev));
+    }
+    ~DevGuard() {
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+};
 }  // namespace
 
 extern "C" {
@@ -97,6 +112,7 @@ mach_status mach_ctx_destroy(mach_ctx* ctx) {
 mach_status mach_ctx_set_stream(mach_ctx* ctx, void* stream) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         MB_CUDA(cudaStreamSynchronize(ctx->c.stream));
         if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
         if (stream) {
@@ -112,6 +128,7 @@ mach_status mach_ctx_set_stream(mach_ctx* ctx, void* stream) {
 mach_status mach_ctx_synchronize(mach_ctx* ctx) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         sync(&ctx->c);
     });
 }
@@ -119,6 +136,7 @@ mach_status mach_ctx_synchronize(mach_ctx* ctx) {
 mach_status mach_ctx_launch_count(mach_ctx* ctx, int64_t* out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         *out = ctx->c.launches;
     });
 }
@@ -128,6 +146,7 @@ mach_status mach_dense_upload(mach_ctx* ctx, mach_dtype dtype, int order, const 
                               mach_dense** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(out, "out");
         auto t = std::make_unique<mach_dense>();
         t->ctx = &ctx->c;
@@ -147,6 +166,7 @@ mach_status mach_dense_upload(mach_ctx* ctx, mach_dtype dtype, int order, const 
 mach_status mach_dense_wrap(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims, void* dev, mach_dense** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(out, "out");
         need(dev, "device_ptr");
         auto t = std::make_unique<mach_dense>();
@@ -163,6 +183,7 @@ mach_status mach_dense_wrap(mach_ctx* ctx, mach_dtype dtype, int order, const in
 mach_status mach_dense_download(const mach_dense* t, void* host) {
     return guard([&] {
         need(t, "tensor");
+        DevGuard dg_(t->ctx->device);
         need(host, "host");
         MB_CUDA(cudaMemcpyAsync(host, t->data, static_cast<std::size_t>(t->numel) * dtype_size(t->dtype),
                                 cudaMemcpyDeviceToHost, t->ctx->stream));
@@ -182,6 +203,7 @@ mach_status mach_dense_free(mach_dense* t) {
 mach_status mach_sparsify(mach_ctx* ctx, const mach_dense* x, double p, uint64_t seed, mach_sparse** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(x, "tensor");
         need(out, "out");
         *out = sample_dense(x, p, seed);
@@ -192,6 +214,7 @@ mach_status mach_sparsify_slab(mach_ctx* ctx, const mach_dense* slab, int order,
                                int64_t offset, double p, uint64_t seed, mach_sparse** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(slab, "slab");
         need(out, "out");
         *out = sample_slab(slab, dims_of(order, global_dims), offset, p, seed);
@@ -201,6 +224,7 @@ mach_status mach_sparsify_slab(mach_ctx* ctx, const mach_dense* slab, int order,
 mach_status mach_sparse_device_view(const mach_sparse* s, void** idx, void** vals, int* idx_bytes) {
     return guard([&] {
         need(s, "tensor");
+        DevGuard dg_(s->ctx->device);
         if (idx) *idx = s->idx;
         if (vals) *vals = s->val;
         if (idx_bytes) *idx_bytes = s->idx64 ? 8 : 4;
@@ -211,6 +235,7 @@ mach_status mach_sparse_from_device(mach_ctx* ctx, mach_dtype dtype, int order, 
                                     const void* idx, const void* vals, mach_sparse** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(out, "out");
         if (nnz < 0) throw_arg("nnz must be >= 0");
         auto t = std::make_unique<mach_sparse>();
@@ -261,6 +286,7 @@ mach_status mach_sparse_upload(mach_ctx* ctx, mach_dtype dtype, int order, const
                                const int64_t* idx, const double* vals, mach_sparse** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(out, "out");
         if (nnz < 0) throw_arg("nnz must be >= 0");
         if (nnz > 0) {
@@ -274,6 +300,7 @@ mach_status mach_sparse_upload(mach_ctx* ctx, mach_dtype dtype, int order, const
 mach_status mach_sparse_nnz(const mach_sparse* s, int64_t* nnz) {
     return guard([&] {
         need(s, "tensor");
+        DevGuard dg_(s->ctx->device);
         *nnz = s->nnz;
     });
 }
@@ -281,6 +308,7 @@ mach_status mach_sparse_nnz(const mach_sparse* s, int64_t* nnz) {
 mach_status mach_sparse_download(const mach_sparse* s, int64_t* idx, double* vals) {
     return guard([&] {
         need(s, "tensor");
+        DevGuard dg_(s->ctx->device);
         sparse_to_host(s, idx, vals);
     });
 }
@@ -300,6 +328,7 @@ static std::vector<int> ranks_of(int order, const int* ranks) {
 mach_status mach_hosvd_sparse(mach_ctx* ctx, const mach_sparse* t, const int* ranks, mach_model** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(t, "tensor");
         need(out, "out");
         *out = tucker_sparse(const_cast<mach_sparse*>(t), ranks_of(static_cast<int>(t->dims.size()), ranks), false, 1, 0.0);
@@ -309,6 +338,7 @@ mach_status mach_hosvd_sparse(mach_ctx* ctx, const mach_sparse* t, const int* ra
 mach_status mach_hosvd_dense(mach_ctx* ctx, const mach_dense* t, const int* ranks, mach_model** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(t, "tensor");
         need(out, "out");
         *out = tucker_dense(t, ranks_of(static_cast<int>(t->dims.size()), ranks), false, 1, 0.0);
@@ -319,6 +349,7 @@ mach_status mach_hooi_sparse(mach_ctx* ctx, const mach_sparse* t, const int* ran
                              double fit_tolerance, mach_model** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(t, "tensor");
         need(out, "out");
         *out = tucker_sparse(const_cast<mach_sparse*>(t), ranks_of(static_cast<int>(t->dims.size()), ranks), true,
@@ -330,6 +361,7 @@ mach_status mach_hooi_dense(mach_ctx* ctx, const mach_dense* t, const int* ranks
                             double fit_tolerance, mach_model** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(t, "tensor");
         need(out, "out");
         *out = tucker_dense(t, ranks_of(static_cast<int>(t->dims.size()), ranks), true, max_iterations, fit_tolerance);
@@ -445,6 +477,7 @@ mach_status mach_model_free(mach_model* m) {
 mach_status mach_accuracy(mach_ctx* ctx, const mach_dense* t, const mach_model* m, double* out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(t, "tensor");
         need(m, "model");
         *out = accuracy_dev(t, m);
@@ -454,6 +487,7 @@ mach_status mach_accuracy(mach_ctx* ctx, const mach_dense* t, const mach_model* 
 mach_status mach_reconstruct(mach_ctx* ctx, const mach_model* m, mach_dense** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(m, "model");
         *out = reconstruct_model(&ctx->c, m);
     });
@@ -463,7 +497,50 @@ mach_status mach_left_singular_basis(mach_ctx* ctx, int rows, int cols, const do
                                      int* numerical_rank, int* completed) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         lsb_host(&ctx->c, rows, cols, a, k, basis, sv, numerical_rank, completed);
+    });
+}
+
+mach_status mach_truncated_svd(mach_ctx* ctx, int rows, int cols, const double* a, int k, double* left, double* sv,
+                               double* right) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
+        need(a, "matrix");
+        need(left, "left");
+        need(sv, "singular_values");
+        need(right, "right");
+        if (rows < 1 || cols < 1) throw_arg("matrix must be nonempty");
+        if (k < 1 || k > std::min(rows, cols)) throw_arg("k must satisfy 1 <= k <= min(rows, cols)");
+        Ctx* c = &ctx->c;
+        DBuf<double> A(c, static_cast<std::size_t>(rows) * cols), L(c, static_cast<std::size_t>(rows) * k),
+            S(c, static_cast<std::size_t>(k)), R(c, static_cast<std::size_t>(cols) * k);
+        to_device(c, A.get(), a, A.n);
+        truncated_svd_dev(c, A.get(), rows, cols, k, L.get(), S.get(), R.get());
+        to_host(c, left, L.get(), L.n);
+        to_host(c, sv, S.get(), S.n);
+        to_host(c, right, R.get(), R.n);
+        sync(c);
+    });
+}
+
+mach_status mach_low_rank_approx(mach_ctx* ctx, int rows, int cols, const double* a, int k, double* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
+        need(a, "matrix");
+        need(out, "out");
+        if (rows < 1 || cols < 1) throw_arg("matrix must be nonempty");
+        if (k < 1 || k > std::min(rows, cols)) throw_arg("k must satisfy 1 <= k <= min(rows, cols)");
+        Ctx* c = &ctx->c;
+        DBuf<double> A(c, static_cast<std::size_t>(rows) * cols), L(c, static_cast<std::size_t>(rows) * k),
+            S(c, static_cast<std::size_t>(k)), R(c, static_cast<std::size_t>(cols) * k);
+        to_device(c, A.get(), a, A.n);
+        truncated_svd_dev(c, A.get(), rows, cols, k, L.get(), S.get(), R.get());
+        low_rank_dev(c, L.get(), S.get(), R.get(), rows, cols, k, A.get());
+        to_host(c, out, A.get(), A.n);
+        sync(c);
     });
 }
 
@@ -471,6 +548,7 @@ mach_status mach_mode_product_dense(mach_ctx* ctx, const mach_dense* t, int rows
                                     mach_dense** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(t, "tensor");
         *out = mode_product_dev(&ctx->c, t, nullptr, rows, cols, m, mode);
     });
@@ -480,6 +558,7 @@ mach_status mach_mode_product_sparse(mach_ctx* ctx, const mach_sparse* t, int ro
                                      mach_dense** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(t, "tensor");
         *out = mode_product_dev(&ctx->c, nullptr, t, rows, cols, m, mode);
     });
@@ -488,6 +567,7 @@ mach_status mach_mode_product_sparse(mach_ctx* ctx, const mach_sparse* t, int ro
 mach_status mach_dense_mode_gram(mach_ctx* ctx, const mach_dense* t, int mode, double* host, int* tensor_cores) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(t, "tensor");
         need(host, "host");
         if (mode < 0 || mode >= static_cast<int>(t->dims.size())) throw_arg("mode out of range");
@@ -547,6 +627,7 @@ extern "C" {
 mach_status mach_hooi_begin(mach_ctx* ctx, const mach_sparse* t, const int* ranks, mach_session** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(t, "tensor");
         need(out, "out");
         auto h = std::make_unique<mach_session>();
@@ -558,6 +639,7 @@ mach_status mach_hooi_begin(mach_ctx* ctx, const mach_sparse* t, const int* rank
 mach_status mach_hooi_begin_dense(mach_ctx* ctx, const mach_dense* t, const int* ranks, mach_session** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(t, "tensor");
         need(out, "out");
         auto h = std::make_unique<mach_session>();
@@ -588,6 +670,7 @@ mach_status mach_hooi_begin_from(mach_ctx* ctx, const mach_sparse* t, const int*
                                  mach_session** out) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         need(t, "tensor");
         need(init, "init");
         need(out, "out");
@@ -657,6 +740,7 @@ mach_status mach_session_free(mach_session* s) {
 mach_status mach_ctx_profile(mach_ctx* ctx, int enable) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         ctx->c.resolve();
         ctx->c.profile = enable != 0;
         if (enable) ctx->c.stats.clear();
@@ -666,6 +750,7 @@ mach_status mach_ctx_profile(mach_ctx* ctx, int enable) {
 mach_status mach_ctx_kernel_stat(mach_ctx* ctx, int i, char* name, size_t len, int64_t* launches, double* total_ms) {
     return guard([&] {
         need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
         ctx->c.resolve();
         if (i < 0 || i >= static_cast<int>(ctx->c.stats.size())) throw_arg("kernel index out of range");
         auto it = ctx->c.stats.begin();

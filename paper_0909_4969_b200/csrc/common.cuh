@@ -233,6 +233,15 @@ struct Split {
 };
 Split split_at(const std::vector<int>& dims, int mode);
 
+// One-time per-device setup (kernel attributes are per device): true the
+// first time `dev` is seen for this mask.
+inline bool first_on_device(std::uint64_t& mask, int dev) {
+    const std::uint64_t bit = 1ull << (static_cast<unsigned>(dev) & 63u);
+    if (mask & bit) return false;
+    mask |= bit;
+    return true;
+}
+
 inline int ceil_div(std::int64_t a, std::int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
 }  // namespace machb

@@ -235,16 +235,29 @@ Matrix transpose(const Matrix& m) {
     return t;
 }
 
+// Pairwise (cascade) summation of f(lo..hi-1) in the reference's order
+// (internal.hpp:36-46): blocks of <= 64 summed left to right, halves added,
+// so host-side norms agree with the reference bit for bit.
+template <typename F>
+double pairwise_sum(std::int64_t lo, std::int64_t hi, F&& f) {
+    const std::int64_t n = hi - lo;
+    if (n <= 64) {
+        double s = 0.0;
+        for (std::int64_t i = lo; i < hi; ++i) s += f(i);
+        return s;
+    }
+    const std::int64_t mid = lo + n / 2;
+    return pairwise_sum(lo, mid, f) + pairwise_sum(mid, hi, f);
+}
+
 double frobenius_norm(const Matrix& m) {
-    double s = 0.0;
-    for (double x : m.values()) s += x * x;
-    return std::sqrt(s);
+    const double* v = m.data();
+    return std::sqrt(pairwise_sum(0, static_cast<std::int64_t>(m.values().size()), [&](std::int64_t i) { return v[i] * v[i]; }));
 }
 
 double tensor_norm(const DenseTensor& t) {
-    double s = 0.0;
-    for (double x : t.values()) s += x * x;
-    return std::sqrt(s);
+    const double* v = t.data();
+    return std::sqrt(pairwise_sum(0, t.size(), [&](std::int64_t i) { return v[i] * v[i]; }));
 }
 
 double tensor_norm(const SparseTensor& t) {
@@ -256,9 +269,7 @@ double tensor_norm(const SparseTensor& t) {
 
 double inner_product(const DenseTensor& x, const DenseTensor& y) {
     if (x.dims() != y.dims()) throw ShapeError("inner_product requires identical shapes");
-    double s = 0.0;
-    for (std::int64_t i = 0; i < x.size(); ++i) s += x.data()[i] * y.data()[i];
-    return s;
+    return pairwise_sum(0, x.size(), [&](std::int64_t i) { return x.data()[i] * y.data()[i]; });
 }
 
 Matrix matricize(const DenseTensor& t, int mode) {
@@ -408,11 +419,10 @@ double accuracy(const DenseTensor& t, const TuckerModel& model) {
     if (nt == 0.0) throw ArgumentError("accuracy needs a reference tensor with nonzero norm");
     DenseTensor rec = reconstruct(model);
     if (rec.dims() != t.dims()) throw ShapeError("model reconstructs to a different shape");
-    double s = 0.0;
-    for (std::int64_t i = 0; i < t.size(); ++i) {
+    const double s = pairwise_sum(0, t.size(), [&](std::int64_t i) {
         const double d = t.data()[i] - rec.data()[i];
-        s += d * d;
-    }
+        return d * d;
+    });
     return 1.0 - std::sqrt(s) / nt;
 }
 
@@ -428,6 +438,28 @@ LeftSingularBasis left_singular_basis(const Matrix& m, int k) {
                                      &nr, &comp));
     out.numerical_rank = nr;
     out.completed = comp != 0;
+    return out;
+}
+
+TruncatedSvd truncated_svd(const Matrix& m, int k) {
+    if (m.rows() < 1 || m.cols() < 1) throw ArgumentError("matrix must be nonempty");
+    if (k < 1 || k > std::min(m.rows(), m.cols())) throw ArgumentError("k must satisfy 1 <= k <= min(rows, cols)");
+    TruncatedSvd out;
+    out.left = Matrix(m.rows(), k);
+    out.right = Matrix(m.cols(), k);
+    out.singular_values.assign(static_cast<std::size_t>(k), 0.0);
+    rethrow(mach_truncated_svd(ctx(), m.rows(), m.cols(), m.data(), k, out.left.data(), out.singular_values.data(),
+                               out.right.data()));
+    return out;
+}
+
+Matrix leading_left_singular_vectors(const Matrix& m, int k) { return truncated_svd(m, k).left; }
+
+Matrix low_rank_approx(const Matrix& m, int k) {
+    if (m.rows() < 1 || m.cols() < 1) throw ArgumentError("matrix must be nonempty");
+    if (k < 1 || k > std::min(m.rows(), m.cols())) throw ArgumentError("k must satisfy 1 <= k <= min(rows, cols)");
+    Matrix out(m.rows(), m.cols());
+    rethrow(mach_low_rank_approx(ctx(), m.rows(), m.cols(), m.data(), k, out.data()));
     return out;
 }
 

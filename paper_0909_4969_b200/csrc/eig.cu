@@ -385,10 +385,9 @@ std::size_t eig_work_doubles(int n, int k) {
 void eig_topk(Ctx* ctx, const double* G, int n, int k, double* work, double* V, double* sig, int* status,
               const int* skip) {
     const std::size_t smem = eig_smem_bytes(n);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::uint64_t attr_set = 0;  // per-device mask
+    if (first_on_device(attr_set, ctx->device)) {
         MB_CUDA(cudaFuncSetAttribute(eig_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_set = true;
     }
     if (smem > 227 * 1024) throw Error(MACH_ERR_INTERNAL, "eigen step too large for one CTA (n=" + std::to_string(n) + ")");
     MB_LAUNCH_PDL(ctx, eig_topk_kernel, 1, kEigThreads, smem, G, n, k, work, V, sig, status, skip);
@@ -398,10 +397,9 @@ template <typename T>
 void mb_fallback_all(Ctx* ctx, const double* Gout, int n, int k, double* work, double* V, double* sig, int* est,
                      const T* Y, int rows, double* W, double* U, double* sv, int* st, T* Ur, int rs, const int* flags) {
     const std::size_t smem = std::max(eig_smem_bytes(n), basis_smem(rows, k));
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::uint64_t attr_set = 0;  // per-device mask
+    if (first_on_device(attr_set, ctx->device)) {
         MB_CUDA(cudaFuncSetAttribute(mb_fallback_all_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_set = true;
     }
     if (smem > 227 * 1024) throw Error(MACH_ERR_INTERNAL, "eigen step too large for one CTA (n=" + std::to_string(n) + ")");
     MB_LAUNCH_PDL(ctx, mb_fallback_all_kernel<T>, 1, kEigThreads, smem, Gout, n, k, work, V, sig, est, Y, rows, W, U, sv,

@@ -314,12 +314,11 @@ bool run_large(Ctx* ctx, const std::vector<EigJob>& jobs) {
     // far inside fp64 range; the equilibrated CholQR2 absorbs the column scales)
     static const int kM = std::getenv("MACH_LG_M") ? std::atoi(std::getenv("MACH_LG_M")) : 6;
     static const int kMaxIt = std::getenv("MACH_LG_IT") ? std::atoi(std::getenv("MACH_LG_IT")) : 16;
-    static bool attr = false;
-    if (!attr) {
+    static std::uint64_t attr = 0;  // per-device mask
+    if (first_on_device(attr, ctx->device)) {
         MB_CUDA(cudaFuncSetAttribute(lg_init_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         MB_CUDA(cudaFuncSetAttribute(lg_rr_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         MB_CUDA(cudaFuncSetAttribute(lg_orth_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = true;
     }
     MB_LAUNCH(ctx, lg_pad_kernel, dim3(64, nj), 256, 0, L);
     MB_LAUNCH(ctx, lg_init_kernel<B>, nj, kThreads, smem, L);

@@ -170,11 +170,10 @@ bool launch_subspace_jobs(Ctx* ctx, std::vector<EigJob>& jobs, std::vector<DBuf<
             J.Bw = ws.back().get();
         }
     }
-    static bool attr = false;
-    if (!attr) {
+    static std::uint64_t attr = 0;  // per-device mask
+    if (first_on_device(attr, ctx->device)) {
         MB_CUDA(cudaFuncSetAttribute(eig_subspace_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kSmemCap)));
-        attr = true;
     }
     if (jobs.size() > static_cast<std::size_t>(kMaxJobs)) return false;
     EigJobs dj{};

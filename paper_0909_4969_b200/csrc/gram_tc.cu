@@ -416,11 +416,10 @@ void gram_tc(Ctx* ctx, const float* x, const std::vector<int>& dims, int n, doub
     nsplit = std::min<long long>(nsplit, std::max<long long>(1, nkt));
     nsplit = std::min<long long>(nsplit, (1ll << 31) / std::max(1, ntile) - 1);
     DBuf<float> part(ctx, static_cast<std::size_t>(nsplit) * ntile * TBM * TBN);
-    static bool attr = false;  // (one device per process in this library's tests and bench)
-    if (!attr) {
+    static std::uint64_t attr = 0;  // per-device mask
+    if (first_on_device(attr, ctx->device)) {
         MB_CUDA(cudaFuncSetAttribute(gram_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGramSmem)));
         MB_CUDA(cudaFuncSetAttribute(gram_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGramSmem)));
-        attr = true;
     }
     const long long grid = nsplit * ntile;
     if (mn)

@@ -533,10 +533,9 @@ void basis_from_products(Ctx* ctx, const double* W, int n, int wc, int k, const 
                          double* U, double* sv, int* st) {
     const std::size_t fsm = 2ull * n * k * sizeof(double);
     if (wc >= k && k <= kFastK && fsm <= 200 * 1024) {
-        static bool attr = false;
-        if (!attr) {
+        static std::uint64_t attr = 0;  // per-device mask
+        if (first_on_device(attr, ctx->device)) {
             MB_CUDA(cudaFuncSetAttribute(basis_products_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            attr = true;
         }
         DBuf<int> slow(ctx, 1);
         MB_LAUNCH(ctx, basis_products_fast_kernel, 1, kB, fsm, W, n, k, sig, U, sv, st, slow.get());

@@ -651,7 +651,8 @@ bool launch_mode_basis(Ctx* ctx, MBArgs<T> A) {
     A.ch = ((A.rows + CL - 2) / (CL - 1) + 3) & ~3;
     auto kern = mode_basis_kernel<B, T>;
     static int dyn_max = -1;
-    if (dyn_max < 0) {
+    static std::uint64_t attr = 0;  // per-device mask
+    if (first_on_device(attr, ctx->device)) {
         cudaFuncAttributes fa{};
         MB_CUDA(cudaFuncGetAttributes(&fa, kern));
         int optin = 0;

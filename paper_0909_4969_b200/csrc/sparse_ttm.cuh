@@ -239,6 +239,12 @@ bool mode_basis_fused(Ctx* ctx, const T* Y, int rows, int n, int k, const double
 template <typename Tin>
 void dense_mode_product(Ctx* ctx, const Tin* in, const std::vector<int>& dims, int mode, const double* U, int J,
                         bool transpose, double* out);
+// mode_product(SparseTensor, Matrix, mode) from the nonzeros, reference
+// summation order (sparse_mode_product.cu); M: J x len column-major
+void sparse_mode_product(Ctx* ctx, const mach_sparse* s, int mode, const double* M, int J, double* y);
+// truncated_svd family on the device (tsvd.cu); A rows x cols column-major
+void truncated_svd_dev(Ctx* ctx, const double* A, int rows, int cols, int k, double* left, double* sv, double* right);
+void low_rank_dev(Ctx* ctx, const double* L, const double* sv, const double* R, int rows, int cols, int k, double* out);
 // dense mode-n Gram X_(n) X_(n)^T on tcgen05 (gram_tc.cu), read in place
 bool gram_tc_applies(const std::vector<int>& dims, int n);
 void gram_tc(Ctx* ctx, const float* x, const std::vector<int>& dims, int n, double* G);

@@ -394,11 +394,10 @@ void launch_ttm_tc(Ctx* ctx, const CUtensorMap& ta, const float* uh, const float
     const cuuint32_t bb[2] = {XBK, NB};
     encode(&tbh, uh, 2, bd, bs, bb, CU_TENSOR_MAP_SWIZZLE_128B);
     encode(&tbl, ul, 2, bd, bs, bb, CU_TENSOR_MAP_SWIZZLE_128B);
-    static bool attr = false;
-    if (!attr) {
+    static std::uint64_t attr = 0;  // per-device mask
+    if (first_on_device(attr, ctx->device)) {
         MB_CUDA(cudaFuncSetAttribute(ttm_tc_kernel<MN, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(XL<NB>::smem)));
-        attr = true;
     }
     const long long nab = MN ? (inner + XBM - 1) / XBM : 1;
     const long long ntiles = MN ? nab * outer : (outer + XBM - 1) / XBM;

@@ -1221,15 +1221,10 @@ mach_dense* mode_product_dev(Ctx* ctx, const mach_dense* t, const mach_sparse* s
         else if (t->dtype == MACH_F32) dense_mode_product<float>(ctx, static_cast<const float*>(t->data), dims, mode, U.get(), rows, true, y.get());
         else dense_mode_product<double>(ctx, static_cast<const double*>(t->data), dims, mode, U.get(), rows, true, y.get());
     } else {
-        DBuf<double> dn(ctx, static_cast<std::size_t>(s->numel));
-        if (s->dtype == MACH_F32) {
-            DBuf<float> df(ctx, static_cast<std::size_t>(s->numel));
-            densify<float>(ctx, s, df.get());
-            dense_mode_product<float>(ctx, df.get(), dims, mode, U.get(), rows, true, y.get());
-        } else {
-            densify<double>(ctx, s, dn.get());
-            dense_mode_product<double>(ctx, dn.get(), dims, mode, U.get(), rows, true, y.get());
-        }
+        // straight from the nonzeros (sparse_mode_product.cu), no densified copy
+        DBuf<double> Md(ctx, static_cast<std::size_t>(rows) * cols);
+        to_device(ctx, Md.get(), m, Md.n);
+        sparse_mode_product(ctx, s, mode, Md.get(), rows, y.get());
     }
     sync(ctx);
     out->data = y.p;

@@ -1,7 +1,9 @@
 // Reference-style caller of the C++ mirror (include/mach/*.hpp): the same
 // code shape as proj/tests/test_sampling.cpp / test_tucker.cpp, linked
 // against libmach_b200.so.  Prints one line per check; exit code = failures.
+#include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <vector>
 
@@ -27,7 +29,9 @@ int main() {
     const DenseTensor t({6, 7, 8}, v);
 
     const SparseTensor keep = sparsify(t, SparsifyConfig{1.0, 3});
-    CHECK(keep.nnz() == t.size());
+    std::int64_t nonzero = 0;  // sparsify skips exact zeros (sampling.cpp:25); v[0] = sin(0) = 0
+    for (double x : v) nonzero += x != 0.0;
+    CHECK(keep.nnz() == nonzero);
     const SparseTensor half = sparsify(t, SparsifyConfig{0.5, 7});
     CHECK(half.nnz() > 0 && half.nnz() < t.size());
     for (const SparseEntry& e : half.entries()) CHECK(e.value * 0.5 == t.values()[static_cast<std::size_t>(e.index)]);
@@ -49,6 +53,39 @@ int main() {
 
     const LeftSingularBasis b = left_singular_basis(matricize(t, 1), 3);
     CHECK(b.numerical_rank == 3 && !b.completed);
+
+    // truncated SVD family (linalg.hpp:11-30): orthonormal factors, sorted
+    // values, the left factor shared with leading_left_singular_vectors,
+    // low_rank_approx = left diag(s) right^T, k checked like the reference
+    const Matrix a = matricize(t, 2);  // 8 x 42
+    const TruncatedSvd svd = truncated_svd(a, 4);
+    CHECK(svd.left.rows() == 8 && svd.left.cols() == 4 && svd.right.rows() == 42 && svd.right.cols() == 4);
+    for (int i = 1; i < 4; ++i) CHECK(svd.singular_values[i] <= svd.singular_values[i - 1]);
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            double l = 0.0, r = 0.0;
+            for (int x = 0; x < 8; ++x) l += svd.left(x, i) * svd.left(x, j);
+            for (int x = 0; x < 42; ++x) r += svd.right(x, i) * svd.right(x, j);
+            CHECK(std::abs(l - (i == j ? 1.0 : 0.0)) < 1e-10 && std::abs(r - (i == j ? 1.0 : 0.0)) < 1e-10);
+        }
+    const Matrix lead = leading_left_singular_vectors(a, 4);
+    CHECK(lead.values() == svd.left.values());
+    const Matrix lr = low_rank_approx(a, 4);
+    double err = 0.0;
+    for (int r = 0; r < 8; ++r)
+        for (int c = 0; c < 42; ++c) {
+            double v = 0.0;
+            for (int i = 0; i < 4; ++i) v += svd.left(r, i) * svd.singular_values[i] * svd.right(c, i);
+            err = std::max(err, std::abs(v - lr(r, c)));
+        }
+    CHECK(err < 1e-12);
+    threw = false;
+    try {
+        truncated_svd(a, 9);
+    } catch (const ArgumentError&) {
+        threw = true;
+    }
+    CHECK(threw);
     std::printf("api_smoke: %d failures\n", failures);
     return failures;
 }
