@@ -212,19 +212,16 @@ def run_mach(args, rank, world, local):
                 full = mb.SparseTensor.from_device(dims, gidx.numel(), gidx.data_ptr(), gval.data_ptr(), np_dt, ctx)
                 hs = mb.HooiSession(full, ranks)
                 sess = mb.HooiSession.from_session(sp_local, ranks, hs)
-                n2 = (val_t.double() ** 2).sum().reshape(1)
-                torch.distributed.all_reduce(n2, group=group)
-                sess.set_norm2(float(n2.item()))
                 hs_model = hs.model()
                 hs.free()
                 full.free()
-            engine = SH.CudaEngine(sess, np_dt, dev)
-
-            def allreduce_(y):
-                torch.distributed.all_reduce(y, group=group)
+            # NCCL inside the library: each mode's partial Y_(n) is all-reduced
+            # on the library stream, inside the sweep's CUDA graph
+            SH.bind_comm(ctx, group)
+            sess.shard()
 
             def run_sweeps(n):
-                SH.sharded_sweeps(engine, allreduce_, len(dims), n, -1.0)
+                sess.step(n, -1.0)
         else:
             sess = mb.HooiSession(sp, ranks)
 
@@ -312,7 +309,7 @@ def run_mach(args, rank, world, local):
         "config": {"workload": f"{args.config.upper()}: {'x'.join(map(str, dims))} {dtype}, ranks {ranks}, "
                                f"noise {noise}, MACH p={p}, step = one HOOI sweep",
                    "nnz": nnz, "numel": int(math.prod(dims)), "seed_data": seed_data, "seed_mach": seed_mach,
-                   "parallelism": (f"time-slab shards x{world} (NCCL all-reduce of Y_(n) per mode)" if sharded
+                   "parallelism": (f"time-slab shards x{world} (in-library NCCL all-reduce of Y_(n) per mode)" if sharded
                                    else "single"),
                    "l2": "flushed (256 MiB memset) before every timed sweep"},
         "gpu_launches": launches,

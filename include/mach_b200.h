@@ -148,7 +148,17 @@ mach_status mach_hooi_ttm_bytes(mach_session* s, int mode, long long* bytes);
    mode's Y (tucker.cpp:80-106 bookkeeping and stop rule). */
 mach_status mach_hooi_begin_from(mach_ctx* ctx, const mach_sparse* t, const int* ranks, const mach_model* init,
                                  mach_session** out);  /* start from init's factors (e.g. a replicated HOSVD) */
-mach_status mach_hooi_set_norm2(mach_session* s, double norm2);  /* global |X|^2 for the fit */
+mach_status mach_hooi_set_norm2(mach_session* s, double norm2);
+/* Time-slab sharding over NCCL inside the library.  Rank 0 gets
+ * a unique id, the caller broadcasts it, every rank binds its context; then
+ * mach_hooi_shard marks a session (built on the rank's slab, e.g. by
+ * mach_hooi_begin_from) as one shard: |X|^2 is all-reduced and every sweep
+ * of mach_hooi_step all-reduces each mode's partial Y_(n) on the library
+ * stream (graph-captured with the rest of the sweep).                      */
+#define MACH_COMM_ID_BYTES 128
+mach_status mach_comm_unique_id(unsigned char* out);
+mach_status mach_ctx_comm_init(mach_ctx* ctx, int world, int rank, const unsigned char* id);
+mach_status mach_hooi_shard(mach_session* s);  /* global |X|^2 for the fit */
 mach_status mach_hooi_mode_y(mach_session* s, int mode, void** y, int* rows, int* cols);
 mach_status mach_hooi_mode_update(mach_session* s, int mode);
 mach_status mach_hooi_sweep_end(mach_session* s, double fit_tolerance, int* stopped);

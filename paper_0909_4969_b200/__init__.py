@@ -22,6 +22,7 @@ from .api import (  # noqa: F401
     TuckerModel,
     truncated_svd,
     accuracy,
+    comm_unique_id,
     default_context,
     hooi,
     kernel_stats,

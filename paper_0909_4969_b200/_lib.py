@@ -97,6 +97,9 @@ _SIGS = {
     "mach_mode_product_dense": (C.c_int, [vp, vp, C.c_int, C.c_int, dp, C.c_int, vpp]),
     "mach_mode_product_sparse": (C.c_int, [vp, vp, C.c_int, C.c_int, dp, C.c_int, vpp]),
     "mach_dense_mode_gram": (C.c_int, [vp, vp, C.c_int, dp, ip]),
+    "mach_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "mach_ctx_comm_init": (C.c_int, [vp, C.c_int, C.c_int, C.c_char_p]),
+    "mach_hooi_shard": (C.c_int, [vp]),
     "mach_truncated_svd": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int, dp, dp, dp]),
     "mach_low_rank_approx": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int, dp]),
 }

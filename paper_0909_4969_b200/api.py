@@ -77,6 +77,10 @@ class Context:
     def set_stream(self, cuda_stream_ptr: int | None):
         _check(L.lib().mach_ctx_set_stream(self.h, C.c_void_p(cuda_stream_ptr or 0)))
 
+    def comm_init(self, world: int, rank: int, unique_id: bytes):
+        """Bind this context to an NCCL communicator (time-slab shards)."""
+        _check(L.lib().mach_ctx_comm_init(self.h, int(world), int(rank), bytes(unique_id)))
+
     def synchronize(self):
         _check(L.lib().mach_ctx_synchronize(self.h))
 
@@ -106,6 +110,13 @@ def default_context() -> Context:
     if _default_ctx is None:
         _default_ctx = Context(0)
     return _default_ctx
+
+
+def comm_unique_id() -> bytes:
+    """NCCL unique id for Context.comm_init (rank 0 creates, the caller broadcasts)."""
+    buf = C.create_string_buffer(128)
+    _check(L.lib().mach_comm_unique_id(buf))
+    return buf.raw
 
 
 def _ctx(ctx):
@@ -559,6 +570,12 @@ class HooiSession:
         self = cls.__new__(cls)
         self.h, self.ctx, self._src = h, t.ctx, t
         return self
+
+    def shard(self):
+        """Make this session one time-slab shard over its context's NCCL
+        communicator: |X|^2 summed over the shards, and every step()
+        all-reduces each mode's partial Y_(n) inside the library."""
+        _check(L.lib().mach_hooi_shard(self.h))
 
     def set_norm2(self, norm2: float):
         _check(L.lib().mach_hooi_set_norm2(self.h, float(norm2)))

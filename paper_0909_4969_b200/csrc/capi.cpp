@@ -104,6 +104,7 @@ mach_status mach_ctx_destroy(mach_ctx* ctx) {
     return guard([&] {
         if (!ctx) return;
         cudaStreamSynchronize(ctx->c.stream);
+        comm_destroy(&ctx->c);
         if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
         delete ctx;
     });
@@ -616,6 +617,7 @@ void* session_mode_y(void* s, int m, int* rows, int* cols);
 void session_mode_update(void* s, int m);
 int session_sweep_end(void* s, double tol);
 void session_set_norm2(void* s, double v);
+void session_shard(void* s);
 }  // namespace machb
 
 struct mach_session {
@@ -677,6 +679,29 @@ mach_status mach_hooi_begin_from(mach_ctx* ctx, const mach_sparse* t, const int*
         auto h = std::make_unique<mach_session>();
         h->s = session_sparse_from(const_cast<mach_sparse*>(t), ranks_of(static_cast<int>(t->dims.size()), ranks), init);
         *out = h.release();
+    });
+}
+
+mach_status mach_comm_unique_id(unsigned char* out) {
+    return guard([&] {
+        need(out, "out");
+        comm_unique_id(out);
+    });
+}
+
+mach_status mach_ctx_comm_init(mach_ctx* ctx, int world, int rank, const unsigned char* id) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
+        need(id, "id");
+        comm_init(&ctx->c, world, rank, id);
+    });
+}
+
+mach_status mach_hooi_shard(mach_session* s) {
+    return guard([&] {
+        need(s, "session");
+        session_shard(s->s);
     });
 }
 

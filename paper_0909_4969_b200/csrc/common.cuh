@@ -53,6 +53,9 @@ struct Ctx {
     // launched right after the next fused mode-basis kernel, ahead of its
     // fallback kernels (consumed once): the overlapped sweep's next stage 1
     std::function<void()> after_basis;
+    // NCCL communicator of the time-slab shards (comm.cpp), or null
+    void* comm = nullptr;
+    int comm_world = 1, comm_rank = 0;
     std::int64_t launches = 0;
     bool profile = false;                      // per-kernel CUDA-event timing (bench roofline)
     std::map<std::string, KStat> stats;
@@ -232,6 +235,12 @@ struct Split {
     int len = 0;
 };
 Split split_at(const std::vector<int>& dims, int mode);
+
+// ---- NCCL (comm.cpp), bound at run time ----
+void comm_unique_id(unsigned char* out);
+void comm_init(Ctx* ctx, int world, int rank, const unsigned char* id);
+void comm_destroy(Ctx* ctx);
+void comm_allreduce_sum(Ctx* ctx, void* buf, std::size_t count, bool f64);
 
 // One-time per-device setup (kernel attributes are per device): true the
 // first time `dev` is seen for this mask.

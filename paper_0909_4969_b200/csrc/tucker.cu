@@ -386,6 +386,7 @@ struct SessionBase {
     virtual void ext_mode_update(int) { throw Error(MACH_ERR_ARGUMENT, "split sweeps need a sparse session"); }
     virtual void ext_core_fit() { throw Error(MACH_ERR_ARGUMENT, "split sweeps need a sparse session"); }
     virtual void set_norm2(double) { throw Error(MACH_ERR_ARGUMENT, "split sweeps need a sparse session"); }
+    virtual void shard() { throw Error(MACH_ERR_ARGUMENT, "sharded sweeps need a sparse session"); }
     int ext_sweep_end(double tol) {
         ext_core_fit();
         sweep_ms.push_back(0.0);
@@ -620,7 +621,15 @@ struct SparseSession : SessionBase {
     bool overlap = false;
     bool split4 = false;    // order 4: stage 1 + the dimension-tree stage 2 (stage2_4way_kernel)
     bool f0_ready = false;  // Fov[0] holds mode 0's stage 1 for the current factors
-    bool overlap_ok() const { return overlap && !sharded; }
+    bool overlap_ok() const { return overlap && (!sharded || comm_shard); }
+    // one shard of a time-slab partition with the library's NCCL communicator:
+    // every mode's partial Y_(n) is all-reduced in stream before its update
+    bool comm_shard = false;
+    void reduce_y(int m) {
+        if (!comm_shard) return;
+        comm_allreduce_sum(ctx, Y.get(), static_cast<std::size_t>(dims[static_cast<std::size_t>(m)]) * C[static_cast<std::size_t>(m)],
+                           sizeof(T) == 8);
+    }
     void stage1(int m) {
         static const int reserve = std::getenv("MACH_OV_RESERVE") ? std::atoi(std::getenv("MACH_OV_RESERVE")) : 16;
         int sms = 148;
@@ -929,7 +938,7 @@ struct SparseSession : SessionBase {
     bool graph_ok() const {
         static const bool off = std::getenv("MACH_NO_GRAPH") || std::getenv("MACH_DEBUG_EIG") ||
                                 std::getenv("MACH_DEBUG_EIG_T") || std::getenv("MACH_TTM_TS");
-        if (off || ctx->profile || sharded) return false;
+        if (off || ctx->profile || (sharded && !comm_shard)) return false;
         // the first sweep seeds the warm blocks of the modes that keep them;
         // from the second on every sweep issues the same launches
         return iterations >= 1;
@@ -941,6 +950,7 @@ struct SparseSession : SessionBase {
             if (!f0_ready) stage1(0);
             for (int i = 0; i < d; ++i) {
                 stage2(i);
+                reduce_y(i);
                 if (i + 1 < d) ctx->after_basis = [this, i]() { stage1(i + 1); };
                 else ctx->after_basis = [this]() { stage1(0); };
                 mode_update(i);
@@ -956,6 +966,7 @@ struct SparseSession : SessionBase {
         }
         for (int i = 0; i < d; ++i) {
             mode_y(i);
+            reduce_y(i);
             mode_update(i);
         }
         core_device();
@@ -1001,6 +1012,22 @@ struct SparseSession : SessionBase {
     void ext_core_fit() override {
         fit = core_and_fit();
         warnings = read_warnings(ctx, fs.st, ranks, all);
+    }
+    void shard() override {
+        if (!ctx->comm) throw Error(MACH_ERR_NCCL, "no communicator on this context (mach_ctx_comm_init)");
+        // |X|^2 of this shard's nonzeros, summed over the shards
+        DBuf<double> n2(ctx, 1);
+        sumsq<T>(ctx, static_cast<const T*>(X->val), X->nnz, fs.red.get(), n2.get());
+        comm_allreduce_sum(ctx, n2.get(), 1, true);
+        double v = 0.0;
+        to_host(ctx, &v, n2.get(), 1);
+        sync(ctx);
+        set_norm2(v);
+        comm_shard = true;
+        // the sweep graph (if any) was captured without the exchange
+        if (graph_exec) { cudaGraphExecDestroy(graph_exec); graph_exec = nullptr; }
+        if (graph) { cudaGraphDestroy(graph); graph = nullptr; }
+        f0_ready = false;
     }
     void set_norm2(double v) override {
         if (!(v >= 0.0)) throw_arg("norm2 must be >= 0");
@@ -1104,6 +1131,7 @@ void* session_mode_y(void* s, int m, int* rows, int* cols) { return S(s)->ext_mo
 void session_mode_update(void* s, int m) { S(s)->ext_mode_update(m); }
 int session_sweep_end(void* s, double tol) { return S(s)->ext_sweep_end(tol); }
 void session_set_norm2(void* s, double v) { S(s)->set_norm2(v); }
+void session_shard(void* s) { S(s)->shard(); }
 
 mach_model* tucker_sparse(mach_sparse* X, const std::vector<int>& ranks, bool do_hooi, int max_it, double tol) {
     check_ranks(X->dims, ranks);

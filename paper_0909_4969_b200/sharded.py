@@ -13,9 +13,12 @@ per mode, TTM -> all-reduce(sum) of Y_(n) (<= 0.5 MB at the configs) ->
 replicated factor update (identical inputs on every rank give identical
 factors, so no broadcast), and the core/fit come from the last mode's summed
 Y.  |X|^2 is all-reduced once.  HOSVD runs once on the all-gathered sampled
-tensor (replicated).  The reductions are NCCL (over NVLink / NVSwitch) on the
-library's stream; `sharded_sweeps` is the host logic shared with the CPU
-(`gloo`) tests.
+tensor (replicated: the time mode's row Gram has cross-slab blocks, SURVEY
+§8e).  With an NCCL group the per-mode all-reduce runs inside the library
+(mach_ctx_comm_init + mach_hooi_shard: on the library stream, inside the
+sweep's CUDA graph, overlapped stage 1 kept); `sharded_sweeps` is the same
+exchange driven from the host, used with `gloo` (CPU tests, and a 2-process
+test of the real CUDA engine).
 """
 from __future__ import annotations
 
@@ -78,10 +81,18 @@ class CudaEngine:
         return self.s.sweep_end(tol)
 
 
+def _host_staged(group) -> bool:
+    """gloo exchanges go through host tensors (its CUDA paths are not used)."""
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
 def _allgather_varlen(t, group):
     """All-gather 1-D tensors of per-rank lengths, concatenated in rank order."""
     import torch
     import torch.distributed as dist
+    if _host_staged(group) and t.is_cuda:
+        return _allgather_varlen(t.cpu(), group).to(t.device)
     world = dist.get_world_size(group)
     n = torch.tensor([t.numel()], device=t.device, dtype=torch.int64)
     ns = [torch.zeros_like(n) for _ in range(world)]
@@ -96,7 +107,7 @@ def _allgather_varlen(t, group):
 
 
 def sharded_mach_hooi(slab_flat, global_dims, ranks, p: float, seed: int, sweeps: int, fit_tolerance: float = 0.0,
-                      group=None, ctx=None):
+                      group=None, ctx=None, in_library=None):
     """MACH-HOOI of a tensor whose time slabs live on the ranks of `group`.
 
     slab_flat: this rank's slab (torch CUDA tensor, first-mode-fastest, the
@@ -109,15 +120,39 @@ def sharded_mach_hooi(slab_flat, global_dims, ranks, p: float, seed: int, sweeps
     from . import api as A
 
     world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if in_library is None:  # the library's NCCL exchange when the group is NCCL, else the host loop
+        in_library = dist.get_backend(group) == "nccl"
     dims = list(global_dims)
-    d = len(dims)
     S = math.prod(dims[:-1])
     t0, t1 = slab_bounds(dims[-1], world, rank)
     if slab_flat.numel() != S * (t1 - t0):
         raise A.ShapeError("slab does not match slab_bounds for this rank")
     dev = slab_flat.device
     ctx = ctx or A.Context(dev.index)
-    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)  # NCCL and the library share one stream
+    # one explicit stream for the library, torch's collectives and copies (a
+    # null handle would give the library a stream of its own)
+    stream = torch.cuda.Stream(device=dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))
+    ctx.set_stream(stream.cuda_stream)
+    ctx._stream_keepalive = stream  # the context (and the returned tensors) keep using it
+    with torch.cuda.stream(stream):
+        out = _sharded_body(slab_flat, dims_=list(global_dims), ranks=ranks, p=p, seed=seed, sweeps=sweeps,
+                            fit_tolerance=fit_tolerance, group=group, ctx=ctx, in_library=in_library, dev=dev)
+    stream.synchronize()
+    return out
+
+
+def _sharded_body(slab_flat, dims_, ranks, p, seed, sweeps, fit_tolerance, group, ctx, in_library, dev):
+    import torch
+    import torch.distributed as dist
+
+    from . import api as A
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    dims = dims_
+    d = len(dims)
+    S = math.prod(dims[:-1])
+    t0, t1 = slab_bounds(dims[-1], world, rank)
     dtype = np.float32 if slab_flat.dtype == torch.float32 else np.float64
     slab = A.DenseTensor.from_torch(slab_flat, dims[:-1] + [t1 - t0], ctx)
     sp = A.sparsify_slab(slab, dims, t0 * S, A.SparsifyConfig(p, seed), ctx)
@@ -135,14 +170,42 @@ def sharded_mach_hooi(slab_flat, global_dims, ranks, p: float, seed: int, sweeps
     hs.free()
     full.free()
 
-    n2 = (val.double() ** 2).sum().reshape(1)
-    dist.all_reduce(n2, group=group)
-    sess.set_norm2(float(n2.item()))
+    if in_library:
+        # NCCL inside the library: the exchange rides the library stream and
+        # the sweep graph (overlapped stage 1 kept)
+        bind_comm(ctx, group)
+        sess.shard()
+        sess.step(sweeps, fit_tolerance)
+    else:
+        host = _host_staged(group)
+        n2 = (val.double() ** 2).sum().reshape(1)
+        n2 = n2.cpu() if host else n2
+        dist.all_reduce(n2, group=group)
+        sess.set_norm2(float(n2.item()))
 
-    def allreduce_sum_(y):
-        dist.all_reduce(y, group=group)
+        def allreduce_sum_(y):
+            if host:
+                torch.cuda.current_stream(dev).synchronize()  # the library's Y_(m) is written
+                yh = y.cpu()
+                dist.all_reduce(yh, group=group)
+                y.copy_(yh)
+            else:
+                dist.all_reduce(y, group=group)
 
-    sharded_sweeps(CudaEngine(sess, dtype, dev), allreduce_sum_, d, sweeps, fit_tolerance)
+        sharded_sweeps(CudaEngine(sess, dtype, dev), allreduce_sum_, d, sweeps, fit_tolerance)
     model = sess.model()
     sess.free()
     return model, sp
+
+
+def bind_comm(ctx, group=None):
+    """Give `ctx` an NCCL communicator over the ranks of `group` (the unique
+    id travels by torch.distributed, whatever its backend)."""
+    import torch.distributed as dist
+
+    from . import api as A
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    obj = [A.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    ctx.comm_init(world, rank, obj[0])

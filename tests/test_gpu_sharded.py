@@ -44,22 +44,28 @@ def test_slab_sampling_bitexact():
     assert np.array_equal(np.concatenate(got_v).view(np.uint64), fv.view(np.uint64))
 
 
-@pytest.mark.parametrize("dtype", ["float64", "float32"])
-def test_sharded_world1_matches_session(dtype):
+@pytest.mark.parametrize("dtype,in_library,dims,ranks", [
+    ("float64", False, (40, 30, 36), (4, 3, 5)), ("float32", False, (40, 30, 36), (4, 3, 5)),
+    ("float64", True, (40, 30, 36), (4, 3, 5)), ("float32", True, (40, 30, 36), (4, 3, 5)),
+    ("float32", True, (12, 10, 8, 14), (3, 3, 2, 4))])
+def test_sharded_world1_matches_session(dtype, in_library, dims, ranks):
+    """in_library: the exchange inside the library (mach_ctx_comm_init +
+    mach_hooi_shard, NCCL on the library stream, sweep graph and overlapped
+    stage 1 kept); otherwise the host loop over torch.distributed."""
     import torch
     import torch.distributed as dist
 
     import paper_0909_4969_b200 as mb
     from paper_0909_4969_b200.sharded import sharded_mach_hooi
 
-    dims, ranks, p, seed, sweeps = (40, 30, 36), (4, 3, 5), 0.2, 7, 3
+    p, seed, sweeps = 0.2, 7, 3
     x = O.random_tensor(list(dims), 13).astype(dtype)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(_port())
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
         flat = torch.from_numpy(x.reshape(-1, order="F").copy()).cuda()
-        model, sp = sharded_mach_hooi(flat, dims, ranks, p, seed, sweeps, 0.0)
+        model, sp = sharded_mach_hooi(flat, dims, ranks, p, seed, sweeps, 0.0, in_library=in_library)
     finally:
         dist.destroy_process_group()
     ref = mb.mach_hooi(mb.DenseTensor.from_numpy(x), ranks, mb.SparsifyConfig(p, seed),
@@ -70,3 +76,57 @@ def test_sharded_world1_matches_session(dtype):
     for a, b in zip(model.factors, ref.factors):
         assert subspace_sin(a, b) <= (1e-9 if dtype == "float64" else 1e-3)
     assert rel(align_core(model.core, model.factors, ref.factors), ref.core) <= tol
+
+
+def _two_rank_worker(rank, port, dims, ranks, p, seed, sweeps, q):
+    """One of two processes sharing cuda:0: its slab, the real CUDA engine,
+    the per-mode exchange over gloo (host staging; no kernel waits on the
+    other process)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_0909_4969_b200.sharded import sharded_mach_hooi, slab_bounds
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        x = O.random_tensor(list(dims), 13).astype("float32")
+        S = int(np.prod(dims[:-1]))
+        t0, t1 = slab_bounds(dims[-1], 2, rank)
+        flat = torch.from_numpy(x.reshape(-1, order="F")[t0 * S: t1 * S].copy()).cuda()
+        model, sp = sharded_mach_hooi(flat, dims, ranks, p, seed, sweeps, 0.0, in_library=False)
+        q.put((rank, model.iterations, list(model.sweep_fits), [f.copy() for f in model.factors], model.core.copy(),
+               sp.nnz))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_two_processes_cuda_engine_gloo():
+    """World size 2 of the product engine (CudaEngine over libmach_b200) on
+    one GPU: every rank ends with the single-GPU model (fp32 bars)."""
+    import torch.multiprocessing as tmp
+
+    import paper_0909_4969_b200 as mb
+
+    dims, ranks, p, seed, sweeps = (40, 30, 36), (4, 3, 5), 0.2, 7, 3
+    ctxm = tmp.get_context("spawn")
+    q = ctxm.Queue()
+    port = _port()
+    procs = [ctxm.Process(target=_two_rank_worker, args=(r, port, dims, ranks, p, seed, sweeps, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    outs = [q.get(timeout=600) for _ in range(2)]
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    x = O.random_tensor(list(dims), 13).astype("float32")
+    res = mb.mach_hooi(mb.DenseTensor.from_numpy(x), ranks, mb.SparsifyConfig(p, seed), mb.HooiConfig(sweeps, 0.0))
+    ref = res.model
+    assert sum(o[5] for o in outs) == res.sparsified.nnz  # the slabs partition the kept set
+    for rank, its, fits, factors, core, _ in outs:
+        assert its == ref.iterations
+        assert np.abs(np.array(fits) - np.array(ref.sweep_fits)).max() <= 1e-4
+        for a, b in zip(factors, ref.factors):
+            assert subspace_sin(a, b) <= 1e-3
+        assert rel(align_core(core, factors, ref.factors), ref.core) <= 1e-4
