@@ -338,7 +338,7 @@ def run_mach(args, rank, world, local):
         torch.distributed.destroy_process_group()
     sess.free()
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
 
 
 def measured_traffic(config):
@@ -470,10 +470,31 @@ def run_reference(args, rank, world):
                                       "restatement built with the reference flags (-O3, 1 thread)"},
            "e2e": {"value": round(nnz * len(sw) / wall / 1e9, 6), "unit": "GNNZ/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
+
+
+# The one JSON line goes to the process's original stdout; everything else
+# written to fd 1 (NCCL's version banner, library diagnostics) is sent to
+# stderr so the driver always reads exactly one line.
+_OUT = None
+
+
+def _own_stdout():
+    global _OUT
+    if _OUT is None:
+        sys.stdout.flush()
+        _OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(obj):
+    _own_stdout()
+    _OUT.write(json.dumps(obj) + "\n")
+    _OUT.flush()
 
 
 def main():
+    _own_stdout()
     os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
     args = parse()
     rank, world, local = dist_env()
