@@ -14,7 +14,10 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+# ORACLE_VARIANT=omp: the all-cores build (-march=native -fopenmp; bit-identical
+# results), used by bench.py's reference arm and all-cores CPU baseline line
+_OMP = os.environ.get("ORACLE_VARIANT") == "omp"
+_LIB_PATH = os.path.join(_HERE, "liboracle_omp.so" if _OMP else "liboracle.so")
 _lib = None
 
 _dp = C.POINTER(C.c_double)
@@ -48,7 +51,7 @@ _KINDS = {1: ArgumentError, 2: ShapeError, 3: ConvergenceError}
 def build(force: bool = False) -> str:
     """Compile liboracle.so with the committed Makefile (g++, -O3, no -march)."""
     if force or not os.path.exists(_LIB_PATH):
-        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+        subprocess.run(["make", "-s", "-C", _HERE] + (["omp"] if _OMP else []), check=True)
     return _LIB_PATH
 
 

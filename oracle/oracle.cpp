@@ -6,6 +6,10 @@
 #include "oracle.hpp"
 
 #include <algorithm>
+#include <cstdlib>
+#include <thread>
+
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -18,7 +22,7 @@ namespace {
 
 // src/internal.hpp:36-46 — cascade summation, base case 64.
 template <typename F>
-double pairwise_sum(std::int64_t lo, std::int64_t hi, F&& f) {
+double pairwise_seq(std::int64_t lo, std::int64_t hi, F&& f) {
     const std::int64_t n = hi - lo;
     if (n <= 64) {
         double s = 0.0;
@@ -26,8 +30,73 @@ double pairwise_sum(std::int64_t lo, std::int64_t hi, F&& f) {
         return s;
     }
     const std::int64_t mid = lo + n / 2;
-    return pairwise_sum(lo, mid, f) + pairwise_sum(mid, hi, f);
+    return pairwise_seq(lo, mid, f) + pairwise_seq(mid, hi, f);
 }
+
+#ifdef ORC_THREADS
+// The all-cores build (liboracle_omp.so, the CPU baseline's second line):
+// std::thread workers (this image's g++ has no OpenMP runtime) over
+// independent outputs; every output is computed by one thread in the serial
+// order, so results are bit-identical to the one-thread build.
+template <typename Fn>
+void parallel_for(std::int64_t n, Fn&& fn) {
+    static const int nt = [] {
+        const char* e = std::getenv("ORC_THREADS");
+        const int v = e ? std::atoi(e) : static_cast<int>(std::thread::hardware_concurrency());
+        return v > 0 ? v : 1;
+    }();
+    const int t = static_cast<int>(std::min<std::int64_t>(nt, n));
+    if (t <= 1) {
+        for (std::int64_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    th.reserve(static_cast<std::size_t>(t));
+    for (int w = 0; w < t; ++w)
+        th.emplace_back([&, w] {
+            for (std::int64_t i = w; i < n; i += t) fn(i);  // cyclic: balanced for any work shape
+        });
+    for (auto& x : th) x.join();
+}
+// the 2^kParDepth subtrees of the cascade's top levels summed in parallel and
+// combined in the reference's order (bit-identical to pairwise_seq)
+constexpr int kParDepth = 7;
+inline double pairwise_combine(std::int64_t lo, std::int64_t hi, int depth, const std::vector<double>& leaf, std::size_t& k) {
+    if (depth == kParDepth || hi - lo <= 64) return leaf[k++];
+    const std::int64_t mid = lo + (hi - lo) / 2;
+    const double a = pairwise_combine(lo, mid, depth + 1, leaf, k);
+    const double b = pairwise_combine(mid, hi, depth + 1, leaf, k);
+    return a + b;
+}
+inline void pairwise_leaves(std::int64_t lo, std::int64_t hi, int depth, std::vector<std::pair<std::int64_t, std::int64_t>>& out) {
+    if (depth == kParDepth || hi - lo <= 64) {
+        out.emplace_back(lo, hi);
+        return;
+    }
+    const std::int64_t mid = lo + (hi - lo) / 2;
+    pairwise_leaves(lo, mid, depth + 1, out);
+    pairwise_leaves(mid, hi, depth + 1, out);
+}
+template <typename F>
+double pairwise_sum(std::int64_t lo, std::int64_t hi, F&& f) {
+    if (hi - lo < (1 << 16)) return pairwise_seq(lo, hi, f);
+    std::vector<std::pair<std::int64_t, std::int64_t>> rg;
+    pairwise_leaves(lo, hi, 0, rg);
+    std::vector<double> leaf(rg.size());
+    parallel_for(static_cast<std::int64_t>(rg.size()), [&](std::int64_t i) { leaf[static_cast<std::size_t>(i)] = pairwise_seq(rg[static_cast<std::size_t>(i)].first, rg[static_cast<std::size_t>(i)].second, f); });
+    std::size_t k = 0;
+    return pairwise_combine(lo, hi, 0, leaf, k);
+}
+#else
+template <typename Fn>
+void parallel_for(std::int64_t n, Fn&& fn) {
+    for (std::int64_t i = 0; i < n; ++i) fn(i);
+}
+template <typename F>
+double pairwise_sum(std::int64_t lo, std::int64_t hi, F&& f) {
+    return pairwise_seq(lo, hi, f);
+}
+#endif
 
 [[noreturn]] void arg_error(const std::string& m) { throw Error(ErrKind::Argument, m); }
 [[noreturn]] void shape_error(const std::string& m) { throw Error(ErrKind::Shape, m); }
@@ -310,18 +379,19 @@ Dense mode_product(const Dense& t, const Mat& m, int mode) {
     od[static_cast<std::size_t>(mode)] = m.rows;
     Dense out{od, std::vector<double>(static_cast<std::size_t>(checked_size(od)), 0.0)};
     const int j = m.rows;
-    for (std::int64_t c = 0; c < s.outer; ++c) {
+    // (c, q) output columns are independent; each is summed in the same order
+    // by one thread, so the all-cores build is bit-identical
+    parallel_for(s.outer * j, [&](std::int64_t cq) {
+        const std::int64_t c = cq / j;
+        const int q = static_cast<int>(cq % j);
         const double* slab = t.v.data() + c * s.inner * s.len;
-        double* dst = out.v.data() + c * s.inner * j;
-        for (int q = 0; q < j; ++q) {
-            double* dcol = dst + static_cast<std::int64_t>(q) * s.inner;
-            for (int r = 0; r < s.len; ++r) {
-                const double f = m(q, r);
-                const double* scol = slab + static_cast<std::int64_t>(r) * s.inner;
-                for (std::int64_t a = 0; a < s.inner; ++a) dcol[a] += scol[a] * f;
-            }
+        double* dcol = out.v.data() + c * s.inner * j + static_cast<std::int64_t>(q) * s.inner;
+        for (int r = 0; r < s.len; ++r) {
+            const double f = m(q, r);
+            const double* scol = slab + static_cast<std::int64_t>(r) * s.inner;
+            for (std::int64_t a = 0; a < s.inner; ++a) dcol[a] += scol[a] * f;
         }
-    }
+    });
     return out;
 }
 

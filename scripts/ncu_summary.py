@@ -34,6 +34,17 @@ KEYS = {
 }
 
 
+def ttm_src_sha():
+    """Hash of the sources that define the sparse TTM kernels: bench.py only
+    takes a capture's DRAM traffic when it matches the build it measures."""
+    import hashlib
+    h = hashlib.sha256()
+    for name in ("ttm_kernel.cuh", "sparse_ttm.cu", "sparse_ttm.cuh", "common.cuh"):
+        with open(os.path.join(ROOT, "paper_0909_4969_b200", "csrc", name), "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def num(v):
     try:
         return float(str(v).replace(",", ""))
@@ -53,7 +64,8 @@ def main():
     head, units, data = rows[0], rows[1], rows[2:]
     d = dict(zip(head, data[a.index]))
     u = dict(zip(head, units))
-    out = {"config": a.config, "report": os.path.basename(a.report), "kernel": d.get("Kernel Name", "")}
+    out = {"config": a.config, "report": os.path.basename(a.report), "kernel": d.get("Kernel Name", ""),
+           "ttm_src_sha": ttm_src_sha()}
     for k, m in KEYS.items():
         out[k] = num(d.get(m))
     # ncu reports bytes in the unit row (byte / Kbyte / Mbyte ...); normalise
