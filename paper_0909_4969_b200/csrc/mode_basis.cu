@@ -684,6 +684,15 @@ bool launch_mode_basis(Ctx* ctx, MBArgs<T> A) {
         tsb.zero(ctx);
     }
     long long* ts = dbg ? tsb.get() : nullptr;
+    DBuf<long long> sb;
+    if (dbg) {  // fine stamps inside the small-matrix helpers
+        sb.alloc(ctx, 200);
+        sb.zero(ctx);
+        long long* p = sb.get();
+        int z = 0;
+        MB_CUDA(cudaMemcpyToSymbolAsync(g_stamp, &p, sizeof(p), 0, cudaMemcpyHostToDevice, ctx->stream));
+        MB_CUDA(cudaMemcpyToSymbolAsync(g_stamp_n, &z, sizeof(z), 0, cudaMemcpyHostToDevice, ctx->stream));
+    }
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (dbg) {
         cudaEventCreate(&ev0);
@@ -709,6 +718,14 @@ bool launch_mode_basis(Ctx* ctx, MBArgs<T> A) {
         for (int q = 1; q < CL; ++q) { emin = std::min(emin, h[160 + q]); emax = std::max(emax, h[160 + q]); }
         std::fprintf(stderr, " | end-start %.1fus | CTA entry spread %.1fus, CTA0 - first %.1fus\n", (h[238] - h[1]) * 1e-3,
                      (emax - emin) * 1e-3, (h[160] - emin) * 1e-3);
+        long long f[200];
+        to_host(ctx, f, sb.get(), 200);
+        sync(ctx);
+        std::fprintf(stderr, "[mb-f]");
+        for (int i = 1; i < 100 && f[2 * i + 1]; ++i) std::fprintf(stderr, " %lld:%.2f", f[2 * i], (f[2 * i + 1] - f[2 * i - 1]) * 1e-3);
+        std::fprintf(stderr, "\n");
+        long long* np = nullptr;
+        cudaMemcpyToSymbol(g_stamp, &np, sizeof(np));
         std::fprintf(stderr, "[mb-t] D(rank1): vload %.1f W %.1f bgram %.1f csync %.1f\n", (h[220] - h[219]) * 1e-3,
                      (h[221] - h[220]) * 1e-3, (h[222] - h[221]) * 1e-3, (h[223] - h[222]) * 1e-3);
     }

@@ -242,6 +242,10 @@ void dense_mode_product(Ctx* ctx, const Tin* in, const std::vector<int>& dims, i
 // mode_product(SparseTensor, Matrix, mode) from the nonzeros, reference
 // summation order (sparse_mode_product.cu); M: J x len column-major
 void sparse_mode_product(Ctx* ctx, const mach_sparse* s, int mode, const double* M, int J, double* y);
+// |x - reconstruct(core, U)|^2 in one fused pass (metrics.cu)
+template <typename T>
+double residual2_fused(Ctx* ctx, const T* x, const std::vector<int>& dims, const std::vector<int>& ranks,
+                       const double* core, const std::vector<const double*>& U);
 // truncated_svd family on the device (tsvd.cu); A rows x cols column-major
 void truncated_svd_dev(Ctx* ctx, const double* A, int rows, int cols, int k, double* left, double* sv, double* right);
 void low_rank_dev(Ctx* ctx, const double* L, const double* sv, const double* R, int rows, int cols, int k, double* out);

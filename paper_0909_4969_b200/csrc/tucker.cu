@@ -1170,12 +1170,12 @@ double accuracy_dev(const mach_dense* t, const mach_model* m) {
     }
     DBuf<double> core(ctx, m->core.size());
     to_device(ctx, core.get(), m->core.data(), m->core.size());
-    DBuf<double> rec = reconstruct_dev(ctx, core.get(), m->ranks, m->dims, U);
-    if (t->dtype == MACH_F32) sumsq_diff<float>(ctx, static_cast<const float*>(t->data), rec.get(), t->numel, red.get(), scal.get() + 1);
-    else sumsq_diff<double>(ctx, static_cast<const double*>(t->data), rec.get(), t->numel, red.get(), scal.get() + 1);
-    double e2 = 0;
-    to_host(ctx, &e2, scal.get() + 1, 1);
-    sync(ctx);
+    // fused reconstruct-and-compare (metrics.cu): no dense reconstruction
+    std::vector<const double*> up;
+    for (auto& u : U) up.push_back(u.get());
+    const double e2 = t->dtype == MACH_F32
+                          ? residual2_fused<float>(ctx, static_cast<const float*>(t->data), t->dims, m->ranks, core.get(), up)
+                          : residual2_fused<double>(ctx, static_cast<const double*>(t->data), t->dims, m->ranks, core.get(), up);
     return 1.0 - std::sqrt(e2) / std::sqrt(n2);
 }
 
