@@ -187,6 +187,15 @@ mach_status mach_model_free(mach_model* m);
 /* ---- model evaluation (tucker.hpp:47-55) --------------------------------- */
 /* accuracy(t, model) = 1 - |t - reconstruct(model)| / |t|                   */
 mach_status mach_accuracy(mach_ctx* ctx, const mach_dense* t, const mach_model* m, double* out);
+/* accuracy(t, model) from host model arrays (core prod(ranks), factors[m]
+ * I_m x r_m column-major): one fused device pass, no reconstruction
+ * (tucker.cpp:211-217; compare, metrics.cpp:155-156)                        */
+mach_status mach_model_accuracy(mach_ctx* ctx, const mach_dense* t, const int* ranks,
+                                const double* core, const double* const* factors, double* out);
+/* subspace_sin (metrics.cpp:59-66): largest principal-angle sine between the
+ * spans of the leading r columns of host n x r column-major a and b          */
+mach_status mach_subspace_sin(mach_ctx* ctx, int n, int r, const double* a, const double* b,
+                              double* out);
 /* reconstruct(model) into a new dense fp64 tensor                           */
 mach_status mach_reconstruct(mach_ctx* ctx, const mach_model* m, mach_dense** out);
 

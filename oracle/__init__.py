@@ -102,6 +102,9 @@ def lib():
         L.orc_jacobi_eig.argtypes = [C.c_int, _dp, _dp, _dp]
         L.orc_left_singular_basis.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _dp, _dp, _ip, _ip]
         L.orc_low_rank_approx.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _dp]
+        L.orc_pearson.argtypes = [C.c_int, _dp, _dp, _dp]
+        L.orc_pc_correlation.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _dp, _ip]
+        L.orc_compare.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, _dp, _ip, _ip, _dp, _dp, _dp]
         L.orc_truncated_svd.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _dp, _dp, _dp]
         L.orc_reconstruct.argtypes = [C.c_void_p, _dp]
         L.orc_last_error.argtypes = [C.c_char_p, C.c_int]
@@ -371,6 +374,36 @@ def left_singular_basis(m: np.ndarray, k: int):
     _check(lib().orc_left_singular_basis(rows, cols, _d(flat), int(k), _d(basis), _d(sv), C.byref(nr),
                                          C.byref(comp)))
     return basis.reshape((rows, k), order="F"), sv[:k].copy(), nr.value, bool(comp.value)
+
+
+def pearson(x, y) -> float:
+    """metrics.cpp:67-96."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if x.size != y.size:
+        raise ShapeError(2, "correlation inputs have different lengths")
+    out = C.c_double()
+    _check(lib().orc_pearson(int(x.size), _d(x), _d(y), C.byref(out)))
+    return out.value
+
+
+def pc_correlation(exact: "Model", approx: "Model", mode: int, component: int = 1):
+    """metrics.cpp:98-122: (rho, flipped)."""
+    out, fl = C.c_double(), C.c_int()
+    _check(lib().orc_pc_correlation(exact._h, approx._h, int(mode), int(component), C.byref(out), C.byref(fl)))
+    return out.value, bool(fl.value)
+
+
+def compare(exact: "Model", approx: "Model", reference: "Dense") -> dict:
+    """metrics.cpp:124-159 (ComparisonReport)."""
+    d = len(exact.factors)
+    rho, ts = np.zeros(d), np.zeros(d)
+    fl, ti = (C.c_int * d)(), (C.c_int * d)()
+    acc, core = np.zeros(2), np.zeros(2)
+    _check(lib().orc_compare(exact._h, approx._h, reference.h, _d(rho), fl, ti, _d(ts), _d(acc), _d(core)))
+    return {"per_mode_rho": rho, "flipped": [bool(v) for v in fl], "tied": [bool(v) for v in ti],
+            "tie_subspace_sin": ts, "accuracy_exact": acc[0], "accuracy_mach": acc[1],
+            "core_interaction": (core[0], core[1])}
 
 
 def truncated_svd(m: np.ndarray, k: int):

@@ -1312,4 +1312,122 @@ double subspace_gap(const Mat& a, const Mat& b) {
     return std::sqrt(std::max(0.0, ev.front()));
 }
 
+// ============================================================================
+// Metrics — src/metrics.cpp:15-159.
+// ============================================================================
+namespace {
+constexpr double kTieGap = 1e-6;  // metrics.cpp:19
+
+void check_models(const Model& a, const Model& b) {  // :21-31
+    if (a.factors.size() != b.factors.size())
+        shape_error("models have orders " + std::to_string(a.factors.size()) + " and " + std::to_string(b.factors.size()));
+    for (std::size_t m = 0; m < a.factors.size(); ++m)
+        if (a.factors[m].rows != b.factors[m].rows)
+            shape_error("mode " + std::to_string(m + 1) + " has " + std::to_string(a.factors[m].rows) +
+                        " rows in one model and " + std::to_string(b.factors[m].rows) + " in the other");
+}
+
+std::vector<double> core_slice_norms(const Dense& core, int mode) {  // :40-50
+    std::int64_t stride = 1;
+    for (int m = 0; m < mode; ++m) stride *= core.dims[static_cast<std::size_t>(m)];
+    const std::int64_t len = core.dims[static_cast<std::size_t>(mode)];
+    std::vector<double> sq(static_cast<std::size_t>(len), 0.0);
+    for (std::int64_t i = 0; i < core.size(); ++i) sq[static_cast<std::size_t>((i / stride) % len)] += core.v[static_cast<std::size_t>(i)] * core.v[static_cast<std::size_t>(i)];
+    for (double& v : sq) v = std::sqrt(v);
+    return sq;
+}
+
+bool top_two_tied(std::vector<double> n) {  // :52-56
+    if (n.size() < 2) return false;
+    std::sort(n.begin(), n.end(), std::greater<>());
+    return n[0] - n[1] <= kTieGap * n[0];
+}
+
+Mat left_cols(const Mat& a, int r) {
+    Mat out(a.rows, r);
+    for (int c = 0; c < r; ++c)
+        for (int i = 0; i < a.rows; ++i) out(i, c) = a(i, c);
+    return out;
+}
+}  // namespace
+
+double pearson(const std::vector<double>& x, const std::vector<double>& y) {
+    if (x.size() != y.size())
+        shape_error("correlation inputs have lengths " + std::to_string(x.size()) + " and " + std::to_string(y.size()));
+    const std::int64_t n = static_cast<std::int64_t>(x.size());
+    if (n < 2) arg_error("correlation needs at least 2 samples");
+    const bool xc = std::all_of(x.begin(), x.end(), [&](double v) { return v == x[0]; });
+    const bool yc = std::all_of(y.begin(), y.end(), [&](double v) { return v == y[0]; });
+    if (xc || yc) arg_error("correlation is undefined for a zero-variance input");
+    const double mx = pairwise_sum(0, n, [&](std::int64_t i) { return x[static_cast<std::size_t>(i)]; }) / static_cast<double>(n);
+    const double my = pairwise_sum(0, n, [&](std::int64_t i) { return y[static_cast<std::size_t>(i)]; }) / static_cast<double>(n);
+    const double sxx = pairwise_sum(0, n, [&](std::int64_t i) {
+        const double d = x[static_cast<std::size_t>(i)] - mx;
+        return d * d;
+    });
+    const double syy = pairwise_sum(0, n, [&](std::int64_t i) {
+        const double d = y[static_cast<std::size_t>(i)] - my;
+        return d * d;
+    });
+    const double sxy = pairwise_sum(0, n, [&](std::int64_t i) {
+        return (x[static_cast<std::size_t>(i)] - mx) * (y[static_cast<std::size_t>(i)] - my);
+    });
+    if (sxx == 0.0 || syy == 0.0) arg_error("correlation is undefined for a zero-variance input");
+    return sxy / std::sqrt(sxx * syy);
+}
+
+double pc_correlation(const Model& exact, const Model& approx, int mode, int component, bool* flipped) {
+    check_models(exact, approx);
+    const int d = static_cast<int>(exact.factors.size());
+    if (mode < 0 || mode >= d) arg_error("mode " + std::to_string(mode + 1) + " out of range for order " + std::to_string(d));
+    const int limit = std::min(exact.ranks[static_cast<std::size_t>(mode)], approx.ranks[static_cast<std::size_t>(mode)]);
+    if (component < 1 || component > limit)
+        arg_error("component " + std::to_string(component) + " out of range; mode " + std::to_string(mode + 1) +
+                  " has at most " + std::to_string(limit) + " shared components");
+    const Mat& fa = exact.factors[static_cast<std::size_t>(mode)];
+    const Mat& fb = approx.factors[static_cast<std::size_t>(mode)];
+    std::vector<double> a(fa.col(component - 1), fa.col(component - 1) + fa.rows);
+    std::vector<double> b(fb.col(component - 1), fb.col(component - 1) + fb.rows);
+    const double dot = pairwise_sum(0, static_cast<std::int64_t>(a.size()),
+                                    [&](std::int64_t i) { return a[static_cast<std::size_t>(i)] * b[static_cast<std::size_t>(i)]; });
+    const bool flip = dot < 0.0;
+    if (flipped) *flipped = flip;
+    if (flip)
+        for (double& v : b) v = -v;
+    return pearson(a, b);
+}
+
+Report compare(const Model& exact, const Model& approx, const Dense& reference) {
+    check_models(exact, approx);
+    const int d = static_cast<int>(exact.factors.size());
+    if (reference.order() != d)
+        shape_error("reference has order " + std::to_string(reference.order()) + ", models have order " + std::to_string(d));
+    for (int m = 0; m < d; ++m)
+        if (reference.dims[static_cast<std::size_t>(m)] != exact.factors[static_cast<std::size_t>(m)].rows)
+            shape_error("mode " + std::to_string(m + 1) + " has " + std::to_string(reference.dims[static_cast<std::size_t>(m)]) +
+                        " entries in the reference and " + std::to_string(exact.factors[static_cast<std::size_t>(m)].rows) +
+                        " in the models");
+    Report r;
+    r.rho.resize(static_cast<std::size_t>(d));
+    r.flipped.assign(static_cast<std::size_t>(d), false);
+    r.tied.assign(static_cast<std::size_t>(d), false);
+    r.tie_sin.assign(static_cast<std::size_t>(d), 0.0);
+    for (int m = 0; m < d; ++m) {
+        bool flip = false;
+        r.rho[static_cast<std::size_t>(m)] = pc_correlation(exact, approx, m, 1, &flip);
+        r.flipped[static_cast<std::size_t>(m)] = flip;
+        if (top_two_tied(core_slice_norms(exact.core, m)) || top_two_tied(core_slice_norms(approx.core, m))) {
+            r.tied[static_cast<std::size_t>(m)] = true;
+            const int rk = std::min(exact.ranks[static_cast<std::size_t>(m)], approx.ranks[static_cast<std::size_t>(m)]);
+            r.tie_sin[static_cast<std::size_t>(m)] = subspace_gap(left_cols(exact.factors[static_cast<std::size_t>(m)], rk),
+                                                                  left_cols(approx.factors[static_cast<std::size_t>(m)], rk));
+        }
+    }
+    r.accuracy_exact = accuracy(reference, exact);
+    r.accuracy_mach = accuracy(reference, approx);
+    r.core_exact = exact.core.v[0];
+    r.core_mach = approx.core.v[0];
+    return r;
+}
+
 }  // namespace orc

@@ -153,6 +153,18 @@ Mat random_orthogonal(int n, std::uint64_t seed);
 void jacobi_eig(const Mat& a, std::vector<double>& evals_desc, Mat& evecs);
 double subspace_gap(const Mat& a, const Mat& b);                 // oracles.hpp:195-227
 
+// ---- metrics (src/metrics.cpp:59-159) ----
+struct Report {                // ComparisonReport (metrics.hpp:19-27)
+    std::vector<double> rho;
+    std::vector<bool> flipped, tied;
+    std::vector<double> tie_sin;
+    double accuracy_exact = 0.0, accuracy_mach = 0.0;
+    double core_exact = 0.0, core_mach = 0.0;
+};
+double pearson(const std::vector<double>& x, const std::vector<double>& y);                  // :67-96
+double pc_correlation(const Model& exact, const Model& approx, int mode, int component, bool* flipped);  // :98-122
+Report compare(const Model& exact, const Model& approx, const Dense& reference);             // :124-159
+
 // Per-phase timing of the last hooi() call (seconds), for the CPU baseline.
 struct PhaseTimes { double sample = 0, hosvd = 0; std::vector<double> sweeps; };
 PhaseTimes& last_phase_times();

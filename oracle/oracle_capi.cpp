@@ -214,6 +214,32 @@ int orc_mach_hosvd(void* dense, const int* ranks, double p, unsigned long long s
         *sparse_out = new Sparse(std::move(r.sparsified));
     });
 }
+int orc_pearson(int n, const double* x, const double* y, double* out) {
+    return guard([&] { *out = pearson(std::vector<double>(x, x + n), std::vector<double>(y, y + n)); });
+}
+int orc_pc_correlation(void* a, void* b, int mode, int component, double* out, int* flipped) {
+    return guard([&] {
+        bool f = false;
+        *out = pc_correlation(*static_cast<Model*>(a), *static_cast<Model*>(b), mode, component, &f);
+        *flipped = f ? 1 : 0;
+    });
+}
+int orc_compare(void* a, void* b, void* ref, double* rho, int* flipped, int* tied, double* tie_sin, double* acc2,
+                double* core2) {
+    return guard([&] {
+        Report r = compare(*static_cast<Model*>(a), *static_cast<Model*>(b), *static_cast<Dense*>(ref));
+        for (std::size_t m = 0; m < r.rho.size(); ++m) {
+            rho[m] = r.rho[m];
+            flipped[m] = r.flipped[m] ? 1 : 0;
+            tied[m] = r.tied[m] ? 1 : 0;
+            tie_sin[m] = r.tie_sin[m];
+        }
+        acc2[0] = r.accuracy_exact;
+        acc2[1] = r.accuracy_mach;
+        core2[0] = r.core_exact;
+        core2[1] = r.core_mach;
+    });
+}
 int orc_accuracy(void* dense, void* model, double* out) {
     return guard([&] { *out = accuracy(*static_cast<Dense*>(dense), *static_cast<Model*>(model)); });
 }

@@ -23,6 +23,7 @@ from .api import (  # noqa: F401
     truncated_svd,
     accuracy,
     comm_unique_id,
+    compare,
     default_context,
     hooi,
     kernel_stats,
@@ -35,9 +36,12 @@ from .api import (  # noqa: F401
     mach_hosvd,
     mode_gram,
     mode_product,
+    pc_correlation,
+    pearson,
     reconstruct,
     sparsify,
     sparsify_slab,
+    subspace_sin,
 )
 
 __version__ = "0.1.0"

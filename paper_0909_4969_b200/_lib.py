@@ -100,6 +100,8 @@ _SIGS = {
     "mach_comm_unique_id": (C.c_int, [C.c_char_p]),
     "mach_ctx_comm_init": (C.c_int, [vp, C.c_int, C.c_int, C.c_char_p]),
     "mach_hooi_shard": (C.c_int, [vp]),
+    "mach_model_accuracy": (C.c_int, [vp, vp, ip, dp, C.POINTER(dp), dp]),
+    "mach_subspace_sin": (C.c_int, [vp, C.c_int, C.c_int, dp, dp, dp]),
     "mach_truncated_svd": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int, dp, dp, dp]),
     "mach_low_rank_approx": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int, dp]),
 }

@@ -415,15 +415,115 @@ def reconstruct(model: TuckerModel, ctx: Context | None = None) -> np.ndarray:
 
 
 def accuracy(t, model: TuckerModel, ctx: Context | None = None) -> float:
-    """tucker.hpp:55 — 1 - |t - reconstruct(model)| / |t|."""
-    x = t.numpy() if isinstance(t, DenseTensor) else np.asarray(t, dtype=np.float64)
-    nt = float(np.sqrt((x.astype(np.float64) ** 2).sum()))
-    if nt == 0.0:
-        raise ArgumentError("accuracy needs a reference tensor with nonzero norm")
-    rec = reconstruct(model, ctx)
-    if rec.shape != x.shape:
+    """tucker.hpp:55 — 1 - |t - reconstruct(model)| / |t|, one fused device
+    pass over t (the reconstruction is never materialised)."""
+    d = _dense(t, ctx)
+    if len(model.factors) != len(d.dims) or any(f.shape[0] != n for f, n in zip(model.factors, d.dims)):
         raise ShapeError("model reconstructs to a different shape")
-    return 1.0 - float(np.sqrt(((x - rec) ** 2).sum())) / nt
+    core = np.ascontiguousarray(np.asarray(model.core, dtype=np.float64).reshape(-1, order="F"))
+    fs = [np.ascontiguousarray(np.asarray(f, dtype=np.float64).reshape(-1, order="F")) for f in model.factors]
+    fp = (L.dp * len(fs))(*[f.ctypes.data_as(L.dp) for f in fs])
+    out = C.c_double()
+    _check(L.lib().mach_model_accuracy(d.ctx.h, d.h, _ranks(model.ranks, len(d.dims)), core.ctypes.data_as(L.dp), fp,
+                                       C.byref(out)))
+    return out.value
+
+
+def subspace_sin(a: np.ndarray, b: np.ndarray, r: int | None = None, ctx: Context | None = None) -> float:
+    """metrics.cpp:59-66 — largest principal-angle sine between the spans of
+    the leading r columns of a and b (on the device)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    r = min(a.shape[1], b.shape[1]) if r is None else int(r)
+    if a.shape[0] != b.shape[0]:
+        raise ShapeError("subspace_sin needs matrices with the same rows")
+    fa = np.ascontiguousarray(a[:, :r].reshape(-1, order="F"))
+    fb = np.ascontiguousarray(b[:, :r].reshape(-1, order="F"))
+    out = C.c_double()
+    _check(L.lib().mach_subspace_sin(_ctx(ctx).h, a.shape[0], r, fa.ctypes.data_as(L.dp), fb.ctypes.data_as(L.dp),
+                                     C.byref(out)))
+    return out.value
+
+
+def _pairwise(v: np.ndarray) -> float:
+    """internal.hpp:36-46 cascade (base 64) — the reference's summation order."""
+    n = v.size
+    if n <= 64:
+        s = 0.0
+        for x in v.tolist():
+            s += x
+        return s
+    mid = n // 2
+    return _pairwise(v[:mid]) + _pairwise(v[mid:])
+
+
+def pearson(x, y) -> float:
+    """metrics.cpp:67-96 (same summation order and errors)."""
+    x = np.asarray(x, dtype=np.float64).ravel()
+    y = np.asarray(y, dtype=np.float64).ravel()
+    if x.size != y.size:
+        raise ShapeError(f"correlation inputs have lengths {x.size} and {y.size}")
+    n = x.size
+    if n < 2:
+        raise ArgumentError("correlation needs at least 2 samples")
+    if np.all(x == x[0]) or np.all(y == y[0]):
+        raise ArgumentError("correlation is undefined for a zero-variance input")
+    mx = _pairwise(x) / n
+    my = _pairwise(y) / n
+    dx, dy = x - mx, y - my
+    sxx, syy, sxy = _pairwise(dx * dx), _pairwise(dy * dy), _pairwise(dx * dy)
+    if sxx == 0.0 or syy == 0.0:
+        raise ArgumentError("correlation is undefined for a zero-variance input")
+    return sxy / float(np.sqrt(sxx * syy))
+
+
+def pc_correlation(exact: TuckerModel, approx: TuckerModel, mode: int, component: int = 1):
+    """metrics.cpp:98-122 — (rho, flipped)."""
+    if len(exact.factors) != len(approx.factors):
+        raise ShapeError("models have different orders")
+    if not 0 <= mode < len(exact.factors):
+        raise ArgumentError(f"mode {mode + 1} out of range for order {len(exact.factors)}")
+    limit = min(exact.ranks[mode], approx.ranks[mode])
+    if not 1 <= component <= limit:
+        raise ArgumentError(f"component {component} out of range; mode {mode + 1} has at most {limit} shared components")
+    a = np.asarray(exact.factors[mode][:, component - 1], dtype=np.float64)
+    b = np.asarray(approx.factors[mode][:, component - 1], dtype=np.float64)
+    if a.size != b.size:
+        raise ShapeError("factor columns of different lengths")
+    flip = _pairwise(a * b) < 0.0
+    return pearson(a, -b if flip else b), bool(flip)
+
+
+def compare(exact: TuckerModel, approx: TuckerModel, reference, ctx: Context | None = None) -> dict:
+    """metrics.cpp:124-159 (ComparisonReport): component-1 correlations per
+    mode, tie detection from the core slice norms with the subspace sine,
+    both accuracies (fused device passes), the leading core entries."""
+    ref = _dense(reference, ctx)
+    d = len(ref.dims)
+    if len(exact.factors) != d or len(approx.factors) != d:
+        raise ShapeError("reference and models have different orders")
+    rep = {"per_mode_rho": [], "flipped": [], "tied": [], "tie_subspace_sin": []}
+
+    def slice_norms(core, m):
+        return np.sqrt((np.moveaxis(np.asarray(core), m, 0).reshape(core.shape[m], -1) ** 2).sum(axis=1))
+
+    def tied(n):
+        n = np.sort(n)[::-1]
+        return n.size >= 2 and n[0] - n[1] <= 1e-6 * n[0]
+
+    for m in range(d):
+        rho, fl = pc_correlation(exact, approx, m, 1)
+        rep["per_mode_rho"].append(rho)
+        rep["flipped"].append(fl)
+        t = tied(slice_norms(exact.core, m)) or tied(slice_norms(approx.core, m))
+        rep["tied"].append(bool(t))
+        r = min(exact.ranks[m], approx.ranks[m])
+        rep["tie_subspace_sin"].append(subspace_sin(exact.factors[m], approx.factors[m], r, ctx) if t else 0.0)
+    rep["accuracy_exact"] = accuracy(ref, exact)
+    rep["accuracy_mach"] = accuracy(ref, approx)
+    rep["core_interaction"] = (float(np.asarray(exact.core).reshape(-1, order="F")[0]),
+                               float(np.asarray(approx.core).reshape(-1, order="F")[0]))
+    return rep
 
 
 def mode_product(t, m: np.ndarray, mode: int, ctx: Context | None = None, keep_on_device=False):

@@ -2,6 +2,7 @@
 // maps the error to a mach_status and stores the message thread-locally; no
 // exception crosses the boundary.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -500,6 +501,64 @@ mach_status mach_left_singular_basis(mach_ctx* ctx, int rows, int cols, const do
         need(ctx, "ctx");
         DevGuard dg_(ctx->c.device);
         lsb_host(&ctx->c, rows, cols, a, k, basis, sv, numerical_rank, completed);
+    });
+}
+
+mach_status mach_model_accuracy(mach_ctx* ctx, const mach_dense* t, const int* ranks, const double* core,
+                                const double* const* factors, double* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
+        need(t, "tensor");
+        need(ranks, "ranks");
+        need(core, "core");
+        need(factors, "factors");
+        need(out, "out");
+        Ctx* c = &ctx->c;
+        const int d = static_cast<int>(t->dims.size());
+        std::vector<int> rk(ranks, ranks + d);
+        std::int64_t cn = 1;
+        for (int m = 0; m < d; ++m) {
+            if (rk[static_cast<std::size_t>(m)] < 1) throw_arg("ranks must be >= 1");
+            cn *= rk[static_cast<std::size_t>(m)];
+        }
+        DBuf<double> red(c, sumsq_scratch()), scal(c, 1), G(c, static_cast<std::size_t>(cn));
+        if (t->dtype == MACH_F32) sumsq<float>(c, static_cast<const float*>(t->data), t->numel, red.get(), scal.get());
+        else sumsq<double>(c, static_cast<const double*>(t->data), t->numel, red.get(), scal.get());
+        double n2 = 0.0;
+        to_host(c, &n2, scal.get(), 1);
+        sync(c);
+        if (n2 == 0.0) throw_arg("accuracy needs a reference tensor with nonzero norm");
+        to_device(c, G.get(), core, G.n);
+        std::vector<DBuf<double>> U(static_cast<std::size_t>(d));
+        std::vector<const double*> up;
+        for (int m = 0; m < d; ++m) {
+            need(factors[m], "factor");
+            const std::size_t n = static_cast<std::size_t>(t->dims[static_cast<std::size_t>(m)]) * rk[static_cast<std::size_t>(m)];
+            U[static_cast<std::size_t>(m)].alloc(c, n);
+            to_device(c, U[static_cast<std::size_t>(m)].get(), factors[m], n);
+            up.push_back(U[static_cast<std::size_t>(m)].get());
+        }
+        const double e2 = t->dtype == MACH_F32
+                              ? residual2_fused<float>(c, static_cast<const float*>(t->data), t->dims, rk, G.get(), up)
+                              : residual2_fused<double>(c, static_cast<const double*>(t->data), t->dims, rk, G.get(), up);
+        *out = 1.0 - std::sqrt(e2) / std::sqrt(n2);
+    });
+}
+
+mach_status mach_subspace_sin(mach_ctx* ctx, int n, int r, const double* a, const double* b, double* out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
+        need(a, "a");
+        need(b, "b");
+        need(out, "out");
+        if (n < 1 || r < 1 || r > n) throw_arg("subspace_sin needs 1 <= r <= n");
+        Ctx* c = &ctx->c;
+        DBuf<double> A(c, static_cast<std::size_t>(n) * r), B(c, static_cast<std::size_t>(n) * r);
+        to_device(c, A.get(), a, A.n);
+        to_device(c, B.get(), b, B.n);
+        *out = subspace_sin_dev(c, A.get(), B.get(), n, r);
     });
 }
 

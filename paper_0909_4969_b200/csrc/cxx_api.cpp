@@ -12,6 +12,7 @@
 
 #include "mach/errors.hpp"
 #include "mach/linalg.hpp"
+#include "mach/metrics.hpp"
 #include "mach/sampling.hpp"
 #include "mach/tensor.hpp"
 #include "mach/tucker.hpp"
@@ -414,16 +415,133 @@ DenseTensor reconstruct(const TuckerModel& model) {
     return y;
 }
 
+// accuracy (tucker.cpp:211-217): one fused device pass over t, the
+// reconstruction is never materialised (metrics.cu)
 double accuracy(const DenseTensor& t, const TuckerModel& model) {
-    const double nt = tensor_norm(t);
-    if (nt == 0.0) throw ArgumentError("accuracy needs a reference tensor with nonzero norm");
-    DenseTensor rec = reconstruct(model);
-    if (rec.dims() != t.dims()) throw ShapeError("model reconstructs to a different shape");
-    const double s = pairwise_sum(0, t.size(), [&](std::int64_t i) {
-        const double d = t.data()[i] - rec.data()[i];
+    if (static_cast<int>(model.factors.size()) != t.order()) throw ShapeError("model reconstructs to a different shape");
+    for (int m = 0; m < t.order(); ++m)
+        if (model.factors[static_cast<std::size_t>(m)].rows() != t.dim(m))
+            throw ShapeError("model reconstructs to a different shape");
+    DenseH h(t);
+    std::vector<const double*> f;
+    for (const Matrix& u : model.factors) f.push_back(u.data());
+    double out = 0.0;
+    rethrow(mach_model_accuracy(ctx(), h.h, model.ranks.data(), model.core.data(), f.data(), &out));
+    return out;
+}
+
+// ---- metrics.hpp (metrics.cpp:15-159) ----
+namespace {
+constexpr double kTieGap = 1e-6;  // metrics.cpp:19
+
+void check_same_shape(const TuckerModel& a, const TuckerModel& b) {
+    if (a.factors.size() != b.factors.size())
+        throw ShapeError("models have orders " + std::to_string(a.factors.size()) + " and " + std::to_string(b.factors.size()));
+    for (std::size_t m = 0; m < a.factors.size(); ++m)
+        if (a.factors[m].rows() != b.factors[m].rows())
+            throw ShapeError("mode " + std::to_string(m + 1) + " has " + std::to_string(a.factors[m].rows()) +
+                             " rows in one model and " + std::to_string(b.factors[m].rows()) + " in the other");
+}
+
+std::vector<double> core_slice_norms(const DenseTensor& core, int mode) {
+    std::int64_t stride = 1;
+    for (int m = 0; m < mode; ++m) stride *= core.dim(m);
+    const std::int64_t len = core.dim(mode);
+    std::vector<double> sq(static_cast<std::size_t>(len), 0.0);
+    for (std::int64_t i = 0; i < core.size(); ++i) sq[static_cast<std::size_t>((i / stride) % len)] += core.data()[i] * core.data()[i];
+    for (double& v : sq) v = std::sqrt(v);
+    return sq;
+}
+
+bool top_two_tied(std::vector<double> n) {
+    if (n.size() < 2) return false;
+    std::sort(n.begin(), n.end(), std::greater<>());
+    return n[0] - n[1] <= kTieGap * n[0];
+}
+}  // namespace
+
+double pearson(std::span<const double> x, std::span<const double> y) {
+    if (x.size() != y.size())
+        throw ShapeError("correlation inputs have lengths " + std::to_string(x.size()) + " and " + std::to_string(y.size()));
+    const std::int64_t n = static_cast<std::int64_t>(x.size());
+    if (n < 2) throw ArgumentError("correlation needs at least 2 samples");
+    const bool xc = std::all_of(x.begin(), x.end(), [&](double v) { return v == x[0]; });
+    const bool yc = std::all_of(y.begin(), y.end(), [&](double v) { return v == y[0]; });
+    if (xc || yc) throw ArgumentError("correlation is undefined for a zero-variance input");
+    const double mx = pairwise_sum(0, n, [&](std::int64_t i) { return x[static_cast<std::size_t>(i)]; }) / static_cast<double>(n);
+    const double my = pairwise_sum(0, n, [&](std::int64_t i) { return y[static_cast<std::size_t>(i)]; }) / static_cast<double>(n);
+    const double sxx = pairwise_sum(0, n, [&](std::int64_t i) {
+        const double d = x[static_cast<std::size_t>(i)] - mx;
         return d * d;
     });
-    return 1.0 - std::sqrt(s) / nt;
+    const double syy = pairwise_sum(0, n, [&](std::int64_t i) {
+        const double d = y[static_cast<std::size_t>(i)] - my;
+        return d * d;
+    });
+    const double sxy = pairwise_sum(0, n, [&](std::int64_t i) {
+        return (x[static_cast<std::size_t>(i)] - mx) * (y[static_cast<std::size_t>(i)] - my);
+    });
+    if (sxx == 0.0 || syy == 0.0) throw ArgumentError("correlation is undefined for a zero-variance input");
+    return sxy / std::sqrt(sxx * syy);
+}
+
+double pc_correlation(const TuckerModel& exact, const TuckerModel& approx, int mode, int component, bool* flipped) {
+    check_same_shape(exact, approx);
+    const int d = static_cast<int>(exact.factors.size());
+    if (mode < 0 || mode >= d)
+        throw ArgumentError("mode " + std::to_string(mode + 1) + " out of range for order " + std::to_string(d));
+    const int limit = std::min(exact.ranks[static_cast<std::size_t>(mode)], approx.ranks[static_cast<std::size_t>(mode)]);
+    if (component < 1 || component > limit)
+        throw ArgumentError("component " + std::to_string(component) + " out of range; mode " + std::to_string(mode + 1) +
+                            " has at most " + std::to_string(limit) + " shared components");
+    const Matrix& fa = exact.factors[static_cast<std::size_t>(mode)];
+    const Matrix& fb = approx.factors[static_cast<std::size_t>(mode)];
+    const std::span<const double> a(fa.data() + static_cast<std::size_t>(component - 1) * fa.rows(), static_cast<std::size_t>(fa.rows()));
+    const std::span<const double> b(fb.data() + static_cast<std::size_t>(component - 1) * fb.rows(), static_cast<std::size_t>(fb.rows()));
+    const double dot = pairwise_sum(0, static_cast<std::int64_t>(a.size()),
+                                    [&](std::int64_t i) { return a[static_cast<std::size_t>(i)] * b[static_cast<std::size_t>(i)]; });
+    const bool flip = dot < 0.0;
+    if (flipped) *flipped = flip;
+    if (!flip) return pearson(a, b);
+    std::vector<double> aligned(b.begin(), b.end());
+    for (double& v : aligned) v = -v;
+    return pearson(a, aligned);
+}
+
+ComparisonReport compare(const TuckerModel& exact, const TuckerModel& approx, const DenseTensor& reference) {
+    check_same_shape(exact, approx);
+    if (reference.order() != static_cast<int>(exact.factors.size()))
+        throw ShapeError("reference has order " + std::to_string(reference.order()) + ", models have order " +
+                         std::to_string(exact.factors.size()));
+    for (int m = 0; m < reference.order(); ++m)
+        if (reference.dim(m) != exact.factors[static_cast<std::size_t>(m)].rows())
+            throw ShapeError("mode " + std::to_string(m + 1) + " has " + std::to_string(reference.dim(m)) +
+                             " entries in the reference and " +
+                             std::to_string(exact.factors[static_cast<std::size_t>(m)].rows()) + " in the models");
+    const int d = reference.order();
+    ComparisonReport rep;
+    rep.per_mode_rho.resize(static_cast<std::size_t>(d));
+    rep.flipped.assign(static_cast<std::size_t>(d), false);
+    rep.tied.assign(static_cast<std::size_t>(d), false);
+    rep.tie_subspace_sin.assign(static_cast<std::size_t>(d), 0.0);
+    for (int m = 0; m < d; ++m) {
+        bool flip = false;
+        rep.per_mode_rho[static_cast<std::size_t>(m)] = pc_correlation(exact, approx, m, 1, &flip);
+        rep.flipped[static_cast<std::size_t>(m)] = flip;
+        if (top_two_tied(core_slice_norms(exact.core, m)) || top_two_tied(core_slice_norms(approx.core, m))) {
+            rep.tied[static_cast<std::size_t>(m)] = true;
+            const int r = std::min(exact.ranks[static_cast<std::size_t>(m)], approx.ranks[static_cast<std::size_t>(m)]);
+            double s = 0.0;
+            rethrow(mach_subspace_sin(ctx(), exact.factors[static_cast<std::size_t>(m)].rows(), r,
+                                      exact.factors[static_cast<std::size_t>(m)].data(),
+                                      approx.factors[static_cast<std::size_t>(m)].data(), &s));
+            rep.tie_subspace_sin[static_cast<std::size_t>(m)] = s;
+        }
+    }
+    rep.accuracy_exact = accuracy(reference, exact);
+    rep.accuracy_mach = accuracy(reference, approx);
+    rep.core_interaction = {exact.core.data()[0], approx.core.data()[0]};
+    return rep;
 }
 
 // ---- linalg.hpp ----

@@ -106,4 +106,49 @@ template double residual2_fused<float>(Ctx*, const float*, const std::vector<int
 template double residual2_fused<double>(Ctx*, const double*, const std::vector<int>&, const std::vector<int>&,
                                         const double*, const std::vector<const double*>&);
 
+namespace {
+// subspace_sin (metrics.cpp:59-66): M = A - B (B^T A) over the leading r
+// columns, H = M^T M (r x r) for the exact eigensolver; one CTA
+__global__ void __launch_bounds__(256) ortho_residual_gram_kernel(const double* __restrict__ A, const double* __restrict__ Bm,
+                                                                  int n, int r, double* __restrict__ M,
+                                                                  double* __restrict__ H) {
+    __shared__ double Cs[32 * 32];
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+        const int l = e % r, j = e / r;
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s = fma(Bm[i + static_cast<long long>(n) * l], A[i + static_cast<long long>(n) * j], s);
+        Cs[l + 32 * j] = s;
+    }
+    __syncthreads();
+    for (long long e = threadIdx.x; e < static_cast<long long>(n) * r; e += blockDim.x) {
+        const int i = static_cast<int>(e % n), j = static_cast<int>(e / n);
+        double v = A[e];
+        for (int l = 0; l < r; ++l) v = fma(-Bm[i + static_cast<long long>(n) * l], Cs[l + 32 * j], v);
+        M[e] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+        const int a = e % r, b = e / r;
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s = fma(M[i + static_cast<long long>(n) * a], M[i + static_cast<long long>(n) * b], s);
+        H[a + r * b] = s;
+    }
+}
+}  // namespace
+
+// largest principal-angle sine between the spans of the leading r columns of
+// A and B (n x >= r, column-major, device)
+double subspace_sin_dev(Ctx* ctx, const double* A, const double* Bm, int n, int r) {
+    if (r < 1 || r > 32) throw_arg("subspace_sin: 1 <= r <= 32");
+    DBuf<double> M(ctx, static_cast<std::size_t>(n) * r), H(ctx, static_cast<std::size_t>(r) * r), V(ctx, static_cast<std::size_t>(r)),
+        sig(ctx, 1), work(ctx, eig_work_doubles(r, 1));
+    DBuf<int> st(ctx, 3);
+    MB_LAUNCH(ctx, ortho_residual_gram_kernel, 1, 256, 0, A, Bm, n, r, M.get(), H.get());
+    eig_topk(ctx, H.get(), r, 1, work.get(), V.get(), sig.get(), st.get());
+    double s = 0.0;
+    to_host(ctx, &s, sig.get(), 1);
+    sync(ctx);
+    return s;  // sqrt(max(0, lambda_max)) as metrics.cpp:65
+}
+
 }  // namespace machb

@@ -246,6 +246,7 @@ void sparse_mode_product(Ctx* ctx, const mach_sparse* s, int mode, const double*
 template <typename T>
 double residual2_fused(Ctx* ctx, const T* x, const std::vector<int>& dims, const std::vector<int>& ranks,
                        const double* core, const std::vector<const double*>& U);
+double subspace_sin_dev(Ctx* ctx, const double* A, const double* B, int n, int r);
 // truncated_svd family on the device (tsvd.cu); A rows x cols column-major
 void truncated_svd_dev(Ctx* ctx, const double* A, int rows, int cols, int k, double* left, double* sv, double* right);
 void low_rank_dev(Ctx* ctx, const double* L, const double* sv, const double* R, int rows, int cols, int k, double* out);

@@ -22,6 +22,11 @@ CONFIGS = {
     "c3": ((128, 128, 64, 256), (8, 8, 8, 8), 0.02, 0.02, 5, "float32"),
     "c4": ((1000, 64, 65536), (10, 6, 20), 0.05, 0.01, 3, "float32"),
     "c5": ((1024, 1024, 1024), (16, 16, 16), 0.01, 0.1, 5, "float32"),
+    # C5's sampling-rate sweep: p = 1 takes the dense route (tcgen05 Gram and
+    # mode products), the others the sparse route
+    "c5p1": ((1024, 1024, 1024), (16, 16, 16), 0.01, 1.0, 5, "float32"),
+    "c5p01": ((1024, 1024, 1024), (16, 16, 16), 0.01, 0.01, 5, "float32"),
+    "c5p001": ((1024, 1024, 1024), (16, 16, 16), 0.01, 0.001, 5, "float32"),
 }
 
 

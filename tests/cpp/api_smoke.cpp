@@ -9,6 +9,7 @@
 
 #include "mach/errors.hpp"
 #include "mach/linalg.hpp"
+#include "mach/metrics.hpp"
 #include "mach/sampling.hpp"
 #include "mach/tensor.hpp"
 #include "mach/tucker.hpp"
@@ -86,6 +87,14 @@ int main() {
         threw = true;
     }
     CHECK(threw);
+    // metrics.hpp: the reference model against the MACH one
+    const ComparisonReport rep = compare(m, r.model, t);
+    CHECK(rep.per_mode_rho.size() == 3 && rep.flipped.size() == 3 && rep.tied.size() == 3);
+    for (double rho : rep.per_mode_rho) CHECK(rho >= -1.0 && rho <= 1.0);
+    CHECK(std::abs(rep.accuracy_exact - accuracy(t, m)) < 1e-14);
+    CHECK(rep.core_interaction.first == m.core.data()[0]);
+    const std::vector<double> px{1.0, 2.0, 3.0}, py{2.0, 4.0, 6.0};
+    CHECK(pearson(px, py) == 1.0);
     std::printf("api_smoke: %d failures\n", failures);
     return failures;
 }
