@@ -97,6 +97,7 @@ __host__ __device__ constexpr int frag_stride(int w) { return w + ((4 - w % 16) 
 // fine-grained phase stamps inside the small-matrix helpers (debug builds of
 // the timing probe only: g_stamp is null unless MACH_DEBUG_EIG_T is set)
 __device__ long long* g_stamp = nullptr;
+__device__ int g_dbg_eig = 0;  // MACH_DEBUG_EIGC: iteration printouts of the one-CTA solver
 __device__ int g_stamp_n = 0;
 __device__ __forceinline__ void sub_stamp(int tag) {
     if (g_stamp && threadIdx.x == 0 && g_stamp_n < 100) {
@@ -118,11 +119,15 @@ struct Sub {
     // OUT = a (G IN) + b1 P1 + b2 P2 over npad rows (rows >= n stay zero: G's
     // padding is zero).  Warp per 8-row tile, all column tiles, fp64 MMA.
     // OUT may alias P1 or P2 (a fragment is read and written by one lane).
+    // [rt0, rt1): the 8-row tiles this CTA computes (all of them by default;
+    // a slice of them in the cluster-distributed solver, where G, OUT, P1, P2
+    // are row slices addressed with absolute row indices)
     __device__ static void gemm(const double* G, int ldg, const double* IN, double* OUT, int npad, double a,
-                                const double* P1, double b1, const double* P2, double b2) {
+                                const double* P1, double b1, const double* P2, double b2, int rt0 = 0, int rt1 = -1) {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int gr = lane >> 2, tq = lane & 3;
-        for (int rt = warp; rt < (npad >> 3); rt += kWarps) {
+        if (rt1 < 0) rt1 = npad >> 3;
+        for (int rt = rt0 + warp; rt < rt1; rt += kWarps) {
             double c[CT][2];
 #pragma unroll
             for (int t = 0; t < CT; ++t) c[t][0] = c[t][1] = 0.0;
@@ -173,7 +178,9 @@ struct Sub {
     // C (B x B, ld HS) = A^T M over npad rows; 8x8 output tiles on the fp64
     // MMA, the row range split into KG interleaved groups when there are
     // fewer tiles than warps, partials summed in a fixed order.
-    __device__ static void gram(const double* A, const double* M, double* C, int npad) {
+    // rows [r0, r1) only when given (multiples of 4; the distributed solver's
+    // partial Gram over its row slice)
+    __device__ static void gram(const double* A, const double* M, double* C, int npad, int r0 = 0, int r1 = -1) {
         constexpr int NT = CT * CT;
         constexpr int KG = (kWarps / NT) > 0 ? kWarps / NT : 1;
         constexpr int TW = kWarps / KG;  // warps per k-group
@@ -181,14 +188,14 @@ struct Sub {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int gr = lane >> 2, tq = lane & 3;
         const int kg = warp % KG;
-        const int KS = npad >> 2;
+        const int KS = (r1 < 0 ? npad : r1) >> 2, KS0 = r0 >> 2;
         for (int t = warp / KG; t < NT; t += TW) {
             const int ti = t % CT, tj = t / CT;
             double c0 = 0.0, c1 = 0.0;
             const double* ap = A + tq * XS + ti * 8 + gr;
             const double* mp = M + tq * XS + tj * 8 + gr;
 #pragma unroll 4
-            for (int ks = kg; ks < KS; ks += KG) dmma(c0, c1, ap[ks * 4 * XS], mp[ks * 4 * XS]);
+            for (int ks = KS0 + kg; ks < KS; ks += KG) dmma(c0, c1, ap[ks * 4 * XS], mp[ks * 4 * XS]);
             if (KG == 1) {
                 C[(ti * 8 + gr) + (tj * 8 + 2 * tq) * HS] = c0;
                 C[(ti * 8 + gr) + (tj * 8 + 2 * tq + 1) * HS] = c1;
@@ -212,10 +219,11 @@ struct Sub {
     }
 
     // OUT = X W (npad x B)(B x B); warp per 8-row tile, fp64 MMA
-    __device__ static void rotate(const double* X, const double* W, double* OUT, int npad) {
+    __device__ static void rotate(const double* X, const double* W, double* OUT, int npad, int rt0 = 0, int rt1 = -1) {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int gr = lane >> 2, tq = lane & 3;
-        for (int rt = warp; rt < (npad >> 3); rt += kWarps) {
+        if (rt1 < 0) rt1 = npad >> 3;
+        for (int rt = rt0 + warp; rt < rt1; rt += kWarps) {
             double c[CT][2];
 #pragma unroll
             for (int t = 0; t < CT; ++t) c[t][0] = c[t][1] = 0.0;
@@ -241,11 +249,28 @@ struct Sub {
     // latter should decide breakdown.
     __device__ static bool cholqr(double*& X, double*& T, double* S, double* Ri, double* rinv, int npad, int* flag,
                                   bool allow_skip = false) {
-        __shared__ double dn[kMaxB];
-        __shared__ int near_identity;
         sub_stamp(500);
         gram(X, X, S, npad);
         sub_stamp(501);
+        bool skip = false;
+        if (!chol_factor(S, Ri, rinv, flag, allow_skip, skip)) return false;
+        if (skip) return true;
+        sub_stamp(504);
+        rotate(X, Ri, T, npad);
+        sub_stamp(505);
+        double* t = X;
+        X = T;
+        T = t;
+        return true;
+    }
+
+    // the small part of CholQR on S = X^T X (B x B): equilibration, Cholesky,
+    // Ri = D R^{-1}.  False on breakdown; skip = S was already the identity
+    // to 1e-14 (with allow_skip).  Uniform across the CTA.
+    __device__ static bool chol_factor(double* S, double* Ri, double* rinv, int* flag, bool allow_skip, bool& skip) {
+        __shared__ double dn[kMaxB];
+        __shared__ int near_identity;
+        skip = false;
         if (threadIdx.x == 0) {
             *flag = 1;
             near_identity = 1;
@@ -261,7 +286,10 @@ struct Sub {
                 if (!(fabs(S[l + m * HS] - (l == m ? 1.0 : 0.0)) <= 1e-14)) near_identity = 0;
             }
             __syncthreads();
-            if (near_identity) return true;
+            if (near_identity) {
+                skip = true;
+                return true;
+            }
         }
         for (int e = threadIdx.x; e < B * B; e += kThreads) {
             const int l = e % B, m = e / B;
@@ -312,12 +340,6 @@ struct Sub {
             for (int r = 0; r < B; ++r) Ri[r + c * HS] = x[r] * dn[r];
         }
         __syncthreads();
-        sub_stamp(504);
-        rotate(X, Ri, T, npad);
-        sub_stamp(505);
-        double* t = X;
-        X = T;
-        T = t;
         return true;
     }
 
@@ -713,6 +735,8 @@ __device__ double* subspace_core(SubWs<B>& ws, const double* G, int ldg, int n, 
         // ---- residual certificate for the wanted k ----
         const double rmax = SB::residual(X, AX, th, n, k, red);
         const double scale = fmax(fabs(th[0]), 1e-300);
+        if (g_dbg_eig && threadIdx.x == 0 && blockIdx.x == 0)
+            printf("[eig1] it %d th0 %.6e thB %.6e rmax/scale %.3e\n", it, th[0], th[B - 1], rmax / scale);
         MB_STAMP(14);
         if (rmax <= tol * scale) { conv = true; break; }
         if (it >= maxit) break;
@@ -758,6 +782,7 @@ __device__ double* subspace_core(SubWs<B>& ws, const double* G, int ldg, int n, 
         }
         MB_STAMP(15);
         SB::orthonormalize(X, Y0, n, npad, S, Z, rinv, coef, red, &flag);
+        if (g_dbg_eig && threadIdx.x == 0 && blockIdx.x == 0) printf("[eig1] it %d ortho flag %d\n", it, flag);
         MB_STAMP(16);
     }
     MB_STAMP(99);

@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "eig_cluster.cuh"
 #include "eig_sub.cuh"
 
 namespace machb {
@@ -179,6 +180,8 @@ bool launch_subspace_jobs(Ctx* ctx, std::vector<EigJob>& jobs, std::vector<DBuf<
     EigJobs dj{};
     for (std::size_t i = 0; i < jobs.size(); ++i) dj.j[i] = jobs[i];
     static const bool dbg = std::getenv("MACH_DEBUG_EIG_T") != nullptr;
+    static const int dbgc = std::getenv("MACH_DEBUG_EIGC") ? 1 : 0;
+    if (dbgc) MB_CUDA(cudaMemcpyToSymbolAsync(g_dbg_eig, &dbgc, sizeof(int), 0, cudaMemcpyHostToDevice, ctx->stream));
     DBuf<long long> ts;
     if (dbg) {
         ts.alloc(ctx, 240);
@@ -240,9 +243,71 @@ bool subspace_applies(int n, int k) {
     return n > kSubMinN && b < n && b <= kMaxB && (b % 8) == 0 && k <= b - 2;
 }
 
+// Cluster-distributed solver (eig_cluster.cuh) for a G that does not fit one
+// CTA; false when it does not apply either.
+template <int B>
+bool launch_cluster(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, double* V,
+                    double* sig, int* status) {
+    static const bool off = std::getenv("MACH_NO_EIG_CLUSTER") != nullptr;
+    if (off) return false;
+    const std::size_t smem = ClusterLayout<B>::doubles(n) * sizeof(double);
+    static int optin = 0;
+    static std::uint64_t attr = 0;
+    auto kern = eig_cluster_kernel<B>;
+    if (first_on_device(attr, ctx->device)) {
+        cudaFuncAttributes fa{};
+        MB_CUDA(cudaFuncGetAttributes(&fa, kern));
+        int mx = 0;
+        MB_CUDA(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+        optin = mx - static_cast<int>(fa.sharedSizeBytes);
+        MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    }
+    if (smem > static_cast<std::size_t>(optin)) return false;
+    const double* th0 = (X0 && x0_cols >= B) ? X0 + static_cast<std::size_t>(n) * B : nullptr;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kECL, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kECL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static const int dbg = std::getenv("MACH_DEBUG_EIGC") ? 1 : 0;
+    MB_LAUNCH_EX(ctx, "eig_cluster_kernel<B>", &cfg, kern, G, n, k, X0, x0_cols, th0, Xkeep, V, sig, status, 4, 40,
+                 1e-12, dbg);
+    return true;
+}
+
 bool eig_select(Ctx* ctx, const double* G, int n, int k, const double* X0, int x0_cols, double* Xkeep, int b,
                 double* V, double* sig, int* status) {
     bool launched = false;
+    if (n > kSubMinN && b < n && b <= kMaxB && (b % 8) == 0 && k <= b - 2) {
+        bool gs = true, bs = true;
+        switch (b) {
+            case 8: job_plan<8>(n, gs, bs); break;
+            case 16: job_plan<16>(n, gs, bs); break;
+            case 24: job_plan<24>(n, gs, bs); break;
+            default: job_plan<32>(n, gs, bs); break;
+        }
+        if (!gs || !bs) {  // G or the blocks would live in L2: the cluster solver instead
+            switch (b) {
+                case 8: launched = launch_cluster<8>(ctx, G, n, k, X0, x0_cols, Xkeep, V, sig, status); break;
+                case 16: launched = launch_cluster<16>(ctx, G, n, k, X0, x0_cols, Xkeep, V, sig, status); break;
+                case 24: launched = launch_cluster<24>(ctx, G, n, k, X0, x0_cols, Xkeep, V, sig, status); break;
+                case 32: launched = launch_cluster<32>(ctx, G, n, k, X0, x0_cols, Xkeep, V, sig, status); break;
+                default: break;
+            }
+        }
+    }
+    if (launched) {
+        DBuf<double> work(ctx, eig_work_doubles(n, k));
+        eig_topk(ctx, G, n, k, work.get(), V, sig, status, status);
+        return true;
+    }
     if (n > kSubMinN && b < n && b <= kMaxB && (b % 8) == 0 && k <= b - 2)
         launched = eig_subspace(ctx, G, n, k, X0, x0_cols, Xkeep, b, V, sig, status);
     DBuf<double> work(ctx, eig_work_doubles(n, k));

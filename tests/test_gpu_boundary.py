@@ -90,3 +90,15 @@ def test_sparse_mode_product_bit_exact(mb, dims, p):
         ref = O.mode_product(sp_ref, m, mode)
         assert got.shape == ref.shape
         assert np.array_equal(got, ref), np.abs(got - ref).max()
+
+
+@pytest.mark.parametrize("rows,cols,k", [(256, 900, 16), (130, 400, 8), (300, 2000, 10)])
+def test_left_singular_basis_large_gram_matches_oracle(mb, rows, cols, k):
+    """Row Grams of 130-300 rows exceed one CTA's shared memory: the
+    cluster-distributed eigensolver (eig_cluster.cuh) takes them."""
+    a = lowrank_matrix(rows, cols, k + 4, rows + cols, noise=1e-2)
+    dev = mb.left_singular_basis(a, k)
+    ref_b, ref_s, ref_nr, ref_c = O.left_singular_basis(a, k)
+    assert np.abs(dev.singular_values - ref_s).max() <= 1e-10 * ref_s[0]
+    r = dev.basis - ref_b @ (ref_b.T @ dev.basis)
+    assert np.linalg.norm(r, 2) <= 1e-9
