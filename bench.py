@@ -296,6 +296,22 @@ def run_mach(args, rank, world, local):
                 "avg_launch_ms": round(per_launch_ms, 5),
                 "share_of_sweep": round(tot / 2.0 / sweep_ms_prof, 3) if sweep_ms_prof else None,
                 "peak_source": peak_src}
+    tc = [(k, v) for k, v in kstats.items() if "ttm_tc_kernel" in k]
+    if roof is None and tc:
+        # dense route (p >= 0.25): the streaming tcgen05 mode product reads the
+        # whole fp32 tensor once per launch (numel * 4 B algorithmic) and
+        # writes the fp64 projection (numel / I_m * r * 8 B)
+        n_l, tot = tc[0][1]
+        per_launch_ms = tot / n_l
+        bytes_per_launch = int(math.prod(dims) * vsize + math.prod(dims) // dims[0] * ranks[0] * 8)
+        achieved = bytes_per_launch / (per_launch_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "ttm_tc_kernel (tcgen05 3xTF32 mode product)", "achieved": round(achieved, 1),
+                "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": None,
+                "bytes_per_launch": bytes_per_launch,
+                "bytes_model": "numel * 4 B read + the fp64 projection written, per launch (2 per sweep)",
+                "avg_launch_ms": round(per_launch_ms, 5),
+                "share_of_sweep": round(tot / 2.0 / sweep_ms_prof, 3) if sweep_ms_prof else None,
+                "peak_source": peak_src}
     breakdown = {k: {"launches_per_sweep": v[0] / 2.0, "ms_per_sweep": round(v[1] / 2.0, 5)}
                  for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][1])}
 
