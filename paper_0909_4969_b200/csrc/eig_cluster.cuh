@@ -58,9 +58,10 @@ struct Dist {
     double* F;     // full gather copy (npad x XS)
     double* Cp;    // B x B partial (ld HS)
     double* colp;  // per-column partials (B)
-    __device__ Dist(cgc::cluster_group c, int n, double* f, double* cp, double* cols)
+    double* red_;  // CTA reduction scratch (32)
+    __device__ Dist(cgc::cluster_group c, int n, double* f, double* cp, double* cols, double* red)
         : cl(c), rank(static_cast<int>(c.block_rank())), CL(static_cast<int>(c.num_blocks())), L(n, rank), F(f),
-          Cp(cp), colp(cols) {}
+          Cp(cp), colp(cols), red_(red) {}
 
     // all slices of block P (absolute rows, each CTA's slice at the same smem
     // offset) into F.  The two cluster barriers: writers done / readers done.
@@ -199,7 +200,16 @@ struct Dist {
     }
     __device__ void orthonormalize(double*& X, double*& T, double* S, double* Ri, double* rinv, double* coef, int n,
                                    int* flag) {
-        if (!cholqr(X, T, S, Ri, rinv, flag, false) || !cholqr(X, T, S, Ri, rinv, flag, true)) cgs2(X, n, coef);
+        if (!cholqr(X, T, S, Ri, rinv, flag, false) || !cholqr(X, T, S, Ri, rinv, flag, true)) {
+            if (rank == 0) sub_stamp(600);
+            // the Gram-Schmidt fallback on a gathered full copy, run by every
+            // CTA (identical results), each keeping its own rows: one gather
+            // instead of ~8 cluster barriers per column
+            gather(X);
+            SB::cgs2(F, n, coef, red_);
+            for (int e = threadIdx.x; e < (L.r1 - L.r0) * XS; e += kThreads) X[L.r0 * XS + e] = F[L.r0 * XS + e];
+            __syncthreads();
+        }
     }
 };
 
@@ -221,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     double* blk = F + static_cast<std::size_t>(L.npad) * XS;
     double* Cp = blk + 4ull * L.rpc * XS;
     double* colp = Cp + B * HS;
-    Dist<B> D(cl, n, F, Cp, colp);
+    Dist<B> D(cl, n, F, Cp, colp, ws.red);
     // absolute-row views of the local slices
     double* Gv = Gl - L.r0;
     double* X = blk - static_cast<std::ptrdiff_t>(L.r0) * XS;
@@ -264,24 +274,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         cl.sync();
         return;
     }
+    auto stamp = [&](int tag) {
+        if (rank == 0) sub_stamp(tag);
+    };
+    stamp(1);
     bool ok = true;
     if (x0_cols < B || !X0) D.orthonormalize(X, Y0, S, Z, rinv, ws.coef, n, &flag);
+    stamp(2);
     const bool filter_first = X0 && x0_cols >= B && th0;
     if (filter_first && threadIdx.x < B) th[threadIdx.x] = th0[threadIdx.x];
     __syncthreads();
-    bool conv = false, ax_valid = false;
+    bool conv = false, ax_valid = false, guards_saved = false;
     int it = 0;
     for (;; ++it) {
         if (!(filter_first && it == 0)) {
             D.gemm(Gv, X, AX, 1.0, nullptr, 0.0, nullptr, 0.0);
+            stamp(10);
             D.gram(X, AX, H);
-            if (!SB::refine_rr(H, Hc, W, Z, Q, S, th, k, &flag)) SB::rr_hybrid(H, Hc, W, Z, Q, S, ws.J7, th, k, &flag, red, it == 0 ? 8 : 3);
+            stamp(11);
+            int nsw = 99;
+            if (!SB::refine_rr(H, Hc, W, Z, Q, S, th, k, &flag)) nsw = SB::rr_hybrid(H, Hc, W, Z, Q, S, ws.J7, th, k, &flag, red, it == 0 ? 8 : 3);
+            stamp(1000 + nsw);
             D.rotate(X, W, Y0);
             { double* t = X; X = Y0; Y0 = t; }
             D.rotate(AX, W, Y0);
             { double* t = AX; AX = Y0; Y0 = t; }
             ax_valid = true;
+            stamp(13);
             const double rmax = D.residual(X, AX, th, n, k, red);
+            stamp(14);
             const double scale = fmax(fabs(th[0]), 1e-300);
             if (dbg && rank == 0 && threadIdx.x == 0)
                 printf("[eigc] it %d th0 %.6e thB %.6e rmax/scale %.3e flag %d\n", it, th[0], th[B - 1], rmax / scale, flag);
@@ -294,6 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const double lo = -1e-12 * scale;
         const double e = 0.5 * (cut - lo), cen = 0.5 * (cut + lo);
         const int lr0 = L.r0, lr1 = L.r1;
+        (void)lr0;
         if (!(e > 0.0)) {
             if (ax_valid) {
                 for (int idx = lr0 * XS + static_cast<int>(threadIdx.x); idx < lr1 * XS; idx += kThreads) Y1[idx] = AX[idx];
@@ -305,12 +327,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             { double* t = X; X = Y1; Y1 = t; }
         } else {
             const double ie = 1.0 / e;
+            guards_saved = false;
             if (ax_valid) {
                 for (int idx = lr0 * XS + static_cast<int>(threadIdx.x); idx < lr1 * XS; idx += kThreads)
                     Y1[idx] = ie * AX[idx] - cen * ie * X[idx];
                 __syncthreads();
+                // keep the pre-filter guard columns (AX is free until the next
+                // Rayleigh-Ritz): if the filter's gain lifts traces of the
+                // leading directions in them above the guards themselves, the
+                // CholQR retries with them instead of falling back to
+                // Gram-Schmidt
+                for (int e = threadIdx.x; e < (lr1 - lr0) * (B - k); e += kThreads) {
+                    const int r = lr0 + e / (B - k), c = k + e % (B - k);
+                    AX[r * XS + c] = X[r * XS + c];
+                }
+                __syncthreads();
+                guards_saved = true;
             } else {
                 D.gemm(Gv, X, Y1, ie, X, -cen * ie, nullptr, 0.0);
+                for (int e = threadIdx.x; e < (lr1 - lr0) * (B - k); e += kThreads) {
+                    const int r = lr0 + e / (B - k), c = k + e % (B - k);
+                    AX[r * XS + c] = X[r * XS + c];
+                }
+                __syncthreads();
+                guards_saved = true;
             }
             ax_valid = false;
             double* y0 = X;
@@ -327,7 +367,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             Y0 = y0;
             Y1 = spare;
         }
+        stamp(15);
+        if (guards_saved && !D.cholqr(X, Y0, S, Z, rinv, &flag, false)) {
+            stamp(601);
+            for (int e = threadIdx.x; e < (lr1 - lr0) * (B - k); e += kThreads) {
+                const int r = lr0 + e / (B - k), c = k + e % (B - k);
+                X[r * XS + c] = AX[r * XS + c];
+            }
+            __syncthreads();
+        } else if (guards_saved) {
+            // first pass done: the second (usually skipped) below
+            if (!D.cholqr(X, Y0, S, Z, rinv, &flag, true)) D.orthonormalize(X, Y0, S, Z, rinv, ws.coef, n, &flag);
+            stamp(16);
+            continue;
+        }
         D.orthonormalize(X, Y0, S, Z, rinv, ws.coef, n, &flag);
+        stamp(16);
     }
     // ---- outputs (column-major, absolute rows of this slice) ----
     const int rn = min(L.r1, n);

@@ -454,7 +454,10 @@ struct Sub {
             for (int e = tid; e < B * B; e += kThreads) {
                 const int i = e % B, j = e / B;
                 double z = 0.0;
-                if (i != j) {
+                // guard-guard pairs (both >= k) are left as they are: the guard
+                // columns only bound the filter, and nearly degenerate noise
+                // pairs there would keep the rounds from converging
+                if (i != j && (i < k || j < k)) {
                     const double hij = Hc[i + j * HS];
                     const double gap = Hc[j + j * HS] - Hc[i + i * HS];
                     if (fabs(hij) > 0.25 * fabs(gap)) {

@@ -277,8 +277,28 @@ bool launch_cluster(Ctx* ctx, const double* G, int n, int k, const double* X0, i
     cfg.attrs = at;
     cfg.numAttrs = 1;
     static const int dbg = std::getenv("MACH_DEBUG_EIGC") ? 1 : 0;
+    static const bool tdbg = std::getenv("MACH_DEBUG_EIG_T") != nullptr;
+    DBuf<long long> sb;
+    if (tdbg) {  // phase stamps of rank 0 (sub_stamp)
+        sb.alloc(ctx, 200);
+        sb.zero(ctx);
+        long long* p = sb.get();
+        int z = 0;
+        MB_CUDA(cudaMemcpyToSymbolAsync(g_stamp, &p, sizeof(p), 0, cudaMemcpyHostToDevice, ctx->stream));
+        MB_CUDA(cudaMemcpyToSymbolAsync(g_stamp_n, &z, sizeof(z), 0, cudaMemcpyHostToDevice, ctx->stream));
+    }
     MB_LAUNCH_EX(ctx, "eig_cluster_kernel<B>", &cfg, kern, G, n, k, X0, x0_cols, th0, Xkeep, V, sig, status, 4, 40,
                  1e-12, dbg);
+    if (tdbg) {
+        long long f[200];
+        to_host(ctx, f, sb.get(), 200);
+        sync(ctx);
+        std::fprintf(stderr, "[eigc-t] n=%d:", n);
+        for (int i = 1; i < 100 && f[2 * i + 1]; ++i) std::fprintf(stderr, " %lld:%.1f", f[2 * i], (f[2 * i + 1] - f[2 * i - 1]) * 1e-3);
+        std::fprintf(stderr, "\n");
+        long long* np = nullptr;
+        cudaMemcpyToSymbol(g_stamp, &np, sizeof(np));
+    }
     return true;
 }
 
