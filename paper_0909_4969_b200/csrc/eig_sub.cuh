@@ -665,21 +665,13 @@ struct SubWs {
         }                                                                              \
     } while (0)
 
-// The solver proper.  G: npad x npad in shared memory (leading dimension ldg,
-// exactly symmetric, zero outside n x n).  Returns the final Ritz block (in
-// ws, row-major, stride Sub<B>::XS, rows >= n zero); Ritz values in ws.th.
+// Start block into the workspace: X0's columns (column-major n x x0_cols),
+// deterministic random columns beyond them; the other three blocks zeroed.
 template <int B>
-__device__ double* subspace_core(SubWs<B>& ws, const double* G, int ldg, int n, int k, int m, int maxit, double tol,
-                                 const double* X0, int x0_cols, bool& conv, int& iters, int* flagp,
-                                 long long* tstamp, int& ns_, const double* th0 = nullptr) {
-    using SB = Sub<B>;
-    constexpr int XS = SB::XS;
+__device__ void load_start_block(SubWs<B>& ws, int n, const double* X0, int x0_cols) {
+    constexpr int XS = Sub<B>::XS;
     const int npad = (n + 7) & ~7;
-    double *H = ws.H, *W = ws.W, *S = ws.S, *Z = ws.Z, *Q = ws.Q, *Hc = ws.Hc, *th = ws.th, *rinv = ws.rinv,
-           *coef = ws.coef, *red = ws.red;
     double *X = ws.X, *AX = ws.AX, *Y0 = ws.Y0, *Y1 = ws.Y1;
-    int& flag = *flagp;
-    // ---- start block (row-major, rows >= n zero in all four blocks) ----
     for (int base = threadIdx.x; base < npad * B; base += 8 * kThreads) {
         double v[8];
 #pragma unroll
@@ -700,6 +692,24 @@ __device__ double* subspace_core(SubWs<B>& ws, const double* G, int ldg, int n, 
             Y1[r * XS + c] = 0.0;
         }
     }
+}
+
+// The solver proper.  G: npad x npad in shared memory (leading dimension ldg,
+// exactly symmetric, zero outside n x n).  Returns the final Ritz block (in
+// ws, row-major, stride Sub<B>::XS, rows >= n zero); Ritz values in ws.th.
+template <int B>
+__device__ double* subspace_core(SubWs<B>& ws, const double* G, int ldg, int n, int k, int m, int maxit, double tol,
+                                 const double* X0, int x0_cols, bool& conv, int& iters, int* flagp,
+                                 long long* tstamp, int& ns_, const double* th0 = nullptr, bool preloaded = false) {
+    using SB = Sub<B>;
+    constexpr int XS = SB::XS;
+    const int npad = (n + 7) & ~7;
+    double *H = ws.H, *W = ws.W, *S = ws.S, *Z = ws.Z, *Q = ws.Q, *Hc = ws.Hc, *th = ws.th, *rinv = ws.rinv,
+           *coef = ws.coef, *red = ws.red;
+    double *X = ws.X, *AX = ws.AX, *Y0 = ws.Y0, *Y1 = ws.Y1;
+    int& flag = *flagp;
+    // ---- start block (row-major, rows >= n zero in all four blocks) ----
+    if (!preloaded) load_start_block<B>(ws, n, X0, x0_cols);
     __syncthreads();
     MB_STAMP(1);
     if (x0_cols < B || !X0) SB::orthonormalize(X, Y0, n, npad, S, Z, rinv, coef, red, &flag);  // a kept Ritz block is orthonormal

@@ -125,6 +125,12 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
     // ---- phase A: partial Gram of this row block ----
     __shared__ __align__(8) std::uint64_t ybar;  // row CTAs: phase A's Y copy (phase 0), phase D's V copy
     std::uint32_t ybar_phase = 0u;
+    if (rank == 0) {
+        // CTA 0 has no rows: it loads the eigensolver's start block (the kept
+        // Ritz block) while the row blocks form their partial Grams
+        SubWs<B> ws0(wsp, npad);
+        load_start_block<B>(ws0, n, A.X0, A.x0_cols);
+    }
     if (rank > 0) {
         const int nr8z = (nr + 7) & ~7;  // rows zero-filled to a whole MMA tile
         // the block's column segments (contiguous in the column-major Y)
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1) mode_basis_kernel(MBArgs<T> A, lo
             int it = 0;
             const double* th0 = (A.filter_first && A.X0 && A.x0_cols >= B) ? A.X0 + static_cast<std::size_t>(n) * B : nullptr;
             double* X = subspace_core<B>(ws, G, ldg, n, k, A.m, A.maxit, A.tol, A.X0, A.x0_cols, conv, it, &flagw,
-                                         tstamp, ns_, th0);
+                                         tstamp, ns_, th0, true);
             if (A.Xkeep) {
                 for (int e = threadIdx.x; e < n * B; e += kThreads) A.Xkeep[e] = X[(e % n) * Sub<B>::XS + e / n];
                 if (threadIdx.x < B) A.Xkeep[n * B + threadIdx.x] = ws.th[threadIdx.x];
