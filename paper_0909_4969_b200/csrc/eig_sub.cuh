@@ -297,7 +297,22 @@ struct Sub {
         }
         __syncthreads();
         sub_stamp(502);
-        // outer-product Cholesky on the upper triangle, one barrier per step
+        // outer-product Cholesky on the upper triangle, one barrier per step;
+        // each thread owns fixed (l, m) entries (l <= m), indices computed once
+        constexpr int NI = B * (B + 1) / 2;
+        constexpr int PT = (NI + kThreads - 1) / kThreads;  // entries per thread
+        int il[PT], im[PT];
+#pragma unroll
+        for (int q = 0; q < PT; ++q) {
+            int e = static_cast<int>(threadIdx.x) + q * kThreads, l = -1, m = -1;
+            if (e < NI) {  // column-major upper triangle: column m holds rows 0..m
+                m = 0;
+                while (e > m) { e -= m + 1; ++m; }
+                l = e;
+            }
+            il[q] = l;
+            im[q] = m;
+        }
         for (int j = 0; j < B; ++j) {
             const double d = S[j + j * HS];
             // breakdown: the column keeps < ~3e-8 of its length after the
@@ -307,10 +322,10 @@ struct Sub {
                 continue;  // uniform: every thread read the same d
             }
             const double inv = 1.0 / d;
-            const int rem = B - 1 - j;
-            for (int e = threadIdx.x; e < rem * rem; e += kThreads) {
-                const int l = j + 1 + e % rem, m = j + 1 + e / rem;
-                if (l <= m) S[l + m * HS] -= S[j + l * HS] * S[j + m * HS] * inv;
+#pragma unroll
+            for (int q = 0; q < PT; ++q) {
+                const int l = il[q], m = im[q];
+                if (l > j) S[l + m * HS] -= S[j + l * HS] * S[j + m * HS] * inv;
             }
             __syncthreads();
         }
