@@ -514,20 +514,28 @@ bool sparse_fast_path_ok(const std::vector<int>& dims, const std::vector<int>& r
 // nnz * RA(r_a) for the fibre sums + expected fibres * r_a * r_b for stage 2
 // (order 4: r_b = the larger rank of the two composite modes; the outer one
 // is contracted once per (row, i_b2) group, see stage2_4way_kernel).
+// Work model of mode n's TTM with inner (gathered) mode a: the nonzero
+// stream's gathers plus the fibre sums' expansion (expected fibre count at
+// the tensor's density).
+double inner_cost(const mach_sparse* X, int n, const std::vector<int>& ranks, int a) {
+    const int d = static_cast<int>(X->dims.size());
+    const double dens = X->numel ? static_cast<double>(X->nnz) / static_cast<double>(X->numel) : 0.0;
+    int rb = 1;
+    for (int m = 0; m < d; ++m)
+        if (m != n && m != a) rb = std::max(rb, ranks[m]);
+    const double Ia = X->dims[a];
+    const double fibres = (static_cast<double>(X->numel) / Ia) * (1.0 - std::pow(1.0 - dens, Ia));
+    return static_cast<double>(X->nnz) * ra_bucket(ranks[a]) + fibres * ranks[a] * rb;
+}
+
 static int choose_inner(const mach_sparse* X, int n, const std::vector<int>& ranks, int avoid) {
     const int d = static_cast<int>(X->dims.size());
     if (d == 2) return 1 - n;
     int best = -1;
     double best_cost = 0;
-    const double dens = X->numel ? static_cast<double>(X->nnz) / static_cast<double>(X->numel) : 0.0;
     for (int a = 0; a < d; ++a) {
         if (a == n || a == avoid) continue;
-        int rb = 1;
-        for (int m = 0; m < d; ++m)
-            if (m != n && m != a) rb = std::max(rb, ranks[m]);
-        const double Ia = X->dims[a];
-        const double fibres = (static_cast<double>(X->numel) / Ia) * (1.0 - std::pow(1.0 - dens, Ia));
-        const double cost = static_cast<double>(X->nnz) * ra_bucket(ranks[a]) + fibres * ranks[a] * rb;
+        const double cost = inner_cost(X, n, ranks, a);
         if (best < 0 || cost < best_cost - 1e-9) { best = a; best_cost = cost; }
     }
     return best;

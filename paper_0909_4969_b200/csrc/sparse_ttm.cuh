@@ -250,6 +250,8 @@ double subspace_sin_dev(Ctx* ctx, const double* A, const double* B, int n, int r
 // truncated_svd family on the device (tsvd.cu); A rows x cols column-major
 void truncated_svd_dev(Ctx* ctx, const double* A, int rows, int cols, int k, double* left, double* sv, double* right);
 void low_rank_dev(Ctx* ctx, const double* L, const double* sv, const double* R, int rows, int cols, int k, double* out);
+// work model of mode n's sparse TTM with inner mode a (sparse_ttm.cu)
+double inner_cost(const mach_sparse* X, int n, const std::vector<int>& ranks, int a);
 // dense mode-n Gram X_(n) X_(n)^T on tcgen05 (gram_tc.cu), read in place
 bool gram_tc_applies(const std::vector<int>& dims, int n);
 void gram_tc(Ctx* ctx, const float* x, const std::vector<int>& dims, int n, double* G);

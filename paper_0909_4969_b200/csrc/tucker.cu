@@ -794,6 +794,22 @@ struct SparseSession : SessionBase {
         plans.resize(static_cast<std::size_t>(d));
         const bool no_overlap = std::getenv("MACH_NO_OVERLAP") != nullptr;  // read per session (tests toggle it)
         overlap = d == 3 && !no_overlap;
+        if (overlap) {
+            // the overlapped sweep fixes mode n's inner mode to n + 1; when that
+            // costs far more than the best inner mode (C4's host mode: 31M
+            // one-nonzero fibres over the 64 metrics instead of 64K time
+            // fibres), the unconstrained plans run without the overlap
+            for (int m = 0; m < d && overlap; ++m) {
+                double best = -1.0;
+                for (int a = 0; a < d; ++a)
+                    if (a != m) {
+                        const double c = inner_cost(sp, m, rk, a);
+                        if (best < 0 || c < best) best = c;
+                    }
+                if (inner_cost(sp, m, rk, (m + 1) % 3) > 2.0 * best) overlap = false;
+            }
+            if (std::getenv("MACH_DEBUG_SETUP")) std::fprintf(stderr, "[setup] overlap %d\n", overlap ? 1 : 0);
+        }
         split4 = d == 4;
         sumsq<T>(ctx, static_cast<const T*>(X->val), X->nnz, fs.red.get(), fs.scal.get());
         to_host(ctx, &normX2, fs.scal.get(), 1);
