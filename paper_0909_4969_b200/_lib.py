@@ -13,7 +13,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libmach_b200.so")
+LIB_PATH = os.environ.get("MACH_LIB_PATH") or os.path.join(HERE, "libmach_b200.so")  # override: A/B builds
 HEADER = os.path.join(ROOT, "include", "mach_b200.h")
 
 _lib = None
