@@ -36,7 +36,9 @@ typedef enum {
     MACH_ERR_CUDA = 4,
     MACH_ERR_OOM = 5,
     MACH_ERR_NCCL = 6,
-    MACH_ERR_INTERNAL = 7
+    MACH_ERR_INTERNAL = 7,
+    MACH_ERR_IO = 8,          /* mach::IoError (errors.hpp:21-25)         */
+    MACH_ERR_PARSE = 9        /* mach::ParseError (errors.hpp:27-35)      */
 } mach_status;
 
 typedef enum { MACH_F32 = 0, MACH_F64 = 1 } mach_dtype;
@@ -224,6 +226,79 @@ mach_status mach_mode_product_sparse(mach_ctx* ctx, const mach_sparse* t, int ro
  * (*tensor_cores = 1); otherwise the fp64 CUDA-core Gram (*tensor_cores = 0). */
 mach_status mach_dense_mode_gram(mach_ctx* ctx, const mach_dense* t, int mode, double* host,
                                  int* tensor_cores);
+
+/* ---- Theorem-1 bound (bounds.hpp:10-66) ---------------------- */
+typedef struct mach_bound_mode {   /* BoundModeReport (bounds.hpp:24-30)       */
+    int rank;
+    double x_residual;             /* |X_(i) - X_(i),r_i|, original tensor      */
+    double xhat_residual;          /* same residual on the sampled tensor       */
+    double x_lowrank_norm;         /* |X_(i),r_i|                               */
+    double t_i;
+} mach_bound_mode;
+typedef struct mach_bound_report { /* BoundReport (bounds.hpp:35-46)            */
+    double b, p, p_min, t, success_probability;
+    int dims_large_enough, dims_balanced, p_above_min, conditions_met;
+} mach_bound_report;
+/* achlioptas_bounds (bounds.hpp:17): (4 b sqrt(n/p), 4 b sqrt(n k/p))         */
+mach_status mach_achlioptas_bounds(double b, int64_t n, int64_t k, double p, double* two_norm,
+                                   double* frobenius);
+/* min_sampling_probability (bounds.hpp:22)                                    */
+mach_status mach_min_sampling_probability(int order, const int* dims, double* out);
+/* theorem1_conditions (bounds.hpp:51): shape-only part of the report          */
+mach_status mach_theorem1_conditions(int order, const int* dims, double p, mach_bound_report* rep);
+/* theorem1_bound (bounds.hpp:62): full mode spectra of x and xhat from the
+ * device Gram kernels and the on-device eigensolver; per_mode holds one entry
+ * per mode (caller-allocated).  The shorter side of every mode unfolding must
+ * be <= 1700 (one-CTA spectrum solver).                                        */
+mach_status mach_theorem1_bound(mach_ctx* ctx, const mach_dense* x, const mach_sparse* xhat,
+                                const int* ranks, double p, mach_bound_report* rep,
+                                mach_bound_mode* per_mode);
+
+/* ---- streaming sample-on-arrival ingest (PAPER Remark 2,
+ * ingest.hpp:44) ------------------------------------------------------------
+ * A stream is a tensor growing along its last (time) mode.  dims gives the
+ * leading modes and, in dims[order-1], the CAPACITY in time ticks.  Every
+ * arriving time slab is sampled on the device with the global flat index as
+ * the RNG counter (sampling.cpp:27) and appended to the sampled tensor in HBM,
+ * so at any time the kept set equals mach_sparsify of the tensor seen so far,
+ * bit for bit.                                                                */
+typedef struct mach_stream mach_stream;
+mach_status mach_stream_begin(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims, double p,
+                              uint64_t seed, mach_stream** out);
+/* append a device-resident slab (leading dims x ticks, first mode fastest)    */
+mach_status mach_stream_append(mach_stream* s, const mach_dense* slab);
+/* append a host slab of `ticks` time ticks (dtype values): the host->device
+ * copy of this slab overlaps the sampling of the previous one (two staging
+ * buffers); the host buffer may be reused on return                           */
+mach_status mach_stream_append_host(mach_stream* s, const void* host, int ticks);
+/* ingest (ingest.cpp:90-134) of one time slab of pre-indexed measurement
+ * records on the device: the cell (machine, metric, tick) means are formed in
+ * (cell, value) order (independent of record order), empty cells are zero or,
+ * with carry_forward, the cell's latest earlier value (state kept across
+ * slabs); the slab is then sampled and appended.  order must be 3.            */
+mach_status mach_stream_append_records(mach_stream* s, int64_t n, const int32_t* machine,
+                                       const int32_t* metric, const int32_t* tick,
+                                       const double* value, int ticks, int carry_forward);
+mach_status mach_stream_state(mach_stream* s, int64_t* ticks, int64_t* nnz);
+/* the sampled tensor seen so far (dims: leading modes x ticks), a copy        */
+mach_status mach_stream_tensor(mach_stream* s, mach_sparse** out);
+/* the last appended dense slab (records / host appends), for inspection       */
+mach_status mach_stream_last_slab(mach_stream* s, mach_dense** out);
+mach_status mach_stream_free(mach_stream* s);
+
+/* ---- binary tensor files (replaces the text formats of
+ * tensor_io.hpp:24-26 at scale) ----------------------------------------------
+ * Little-endian: "MACHB2\0\0", u32 version (1), u32 kind (0 dense, 1 sparse),
+ * u32 dtype (mach_dtype), u32 order, i32 dims[order], i64 nnz (numel for
+ * dense), u32 index bytes (0 dense, 4|8 sparse), u32 reserved; then the raw
+ * arrays (sparse: ascending flat indices, then values).                       */
+mach_status mach_dense_save(const mach_dense* t, const char* path);
+mach_status mach_dense_load(mach_ctx* ctx, const char* path, mach_dense** out);
+mach_status mach_sparse_save(const mach_sparse* t, const char* path);
+mach_status mach_sparse_load(mach_ctx* ctx, const char* path, mach_sparse** out);
+/* kind of a tensor file without loading it: 0 dense, 1 sparse                 */
+mach_status mach_tensor_file_kind(const char* path, int* kind, mach_dtype* dtype, int* order,
+                                  int* dims /* >= 8 */, int64_t* nnz);
 
 #ifdef __cplusplus
 }

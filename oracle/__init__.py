@@ -109,6 +109,14 @@ def lib():
         L.orc_reconstruct.argtypes = [C.c_void_p, _dp]
         L.orc_last_error.argtypes = [C.c_char_p, C.c_int]
         L.orc_phase_times.argtypes = [_dp, _dp, _dp, C.c_int, _ip]
+        # SURVEY §8(f) rows (oracle_ext.cpp)
+        L.orc_ext_last_error.restype = C.c_char_p
+        L.orc_theorem1_bound.argtypes = [C.c_void_p, C.c_void_p, _ip, C.c_double, _dp, _ip, _dp]
+        L.orc_theorem1_conditions.argtypes = [C.c_int, _ip, C.c_double, _dp, _ip]
+        L.orc_min_sampling_probability.argtypes = [C.c_int, _ip, _dp]
+        L.orc_ingest_buckets.restype = C.c_longlong
+        L.orc_ingest_buckets.argtypes = [C.c_longlong, _llp, C.c_longlong, _llp]
+        L.orc_ingest_indexed.argtypes = [C.c_longlong, _ip, _ip, _llp, _dp, C.c_int, C.c_int, C.c_longlong, C.c_int, _dp]
         _lib = L
     return _lib
 
@@ -433,6 +441,66 @@ def subspace_gap(a: np.ndarray, b: np.ndarray) -> float:
     n, k = b2.shape
     b = np.ascontiguousarray(b2.reshape(-1, order="F"))
     return lib().orc_subspace_gap(n, k, _d(a), _d(b))
+
+
+def _check_ext(rc: int):
+    if rc != 0:
+        raise _KINDS.get(rc, OracleError)(rc, lib().orc_ext_last_error().decode(), 0)
+
+
+def _bound_dict(scal, flags, per_mode=None):
+    out = {"b": scal[0], "p": scal[1], "p_min": scal[2], "t": scal[3], "success_probability": scal[4],
+           "dims_large_enough": bool(flags[0]), "dims_balanced": bool(flags[1]), "p_above_min": bool(flags[2]),
+           "conditions_met": bool(flags[3]), "per_mode": []}
+    if per_mode is not None:
+        for r in per_mode.reshape(-1, 5):
+            out["per_mode"].append({"rank": int(r[0]), "x_residual": r[1], "xhat_residual": r[2],
+                                    "x_lowrank_norm": r[3], "t_i": r[4]})
+    return out
+
+
+def theorem1_bound(x: "Dense", xhat: "Sparse", ranks, p: float) -> dict:
+    """BoundReport as a dict — bounds.cpp:152-184."""
+    d = len(x.dims)
+    scal = np.zeros(5)
+    flags = (C.c_int * 4)()
+    pm = np.zeros(5 * d)
+    rk = (C.c_int * max(len(ranks), d))(*[int(r) for r in ranks])
+    if len(ranks) != d:
+        raise ArgumentError(1, "ranks must name one rank per mode")
+    _check_ext(lib().orc_theorem1_bound(x.h, xhat.h, rk, float(p), _d(scal), flags, _d(pm)))
+    return _bound_dict(scal, flags, pm)
+
+
+def theorem1_conditions(dims, p: float) -> dict:
+    scal = np.zeros(5)
+    flags = (C.c_int * 4)()
+    _check_ext(lib().orc_theorem1_conditions(len(dims), _dims(dims) if len(dims) else None, float(p), _d(scal), flags))
+    return _bound_dict(scal, flags)
+
+
+def min_sampling_probability(dims) -> float:
+    out = np.zeros(1)
+    _check_ext(lib().orc_min_sampling_probability(len(dims), _dims(dims) if len(dims) else None, _d(out)))
+    return float(out[0])
+
+
+def ingest_indexed(machine, metric, ts, value, n_machines: int, n_metrics: int, bucket_seconds: int = 300,
+                   carry_forward: bool = False):
+    """(tensor machines x metrics x buckets, first bucket start) — ingest.cpp:51-135 on pre-indexed records."""
+    machine = np.ascontiguousarray(machine, dtype=np.int32)
+    metric = np.ascontiguousarray(metric, dtype=np.int32)
+    ts = np.ascontiguousarray(ts, dtype=np.int64)
+    value = _f64(value)
+    n = len(ts)
+    llp = C.POINTER(C.c_longlong)
+    fb = C.c_longlong(0)
+    buckets = lib().orc_ingest_buckets(n, ts.ctypes.data_as(llp), int(bucket_seconds), C.byref(fb))
+    out = np.zeros(n_machines * n_metrics * buckets)
+    _check_ext(lib().orc_ingest_indexed(n, machine.ctypes.data_as(_ip), metric.ctypes.data_as(_ip),
+                                        ts.ctypes.data_as(llp), _d(value), n_machines, n_metrics, int(bucket_seconds),
+                                        1 if carry_forward else 0, _d(out)))
+    return out.reshape((n_machines, n_metrics, buckets), order="F"), int(fb.value)
 
 
 def random_tensor(dims, seed: int) -> np.ndarray:

@@ -7,6 +7,16 @@ ABI in include/mach_b200.h); this package is the ctypes face of it.
 from ._lib import build, header_symbols, lib  # noqa: F401
 from .api import (  # noqa: F401
     ArgumentError,
+    IoError,
+    ParseError,
+    SampleStream,
+    achlioptas_bounds,
+    load_tensor,
+    min_sampling_probability,
+    save_tensor,
+    tensor_file_info,
+    theorem1_bound,
+    theorem1_conditions,
     Context,
     ConvergenceError,
     DenseTensor,

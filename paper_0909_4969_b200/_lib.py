@@ -20,7 +20,19 @@ _lib = None
 
 MACH_OK, MACH_ERR_ARGUMENT, MACH_ERR_SHAPE, MACH_ERR_CONVERGENCE = 0, 1, 2, 3
 MACH_ERR_CUDA, MACH_ERR_OOM, MACH_ERR_NCCL, MACH_ERR_INTERNAL = 4, 5, 6, 7
+MACH_ERR_IO, MACH_ERR_PARSE = 8, 9
 MACH_F32, MACH_F64 = 0, 1
+
+
+class BoundMode(C.Structure):
+    _fields_ = [("rank", C.c_int), ("x_residual", C.c_double), ("xhat_residual", C.c_double),
+                ("x_lowrank_norm", C.c_double), ("t_i", C.c_double)]
+
+
+class BoundReport(C.Structure):
+    _fields_ = [("b", C.c_double), ("p", C.c_double), ("p_min", C.c_double), ("t", C.c_double),
+                ("success_probability", C.c_double), ("dims_large_enough", C.c_int), ("dims_balanced", C.c_int),
+                ("p_above_min", C.c_int), ("conditions_met", C.c_int)]
 
 
 def build(force: bool = False) -> str:
@@ -104,6 +116,24 @@ _SIGS = {
     "mach_subspace_sin": (C.c_int, [vp, C.c_int, C.c_int, dp, dp, dp]),
     "mach_truncated_svd": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int, dp, dp, dp]),
     "mach_low_rank_approx": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int, dp]),
+    "mach_achlioptas_bounds": (C.c_int, [C.c_double, i64, i64, C.c_double, dp, dp]),
+    "mach_min_sampling_probability": (C.c_int, [C.c_int, ip, dp]),
+    "mach_theorem1_conditions": (C.c_int, [C.c_int, ip, C.c_double, C.POINTER(BoundReport)]),
+    "mach_theorem1_bound": (C.c_int, [vp, vp, vp, ip, C.c_double, C.POINTER(BoundReport), C.POINTER(BoundMode)]),
+    "mach_stream_begin": (C.c_int, [vp, C.c_int, C.c_int, ip, C.c_double, C.c_uint64, vpp]),
+    "mach_stream_append": (C.c_int, [vp, vp]),
+    "mach_stream_append_host": (C.c_int, [vp, vp, C.c_int]),
+    "mach_stream_append_records": (C.c_int, [vp, i64, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                             dp, C.c_int, C.c_int]),
+    "mach_stream_state": (C.c_int, [vp, i64p, i64p]),
+    "mach_stream_tensor": (C.c_int, [vp, vpp]),
+    "mach_stream_last_slab": (C.c_int, [vp, vpp]),
+    "mach_stream_free": (C.c_int, [vp]),
+    "mach_dense_save": (C.c_int, [vp, C.c_char_p]),
+    "mach_dense_load": (C.c_int, [vp, C.c_char_p, vpp]),
+    "mach_sparse_save": (C.c_int, [vp, C.c_char_p]),
+    "mach_sparse_load": (C.c_int, [vp, C.c_char_p, vpp]),
+    "mach_tensor_file_kind": (C.c_int, [C.c_char_p, ip, ip, ip, ip, i64p]),
 }
 
 

@@ -48,6 +48,14 @@ class DeviceError(MachError, RuntimeError):
     code = L.MACH_ERR_CUDA
 
 
+class IoError(MachError, OSError):
+    code = L.MACH_ERR_IO
+
+
+class ParseError(MachError, RuntimeError):
+    code = L.MACH_ERR_PARSE
+
+
 def _check(rc: int):
     if rc == L.MACH_OK:
         return
@@ -59,6 +67,10 @@ def _check(rc: int):
         raise ShapeError(msg)
     if rc == L.MACH_ERR_CONVERGENCE:
         raise ConvergenceError(msg, lib.mach_last_error_index())
+    if rc == L.MACH_ERR_IO:
+        raise IoError(msg)
+    if rc == L.MACH_ERR_PARSE:
+        raise ParseError(msg)
     raise DeviceError(f"[{rc}] {msg}")
 
 
@@ -729,3 +741,148 @@ def kernel_stats(ctx: Context) -> dict:
         out[buf.value.decode()] = (n.value, ms.value)
         i += 1
     return out
+
+
+# ---------------------------------------------------------------------------
+# Theorem-1 bound (bounds.hpp:10-66), SURVEY 8f.3
+# ---------------------------------------------------------------------------
+def _bound_dict(rep, modes=None) -> dict:
+    out = {k: getattr(rep, k) for k in ("b", "p", "p_min", "t", "success_probability")}
+    for k in ("dims_large_enough", "dims_balanced", "p_above_min", "conditions_met"):
+        out[k] = bool(getattr(rep, k))
+    out["per_mode"] = [] if modes is None else [
+        {k: getattr(m, k) for k in ("rank", "x_residual", "xhat_residual", "x_lowrank_norm", "t_i")} for m in modes]
+    return out
+
+
+def achlioptas_bounds(b: float, n: int, k: int, p: float):
+    """(two_norm, frobenius) — bounds.hpp:17."""
+    a, f = C.c_double(), C.c_double()
+    _check(L.lib().mach_achlioptas_bounds(float(b), int(n), int(k), float(p), C.byref(a), C.byref(f)))
+    return a.value, f.value
+
+
+def min_sampling_probability(dims) -> float:
+    out = C.c_double()
+    _check(L.lib().mach_min_sampling_probability(len(dims), _dims_arr(dims) if len(dims) else None, C.byref(out)))
+    return out.value
+
+
+def theorem1_conditions(dims, p: float) -> dict:
+    rep = L.BoundReport()
+    _check(L.lib().mach_theorem1_conditions(len(dims), _dims_arr(dims) if len(dims) else None, float(p), C.byref(rep)))
+    return _bound_dict(rep)
+
+
+def theorem1_bound(x: "DenseTensor", xhat: "SparseTensor", ranks, p: float, ctx: Context | None = None) -> dict:
+    """BoundReport as a dict; the mode spectra are computed on the device (bounds.hpp:62)."""
+    ctx = _ctx(ctx or x.ctx)
+    d = len(x.dims)
+    if len(ranks) != d:
+        raise ArgumentError("ranks must name one rank per mode")
+    rep = L.BoundReport()
+    modes = (L.BoundMode * d)()
+    _check(L.lib().mach_theorem1_bound(ctx.h, x.h, xhat.h, (C.c_int * d)(*[int(r) for r in ranks]), float(p),
+                                       C.byref(rep), modes))
+    return _bound_dict(rep, modes)
+
+
+# ---------------------------------------------------------------------------
+# streaming sample-on-arrival ingest (SURVEY 8f.2)
+# ---------------------------------------------------------------------------
+class SampleStream:
+    """A tensor growing along its last (time) mode, sampled slab by slab on the device.
+
+    dims: the leading dims and, last, the capacity in time ticks.  At any time
+    `tensor()` equals sparsify() of everything appended so far, bit for bit."""
+
+    def __init__(self, dims, cfg: "SparsifyConfig", dtype=np.float32, ctx: Context | None = None):
+        self.ctx = _ctx(ctx)
+        self.dims, self.dtype = tuple(int(d) for d in dims), np.dtype(dtype)
+        self.h = C.c_void_p()
+        _check(L.lib().mach_stream_begin(self.ctx.h, _DT[self.dtype], len(self.dims), _dims_arr(self.dims), float(cfg.p),
+                                         int(cfg.seed), C.byref(self.h)))
+
+    def append(self, slab):
+        """slab: a DenseTensor in HBM, or a numpy array (leading dims x ticks) copied from the host."""
+        if isinstance(slab, DenseTensor):
+            _check(L.lib().mach_stream_append(self.h, slab.h))
+            return
+        a = np.asarray(slab)
+        if a.shape[:-1] != self.dims[:-1]:
+            raise ShapeError("slab leading dims differ from the stream's")
+        flat = np.ascontiguousarray(a.astype(self.dtype, copy=False).reshape(-1, order="F"))
+        _check(L.lib().mach_stream_append_host(self.h, flat.ctypes.data_as(C.c_void_p), int(a.shape[-1])))
+        self._last_ticks = int(a.shape[-1])
+
+    def append_host_ptr(self, ptr: int, ticks: int):
+        """Host slab by address (e.g. a pinned torch tensor's data_ptr())."""
+        _check(L.lib().mach_stream_append_host(self.h, C.c_void_p(ptr), int(ticks)))
+        self._last_ticks = int(ticks)
+
+    def append_records(self, machine, metric, tick, value, ticks: int, carry_forward: bool = False):
+        """One time slab of pre-indexed measurement records (ingest.cpp:90-134 on the device)."""
+        m = np.ascontiguousarray(machine, dtype=np.int32)
+        j = np.ascontiguousarray(metric, dtype=np.int32)
+        t = np.ascontiguousarray(tick, dtype=np.int32)
+        v = np.ascontiguousarray(value, dtype=np.float64)
+        i32p = C.POINTER(C.c_int32)
+        _check(L.lib().mach_stream_append_records(self.h, len(v), m.ctypes.data_as(i32p), j.ctypes.data_as(i32p),
+                                                  t.ctypes.data_as(i32p), v.ctypes.data_as(L.dp), int(ticks),
+                                                  1 if carry_forward else 0))
+        self._last_ticks = int(ticks)
+
+    def state(self):
+        t, z = C.c_int64(), C.c_int64()
+        _check(L.lib().mach_stream_state(self.h, C.byref(t), C.byref(z)))
+        return t.value, z.value
+
+    def tensor(self) -> "SparseTensor":
+        h = C.c_void_p()
+        _check(L.lib().mach_stream_tensor(self.h, C.byref(h)))
+        ticks, _ = self.state()
+        return SparseTensor(h, self.dims[:-1] + (ticks,), self.dtype, self.ctx)
+
+    def last_slab(self) -> "DenseTensor":
+        h = C.c_void_p()
+        _check(L.lib().mach_stream_last_slab(self.h, C.byref(h)))
+        return DenseTensor(h, self.dims[:-1] + (self._last_ticks,), self.dtype, self.ctx)
+
+    def free(self):
+        if getattr(self, "h", None):
+            L.lib().mach_stream_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# binary tensor files (SURVEY 8f.4)
+# ---------------------------------------------------------------------------
+def tensor_file_info(path: str) -> dict:
+    kind, dt, order, nnz = C.c_int(), C.c_int(), C.c_int(), C.c_int64()
+    dims = (C.c_int * 8)()
+    _check(L.lib().mach_tensor_file_kind(str(path).encode(), C.byref(kind), C.byref(dt), C.byref(order), dims, C.byref(nnz)))
+    return {"kind": "sparse" if kind.value else "dense", "dtype": np.dtype(np.float64 if dt.value else np.float32),
+            "dims": tuple(dims[i] for i in range(order.value)), "count": nnz.value}
+
+
+def save_tensor(t, path: str):
+    fn = L.lib().mach_sparse_save if isinstance(t, SparseTensor) else L.lib().mach_dense_save
+    _check(fn(t.h, str(path).encode()))
+
+
+def load_tensor(path: str, ctx: Context | None = None):
+    """DenseTensor or SparseTensor in HBM from a MACHB2 binary file."""
+    ctx = _ctx(ctx)
+    info = tensor_file_info(path)
+    h = C.c_void_p()
+    if info["kind"] == "sparse":
+        _check(L.lib().mach_sparse_load(ctx.h, str(path).encode(), C.byref(h)))
+        return SparseTensor(h, info["dims"], info["dtype"], ctx)
+    _check(L.lib().mach_dense_load(ctx.h, str(path).encode(), C.byref(h)))
+    return DenseTensor(h, info["dims"], info["dtype"], ctx)

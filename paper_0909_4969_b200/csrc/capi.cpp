@@ -849,3 +849,191 @@ mach_status mach_ctx_kernel_stat(mach_ctx* ctx, int i, char* name, size_t len, i
 }
 
 }  // extern "C"
+
+// ---- Theorem-1 bound, streaming ingest, binary files ----
+namespace machb {
+void bound_conditions(const std::vector<int>& dims, double p, mach_bound_report* rep);
+double bound_min_probability(const std::vector<int>& dims);
+void theorem1_bound_dev(Ctx* ctx, const mach_dense* x, mach_sparse* xhat, const std::vector<int>& ranks, double p,
+                        mach_bound_report* rep, mach_bound_mode* per_mode);
+mach_stream* stream_begin(Ctx* ctx, int dtype, const std::vector<int>& dims, double p, std::uint64_t seed);
+void stream_append(mach_stream* s, const mach_dense* slab);
+void stream_append_host(mach_stream* s, const void* host, int ticks);
+void stream_append_records(mach_stream* s, std::int64_t n, const std::int32_t* machine, const std::int32_t* metric,
+                           const std::int32_t* tick, const double* value, int ticks, bool carry);
+void stream_state(mach_stream* s, std::int64_t* ticks, std::int64_t* nnz);
+mach_sparse* stream_tensor(mach_stream* s);
+mach_dense* stream_last_slab(mach_stream* s);
+void stream_free(mach_stream* s);
+int stream_device(const mach_stream* s);
+void dense_save(const mach_dense* t, const char* path);
+mach_dense* dense_load(Ctx* ctx, const char* path);
+void sparse_save(const mach_sparse* t, const char* path);
+mach_sparse* sparse_load(Ctx* ctx, const char* path);
+void tensor_file_kind(const char* path, int* kind, int* dtype, int* order, int* dims, std::int64_t* count);
+}  // namespace machb
+
+extern "C" {
+
+mach_status mach_achlioptas_bounds(double b, int64_t n, int64_t k, double p, double* two_norm, double* frobenius) {
+    return guard([&] {  // bounds.cpp:132-143
+        if (!(b >= 0.0)) throw_arg("b must be >= 0");
+        if (n < 1) throw_arg("n must be >= 1");
+        if (k < 1) throw_arg("k must be >= 1");
+        if (!(p > 0.0 && p <= 1.0)) throw_arg("p must be in (0, 1]");
+        const double nd = static_cast<double>(n), kd = static_cast<double>(k);
+        if (two_norm) *two_norm = 4.0 * b * std::sqrt(nd / p);
+        if (frobenius) *frobenius = 4.0 * b * std::sqrt(nd * kd / p);
+    });
+}
+
+mach_status mach_min_sampling_probability(int order, const int* dims, double* out) {
+    return guard([&] {
+        need(out, "out");
+        *out = bound_min_probability(order > 0 && dims ? std::vector<int>(dims, dims + order) : std::vector<int>());
+    });
+}
+
+mach_status mach_theorem1_conditions(int order, const int* dims, double p, mach_bound_report* rep) {
+    return guard([&] {  // bounds.cpp:152-158
+        need(rep, "rep");
+        const std::vector<int> d = order > 0 && dims ? std::vector<int>(dims, dims + order) : std::vector<int>();
+        bound_min_probability(d);  // the same shape checks
+        if (!(p > 0.0 && p <= 1.0)) throw_arg("p must be in (0, 1]");
+        bound_conditions(d, p, rep);
+    });
+}
+
+mach_status mach_theorem1_bound(mach_ctx* ctx, const mach_dense* x, const mach_sparse* xhat, const int* ranks, double p,
+                                mach_bound_report* rep, mach_bound_mode* per_mode) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
+        need(x, "x");
+        need(xhat, "xhat");
+        need(ranks, "ranks");
+        need(rep, "rep");
+        need(per_mode, "per_mode");
+        theorem1_bound_dev(&ctx->c, x, const_cast<mach_sparse*>(xhat),
+                           std::vector<int>(ranks, ranks + x->dims.size()), p, rep, per_mode);
+    });
+}
+
+mach_status mach_stream_begin(mach_ctx* ctx, mach_dtype dtype, int order, const int* dims, double p, uint64_t seed,
+                              mach_stream** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
+        need(out, "out");
+        *out = stream_begin(&ctx->c, dtype, dims_of(order, dims), p, seed);
+    });
+}
+
+mach_status mach_stream_append(mach_stream* s, const mach_dense* slab) {
+    return guard([&] {
+        need(s, "stream");
+        DevGuard dg_(stream_device(s));
+        need(slab, "slab");
+        stream_append(s, slab);
+    });
+}
+
+mach_status mach_stream_append_host(mach_stream* s, const void* host, int ticks) {
+    return guard([&] {
+        need(s, "stream");
+        DevGuard dg_(stream_device(s));
+        stream_append_host(s, host, ticks);
+    });
+}
+
+mach_status mach_stream_append_records(mach_stream* s, int64_t n, const int32_t* machine, const int32_t* metric,
+                                       const int32_t* tick, const double* value, int ticks, int carry_forward) {
+    return guard([&] {
+        need(s, "stream");
+        DevGuard dg_(stream_device(s));
+        stream_append_records(s, n, machine, metric, tick, value, ticks, carry_forward != 0);
+    });
+}
+
+mach_status mach_stream_state(mach_stream* s, int64_t* ticks, int64_t* nnz) {
+    return guard([&] {
+        need(s, "stream");
+        DevGuard dg_(stream_device(s));
+        std::int64_t t = 0, z = 0;
+        stream_state(s, &t, &z);
+        if (ticks) *ticks = t;
+        if (nnz) *nnz = z;
+    });
+}
+
+mach_status mach_stream_tensor(mach_stream* s, mach_sparse** out) {
+    return guard([&] {
+        need(s, "stream");
+        DevGuard dg_(stream_device(s));
+        need(out, "out");
+        *out = stream_tensor(s);
+    });
+}
+
+mach_status mach_stream_last_slab(mach_stream* s, mach_dense** out) {
+    return guard([&] {
+        need(s, "stream");
+        DevGuard dg_(stream_device(s));
+        need(out, "out");
+        *out = stream_last_slab(s);
+    });
+}
+
+mach_status mach_stream_free(mach_stream* s) {
+    return guard([&] {
+        if (!s) return;
+        DevGuard dg_(stream_device(s));
+        stream_free(s);
+    });
+}
+
+mach_status mach_dense_save(const mach_dense* t, const char* path) {
+    return guard([&] {
+        need(t, "tensor");
+        DevGuard dg_(t->ctx->device);
+        dense_save(t, path);
+    });
+}
+
+mach_status mach_dense_load(mach_ctx* ctx, const char* path, mach_dense** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
+        need(out, "out");
+        *out = dense_load(&ctx->c, path);
+    });
+}
+
+mach_status mach_sparse_save(const mach_sparse* t, const char* path) {
+    return guard([&] {
+        need(t, "tensor");
+        DevGuard dg_(t->ctx->device);
+        sparse_save(t, path);
+    });
+}
+
+mach_status mach_sparse_load(mach_ctx* ctx, const char* path, mach_sparse** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
+        need(out, "out");
+        *out = sparse_load(&ctx->c, path);
+    });
+}
+
+mach_status mach_tensor_file_kind(const char* path, int* kind, mach_dtype* dtype, int* order, int* dims, int64_t* nnz) {
+    return guard([&] {
+        int dt = 0;
+        std::int64_t c = 0;
+        tensor_file_kind(path, kind, &dt, order, dims, &c);
+        if (dtype) *dtype = static_cast<mach_dtype>(dt);
+        if (nnz) *nnz = c;
+    });
+}
+
+}  // extern "C"

@@ -33,6 +33,8 @@ void rethrow(mach_status st) {
             if (p != std::string::npos) msg = msg.substr(0, p);
             throw ConvergenceError(msg, mach_last_error_index());
         }
+        case MACH_ERR_IO: throw IoError(msg);
+        case MACH_ERR_PARSE: throw ParseError(msg, 1);
         default: throw std::runtime_error("mach-b200: " + msg);
     }
 }
@@ -50,6 +52,15 @@ mach_ctx* ctx() {
     thread_local CtxHolder h;
     return h.ctx;
 }
+
+}  // namespace
+
+namespace b200 {  // shared with cxx_api_ext.cpp
+mach_ctx* context() { return ctx(); }
+void check(mach_status st) { rethrow(st); }
+}  // namespace b200
+
+namespace {
 
 std::int64_t checked_size(const std::vector<int>& dims) {
     if (dims.empty()) throw ArgumentError("tensor must have at least one mode");

@@ -110,8 +110,9 @@ __device__ void eig_topk_cta(const double* __restrict__ G, int n, int k, double*
     fro = block_sum(fro, red_small);
     // exactly-zero Gram (zero matricization): identity basis, flagged
     if (fro == 0.0) {
-        for (int c = warp; c < k; c += kEigWarps)
-            for (int r = lane; r < n; r += 32) V[r + static_cast<std::size_t>(c) * n] = (r == c) ? 1.0 : 0.0;
+        if (V)
+            for (int c = warp; c < k; c += kEigWarps)
+                for (int r = lane; r < n; r += 32) V[r + static_cast<std::size_t>(c) * n] = (r == c) ? 1.0 : 0.0;
         for (int i = t; i < k; i += kEigThreads) sig[i] = 0.0;
         if (t == 0) {
             status[0] = 0;
@@ -232,6 +233,14 @@ __device__ void eig_topk_cta(const double* __restrict__ G, int n, int k, double*
         if (lane == 0) slam[tk] = 0.5 * (a + b);
     }
     __syncthreads();
+    if (!V) {  // eigenvalues only (the Theorem-1 bound's full spectra, bounds.cu)
+        for (int i = t; i < k; i += kEigThreads) sig[i] = sqrt(fmax(0.0, slam[i] * gmax));
+        if (t == 0) {
+            status[0] = 0;
+            status[1] = 0;
+        }
+        return;
+    }
 
     // ---- 4. inverse iteration (thread per cluster leader) ----
     // scratch layout per target q: U0,U1,U2,mult,swap (5n) ; z_T at scratch + 5nk

@@ -57,3 +57,31 @@ def test_cxx_headers_compile_against_the_library():
     subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), src, "-o", out,
                     _lib.LIB_PATH, f"-Wl,-rpath,{os.path.dirname(_lib.LIB_PATH)}"], check=True)
     assert os.path.exists(out)
+
+
+def test_next_row_mirrors_compile_and_host_only_calls_work(tmp_path):
+    """bounds.hpp / ingest.hpp / tensor_io.hpp / cli.hpp callers link; the
+    closed-form bound entry points and the CLI's usage errors need no GPU."""
+    src = os.path.join(ROOT, "tests", "cpp", "ext_smoke.cpp")
+    out = os.path.join(ROOT, "tests", "cpp", "ext_smoke")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), src, "-o", out,
+                    _lib.LIB_PATH, f"-Wl,-rpath,{os.path.dirname(_lib.LIB_PATH)}"], check=True)
+    assert mb.min_sampling_probability((100, 100, 100)) > 1.0
+    c = mb.theorem1_conditions((200, 200, 200), 0.5)
+    assert c["dims_large_enough"] and c["dims_balanced"] and not c["p_above_min"] and c["per_mode"] == []
+    two, fro = mb.achlioptas_bounds(1.0, 1000, 4, 1.0)
+    assert abs(two - 4.0 * 1000 ** 0.5) < 1e-9 and abs(fro - 4.0 * 4000 ** 0.5) < 1e-9
+    with pytest.raises(mb.ArgumentError):
+        mb.theorem1_conditions((5, 5), 1.5)
+    cli = os.path.join(ROOT, "paper_0909_4969_b200", "mach_b200")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_0909_4969_b200"), "cli"], check=True)
+    assert subprocess.run([cli], capture_output=True).returncode == 2
+    assert subprocess.run([cli, "frobnicate"], capture_output=True).returncode == 2
+    assert subprocess.run([cli, "hooi", "--input", "x", "--bogus", "1"], capture_output=True).returncode == 2
+    assert subprocess.run([cli, "hooi", "--input", str(tmp_path / "none"), "--ranks", "2,2", "--output", "o"],
+                          capture_output=True).returncode == 3
+    with pytest.raises(mb.IoError):
+        mb.tensor_file_info(str(tmp_path / "none.machb"))
+    (tmp_path / "junk.machb").write_bytes(b"x" * 100)
+    with pytest.raises(mb.ParseError):
+        mb.tensor_file_info(str(tmp_path / "junk.machb"))

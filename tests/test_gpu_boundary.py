@@ -102,3 +102,14 @@ def test_left_singular_basis_large_gram_matches_oracle(mb, rows, cols, k):
     assert np.abs(dev.singular_values - ref_s).max() <= 1e-10 * ref_s[0]
     r = dev.basis - ref_b @ (ref_b.T @ dev.basis)
     assert np.linalg.norm(r, 2) <= 1e-9
+
+
+def test_next_row_mirrors_reference_style_caller_runs(tmp_path):
+    """bounds / ingest (+ sample-on-arrival) / tensor files / CLI through the C++ mirror (tests/cpp/ext_smoke.cpp)."""
+    src = os.path.join(ROOT, "tests", "cpp", "ext_smoke.cpp")
+    exe = os.path.join(ROOT, "tests", "cpp", "ext_smoke")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), src, "-o", exe, _lib.LIB_PATH,
+                    f"-Wl,-rpath,{os.path.dirname(_lib.LIB_PATH)}"], check=True)
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "ext_smoke: 0 failures" in r.stdout
