@@ -202,6 +202,17 @@ __global__ void densify_kernel(const IdxT* __restrict__ idx, const T* __restrict
     if (i < nnz) out[idx[i]] = val[i];
 }
 
+// values rounded to TF32 (round to nearest, ties away): the tensor core then reads them exactly
+template <typename IdxT>
+__global__ void densify_tf32_kernel(const IdxT* __restrict__ idx, const float* __restrict__ val, long long nnz,
+                                    float* __restrict__ out) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= nnz) return;
+    std::uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(val[i]));
+    out[idx[i]] = __uint_as_float(r);
+}
+
 template <typename T, typename IdxT>
 __global__ void scatter_sub_kernel(const IdxT* __restrict__ idx, const T* __restrict__ val, long long nnz,
                                    double* __restrict__ out) {
@@ -334,6 +345,17 @@ void densify(Ctx* ctx, const mach_sparse* X, T* out) {
                   static_cast<const unsigned int*>(X->idx), static_cast<const T*>(X->val), X->nnz, out);
 }
 template void densify<float>(Ctx*, const mach_sparse*, float*);
+
+void densify_tf32(Ctx* ctx, const mach_sparse* X, float* out) {
+    MB_CUDA(cudaMemsetAsync(out, 0, static_cast<std::size_t>(X->numel) * sizeof(float), ctx->stream));
+    if (X->nnz == 0) return;
+    if (X->idx64)
+        MB_LAUNCH(ctx, densify_tf32_kernel<unsigned long long>, ceil_div(X->nnz, 256), 256, 0,
+                  static_cast<const unsigned long long*>(X->idx), static_cast<const float*>(X->val), X->nnz, out);
+    else
+        MB_LAUNCH(ctx, densify_tf32_kernel<unsigned int>, ceil_div(X->nnz, 256), 256, 0,
+                  static_cast<const unsigned int*>(X->idx), static_cast<const float*>(X->val), X->nnz, out);
+}
 template void densify<double>(Ctx*, const mach_sparse*, double*);
 
 template <typename T>

@@ -262,6 +262,8 @@ template <typename Tin, typename Tout>
 void dense_matricize(Ctx* ctx, const Tin* in, const std::vector<int>& dims, int mode, Tout* out);
 template <typename T>
 void densify(Ctx* ctx, const mach_sparse* X, T* out);
+// fp32 sampled tensor into a zeroed dense buffer, values rounded to TF32 (for the tensor-core Gram)
+void densify_tf32(Ctx* ctx, const mach_sparse* X, float* out);
 template <typename T>
 void sumsq_diff(Ctx* ctx, const T* x, const double* y, long long n, double* scratch, double* out);
 template <typename T>

@@ -735,6 +735,35 @@ struct SparseSession : SessionBase {
     std::vector<DBuf<double>> preG;
     cudaStream_t side = nullptr;
     cudaEvent_t grams_done = nullptr;
+    // Row Gram X_(m) X_(m)^T of the sampled tensor (sparse_kernels.cpp:60-63).
+    // The nonzero route forms every pair of a mode-m fibre (p^2 I_m / 2 pair
+    // products per element of the tensor); when that exceeds the dense
+    // contraction's work by a margin (C5 p = 0.1: 5.5e9 pairs per mode, 27 ms)
+    // the fp32 tensor is densified once (values rounded to TF32 to nearest,
+    // so the tensor core's operand truncation is exact and unbiased) and the
+    // Gram runs on tcgen05 (gram_tc.cu), read in place for every mode.
+    DBuf<float> xdense;
+    bool dense_gram_pays(int m) const {
+        if constexpr (!std::is_same_v<T, float>) return false;
+        const char* e = std::getenv("MACH_SPARSE_GRAM_TC_MIN");  // read per session (tests toggle it); <= 0: off
+        const double thr = e ? std::atof(e) : 1.5;
+        if (thr <= 0.0 || !gram_tc_applies(dims, m)) return false;
+        const double dens = static_cast<double>(X->nnz) / static_cast<double>(X->numel);
+        return 0.5 * dens * dens * dims[static_cast<std::size_t>(m)] >= thr;
+    }
+    void row_gram(int m, double* G) {
+        if constexpr (std::is_same_v<T, float>) {
+            if (dense_gram_pays(m)) {
+                if (!xdense.get()) {
+                    xdense.alloc(ctx, static_cast<std::size_t>(X->numel));
+                    densify_tf32(ctx, X, xdense.get());
+                }
+                gram_tc(ctx, xdense.get(), dims, m, G);
+                return;
+            }
+        }
+        sparse_row_gram<T>(ctx, X, m, normX2, G);
+    }
     void launch_row_grams() {
         if (std::getenv("MACH_NO_ASYNC_GRAMS")) return;  // read per session (tests toggle it)
         preG.clear();
@@ -759,8 +788,9 @@ struct SparseSession : SessionBase {
                 const int rows = dims[static_cast<std::size_t>(m)];
                 if (static_cast<long long>(rows) > X->numel / rows) continue;  // column side: needs the layouts
                 preG[static_cast<std::size_t>(m)].alloc(ctx, static_cast<std::size_t>(rows) * rows);
-                sparse_row_gram<T>(ctx, X, m, normX2, preG[static_cast<std::size_t>(m)].get());
+                row_gram(m, preG[static_cast<std::size_t>(m)].get());
             }
+            xdense.release();  // (stream-ordered: after the last tensor-core Gram on this stream)
         } catch (...) {
             ctx->stream = main;
             throw;
@@ -887,7 +917,7 @@ struct SparseSession : SessionBase {
                 w.G.s = ctx->stream;  // released in this stream's order, after its last use here
             } else {
                 w.G.alloc(ctx, static_cast<std::size_t>(w.n) * w.n);
-                if (w.row) sparse_row_gram<T>(ctx, X, m, normX2, w.G.get());
+                if (w.row) row_gram(m, w.G.get());
                 else sparse_col_gram<T>(ctx, X, *plans[static_cast<std::size_t>(m)], cols, normX2, w.G.get());
             }
             w.V.alloc(ctx, static_cast<std::size_t>(w.n) * w.kc);
@@ -896,6 +926,7 @@ struct SparseSession : SessionBase {
             jobs.push_back(EigJob{w.G.get(), w.n, w.kc, nullptr, 0, nullptr, w.V.get(), w.sig.get(), w.est.get(),
                                   nullptr, nullptr});
         }
+        xdense.release();
         if (grams_done) MB_CUDA(cudaStreamWaitEvent(ctx->stream, grams_done, 0));  // join the side stream's Grams
         if (!jobs.empty()) eig_select_batched(ctx, jobs);
         for (int m = 0; m < d; ++m) {

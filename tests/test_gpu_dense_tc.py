@@ -98,3 +98,46 @@ def test_mode_product_tf32x3_matches_fp64(mb, dims, mode, r):
     ref = np.moveaxis(np.tensordot(m, x.astype(np.float64), axes=([1], [mode])), 0, mode)
     scale = np.sqrt(dims[mode])  # typical magnitude of an output entry
     assert np.abs(got - ref).max() <= 2e-6 * scale, np.abs(got - ref).max() / scale
+
+
+def test_sampled_hosvd_gram_on_tensor_cores_when_dense_enough(monkeypatch):
+    """a sampled fp32 tensor whose mode fibres are long
+    (p^2 I_n / 2 >= 1.5 pair products per element) takes its HOSVD row Grams
+    from the densified tcgen05 Gram instead of the per-pair nonzero route.
+    Bars (north_star, fp32): factor sine <= 1e-3 against the oracle, fit and
+    core within 1e-4 relative; the two device routes agree the same way."""
+    import paper_0909_4969_b200 as mb
+
+    dims, ranks, p, seed = (256, 192, 320), (8, 6, 7), 0.2, 5  # below the 0.25 densify switch
+    x = lowrank_numpy(dims, ranks, 0.01, seed=9).astype(np.float32)
+    ctx = mb.Context(0)
+    xd = mb.DenseTensor.from_numpy(x, ctx)
+    mb.profile(ctx, True)
+    tc = mb.mach_hosvd(xd, ranks, mb.SparsifyConfig(p, seed), ctx=ctx)
+    ctx.synchronize()
+    stats = mb.kernel_stats(ctx)
+    mb.profile(ctx, False)
+    assert any("gram_tc" in k for k in stats), sorted(stats)
+    assert not any("row_gram_kernel" in k for k in stats), sorted(stats)
+    monkeypatch.setenv("MACH_SPARSE_GRAM_TC_MIN", "0")
+    mb.profile(ctx, True)
+    nz = mb.mach_hosvd(xd, ranks, mb.SparsifyConfig(p, seed), ctx=ctx)
+    ctx.synchronize()
+    stats = mb.kernel_stats(ctx)
+    mb.profile(ctx, False)
+    assert any("row_gram_kernel" in k for k in stats) and not any("gram_tc" in k for k in stats)
+    monkeypatch.delenv("MACH_SPARSE_GRAM_TC_MIN")
+    ref, ref_sp = O.mach_hosvd(O.Dense(x.astype(np.float64)), ranks, p, seed)
+    assert np.array_equal(tc.sparsified.entries()[0], ref_sp.entries()[0])
+    for got in (tc.model, nz.model):
+        for fd, fr in zip(got.factors, ref.factors):
+            assert subspace_sin(fd, fr) <= 1e-3
+        assert abs(got.fit - ref.fit) <= 1e-4 * max(abs(ref.fit), 1e-30) + 1e-6
+        assert rel(align_core(got.core, got.factors, ref.factors), ref.core) <= 1e-4
+    # and through HOOI (the Grams only seed it)
+    h = mb.mach_hooi(xd, ranks, mb.SparsifyConfig(p, seed), mb.HooiConfig(3, 0.0), ctx=ctx)
+    href, _ = O.mach_hooi(O.Dense(x.astype(np.float64)), ranks, p, seed, 3, 0.0)
+    assert h.model.iterations == href.iterations
+    assert abs(h.model.fit - href.fit) <= 1e-4 * abs(href.fit) + 1e-6
+    for fd, fr in zip(h.model.factors, href.factors):
+        assert subspace_sin(fd, fr) <= 1e-3
