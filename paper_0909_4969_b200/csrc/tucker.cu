@@ -116,15 +116,21 @@ struct Warm {
     int b = 0;
 };
 
+// out (C x k) = Y^T U: one warp per entry, lanes over the rows (fixed-order shuffle reduction)
 template <typename T>
 __global__ void yt_u_kernel(const T* __restrict__ Y, int rows, int C, const double* __restrict__ U, int k,
                             double* __restrict__ out) {
-    const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const long long idx = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (idx >= static_cast<long long>(C) * k) return;
     const int c = static_cast<int>(idx % C), j = static_cast<int>(idx / C);
+    const T* y = Y + static_cast<std::size_t>(c) * rows;
+    const double* u = U + static_cast<std::size_t>(j) * rows;
     double s = 0.0;
-    for (int i = 0; i < rows; ++i) s += static_cast<double>(Y[i + static_cast<std::size_t>(c) * rows]) * U[i + static_cast<std::size_t>(j) * rows];
-    out[idx] = s;
+    for (int i = lane; i < rows; i += 32) s += static_cast<double>(y[i]) * u[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[idx] = s;
 }
 
 template <typename T>
@@ -170,7 +176,7 @@ void lsb_device(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U
                 x0c = kk;
             } else {
                 seed.alloc(ctx, static_cast<std::size_t>(side) * kk);
-                MB_LAUNCH(ctx, yt_u_kernel<T>, ceil_div(static_cast<long long>(side) * kk, 256), 256, 0, Y, rows, side, Uprev,
+                MB_LAUNCH(ctx, yt_u_kernel<T>, ceil_div(static_cast<long long>(side) * kk * 32, 256), 256, 0, Y, rows, side, Uprev,
                           kk, seed.get());
                 X0 = seed.get();
                 x0c = kk;
@@ -236,7 +242,7 @@ bool lsb_fused(Ctx* ctx, const T* Y, int rows, long long cols, int k, double* U,
         x0c = warm->cols;
     } else if (Uprev) {
         seed.alloc(ctx, static_cast<std::size_t>(side) * k);
-        MB_LAUNCH(ctx, yt_u_kernel<T>, ceil_div(static_cast<long long>(side) * k, 256), 256, 0, Y, rows, side, Uprev, k,
+        MB_LAUNCH(ctx, yt_u_kernel<T>, ceil_div(static_cast<long long>(side) * k * 32, 256), 256, 0, Y, rows, side, Uprev, k,
                   seed.get());
         X0 = seed.get();
         x0c = k;
