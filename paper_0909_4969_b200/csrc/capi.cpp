@@ -387,7 +387,12 @@ static mach_status mach_pipeline(mach_ctx* ctx, const mach_dense* t, const int* 
         cudaEventElapsedTime(&ms, a, b);
         cudaEventDestroy(a);
         cudaEventDestroy(b);
-        mach_model* m = tucker_sparse(s.get(), ranks_of(static_cast<int>(t->dims.size()), ranks), do_hooi, max_it, tol);
+        // p == 1 keeps every nonzero entry unchanged: the densified sample (the
+        // densify switch, tucker.cpp:154-155) is the input itself, so the dense
+        // route reads t in place instead of a scattered copy
+        mach_model* m = p == 1.0
+                            ? tucker_dense(t, ranks_of(static_cast<int>(t->dims.size()), ranks), do_hooi, max_it, tol)
+                            : tucker_sparse(s.get(), ranks_of(static_cast<int>(t->dims.size()), ranks), do_hooi, max_it, tol);
         m->sample_ms = ms;
         *out = m;
         if (sampled) *sampled = s.release();

@@ -537,6 +537,127 @@ std::int64_t launch_sample(Ctx* ctx, const T* x, std::int64_t numel, std::int64_
     return launch_sample_tb<T, IdxT, 128>(ctx, x, numel, gofs, seed, p, capacity, out_idx, out_val, flags_host);
 }
 
+// ---- p == 1: every nonzero entry is kept (sampling.cpp:25-27 with u < 1 always) ----
+// The look-back kernel above stages at most TILE / 8 kept entries per tile and
+// falls back to per-thread strided stores beyond that (16 ms at 1024^3).  With
+// p = 1 no hash is needed: count the nonzeros per block, scan the block
+// counts, and write index and value runs coalesced (two streaming passes).
+constexpr int kAllBlock = 256, kAllPer = 16, kAllTile = kAllBlock * kAllPer;
+
+template <typename T>
+__global__ void __launch_bounds__(kAllBlock) keep_all_count_kernel(const T* __restrict__ x, std::int64_t numel,
+                                                                   unsigned* __restrict__ counts, int* __restrict__ flags) {
+    const std::int64_t base = static_cast<std::int64_t>(blockIdx.x) * kAllTile;
+    unsigned c = 0;
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < kAllPer; ++k) {
+        const std::int64_t i = base + k * kAllBlock + threadIdx.x;
+        if (i < numel) {
+            const T v = x[i];
+            c += v != T(0);
+            bad |= !isfinite(v);
+        }
+    }
+    if (bad) atomicOr(flags, 1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    __shared__ unsigned red[kAllBlock / 32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t = 0;
+        for (int w = 0; w < kAllBlock / 32; ++w) t += red[w];
+        counts[blockIdx.x] = t;
+    }
+}
+
+// one block: exclusive scan of the block counts into 64-bit offsets (+ the total)
+__global__ void __launch_bounds__(1024) keep_all_scan_kernel(const unsigned* __restrict__ counts, std::int64_t n,
+                                                             long long* __restrict__ offs, long long* __restrict__ total) {
+    __shared__ long long part[1024];
+    const std::int64_t per = (n + 1023) / 1024;
+    const std::int64_t b0 = threadIdx.x * per, b1 = min(n, b0 + per);
+    long long s = 0;
+    for (std::int64_t i = b0; i < b1; ++i) s += counts[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long run = 0;
+        for (int i = 0; i < 1024; ++i) {
+            const long long v = part[i];
+            part[i] = run;
+            run += v;
+        }
+        *total = run;
+    }
+    __syncthreads();
+    long long run = part[threadIdx.x];
+    for (std::int64_t i = b0; i < b1; ++i) {
+        offs[i] = run;
+        run += counts[i];
+    }
+}
+
+template <typename T, typename IdxT>
+__global__ void __launch_bounds__(kAllBlock) keep_all_write_kernel(const T* __restrict__ x, std::int64_t numel,
+                                                                   std::int64_t gofs, const long long* __restrict__ offs,
+                                                                   IdxT* __restrict__ out_idx, T* __restrict__ out_val) {
+    const std::int64_t base = static_cast<std::int64_t>(blockIdx.x) * kAllTile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ unsigned wsum[kAllBlock / 32];
+    __shared__ long long run_s;
+    if (threadIdx.x == 0) run_s = offs[blockIdx.x];
+    __syncthreads();
+#pragma unroll 1
+    for (int k = 0; k < kAllPer; ++k) {
+        const std::int64_t i = base + k * kAllBlock + threadIdx.x;
+        T v = T(0);
+        if (i < numel) v = x[i];
+        const bool keep = v != T(0);
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wsum[warp] = __popc(m);
+        __syncthreads();
+        unsigned before = 0, all = 0;
+#pragma unroll
+        for (int w = 0; w < kAllBlock / 32; ++w) {
+            const unsigned c = wsum[w];
+            before += w < warp ? c : 0u;
+            all += c;
+        }
+        const long long run = run_s;
+        if (keep) {
+            const long long o = run + before + __popc(m & ((1u << lane) - 1u));
+            out_idx[o] = static_cast<IdxT>(gofs + i);
+            out_val[o] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) run_s = run + all;
+    }
+}
+
+template <typename T, typename IdxT>
+std::int64_t launch_keep_all(Ctx* ctx, const T* x, std::int64_t numel, std::int64_t gofs, void** out_idx, void** out_val,
+                             int* flags_host) {
+    const std::int64_t nb = (numel + kAllTile - 1) / kAllTile;
+    DBuf<unsigned> counts(ctx, static_cast<std::size_t>(nb));
+    DBuf<long long> offs(ctx, static_cast<std::size_t>(nb) + 1);
+    DBuf<int> flags(ctx, 1);
+    flags.zero(ctx);
+    MB_LAUNCH(ctx, keep_all_count_kernel<T>, static_cast<unsigned>(nb), kAllBlock, 0, x, numel, counts.get(), flags.get());
+    MB_LAUNCH(ctx, keep_all_scan_kernel, 1, 1024, 0, counts.get(), nb, offs.get(), offs.get() + nb);
+    long long tot = 0;
+    to_host(ctx, &tot, offs.get() + nb, 1);
+    to_host(ctx, flags_host, flags.get(), 1);
+    sync(ctx);
+    if ((*flags_host & 1) || tot == 0) return tot;
+    MB_CUDA(cudaMallocAsync(out_idx, static_cast<std::size_t>(tot) * sizeof(IdxT), ctx->stream));
+    MB_CUDA(cudaMallocAsync(out_val, static_cast<std::size_t>(tot) * sizeof(T), ctx->stream));
+    MB_LAUNCH(ctx, (keep_all_write_kernel<T, IdxT>), static_cast<unsigned>(nb), kAllBlock, 0, x, numel, gofs, offs.get(),
+              static_cast<IdxT*>(*out_idx), static_cast<T*>(*out_val));
+    return tot;
+}
+
 }  // namespace
 
 // Host entry: returns a new canonical sparse tensor in HBM.  With a slab, x
@@ -560,6 +681,26 @@ mach_sparse* sample_slab(const mach_dense* x, const std::vector<int>& gdims, std
     const double mean = p * static_cast<double>(x->numel);
     std::int64_t cap = static_cast<std::int64_t>(mean + 12.0 * std::sqrt(mean + 1.0) + 8192.0);
     if (cap > x->numel) cap = x->numel;
+    if (p == 1.0 && x->numel > 0 && x->numel / kAllTile < 0x7fffffffll && !std::getenv("MACH_SAMPLER_NO_KEEP_ALL")) {
+        void *di = nullptr, *dv = nullptr;
+        int flags = 0;
+        std::int64_t nnz = 0;
+        if (x->dtype == MACH_F32)
+            nnz = out->idx64 ? launch_keep_all<float, unsigned long long>(ctx, static_cast<const float*>(x->data), x->numel,
+                                                                          offset, &di, &dv, &flags)
+                             : launch_keep_all<float, unsigned int>(ctx, static_cast<const float*>(x->data), x->numel, offset,
+                                                                    &di, &dv, &flags);
+        else
+            nnz = out->idx64 ? launch_keep_all<double, unsigned long long>(ctx, static_cast<const double*>(x->data), x->numel,
+                                                                           offset, &di, &dv, &flags)
+                             : launch_keep_all<double, unsigned int>(ctx, static_cast<const double*>(x->data), x->numel,
+                                                                     offset, &di, &dv, &flags);
+        if (flags & 1) throw_arg("tensor values must be finite");
+        out->nnz = nnz;
+        out->idx = di;
+        out->val = dv;
+        return out.release();
+    }
     for (int attempt = 0; attempt < 2; ++attempt) {
         void *di = nullptr, *dv = nullptr;
         if (cap > 0) {

@@ -103,3 +103,33 @@ def test_large_size_properties(mb):
     got = idx[(idx >= lo) & (idx < lo + 20000)]
     assert np.array_equal(got, want)
     del torch
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("n", [1, 4095, 4096, 4097, 70001])
+def test_keep_all_path_p1(mb, dtype, n):
+    """p = 1 (sampling.cpp:25-27: every nonzero entry, values unchanged) runs the
+    two-pass keep-all kernels: kept set and values equal the oracle's, zeros
+    (and -0.0) skipped, ragged sizes, slab offsets, non-finite input rejected."""
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(n).astype(dtype)
+    x[rng.random(n) < 0.3] = 0.0
+    if n > 10:
+        x[7] = -0.0
+    dims = (n, 1, 1) if n < 100 else (n,)
+    x = x.reshape(dims)
+    ref_idx, ref_val = O.sparsify(O.Dense(x.astype(np.float64)), 1.0, 3).entries()
+    sp = mb.sparsify(mb.DenseTensor.from_numpy(x), mb.SparsifyConfig(1.0, 3))
+    idx, val = sp.entries()
+    assert np.array_equal(idx, ref_idx) and np.array_equal(val, ref_val)
+    if n > 4096:
+        off = 1000
+        part = mb.sparsify_slab(mb.DenseTensor.from_numpy(x.reshape(-1)[off:].reshape(-1)), (n,), off, mb.SparsifyConfig(1.0, 3))
+        pi, pv = part.entries()
+        assert np.array_equal(pi, ref_idx[ref_idx >= off]) and np.array_equal(pv, ref_val[ref_idx >= off])
+        bad = x.copy().reshape(-1)
+        bad[n // 2] = np.inf
+        with pytest.raises(mb.ArgumentError):
+            mb.sparsify(mb.DenseTensor.from_numpy(bad), mb.SparsifyConfig(1.0, 3))
+    z = mb.sparsify(mb.DenseTensor.from_numpy(np.zeros((5, 4), dtype=dtype)), mb.SparsifyConfig(1.0, 3))
+    assert z.nnz == 0
