@@ -636,12 +636,21 @@ struct SparseSession : SessionBase {
         comm_allreduce_sum(ctx, Y.get(), static_cast<std::size_t>(dims[static_cast<std::size_t>(m)]) * C[static_cast<std::size_t>(m)],
                            sizeof(T) == 8);
     }
+    bool stage1_waits = false;  // side-stream launch beside an unfused basis chain: wait at entry
     void stage1(int m) {
+        // SMs left to the concurrent basis work: the fused 16-CTA cluster is
+        // already resident when stage 1 starts (16); the unfused chain's
+        // kernels arrive later and its 8-CTA cluster solver needs 8 free SMs
+        // inside one GPC (measured at C5: 16 or 32 free SMs leave the cluster
+        // waiting for stage 1 to drain, 1.7 ms instead of 0.43; 40 and more do not)
         static const int reserve = std::getenv("MACH_OV_RESERVE") ? std::atoi(std::getenv("MACH_OV_RESERVE")) : 16;
+        static const int reserve_side =
+            std::getenv("MACH_OV_RESERVE_SIDE") ? std::atoi(std::getenv("MACH_OV_RESERVE_SIDE")) : 40;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
         sparse_mode_stage1<T>(ctx, *plans[static_cast<std::size_t>(m)], dims, ranks, Urp,
-                              Fov[static_cast<std::size_t>(m)].get(), sms - reserve);
+                              Fov[static_cast<std::size_t>(m)].get(),
+                              std::max(8, sms - (stage1_waits ? reserve_side : reserve)), !stage1_waits);
     }
     void stage2(int m) {
         auto& P = *plans[static_cast<std::size_t>(m)];
@@ -971,10 +980,42 @@ struct SparseSession : SessionBase {
                                     fs.st.get() + 3 * i, &warm[si], fs.U[si].get(), Ur[si].get(),
                                     ttm_stride(ranks[si], sizeof(T))))
             return;
+        // Unfused basis chain (Grams too large for the fused cluster: C5's 256
+        // columns): the next mode's stage 1, queued in after_basis, needs only
+        // factors this update does not touch, so it runs beside the chain on
+        // the side stream (fork / join by events: a parallel branch of the
+        // sweep graph), on the SMs stage1() does not reserve.
+        bool forked = false;
+        static const bool no_side = std::getenv("MACH_NO_SIDE_STAGE1") != nullptr;
+        if (ctx->after_basis && !no_side) {
+            auto cb = std::move(ctx->after_basis);
+            ctx->after_basis = nullptr;
+            if (!side) MB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+            if (!ev_fork) MB_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+            if (!ev_join) MB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+            MB_CUDA(cudaEventRecord(ev_fork, ctx->stream));
+            MB_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+            cudaStream_t main = ctx->stream;
+            ctx->stream = side;
+            stage1_waits = true;
+            try {
+                cb();
+            } catch (...) {
+                ctx->stream = main;
+                stage1_waits = false;
+                throw;
+            }
+            ctx->stream = main;
+            stage1_waits = false;
+            MB_CUDA(cudaEventRecord(ev_join, side));
+            forked = true;
+        }
         lsb_device<T>(ctx, Y.get(), dims[si], C[si], ranks[si], fs.U[si].get(), sv_at(i), fs.st.get() + 3 * i,
                       &warm[si], fs.U[si].get());
         refresh(i);
+        if (forked) MB_CUDA(cudaStreamWaitEvent(ctx->stream, ev_join, 0));
     }
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // Steady-state sweeps (every mode warm-started) are captured once into a
     // CUDA graph and replayed: one launch per sweep instead of ~40 host
     // submissions.  Only the fit read-back (and its rare entrywise-residual
@@ -986,6 +1027,8 @@ struct SparseSession : SessionBase {
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         if (graph) cudaGraphDestroy(graph);
         if (grams_done) cudaEventDestroy(grams_done);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
         if (side) cudaStreamDestroy(side);
     }
     bool graph_ok() const {
