@@ -1029,7 +1029,13 @@ void y_from_segments(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const 
     const int G = threads / ra;
     const int rns = ttm_stride(rn, sizeof(T));
     const std::size_t ubytes = static_cast<std::size_t>(dims[n]) * rns * sizeof(T);
-    const bool stage = ubytes <= 64 * 1024;
+    // U_n rows are staged in shared memory when they fit beside two resident
+    // CTAs (C5: 1024 rows x 80 B = 80 KB; gathering them from L2 instead made
+    // this kernel latency-bound); large staged copies run on a persistent grid
+    // whose CTAs keep the copy across their rows
+    static const std::size_t stage_max =
+        std::getenv("MACH_S2_STAGE_MAX") ? static_cast<std::size_t>(std::atoll(std::getenv("MACH_S2_STAGE_MAX"))) : 80 * 1024;
+    const bool stage = ubytes <= stage_max;
     const int chunk = static_cast<int>(std::min<std::size_t>(2048, (24 * 1024) / (ra * sizeof(T))));
     // shared memory: [U][fibre-sum chunk, later the group partials][i_n chunk]; ~55 KB at C2: four CTAs per SM
     const std::size_t fbytes = std::max(static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16,
@@ -1039,7 +1045,13 @@ void y_from_segments(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const 
     auto launch = [&](auto y_from_segments_kernel_rn) {  // (the name is the profiler's kernel label)
         auto kern = y_from_segments_kernel_rn;
         MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        MB_LAUNCH_PDL(ctx, y_from_segments_kernel_rn, rows, threads, smem, P.seg_ptr.get(), P.seg_row.get(), fseg, ra, Un, rns, rn, sa, sn, rows,
+        int grid = rows;
+        if (stage && ubytes > 32 * 1024) {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+            grid = std::min<int>(rows, sms * std::max<int>(1, static_cast<int>((227 * 1024) / (smem + 1024))));
+        }
+        MB_LAUNCH_PDL(ctx, y_from_segments_kernel_rn, grid, threads, smem, P.seg_ptr.get(), P.seg_row.get(), fseg, ra, Un, rns, rn, sa, sn, rows,
                   stage ? dims[n] : 0, chunk, 1, Y);
     };
     // RN >= rn register accumulators
@@ -1113,7 +1125,13 @@ void sparse_mode_stage2(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, con
     const int G = threads / ra;
     const int rbs = ttm_stride(rb, sizeof(T));
     const std::size_t ubytes = static_cast<std::size_t>(dims[b]) * rbs * sizeof(T);
-    const bool stage = ubytes <= 64 * 1024;
+    // U_n rows are staged in shared memory when they fit beside two resident
+    // CTAs (C5: 1024 rows x 80 B = 80 KB; gathering them from L2 instead made
+    // this kernel latency-bound); large staged copies run on a persistent grid
+    // whose CTAs keep the copy across their rows
+    static const std::size_t stage_max =
+        std::getenv("MACH_S2_STAGE_MAX") ? static_cast<std::size_t>(std::atoll(std::getenv("MACH_S2_STAGE_MAX"))) : 80 * 1024;
+    const bool stage = ubytes <= stage_max;
     const int chunk = static_cast<int>(std::min<std::size_t>(2048, (24 * 1024) / (ra * sizeof(T))));
     const std::size_t fbytes = std::max(static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16,
                                         static_cast<std::size_t>(G) * ra * rb * sizeof(T));
@@ -1123,7 +1141,13 @@ void sparse_mode_stage2(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, con
         auto kern = y_from_segments_kernel_rn;
         MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         static const int rpc = std::getenv("MACH_S2_RPC") ? std::atoi(std::getenv("MACH_S2_RPC")) : 1;  // rows per CTA (1 measured best)
-        MB_LAUNCH_PDL(ctx, y_from_segments_kernel_rn, (rows + rpc - 1) / rpc, threads, smem, P.st_base.get(), P.seg_ib.get(), F, ra, Ub, rbs,
+        int grid = (rows + rpc - 1) / rpc;
+        if (stage && ubytes > 32 * 1024) {  // persistent: each CTA stages the large U_b once
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+            grid = std::min<int>(grid, sms * std::max<int>(1, static_cast<int>((227 * 1024) / (smem + 1024))));
+        }
+        MB_LAUNCH_PDL(ctx, y_from_segments_kernel_rn, grid, threads, smem, P.st_base.get(), P.seg_ib.get(), F, ra, Ub, rbs,
                       rb, sa, sb, rows, stage ? dims[b] : 0, chunk, 32, Y);
     };
     if (rb <= 4) launch(y_from_segments_kernel<T, 4>);

@@ -69,7 +69,12 @@ idx, _ = st.tensor().entries()
 assert np.array_equal(idx, ref_idx), "streamed kept set differs from the one-shot sampler"
 st.free()
 dev_buf = torch.empty_like(x)
-copy_only = wall(lambda: dev_buf.copy_(host, non_blocking=True))
+def copy_all():
+    dev_buf.copy_(host, non_blocking=True)
+    torch.cuda.synchronize()
+
+
+copy_only = wall(copy_all)
 t_host = wall(lambda: stream_host().free())
 t_dev = wall(lambda: stream_dev().free())
 gb = x.numel() * 4 / 1e9
