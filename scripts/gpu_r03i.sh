@@ -1,4 +1,5 @@
-# round 2 final-state evidence: GPU tests, bench lines (all configs), reference arm, launch lists, ncu captures, 8(f) timings
+# round 2 final-state evidence: GPU tests, bench lines (all configs), reference arm, launch lists, ncu captures
+# (summarised on the box: the .ncu-rep files are too large to bring back), 8(f) timings
 timeout 2400 python -m pytest tests -m gpu -x -q 2>&1 | tail -6 > gpurun_out/r03i_pytest.txt; cat gpurun_out/r03i_pytest.txt
 timeout 900 python bench.py > gpurun_out/r03i_c2.json 2> gpurun_out/r03i_c2.err; echo c2 rc=$?
 timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/r03i_ref.json 2> gpurun_out/r03i_ref.err; echo ref rc=$?
@@ -8,13 +9,20 @@ done
 timeout 900 python scripts/next_rows_time.py > gpurun_out/r03i_next_rows.jsonl 2> gpurun_out/r03i_next_rows.err; echo next rc=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r03i_launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r03i_ncu_ll.log 2>&1; echo ll rc=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r03i_launches_c5.csv python bench.py --config c5 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r03i_ncu_ll5.log 2>&1; echo ll5 rc=$?
-CMD="python scripts/prof_sweep.py --config c2 --sweeps 3"
-$CMD > gpurun_out/plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:ttm_mode_kernel -s 3 -c 1 -o gpurun_out/r03i_ttm_stage1 $CMD > gpurun_out/ncu1.log 2>&1; echo ncu1 rc=$?
-$CMD > gpurun_out/plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:mode_basis_kernel -s 6 -c 1 -o gpurun_out/r03i_mode_basis $CMD > gpurun_out/ncu2.log 2>&1; echo ncu2 rc=$?
-python scripts/samp_prof.py > gpurun_out/plain_s.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:sample_kernel -s 1 -c 1 -o gpurun_out/r03i_sampler python scripts/samp_prof.py > gpurun_out/ncu3.log 2>&1; echo ncu3 rc=$?
-CMD5="python scripts/prof_sweep.py --config c5 --sweeps 2"
-$CMD5 > gpurun_out/plain5.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:gram_tc_kernel -s 1 -c 1 -o gpurun_out/r03i_gram_tc_sampled $CMD5 > gpurun_out/ncu5.log 2>&1; echo ncu5 rc=$?
-$CMD5 > gpurun_out/plain5.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:ttm_mode_kernel -s 4 -c 1 -o gpurun_out/r03i_ttm_stage1_c5 $CMD5 > gpurun_out/ncu6.log 2>&1; echo ncu6 rc=$?
-CMD1="python scripts/prof_sweep.py --config c5p1 --sweeps 1"
-$CMD1 > gpurun_out/plain1.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:keep_all_write_kernel -c 1 -o gpurun_out/r03i_keep_all $CMD1 > gpurun_out/ncu7.log 2>&1; echo ncu7 rc=$?
-ls -la gpurun_out/r03i_*.ncu-rep
+cap() {  # cap <tag> <config> <kernel regex> <skip> <command...>
+  local tag=$1 cfg=$2 k=$3 skip=$4; shift 4
+  "$@" > gpurun_out/plain.log 2>&1 || { echo "$tag plain run failed"; return; }
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c 1 -o /tmp/$tag "$@" > gpurun_out/ncu_$tag.log 2>&1
+  echo "$tag ncu rc=$?"
+  python scripts/ncu_summary.py /tmp/$tag.ncu-rep --config $cfg --tag $tag > /dev/null 2>&1 && cp profiles/$tag.json profiles/$tag.md gpurun_out/
+  ncu -i /tmp/$tag.ncu-rep --page source --csv > /tmp/$tag.src.csv 2>/dev/null && python scripts/ncu_hot.py /tmp/$tag.src.csv 25 > gpurun_out/${tag}_hotlines.txt 2>/dev/null
+  rm -f /tmp/$tag.ncu-rep
+}
+cap r03i_ttm_stage1_ncu c2 ttm_mode_kernel 3 python scripts/prof_sweep.py --config c2 --sweeps 3
+cap r03i_mode_basis_ncu c2 mode_basis_kernel 6 python scripts/prof_sweep.py --config c2 --sweeps 3
+cap r03i_sampler_ncu c2 sample_kernel 1 python scripts/samp_prof.py
+cap r03i_ttm_stage1_c5_ncu c5 ttm_mode_kernel 4 python scripts/prof_sweep.py --config c5 --sweeps 2
+cap r03i_gram_tc_sampled_ncu c5 gram_tc_kernel 1 python scripts/prof_sweep.py --config c5 --sweeps 1
+cap r03i_stage2_c5_ncu c5 y_from_segments_kernel 4 python scripts/prof_sweep.py --config c5 --sweeps 2
+cap r03i_keep_all_ncu c5p1 keep_all_write_kernel 0 python scripts/prof_sweep.py --config c5p1 --sweeps 1
+du -sh gpurun_out
