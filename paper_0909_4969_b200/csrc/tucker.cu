@@ -627,6 +627,17 @@ struct SparseSession : SessionBase {
     bool overlap = false;
     bool split4 = false;    // order 4: stage 1 + the dimension-tree stage 2 (stage2_4way_kernel)
     bool f0_ready = false;  // Fov[0] holds mode 0's stage 1 for the current factors
+    // order 4: Fov[m] already holds mode m's stage 1 for the current factors
+    // (launched beside the previous mode's unfused basis chain, sweep_body)
+    std::vector<char> s1_ready;
+    bool prefetch4(int i, int nx) const {
+        static const bool off = std::getenv("MACH_NO_SIDE_STAGE1") != nullptr;
+        if (off || !split4 || (sharded && !comm_shard)) return false;
+        if (plans[static_cast<std::size_t>(nx)]->a == i) return false;  // stage 1 of nx gathers the factor being updated
+        const long long rows = dims[static_cast<std::size_t>(i)], cols = C[static_cast<std::size_t>(i)];
+        const bool row_side = rows <= cols && ranks[static_cast<std::size_t>(i)] <= cols;
+        return row_side || cols > 4096;  // the update is the unfused chain (lsb_fused declines these)
+    }
     bool overlap_ok() const { return overlap && (!sharded || comm_shard); }
     // one shard of a time-slab partition with the library's NCCL communicator:
     // every mode's partial Y_(n) is all-reduced in stream before its update
@@ -665,10 +676,13 @@ struct SparseSession : SessionBase {
     void mode_y(int m) {
         const std::size_t sm = static_cast<std::size_t>(m);
         if (split4) {  // order 4: fibre sums (waiting launch), then the two-level stage 2
-            int sms = 148;
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-            sparse_mode_stage1<T>(ctx, *plans[sm], dims, ranks, Urp, Fov[0].get(), sms, false);
-            sparse_mode_stage2_4way<T>(ctx, *plans[sm], dims, ranks, Fov[0].get(), Urp, Y.get());
+            if (!s1_ready[sm]) {  // not prefetched beside the previous mode's basis chain
+                int sms = 148;
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+                sparse_mode_stage1<T>(ctx, *plans[sm], dims, ranks, Urp, Fov[sm].get(), sms, false);
+            }
+            s1_ready[sm] = 0;
+            sparse_mode_stage2_4way<T>(ctx, *plans[sm], dims, ranks, Fov[sm].get(), Urp, Y.get());
             return;
         }
         if (m >= 1 && fseg_for == m) {
@@ -829,6 +843,7 @@ struct SparseSession : SessionBase {
         warnings = init->warnings;
         fseg_for = -1;
         f0_ready = false;
+        std::fill(s1_ready.begin(), s1_ready.end(), 0);
     }
     void setup(mach_sparse* sp, const std::vector<int>& rk) {
         X = sp;
@@ -889,11 +904,12 @@ struct SparseSession : SessionBase {
         Y.alloc(ctx, maxY);
         if (overlap || split4) {
             Fov.clear();
-            Fov.resize(overlap ? static_cast<std::size_t>(d) : 1);
+            Fov.resize(static_cast<std::size_t>(d));  // one fibre-sum buffer per mode (3-way overlap, 4-way prefetch)
+            s1_ready.assign(static_cast<std::size_t>(d), 0);
             for (int m = 0; m < d; ++m) {
                 const std::size_t need = static_cast<std::size_t>(plans[static_cast<std::size_t>(m)]->n_task) * 32 *
                                              ranks[static_cast<std::size_t>(plans[static_cast<std::size_t>(m)]->a)] + 16;
-                auto& B = Fov[overlap ? static_cast<std::size_t>(m) : 0];  // slack: stage 2 bulk-copies aligned supersets
+                auto& B = Fov[static_cast<std::size_t>(m)];  // slack: stage 2 bulk-copies aligned supersets
                 if (B.n < need) B.alloc(ctx, need);
             }
         }
@@ -965,6 +981,7 @@ struct SparseSession : SessionBase {
         warnings = read_warnings(ctx, fs.st, ranks, all);
         fseg_for = -1;
         f0_ready = false;
+        std::fill(s1_ready.begin(), s1_ready.end(), 0);
         mode_y(d - 1);
         fit = prev_fit = core_and_fit();
         hosvd_ms = tm.stop_ms();
@@ -976,6 +993,8 @@ struct SparseSession : SessionBase {
         const std::size_t si = static_cast<std::size_t>(i);
         if (fseg_for >= 1 && plans[static_cast<std::size_t>(fseg_for - 1)]->a == i) fseg_for = -1;  // F used U_i
         if (plans[0]->a == i) f0_ready = false;  // the prefetched mode-0 stage 1 used U_i
+        for (std::size_t m = 0; m < s1_ready.size(); ++m)
+            if (plans[m]->a == i) s1_ready[m] = 0;
         if (!nofuse && lsb_fused<T>(ctx, Y.get(), dims[si], C[si], ranks[si], fs.U[si].get(), sv_at(i),
                                     fs.st.get() + 3 * i, &warm[si], fs.U[si].get(), Ur[si].get(),
                                     ttm_stride(ranks[si], sizeof(T))))
@@ -1063,7 +1082,14 @@ struct SparseSession : SessionBase {
         for (int i = 0; i < d; ++i) {
             mode_y(i);
             reduce_y(i);
+            const int nx = (i + 1) % d;
+            if (prefetch4(i, nx))  // order 4: the next mode's stage 1 beside this mode's basis chain (side stream)
+                ctx->after_basis = [this, nx]() {
+                    stage1(nx);
+                    s1_ready[static_cast<std::size_t>(nx)] = 1;
+                };
             mode_update(i);
+            ctx->after_basis = nullptr;  // not taken (side launches off): mode_y runs it in line
         }
         core_device();
     }
@@ -1124,6 +1150,7 @@ struct SparseSession : SessionBase {
         if (graph_exec) { cudaGraphExecDestroy(graph_exec); graph_exec = nullptr; }
         if (graph) { cudaGraphDestroy(graph); graph = nullptr; }
         f0_ready = false;
+        std::fill(s1_ready.begin(), s1_ready.end(), 0);
     }
     void set_norm2(double v) override {
         if (!(v >= 0.0)) throw_arg("norm2 must be >= 0");
