@@ -596,25 +596,48 @@ template void core_from_last<double>(Ctx*, const double*, int, int, const double
 // core_from_last and |core|^2 in one launch: each CTA's partial sum of
 // squares goes to part[block]; the last CTA to finish (atomic ticket) sums
 // the partials in block order (deterministic) and re-arms the ticket.
-template <typename T>
+template <typename T, int WPO>  // WPO warps per output entry (row range split in WPO contiguous parts)
 __global__ void __launch_bounds__(256) core_sumsq_kernel(const T* __restrict__ Y, int rows, int C,
                                                          const double* __restrict__ U, int r, double* __restrict__ core,
                                                          double* __restrict__ part, unsigned* __restrict__ ticket,
                                                          double* __restrict__ out) {
     pdl_enter();  // programmatic dependent launch: predecessor complete and visible
     __shared__ double red[8];
+    __shared__ double wsum[8];
     __shared__ bool last;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int entry = blockIdx.x * (8 / WPO) + wib / WPO, sub = wib % WPO;
     double s = 0.0;
-    if (warp < C * r) {
-        const int col = warp % C, alpha = warp / C;
-        for (int i = lane; i < rows; i += 32)
-            s += U[i + static_cast<std::size_t>(alpha) * rows] * static_cast<double>(Y[i + static_cast<std::size_t>(col) * rows]);
+    if (entry < C * r) {
+        const int col = entry % C, alpha = entry / C;
+        // eight independent chains per lane (fixed combination order): a tall
+        // last mode (C4: 65536 rows) made the single chain L2-latency-bound
+        const double* u = U + static_cast<std::size_t>(alpha) * rows;
+        const T* y = Y + static_cast<std::size_t>(col) * rows;
+        const int per = ((rows + WPO - 1) / WPO + 31) & ~31;
+        const int r0 = sub * per, r1 = min(rows, r0 + per);
+        double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int i = r0 + lane;
+        for (; i + 7 * 32 < r1; i += 256) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a[q] = fma(u[i + 32 * q], static_cast<double>(y[i + 32 * q]), a[q]);
+        }
+        for (; i < r1; i += 32) a[0] = fma(u[i], static_cast<double>(y[i]), a[0]);
+        s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) core[col + static_cast<std::size_t>(C) * alpha] = s;
     }
-    if (lane == 0) red[threadIdx.x >> 5] = s * s;
+    if (lane == 0) wsum[wib] = s;
+    __syncthreads();
+    double sq = 0.0;
+    if (lane == 0 && sub == 0 && entry < C * r) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < WPO; ++q) t += wsum[wib + q];  // parts in row order
+        core[(entry % C) + static_cast<std::size_t>(C) * (entry / C)] = t;
+        sq = t * t;
+    }
+    if (lane == 0) red[wib] = sq;
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
@@ -633,11 +656,20 @@ __global__ void __launch_bounds__(256) core_sumsq_kernel(const T* __restrict__ Y
     }
 }
 
+int core_sumsq_blocks(int rows, int C, int r) {
+    const long long entries = static_cast<long long>(C) * r;
+    const int wpo = rows >= 8192 ? 4 : 1;
+    return static_cast<int>((entries + (8 / wpo) - 1) / (8 / wpo));
+}
+
 template <typename T>
 void core_sumsq(Ctx* ctx, const T* Y, int rows, int C, const double* U, int r, double* core, double* part,
                 unsigned* ticket, double* out) {
-    const long long warps = static_cast<long long>(C) * r;
-    MB_LAUNCH_PDL(ctx, core_sumsq_kernel<T>, ceil_div(warps * 32, 256), 256, 0, Y, rows, C, U, r, core, part, ticket, out);
+    const int blocks = core_sumsq_blocks(rows, C, r);
+    if (rows >= 8192)
+        MB_LAUNCH_PDL(ctx, (core_sumsq_kernel<T, 4>), blocks, 256, 0, Y, rows, C, U, r, core, part, ticket, out);
+    else
+        MB_LAUNCH_PDL(ctx, (core_sumsq_kernel<T, 1>), blocks, 256, 0, Y, rows, C, U, r, core, part, ticket, out);
 }
 template void core_sumsq<float>(Ctx*, const float*, int, int, const double*, int, double*, double*, unsigned*, double*);
 template void core_sumsq<double>(Ctx*, const double*, int, int, const double*, int, double*, double*, unsigned*, double*);

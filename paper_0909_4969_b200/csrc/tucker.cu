@@ -14,6 +14,7 @@
 namespace machb {
 
 mach_sparse* sample_dense(const mach_dense* x, double p, std::uint64_t seed);
+int core_sumsq_blocks(int rows, int C, int r);  // linalg.cu: grid of core_sumsq (must fit the sumsq_scratch() partials)
 
 std::int64_t checked_size(const std::vector<int>& dims) {
     if (dims.empty()) throw_arg("tensor must have at least one mode");
@@ -711,7 +712,7 @@ struct SparseSession : SessionBase {
         const int last = d - 1;
         const int rows = dims[static_cast<std::size_t>(last)], cols = C[static_cast<std::size_t>(last)];
         const int r = ranks[static_cast<std::size_t>(last)];
-        const long long blocks = (static_cast<long long>(cols) * r * 32 + 255) / 256;
+        const long long blocks = core_sumsq_blocks(rows, cols, r);
         if (blocks <= sumsq_scratch()) {  // one launch: core + |core|^2
             if (!ticket.get()) {
                 ticket.alloc(ctx, 1);
