@@ -908,36 +908,43 @@ __global__ void __launch_bounds__(512, 3) y_from_segments_kernel(const int* __re
                                                               const int* __restrict__ seg_row, const T* __restrict__ fseg,
                                                               int ra, const T* __restrict__ Un, int rns, int rn, int sa,
                                                               int sn, int rows, int un_rows, int chunk, int ptr_mul,
-                                                              T* __restrict__ Y) {
+                                                              int nbuf, T* __restrict__ Y) {
     // wait, then trigger: the overlapped stage 1 launched two kernels later
     // (which does not wait at entry) then starts only after this grid's
     // predecessors are complete: it cannot overwrite fibre sums or factor
     // copies still being read (see SparseSession::sweep_body)
     pdl_enter_strict();
     extern __shared__ __align__(128) unsigned char ysm[];
-    __shared__ __align__(8) std::uint64_t bar;
+    __shared__ __align__(8) std::uint64_t bar[2];
     const int G = blockDim.x / ra;
     const int tid = threadIdx.x;
     const int g = tid / ra, r_a = tid - (tid / ra) * ra;
     const bool on = g < G;
     const std::size_t ub = static_cast<std::size_t>(un_rows) * rns * sizeof(T);  // multiple of 16
+    // [U][nbuf fibre-sum chunks, later the group partials][nbuf i_n chunks]; nbuf = 2: the next chunk's bulk copies
+    // fly while the current one is consumed (persistent CTAs with a large staged U: one CTA per SM)
+    const std::size_t fcap = (static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16 + 15) & ~std::size_t(15);
+    const std::size_t rcap = (static_cast<std::size_t>(chunk) * sizeof(int) + 16 + 15) & ~std::size_t(15);
     T* sU = reinterpret_cast<T*>(ysm);
-    unsigned char* sFb = ysm + ub;
-    unsigned char* sRb = sFb + ((static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16 + 15) & ~std::size_t(15));
-    T* part = reinterpret_cast<T*>(sFb);  // the group partials reuse the fibre-sum chunk once it is consumed
+    unsigned char* sFb0 = ysm + ub;
+    unsigned char* sRb0 = sFb0 + max(static_cast<std::size_t>(nbuf) * fcap,
+                                     (static_cast<std::size_t>(G) * ra * rn * sizeof(T) + 15) & ~std::size_t(15));
+    T* part = reinterpret_cast<T*>(sFb0);  // the group partials reuse the fibre-sum chunks once they are consumed
     if (tid == 0) {
-        ttm::mbar_init(&bar, 1);
+        ttm::mbar_init(&bar[0], 1);
+        ttm::mbar_init(&bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    std::uint32_t phase = 0;
+    std::uint32_t phase[2] = {0u, 0u};
     bool ustaged = false;
     for (int row = blockIdx.x; row < rows; row += gridDim.x) {  // rows share the staged U
     const int s0 = seg_ptr[row] * ptr_mul, s1 = seg_ptr[row + 1] * ptr_mul;
     T acc[RN];
 #pragma unroll
     for (int q = 0; q < RN; ++q) acc[q] = T(0);
-    for (int base = s0, first = 1; base < s1 || first; base += chunk, first = 0) {
+    // chunk c of this row covers segments [s0 + c * chunk, ...); its copies are 16-byte-aligned supersets
+    auto issue = [&](int base, int buf, bool with_u) {
         const int m = max(0, min(chunk, s1 - base));
         const unsigned char* fsrc = reinterpret_cast<const unsigned char*>(fseg + static_cast<long long>(base) * ra);
         const unsigned char* rsrc = reinterpret_cast<const unsigned char*>(seg_row + base);
@@ -945,20 +952,26 @@ __global__ void __launch_bounds__(512, 3) y_from_segments_kernel(const int* __re
         const unsigned char* r0 = reinterpret_cast<const unsigned char*>(reinterpret_cast<std::uintptr_t>(rsrc) & ~std::uintptr_t(15));
         const std::uint32_t fb = static_cast<std::uint32_t>(((fsrc - f0) + static_cast<std::size_t>(m) * ra * sizeof(T) + 15) & ~std::size_t(15));
         const std::uint32_t rb = static_cast<std::uint32_t>(((rsrc - r0) + static_cast<std::size_t>(m) * sizeof(int) + 15) & ~std::size_t(15));
-        if (tid == 0) {
-            const std::uint32_t ubytes = !ustaged && un_rows > 0 ? static_cast<std::uint32_t>(ub) : 0u;
-            ttm::mbar_expect_tx(&bar, ubytes + (m ? fb + rb : 0u));
-            if (ubytes) ttm::bulk_g2s(sU, Un, ubytes, &bar);
-            if (m) {
-                ttm::bulk_g2s(sFb, f0, fb, &bar);
-                ttm::bulk_g2s(sRb, r0, rb, &bar);
-            }
+        const std::uint32_t ubytes = with_u && un_rows > 0 ? static_cast<std::uint32_t>(ub) : 0u;
+        ttm::mbar_expect_tx(&bar[buf], ubytes + (m ? fb + rb : 0u));
+        if (ubytes) ttm::bulk_g2s(sU, Un, ubytes, &bar[buf]);
+        if (m) {
+            ttm::bulk_g2s(sFb0 + buf * fcap, f0, fb, &bar[buf]);
+            ttm::bulk_g2s(sRb0 + buf * rcap, r0, rb, &bar[buf]);
         }
-        ttm::mbar_wait(&bar, phase);
-        phase ^= 1u;
+    };
+    if (tid == 0) issue(s0, 0, !ustaged);
+    int buf = 0;
+    for (int base = s0, first = 1; base < s1 || first; base += chunk, first = 0) {
+        const int m = max(0, min(chunk, s1 - base));
+        if (nbuf == 2 && tid == 0 && base + chunk < s1) issue(base + chunk, buf ^ 1, false);  // (its last readers passed the barrier below)
+        ttm::mbar_wait(&bar[buf], phase[buf]);
+        phase[buf] ^= 1u;
         ustaged = true;
-        const T* sF = reinterpret_cast<const T*>(sFb + (fsrc - f0));
-        const int* sR = reinterpret_cast<const int*>(sRb + (rsrc - r0));
+        const unsigned char* fsrc = reinterpret_cast<const unsigned char*>(fseg + static_cast<long long>(base) * ra);
+        const unsigned char* rsrc = reinterpret_cast<const unsigned char*>(seg_row + base);
+        const T* sF = reinterpret_cast<const T*>(sFb0 + buf * fcap + (reinterpret_cast<std::uintptr_t>(fsrc) & 15));
+        const int* sR = reinterpret_cast<const int*>(sRb0 + buf * rcap + (reinterpret_cast<std::uintptr_t>(rsrc) & 15));
         // two copies of the loop so the staged case compiles to shared-memory loads
         auto run = [&](const T* U) {
             for (int j = g; j < m; j += G) {
@@ -987,7 +1000,9 @@ __global__ void __launch_bounds__(512, 3) y_from_segments_kernel(const int* __re
             if (un_rows > 0) run(sU);
             else run(Un);
         }
-        __syncthreads();  // the next chunk's bulk copies overwrite sF / sR
+        __syncthreads();  // this buffer may be refilled (by the issue two chunks ahead, or the next row's first)
+        if (nbuf == 2) buf ^= 1;
+        else if (tid == 0 && base + chunk < s1) issue(base + chunk, 0, false);
     }
     const int C = ra * rn;
     if (on)
@@ -1060,10 +1075,12 @@ void y_from_segments(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const 
     const bool stage = ubytes <= stage_max;
     const int chunk = static_cast<int>(std::min<std::size_t>(2048, (24 * 1024) / (ra * sizeof(T))));
     // shared memory: [U][fibre-sum chunk, later the group partials][i_n chunk]; ~55 KB at C2: four CTAs per SM
-    const std::size_t fbytes = std::max(static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16,
-                                        static_cast<std::size_t>(G) * ra * rn * sizeof(T));
-    const std::size_t smem = (stage ? ubytes : 0) + ((fbytes + 15) & ~std::size_t(15)) +
-                             ((static_cast<std::size_t>(chunk) * sizeof(int) + 16 + 15) & ~std::size_t(15));
+    // large staged U: one persistent CTA per SM, so its chunk loads are double-buffered against the compute
+    const int nbuf = (stage && ubytes > 32 * 1024) ? 2 : 1;
+    const std::size_t fcap = (static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16 + 15) & ~std::size_t(15);
+    const std::size_t rcap = (static_cast<std::size_t>(chunk) * sizeof(int) + 16 + 15) & ~std::size_t(15);
+    const std::size_t fbytes = std::max(nbuf * fcap, (static_cast<std::size_t>(G) * ra * rn * sizeof(T) + 15) & ~std::size_t(15));
+    const std::size_t smem = (stage ? ubytes : 0) + fbytes + nbuf * rcap;
     auto launch = [&](auto y_from_segments_kernel_rn) {  // (the name is the profiler's kernel label)
         auto kern = y_from_segments_kernel_rn;
         MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -1074,7 +1091,7 @@ void y_from_segments(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, const 
             grid = std::min<int>(rows, sms * std::max<int>(1, static_cast<int>((227 * 1024) / (smem + 1024))));
         }
         MB_LAUNCH_PDL(ctx, y_from_segments_kernel_rn, grid, threads, smem, P.seg_ptr.get(), P.seg_row.get(), fseg, ra, Un, rns, rn, sa, sn, rows,
-                  stage ? dims[n] : 0, chunk, 1, Y);
+                  stage ? dims[n] : 0, chunk, 1, nbuf, Y);
     };
     // RN >= rn register accumulators
     if (rn <= 4) launch(y_from_segments_kernel<T, 4>);
@@ -1155,10 +1172,11 @@ void sparse_mode_stage2(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, con
         std::getenv("MACH_S2_STAGE_MAX") ? static_cast<std::size_t>(std::atoll(std::getenv("MACH_S2_STAGE_MAX"))) : 80 * 1024;
     const bool stage = ubytes <= stage_max;
     const int chunk = static_cast<int>(std::min<std::size_t>(2048, (24 * 1024) / (ra * sizeof(T))));
-    const std::size_t fbytes = std::max(static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16,
-                                        static_cast<std::size_t>(G) * ra * rb * sizeof(T));
-    const std::size_t smem = (stage ? ubytes : 0) + ((fbytes + 15) & ~std::size_t(15)) +
-                             ((static_cast<std::size_t>(chunk) * sizeof(int) + 16 + 15) & ~std::size_t(15));
+    const int nbuf = (stage && ubytes > 32 * 1024) ? 2 : 1;  // see y_from_segments
+    const std::size_t fcap = (static_cast<std::size_t>(chunk) * ra * sizeof(T) + 16 + 15) & ~std::size_t(15);
+    const std::size_t rcap = (static_cast<std::size_t>(chunk) * sizeof(int) + 16 + 15) & ~std::size_t(15);
+    const std::size_t fbytes = std::max(nbuf * fcap, (static_cast<std::size_t>(G) * ra * rb * sizeof(T) + 15) & ~std::size_t(15));
+    const std::size_t smem = (stage ? ubytes : 0) + fbytes + nbuf * rcap;
     auto launch = [&](auto y_from_segments_kernel_rn) {  // (the name is the profiler's kernel label)
         auto kern = y_from_segments_kernel_rn;
         MB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -1170,7 +1188,7 @@ void sparse_mode_stage2(Ctx* ctx, ModePlan& P, const std::vector<int>& dims, con
             grid = std::min<int>(grid, sms * std::max<int>(1, static_cast<int>((227 * 1024) / (smem + 1024))));
         }
         MB_LAUNCH_PDL(ctx, y_from_segments_kernel_rn, grid, threads, smem, P.st_base.get(), P.seg_ib.get(), F, ra, Ub, rbs,
-                      rb, sa, sb, rows, stage ? dims[b] : 0, chunk, 32, Y);
+                      rb, sa, sb, rows, stage ? dims[b] : 0, chunk, 32, nbuf, Y);
     };
     if (rb <= 4) launch(y_from_segments_kernel<T, 4>);
     else if (rb <= 8) launch(y_from_segments_kernel<T, 8>);
