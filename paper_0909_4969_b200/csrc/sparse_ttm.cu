@@ -265,36 +265,41 @@ __global__ void jds_kernel(const K* __restrict__ keys, const T* __restrict__ val
         // free residue twice as often (simulated on Poisson fibres: 0.60 ->
         // 0.42 extra wavefronts per gather wavefront; a per-step maximum
         // matching reaches 0.38)
-        unsigned av[8];
+        // (the keys are formed by all lanes at once; only the choice among
+        // the still-free residues runs lane after lane)
+        const bool run = j < len;
+        const unsigned later = ((0xFEu << (lane & 7)) & 0xFFu) << grp;
+        int key[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) av[c] = __ballot_sync(0xffffffffu, j < len && (cm[c] & rem) != 0u);
+        for (int c = 0; c < 8; ++c) {
+            const unsigned mine = cm[c] & rem;
+            const unsigned avc = __ballot_sync(0xffffffffu, run && mine != 0u);
+            key[c] = mine ? __popc(avc & later) * 64 - __popc(mine) : (1 << 30);
+        }
         unsigned taken = 0u;
         int pick = 0;
         for (int q = 0; q < 8; ++q) {
-            if ((lane & 7) == q && j < len) {
-                const unsigned later = ((0xFEu << q) & 0xFFu) << grp;
-                int best = -1, bestkey = 1 << 30;
+            if ((lane & 7) == q && run) {
+                int bestkey = 1 << 30;
+                unsigned pref = 0u, pbit = 0u;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
-                    const unsigned mine = cm[c] & rem;
-                    if (!((taken >> c) & 1u) && mine) {
-                        const int key = __popc(av[c] & later) * 64 - __popc(mine);
-                        if (key < bestkey) {
-                            bestkey = key;
-                            best = c;
-                        }
+                    if (!((taken >> c) & 1u) && key[c] < bestkey) {
+                        bestkey = key[c];
+                        pref = cm[c] & rem;
+                        pbit = 1u << c;
                     }
                 }
-                unsigned pref = 0u;
-#pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    if (c == best) pref = cm[c] & rem;
                 const unsigned choose = pref ? pref : rem;
                 pick = __ffs(static_cast<int>(choose)) - 1;
                 rem &= ~(1u << pick);
+                if (pref) {
+                    taken |= pbit;
+                } else {  // no free residue left: the pick conflicts, its residue is already taken
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    if ((cm[c] >> pick) & 1u) taken |= 1u << c;
+                    for (int c = 0; c < 8; ++c)
+                        if ((cm[c] >> pick) & 1u) taken |= 1u << c;
+                }
             }
             taken = __shfl_sync(0xffffffffu, taken, grp | q);
         }
