@@ -43,11 +43,15 @@ __global__ void maxabs_kernel(const T* __restrict__ x, long long n, double* __re
 
 constexpr int kMaxSpectrumN = 1700;  // one-CTA tridiagonal solver's shared-memory limit (eig.cu)
 
-// descending sigma^2 (clamped at 0) of the symmetric n x n Gram G (device)
-std::vector<double> gram_spectrum(Ctx* ctx, const double* G, int n) {
+void check_spectrum_side(long long n) {
     if (n > kMaxSpectrumN)
         throw Error(MACH_ERR_INTERNAL, "full mode spectrum: shorter side " + std::to_string(n) + " exceeds " +
                                            std::to_string(kMaxSpectrumN));
+}
+
+// descending sigma^2 (clamped at 0) of the symmetric n x n Gram G (device)
+std::vector<double> gram_spectrum(Ctx* ctx, const double* G, int n) {
+    check_spectrum_side(n);
     DBuf<double> work(ctx, eig_work_doubles(n, 1) + static_cast<std::size_t>(8) * n);
     DBuf<double> sig(ctx, static_cast<std::size_t>(n));
     DBuf<int> est(ctx, 3);
@@ -64,11 +68,11 @@ std::vector<double> dense_mode_spectrum(Ctx* ctx, const mach_dense* t, int mode)
     const int rows = t->dims[static_cast<std::size_t>(mode)];
     const long long cols = t->numel / rows;
     if (std::max<long long>(rows, cols) > (1ll << 31) - 1) throw_shape("mode unfolding too wide for the Gram kernel");
-    DBuf<T> xm(ctx, static_cast<std::size_t>(t->numel));
-    dense_matricize<T, T>(ctx, static_cast<const T*>(t->data), t->dims, mode, xm.get());
     const bool row_side = rows <= cols;
     const int n = row_side ? rows : static_cast<int>(cols);
-    if (n > kMaxSpectrumN) gram_spectrum(ctx, nullptr, n);  // throws with the size
+    check_spectrum_side(n);
+    DBuf<T> xm(ctx, static_cast<std::size_t>(t->numel));
+    dense_matricize<T, T>(ctx, static_cast<const T*>(t->data), t->dims, mode, xm.get());
     DBuf<double> G(ctx, static_cast<std::size_t>(n) * n);
     if (row_side) gram<T>(ctx, xm.get(), rows, 1, static_cast<int>(cols), rows, G.get());
     else gram<T>(ctx, xm.get(), 1, rows, rows, n, G.get());
@@ -82,7 +86,7 @@ std::vector<double> sparse_mode_spectrum(Ctx* ctx, mach_sparse* X, int mode, con
     const long long cols = X->numel / rows;
     const bool row_side = rows <= cols;
     const int n = row_side ? rows : static_cast<int>(std::min<long long>(cols, 1 << 30));
-    if (n > kMaxSpectrumN) gram_spectrum(ctx, nullptr, n);
+    check_spectrum_side(n);
     DBuf<double> G(ctx, static_cast<std::size_t>(n) * n);
     if (X->nnz == 0) {
         G.zero(ctx);

@@ -50,7 +50,6 @@ struct mach_stream {
     int next = 0;
     // last dense slab (records / host appends)
     void* last = nullptr;
-    std::size_t last_bytes = 0;
     int last_ticks = 0;
     // carry-forward state per (machine, metric)
     double* cf_last = nullptr;

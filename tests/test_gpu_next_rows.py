@@ -256,3 +256,21 @@ def test_binary_rejects_malformed(mb, tmp_path):
         mb.load_tensor(str(tmp_path / "unsorted.machb"))
     with pytest.raises(mb.IoError):
         mb.save_tensor(x, str(tmp_path / "no_such_dir" / "x.machb"))
+
+
+def test_stream_wide_capacity_narrows_indices(mb):
+    """A stream whose capacity exceeds 2^32 elements stores 64-bit indices; a
+    snapshot that still fits 32 bits is narrowed to the canonical u32 layout
+    and equals the offline sampler's kept set."""
+    lead, ticks, p, seed = (2048, 128), 6, 0.05, 9
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(lead + (ticks,)).astype(np.float32)
+    st = mb.SampleStream(lead + (20000,), mb.SparsifyConfig(p, seed), dtype=np.float32)  # 5.2e9 > 2^32
+    st.append(np.asfortranarray(x[:, :, :4]))
+    st.append(mb.DenseTensor.from_numpy(np.asfortranarray(x[:, :, 4:])))
+    sp = st.tensor()
+    idx, val = sp.entries()
+    ref_idx, _ = O.sparsify(O.Dense(x.astype(np.float64)), p, seed).entries()
+    assert sp.dims == lead + (ticks,) and np.array_equal(idx, ref_idx)
+    m = mb.hosvd(sp, (3, 3, 2))
+    assert m.fit == m.fit  # the narrowed tensor drives the decomposition
