@@ -1,6 +1,6 @@
 """Debug: 2 processes on one GPU, host-staged exchange; print Y checksums per mode."""
 import os, sys, numpy as np
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch, torch.multiprocessing as tmp
 import oracle as O
 def w(rank, port, q):

@@ -1,6 +1,6 @@
 """Generate tests/golden/ fixtures from the pinned CPU oracle.
 
-  python scripts/make_golden.py
+  python tests/tools/make_golden.py
 
 Inputs are regenerated deterministically from mt19937_64 streams
 (oracle.random_tensor), so only the small outputs are stored: sampler kept
@@ -15,7 +15,7 @@ import sys
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import oracle as O  # noqa: E402
 
@@ -44,7 +44,7 @@ def main():
         cases.append({"dims": list(dims), "p": p, "seed": str(seed), "tensor_seed": ts, "zero_every": 7,
                       "idx": idx.tolist(), "vals_hex": [f"{v:016x}" for v in vals.view(np.uint64)]})
     with open(os.path.join(OUT, "sampler.json"), "w") as f:
-        json.dump({"generator": "scripts/make_golden.py", "cases": cases}, f)
+        json.dump({"generator": "tests/tools/make_golden.py", "cases": cases}, f)
     models = []
     for dims, ranks, p, seed, sweeps, ts in HOOI:
         x = O.random_tensor(list(dims), ts)
@@ -55,7 +55,7 @@ def main():
                        "core": m.core.reshape(-1, order="F").tolist(),
                        "factors": [f.reshape(-1, order="F").tolist() for f in m.factors]})
     with open(os.path.join(OUT, "mach_hooi.json"), "w") as f:
-        json.dump({"generator": "scripts/make_golden.py", "cases": models}, f)
+        json.dump({"generator": "tests/tools/make_golden.py", "cases": models}, f)
     print("wrote", OUT)
 
 
