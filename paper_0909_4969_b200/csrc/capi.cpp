@@ -390,7 +390,10 @@ static mach_status mach_pipeline(mach_ctx* ctx, const mach_dense* t, const int* 
         // p == 1 keeps every nonzero entry unchanged: the densified sample (the
         // densify switch, tucker.cpp:154-155) is the input itself, so the dense
         // route reads t in place instead of a scattered copy
-        mach_model* m = p == 1.0
+        // (only when the sample is dense enough for that switch: a mostly-zero
+        // input keeps the sparse route)
+        const bool in_place = p == 1.0 && static_cast<double>(s->nnz) >= 0.25 * static_cast<double>(s->numel);
+        mach_model* m = in_place
                             ? tucker_dense(t, ranks_of(static_cast<int>(t->dims.size()), ranks), do_hooi, max_it, tol)
                             : tucker_sparse(s.get(), ranks_of(static_cast<int>(t->dims.size()), ranks), do_hooi, max_it, tol);
         m->sample_ms = ms;
