@@ -265,10 +265,8 @@ __global__ void jds_kernel(const K* __restrict__ keys, const T* __restrict__ val
         // free residue twice as often (simulated on Poisson fibres: 0.60 ->
         // 0.42 extra wavefronts per gather wavefront; a per-step maximum
         // matching reaches 0.38)
-        // (the keys are formed by all lanes at once; only the choice among
-        // the still-free residues runs lane after lane)
         const bool run = j < len;
-        const unsigned later = ((0xFEu << (lane & 7)) & 0xFFu) << grp;
+        const unsigned later = ((0xFEu << (lane & 7)) & 0xFFu) << grp;  // the lanes that lose ties to this one
         int key[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -276,32 +274,41 @@ __global__ void jds_kernel(const K* __restrict__ keys, const T* __restrict__ val
             const unsigned avc = __ballot_sync(0xffffffffu, run && mine != 0u);
             key[c] = mine ? __popc(avc & later) * 64 - __popc(mine) : (1 << 30);
         }
+        // Rounds of propose / resolve inside each quarter instead of a
+        // lane-after-lane pass: every unplaced lane proposes its best free
+        // residue, the lowest lane among equal proposals wins, losers retry
+        // against the updated free set (2-3 rounds as a rule); a lane with no
+        // free residue left takes its first remaining element and conflicts.
         unsigned taken = 0u;
         int pick = 0;
-        for (int q = 0; q < 8; ++q) {
-            if ((lane & 7) == q && run) {
-                int bestkey = 1 << 30;
-                unsigned pref = 0u, pbit = 0u;
+        bool placed = !run;
+        while (__any_sync(0xffffffffu, !placed)) {
+            int bestkey = 1 << 30, prop = 8;
+            unsigned pref = 0u;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    if (!((taken >> c) & 1u) && key[c] < bestkey) {
-                        bestkey = key[c];
-                        pref = cm[c] & rem;
-                        pbit = 1u << c;
-                    }
-                }
-                const unsigned choose = pref ? pref : rem;
-                pick = __ffs(static_cast<int>(choose)) - 1;
-                rem &= ~(1u << pick);
-                if (pref) {
-                    taken |= pbit;
-                } else {  // no free residue left: the pick conflicts, its residue is already taken
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        if ((cm[c] >> pick) & 1u) taken |= 1u << c;
+            for (int c = 0; c < 8; ++c) {
+                if (!((taken >> c) & 1u) && key[c] < bestkey) {
+                    bestkey = key[c];
+                    pref = cm[c] & rem;
+                    prop = c;
                 }
             }
-            taken = __shfl_sync(0xffffffffu, taken, grp | q);
+            // lanes that are placed already, or have nothing free, do not compete
+            const bool compete = !placed && prop < 8;
+            const unsigned same = __match_any_sync(0xffffffffu, compete ? (grp | prop) : (0x100 | lane));
+            const bool win = compete && (__ffs(static_cast<int>(same)) - 1) == lane;
+            const bool forced = !placed && prop == 8;  // conflict: first remaining element
+            if (win || forced) {
+                const unsigned choose = win ? pref : rem;
+                pick = __ffs(static_cast<int>(choose)) - 1;
+                rem &= ~(1u << pick);
+                placed = true;
+            }
+            unsigned won = win ? (1u << prop) : 0u;
+            won |= __shfl_xor_sync(0xffffffffu, won, 1);
+            won |= __shfl_xor_sync(0xffffffffu, won, 2);
+            won |= __shfl_xor_sync(0xffffffffu, won, 4);
+            taken |= won;
         }
         if (j < len) {
             const long long dst = ptr + lane;
