@@ -238,7 +238,12 @@ void stream_append_host(mach_stream* s, const void* host, int ticks) {
     MB_CUDA(cudaMemcpyAsync(s->stage[b], host, bytes, cudaMemcpyHostToDevice, s->copy));
     MB_CUDA(cudaEventRecord(s->ready[b], s->copy));
     // sample the previous slab while this one is in flight
-    flush_pending(s);
+    try {
+        flush_pending(s);
+    } catch (...) {  // (e.g. a non-finite value in the previous slab) this slab is dropped with it
+        cudaStreamSynchronize(s->copy);  // the host buffer must not be read after we return
+        throw;
+    }
     s->pending = b;
     s->pending_ticks = ticks;
     MB_CUDA(cudaStreamSynchronize(s->copy));  // the host buffer may be reused on return
