@@ -164,6 +164,19 @@ mach_status mach_hooi_shard(mach_session* s);  /* global |X|^2 for the fit */
 mach_status mach_hooi_mode_y(mach_session* s, int mode, void** y, int* rows, int* cols);
 mach_status mach_hooi_mode_update(mach_session* s, int mode);
 mach_status mach_hooi_sweep_end(mach_session* s, double fit_tolerance, int* stopped);
+/* Shard HOSVD from partial Grams: with time-slab shards the row
+ * Gram of every mode but the last is the sum of the shards' Grams
+ * (mach_sparse_row_gram of the local tensor, all-reduced by the caller; the
+ * last mode's Gram has cross-slab blocks and comes from the gathered
+ * nonzeros).  mach_hosvd_from_grams turns the d full Grams (host, I_n x I_n
+ * column-major) into the HOSVD factors (model core / fit left zero);
+ * mach_hooi_begin_from starts the shard session from them, and after the
+ * caller has reduced mach_hooi_mode_y(order-1), mach_hooi_refresh_fit sets
+ * the starting fit (sweep_fits[0]).                                          */
+mach_status mach_sparse_row_gram(mach_ctx* ctx, const mach_sparse* t, int mode, double* host);
+mach_status mach_hosvd_from_grams(mach_ctx* ctx, int order, const int* dims, const int* ranks,
+                                  const double* const* grams, mach_model** out);
+mach_status mach_hooi_refresh_fit(mach_session* s);
 mach_status mach_session_free(mach_session* s);
 
 /* ---- per-kernel device timing (CUDA events on the context stream) -------- */

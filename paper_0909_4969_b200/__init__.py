@@ -50,6 +50,7 @@ from .api import (  # noqa: F401
     pearson,
     reconstruct,
     sparsify,
+    sparse_row_gram,
     sparsify_slab,
     subspace_sin,
 )

@@ -116,6 +116,9 @@ _SIGS = {
     "mach_subspace_sin": (C.c_int, [vp, C.c_int, C.c_int, dp, dp, dp]),
     "mach_truncated_svd": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int, dp, dp, dp]),
     "mach_low_rank_approx": (C.c_int, [vp, C.c_int, C.c_int, dp, C.c_int, dp]),
+    "mach_sparse_row_gram": (C.c_int, [vp, vp, C.c_int, dp]),
+    "mach_hosvd_from_grams": (C.c_int, [vp, C.c_int, ip, ip, C.POINTER(dp), vpp]),
+    "mach_hooi_refresh_fit": (C.c_int, [vp]),
     "mach_achlioptas_bounds": (C.c_int, [C.c_double, i64, i64, C.c_double, dp, dp]),
     "mach_min_sampling_probability": (C.c_int, [C.c_int, ip, dp]),
     "mach_theorem1_conditions": (C.c_int, [C.c_int, ip, C.c_double, C.POINTER(BoundReport)]),

@@ -558,6 +558,14 @@ def mode_product(t, m: np.ndarray, mode: int, ctx: Context | None = None, keep_o
     return out if keep_on_device else out.numpy()
 
 
+def sparse_row_gram(t: "SparseTensor", mode: int) -> np.ndarray:
+    """Row Gram X_(mode) X_(mode)^T of a sampled tensor (I x I, fp64)."""
+    n = int(t.dims[mode])
+    out = np.empty(n * n, dtype=np.float64)
+    _check(L.lib().mach_sparse_row_gram(t.ctx.h, t.h, int(mode), out.ctypes.data_as(L.dp)))
+    return out.reshape((n, n), order="F")
+
+
 def mode_gram(t, mode: int, ctx: Context | None = None):
     """X_(mode) X_(mode)^T of a dense tensor (the dense HOSVD's row-side Gram,
     linalg.cpp:340).  Returns (G, tensor_cores): fp32 tensors of supported
@@ -682,6 +690,29 @@ class HooiSession:
         self = cls.__new__(cls)
         self.h, self.ctx, self._src = h, t.ctx, t
         return self
+
+    @classmethod
+    def from_grams(cls, t: "SparseTensor", ranks, grams):
+        """Shard session on `t` whose HOSVD factors come from the full row Grams
+        `grams` (one I_n x I_n array per mode; partial Grams summed
+        over the shards).  Call refresh_fit() once mode_y(last) is reduced."""
+        d = len(t.dims)
+        gs = [np.ascontiguousarray(np.asarray(g, dtype=np.float64).reshape(-1, order="F")) for g in grams]
+        ptrs = (L.dp * d)(*[g.ctypes.data_as(L.dp) for g in gs])
+        hm = C.c_void_p()
+        _check(L.lib().mach_hosvd_from_grams(t.ctx.h, d, _dims_arr(t.dims), _ranks(ranks, d), ptrs, C.byref(hm)))
+        try:
+            h = C.c_void_p()
+            _check(L.lib().mach_hooi_begin_from(t.ctx.h, t.h, _ranks(ranks, d), hm, C.byref(h)))
+        finally:
+            L.lib().mach_model_free(hm)
+        self = cls.__new__(cls)
+        self.h, self.ctx, self._src = h, t.ctx, t
+        return self
+
+    def refresh_fit(self):
+        """Starting fit (sweep_fits[0]) from the last mode's (reduced) Y."""
+        _check(L.lib().mach_hooi_refresh_fit(self.h))
 
     def shard(self):
         """Make this session one time-slab shard over its context's NCCL

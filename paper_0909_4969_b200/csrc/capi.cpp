@@ -685,6 +685,10 @@ void session_mode_update(void* s, int m);
 int session_sweep_end(void* s, double tol);
 void session_set_norm2(void* s, double v);
 void session_shard(void* s);
+void session_refresh_fit(void* s);
+void sparse_row_gram_host(Ctx* ctx, const mach_sparse* X, int n, double* host);
+mach_model* hosvd_from_grams(Ctx* ctx, const std::vector<int>& dims, const std::vector<int>& ranks,
+                             const double* const* grams);
 }  // namespace machb
 
 struct mach_session {
@@ -818,6 +822,34 @@ mach_status mach_hooi_model(mach_session* s, mach_model** out) {
         need(s, "session");
         need(out, "out");
         *out = session_snapshot(s->s);
+    });
+}
+
+mach_status mach_hooi_refresh_fit(mach_session* s) {
+    return guard([&] {
+        need(s, "session");
+        session_refresh_fit(s->s);
+    });
+}
+
+mach_status mach_sparse_row_gram(mach_ctx* ctx, const mach_sparse* t, int mode, double* host) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
+        need(t, "tensor");
+        need(host, "host");
+        sparse_row_gram_host(&ctx->c, t, mode, host);
+    });
+}
+
+mach_status mach_hosvd_from_grams(mach_ctx* ctx, int order, const int* dims, const int* ranks,
+                                  const double* const* grams, mach_model** out) {
+    return guard([&] {
+        need(ctx, "ctx");
+        DevGuard dg_(ctx->c.device);
+        need(grams, "grams");
+        need(out, "out");
+        *out = hosvd_from_grams(&ctx->c, dims_of(order, dims), ranks_of(order, ranks), grams);
     });
 }
 

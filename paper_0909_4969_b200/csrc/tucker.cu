@@ -392,6 +392,13 @@ struct SessionBase {
     virtual void* ext_mode_y(int, int*, int*) { throw Error(MACH_ERR_ARGUMENT, "split sweeps need a sparse session"); }
     virtual void ext_mode_update(int) { throw Error(MACH_ERR_ARGUMENT, "split sweeps need a sparse session"); }
     virtual void ext_core_fit() { throw Error(MACH_ERR_ARGUMENT, "split sweeps need a sparse session"); }
+    // the starting fit (sweep_fits[0]) from the last mode's Y as it stands
+    // (after an external reduction): a shard session started from factors
+    void ext_refresh_fit() {
+        ext_core_fit();
+        prev_fit = fit;
+        sweep_fits.assign(1, fit);
+    }
     virtual void set_norm2(double) { throw Error(MACH_ERR_ARGUMENT, "split sweeps need a sparse session"); }
     virtual void shard() { throw Error(MACH_ERR_ARGUMENT, "sharded sweeps need a sparse session"); }
     int ext_sweep_end(double tol) {
@@ -1265,6 +1272,86 @@ void session_mode_update(void* s, int m) { S(s)->ext_mode_update(m); }
 int session_sweep_end(void* s, double tol) { return S(s)->ext_sweep_end(tol); }
 void session_set_norm2(void* s, double v) { S(s)->set_norm2(v); }
 void session_shard(void* s) { S(s)->shard(); }
+
+void session_refresh_fit(void* s) { S(s)->ext_refresh_fit(); }
+
+// Row Gram X_(n) X_(n)^T of a sampled tensor into host memory (n x n,
+// column-major).  With time-slab shards the columns of X_(n), n != last, are
+// partitioned by the slabs, so the shards' Grams add up to the full one
+// (partial Grams + all-reduce).
+void sparse_row_gram_host(Ctx* ctx, const mach_sparse* X, int n, double* host) {
+    if (n < 0 || n >= static_cast<int>(X->dims.size())) throw_arg("mode out of range");
+    const int rows = X->dims[static_cast<std::size_t>(n)];
+    if (static_cast<long long>(rows) > X->numel / rows) throw_arg("the row Gram needs rows <= columns of the unfolding");
+    DBuf<double> G(ctx, static_cast<std::size_t>(rows) * rows);
+    if (X->nnz == 0) {
+        G.zero(ctx);
+    } else {
+        DBuf<double> red(ctx, sumsq_scratch()), n2(ctx, 1);
+        double norm2 = 0.0;
+        if (X->dtype == MACH_F32) sumsq<float>(ctx, static_cast<const float*>(X->val), X->nnz, red.get(), n2.get());
+        else sumsq<double>(ctx, static_cast<const double*>(X->val), X->nnz, red.get(), n2.get());
+        to_host(ctx, &norm2, n2.get(), 1);
+        sync(ctx);
+        if (X->dtype == MACH_F32) sparse_row_gram<float>(ctx, X, n, norm2, G.get());
+        else sparse_row_gram<double>(ctx, X, n, norm2, G.get());
+    }
+    to_host(ctx, host, G.get(), static_cast<std::size_t>(rows) * rows);
+    sync(ctx);
+}
+
+// HOSVD factors from full row Grams (host, one per mode): the eigen step and
+// the basis of sparse_mode_basis's row side (sparse_kernels.cpp:82-84 ->
+// linalg.cpp:106-120).  The model carries the factors and warnings; its core
+// and fit are left to the caller (mach_hooi_begin_from + mach_hooi_refresh_fit).
+mach_model* hosvd_from_grams(Ctx* ctx, const std::vector<int>& dims, const std::vector<int>& ranks,
+                             const double* const* grams) {
+    check_ranks(dims, ranks);
+    const int d = static_cast<int>(dims.size());
+    FactorSet fs;
+    fs.init(ctx, dims, ranks);
+    struct ModeWork {
+        DBuf<double> G, V, sig;
+        DBuf<int> est;
+    };
+    std::vector<ModeWork> mw(static_cast<std::size_t>(d));
+    std::vector<EigJob> jobs;
+    for (int m = 0; m < d; ++m) {
+        const int n = dims[static_cast<std::size_t>(m)], k = ranks[static_cast<std::size_t>(m)];
+        if (!grams[m]) throw_arg("a Gram is missing");
+        ModeWork& w = mw[static_cast<std::size_t>(m)];
+        w.G.alloc(ctx, static_cast<std::size_t>(n) * n);
+        to_device(ctx, w.G.get(), grams[m], static_cast<std::size_t>(n) * n);
+        w.V.alloc(ctx, static_cast<std::size_t>(n) * k);
+        w.sig.alloc(ctx, k);
+        w.est.alloc(ctx, 3);
+        jobs.push_back(EigJob{w.G.get(), n, k, nullptr, 0, nullptr, w.V.get(), w.sig.get(), w.est.get(), nullptr, nullptr});
+    }
+    eig_select_batched(ctx, jobs);
+    int so = 0;
+    for (int m = 0; m < d; ++m) {
+        ModeWork& w = mw[static_cast<std::size_t>(m)];
+        basis_from_side(ctx, w.V.get(), w.sig.get(), dims[static_cast<std::size_t>(m)], ranks[static_cast<std::size_t>(m)],
+                        w.est.get(), fs.U[static_cast<std::size_t>(m)].get(), fs.sv.get() + so, fs.st.get() + 3 * m);
+        so += ranks[static_cast<std::size_t>(m)];
+    }
+    auto out = std::make_unique<mach_model>();
+    out->order = d;
+    out->dims = dims;
+    out->ranks = ranks;
+    out->core.assign(static_cast<std::size_t>(checked_size(ranks)), 0.0);
+    for (int m = 0; m < d; ++m) {
+        std::vector<double> f(fs.U[static_cast<std::size_t>(m)].n);
+        to_host(ctx, f.data(), fs.U[static_cast<std::size_t>(m)].get(), f.size());
+        out->factors.push_back(std::move(f));
+    }
+    std::vector<int> all(static_cast<std::size_t>(d));
+    for (int m = 0; m < d; ++m) all[static_cast<std::size_t>(m)] = m;
+    out->warnings = read_warnings(ctx, fs.st, ranks, all);
+    sync(ctx);
+    out->sweep_fits.assign(1, 0.0);
+    return out.release();
+}
 
 mach_model* tucker_sparse(mach_sparse* X, const std::vector<int>& ranks, bool do_hooi, int max_it, double tol) {
     check_ranks(X->dims, ranks);

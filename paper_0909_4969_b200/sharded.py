@@ -23,6 +23,7 @@ test of the real CUDA engine).
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 
@@ -157,7 +158,14 @@ def _sharded_body(slab_flat, dims_, ranks, p, seed, sweeps, fit_tolerance, group
     slab = A.DenseTensor.from_torch(slab_flat, dims[:-1] + [t1 - t0], ctx)
     sp = A.sparsify_slab(slab, dims, t0 * S, A.SparsifyConfig(p, seed), ctx)
 
-    # HOSVD once, replicated, on the all-gathered sampled tensor
+    # HOSVD.  Every mode but the last: the row Gram of X_(n) is a
+    # sum over its columns, which the time slabs partition, so each rank forms
+    # the Gram of its own nonzeros and the Grams are all-reduced.  The last
+    # mode's Gram has cross-slab blocks: it is formed once from the gathered
+    # nonzeros.  The eigen step runs replicated on identical Grams.  (Modes
+    # whose unfolding is taller than wide take the replicated route below.)
+    numel = math.prod(dims)
+    partial = all(dims[m] <= numel // dims[m] for m in range(d)) and os.environ.get("MACH_SHARD_REPLICATED_HOSVD") is None
     ip, vp, ib = sp.device_view()
     nnz = sp.nnz
     idx = device_view(ip, nnz, np.int32 if ib == 4 else np.int64, dev) if nnz else torch.zeros(0, dtype=torch.int32, device=dev)
@@ -165,16 +173,40 @@ def _sharded_body(slab_flat, dims_, ranks, p, seed, sweeps, fit_tolerance, group
     gidx = _allgather_varlen(idx, group)
     gval = _allgather_varlen(val, group)
     full = A.SparseTensor.from_device(dims, gidx.numel(), gidx.data_ptr(), gval.data_ptr(), dtype, ctx)
-    hs = A.HooiSession(full, ranks)
-    sess = A.HooiSession.from_session(sp, ranks, hs)
-    hs.free()
-    full.free()
+    if partial:
+        grams = []
+        for m in range(d - 1):
+            g = torch.from_numpy(np.ascontiguousarray(A.sparse_row_gram(sp, m)))
+            if _host_staged(group):
+                dist.all_reduce(g, group=group)
+            else:
+                gd = g.to(dev)
+                dist.all_reduce(gd, group=group)
+                g = gd.cpu()
+            grams.append(g.numpy())
+        grams.append(A.sparse_row_gram(full, d - 1))
+        full.free()
+        sess = A.HooiSession.from_grams(sp, ranks, grams)
+    else:  # replicated on the gathered tensor
+        hs = A.HooiSession(full, ranks)
+        sess = A.HooiSession.from_session(sp, ranks, hs)
+        hs.free()
+        full.free()
+
+    def start_fit(allreduce):
+        """sweep_fits[0] of the shard session: the last mode's partial Y summed over the ranks."""
+        if not partial:
+            return
+        ptr, rows, cols = sess.mode_y(d - 1)
+        allreduce(device_view(ptr, rows * cols, dtype, dev))
+        sess.refresh_fit()
 
     if in_library:
         # NCCL inside the library: the exchange rides the library stream and
         # the sweep graph (overlapped stage 1 kept)
         bind_comm(ctx, group)
         sess.shard()
+        start_fit(lambda y: dist.all_reduce(y, group=group))
         sess.step(sweeps, fit_tolerance)
     else:
         host = _host_staged(group)
@@ -192,6 +224,7 @@ def _sharded_body(slab_flat, dims_, ranks, p, seed, sweeps, fit_tolerance, group
             else:
                 dist.all_reduce(y, group=group)
 
+        start_fit(allreduce_sum_)
         sharded_sweeps(CudaEngine(sess, dtype, dev), allreduce_sum_, d, sweeps, fit_tolerance)
     model = sess.model()
     sess.free()

@@ -130,3 +130,35 @@ def test_sharded_two_processes_cuda_engine_gloo():
         for a, b in zip(factors, ref.factors):
             assert subspace_sin(a, b) <= 1e-3
         assert rel(align_core(core, factors, ref.factors), ref.core) <= 1e-4
+
+
+def test_partial_grams_sum_to_the_full_gram_and_give_the_hosvd():
+    """for every mode but the last the time slabs partition the
+    columns of X_(n), so the shards' row Grams add up to the full one; the
+    HOSVD from the summed Grams (+ the last mode's Gram of the gathered
+    nonzeros) equals the one-shot sparse HOSVD."""
+    import paper_0909_4969_b200 as mb
+    from tests.helpers import subspace_sin
+    dims, ranks, p, seed = (30, 24, 40), (3, 4, 5), 0.3, 11
+    x = O.random_tensor(list(dims), 8)
+    full = mb.sparsify(x, mb.SparsifyConfig(p, seed))
+    S = dims[0] * dims[1]
+    parts = [mb.sparsify_slab(np.ascontiguousarray(x[..., t0:t1]), dims, t0 * S, mb.SparsifyConfig(p, seed))
+             for t0, t1 in ((0, 13), (13, 14), (14, 40))]
+    d = full.densify()
+    for m in range(2):
+        a = np.moveaxis(d, m, 0).reshape(dims[m], -1, order="F")
+        g = sum(mb.sparse_row_gram(sp, m) for sp in parts)
+        assert np.abs(g - a @ a.T).max() <= 1e-12 * np.abs(a @ a.T).max()
+        assert np.abs(g - mb.sparse_row_gram(full, m)).max() <= 1e-12 * np.abs(g).max()
+    grams = [sum(mb.sparse_row_gram(sp, m) for sp in parts) for m in range(2)] + [mb.sparse_row_gram(full, 2)]
+    ref = mb.hosvd(full, ranks)
+    sess = mb.HooiSession.from_grams(full, ranks, grams)  # (one shard holding everything)
+    sess.mode_y(2)
+    sess.refresh_fit()
+    got = sess.model()
+    assert abs(got.fit - ref.fit) <= 1e-12 and got.sweep_fits[0] == got.fit
+    for fd, fr in zip(got.factors, ref.factors):
+        assert subspace_sin(fd, fr) <= 1e-10
+    with pytest.raises(mb.ArgumentError):
+        mb.sparse_row_gram(mb.sparsify(O.random_tensor([50, 3, 4], 1), mb.SparsifyConfig(0.5, 1)), 0)  # rows > columns
