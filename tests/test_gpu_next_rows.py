@@ -274,3 +274,32 @@ def test_stream_wide_capacity_narrows_indices(mb):
     assert sp.dims == lead + (ticks,) and np.array_equal(idx, ref_idx)
     m = mb.hosvd(sp, (3, 3, 2))
     assert m.fit == m.fit  # the narrowed tensor drives the decomposition
+
+
+def test_cli_decomposes_fp32_binary_in_place(mb, tmp_path):
+    """(f)4: an fp32 MACHB2 file goes file -> HBM -> mach-hooi in its stored
+    precision (no fp64 host round trip); the CLI's model equals the API's."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cli = os.path.join(root, "paper_0909_4969_b200", "mach_b200")
+    dims, ranks, p, seed = (64, 48, 80), (4, 3, 5), 0.3, 6
+    x = lowrank_numpy(dims, ranks, 0.02, seed=12).astype(np.float32)
+    xd = mb.DenseTensor.from_numpy(x)
+    src = str(tmp_path / "x.machb")
+    mb.save_tensor(xd, src)
+    out, sp_path = str(tmp_path / "model"), str(tmp_path / "s.machb")
+    r = subprocess.run([cli, "mach-hooi", "--input", src, "--ranks", ",".join(map(str, ranks)), "--p", str(p), "--seed", str(seed),
+                        "--max-iters", "3", "--fit-tol", "0", "--output", out, "--sparsified", sp_path],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    ref = mb.mach_hooi(xd, ranks, mb.SparsifyConfig(p, seed), mb.HooiConfig(3, 0.0))
+    meta = dict(ln.split(":", 1) for ln in open(os.path.join(out, "metadata")).read().splitlines() if ":" in ln)
+    assert float(meta["fit"]) == ref.model.fit and int(meta["iterations"]) == ref.model.iterations
+    info = mb.tensor_file_info(sp_path)
+    assert info["kind"] == "sparse" and info["dtype"] == np.dtype(np.float32) and info["count"] == ref.sparsified.nnz
+    i0, v0 = mb.load_tensor(sp_path).entries()
+    i1, v1 = ref.sparsified.entries()
+    assert np.array_equal(i0, i1) and np.array_equal(v0, v1)
+    # exit codes (cli.hpp:9-14): data error for a missing file, usage error for a bad p
+    assert subprocess.run([cli, "hosvd", "--input", str(tmp_path / "none"), "--ranks", "2,2,2", "--output", out]).returncode == 3
+    assert subprocess.run([cli, "sparsify", "--input", src, "--p", "0", "--output", sp_path], capture_output=True).returncode == 2
